@@ -1,0 +1,383 @@
+#!/usr/bin/env python
+"""Benchmark of the FastCHGNet training step on B200 (one JSON line on rank 0).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Step = chg_build_graph (A1) + chg_forward(train) (A2-A6) + chg_backward (A7-A8)
++ chg_step (A9: NCCL allreduce when N > 1, finite check, fused Adam) on one
+synthetic batch.  Workload: N = 1 -> C2 (40 MPtrj-shaped structures, BASELINE
+configs[1]); N > 1 -> C3 (128 structures per GPU, load-balanced with
+chg_balance, weak scaling).  `value` is device-timed (CUDA events on the
+library stream, inputs resident in HBM, L2 flushed between steps, max over
+ranks); `e2e` is the same step through the C ABI from pinned HOST buffers with
+the H2D copies and the loss D2H inside the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "train structures/s (fwd+bwd) at 1/2/4/8 B200; gather-scatter HBM GB/s"
+PEAKS = {"hbm_gbs": 6547.5, "sm_max_mhz": 1965.0}
+try:
+    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+        PEAKS.update(json.load(f))
+    PEAK_SRC = "measured (MEASURED_PEAKS.json)"
+except Exception:
+    PEAK_SRC = "fallback (B200_PROFILING.md)"
+# FP32 CUDA-core peak: 148 SMs x 128 FMA/clk x 2 flop x max SM clock
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * PEAKS.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+HBM_TAGS = {"segsum", "gate_fwd", "gate_bwd", "basis", "basis_bwd", "embed", "adam", "heads", "loss", "transpose"}
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batches", type=int, default=4, help="distinct pre-generated batches cycled through")
+    ap.add_argument("--per-gpu", type=int, default=0, help="structures per GPU (default: 40 at N=1, 128 at N>1)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _workload(n_gpus: int, per_gpu: int):
+    if n_gpus == 1 and per_gpu in (0, 40):
+        return "C2", 40
+    return "C3", per_gpu or 128
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100", "-i", str(self.device)], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": PEAKS.get("sm_max_mhz"), "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=5)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for k, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(k)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm / cpu baseline: the fp64 oracle on the host cores
+# ---------------------------------------------------------------------------
+def _oracle_step(batch, params, cfg, lc, state):
+    from oracle.graph import build_graph_batch
+    from oracle.train import adam_step, loss_and_grad
+    g = build_graph_batch(batch)
+    _, grad, _ = loss_and_grad(g, batch, params, cfg, lc)
+    state["t"] += 1
+    p, state["m"], state["v"] = adam_step(params, state["m"], state["v"], grad, state["t"], 3e-4)
+    return p
+
+
+def _oracle_sample(wl: str, per: int, budget_s: float):
+    """Largest prefix of the workload's first batch whose oracle step fits the budget."""
+    import torch
+    from chg_inputs import init_flat_params, make_config_batch, split_batch
+    from oracle.model import ModelConfig, param_layout
+    from oracle.train import LossConfig
+    cfg = ModelConfig()
+    full = make_config_batch(wl, 0, n_struct=per)
+    params = init_flat_params(param_layout(cfg), seed=0).astype(np.float32).astype(np.float64)
+    lc = LossConfig()
+    n = full.n_struct
+    sample = full
+    state = {"t": 0, "m": np.zeros_like(params), "v": np.zeros_like(params)}
+    t0 = time.time()
+    _oracle_step(split_batch(full, list(range(min(4, n)))), params, cfg, lc, state)
+    per_struct = (time.time() - t0) / min(4, n)
+    fit = max(1, min(n, int(budget_s / max(per_struct, 1e-3))))
+    if fit < n:
+        sample = split_batch(full, list(range(fit)))
+    return sample, params, cfg, lc, torch.get_num_threads()
+
+
+def cpu_baseline(wl: str, per: int, seconds: float):
+    sample, params, cfg, lc, cores = _oracle_sample(wl, per, seconds / 2)
+    state = {"t": 0, "m": np.zeros_like(params), "v": np.zeros_like(params)}
+    t0 = time.time()
+    done = 0
+    while True:
+        params = _oracle_step(sample, params, cfg, lc, state)
+        done += sample.n_struct
+        if time.time() - t0 >= seconds / 2:
+            break
+    dt = time.time() - t0
+    return {"value": done / dt, "unit": "structures/s", "cores": cores, "kind": "oracle",
+            "sample": f"{sample.n_struct} of the {wl} batch's {per} structures, fp64 torch CPU oracle fwd+bwd+Adam "
+                      f"({done} structure-steps in {dt:.1f} s)"}
+
+
+def run_reference(a, ws, rank):
+    if rank != 0:
+        return
+    wl, per = _workload(ws, a.per_gpu)
+    sample, params, cfg, lc, cores = _oracle_sample(wl, per, 8.0)
+    state = {"t": 0, "m": np.zeros_like(params), "v": np.zeros_like(params)}
+    for _ in range(a.warmup):
+        params = _oracle_step(sample, params, cfg, lc, state)
+    t0 = time.time()
+    for _ in range(a.steps):
+        params = _oracle_step(sample, params, cfg, lc, state)
+    dt = time.time() - t0
+    v = sample.n_struct * a.steps / dt
+    cb = {"value": v, "unit": "structures/s", "cores": cores, "kind": "oracle",
+          "sample": f"{sample.n_struct} structures of the {wl} batch per step (fp64 torch CPU oracle fwd+bwd+Adam)"}
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "structures/s", "n_gpus": ws, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": 1e3 * dt / a.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl, "structures_per_step": sample.n_struct, "host_threads": cores},
+        "cpu_baseline": cb, "e2e": {"value": v, "unit": "structures/s", "h2d_bytes_per_step": 0,
+                                    "d2h_bytes_per_step": 0}}), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def main():
+    a = _args()
+    ws, rank, local = _dist()
+    if a.impl == "reference":
+        run_reference(a, ws, rank)
+        return
+    import torch
+    import torch.distributed as dist
+    from chg_inputs import init_flat_params, make_config_batch, split_batch
+    from paper_2412_20796_b200 import chg
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    wl, per = _workload(ws, a.per_gpu)
+    stream = torch.cuda.Stream()
+    ctx = chg.Context(local, stream=stream.cuda_stream)
+    if ws > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(chg.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        ctx.set_nccl(bytes(uid.cpu().numpy()), ws, rank)
+    model = chg.Model(ctx)
+    layout = [(n, s) for n, s, _ in model.layout()]     # the library's own layout table
+    model.set_params(init_flat_params(layout, seed=0).astype(np.float32))
+
+    # ---- batches: global batch per index, balanced over ranks
+    batches = []
+    for bi in range(a.batches):
+        glob = make_config_batch(wl, bi, n_struct=per * ws)
+        if ws > 1:
+            g_all = ctx.build_graph(glob.atom_ptr, glob.positions, glob.lattice, glob.species)
+            ps = g_all.per_struct()
+            g_all.close()
+            loads = ps[:, 0] + ps[:, 1] + ps[:, 3]              # atoms + edges + angles (Q31)
+            rank_of = chg.balance(loads, ws)
+            mine = split_batch(glob, np.nonzero(rank_of == rank)[0].tolist())
+            per_rank_load = np.bincount(rank_of, weights=loads, minlength=ws)
+            contiguous = loads.reshape(ws, -1).sum(1) if glob.n_struct % ws == 0 else per_rank_load
+            cv = (float(per_rank_load.std() / per_rank_load.mean()), float(contiguous.std() / contiguous.mean()))
+        else:
+            mine, cv = glob, (0.0, 0.0)
+        gl = dict(S=glob.n_struct, N=glob.n_atoms, M=int(glob.magmom_mask.sum()))
+        dev = dict(pos=torch.as_tensor(mine.positions, device="cuda"),
+                   lat=torch.as_tensor(mine.lattice, device="cuda"),
+                   spec=torch.as_tensor(mine.species, device="cuda"),
+                   lab=dict(energy_per_atom=torch.as_tensor(mine.energy_per_atom, dtype=torch.float32, device="cuda"),
+                            forces=torch.as_tensor(mine.forces, dtype=torch.float32, device="cuda"),
+                            stress=torch.as_tensor(mine.stress, dtype=torch.float32, device="cuda"),
+                            magmom=torch.as_tensor(mine.magmom, dtype=torch.float32, device="cuda"),
+                            magmom_mask=torch.as_tensor(mine.magmom_mask, device="cuda")))
+
+        def pinned(x, dt):
+            t = torch.empty(x.shape, dtype=dt, pin_memory=True)
+            t.copy_(torch.as_tensor(np.ascontiguousarray(x)).to(dt))
+            return t.numpy()
+        host = dict(pos=pinned(mine.positions, torch.float64), lat=pinned(mine.lattice, torch.float64),
+                    spec=pinned(mine.species, torch.int32),
+                    lab=dict(energy_per_atom=pinned(mine.energy_per_atom, torch.float32),
+                             forces=pinned(mine.forces, torch.float32),
+                             stress=pinned(mine.stress, torch.float32),
+                             magmom=pinned(mine.magmom, torch.float32),
+                             magmom_mask=pinned(mine.magmom_mask, torch.uint8)))
+        h2d = sum(v.nbytes for k, v in host.items() if k != "lab") + sum(v.nbytes for v in host["lab"].values()) \
+            + mine.atom_ptr.nbytes
+        batches.append(dict(ap=mine.atom_ptr, dev=dev, host=host, gl=gl, S=mine.n_struct, cv=cv, h2d=h2d))
+
+    lr0 = (per * ws) / 128 * 3e-4                      # Eq. 14
+    total_steps = 2 * (a.warmup + a.steps) + 8
+    step_no = [0]
+
+    def one_step(b, on_host: bool):
+        step_no[0] += 1
+        lr = lr0 * 0.5 * (1 + math.cos(math.pi * step_no[0] / total_steps))   # cosine
+        src = b["host"] if on_host else b["dev"]
+        g = ctx.build_graph(b["ap"], src["pos"], src["lat"], src["spec"], 5.0, 3.0)
+        ctx.forward(model, g, train=True, host=False)
+        loss = ctx.backward(model, g, src["lab"], n_struct_global=b["gl"]["S"], n_atoms_global=b["gl"]["N"],
+                            n_magmom_global=b["gl"]["M"], sync_loss=on_host)
+        ctx.step(model, lr=lr, step=step_no[0], allreduce=ws > 1)
+        g.close()
+        return loss
+
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")     # 256 MiB > 126 MB L2
+
+    def barrier():
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(on_host: bool, profile: bool = False):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+        if profile:
+            ctx.profile(True)
+        l0 = ctx.launch_count()
+        barrier()
+        for k in range(a.steps):
+            b = batches[k % len(batches)]
+            ev[k][0].record(stream)
+            one_step(b, on_host)
+            ev[k][1].record(stream)
+            with torch.cuda.stream(stream):
+                flush.zero_()                              # L2 flush outside the timed events
+        barrier()
+        launches = ctx.launch_count() - l0
+        ms = sum(s.elapsed_time(e) for s, e in ev)
+        rep = ctx.profile_report() if profile else None
+        if profile:
+            ctx.profile(False)
+        if ws > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, launches, rep
+
+    for k in range(a.warmup):
+        one_step(batches[k % len(batches)], False)
+        one_step(batches[k % len(batches)], True)
+    clocks = Clocks(local)
+    clocks.start()
+    ms, launches, _ = timed(False)
+    clk = clocks.stop()
+    ms_e2e, _, _ = timed(True)
+    ms_prof, _, rep = timed(False, profile=True)
+
+    structs = sum(batches[k % len(batches)]["gl"]["S"] for k in range(a.steps)) / ws * ws
+    value = structs / (ms / 1e3)
+    e2e = structs / (ms_e2e / 1e3)
+    h2d = int(np.mean([batches[k % len(batches)]["h2d"] for k in range(a.steps)]))
+
+    # ---- roofline of the dominant op (live CUDA events, profiled pass of the same steps)
+    dom = max(rep, key=lambda t: rep[t]["ms"])
+    r = rep[dom]
+    per_launch_s = r["ms"] / 1e3 / max(r["launches"], 1)
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(dom)
+    except Exception:
+        pass
+    if dom in HBM_TAGS:
+        ach = r["bytes"] / (r["ms"] / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": PEAKS["hbm_gbs"], "unit": "GB/s"}
+    else:
+        ach = r["flops"] / (r["ms"] / 1e3) / 1e12
+        roof = {"bound": "alu", "achieved": ach, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s"}
+    roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": traffic, "kernel": dom,
+                 "algorithmic_per_launch": (r["bytes"] if roof["bound"] == "hbm" else r["flops"]) / max(r["launches"], 1),
+                 "avg_launch_us": per_launch_s * 1e6, "share_of_step": r["ms"] / ms_prof,
+                 "peak_source": PEAK_SRC if roof["bound"] == "hbm" else
+                 "FP32 CUDA cores: 148 SM x 128 FMA/clk x 2 x sm_max_mhz (DESIGN.md)"})
+    gs = rep.get("segsum", {"bytes": 0.0, "ms": 1e-9})
+    gather = {"kernel": "segsum (atomic-free CSR / rev / swap segmented gather-reduce)",
+              "achieved_gbs": gs["bytes"] / (gs["ms"] / 1e3) / 1e9,
+              "frac": gs["bytes"] / (gs["ms"] / 1e3) / 1e9 / PEAKS["hbm_gbs"], "peak_gbs": PEAKS["hbm_gbs"]}
+    ops = {t: {"ms_per_step": v["ms"] / a.steps, "launches_per_step": v["launches"] / a.steps,
+               "share": v["ms"] / ms_prof} for t, v in sorted(rep.items(), key=lambda kv: -kv[1]["ms"])}
+
+    if rank == 0:
+        cb = None
+        if not a.no_cpu_baseline and ws == 1:
+            cb = cpu_baseline(wl, per, a.cpu_seconds)
+        b0 = batches[0]
+        line = {
+            "metric": METRIC, "value": value, "unit": "structures/s", "n_gpus": ws, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{wl}: MPtrj-shaped synthetic batch, {per} structures per GPU "
+                                   f"(5/3 Å cutoffs, d=64, 4 atom-conv / 3 bond-conv)",
+                       "structures_per_gpu": per, "global_batch": per * ws, "parallelism": f"dp{ws}",
+                       "step": "build_graph + forward + backward + allreduce + Adam",
+                       "l2": "flushed between steps (256 MiB write, outside the timed events)",
+                       "batches_cycled": len(batches), "cv_balanced_vs_contiguous": b0["cv"],
+                       "rank0_counts_first_batch": None},
+            "e2e": {"value": e2e, "unit": "structures/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 40 + 4},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "roofline": roof,
+            "gather_scatter": gather,
+            "ops": ops,
+            "cpu_baseline": cb,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

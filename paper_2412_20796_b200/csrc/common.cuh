@@ -1,0 +1,204 @@
+// common.cuh — internal types and helpers of libchg (FastCHGNet training step, sm_100a).
+// Not part of the ABI; see include/chg.h for the public contract.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/chg.h"
+
+#define CHG_D 64          // feature width
+#define CHG_K 31          // radial / angular basis size
+#define CHG_KP 32         // padded basis row stride
+
+// ---------------------------------------------------------------------------
+// error handling: C++ exception inside the library, converted at the ABI edge
+// ---------------------------------------------------------------------------
+struct ChgError {
+  chg_status code;
+  std::string msg;
+};
+
+#define CHG_THROW(code, ...)                                   \
+  do {                                                         \
+    char _b[512];                                              \
+    snprintf(_b, sizeof(_b), __VA_ARGS__);                     \
+    throw ChgError{code, std::string(_b)};                     \
+  } while (0)
+
+#define CUDA_OK(x)                                                                       \
+  do {                                                                                   \
+    cudaError_t _e = (x);                                                                \
+    if (_e != cudaSuccess)                                                               \
+      CHG_THROW(CHG_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #x, cudaGetErrorString(_e)); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// context
+// ---------------------------------------------------------------------------
+struct chg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  int64_t launches = 0;
+  // named device workspaces (grow-only, stream-ordered reallocation)
+  std::map<std::string, std::pair<void *, size_t>> ws;
+  // pinned host staging
+  void *pinned = nullptr;
+  size_t pinned_bytes = 0;
+  // NCCL
+  void *nccl_comm = nullptr;
+  int nranks = 1, rank = 0;
+  // forward bookkeeping for backward
+  const chg_graph *fwd_graph = nullptr;
+  uint64_t fwd_graph_id = 0;
+  bool fwd_train = false;
+  // debug name -> (ptr, rows, cols, ld)
+  struct Dbg { const float *p; int64_t rows, cols, ld; };
+  std::map<std::string, Dbg> dbg;
+  // device scratch for flags / loss
+  int *d_flag = nullptr;
+  double *d_loss = nullptr;
+
+  // optional per-op device timing (chg_profile_*): CUDA events on the ctx stream
+  struct ProfRec { const char *tag; int ev; double flops, bytes; };
+  bool prof_on = false;
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  cudaEvent_t next_event();
+
+  void *get(const std::string &name, size_t bytes);
+  float *getf(const std::string &name, size_t n) { return (float *)get(name, n * sizeof(float)); }
+  void *pinned_get(size_t bytes);
+  void launched(int n = 1) { launches += n; }
+};
+
+// ---------------------------------------------------------------------------
+// graph (device CSR lists + per-structure data)
+// ---------------------------------------------------------------------------
+struct chg_graph {
+  chg_ctx *ctx = nullptr;
+  uint64_t id = 0;
+  int S = 0;
+  int64_t N = 0, E = 0, B = 0, A = 0;
+  double r_atom = 5.0, r_bond = 3.0;
+  std::vector<int64_t> atom_ptr_h;     // [S+1]
+  std::vector<int64_t> counts_h;       // [S*4] N,E,B,A
+  void *block = nullptr;               // one allocation for all arrays below
+  // per atom
+  int32_t *atom_ptr = nullptr;         // [S+1]
+  int32_t *struct_of_atom = nullptr;   // [N]
+  int32_t *species = nullptr;          // [N]
+  int32_t *row_ptr = nullptr;          // [N+1] edges by centre
+  int32_t *bond_ptr = nullptr;         // [N+1] bonds by centre
+  int32_t *atom_angle_ptr = nullptr;   // [N+1] angles by centre
+  int32_t *species_perm = nullptr;     // [N] atoms sorted by species
+  int32_t *species_ptr = nullptr;      // [n_species+1]
+  // per edge
+  int32_t *center = nullptr;           // [E]
+  int32_t *nbr = nullptr;              // [E]
+  char4 *img = nullptr;                // [E] (n1,n2,n3,0)
+  float4 *vec = nullptr;               // [E] (dx,dy,dz,|d|) fp32
+  double4 *vec64 = nullptr;            // [E] (dx,dy,dz,|d|) fp64 (basis geometry)
+  int32_t *bond_id = nullptr;          // [E] or -1
+  int32_t *rev = nullptr;              // [E]
+  // per bond
+  int32_t *bond_edge = nullptr;        // [B]
+  int32_t *angle_ptr = nullptr;        // [B+1]
+  // per angle
+  int32_t *angle_b1 = nullptr;         // [A]
+  int32_t *angle_b2 = nullptr;         // [A]
+  int32_t *angle_e1 = nullptr;         // [A] edge of b1
+  int32_t *angle_e2 = nullptr;         // [A] edge of b2
+  int32_t *angle_ctr = nullptr;        // [A] centre atom
+  int32_t *swap = nullptr;             // [A]
+  // per structure
+  float *lattice_f = nullptr;          // [S*9]
+  float *inv_natoms = nullptr;         // [S]
+};
+
+// ---------------------------------------------------------------------------
+// model
+// ---------------------------------------------------------------------------
+struct chg_model {
+  chg_ctx *ctx = nullptr;
+  chg_model_cfg cfg{};
+  int64_t P = 0;
+  float *params = nullptr, *grads = nullptr, *m = nullptr, *v = nullptr;
+  std::vector<std::string> names;
+  std::vector<const char *> name_ptrs;
+  std::vector<int64_t> offsets;
+  std::vector<int32_t> shapes;   // 2 per tensor
+  std::map<std::string, int> index;
+  // table of 2-D tensors for the transposed-weight copy used by the backward
+  int n2d = 0;
+  int64_t *d_toff = nullptr;
+  int32_t *d_trc = nullptr;
+
+  int64_t off(const std::string &n) const {
+    auto it = index.find(n);
+    if (it == index.end()) CHG_THROW(CHG_ERR_ARG, "no parameter %s", n.c_str());
+    return offsets[it->second];
+  }
+  float *p(const std::string &n) const { return params + off(n); }
+  float *g(const std::string &n) const { return grads + off(n); }
+};
+
+// ---------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float sigmoidf_(float x) { return 1.0f / (1.0f + __expf(-x)); }
+__device__ __forceinline__ float siluf_(float x) { return x * sigmoidf_(x); }
+__device__ __forceinline__ float dsiluf_(float x) {
+  float s = sigmoidf_(x);
+  return s * (1.0f + x * (1.0f - s));
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// RAII device-time scope: records an event pair around the launches it covers
+// when profiling is on (algorithmic flops / bytes supplied by the caller).
+struct ProfScope {
+  chg_ctx *ctx;
+  int ev = -1;
+  ProfScope(chg_ctx *c, const char *tag, double flops, double bytes) : ctx(c) {
+    if (!ctx->prof_on) return;
+    cudaEvent_t a = ctx->next_event();
+    ctx->next_event();
+    ev = (int)ctx->ev_used - 2;
+    cudaEventRecord(a, ctx->stream);
+    ctx->prof.push_back({tag, ev, flops, bytes});
+  }
+  ~ProfScope() {
+    if (ev >= 0) cudaEventRecord(ctx->ev_pool[ev + 1], ctx->stream);
+  }
+};
+
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+inline void check_launch(chg_ctx *ctx) {
+  ctx->launched();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) CHG_THROW(CHG_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+}
+
+// graph.cu
+chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const double *pos,
+                            const double *lat, const int32_t *species, double r_atom, double r_bond,
+                            int on_device, int n_species);

@@ -1,0 +1,305 @@
+// gemm.cu — fp32 CUDA-core GEMMs of the strict-parity path (see gemm.cuh).
+#include "gemm.cuh"
+
+namespace {
+
+constexpr int TM = 128, TN = 64, TK = 32;
+
+// A(m, col) for 4 consecutive columns (segment widths are multiples of 4)
+__device__ __forceinline__ float4 loadA4(const AOp &A, int m, int col) {
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  int start = 0;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    if (s < A.nseg) {
+      int w = A.seg[s].width;
+      if (col >= start && col < start + w) {
+        int row = A.seg[s].idx ? __ldg(A.seg[s].idx + m) : m;
+        if (row >= 0) v = __ldg((const float4 *)(A.seg[s].base + (size_t)row * A.seg[s].ld + (col - start)));
+      }
+      start += w;
+    }
+  }
+  if (A.act == 1) { v.x = siluf_(v.x); v.y = siluf_(v.y); v.z = siluf_(v.z); v.w = siluf_(v.w); }
+  return v;
+}
+
+__device__ __forceinline__ float loadA1(const AOp &A, int m, int col) {
+  float v = 0.f;
+  int start = 0;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    if (s < A.nseg) {
+      int w = A.seg[s].width;
+      if (col >= start && col < start + w) {
+        int row = A.seg[s].idx ? __ldg(A.seg[s].idx + m) : m;
+        if (row >= 0) v = __ldg(A.seg[s].base + (size_t)row * A.seg[s].ld + (col - start));
+      }
+      start += w;
+    }
+  }
+  if (A.act == 1) v = siluf_(v);
+  return v;
+}
+
+__device__ __forceinline__ float loadW(const Chunk &c, int k, int n) {
+  if (n >= c.ncols) return 0.f;
+#pragma unroll
+  for (int b = 0; b < 4; ++b)
+    if (b < c.nwb && k >= c.wk0[b] && k < c.wk0[b + 1])
+      return __ldg(c.W[b] + (size_t)(k - c.wk0[b]) * c.ldw[b] + n);
+  return 0.f;
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(256) k_rowgemm(const RowGemm g) {
+  __shared__ __align__(16) float As[TK][TM + 4];
+  __shared__ __align__(16) float Ws[TK][TN];
+  const Chunk &c = g.ch[blockIdx.y];
+  const int m0 = blockIdx.x * TM;
+  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+  float acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+
+  for (int k0 = 0; k0 < g.K; k0 += TK) {
+    if (VEC) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        int r = (t >> 3) + 32 * i, c4 = t & 7;
+        int m = m0 + r, kk = k0 + 4 * c4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (m < g.M && kk < g.K) v = loadA4(g.A, m, c.a_k0 + kk);
+        As[4 * c4 + 0][r] = v.x; As[4 * c4 + 1][r] = v.y; As[4 * c4 + 2][r] = v.z; As[4 * c4 + 3][r] = v.w;
+      }
+    } else {
+#pragma unroll 4
+      for (int i = 0; i < (TM * TK) / 256; ++i) {
+        int e = t + 256 * i, r = e / TK, kk = e % TK;
+        int m = m0 + r, k = k0 + kk;
+        As[kk][r] = (m < g.M && k < g.K) ? loadA1(g.A, m, c.a_k0 + k) : 0.f;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < (TK * TN) / 256; ++i) {
+      int e = t + 256 * i, kr = e / TN, n = e % TN;
+      int k = k0 + kr;
+      Ws[kr][n] = (k < g.K) ? loadW(c, k, n) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < TK; ++kk) {
+      float4 a0 = *(const float4 *)&As[kk][ty * 8];
+      float4 a1 = *(const float4 *)&As[kk][ty * 8 + 4];
+      float4 b = *(const float4 *)&Ws[kk][tx * 4];
+      float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      float bb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], bb[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  // epilogue
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    int m = m0 + ty * 8 + i;
+    if (m >= g.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int n = tx * 4 + j;
+      if (n >= c.ncols) continue;
+      float v = acc[i][j];
+      if (c.bias) v += __ldg(c.bias + n);
+      if (c.pre) c.pre[(size_t)m * c.ldp + n] = v;
+      if (g.act == 1) v = siluf_(v);
+      if (c.mul) v *= dsiluf_(c.mul[(size_t)m * c.ldm + n]);
+      if (c.resid) v += c.resid[(size_t)m * c.ldr + n];
+      c.out[(size_t)m * c.ldo + n] = v;
+    }
+  }
+}
+
+constexpr int WK = 64, WN = 64, WM = 32;
+
+template <bool VEC>
+__global__ void __launch_bounds__(256) k_wgrad(const WGrad g, float *__restrict__ partial, int Kp, int rows_per_split) {
+  __shared__ __align__(16) float As[WM][WK + 4];
+  __shared__ __align__(16) float Ds[WM][WN + 4];
+  const int kt = blockIdx.x, nt = blockIdx.y, sp = blockIdx.z;
+  const int mb = sp * rows_per_split, me = min(g.M, mb + rows_per_split);
+  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  const bool dvec = VEC && (g.ldd % 4 == 0) && (g.N % 4 == 0);
+  for (int m0 = mb; m0 < me; m0 += WM) {
+    // A tile [WM][WK]
+    if (VEC) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        int e = t + 256 * i, r = e >> 4, c4 = e & 15;
+        int m = m0 + r, col = kt * WK + 4 * c4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (m < me) {
+          if (col < g.K) v = loadA4(g.A, m, col);
+          float *pv = &v.x;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (col + q >= g.K) pv[q] = 0.f;
+            if (g.bias && col + q == g.K) pv[q] = 1.f;
+          }
+        }
+        *(float4 *)&As[r][4 * c4] = v;
+      }
+    } else {
+#pragma unroll 4
+      for (int i = 0; i < (WM * WK) / 256; ++i) {
+        int e = t + 256 * i, r = e / WK, cc = e % WK;
+        int m = m0 + r, col = kt * WK + cc;
+        float v = 0.f;
+        if (m < me) {
+          if (col < g.K) v = loadA1(g.A, m, col);
+          else if (g.bias && col == g.K) v = 1.f;
+        }
+        As[r][cc] = v;
+      }
+    }
+    // D tile [WM][WN]
+    if (dvec) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        int e = t + 256 * i, r = e >> 4, c4 = e & 15;
+        int m = m0 + r, n = nt * WN + 4 * c4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (m < me && n < g.N) {
+          int row = g.didx ? __ldg(g.didx + m) : m;
+          v = __ldg((const float4 *)(g.D + (size_t)row * g.ldd + n));
+        }
+        *(float4 *)&Ds[r][4 * c4] = v;
+      }
+    } else {
+#pragma unroll 4
+      for (int i = 0; i < (WM * WN) / 256; ++i) {
+        int e = t + 256 * i, r = e / WN, cc = e % WN;
+        int m = m0 + r, n = nt * WN + cc;
+        float v = 0.f;
+        if (m < me && n < g.N) {
+          int row = g.didx ? __ldg(g.didx + m) : m;
+          v = __ldg(g.D + (size_t)row * g.ldd + n);
+        }
+        Ds[r][cc] = v;
+      }
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int r = 0; r < WM; ++r) {
+      float4 a = *(const float4 *)&As[r][ty * 4];
+      float4 d = *(const float4 *)&Ds[r][tx * 4];
+      float av[4] = {a.x, a.y, a.z, a.w}, dv[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], dv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  float *P = partial + (size_t)sp * Kp * g.N;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int k = kt * WK + ty * 4 + i;
+    if (k >= Kp) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int n = nt * WN + tx * 4 + j;
+      if (n < g.N) P[(size_t)k * g.N + n] = acc[i][j];
+    }
+  }
+}
+
+__global__ void k_wgrad_reduce(const WGrad g, const float *__restrict__ partial, int Kp, int splits) {
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= Kp * g.N) return;
+  int k = idx / g.N, n = idx % g.N;
+  float s = 0.f;
+  for (int sp = 0; sp < splits; ++sp) s += partial[(size_t)sp * Kp * g.N + idx];
+  const WGradDst &d = g.dst[n / 64];
+  int nn = n % 64;
+  if (k < g.K) {
+    if (d.W) d.W[(size_t)k * d.ldw + nn] += s;
+  } else if (d.b) {
+    d.b[nn] += s;
+  }
+}
+
+bool aop_vec(const AOp &A) {
+  for (int s = 0; s < A.nseg; ++s) {
+    const ASeg &S = A.seg[s];
+    if (S.width % 4 || S.ld % 4 || ((uintptr_t)S.base & 15)) return false;
+  }
+  return true;
+}
+
+}  // namespace
+
+void rowgemm(chg_ctx *ctx, const RowGemm &g) {
+  if (g.M <= 0) return;
+  bool vec = aop_vec(g.A);
+  int tot = 0;
+  for (int s = 0; s < g.A.nseg; ++s) tot += g.A.seg[s].width;
+  for (int c = 0; c < g.nchunk; ++c)
+    if (g.ch[c].a_k0 + ((g.K + 3) & ~3) > tot) vec = false;
+  // algorithmic work: 2·M·K·Σncols flops; bytes = A columns read once (union of
+  // chunk windows) + gather indices + outputs (+pre/mul/resid) + weights
+  double cols = 0, outb = 0, wb = 0;
+  int lo = 1 << 30, hi = 0;
+  for (int c = 0; c < g.nchunk; ++c) {
+    const Chunk &C = g.ch[c];
+    cols += C.ncols;
+    outb += C.ncols * (1.0 + (C.pre != nullptr) + (C.mul != nullptr) + (C.resid != nullptr));
+    wb += (double)g.K * C.ncols;
+    lo = std::min(lo, C.a_k0);
+    hi = std::max(hi, C.a_k0 + g.K);
+  }
+  double idxb = 0;
+  for (int s = 0; s < g.A.nseg; ++s) idxb += g.A.seg[s].idx ? 4.0 : 0.0;
+  ProfScope ps(ctx, "rowgemm", 2.0 * g.M * (double)g.K * cols,
+               (double)g.M * (4.0 * std::min(hi - lo, tot) + idxb + 4.0 * outb) + 4.0 * wb);
+  dim3 grid(ceil_div(g.M, TM), g.nchunk);
+  if (vec)
+    k_rowgemm<true><<<grid, 256, 0, ctx->stream>>>(g);
+  else
+    k_rowgemm<false><<<grid, 256, 0, ctx->stream>>>(g);
+  check_launch(ctx);
+}
+
+void wgrad(chg_ctx *ctx, const WGrad &g) {
+  int Kp = g.K + (g.bias ? 1 : 0);
+  if (Kp <= 0 || g.N <= 0) return;
+  int ktiles = ceil_div(Kp, WK), ntiles = ceil_div(g.N, WN);
+  int splits = 1;
+  if (g.M > 0) {
+    splits = std::max(1, std::min(ceil_div(g.M, WM), 296 / (ktiles * ntiles)));
+  }
+  int rps = g.M > 0 ? ceil_div(ceil_div(g.M, splits), WM) * WM : WM;
+  splits = g.M > 0 ? ceil_div(g.M, rps) : 1;
+  float *partial = ctx->getf("wgrad_partial", (size_t)splits * Kp * g.N);
+  double idxb = 0;
+  for (int s = 0; s < g.A.nseg; ++s) idxb += g.A.seg[s].idx ? 4.0 : 0.0;
+  ProfScope ps(ctx, "wgrad", 2.0 * g.M * (double)Kp * g.N,
+               (double)g.M * (4.0 * g.K + idxb + 4.0 * g.N + (g.didx ? 4.0 : 0.0)) + 4.0 * Kp * g.N);
+  bool vec = aop_vec(g.A);
+  dim3 grid(ktiles, ntiles, splits);
+  if (vec)
+    k_wgrad<true><<<grid, 256, 0, ctx->stream>>>(g, partial, Kp, rps);
+  else
+    k_wgrad<false><<<grid, 256, 0, ctx->stream>>>(g, partial, Kp, rps);
+  check_launch(ctx);
+  k_wgrad_reduce<<<ceil_div(Kp * g.N, 256), 256, 0, ctx->stream>>>(g, partial, Kp, splits);
+  check_launch(ctx);
+}

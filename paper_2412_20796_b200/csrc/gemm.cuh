@@ -1,0 +1,78 @@
+// gemm.cuh — fp32 CUDA-core GEMM engine of the strict-parity path.
+//
+// Row GEMM: out[m, n] = epi( Σ_k A(m, k) · W(k, n) + b[n] ) with A gathered on the
+// fly from up to 4 row tables (the concatenations [v_i, v_j, e_ij] of Eq. 4 and
+// [v_i, e_ij, e_ik, a_ijk] of Eq. 5/6 are never materialised), W split in up to
+// 4 row blocks (weight concatenation of Fig. 3a without copying), and up to 4
+// output column chunks of 64 with their own W / bias / destination (core and
+// gate branches of Fig. 3b in one launch).
+//
+// Weight-gradient GEMM: G[k, n] += Σ_m A(m, k) · D(m, n) (+ column sums of D as
+// the bias gradient), split over m across CTAs, partials reduced in a fixed
+// order (deterministic, no atomics).
+#pragma once
+#include "common.cuh"
+
+struct ASeg {
+  const float *base = nullptr;   // row table
+  const int32_t *idx = nullptr;  // row index per m (nullptr = m); idx < 0 -> zero row
+  int ld = 0;                    // row stride (floats)
+  int width = 0;                 // columns contributed by this segment
+};
+
+struct AOp {
+  ASeg seg[4];
+  int nseg = 0;
+  int act = 0;                   // 0: identity, 1: silu applied on load
+};
+
+struct Chunk {
+  const float *W[4] = {nullptr, nullptr, nullptr, nullptr};  // row blocks of W
+  int ldw[4] = {0, 0, 0, 0};
+  int wk0[5] = {0, 0, 0, 0, 0};  // row-block starts, wk0[nwb] = K
+  int nwb = 1;
+  const float *bias = nullptr;
+  int a_k0 = 0;                  // first A column read by this chunk
+  int ncols = 64;                // valid output columns (<= 64)
+  float *out = nullptr; int ldo = 0;
+  const float *resid = nullptr; int ldr = 0;   // added after activation
+  float *pre = nullptr; int ldp = 0;           // pre-activation store
+  const float *mul = nullptr; int ldm = 0;     // v *= dsilu(mul) (backward of silu)
+};
+
+struct RowGemm {
+  AOp A;
+  int M = 0;
+  int K = 0;                     // reduction length (per chunk)
+  int act = 0;                   // 0 none, 1 silu
+  int nchunk = 1;
+  Chunk ch[4];
+};
+
+struct WGradDst {
+  float *W = nullptr; int ldw = 0;   // gradient of W columns [n0, n0+64), rows 0..K-1
+  float *b = nullptr;                // gradient of bias (column sums), optional
+};
+
+struct WGrad {
+  AOp A;                         // A(m, k), k < K
+  int M = 0, K = 0;
+  const float *D = nullptr;      // D(m, n) = D[(didx ? didx[m] : m) * ldd + n]
+  const int32_t *didx = nullptr;
+  int ldd = 0;
+  int N = 0;                     // columns of D (<= 256)
+  int bias = 0;                  // 1: also column sums of D -> dst.b
+  WGradDst dst[4];               // per 64-column chunk of N
+};
+
+void rowgemm(chg_ctx *ctx, const RowGemm &g);
+void wgrad(chg_ctx *ctx, const WGrad &g);
+
+// helpers to fill descriptors
+inline ASeg aseg(const float *base, int ld, int width, const int32_t *idx = nullptr) {
+  ASeg s; s.base = base; s.ld = ld; s.width = width; s.idx = idx; return s;
+}
+inline Chunk chunk1(const float *W, int ldw, int K, const float *bias, float *out, int ldo, int ncols = 64) {
+  Chunk c; c.W[0] = W; c.ldw[0] = ldw; c.wk0[0] = 0; c.wk0[1] = K; c.nwb = 1; c.bias = bias;
+  c.out = out; c.ldo = ldo; c.ncols = ncols; return c;
+}

@@ -1,0 +1,588 @@
+// graph.cu — A1: periodic atom graph, bond graph and angle list on the GPU.
+//
+// Paper: P:95 (§II-B(1) graph extraction), Alg. 1 lines P:253-256 (r_j += I@L,
+// r_ij = r_i − r_j), Alg. 2 P:294-326 (whole batch at once; the block-diagonal
+// image matrix is realised per structure segment, never materialised).
+// Readings: Q8 directed edges, Q9 ordered angle pairs of distinct
+// bond edges, Q10 closed cutoff with ONE canonical fp64 evaluation per
+// unordered pair (no FMA: __dmul_rn/__dadd_rn), Q11 d = r_i − (r_j + nL).
+//
+// Kernels (one warp per centre atom for the pair search, which keeps the
+// (i, j, n1, n2, n3) output order without a sort):
+//   k_frac      fractional coordinates (image ranges only) + finite/species checks
+//   k_count     per centre atom: accepted edges and bond edges          (G1)
+//   k_scan      exclusive scans: edges, bonds, angles m(m−1) per atom    (G2)
+//   k_fill      ordered emission with warp ballot/scan                  (G3)
+//   k_angles    angle pairs, swap map, per-angle edge/centre indices    (G4)
+//   k_rev       reverse-edge map by binary search in row j              (G4)
+//   k_species   stable counting sort of atoms by species (embedding grad)
+#include <cmath>
+
+#include "common.cuh"
+
+namespace {
+
+struct StructGeo {
+  double L[9];      // rows = lattice vectors
+  double Linv[9];
+  double rw[3];     // r_atom / perpendicular width
+  double pad;
+};
+
+__device__ __forceinline__ bool lexpos(int n1, int n2, int n3) {
+  return n1 > 0 || (n1 == 0 && (n2 > 0 || (n2 == 0 && n3 > 0)));
+}
+
+// Canonical evaluation of candidate (i, j, n): see oracle/graph.py docstring.
+__device__ __forceinline__ void eval_pair(const double *__restrict__ pos, const double *L, int i, int j,
+                                          int n1, int n2, int n3, double &dx, double &dy, double &dz,
+                                          double &q) {
+  bool flip = (i > j) || (i == j && !lexpos(n1, n2, n3));
+  int a = flip ? j : i, b = flip ? i : j;
+  double m1 = flip ? -n1 : n1, m2 = flip ? -n2 : n2, m3 = flip ? -n3 : n3;
+  double t[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    double v = pos[3 * b + c];
+    v = __dadd_rn(v, __dmul_rn(m1, L[0 + c]));
+    v = __dadd_rn(v, __dmul_rn(m2, L[3 + c]));
+    v = __dadd_rn(v, __dmul_rn(m3, L[6 + c]));
+    t[c] = v;
+  }
+  dx = __dsub_rn(pos[3 * a + 0], t[0]);
+  dy = __dsub_rn(pos[3 * a + 1], t[1]);
+  dz = __dsub_rn(pos[3 * a + 2], t[2]);
+  q = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+  if (flip) { dx = -dx; dy = -dy; dz = -dz; }
+}
+
+struct Range { int lo[3], hi[3]; };
+
+__device__ __forceinline__ Range pair_range(const double *fi, const double *fj, const double *rw) {
+  Range r;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double df = fi[k] - fj[k];
+    r.lo[k] = (int)ceil(df - rw[k]) - 1;
+    r.hi[k] = (int)floor(df + rw[k]) + 1;
+  }
+  return r;
+}
+
+__global__ void k_frac(int N, const double *__restrict__ pos, const int32_t *__restrict__ soa,
+                       const StructGeo *__restrict__ geo, const int32_t *__restrict__ species,
+                       int n_species, double *__restrict__ frac, int *flag) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const StructGeo &g = geo[soa[i]];
+  double p[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+  if (!isfinite(p[0]) || !isfinite(p[1]) || !isfinite(p[2])) atomicOr(flag, 1);
+  int z = species[i];
+  if (z < 1 || z > n_species) atomicOr(flag, 2);
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+    frac[3 * i + c] = p[0] * g.Linv[0 + c] + p[1] * g.Linv[3 + c] + p[2] * g.Linv[6 + c];
+}
+
+__global__ void k_count(int N, const double *__restrict__ pos, const double *__restrict__ frac,
+                        const int32_t *__restrict__ soa, const int32_t *__restrict__ atom_ptr,
+                        const StructGeo *__restrict__ geo, double ra2, double rb2,
+                        int32_t *__restrict__ cnt_e, int32_t *__restrict__ cnt_b, int *flag) {
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (warp >= N) return;
+  int i = warp;
+  int s = soa[i];
+  int a0 = atom_ptr[s], a1 = atom_ptr[s + 1];
+  const StructGeo &g = geo[s];
+  double L[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) L[k] = g.L[k];
+  double fi[3] = {frac[3 * i], frac[3 * i + 1], frac[3 * i + 2]};
+  int ce = 0, cb = 0, bad = 0;
+  for (int j = a0 + lane; j < a1; j += 32) {
+    double fj[3] = {frac[3 * j], frac[3 * j + 1], frac[3 * j + 2]};
+    Range r = pair_range(fi, fj, g.rw);
+    for (int n1 = r.lo[0]; n1 <= r.hi[0]; ++n1)
+      for (int n2 = r.lo[1]; n2 <= r.hi[1]; ++n2)
+        for (int n3 = r.lo[2]; n3 <= r.hi[2]; ++n3) {
+          if (i == j && n1 == 0 && n2 == 0 && n3 == 0) continue;
+          double dx, dy, dz, q;
+          eval_pair(pos, L, i, j, n1, n2, n3, dx, dy, dz, q);
+          if (q <= ra2) {
+            ++ce;
+            cb += (q <= rb2);
+            bad |= (q < 1e-12);
+          }
+        }
+  }
+  ce = __reduce_add_sync(0xffffffffu, ce);
+  cb = __reduce_add_sync(0xffffffffu, cb);
+  bad = __any_sync(0xffffffffu, bad);
+  if (lane == 0) {
+    cnt_e[i] = ce;
+    cnt_b[i] = cb;
+    if (bad) atomicOr(flag, 4);
+  }
+}
+
+// single-block exclusive scans of cnt_e, cnt_b and m(m-1); totals (int64) to tot[0..2]
+__global__ void k_scan(int N, const int32_t *__restrict__ cnt_e, const int32_t *__restrict__ cnt_b,
+                       int32_t *__restrict__ row_ptr, int32_t *__restrict__ bond_ptr,
+                       int32_t *__restrict__ ang_ptr, long long *tot) {
+  __shared__ long long sh[3][1024];
+  int t = threadIdx.x;
+  int per = (N + blockDim.x - 1) / blockDim.x;
+  int i0 = min(N, t * per), i1 = min(N, i0 + per);
+  long long se = 0, sb = 0, sa = 0;
+  for (int i = i0; i < i1; ++i) {
+    long long m = cnt_b[i];
+    se += cnt_e[i]; sb += m; sa += m * (m - 1);
+  }
+  sh[0][t] = se; sh[1][t] = sb; sh[2][t] = sa;
+  __syncthreads();
+  for (int off = 1; off < blockDim.x; off <<= 1) {
+    long long v0 = 0, v1 = 0, v2 = 0;
+    if (t >= off) { v0 = sh[0][t - off]; v1 = sh[1][t - off]; v2 = sh[2][t - off]; }
+    __syncthreads();
+    sh[0][t] += v0; sh[1][t] += v1; sh[2][t] += v2;
+    __syncthreads();
+  }
+  long long be = sh[0][t] - se, bb = sh[1][t] - sb, ba = sh[2][t] - sa;
+  for (int i = i0; i < i1; ++i) {
+    long long m = cnt_b[i];
+    row_ptr[i] = (int32_t)be; bond_ptr[i] = (int32_t)bb; ang_ptr[i] = (int32_t)ba;
+    be += cnt_e[i]; bb += m; ba += m * (m - 1);
+  }
+  if (t == blockDim.x - 1) {
+    tot[0] = sh[0][t]; tot[1] = sh[1][t]; tot[2] = sh[2][t];
+    if (sh[0][t] < 2147483647LL && sh[2][t] < 2147483647LL) {
+      row_ptr[N] = (int32_t)sh[0][t]; bond_ptr[N] = (int32_t)sh[1][t]; ang_ptr[N] = (int32_t)sh[2][t];
+    }
+  }
+}
+
+__device__ __forceinline__ int warp_excl_scan(int v, int lane, int &total) {
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  total = __shfl_sync(0xffffffffu, x, 31);
+  return x - v;
+}
+
+__global__ void k_fill(int N, const double *__restrict__ pos, const double *__restrict__ frac,
+                       const int32_t *__restrict__ soa, const int32_t *__restrict__ atom_ptr,
+                       const StructGeo *__restrict__ geo, double ra2, double rb2,
+                       const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ bond_ptr,
+                       int32_t *__restrict__ center, int32_t *__restrict__ nbr, char4 *__restrict__ img,
+                       float4 *__restrict__ vec, double4 *__restrict__ vec64, int32_t *__restrict__ bond_id,
+                       int32_t *__restrict__ bond_edge) {
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (warp >= N) return;
+  int i = warp;
+  int s = soa[i];
+  int a0 = atom_ptr[s], a1 = atom_ptr[s + 1];
+  const StructGeo &g = geo[s];
+  double L[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) L[k] = g.L[k];
+  double fi[3] = {frac[3 * i], frac[3 * i + 1], frac[3 * i + 2]};
+  int be = row_ptr[i], bb = bond_ptr[i];
+  for (int j0 = a0; j0 < a1; j0 += 32) {
+    int j = j0 + lane;
+    bool act = j < a1;
+    Range r;
+    int ce = 0, cb = 0;
+    if (act) {
+      double fj[3] = {frac[3 * j], frac[3 * j + 1], frac[3 * j + 2]};
+      r = pair_range(fi, fj, g.rw);
+      for (int n1 = r.lo[0]; n1 <= r.hi[0]; ++n1)
+        for (int n2 = r.lo[1]; n2 <= r.hi[1]; ++n2)
+          for (int n3 = r.lo[2]; n3 <= r.hi[2]; ++n3) {
+            if (i == j && n1 == 0 && n2 == 0 && n3 == 0) continue;
+            double dx, dy, dz, q;
+            eval_pair(pos, L, i, j, n1, n2, n3, dx, dy, dz, q);
+            if (q <= ra2) { ++ce; cb += (q <= rb2); }
+          }
+    }
+    int te, tb;
+    int oe = warp_excl_scan(ce, lane, te);
+    int ob = warp_excl_scan(cb, lane, tb);
+    if (act && ce > 0) {
+      int e = be + oe, b = bb + ob;
+      for (int n1 = r.lo[0]; n1 <= r.hi[0]; ++n1)
+        for (int n2 = r.lo[1]; n2 <= r.hi[1]; ++n2)
+          for (int n3 = r.lo[2]; n3 <= r.hi[2]; ++n3) {
+            if (i == j && n1 == 0 && n2 == 0 && n3 == 0) continue;
+            double dx, dy, dz, q;
+            eval_pair(pos, L, i, j, n1, n2, n3, dx, dy, dz, q);
+            if (q <= ra2) {
+              center[e] = i;
+              nbr[e] = j;
+              img[e] = make_char4((signed char)n1, (signed char)n2, (signed char)n3, 0);
+              double rr = sqrt(q);
+              vec[e] = make_float4((float)dx, (float)dy, (float)dz, (float)rr);
+              vec64[e] = make_double4(dx, dy, dz, rr);
+              if (q <= rb2) {
+                bond_id[e] = b;
+                bond_edge[b] = e;
+                ++b;
+              } else {
+                bond_id[e] = -1;
+              }
+              ++e;
+            }
+          }
+    }
+    be += te;
+    bb += tb;
+  }
+}
+
+__global__ void k_angles(int B, const int32_t *__restrict__ bond_edge, const int32_t *__restrict__ center,
+                         const int32_t *__restrict__ bond_ptr, const int32_t *__restrict__ atom_angle_ptr,
+                         int32_t *__restrict__ angle_ptr, int32_t *__restrict__ ab1,
+                         int32_t *__restrict__ ab2, int32_t *__restrict__ ae1, int32_t *__restrict__ ae2,
+                         int32_t *__restrict__ actr, int32_t *__restrict__ swp, int A) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) {
+    if (b == B) angle_ptr[B] = A;
+    return;
+  }
+  int e = bond_edge[b];
+  int i = center[e];
+  int bs = bond_ptr[i], m = bond_ptr[i + 1] - bs, p = b - bs;
+  int abase = atom_angle_ptr[i];
+  int row = abase + p * (m - 1);
+  angle_ptr[b] = row;
+  int k = 0;
+  for (int q = 0; q < m; ++q) {
+    if (q == p) continue;
+    int idx = row + k;
+    ab1[idx] = b;
+    ab2[idx] = bs + q;
+    ae1[idx] = e;
+    ae2[idx] = bond_edge[bs + q];
+    actr[idx] = i;
+    swp[idx] = abase + q * (m - 1) + (p < q ? p : p - 1);
+    ++k;
+  }
+}
+
+__device__ __forceinline__ long long edge_key(int nb, char4 im) {
+  return ((long long)nb << 24) | ((long long)((int)im.x + 128) << 16) | ((long long)((int)im.y + 128) << 8) |
+         (long long)((int)im.z + 128);
+}
+
+__global__ void k_rev(int E, const int32_t *__restrict__ center, const int32_t *__restrict__ nbr,
+                      const char4 *__restrict__ img, const int32_t *__restrict__ row_ptr,
+                      int32_t *__restrict__ rev, int *flag) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  int i = center[e], j = nbr[e];
+  char4 n = img[e];
+  char4 mn = make_char4(-n.x, -n.y, -n.z, 0);
+  long long key = edge_key(i, mn);
+  int lo = row_ptr[j], hi = row_ptr[j + 1] - 1, found = -1;
+  while (lo <= hi) {
+    int mid = (lo + hi) >> 1;
+    long long k = edge_key(nbr[mid], img[mid]);
+    if (k == key) { found = mid; break; }
+    if (k < key) lo = mid + 1; else hi = mid - 1;
+  }
+  rev[e] = found;
+  if (found < 0) atomicOr(flag, 8);
+}
+
+// stable counting sort of atoms by species, one warp (deterministic)
+__global__ void k_species(int N, int n_species, const int32_t *__restrict__ species,
+                          int32_t *__restrict__ perm, int32_t *__restrict__ sptr) {
+  extern __shared__ int cnt[];   // n_species + 1
+  int lane = threadIdx.x;
+  for (int z = lane; z <= n_species; z += 32) cnt[z] = 0;
+  __syncwarp();
+  for (int i0 = 0; i0 < N; i0 += 32) {
+    int i = i0 + lane;
+    int z = i < N ? species[i] : -1;
+    unsigned m = __match_any_sync(0xffffffffu, z);
+    int leader = __ffs(m) - 1;
+    if (i < N && lane == leader) cnt[z] += __popc(m);
+    __syncwarp();
+  }
+  if (lane == 0) {
+    int acc = 0;
+    for (int z = 0; z <= n_species; ++z) { int c = cnt[z]; cnt[z] = acc; sptr[z] = acc; acc += c; }
+    sptr[n_species + 1] = acc;
+  }
+  __syncwarp();
+  for (int i0 = 0; i0 < N; i0 += 32) {
+    int i = i0 + lane;
+    int z = i < N ? species[i] : -1;
+    unsigned m = __match_any_sync(0xffffffffu, z);
+    int rank = __popc(m & ((1u << lane) - 1));
+    int leader = __ffs(m) - 1;
+    if (i < N) perm[cnt[z] + rank] = i;
+    __syncwarp();
+    if (i < N && lane == leader) cnt[z] += __popc(m);
+    __syncwarp();
+  }
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct GraphBlocks { void *a = nullptr, *b = nullptr; };
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host orchestration
+// ---------------------------------------------------------------------------
+static uint64_t g_graph_counter = 0;
+
+chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const double *pos,
+                            const double *lat, const int32_t *species, double r_atom, double r_bond,
+                            int on_device, int n_species) {
+  if (S < 0 || (S > 0 && (!atom_ptr || !pos || !lat || !species)))
+    CHG_THROW(CHG_ERR_ARG, "null input");
+  if (!(r_bond > 0 && r_bond <= r_atom) || !std::isfinite(r_atom))
+    CHG_THROW(CHG_ERR_ARG, "need 0 < r_bond <= r_atom (got %g, %g)", r_atom, r_bond);
+  if (S > 0 && atom_ptr[0] != 0) CHG_THROW(CHG_ERR_ARG, "atom_ptr[0] must be 0");
+  for (int s = 0; s < S; ++s)
+    if (atom_ptr[s + 1] < atom_ptr[s]) CHG_THROW(CHG_ERR_ARG, "atom_ptr not monotone at %d", s);
+  int64_t N = S > 0 ? atom_ptr[S] : 0;
+  if (N >= (1LL << 31) / 64) CHG_THROW(CHG_ERR_CAPACITY, "too many atoms (%lld)", (long long)N);
+  cudaStream_t st = ctx->stream;
+
+  // lattice on host (S*72 B) for validation and per-structure geometry
+  std::vector<double> L(9 * (size_t)S);
+  if (S > 0) {
+    if (on_device) {
+      CUDA_OK(cudaMemcpyAsync(L.data(), lat, 9 * sizeof(double) * S, cudaMemcpyDeviceToHost, st));
+      CUDA_OK(cudaStreamSynchronize(st));
+    } else {
+      std::copy(lat, lat + 9 * (size_t)S, L.begin());
+    }
+  }
+  std::vector<StructGeo> geo(S > 0 ? S : 1);
+  for (int s = 0; s < S; ++s) {
+    const double *l = &L[9 * s];
+    for (int k = 0; k < 9; ++k)
+      if (!std::isfinite(l[k])) CHG_THROW(CHG_ERR_GEOMETRY, "structure %d: non-finite lattice", s);
+    double det = l[0] * (l[4] * l[8] - l[5] * l[7]) - l[1] * (l[3] * l[8] - l[5] * l[6]) +
+                 l[2] * (l[3] * l[7] - l[4] * l[6]);
+    double V = std::fabs(det);
+    if (!(V > 1e-6)) CHG_THROW(CHG_ERR_GEOMETRY, "structure %d: |det L| = %g", s, V);
+    StructGeo &g = geo[s];
+    for (int k = 0; k < 9; ++k) g.L[k] = l[k];
+    // inverse (row-vector convention: f = r Linv)
+    double inv[9] = {l[4] * l[8] - l[5] * l[7], l[2] * l[7] - l[1] * l[8], l[1] * l[5] - l[2] * l[4],
+                     l[5] * l[6] - l[3] * l[8], l[0] * l[8] - l[2] * l[6], l[2] * l[3] - l[0] * l[5],
+                     l[3] * l[7] - l[4] * l[6], l[1] * l[6] - l[0] * l[7], l[0] * l[4] - l[1] * l[3]};
+    for (int k = 0; k < 9; ++k) g.Linv[k] = inv[k] / det;
+    for (int k = 0; k < 3; ++k) {
+      const double *u = &l[3 * ((k + 1) % 3)], *w = &l[3 * ((k + 2) % 3)];
+      double cx = u[1] * w[2] - u[2] * w[1], cy = u[2] * w[0] - u[0] * w[2], cz = u[0] * w[1] - u[1] * w[0];
+      double width = V / std::sqrt(cx * cx + cy * cy + cz * cz);
+      g.rw[k] = r_atom / width;
+      if (g.rw[k] > 100.0) CHG_THROW(CHG_ERR_GEOMETRY, "structure %d: cell too thin for cutoff", s);
+    }
+  }
+
+  chg_graph *G = new chg_graph();
+  G->ctx = ctx;
+  G->id = ++g_graph_counter;
+  G->S = S;
+  G->N = N;
+  G->r_atom = r_atom;
+  G->r_bond = r_bond;
+  G->atom_ptr_h.assign(atom_ptr, atom_ptr + S + 1);
+  if (S == 0) G->atom_ptr_h.assign(1, 0);
+  GraphBlocks *bl = new GraphBlocks();
+  G->block = bl;
+
+  try {
+    // ---- phase 1 allocation: per-atom / per-structure arrays + scratch
+    size_t n1 = N + 1;
+    size_t sz_atom = align_up(4 * (S + 1)) + align_up(4 * N) * 3 + align_up(4 * n1) * 3 +
+                     align_up(4 * (size_t)(n_species + 2)) + align_up(4 * 9 * (size_t)S) +
+                     align_up(4 * (size_t)S) + align_up(sizeof(StructGeo) * geo.size()) +
+                     align_up(8 * 3 * N) * 2 + align_up(4 * N) * 2 + align_up(64);
+    void *blk1 = nullptr;
+    CUDA_OK(cudaMallocAsync(&blk1, sz_atom, st));
+    bl->a = blk1;
+    char *c = (char *)blk1;
+    auto take = [&](size_t bytes) { void *p = c; c += align_up(bytes); return p; };
+    G->atom_ptr = (int32_t *)take(4 * (S + 1));
+    G->struct_of_atom = (int32_t *)take(4 * N);
+    G->species = (int32_t *)take(4 * N);
+    G->species_perm = (int32_t *)take(4 * N);
+    G->row_ptr = (int32_t *)take(4 * n1);
+    G->bond_ptr = (int32_t *)take(4 * n1);
+    G->atom_angle_ptr = (int32_t *)take(4 * n1);
+    G->species_ptr = (int32_t *)take(4 * (n_species + 2));
+    G->lattice_f = (float *)take(4 * 9 * (size_t)S);
+    G->inv_natoms = (float *)take(4 * (size_t)S);
+    StructGeo *d_geo = (StructGeo *)take(sizeof(StructGeo) * geo.size());
+    double *d_pos = (double *)take(8 * 3 * N);
+    double *d_frac = (double *)take(8 * 3 * N);
+    int32_t *cnt_e = (int32_t *)take(4 * N);
+    int32_t *cnt_b = (int32_t *)take(4 * N);
+    long long *d_tot = (long long *)take(64);
+
+    // host-side per-atom/per-structure arrays via pinned staging
+    size_t hbytes = 4 * (S + 1) + 4 * N + 4 * 9 * (size_t)S + 4 * (size_t)S + sizeof(StructGeo) * geo.size();
+    char *h = (char *)ctx->pinned_get(hbytes + 8 * 3 * N + 4 * N);
+    char *hp = h;
+    int32_t *h_ap = (int32_t *)hp; hp += 4 * (S + 1);
+    int32_t *h_soa = (int32_t *)hp; hp += 4 * N;
+    float *h_lat = (float *)hp; hp += 4 * 9 * (size_t)S;
+    float *h_inv = (float *)hp; hp += 4 * (size_t)S;
+    StructGeo *h_geo = (StructGeo *)hp; hp += sizeof(StructGeo) * geo.size();
+    for (int s = 0; s <= S; ++s) h_ap[s] = (int32_t)G->atom_ptr_h[s];
+    for (int s = 0; s < S; ++s) {
+      for (int64_t a = atom_ptr[s]; a < atom_ptr[s + 1]; ++a) h_soa[a] = s;
+      for (int k = 0; k < 9; ++k) h_lat[9 * s + k] = (float)L[9 * s + k];
+      int64_t ns = atom_ptr[s + 1] - atom_ptr[s];
+      h_inv[s] = ns > 0 ? 1.0f / (float)ns : 0.0f;
+    }
+    std::copy(geo.begin(), geo.end(), h_geo);
+    CUDA_OK(cudaMemcpyAsync(G->atom_ptr, h_ap, 4 * (S + 1), cudaMemcpyHostToDevice, st));
+    if (N) CUDA_OK(cudaMemcpyAsync(G->struct_of_atom, h_soa, 4 * N, cudaMemcpyHostToDevice, st));
+    if (S) {
+      CUDA_OK(cudaMemcpyAsync(G->lattice_f, h_lat, 4 * 9 * (size_t)S, cudaMemcpyHostToDevice, st));
+      CUDA_OK(cudaMemcpyAsync(G->inv_natoms, h_inv, 4 * (size_t)S, cudaMemcpyHostToDevice, st));
+    }
+    CUDA_OK(cudaMemcpyAsync(d_geo, h_geo, sizeof(StructGeo) * geo.size(), cudaMemcpyHostToDevice, st));
+    if (N) {
+      if (on_device) {
+        CUDA_OK(cudaMemcpyAsync(d_pos, pos, 8 * 3 * N, cudaMemcpyDeviceToDevice, st));
+        CUDA_OK(cudaMemcpyAsync(G->species, species, 4 * N, cudaMemcpyDeviceToDevice, st));
+      } else {
+        double *hpos = (double *)hp;
+        int32_t *hsp = (int32_t *)(hp + 8 * 3 * N);
+        std::copy(pos, pos + 3 * N, hpos);
+        std::copy(species, species + N, hsp);
+        CUDA_OK(cudaMemcpyAsync(d_pos, hpos, 8 * 3 * N, cudaMemcpyHostToDevice, st));
+        CUDA_OK(cudaMemcpyAsync(G->species, hsp, 4 * N, cudaMemcpyHostToDevice, st));
+      }
+    }
+    int *flag = ctx->d_flag;
+    ProfScope ps1(ctx, "graph", 0.0, 0.0);
+    CUDA_OK(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    CUDA_OK(cudaMemsetAsync(d_tot, 0, 64, st));
+    double ra2 = r_atom * r_atom, rb2 = r_bond * r_bond;
+    if (N) {
+      k_frac<<<ceil_div(N, 256), 256, 0, st>>>((int)N, d_pos, G->struct_of_atom, d_geo, G->species,
+                                                n_species, d_frac, flag);
+      check_launch(ctx);
+      k_count<<<ceil_div(N * 32, 256), 256, 0, st>>>((int)N, d_pos, d_frac, G->struct_of_atom, G->atom_ptr,
+                                                      d_geo, ra2, rb2, cnt_e, cnt_b, flag);
+      check_launch(ctx);
+      k_scan<<<1, 1024, 0, st>>>((int)N, cnt_e, cnt_b, G->row_ptr, G->bond_ptr, G->atom_angle_ptr, d_tot);
+      check_launch(ctx);
+    } else {
+      CUDA_OK(cudaMemsetAsync(G->row_ptr, 0, 4, st));
+      CUDA_OK(cudaMemsetAsync(G->bond_ptr, 0, 4, st));
+      CUDA_OK(cudaMemsetAsync(G->atom_angle_ptr, 0, 4, st));
+    }
+    // totals + flags to host (the one synchronisation of the build: sizes)
+    long long *h_tot = (long long *)ctx->pinned_get(64);
+    CUDA_OK(cudaMemcpyAsync(h_tot, d_tot, 32, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaMemcpyAsync(((char *)h_tot) + 32, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+    int hflag = *(int *)(((char *)h_tot) + 32);
+    if (hflag & 1) CHG_THROW(CHG_ERR_GEOMETRY, "non-finite positions");
+    if (hflag & 2) CHG_THROW(CHG_ERR_SPECIES, "species outside 1..%d", n_species);
+    if (hflag & 4) CHG_THROW(CHG_ERR_GEOMETRY, "coincident atoms (accepted pair with d^2 < 1e-12)");
+    long long E = h_tot[0], B = h_tot[1], A = h_tot[2];
+    if (E >= 2147483647LL || A >= 2147483647LL)
+      CHG_THROW(CHG_ERR_CAPACITY, "edge/angle count exceeds int32 (E=%lld A=%lld)", E, A);
+    G->E = E; G->B = B; G->A = A;
+
+    // ---- phase 2 allocation: edge / bond / angle arrays
+    size_t sz2 = align_up(4 * E) * 4 + align_up(4 * E) /*img*/ + align_up(16 * E) + align_up(32 * E) + align_up(4 * B) +
+                 align_up(4 * (B + 1)) + align_up(4 * A) * 6 + 256;
+    void *blk2 = nullptr;
+    CUDA_OK(cudaMallocAsync(&blk2, sz2, st));
+    bl->b = blk2;
+    c = (char *)blk2;
+    G->center = (int32_t *)take(4 * E);
+    G->nbr = (int32_t *)take(4 * E);
+    G->bond_id = (int32_t *)take(4 * E);
+    G->rev = (int32_t *)take(4 * E);
+    G->img = (char4 *)take(4 * E);
+    G->vec = (float4 *)take(16 * E);
+    G->vec64 = (double4 *)take(32 * E);
+    G->bond_edge = (int32_t *)take(4 * B);
+    G->angle_ptr = (int32_t *)take(4 * (B + 1));
+    G->angle_b1 = (int32_t *)take(4 * A);
+    G->angle_b2 = (int32_t *)take(4 * A);
+    G->angle_e1 = (int32_t *)take(4 * A);
+    G->angle_e2 = (int32_t *)take(4 * A);
+    G->angle_ctr = (int32_t *)take(4 * A);
+    G->swap = (int32_t *)take(4 * A);
+
+    ProfScope ps2(ctx, "graph", 0.0, 0.0);
+    if (N) {
+      k_fill<<<ceil_div(N * 32, 256), 256, 0, st>>>((int)N, d_pos, d_frac, G->struct_of_atom, G->atom_ptr,
+                                                     d_geo, ra2, rb2, G->row_ptr, G->bond_ptr, G->center,
+                                                     G->nbr, G->img, G->vec, G->vec64, G->bond_id, G->bond_edge);
+      check_launch(ctx);
+      k_angles<<<ceil_div(B + 1, 256), 256, 0, st>>>((int)B, G->bond_edge, G->center, G->bond_ptr,
+                                                      G->atom_angle_ptr, G->angle_ptr, G->angle_b1,
+                                                      G->angle_b2, G->angle_e1, G->angle_e2, G->angle_ctr,
+                                                      G->swap, (int)A);
+      check_launch(ctx);
+      if (E) {
+        k_rev<<<ceil_div(E, 256), 256, 0, st>>>((int)E, G->center, G->nbr, G->img, G->row_ptr, G->rev, flag);
+        check_launch(ctx);
+      }
+      k_species<<<1, 32, 4 * (n_species + 1), st>>>((int)N, n_species, G->species, G->species_perm,
+                                                     G->species_ptr);
+      check_launch(ctx);
+    } else {
+      CUDA_OK(cudaMemsetAsync(G->angle_ptr, 0, 4, st));
+      CUDA_OK(cudaMemsetAsync(G->species_ptr, 0, 4 * (n_species + 2), st));
+    }
+    // per-structure counts on host (from row_ptr etc. at structure boundaries)
+    G->counts_h.assign(4 * (size_t)S, 0);
+    if (S) {
+      int32_t *hrp = (int32_t *)ctx->pinned_get(4 * (N + 1) * 3 + 64);
+      CUDA_OK(cudaMemcpyAsync(hrp, G->row_ptr, 4 * (N + 1), cudaMemcpyDeviceToHost, st));
+      CUDA_OK(cudaMemcpyAsync(hrp + (N + 1), G->bond_ptr, 4 * (N + 1), cudaMemcpyDeviceToHost, st));
+      CUDA_OK(cudaMemcpyAsync(hrp + 2 * (N + 1), G->atom_angle_ptr, 4 * (N + 1), cudaMemcpyDeviceToHost, st));
+      CUDA_OK(cudaMemcpyAsync(hrp + 3 * (N + 1), flag, 4, cudaMemcpyDeviceToHost, st));
+      CUDA_OK(cudaStreamSynchronize(st));
+      if (hrp[3 * (N + 1)] & 8) CHG_THROW(CHG_ERR_GEOMETRY, "internal: reverse edge not found");
+      for (int s = 0; s < S; ++s) {
+        int64_t a0 = atom_ptr[s], a1 = atom_ptr[s + 1];
+        G->counts_h[4 * s + 0] = a1 - a0;
+        G->counts_h[4 * s + 1] = hrp[a1] - hrp[a0];
+        G->counts_h[4 * s + 2] = hrp[N + 1 + a1] - hrp[N + 1 + a0];
+        G->counts_h[4 * s + 3] = hrp[2 * (N + 1) + a1] - hrp[2 * (N + 1) + a0];
+      }
+    }
+  } catch (...) {
+    if (bl->a) cudaFreeAsync(bl->a, st);
+    if (bl->b) cudaFreeAsync(bl->b, st);
+    delete bl;
+    delete G;
+    throw;
+  }
+  return G;
+}
+
+void destroy_graph_impl(chg_graph *G) {
+  if (!G) return;
+  if (G->block) {
+    GraphBlocks *bl = (GraphBlocks *)G->block;
+    if (bl->a) cudaFreeAsync(bl->a, G->ctx->stream);
+    if (bl->b) cudaFreeAsync(bl->b, G->ctx->stream);
+    delete bl;
+  }
+  delete G;
+}

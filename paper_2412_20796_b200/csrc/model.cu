@@ -1,0 +1,677 @@
+// model.cu — forward / backward / step orchestration of the FastCHGNet
+// training step (A2–A9 of DESIGN.md §"Hot path").
+//
+// Forward (Fig. 2a): basis (Alg. 2) → embedding + projections (Eq. 2) → for
+// t = 0..T-1 { atom conv (Eq. 4) ∥ bond conv (Eq. 5) ∥ angle update (Eq. 6),
+// all reading layer-t features (Eq. 11) } → final atom conv → energy, magmom,
+// force (Eq. 7) and stress (Eq. 9) heads.
+// Backward: first-order reverse mode only (the decomposed heads need no
+// derivative of E); gather adjoints are segmented reductions
+// through the CSR rows, the reverse-edge map (rev) and the angle swap map
+// (swap) — no atomics, fixed order, deterministic.
+#include <nccl.h>
+
+#include <cmath>
+
+#include "gemm.cuh"
+#include "ops.cuh"
+
+namespace {
+
+struct Fwd {
+  chg_ctx *ctx;
+  chg_model *m;
+  chg_graph *g;
+  float *buf(const std::string &n, int64_t rows, int cols) {
+    float *q = ctx->getf(n, (size_t)std::max<int64_t>(rows, 1) * cols);
+    ctx->dbg[n] = {q, rows, cols, cols};
+    return q;
+  }
+  GateLN ln(const std::string &pre) {
+    return GateLN{m->p(pre + ".ln_core.g"), m->p(pre + ".ln_core.b"), m->p(pre + ".ln_gate.g"),
+                  m->p(pre + ".ln_gate.b")};
+  }
+};
+
+// --- Atom Conv (Eq. 4) ------------------------------------------------------
+void atom_conv_fwd(Fwd &F, int t, const float *v, const float *e, const float *ea, float *v_out) {
+  chg_ctx *ctx = F.ctx;
+  chg_model *m = F.m;
+  chg_graph *g = F.g;
+  const int64_t N = g->N, E = g->E;
+  std::string pre = "atom" + std::to_string(t);
+  float *z1 = F.buf("ac_z1_" + std::to_string(t), E, 128);
+  float *y = F.buf("ac_y_" + std::to_string(t), E, 128);
+  float *agg = F.buf("ac_agg_" + std::to_string(t), N, 64);
+  float *msg = ctx->getf("msg_edge", std::max<int64_t>(E, 1) * 64);
+  {  // [v_i, v_j, e_ij] · [W1_core | W1_gate] + b1   (gather fused in the A load)
+    RowGemm G;
+    G.A.seg[0] = aseg(v, 64, 64, g->center);
+    G.A.seg[1] = aseg(v, 64, 64, g->nbr);
+    G.A.seg[2] = aseg(e, 64, 64);
+    G.A.nseg = 3;
+    G.M = (int)E; G.K = 192; G.nchunk = 2;
+    G.ch[0] = chunk1(m->p(pre + ".core.W1"), 64, 192, m->p(pre + ".core.b1"), z1, 128);
+    G.ch[1] = chunk1(m->p(pre + ".gate.W1"), 64, 192, m->p(pre + ".gate.b1"), z1 + 64, 128);
+    rowgemm(ctx, G);
+  }
+  {  // SiLU(z1) · blockdiag(W2_core, W2_gate) + b2
+    RowGemm G;
+    G.A.seg[0] = aseg(z1, 128, 128);
+    G.A.nseg = 1; G.A.act = 1;
+    G.M = (int)E; G.K = 64; G.nchunk = 2;
+    G.ch[0] = chunk1(m->p(pre + ".core.W2"), 64, 64, m->p(pre + ".core.b2"), y, 128);
+    G.ch[1] = chunk1(m->p(pre + ".gate.W2"), 64, 64, m->p(pre + ".gate.b2"), y + 64, 128);
+    G.ch[1].a_k0 = 64;
+    rowgemm(ctx, G);
+  }
+  // m_e = eᵃ_e ⊙ σ(LN_g(y_g)) ⊙ SiLU(LN_c(y_c))
+  gate_fwd(ctx, E, y, 128, F.ln(pre), GATE_MUL_W, ea, nullptr, nullptr, nullptr, msg);
+  SegSrc s;
+  s.in = msg; s.ptr = g->row_ptr; s.rows = E;
+  segsum(ctx, N, agg, 64, 0, 1, &s);
+  {  // v' = v + agg · W_out + b_out
+    RowGemm G;
+    G.A.seg[0] = aseg(agg, 64, 64);
+    G.A.nseg = 1;
+    G.M = (int)N; G.K = 64; G.nchunk = 1;
+    G.ch[0] = chunk1(m->p(pre + ".out.W"), 64, 64, m->p(pre + ".out.b"), v_out, 64);
+    G.ch[0].resid = v; G.ch[0].ldr = 64;
+    rowgemm(ctx, G);
+  }
+}
+
+// --- Bond Conv (Eq. 5) + Angle Update (Eq. 6) with Eq. 11 inputs ------------
+void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float *e, const float *a, const float *eb,
+                   float *e_out, float *a_out) {
+  chg_ctx *ctx = F.ctx;
+  chg_model *m = F.m;
+  chg_graph *g = F.g;
+  const int64_t E = g->E, B = g->B, A = g->A;
+  std::string bp = "bond" + std::to_string(t), ap = "angle" + std::to_string(t), ts = std::to_string(t);
+  float *z1 = F.buf("bc_z1_" + ts, A, 128);
+  float *yb = F.buf("bc_yb_" + ts, A, 128);
+  float *ya = angle_branch ? F.buf("bc_ya_" + ts, A, 128) : nullptr;
+  float *aggb = F.buf("bc_aggb_" + ts, B, 64);
+  float *q = ctx->getf("msg_angle", std::max<int64_t>(A, 1) * 64);
+  if (A > 0) {
+    // shared input [v_i, e_ij, e_ik, a_ijk] against the packed first
+    // layers of both modules (Fig. 3a): bond core/gate hidden, angle core/gate
+    RowGemm G;
+    G.A.seg[0] = aseg(v, 64, 64, g->angle_ctr);
+    G.A.seg[1] = aseg(e, 64, 64, g->angle_e1);
+    G.A.seg[2] = aseg(e, 64, 64, g->angle_e2);
+    G.A.seg[3] = aseg(a, 64, 64);
+    G.A.nseg = 4;
+    G.M = (int)A; G.K = 256; G.nchunk = angle_branch ? 4 : 2;
+    G.ch[0] = chunk1(m->p(bp + ".core.W1"), 64, 256, m->p(bp + ".core.b1"), z1, 128);
+    G.ch[1] = chunk1(m->p(bp + ".gate.W1"), 64, 256, m->p(bp + ".gate.b1"), z1 + 64, 128);
+    if (angle_branch) {
+      G.ch[2] = chunk1(m->p(ap + ".core.W"), 64, 256, m->p(ap + ".core.b"), ya, 128);
+      G.ch[3] = chunk1(m->p(ap + ".gate.W"), 64, 256, m->p(ap + ".gate.b"), ya + 64, 128);
+    }
+    rowgemm(ctx, G);
+    RowGemm H;
+    H.A.seg[0] = aseg(z1, 128, 128);
+    H.A.nseg = 1; H.A.act = 1;
+    H.M = (int)A; H.K = 64; H.nchunk = 2;
+    H.ch[0] = chunk1(m->p(bp + ".core.W2"), 64, 64, m->p(bp + ".core.b2"), yb, 128);
+    H.ch[1] = chunk1(m->p(bp + ".gate.W2"), 64, 64, m->p(bp + ".gate.b2"), yb + 64, 128);
+    H.ch[1].a_k0 = 64;
+    rowgemm(ctx, H);
+    // q = eᵇ_ij ⊙ eᵇ_ik ⊙ φ_e
+    gate_fwd(ctx, A, yb, 128, F.ln(bp), GATE_MUL_W1W2, eb, g->angle_b1, g->angle_b2, nullptr, q);
+  }
+  SegSrc s;
+  s.in = q; s.ptr = g->angle_ptr; s.rows = A;
+  segsum(ctx, B, aggb, 64, 0, 1, &s);      // Σ over angles with first bond b (empty -> 0)
+  {  // e' = e + 𝓛_e(agg) on all E edges (non-bond rows gather a zero row, Q16)
+    RowGemm G;
+    G.A.seg[0] = aseg(aggb, 64, 64, g->bond_id);
+    G.A.nseg = 1;
+    G.M = (int)E; G.K = 64; G.nchunk = 1;
+    G.ch[0] = chunk1(m->p(bp + ".out.W"), 64, 64, m->p(bp + ".out.b"), e_out, 64);
+    G.ch[0].resid = e; G.ch[0].ldr = 64;
+    rowgemm(ctx, G);
+  }
+  if (angle_branch && A > 0)   // a' = a + φ_a
+    gate_fwd(ctx, A, ya, 128, F.ln(ap), GATE_RESID, nullptr, nullptr, nullptr, a, a_out);
+}
+
+// --- MLP heads: hidden layers Linear+SiLU, last Linear -------------------------
+void mlp_fwd(Fwd &F, const std::string &pre, int nl, const float *x, int64_t rows, int nout, float *out, int ldo) {
+  chg_model *m = F.m;
+  const float *h = x;
+  for (int k = 0; k < nl; ++k) {
+    RowGemm G;
+    G.A.seg[0] = aseg(h, 64, 64);
+    G.A.nseg = 1;
+    G.M = (int)rows; G.K = 64; G.nchunk = 1;
+    std::string W = pre + ".W" + std::to_string(k), b = pre + ".b" + std::to_string(k);
+    if (k + 1 < nl) {
+      float *z = F.buf(pre + "_z" + std::to_string(k), rows, 64);
+      float *hn = F.buf(pre + "_h" + std::to_string(k), rows, 64);
+      G.act = 1;
+      G.ch[0] = chunk1(m->p(W), 64, 64, m->p(b), hn, 64);
+      G.ch[0].pre = z; G.ch[0].ldp = 64;
+      rowgemm(F.ctx, G);
+      h = hn;
+    } else {
+      G.ch[0] = chunk1(m->p(W), nout, 64, m->p(b), out, ldo, nout);
+      rowgemm(F.ctx, G);
+    }
+  }
+}
+
+void copy_out(chg_ctx *ctx, float *dst, const float *src, int64_t n, int on_device) {
+  if (!dst || n <= 0) return;
+  CUDA_OK(cudaMemcpyAsync(dst, src, 4 * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                          ctx->stream));
+}
+
+}  // namespace
+
+void forward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, int train, chg_pred *out) {
+  Fwd F{ctx, m, g};
+  const int64_t N = g->N, E = g->E, B = g->B, A = g->A;
+  const int T = m->cfg.n_bond_conv;
+  const int p = m->cfg.envelope_p;
+  ctx->dbg.clear();
+  ctx->fwd_train = false;
+  // A2 bases (fp64 geometry, fp32 features)
+  float *ea_t = F.buf("ea_t", E, 32), *eb_t = F.buf("eb_t", B, 32), *a_t = F.buf("a_t", A, 32);
+  basis_radial(ctx, E, g->vec64, nullptr, m->p("rbf_a.freq"), g->r_atom, p, ea_t);
+  basis_radial(ctx, B, g->vec64, g->bond_edge, m->p("rbf_b.freq"), g->r_bond, p, eb_t);
+  basis_angle(ctx, A, g->vec64, g->angle_e1, g->angle_e2, a_t);
+  // A3 embedding and projections (Eq. 2; no bias, Q5)
+  std::vector<float *> v(T + 2), e(T + 1), a(T);
+  v[0] = F.buf("v0", N, 64);
+  embed_fwd(ctx, N, g->species, m->p("embed.W"), v[0]);
+  e[0] = F.buf("e0", E, 64);
+  float *ea = F.buf("ea", E, 64), *eb = F.buf("eb", B, 64);
+  a[0] = F.buf("a0", A, 64);
+  {
+    RowGemm G;
+    G.A.seg[0] = aseg(ea_t, 32, 32);
+    G.A.nseg = 1;
+    G.M = (int)E; G.K = CHG_K; G.nchunk = 2;
+    G.ch[0] = chunk1(m->p("proj.W0"), 64, CHG_K, nullptr, e[0], 64);
+    G.ch[1] = chunk1(m->p("proj.Wa"), 64, CHG_K, nullptr, ea, 64);
+    rowgemm(ctx, G);
+    G.A.seg[0] = aseg(eb_t, 32, 32);
+    G.M = (int)B; G.nchunk = 1;
+    G.ch[0] = chunk1(m->p("proj.Wb"), 64, CHG_K, nullptr, eb, 64);
+    rowgemm(ctx, G);
+    G.A.seg[0] = aseg(a_t, 32, 32);
+    G.M = (int)A;
+    G.ch[0] = chunk1(m->p("proj.Wtheta"), 64, CHG_K, nullptr, a[0], 64);
+    rowgemm(ctx, G);
+  }
+  // A4/A5 interaction blocks
+  for (int t = 0; t < T; ++t) {
+    v[t + 1] = F.buf("v" + std::to_string(t + 1), N, 64);
+    e[t + 1] = F.buf("e" + std::to_string(t + 1), E, 64);
+    bool ab = t + 1 < T;
+    if (ab) a[t + 1] = F.buf("a" + std::to_string(t + 1), A, 64);
+    atom_conv_fwd(F, t, v[t], e[t], ea, v[t + 1]);
+    bond_conv_fwd(F, t, ab, v[t], e[t], a[t], eb, e[t + 1], ab ? a[t + 1] : nullptr);
+  }
+  v[T + 1] = F.buf("v" + std::to_string(T + 1), N, 64);
+  atom_conv_fwd(F, T, v[T], e[T], ea, v[T + 1]);
+  // A6 heads
+  float *vf = v[T + 1], *ef = e[T];
+  float *e_atom = F.buf("e_atom", N, 1), *mag = F.buf("magmom", N, 1), *n_e = F.buf("n_e", E, 1);
+  float *M9 = F.buf("M9", N, 9);
+  mlp_fwd(F, "head_E", 4, vf, N, 1, e_atom, 1);
+  {
+    RowGemm G;
+    G.A.seg[0] = aseg(vf, 64, 64);
+    G.A.nseg = 1;
+    G.M = (int)N; G.K = 64;
+    G.ch[0] = chunk1(m->p("head_M.W"), 1, 64, m->p("head_M.b"), mag, 1, 1);
+    rowgemm(ctx, G);
+  }
+  mlp_fwd(F, "head_F", 3, ef, E, 1, n_e, 1);
+  mlp_fwd(F, "head_S", 3, vf, N, 9, M9, 9);
+  float *energy = F.buf("energy", g->S, 1), *epa = F.buf("energy_per_atom", g->S, 1);
+  float *forces = F.buf("forces", N, 3), *stress = F.buf("stress", g->S, 9);
+  heads_forces(ctx, g, n_e, forces);
+  heads_struct(ctx, g, e_atom, M9, energy, epa, stress);
+  if (out) {
+    copy_out(ctx, out->energy, energy, g->S, out->on_device);
+    copy_out(ctx, out->energy_per_atom, epa, g->S, out->on_device);
+    copy_out(ctx, out->forces, forces, 3 * N, out->on_device);
+    copy_out(ctx, out->stress, stress, 9 * (int64_t)g->S, out->on_device);
+    copy_out(ctx, out->magmom, mag, N, out->on_device);
+    if (!out->on_device) CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  }
+  ctx->fwd_graph = g;
+  ctx->fwd_graph_id = g->id;
+  ctx->fwd_train = train != 0;
+}
+
+// ===========================================================================
+// backward
+// ===========================================================================
+namespace {
+
+struct Bwd {
+  chg_ctx *ctx;
+  chg_model *m;
+  chg_graph *g;
+  float *wt;   // transposed copy of every 2-D weight at its own flat offset
+  const float *WT(const std::string &n) const { return wt + m->off(n); }
+  float *G(const std::string &n) const { return m->g(n); }
+  const float *act(const std::string &n) const {
+    auto it = ctx->dbg.find(n);
+    if (it == ctx->dbg.end()) CHG_THROW(CHG_ERR_STATE, "missing forward activation %s", n.c_str());
+    return it->second.p;
+  }
+  GateLN ln(const std::string &pre) const {
+    return GateLN{m->p(pre + ".ln_core.g"), m->p(pre + ".ln_core.b"), m->p(pre + ".ln_gate.g"),
+                  m->p(pre + ".ln_gate.b")};
+  }
+  GateLNGrad lng(const std::string &pre) const {
+    return GateLNGrad{G(pre + ".ln_core.g"), G(pre + ".ln_core.b"), G(pre + ".ln_gate.g"), G(pre + ".ln_gate.b")};
+  }
+  float *scratch(const char *n, int64_t rows, int cols) {
+    return ctx->getf(n, (size_t)std::max<int64_t>(rows, 1) * cols);
+  }
+};
+
+// dv/dx accumulation through an MLP head (hidden SiLU layers saved as z_k)
+void mlp_bwd(Bwd &Bw, const std::string &pre, int nl, const float *x, int64_t rows, const float *dout, int nout,
+             float *dx) {
+  chg_ctx *ctx = Bw.ctx;
+  const float *dz = dout;
+  int ncol = nout;
+  for (int k = nl - 1; k >= 0; --k) {
+    std::string W = pre + ".W" + std::to_string(k), b = pre + ".b" + std::to_string(k);
+    const float *in = k == 0 ? x : Bw.act(pre + "_z" + std::to_string(k - 1));
+    WGrad wg;
+    wg.A.seg[0] = aseg(in, 64, 64);
+    wg.A.nseg = 1;
+    wg.A.act = k > 0 ? 1 : 0;
+    wg.M = (int)rows; wg.K = 64;
+    wg.D = dz; wg.ldd = ncol; wg.N = ncol; wg.bias = 1;
+    wg.dst[0].W = Bw.G(W); wg.dst[0].ldw = ncol; wg.dst[0].b = Bw.G(b);
+    wgrad(ctx, wg);
+    RowGemm G;
+    G.A.seg[0] = aseg(dz, ncol, ncol);
+    G.A.nseg = 1;
+    G.M = (int)rows; G.K = ncol;
+    if (k > 0) {
+      float *dzn = ctx->getf(pre + "_dz" + std::to_string(k - 1), (size_t)std::max<int64_t>(rows, 1) * 64);
+      G.ch[0] = chunk1(Bw.WT(W), 64, ncol, nullptr, dzn, 64);
+      G.ch[0].mul = Bw.act(pre + "_z" + std::to_string(k - 1)); G.ch[0].ldm = 64;
+      rowgemm(ctx, G);
+      dz = dzn;
+      ncol = 64;
+    } else {
+      G.ch[0] = chunk1(Bw.WT(W), 64, ncol, nullptr, dx, 64);
+      G.ch[0].resid = dx; G.ch[0].ldr = 64;
+      rowgemm(ctx, G);
+    }
+  }
+}
+
+// contributions of the output linear of atom conv t: dagg = dv · W_outᵀ, dW_out, db_out
+void ac_bwd_head(Bwd &Bw, int t, const float *dv, float *dagg) {
+  chg_graph *g = Bw.g;
+  std::string pre = "atom" + std::to_string(t);
+  const float *agg = Bw.act("ac_agg_" + std::to_string(t));
+  RowGemm G;
+  G.A.seg[0] = aseg(dv, 64, 64);
+  G.A.nseg = 1;
+  G.M = (int)g->N; G.K = 64;
+  G.ch[0] = chunk1(Bw.WT(pre + ".out.W"), 64, 64, nullptr, dagg, 64);
+  rowgemm(Bw.ctx, G);
+  WGrad wg;
+  wg.A.seg[0] = aseg(agg, 64, 64);
+  wg.A.nseg = 1;
+  wg.M = (int)g->N; wg.K = 64;
+  wg.D = dv; wg.ldd = 64; wg.N = 64; wg.bias = 1;
+  wg.dst[0].W = Bw.G(pre + ".out.W"); wg.dst[0].ldw = 64; wg.dst[0].b = Bw.G(pre + ".out.b");
+  wgrad(Bw.ctx, wg);
+}
+
+void bc_bwd_head(Bwd &Bw, int t, const float *de, float *daggb) {
+  chg_graph *g = Bw.g;
+  std::string pre = "bond" + std::to_string(t);
+  const float *aggb = Bw.act("bc_aggb_" + std::to_string(t));
+  RowGemm G;
+  G.A.seg[0] = aseg(de, 64, 64, g->bond_edge);
+  G.A.nseg = 1;
+  G.M = (int)g->B; G.K = 64;
+  G.ch[0] = chunk1(Bw.WT(pre + ".out.W"), 64, 64, nullptr, daggb, 64);
+  rowgemm(Bw.ctx, G);
+  WGrad wg;   // dW_out = aggbᵀ · de[bond_edge] (non-bond rows of agg are zero)
+  wg.A.seg[0] = aseg(aggb, 64, 64);
+  wg.A.nseg = 1;
+  wg.M = (int)g->B; wg.K = 64;
+  wg.D = de; wg.didx = g->bond_edge; wg.ldd = 64; wg.N = 64; wg.bias = 0;
+  wg.dst[0].W = Bw.G(pre + ".out.W"); wg.dst[0].ldw = 64;
+  wgrad(Bw.ctx, wg);
+  WGrad wb;   // db_out = Σ over ALL edges of de
+  wb.A.nseg = 0;
+  wb.M = (int)g->E; wb.K = 0;
+  wb.D = de; wb.ldd = 64; wb.N = 64; wb.bias = 1;
+  wb.dst[0].b = Bw.G(pre + ".out.b");
+  wgrad(Bw.ctx, wb);
+}
+
+void ac_bwd_body(Bwd &Bw, int t, const float *v, const float *e, const float *ea, const float *dagg, float *dv,
+                 float *de, float *dea) {
+  chg_ctx *ctx = Bw.ctx;
+  chg_graph *g = Bw.g;
+  const int64_t N = g->N, E = g->E;
+  std::string pre = "atom" + std::to_string(t), ts = std::to_string(t);
+  const float *z1 = Bw.act("ac_z1_" + ts), *y = Bw.act("ac_y_" + ts);
+  float *dY = Bw.scratch("ac_dY", E, 128), *dZ = Bw.scratch("ac_dZ", E, 128);
+  float *ti = Bw.scratch("tmp_i", E, 64), *tj = Bw.scratch("tmp_j", E, 64);
+  gate_bwd(ctx, E, y, 128, Bw.ln(pre), GATE_MUL_W, ea, nullptr, nullptr, dagg, g->center, dY, 128, dea, nullptr,
+           nullptr, Bw.lng(pre));
+  {  // dZ1 = (dY · blockdiag(W2ᵀ)) ⊙ SiLU'(z1)
+    RowGemm G;
+    G.A.seg[0] = aseg(dY, 128, 128);
+    G.A.nseg = 1;
+    G.M = (int)E; G.K = 64; G.nchunk = 2;
+    G.ch[0] = chunk1(Bw.WT(pre + ".core.W2"), 64, 64, nullptr, dZ, 128);
+    G.ch[0].mul = z1; G.ch[0].ldm = 128;
+    G.ch[1] = chunk1(Bw.WT(pre + ".gate.W2"), 64, 64, nullptr, dZ + 64, 128);
+    G.ch[1].mul = z1 + 64; G.ch[1].ldm = 128; G.ch[1].a_k0 = 64;
+    rowgemm(ctx, G);
+  }
+  for (int br = 0; br < 2; ++br) {  // dW2, db2
+    const char *b = br ? ".gate" : ".core";
+    WGrad wg;
+    wg.A.seg[0] = aseg(z1 + 64 * br, 128, 64);
+    wg.A.nseg = 1; wg.A.act = 1;
+    wg.M = (int)E; wg.K = 64;
+    wg.D = dY + 64 * br; wg.ldd = 128; wg.N = 64; wg.bias = 1;
+    wg.dst[0].W = Bw.G(pre + b + ".W2"); wg.dst[0].ldw = 64; wg.dst[0].b = Bw.G(pre + b + ".b2");
+    wgrad(ctx, wg);
+  }
+  {  // dX = dZ1 · [W1_coreᵀ ; W1_gateᵀ] -> (v_i part, v_j part, e part)
+    RowGemm G;
+    G.A.seg[0] = aseg(dZ, 128, 128);
+    G.A.nseg = 1;
+    G.M = (int)E; G.K = 128; G.nchunk = 3;
+    float *outs[3] = {ti, tj, de};
+    for (int c = 0; c < 3; ++c) {
+      Chunk &C = G.ch[c];
+      C.W[0] = Bw.WT(pre + ".core.W1") + 64 * c; C.ldw[0] = 192;
+      C.W[1] = Bw.WT(pre + ".gate.W1") + 64 * c; C.ldw[1] = 192;
+      C.wk0[0] = 0; C.wk0[1] = 64; C.wk0[2] = 128; C.nwb = 2;
+      C.out = outs[c]; C.ldo = 64;
+      if (c == 2) { C.resid = de; C.ldr = 64; }
+    }
+    rowgemm(ctx, G);
+  }
+  {  // dW1 = Xᵀ dZ1 with X = [v_i, v_j, e] gathered again
+    WGrad wg;
+    wg.A.seg[0] = aseg(v, 64, 64, g->center);
+    wg.A.seg[1] = aseg(v, 64, 64, g->nbr);
+    wg.A.seg[2] = aseg(e, 64, 64);
+    wg.A.nseg = 3;
+    wg.M = (int)E; wg.K = 192;
+    wg.D = dZ; wg.ldd = 128; wg.N = 128; wg.bias = 1;
+    wg.dst[0].W = Bw.G(pre + ".core.W1"); wg.dst[0].ldw = 64; wg.dst[0].b = Bw.G(pre + ".core.b1");
+    wg.dst[1].W = Bw.G(pre + ".gate.W1"); wg.dst[1].ldw = 64; wg.dst[1].b = Bw.G(pre + ".gate.b1");
+    wgrad(ctx, wg);
+  }
+  // dv_i: CSR row sum; dv_j: rows of j through the reverse-edge map (no atomics)
+  SegSrc s[2];
+  s[0].in = ti; s[0].ptr = g->row_ptr; s[0].rows = E;
+  s[1].in = tj; s[1].ptr = g->row_ptr; s[1].perm = g->rev; s[1].rows = E;
+  segsum(ctx, N, dv, 64, 1, 2, s);
+}
+
+void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float *e, const float *a, const float *eb,
+                 const float *daggb, float *dv, float *de, float *da, float *deb) {
+  chg_ctx *ctx = Bw.ctx;
+  chg_graph *g = Bw.g;
+  const int64_t N = g->N, E = g->E, B = g->B, A = g->A;
+  if (A == 0) return;
+  std::string bp = "bond" + std::to_string(t), ap = "angle" + std::to_string(t), ts = std::to_string(t);
+  const float *z1 = Bw.act("bc_z1_" + ts), *yb = Bw.act("bc_yb_" + ts);
+  float *dYb = Bw.scratch("bc_dYb", A, 128), *dZ = Bw.scratch("bc_dZ", A, 256);
+  float *q1 = Bw.scratch("bc_q1", A, 64), *q2 = Bw.scratch("bc_q2", A, 64);
+  float *tv = Bw.scratch("tmp_vi", A, 64), *t1 = Bw.scratch("tmp_e1", A, 64), *t2 = Bw.scratch("tmp_e2", A, 64);
+  gate_bwd(ctx, A, yb, 128, Bw.ln(bp), GATE_MUL_W1W2, eb, g->angle_b1, g->angle_b2, daggb, g->angle_b1, dYb, 128,
+           nullptr, q1, q2, Bw.lng(bp));
+  if (angle_branch)
+    gate_bwd(ctx, A, Bw.act("bc_ya_" + ts), 128, Bw.ln(ap), GATE_RESID, nullptr, nullptr, nullptr, da, nullptr,
+             dZ + 128, 256, nullptr, nullptr, nullptr, Bw.lng(ap));
+  {
+    RowGemm G;
+    G.A.seg[0] = aseg(dYb, 128, 128);
+    G.A.nseg = 1;
+    G.M = (int)A; G.K = 64; G.nchunk = 2;
+    G.ch[0] = chunk1(Bw.WT(bp + ".core.W2"), 64, 64, nullptr, dZ, 256);
+    G.ch[0].mul = z1; G.ch[0].ldm = 128;
+    G.ch[1] = chunk1(Bw.WT(bp + ".gate.W2"), 64, 64, nullptr, dZ + 64, 256);
+    G.ch[1].mul = z1 + 64; G.ch[1].ldm = 128; G.ch[1].a_k0 = 64;
+    rowgemm(ctx, G);
+  }
+  for (int br = 0; br < 2; ++br) {
+    const char *b = br ? ".gate" : ".core";
+    WGrad wg;
+    wg.A.seg[0] = aseg(z1 + 64 * br, 128, 64);
+    wg.A.nseg = 1; wg.A.act = 1;
+    wg.M = (int)A; wg.K = 64;
+    wg.D = dYb + 64 * br; wg.ldd = 128; wg.N = 64; wg.bias = 1;
+    wg.dst[0].W = Bw.G(bp + b + ".W2"); wg.dst[0].ldw = 64; wg.dst[0].b = Bw.G(bp + b + ".b2");
+    wgrad(ctx, wg);
+  }
+  const int Kx = angle_branch ? 256 : 128;
+  {  // dX = [dZ1_bond | dY_angle] · [W1_bcᵀ; W1_bgᵀ; W_acᵀ; W_agᵀ] -> (v_i, e_ij, e_ik, a)
+    RowGemm G;
+    G.A.seg[0] = aseg(dZ, 256, Kx);
+    G.A.nseg = 1;
+    G.M = (int)A; G.K = Kx; G.nchunk = 4;
+    float *outs[4] = {tv, t1, t2, da};
+    for (int c = 0; c < 4; ++c) {
+      Chunk &C = G.ch[c];
+      C.W[0] = Bw.WT(bp + ".core.W1") + 64 * c; C.ldw[0] = 256;
+      C.W[1] = Bw.WT(bp + ".gate.W1") + 64 * c; C.ldw[1] = 256;
+      C.wk0[0] = 0; C.wk0[1] = 64; C.wk0[2] = 128; C.nwb = 2;
+      if (angle_branch) {
+        C.W[2] = Bw.WT(ap + ".core.W") + 64 * c; C.ldw[2] = 256;
+        C.W[3] = Bw.WT(ap + ".gate.W") + 64 * c; C.ldw[3] = 256;
+        C.wk0[3] = 192; C.wk0[4] = 256; C.nwb = 4;
+      }
+      C.out = outs[c]; C.ldo = 64;
+      if (c == 3) { C.resid = da; C.ldr = 64; }
+    }
+    rowgemm(ctx, G);
+  }
+  {  // dW1 (bond) and dW (angle) = Xᵀ [dZ1 | dY_a]
+    WGrad wg;
+    wg.A.seg[0] = aseg(v, 64, 64, g->angle_ctr);
+    wg.A.seg[1] = aseg(e, 64, 64, g->angle_e1);
+    wg.A.seg[2] = aseg(e, 64, 64, g->angle_e2);
+    wg.A.seg[3] = aseg(a, 64, 64);
+    wg.A.nseg = 4;
+    wg.M = (int)A; wg.K = 256;
+    wg.D = dZ; wg.ldd = 256; wg.N = Kx; wg.bias = 1;
+    wg.dst[0].W = Bw.G(bp + ".core.W1"); wg.dst[0].ldw = 64; wg.dst[0].b = Bw.G(bp + ".core.b1");
+    wg.dst[1].W = Bw.G(bp + ".gate.W1"); wg.dst[1].ldw = 64; wg.dst[1].b = Bw.G(bp + ".gate.b1");
+    if (angle_branch) {
+      wg.dst[2].W = Bw.G(ap + ".core.W"); wg.dst[2].ldw = 64; wg.dst[2].b = Bw.G(ap + ".core.b");
+      wg.dst[3].W = Bw.G(ap + ".gate.W"); wg.dst[3].ldw = 64; wg.dst[3].b = Bw.G(ap + ".gate.b");
+    }
+    wgrad(ctx, wg);
+  }
+  SegSrc s[2];
+ s[0].in = tv; s[0].ptr = g->atom_angle_ptr; s[0].rows = A;                // angles of centre i are contiguous
+  segsum(ctx, N, dv, 64, 1, 1, s);
+  s[0] = SegSrc(); s[0].in = t1; s[0].ptr = g->angle_ptr; s[0].segmap = g->bond_id; s[0].rows = A;
+  s[1] = SegSrc(); s[1].in = t2; s[1].ptr = g->angle_ptr; s[1].segmap = g->bond_id; s[1].perm = g->swap; s[1].rows = A;
+  segsum(ctx, E, de, 64, 1, 2, s);
+  s[0] = SegSrc(); s[0].in = q1; s[0].ptr = g->angle_ptr; s[0].rows = A;
+  s[1] = SegSrc(); s[1].in = q2; s[1].ptr = g->angle_ptr; s[1].perm = g->swap; s[1].rows = A;
+  segsum(ctx, B, deb, 64, 1, 2, s);
+}
+
+const float *labels_dev(chg_ctx *ctx, const void *p, size_t bytes, const char *name, int on_device) {
+  if (on_device) return (const float *)p;
+  void *d = ctx->get(name, bytes);
+  if (bytes) CUDA_OK(cudaMemcpyAsync(d, p, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  return (const float *)d;
+}
+
+}  // namespace
+
+void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *lab_in, const chg_loss_cfg *cfg,
+                   double *loss_out) {
+  const int64_t N = g->N, E = g->E, B = g->B, A = g->A;
+  const int S = g->S, T = m->cfg.n_bond_conv;
+  if (!lab_in->energy_per_atom || !lab_in->forces || !lab_in->stress || !lab_in->magmom || !lab_in->magmom_mask)
+    CHG_THROW(CHG_ERR_ARG, "all label arrays are required");
+  Bwd Bw{ctx, m, g, nullptr};
+  chg_labels lab = *lab_in;
+  lab.energy_per_atom = labels_dev(ctx, lab_in->energy_per_atom, 4 * S, "lab_epa", lab_in->on_device);
+  lab.forces = labels_dev(ctx, lab_in->forces, 12 * N, "lab_f", lab_in->on_device);
+  lab.stress = labels_dev(ctx, lab_in->stress, 36 * (size_t)S, "lab_s", lab_in->on_device);
+  lab.magmom = labels_dev(ctx, lab_in->magmom, 4 * N, "lab_m", lab_in->on_device);
+  lab.magmom_mask = (const uint8_t *)labels_dev(ctx, lab_in->magmom_mask, N, "lab_mask", lab_in->on_device);
+  lab.on_device = 1;
+  // A7 loss + seeds
+  LossSeeds sd;
+  sd.d_eatom = Bw.scratch("seed_eatom", N, 1);
+  sd.d_M9 = Bw.scratch("seed_M9", N, 9);
+  sd.d_mag = Bw.scratch("seed_mag", N, 1);
+  sd.d_ne = Bw.scratch("seed_ne", E, 1);
+  loss_and_seeds(ctx, g, Bw.act("energy_per_atom"), Bw.act("forces"), Bw.act("stress"), Bw.act("magmom"), lab, *cfg,
+                 sd);
+  Bw.wt = ctx->getf("wt", m->P);
+  transpose_params(ctx, m, Bw.wt);
+  float *dv = Bw.scratch("dv", N, 64), *de = Bw.scratch("de", E, 64), *da = Bw.scratch("da", A, 64);
+  float *dea = Bw.scratch("dea", E, 64), *deb = Bw.scratch("deb", B, 64);
+  fill_zero(ctx, dv, 4 * 64 * N);
+  fill_zero(ctx, de, 4 * 64 * E);
+  fill_zero(ctx, da, 4 * 64 * A);
+  fill_zero(ctx, dea, 4 * 64 * E);
+  fill_zero(ctx, deb, 4 * 64 * B);
+  const float *vf = Bw.act("v" + std::to_string(T + 1)), *ef = Bw.act("e" + std::to_string(T));
+  // heads backward
+  mlp_bwd(Bw, "head_E", 4, vf, N, sd.d_eatom, 1, dv);
+  {
+    WGrad wg;
+    wg.A.seg[0] = aseg(vf, 64, 64);
+    wg.A.nseg = 1;
+    wg.M = (int)N; wg.K = 64;
+    wg.D = sd.d_mag; wg.ldd = 1; wg.N = 1; wg.bias = 1;
+    wg.dst[0].W = Bw.G("head_M.W"); wg.dst[0].ldw = 1; wg.dst[0].b = Bw.G("head_M.b");
+    wgrad(ctx, wg);
+    RowGemm G;
+    G.A.seg[0] = aseg(sd.d_mag, 1, 1);
+    G.A.nseg = 1;
+    G.M = (int)N; G.K = 1;
+    G.ch[0] = chunk1(Bw.WT("head_M.W"), 64, 1, nullptr, dv, 64);
+    G.ch[0].resid = dv; G.ch[0].ldr = 64;
+    rowgemm(ctx, G);
+  }
+  mlp_bwd(Bw, "head_S", 3, vf, N, sd.d_M9, 9, dv);
+  mlp_bwd(Bw, "head_F", 3, ef, E, sd.d_ne, 1, de);
+  // A8 interaction blocks, last to first
+  const float *ea = Bw.act("ea"), *eb = Bw.act("eb");
+  float *dagg = Bw.scratch("dagg", N, 64), *daggb = Bw.scratch("daggb", B, 64);
+  auto V = [&](int t) { return Bw.act("v" + std::to_string(t)); };
+  auto Ef = [&](int t) { return Bw.act("e" + std::to_string(t)); };
+  auto Af = [&](int t) { return Bw.act("a" + std::to_string(t)); };
+  ac_bwd_head(Bw, T, dv, dagg);
+  ac_bwd_body(Bw, T, V(T), Ef(T), ea, dagg, dv, de, dea);
+  for (int t = T - 1; t >= 0; --t) {
+    bool ab = t + 1 < T;
+    // both output linears read the incoming gradients before any update
+    ac_bwd_head(Bw, t, dv, dagg);
+    bc_bwd_head(Bw, t, de, daggb);
+    ac_bwd_body(Bw, t, V(t), Ef(t), ea, dagg, dv, de, dea);
+    bc_bwd_body(Bw, t, ab, V(t), Ef(t), Af(t), eb, daggb, dv, de, da, deb);
+  }
+  // embedding (rows of W_v gathered by species -> grouped sum, no atomics)
+  {
+    SegSrc s;
+    s.in = dv; s.ptr = g->species_ptr; s.perm = g->species_perm; s.ptr_off = 1; s.rows = N;
+    segsum(ctx, m->cfg.n_species, Bw.G("embed.W"), 64, 1, 1, &s);
+  }
+  // projections (Eq. 2) and trainable frequencies
+  auto proj_grad = [&](const float *basis, int64_t rows, const float *d, const char *W) {
+    WGrad wg;
+    wg.A.seg[0] = aseg(basis, 32, 32);
+    wg.A.nseg = 1;
+    wg.M = (int)rows; wg.K = CHG_K;
+    wg.D = d; wg.ldd = 64; wg.N = 64; wg.bias = 0;
+    wg.dst[0].W = Bw.G(W); wg.dst[0].ldw = 64;
+    wgrad(ctx, wg);
+  };
+  const float *ea_t = Bw.act("ea_t"), *eb_t = Bw.act("eb_t"), *a_t = Bw.act("a_t");
+  proj_grad(ea_t, E, de, "proj.W0");
+  proj_grad(ea_t, E, dea, "proj.Wa");
+  proj_grad(eb_t, B, deb, "proj.Wb");
+  proj_grad(a_t, A, da, "proj.Wtheta");
+  {
+    float *dbt = Bw.scratch("d_basis", std::max(E, B), 32);
+    RowGemm G;
+    G.A.seg[0] = aseg(de, 64, 64);
+    G.A.seg[1] = aseg(dea, 64, 64);
+    G.A.nseg = 2;
+    G.M = (int)E; G.K = 128;
+    Chunk &C = G.ch[0];
+    C.W[0] = Bw.WT("proj.W0"); C.ldw[0] = CHG_K;
+    C.W[1] = Bw.WT("proj.Wa"); C.ldw[1] = CHG_K;
+    C.wk0[0] = 0; C.wk0[1] = 64; C.wk0[2] = 128; C.nwb = 2;
+    C.ncols = CHG_K; C.out = dbt; C.ldo = 32;
+    rowgemm(ctx, G);
+    basis_freq_grad(ctx, E, g->vec64, nullptr, m->p("rbf_a.freq"), g->r_atom, m->cfg.envelope_p, dbt,
+                    Bw.G("rbf_a.freq"));
+    RowGemm H;
+    H.A.seg[0] = aseg(deb, 64, 64);
+    H.A.nseg = 1;
+    H.M = (int)B; H.K = 64;
+    H.ch[0] = chunk1(Bw.WT("proj.Wb"), CHG_K, 64, nullptr, dbt, 32, CHG_K);
+    rowgemm(ctx, H);
+    basis_freq_grad(ctx, B, g->vec64, g->bond_edge, m->p("rbf_b.freq"), g->r_bond, m->cfg.envelope_p, dbt,
+                    Bw.G("rbf_b.freq"));
+  }
+  if (loss_out) {
+    double *h = (double *)ctx->pinned_get(64);
+    CUDA_OK(cudaMemcpyAsync(h, ctx->d_loss, 5 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    for (int k = 0; k < 5; ++k) loss_out[k] = h[k];
+  }
+  // debug views of the main gradients
+  ctx->dbg["dv0"] = {dv, N, 64, 64};
+  ctx->dbg["de0"] = {de, E, 64, 64};
+  ctx->dbg["da0"] = {da, A, 64, 64};
+  ctx->dbg["dea"] = {dea, E, 64, 64};
+  ctx->dbg["deb"] = {deb, B, 64, 64};
+}
+
+// ===========================================================================
+// A9 allreduce + Adam
+// ===========================================================================
+
+void step_impl(chg_ctx *ctx, chg_model *m, const chg_adam_cfg *cfg) {
+  if (cfg->step < 1) CHG_THROW(CHG_ERR_ARG, "adam step must be >= 1");
+  if (cfg->allreduce && ctx->nccl_comm && ctx->nranks > 1) {
+    ProfScope ps(ctx, "allreduce", 0.0, 4.0 * m->P);
+    ncclResult_t r = ncclAllReduce(m->grads, m->grads, (size_t)m->P, ncclFloat32, ncclSum,
+                                   (ncclComm_t)ctx->nccl_comm, ctx->stream);
+    if (r != ncclSuccess) CHG_THROW(CHG_ERR_NCCL, "ncclAllReduce: %s", ncclGetErrorString(r));
+  } else if (cfg->allreduce && ctx->nranks > 1) {
+    CHG_THROW(CHG_ERR_STATE, "allreduce requested but no NCCL communicator");
+  }
+  int bad = finite_check(ctx, m->grads, m->P);
+  if (bad >= 0) {
+    std::string name = "?";
+    for (size_t t = 0; t < m->names.size(); ++t)
+      if (m->offsets[t] <= bad) name = m->names[t];
+    CHG_THROW(CHG_ERR_NONFINITE, "non-finite gradient in %s (flat index %d)", name.c_str(), bad);
+  }
+  double bc1 = 1.0 - std::pow((double)cfg->beta1, (double)cfg->step);
+  double bc2 = 1.0 - std::pow((double)cfg->beta2, (double)cfg->step);
+  adam_update(ctx, m->P, m->params, m->grads, m->m, m->v, cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, bc1, bc2);
+}

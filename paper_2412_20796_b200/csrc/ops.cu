@@ -1,0 +1,576 @@
+// ops.cu — non-GEMM kernels of the FastCHGNet training step (see ops.cuh).
+#include <climits>
+#include <cmath>
+
+#include "ops.cuh"
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// A2 basis.  Geometry is read in fp64 (vec64 from the graph builder), the
+// envelope is evaluated with ONE ξ^p and a factored quadratic (redundancy
+// removal of Eq. 13, with the DimeNet coefficients of reading Q2),
+// the result is rounded once to fp32.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double envelope_d(double xi, int p) {
+  double xp = 1.0;
+  for (int k = 0; k < p; ++k) xp *= xi;
+  double a = 0.5 * (p + 1) * (p + 2), b = (double)p * (p + 2), c = 0.5 * p * (p + 1);
+  return 1.0 - xp * (a - xi * (b - c * xi));
+}
+
+__global__ void k_basis_radial(int64_t rows, const double4 *__restrict__ vec, const int32_t *__restrict__ eor,
+                               const float *__restrict__ freq, double rc, int p, float *__restrict__ out) {
+  int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t row = gt >> 5;
+  int n = (int)(gt & 31);
+  if (row >= rows) return;
+  int e = eor ? eor[row] : (int)row;
+  double r = vec[e].w;
+  float val = 0.f;
+  if (n < CHG_K) {
+    double xi = r / rc;
+    double u = envelope_d(xi, p);
+    val = (float)(u * sqrt(2.0 / rc) * sin((double)freq[n] * xi) / r);
+  }
+  out[row * CHG_KP + n] = val;
+}
+
+__global__ void k_basis_freq_grad(int64_t rows, const double4 *__restrict__ vec, const int32_t *__restrict__ eor,
+                                  const float *__restrict__ freq, double rc, int p, const float *__restrict__ db,
+                                  float *__restrict__ partial) {
+  __shared__ float sh[8][32];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t gw = blockIdx.x * 8 + w, nw = (int64_t)gridDim.x * 8;
+  double acc = 0.0;
+  if (lane < CHG_K) {
+    double f = freq[lane];
+    for (int64_t row = gw; row < rows; row += nw) {
+      int e = eor ? eor[row] : (int)row;
+      double r = vec[e].w, xi = r / rc;
+      double u = envelope_d(xi, p);
+      acc += (double)db[row * CHG_KP + lane] * u * sqrt(2.0 / rc) * cos(f * xi) / rc;
+    }
+  }
+  sh[w][lane] = (float)acc;
+  __syncthreads();
+  if (w == 0) {
+    float s = 0.f;
+    for (int k = 0; k < 8; ++k) s += sh[k][lane];
+    partial[blockIdx.x * 32 + lane] = s;
+  }
+}
+
+__global__ void k_reduce_cols(int nblocks, int ncols, int stride, const float *__restrict__ partial,
+                              float *__restrict__ grad) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= ncols) return;
+  float s = 0.f;
+  for (int b = 0; b < nblocks; ++b) s += partial[(size_t)b * stride + j];
+  grad[j] += s;
+}
+
+__global__ void k_basis_angle(int64_t A, const double4 *__restrict__ vec, const int32_t *__restrict__ e1,
+                              const int32_t *__restrict__ e2, float *__restrict__ out) {
+  int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (a >= A) return;
+  double4 d1 = vec[e1[a]], d2 = vec[e2[a]];
+  double c = (d1.x * d2.x + d1.y * d2.y + d1.z * d2.z) / (d1.w * d2.w);
+  c = fmin(1.0, fmax(-1.0, c));
+  double s = sqrt(fmax(0.0, 1.0 - c * c));   // sin θ >= 0 for θ in [0, π]
+  const double isp = 0.56418958354775628695, is2p = 0.39894228040143267794;  // 1/√π, 1/√(2π)
+  float v[32];
+  v[0] = (float)is2p;
+  double ck = c, sk = s;
+#pragma unroll
+  for (int k = 1; k <= 15; ++k) {
+    v[2 * k - 1] = (float)(ck * isp);
+    v[2 * k] = (float)(sk * isp);
+    double cn = ck * c - sk * s, sn = sk * c + ck * s;   // angle addition: (k+1)θ
+    ck = cn; sk = sn;
+  }
+  v[31] = 0.f;
+  float4 *o = (float4 *)(out + a * CHG_KP);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+}
+
+// ---------------------------------------------------------------------------
+// GatedMLP output stage
+// ---------------------------------------------------------------------------
+struct RowStats { float mu, rstd; };
+__device__ __forceinline__ RowStats ln_stats(float a, float b) {
+  float mu = warp_sum(a + b) * (1.0f / 64.0f);
+  float da = a - mu, db = b - mu;
+  float var = warp_sum(da * da + db * db) * (1.0f / 64.0f);
+  return {mu, rsqrtf(var + 1e-5f)};
+}
+
+__global__ void k_gate_fwd(int64_t rows, const float *__restrict__ y, int ldy, GateLN ln, int mode,
+                           const float *__restrict__ w, const int32_t *__restrict__ i1, const int32_t *__restrict__ i2,
+                           const float *__restrict__ resid, float *__restrict__ out) {
+  int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int l = threadIdx.x & 31;
+  if (row >= rows) return;
+  int c0 = 2 * l;
+  float2 yc = *(const float2 *)(y + row * ldy + c0);
+  float2 yg = *(const float2 *)(y + row * ldy + 64 + c0);
+  RowStats sc = ln_stats(yc.x, yc.y), sg = ln_stats(yg.x, yg.y);
+  float2 gc = *(const float2 *)(ln.gc + c0), bc = *(const float2 *)(ln.bc + c0);
+  float2 gg = *(const float2 *)(ln.gg + c0), bg = *(const float2 *)(ln.bg + c0);
+  float nc0 = gc.x * (yc.x - sc.mu) * sc.rstd + bc.x, nc1 = gc.y * (yc.y - sc.mu) * sc.rstd + bc.y;
+  float ng0 = gg.x * (yg.x - sg.mu) * sg.rstd + bg.x, ng1 = gg.y * (yg.y - sg.mu) * sg.rstd + bg.y;
+  float p0 = sigmoidf_(ng0) * siluf_(nc0), p1 = sigmoidf_(ng1) * siluf_(nc1);
+  float2 o;
+  if (mode == GATE_MUL_W) {
+    float2 wv = *(const float2 *)(w + row * 64 + c0);
+    o = make_float2(p0 * wv.x, p1 * wv.y);
+  } else if (mode == GATE_MUL_W1W2) {
+    float2 w1 = *(const float2 *)(w + (int64_t)i1[row] * 64 + c0);
+    float2 w2 = *(const float2 *)(w + (int64_t)i2[row] * 64 + c0);
+    o = make_float2(p0 * w1.x * w2.x, p1 * w1.y * w2.y);
+  } else {
+    float2 r = *(const float2 *)(resid + row * 64 + c0);
+    o = make_float2(r.x + p0, r.y + p1);
+  }
+  *(float2 *)(out + row * 64 + c0) = o;
+}
+
+__global__ void __launch_bounds__(256) k_gate_bwd(int64_t rows, int64_t rpb, const float *__restrict__ y, int ldy,
+                                                  GateLN ln, int mode, const float *__restrict__ w,
+                                                  const int32_t *__restrict__ i1, const int32_t *__restrict__ i2,
+                                                  const float *__restrict__ dout, const int32_t *__restrict__ didx,
+                                                  float *__restrict__ dy, int lddy, float *__restrict__ dw_acc,
+                                                  float *__restrict__ q1, float *__restrict__ q2,
+                                                  float *__restrict__ partial) {
+  __shared__ float sh[8][256];
+  int l = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int c0 = 2 * l;
+  int64_t r0 = blockIdx.x * rpb, r1 = min(rows, r0 + rpb);
+  float2 gc = *(const float2 *)(ln.gc + c0), bc = *(const float2 *)(ln.bc + c0);
+  float2 gg = *(const float2 *)(ln.gg + c0), bg = *(const float2 *)(ln.bg + c0);
+  float a_gc[2] = {0, 0}, a_bc[2] = {0, 0}, a_gg[2] = {0, 0}, a_bg[2] = {0, 0};
+  for (int64_t row = r0 + wid; row < r1; row += 8) {
+    float2 yc = *(const float2 *)(y + row * ldy + c0);
+    float2 yg = *(const float2 *)(y + row * ldy + 64 + c0);
+    RowStats sc = ln_stats(yc.x, yc.y), sg = ln_stats(yg.x, yg.y);
+    float xc[2] = {(yc.x - sc.mu) * sc.rstd, (yc.y - sc.mu) * sc.rstd};
+    float xg[2] = {(yg.x - sg.mu) * sg.rstd, (yg.y - sg.mu) * sg.rstd};
+    float nc[2] = {gc.x * xc[0] + bc.x, gc.y * xc[1] + bc.y};
+    float ng[2] = {gg.x * xg[0] + bg.x, gg.y * xg[1] + bg.y};
+    float s_g[2] = {sigmoidf_(ng[0]), sigmoidf_(ng[1])};
+    float s_c[2] = {siluf_(nc[0]), siluf_(nc[1])};
+    float phi[2] = {s_g[0] * s_c[0], s_g[1] * s_c[1]};
+    int64_t drow = didx ? didx[row] : row;
+    float2 d2 = *(const float2 *)(dout + drow * 64 + c0);
+    float d[2] = {d2.x, d2.y};
+    float dphi[2];
+    if (mode == GATE_MUL_W) {
+      float2 wv = *(const float2 *)(w + row * 64 + c0);
+      dphi[0] = d[0] * wv.x; dphi[1] = d[1] * wv.y;
+      float2 acc = *(float2 *)(dw_acc + row * 64 + c0);
+      acc.x += d[0] * phi[0]; acc.y += d[1] * phi[1];
+      *(float2 *)(dw_acc + row * 64 + c0) = acc;
+    } else if (mode == GATE_MUL_W1W2) {
+      float2 w1 = *(const float2 *)(w + (int64_t)i1[row] * 64 + c0);
+      float2 w2 = *(const float2 *)(w + (int64_t)i2[row] * 64 + c0);
+      dphi[0] = d[0] * w1.x * w2.x; dphi[1] = d[1] * w1.y * w2.y;
+      *(float2 *)(q1 + row * 64 + c0) = make_float2(d[0] * phi[0] * w2.x, d[1] * phi[1] * w2.y);
+      *(float2 *)(q2 + row * 64 + c0) = make_float2(d[0] * phi[0] * w1.x, d[1] * phi[1] * w1.y);
+    } else {
+      dphi[0] = d[0]; dphi[1] = d[1];
+    }
+    float dnc[2], dng[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      dnc[q] = dphi[q] * s_g[q] * dsiluf_(nc[q]);
+      dng[q] = dphi[q] * s_c[q] * s_g[q] * (1.0f - s_g[q]);
+      a_gc[q] += dnc[q] * xc[q]; a_bc[q] += dnc[q];
+      a_gg[q] += dng[q] * xg[q]; a_bg[q] += dng[q];
+    }
+    float gdc[2] = {gc.x * dnc[0], gc.y * dnc[1]}, gdg[2] = {gg.x * dng[0], gg.y * dng[1]};
+    float m1c = warp_sum(gdc[0] + gdc[1]) * (1.0f / 64.0f);
+    float m2c = warp_sum(gdc[0] * xc[0] + gdc[1] * xc[1]) * (1.0f / 64.0f);
+    float m1g = warp_sum(gdg[0] + gdg[1]) * (1.0f / 64.0f);
+    float m2g = warp_sum(gdg[0] * xg[0] + gdg[1] * xg[1]) * (1.0f / 64.0f);
+    *(float2 *)(dy + row * lddy + c0) =
+        make_float2(sc.rstd * (gdc[0] - m1c - xc[0] * m2c), sc.rstd * (gdc[1] - m1c - xc[1] * m2c));
+    *(float2 *)(dy + row * lddy + 64 + c0) =
+        make_float2(sg.rstd * (gdg[0] - m1g - xg[0] * m2g), sg.rstd * (gdg[1] - m1g - xg[1] * m2g));
+  }
+  sh[wid][c0] = a_gc[0]; sh[wid][c0 + 1] = a_gc[1];
+  sh[wid][64 + c0] = a_bc[0]; sh[wid][64 + c0 + 1] = a_bc[1];
+  sh[wid][128 + c0] = a_gg[0]; sh[wid][128 + c0 + 1] = a_gg[1];
+  sh[wid][192 + c0] = a_bg[0]; sh[wid][192 + c0 + 1] = a_bg[1];
+  __syncthreads();
+  float s = 0.f;
+  for (int k = 0; k < 8; ++k) s += sh[k][threadIdx.x];
+  partial[blockIdx.x * 256 + threadIdx.x] = s;
+}
+
+__global__ void k_reduce_ln(int nblocks, const float *__restrict__ partial, GateLNGrad g) {
+  int j = threadIdx.x;   // 256
+  float s = 0.f;
+  for (int b = 0; b < nblocks; ++b) s += partial[(size_t)b * 256 + j];
+  float *dst = j < 64 ? g.gc : j < 128 ? g.bc : j < 192 ? g.gg : g.bg;
+  dst[j & 63] += s;
+}
+
+// ---------------------------------------------------------------------------
+// segmented sums (warp per target row, 2 columns per lane, fixed order)
+// ---------------------------------------------------------------------------
+struct SegArgs { SegSrc s[3]; int n; };
+
+__global__ void k_segsum(int64_t targets, float *__restrict__ out, int ldo, int accumulate, SegArgs a) {
+  int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int l = threadIdx.x & 31;
+  if (t >= targets) return;
+  float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (k >= a.n) break;
+    const SegSrc &S = a.s[k];
+    int64_t s = S.segmap ? (int64_t)S.segmap[t] : t + S.ptr_off;
+    if (s < 0) continue;
+    int r0 = S.ptr[s], r1 = S.ptr[s + 1];
+#pragma unroll 4
+    for (int r = r0; r < r1; ++r) {
+      int64_t row = S.perm ? S.perm[r] : r;
+      float2 v = *(const float2 *)(S.in + row * 64 + 2 * l);
+      acc.x += v.x; acc.y += v.y;
+    }
+  }
+  float2 *o = (float2 *)(out + t * ldo + 2 * l);
+  if (accumulate) { float2 p = *o; acc.x += p.x; acc.y += p.y; }
+  *o = acc;
+}
+
+// ---------------------------------------------------------------------------
+// heads
+// ---------------------------------------------------------------------------
+__global__ void k_heads_forces(int N, const int32_t *__restrict__ row_ptr, const float4 *__restrict__ vec,
+                               const float *__restrict__ n_e, float *__restrict__ F) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  float fx = 0.f, fy = 0.f, fz = 0.f;
+  for (int e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+    float4 d = vec[e];
+    float s = n_e[e] / d.w;
+    fx += s * d.x; fy += s * d.y; fz += s * d.z;
+  }
+  F[3 * i] = fx; F[3 * i + 1] = fy; F[3 * i + 2] = fz;
+}
+
+__device__ __forceinline__ void lattice_G(const float *L, float G[9]) {
+  float sh[3] = {0.f, 0.f, 0.f};
+  for (int p = 0; p < 3; ++p) {
+    float nx = L[3 * p], ny = L[3 * p + 1], nz = L[3 * p + 2];
+    float inv = rsqrtf(nx * nx + ny * ny + nz * nz);
+    sh[0] += nx * inv; sh[1] += ny * inv; sh[2] += nz * inv;
+  }
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) G[3 * a + b] = sh[a] * sh[b];
+}
+
+__global__ void k_heads_struct(const int32_t *__restrict__ atom_ptr, const float *__restrict__ lat,
+                               const float *__restrict__ inv_n, const float *__restrict__ e_atom,
+                               const float *__restrict__ M9, float *__restrict__ energy, float *__restrict__ epa,
+                               float *__restrict__ stress) {
+  __shared__ double sh[10][128];
+  int s = blockIdx.x, t = threadIdx.x;
+  int a0 = atom_ptr[s], a1 = atom_ptr[s + 1];
+  double acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int i = a0 + t; i < a1; i += blockDim.x) {
+    acc[0] += e_atom[i];
+    const float *M = M9 + (int64_t)i * 9;
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) acc[1 + 3 * a + b] += 0.5 * ((double)M[3 * a + b] + (double)M[3 * b + a]);
+  }
+  for (int k = 0; k < 10; ++k) sh[k][t] = acc[k];
+  __syncthreads();
+  for (int off = 64; off > 0; off >>= 1) {
+    if (t < off)
+      for (int k = 0; k < 10; ++k) sh[k][t] += sh[k][t + off];
+    __syncthreads();
+  }
+  if (t == 0) {
+    float G[9];
+    lattice_G(lat + 9 * s, G);
+    energy[s] = (float)sh[0][0];
+    epa[s] = (float)(sh[0][0] * inv_n[s]);
+    for (int k = 0; k < 9; ++k) stress[9 * s + k] = (float)(sh[1 + k][0] * inv_n[s] * G[k]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// loss + seeds (readings Q22, Q23)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double huber_d(double x, double d) {
+  double ax = fabs(x);
+  return ax < d ? 0.5 * x * x : d * (ax - 0.5 * d);
+}
+__device__ __forceinline__ float dhuber(float x, float d) { return fabsf(x) < d ? x : copysignf(d, x); }
+
+struct LossArgs {
+  int S, N;
+  const float *epa, *forces, *stress, *mag;
+  const float *l_epa, *l_forces, *l_stress, *l_mag;
+  const uint8_t *l_mask;
+  const int32_t *soa;
+  const float *inv_n, *lat;
+  float w_e, w_f, w_s, w_m, delta;
+  double Sg, Ng, Mg;   // Mg < 0: count the mask here
+};
+
+__global__ void k_loss(LossArgs a, double *out) {
+  __shared__ double sh[5][1024];
+  int t = threadIdx.x;
+  double le = 0, lf = 0, ls = 0, lm = 0, cm = 0;
+  for (int s = t; s < a.S; s += blockDim.x) {
+    le += huber_d((double)a.epa[s] - a.l_epa[s], a.delta);
+    for (int k = 0; k < 9; ++k) ls += huber_d((double)a.stress[9 * s + k] - a.l_stress[9 * s + k], a.delta);
+  }
+  for (int i = t; i < a.N; i += blockDim.x) {
+    for (int c = 0; c < 3; ++c) lf += huber_d((double)a.forces[3 * i + c] - a.l_forces[3 * i + c], a.delta);
+    if (a.l_mask[i]) { lm += huber_d((double)a.mag[i] - a.l_mag[i], a.delta); cm += 1.0; }
+  }
+  sh[0][t] = le; sh[1][t] = lf; sh[2][t] = ls; sh[3][t] = lm; sh[4][t] = cm;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if (t < off)
+      for (int k = 0; k < 5; ++k) sh[k][t] += sh[k][t + off];
+    __syncthreads();
+  }
+  if (t == 0) {
+    double Mg = a.Mg >= 0 ? a.Mg : sh[4][0];
+    double LE = a.w_e / a.Sg * sh[0][0], LF = a.w_f / (3.0 * a.Ng) * sh[1][0];
+    double LS = a.w_s / (9.0 * a.Sg) * sh[2][0], LM = Mg > 0 ? a.w_m / Mg * sh[3][0] : 0.0;
+    out[0] = LE + LF + LS + LM; out[1] = LE; out[2] = LF; out[3] = LS; out[4] = LM;
+    out[5] = Mg;
+  }
+}
+
+__global__ void k_seed_atom(LossArgs a, const double *lossbuf, float *__restrict__ d_eatom, float *__restrict__ dM9,
+                            float *__restrict__ d_mag, float *__restrict__ seedF) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.N) return;
+  int s = a.soa[i];
+  float in = a.inv_n[s];
+  d_eatom[i] = (float)(a.w_e / a.Sg) * dhuber(a.epa[s] - a.l_epa[s], a.delta) * in;
+  float G[9];
+  lattice_G(a.lat + 9 * s, G);
+  float cs = (float)(a.w_s / (9.0 * a.Sg));
+  float ds[9];
+  for (int k = 0; k < 9; ++k) ds[k] = cs * dhuber(a.stress[9 * s + k] - a.l_stress[9 * s + k], a.delta);
+  for (int p = 0; p < 3; ++p)
+    for (int q = 0; q < 3; ++q)
+      dM9[(int64_t)i * 9 + 3 * p + q] = in * 0.5f * (ds[3 * p + q] * G[3 * p + q] + ds[3 * q + p] * G[3 * q + p]);
+  float cf = (float)(a.w_f / (3.0 * a.Ng));
+  for (int c = 0; c < 3; ++c) seedF[3 * i + c] = cf * dhuber(a.forces[3 * i + c] - a.l_forces[3 * i + c], a.delta);
+  double Mg = lossbuf[5];
+  d_mag[i] = (Mg > 0 && a.l_mask[i]) ? (float)(a.w_m / Mg) * dhuber(a.mag[i] - a.l_mag[i], a.delta) : 0.f;
+}
+
+__global__ void k_seed_edge(int64_t E, const int32_t *__restrict__ center, const float4 *__restrict__ vec,
+                            const float *__restrict__ seedF, float *__restrict__ dn) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  float4 d = vec[e];
+  int i = center[e];
+  dn[e] = (seedF[3 * i] * d.x + seedF[3 * i + 1] * d.y + seedF[3 * i + 2] * d.z) / d.w;
+}
+
+// ---------------------------------------------------------------------------
+// utilities
+// ---------------------------------------------------------------------------
+__global__ void k_transpose(const int64_t *__restrict__ off, const int32_t *__restrict__ rc, const float *__restrict__ p,
+                            float *__restrict__ wt) {
+  int t = blockIdx.x;
+  int64_t o = off[t];
+  int R = rc[2 * t], C = rc[2 * t + 1];
+  for (int idx = threadIdx.x; idx < R * C; idx += blockDim.x) {
+    int i = idx / C, j = idx % C;
+    wt[o + (int64_t)j * R + i] = p[o + idx];
+  }
+}
+
+__global__ void k_embed(int64_t N, const int32_t *__restrict__ species, const float *__restrict__ W, float *__restrict__ v) {
+  int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t i = gt >> 4;
+  int c4 = (int)(gt & 15);
+  if (i >= N) return;
+  ((float4 *)(v + i * 64))[c4] = ((const float4 *)(W + (int64_t)(species[i] - 1) * 64))[c4];
+}
+
+__global__ void k_finite(int64_t n, const float *__restrict__ g, int *bad) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n && !isfinite(g[i])) atomicMin(bad, (int)i);
+}
+
+__global__ void k_adam(int64_t n, float *__restrict__ p, float *__restrict__ g, float *__restrict__ m,
+                       float *__restrict__ v, float lr, float b1, float b2, float eps, float step_size,
+                       float inv_sqrt_bc2) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float gi = g[i];
+  float mi = b1 * m[i] + (1.f - b1) * gi;
+  float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+  m[i] = mi;
+  v[i] = vi;
+  p[i] -= step_size * mi / (sqrtf(vi) * inv_sqrt_bc2 + eps);
+  g[i] = 0.f;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host wrappers
+// ---------------------------------------------------------------------------
+void basis_radial(chg_ctx *ctx, int64_t rows, const double4 *vec64, const int32_t *eor, const float *freq,
+                  double rc, int p, float *out) {
+  if (rows <= 0) return;
+  ProfScope ps(ctx, "basis", 0.0, rows * (4.0 + 32.0 + 128.0));
+  k_basis_radial<<<ceil_div(rows * 32, 256), 256, 0, ctx->stream>>>(rows, vec64, eor, freq, rc, p, out);
+  check_launch(ctx);
+}
+
+void basis_angle(chg_ctx *ctx, int64_t A, const double4 *vec64, const int32_t *e1, const int32_t *e2, float *out) {
+  if (A <= 0) return;
+  ProfScope ps(ctx, "basis", 0.0, A * (8.0 + 64.0 + 128.0));
+  k_basis_angle<<<ceil_div(A, 128), 128, 0, ctx->stream>>>(A, vec64, e1, e2, out);
+  check_launch(ctx);
+}
+
+void basis_freq_grad(chg_ctx *ctx, int64_t rows, const double4 *vec64, const int32_t *eor, const float *freq,
+                     double rc, int p, const float *dbasis, float *grad) {
+  if (rows <= 0) return;
+  int nb = std::min<int64_t>(296, ceil_div(rows, 8));
+  float *part = ctx->getf("freq_partial", (size_t)nb * 32);
+  ProfScope ps(ctx, "basis_bwd", 0.0, rows * (4.0 + 32.0 + 128.0));
+  k_basis_freq_grad<<<nb, 256, 0, ctx->stream>>>(rows, vec64, eor, freq, rc, p, dbasis, part);
+  check_launch(ctx);
+  k_reduce_cols<<<1, 32, 0, ctx->stream>>>(nb, CHG_K, 32, part, grad);
+  check_launch(ctx);
+}
+
+void gate_fwd(chg_ctx *ctx, int64_t rows, const float *y, int ldy, GateLN ln, int mode, const float *w,
+              const int32_t *i1, const int32_t *i2, const float *resid, float *out) {
+  if (rows <= 0) return;
+  ProfScope ps(ctx, "gate_fwd", 0.0, rows * (512.0 + 256.0 + (mode == GATE_MUL_W1W2 ? 520.0 : 256.0)));
+  k_gate_fwd<<<ceil_div(rows * 32, 256), 256, 0, ctx->stream>>>(rows, y, ldy, ln, mode, w, i1, i2, resid, out);
+  check_launch(ctx);
+}
+
+void gate_bwd(chg_ctx *ctx, int64_t rows, const float *y, int ldy, GateLN ln, int mode, const float *w,
+              const int32_t *i1, const int32_t *i2, const float *dout, const int32_t *didx, float *dy, int lddy,
+              float *dw_acc, float *q1, float *q2, GateLNGrad g) {
+  int64_t rpb = std::max<int64_t>(64, (rows + 591) / 592);
+  int nb = rows > 0 ? ceil_div(rows, rpb) : 0;
+  if (nb == 0) return;
+  float *part = ctx->getf("ln_partial", (size_t)nb * 256);
+  ProfScope ps(ctx, "gate_bwd", 0.0,
+               rows * (512.0 + 260.0 + 512.0 + (mode == GATE_MUL_W ? 768.0 : mode == GATE_MUL_W1W2 ? 1032.0 : 0.0)));
+  k_gate_bwd<<<nb, 256, 0, ctx->stream>>>(rows, rpb, y, ldy, ln, mode, w, i1, i2, dout, didx, dy, lddy, dw_acc, q1,
+                                          q2, part);
+  check_launch(ctx);
+  k_reduce_ln<<<1, 256, 0, ctx->stream>>>(nb, part, g);
+  check_launch(ctx);
+}
+
+void segsum(chg_ctx *ctx, int64_t targets, float *out, int ldo, int accumulate, int nsrc, const SegSrc *src) {
+  if (targets <= 0) return;
+  SegArgs a;
+  a.n = nsrc;
+  double bytes = targets * 256.0 * (1 + accumulate);
+  for (int k = 0; k < nsrc; ++k) {
+    a.s[k] = src[k];
+    bytes += src[k].rows * (256.0 + (src[k].perm ? 4.0 : 0.0)) + targets * (src[k].segmap ? 12.0 : 8.0);
+  }
+  ProfScope ps(ctx, "segsum", 0.0, bytes);
+  k_segsum<<<ceil_div(targets * 32, 256), 256, 0, ctx->stream>>>(targets, out, ldo, accumulate, a);
+  check_launch(ctx);
+}
+
+void heads_forces(chg_ctx *ctx, const chg_graph *g, const float *n_e, float *forces) {
+  if (g->N <= 0) return;
+  ProfScope ps(ctx, "heads", 0.0, g->E * 20.0 + g->N * 12.0);
+  k_heads_forces<<<ceil_div(g->N, 128), 128, 0, ctx->stream>>>((int)g->N, g->row_ptr, g->vec, n_e, forces);
+  check_launch(ctx);
+}
+
+void heads_struct(chg_ctx *ctx, const chg_graph *g, const float *e_atom, const float *M9, float *energy, float *epa,
+                  float *stress) {
+  if (g->S <= 0) return;
+  ProfScope ps(ctx, "heads", 0.0, g->N * 40.0 + g->S * 48.0);
+  k_heads_struct<<<g->S, 128, 0, ctx->stream>>>(g->atom_ptr, g->lattice_f, g->inv_natoms, e_atom, M9, energy, epa,
+                                                stress);
+  check_launch(ctx);
+}
+
+void loss_and_seeds(chg_ctx *ctx, const chg_graph *g, const float *epa, const float *forces, const float *stress,
+                    const float *mag, const chg_labels &lab, const chg_loss_cfg &cfg, LossSeeds seeds) {
+  LossArgs a;
+  a.S = g->S; a.N = (int)g->N;
+  a.epa = epa; a.forces = forces; a.stress = stress; a.mag = mag;
+  a.l_epa = lab.energy_per_atom; a.l_forces = lab.forces; a.l_stress = lab.stress; a.l_mag = lab.magmom;
+  a.l_mask = lab.magmom_mask;
+  a.soa = g->struct_of_atom; a.inv_n = g->inv_natoms; a.lat = g->lattice_f;
+  a.w_e = cfg.w_e; a.w_f = cfg.w_f; a.w_s = cfg.w_s; a.w_m = cfg.w_m; a.delta = cfg.huber_delta;
+  a.Sg = cfg.n_struct_global > 0 ? (double)cfg.n_struct_global : (double)g->S;
+  a.Ng = cfg.n_atoms_global > 0 ? (double)cfg.n_atoms_global : (double)g->N;
+  a.Mg = cfg.n_magmom_global > 0 ? (double)cfg.n_magmom_global : -1.0;
+  if (a.Sg <= 0) a.Sg = 1;
+  if (a.Ng <= 0) a.Ng = 1;
+  ProfScope ps(ctx, "loss", 0.0, g->N * 60.0 + g->S * 80.0 + g->E * 24.0);
+  k_loss<<<1, 1024, 0, ctx->stream>>>(a, ctx->d_loss);
+  check_launch(ctx);
+  if (g->N > 0) {
+    float *seedF = ctx->getf("seedF", 3 * g->N);
+    k_seed_atom<<<ceil_div(g->N, 128), 128, 0, ctx->stream>>>(a, ctx->d_loss, seeds.d_eatom, seeds.d_M9, seeds.d_mag,
+                                                              seedF);
+    check_launch(ctx);
+    if (g->E > 0) {
+      k_seed_edge<<<ceil_div(g->E, 256), 256, 0, ctx->stream>>>(g->E, g->center, g->vec, seedF, seeds.d_ne);
+      check_launch(ctx);
+    }
+  }
+}
+
+void transpose_params(chg_ctx *ctx, const chg_model *m, float *wt) {
+  if (m->n2d <= 0) return;
+  ProfScope ps(ctx, "transpose", 0.0, 8.0 * m->P);
+  k_transpose<<<m->n2d, 256, 0, ctx->stream>>>(m->d_toff, m->d_trc, m->params, wt);
+  check_launch(ctx);
+}
+
+void fill_zero(chg_ctx *ctx, void *p, size_t bytes) {
+  if (bytes) CUDA_OK(cudaMemsetAsync(p, 0, bytes, ctx->stream));
+}
+
+void embed_fwd(chg_ctx *ctx, int64_t N, const int32_t *species, const float *W, float *v) {
+  if (N <= 0) return;
+  ProfScope ps(ctx, "embed", 0.0, N * 260.0);
+  k_embed<<<ceil_div(N * 16, 256), 256, 0, ctx->stream>>>(N, species, W, v);
+  check_launch(ctx);
+}
+
+int finite_check(chg_ctx *ctx, const float *g, int64_t n) {
+  int *bad = ctx->d_flag;
+  ProfScope ps(ctx, "adam", 0.0, 4.0 * n);
+  CUDA_OK(cudaMemsetAsync(bad, 0x7f, 4, ctx->stream));   // 0x7f7f7f7f means none
+  k_finite<<<ceil_div(n, 256), 256, 0, ctx->stream>>>(n, g, bad);
+  check_launch(ctx);
+  int *h = (int *)ctx->pinned_get(64);
+  CUDA_OK(cudaMemcpyAsync(h, bad, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  return *h == 0x7f7f7f7f ? -1 : *h;
+}
+
+void adam_update(chg_ctx *ctx, int64_t n, float *p, float *g, float *m, float *v, float lr, float b1, float b2,
+                 float eps, double bc1, double bc2) {
+  float step_size = (float)(lr / bc1);
+  float inv_sqrt_bc2 = (float)(1.0 / std::sqrt(bc2));
+  ProfScope ps(ctx, "adam", 0.0, 28.0 * n);
+  k_adam<<<ceil_div(n, 256), 256, 0, ctx->stream>>>(n, p, g, m, v, lr, b1, b2, eps, step_size, inv_sqrt_bc2);
+  check_launch(ctx);
+}

@@ -1,0 +1,52 @@
+// ops.cuh — non-GEMM kernels of the hot path (declarations; see ops.cu).
+#pragma once
+#include "common.cuh"
+
+// A2 basis (Eq. 12/13 reading Q2, Alg. 2): out [rows, 32] fp32, col 31 = 0
+void basis_radial(chg_ctx *ctx, int64_t rows, const double4 *vec64, const int32_t *edge_of_row,
+                  const float *freq, double r_cut, int p, float *out);
+void basis_angle(chg_ctx *ctx, int64_t A, const double4 *vec64, const int32_t *e1, const int32_t *e2,
+                 float *out);
+// ∂L/∂f_n = Σ_rows dẽ[row, n] · u · sqrt(2/rc) · cos(f_n r / rc) / rc  (accumulated into grad)
+void basis_freq_grad(chg_ctx *ctx, int64_t rows, const double4 *vec64, const int32_t *edge_of_row,
+                     const float *freq, double r_cut, int p, const float *dbasis, float *grad);
+
+// GatedMLP output stage: φ = σ(LN_g(y_g)) ⊙ SiLU(LN_c(y_c)); y [rows,128] = [core | gate]
+struct GateLN { const float *gc, *bc, *gg, *bg; };
+enum GateMode { GATE_MUL_W = 0, GATE_MUL_W1W2 = 1, GATE_RESID = 2 };
+void gate_fwd(chg_ctx *ctx, int64_t rows, const float *y, int ldy, GateLN ln, int mode, const float *w,
+              const int32_t *i1, const int32_t *i2, const float *resid, float *out);
+// backward: dout gathered via didx (nullptr = row); writes dy [rows, 128] (ldd), LN grads
+// accumulated into (dgc, dbc, dgg, dbg).  mode GATE_MUL_W: dw_out[row] += dout*φ (dea).
+// mode GATE_MUL_W1W2: q1[row] = dout*φ*w[i2], q2[row] = dout*φ*w[i1].
+struct GateLNGrad { float *gc, *bc, *gg, *bg; };
+void gate_bwd(chg_ctx *ctx, int64_t rows, const float *y, int ldy, GateLN ln, int mode, const float *w,
+              const int32_t *i1, const int32_t *i2, const float *dout, const int32_t *didx, float *dy,
+              int lddy, float *dw_acc, float *q1, float *q2, GateLNGrad g);
+
+// segmented row sums: out[t] (+)= Σ_src Σ_{r ∈ [ptr[s], ptr[s+1])} in[perm ? perm[r] : r]
+// with s = segmap ? segmap[t] : t + ptr_off (segmap < 0 -> nothing).  64 columns.
+struct SegSrc { const float *in = nullptr; const int32_t *ptr = nullptr; const int32_t *perm = nullptr;
+                const int32_t *segmap = nullptr; int ptr_off = 0;
+                int64_t rows = 0;   // total input rows summed (algorithmic-bytes bookkeeping only)
+};
+void segsum(chg_ctx *ctx, int64_t targets, float *out, int ldo, int accumulate, int nsrc, const SegSrc *src);
+
+// heads (Eq. 7, Eq. 9)
+void heads_forces(chg_ctx *ctx, const chg_graph *g, const float *n_e, float *forces);
+void heads_struct(chg_ctx *ctx, const chg_graph *g, const float *e_atom, const float *M9, float *energy,
+                  float *epa, float *stress);
+// loss + seeds; returns nothing, writes ctx->d_loss[0..4]
+struct LossSeeds { float *d_eatom, *d_M9, *d_mag, *d_ne; };
+void loss_and_seeds(chg_ctx *ctx, const chg_graph *g, const float *epa, const float *forces,
+                    const float *stress, const float *mag, const chg_labels &lab, const chg_loss_cfg &cfg,
+                    LossSeeds seeds);
+
+// utilities
+void transpose_params(chg_ctx *ctx, const chg_model *m, float *wt);
+void fill_zero(chg_ctx *ctx, void *p, size_t bytes);
+void embed_fwd(chg_ctx *ctx, int64_t N, const int32_t *species, const float *W, float *v);
+// Adam (PyTorch semantics) + finite check
+int finite_check(chg_ctx *ctx, const float *g, int64_t n);   // returns first bad index or -1 (syncs)
+void adam_update(chg_ctx *ctx, int64_t n, float *p, float *g, float *m, float *v, float lr, float b1,
+                 float b2, float eps, double bc1, double bc2);
