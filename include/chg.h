@@ -52,7 +52,9 @@ typedef struct { double r_atom, r_bond; } chg_cutoffs;
  * t = 0,1,2) plus a final atom conv; the angle update of the last block has no
  * consumer and is skipped (reading Q17).  gmlp_hidden = 64: each
  * GatedMLP branch of atom/bond conv is Linear-SiLU-Linear (reading Q12).
- * mlp_precision: 0 = fp32 CUDA cores (strict parity). Only d = 64,
+ * mlp_precision: 0 = fp32 CUDA cores (strict parity: gradients <= 1e-4);
+ * 2 = TF32 on the tcgen05 tensor cores for the GatedMLP / linear GEMMs
+ * (gradients <= 2e-3, NS "loosened" mode), fp32 everywhere else. Only d = 64,
  * n_radial = n_angular = 31, gmlp_hidden = head_hidden = 64 are built. */
 typedef struct {
   int d, n_radial, n_angular, envelope_p, n_atom_conv, n_bond_conv, gmlp_hidden,

@@ -263,9 +263,9 @@ chg_status chg_model_create(chg_ctx *ctx, const chg_model_cfg *cfg, chg_model **
     const chg_model_cfg &c = *cfg;
     if (c.d != 64 || c.n_radial != 31 || c.n_angular != 31 || c.gmlp_hidden != 64 || c.head_hidden != 64 ||
         c.n_atom_conv != c.n_bond_conv + 1 || c.n_bond_conv < 1 || c.n_species != 94 || c.envelope_p < 2 ||
-        c.mlp_precision != 0)
+        (c.mlp_precision != 0 && c.mlp_precision != 2))
       CHG_THROW(CHG_ERR_ARG, "unsupported model config (built: d=64, K=31, hidden 64, n_atom_conv = n_bond_conv+1, "
-                             "94 species, mlp_precision 0)");
+                             "94 species, mlp_precision 0 (fp32) or 2 (tf32 tcgen05))");
     build_layout(m);
     CUDA_OK(cudaSetDevice(ctx->device));
     CUDA_OK(cudaMalloc(&m->params, 4 * m->P * 4));

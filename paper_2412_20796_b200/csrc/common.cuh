@@ -61,6 +61,10 @@ struct chg_ctx {
   const chg_graph *fwd_graph = nullptr;
   uint64_t fwd_graph_id = 0;
   bool fwd_train = false;
+  // GEMM engine for the current call: false = fp32 CUDA cores, true = tcgen05 TF32
+  bool use_tc = false;
+  const struct chg_model *cur_model = nullptr;   // model of the current forward/backward
+  const float *cur_wt = nullptr;                 // its transposed weight copy (same flat offsets)
   // debug name -> (ptr, rows, cols, ld)
   struct Dbg { const float *p; int64_t rows, cols, ld; };
   std::map<std::string, Dbg> dbg;

@@ -247,8 +247,42 @@ bool aop_vec(const AOp &A) {
 
 }  // namespace
 
+// K-major view of an N-major weight block through the transposed parameter copy
+// (params and wt share flat offsets; tensor t = [R, C] in params, [C, R] in wt).
+static bool kmajor_of(const chg_model *m, const float *wt, const float *p, int ldw, const float **pk, int *ldk) {
+  for (int side = 0; side < 2; ++side) {
+    const float *base = side == 0 ? m->params : wt;
+    if (p < base || p >= base + m->P) continue;
+    int64_t rel = p - base;
+    auto it = std::upper_bound(m->offsets.begin(), m->offsets.end(), rel);
+    int t = (int)(it - m->offsets.begin()) - 1;
+    int R = m->shapes[2 * t], C = m->shapes[2 * t + 1];
+    if (C == 0) return false;
+    int64_t o = m->offsets[t], r = rel - o;
+    if (side == 0) {                      // W [R, C] used N-major with ld C
+      if (ldw != C) return false;
+      int64_t k0 = r / C, n0 = r % C;
+      *pk = wt + o + n0 * R + k0; *ldk = R;
+    } else {                              // Wᵀ [C, R] used N-major with ld R
+      if (ldw != R) return false;
+      int64_t k0 = r / R, n0 = r % R;
+      *pk = m->params + o + n0 * C + k0; *ldk = C;
+    }
+    return true;
+  }
+  return false;
+}
+
 void rowgemm(chg_ctx *ctx, const RowGemm &g) {
   if (g.M <= 0) return;
+  if (g.tc && ctx->use_tc && ctx->cur_model && ctx->cur_wt) {
+    RowGemm h = g;
+    bool ok = true;
+    for (int c = 0; c < h.nchunk && ok; ++c)
+      for (int b = 0; b < h.ch[c].nwb && ok; ++b)
+        ok = kmajor_of(ctx->cur_model, ctx->cur_wt, h.ch[c].W[b], h.ch[c].ldw[b], &h.ch[c].Wk[b], &h.ch[c].ldwk[b]);
+    if (ok && rowgemm_tc(ctx, h)) return;
+  }
   bool vec = aop_vec(g.A);
   int tot = 0;
   for (int s = 0; s < g.A.nseg; ++s) tot += g.A.seg[s].width;

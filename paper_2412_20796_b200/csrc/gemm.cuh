@@ -38,6 +38,10 @@ struct Chunk {
   const float *resid = nullptr; int ldr = 0;   // added after activation
   float *pre = nullptr; int ldp = 0;           // pre-activation store
   const float *mul = nullptr; int ldm = 0;     // v *= dsilu(mul) (backward of silu)
+  // K-major view of the same weight blocks (element (n, k) at Wk[b][n*ldwk[b] + k - wk0[b]]),
+  // filled by the orchestration for the tensor-core path (tc_gemm.cu)
+  const float *Wk[4] = {nullptr, nullptr, nullptr, nullptr};
+  int ldwk[4] = {0, 0, 0, 0};
 };
 
 struct RowGemm {
@@ -46,6 +50,7 @@ struct RowGemm {
   int K = 0;                     // reduction length (per chunk)
   int act = 0;                   // 0 none, 1 silu
   int nchunk = 1;
+  int tc = 0;                    // 1: a GatedMLP contraction -> tensor cores in TF32 mode (NS)
   Chunk ch[4];
 };
 
@@ -65,7 +70,8 @@ struct WGrad {
   WGradDst dst[4];               // per 64-column chunk of N
 };
 
-void rowgemm(chg_ctx *ctx, const RowGemm &g);
+void rowgemm(chg_ctx *ctx, const RowGemm &g);      // tcgen05 when ctx->use_tc and eligible, else SIMT
+bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g);   // false if the shape does not fit the tensor-core path
 void wgrad(chg_ctx *ctx, const WGrad &g);
 
 // helpers to fill descriptors

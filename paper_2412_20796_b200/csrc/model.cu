@@ -50,7 +50,7 @@ void atom_conv_fwd(Fwd &F, int t, const float *v, const float *e, const float *e
     G.A.seg[1] = aseg(v, 64, 64, g->nbr);
     G.A.seg[2] = aseg(e, 64, 64);
     G.A.nseg = 3;
-    G.M = (int)E; G.K = 192; G.nchunk = 2;
+    G.M = (int)E; G.K = 192; G.nchunk = 2; G.tc = 1;
     G.ch[0] = chunk1(m->p(pre + ".core.W1"), 64, 192, m->p(pre + ".core.b1"), z1, 128);
     G.ch[1] = chunk1(m->p(pre + ".gate.W1"), 64, 192, m->p(pre + ".gate.b1"), z1 + 64, 128);
     rowgemm(ctx, G);
@@ -59,7 +59,7 @@ void atom_conv_fwd(Fwd &F, int t, const float *v, const float *e, const float *e
     RowGemm G;
     G.A.seg[0] = aseg(z1, 128, 128);
     G.A.nseg = 1; G.A.act = 1;
-    G.M = (int)E; G.K = 64; G.nchunk = 2;
+    G.M = (int)E; G.K = 64; G.nchunk = 2; G.tc = 1;
     G.ch[0] = chunk1(m->p(pre + ".core.W2"), 64, 64, m->p(pre + ".core.b2"), y, 128);
     G.ch[1] = chunk1(m->p(pre + ".gate.W2"), 64, 64, m->p(pre + ".gate.b2"), y + 64, 128);
     G.ch[1].a_k0 = 64;
@@ -103,7 +103,7 @@ void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float
     G.A.seg[2] = aseg(e, 64, 64, g->angle_e2);
     G.A.seg[3] = aseg(a, 64, 64);
     G.A.nseg = 4;
-    G.M = (int)A; G.K = 256; G.nchunk = angle_branch ? 4 : 2;
+    G.M = (int)A; G.K = 256; G.nchunk = angle_branch ? 4 : 2; G.tc = 1;
     G.ch[0] = chunk1(m->p(bp + ".core.W1"), 64, 256, m->p(bp + ".core.b1"), z1, 128);
     G.ch[1] = chunk1(m->p(bp + ".gate.W1"), 64, 256, m->p(bp + ".gate.b1"), z1 + 64, 128);
     if (angle_branch) {
@@ -114,7 +114,7 @@ void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float
     RowGemm H;
     H.A.seg[0] = aseg(z1, 128, 128);
     H.A.nseg = 1; H.A.act = 1;
-    H.M = (int)A; H.K = 64; H.nchunk = 2;
+    H.M = (int)A; H.K = 64; H.nchunk = 2; H.tc = 1;
     H.ch[0] = chunk1(m->p(bp + ".core.W2"), 64, 64, m->p(bp + ".core.b2"), yb, 128);
     H.ch[1] = chunk1(m->p(bp + ".gate.W2"), 64, 64, m->p(bp + ".gate.b2"), yb + 64, 128);
     H.ch[1].a_k0 = 64;
@@ -178,6 +178,14 @@ void forward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, int train, chg_pred 
   const int p = m->cfg.envelope_p;
   ctx->dbg.clear();
   ctx->fwd_train = false;
+  ctx->use_tc = m->cfg.mlp_precision == 2;
+  ctx->cur_model = m;
+  ctx->cur_wt = nullptr;
+  if (ctx->use_tc) {   // K-major weight copy for the tensor-core operands
+    float *wt = ctx->getf("wt", m->P);
+    transpose_params(ctx, m, wt);
+    ctx->cur_wt = wt;
+  }
   // A2 bases (fp64 geometry, fp32 features)
   float *ea_t = F.buf("ea_t", E, 32), *eb_t = F.buf("eb_t", B, 32), *a_t = F.buf("a_t", A, 32);
   basis_radial(ctx, E, g->vec64, nullptr, m->p("rbf_a.freq"), g->r_atom, p, ea_t);
@@ -375,7 +383,7 @@ void ac_bwd_body(Bwd &Bw, int t, const float *v, const float *e, const float *ea
     RowGemm G;
     G.A.seg[0] = aseg(dY, 128, 128);
     G.A.nseg = 1;
-    G.M = (int)E; G.K = 64; G.nchunk = 2;
+    G.M = (int)E; G.K = 64; G.nchunk = 2; G.tc = 1;
     G.ch[0] = chunk1(Bw.WT(pre + ".core.W2"), 64, 64, nullptr, dZ, 128);
     G.ch[0].mul = z1; G.ch[0].ldm = 128;
     G.ch[1] = chunk1(Bw.WT(pre + ".gate.W2"), 64, 64, nullptr, dZ + 64, 128);
@@ -396,7 +404,7 @@ void ac_bwd_body(Bwd &Bw, int t, const float *v, const float *e, const float *ea
     RowGemm G;
     G.A.seg[0] = aseg(dZ, 128, 128);
     G.A.nseg = 1;
-    G.M = (int)E; G.K = 128; G.nchunk = 3;
+    G.M = (int)E; G.K = 128; G.nchunk = 3; G.tc = 1;
     float *outs[3] = {ti, tj, de};
     for (int c = 0; c < 3; ++c) {
       Chunk &C = G.ch[c];
@@ -447,7 +455,7 @@ void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float 
     RowGemm G;
     G.A.seg[0] = aseg(dYb, 128, 128);
     G.A.nseg = 1;
-    G.M = (int)A; G.K = 64; G.nchunk = 2;
+    G.M = (int)A; G.K = 64; G.nchunk = 2; G.tc = 1;
     G.ch[0] = chunk1(Bw.WT(bp + ".core.W2"), 64, 64, nullptr, dZ, 256);
     G.ch[0].mul = z1; G.ch[0].ldm = 128;
     G.ch[1] = chunk1(Bw.WT(bp + ".gate.W2"), 64, 64, nullptr, dZ + 64, 256);
@@ -469,7 +477,7 @@ void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float 
     RowGemm G;
     G.A.seg[0] = aseg(dZ, 256, Kx);
     G.A.nseg = 1;
-    G.M = (int)A; G.K = Kx; G.nchunk = 4;
+    G.M = (int)A; G.K = Kx; G.nchunk = 4; G.tc = 1;
     float *outs[4] = {tv, t1, t2, da};
     for (int c = 0; c < 4; ++c) {
       Chunk &C = G.ch[c];
@@ -547,6 +555,9 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
                  sd);
   Bw.wt = ctx->getf("wt", m->P);
   transpose_params(ctx, m, Bw.wt);
+  ctx->use_tc = m->cfg.mlp_precision == 2;
+  ctx->cur_model = m;
+  ctx->cur_wt = Bw.wt;
   float *dv = Bw.scratch("dv", N, 64), *de = Bw.scratch("de", E, 64), *da = Bw.scratch("da", A, 64);
   float *dea = Bw.scratch("dea", E, 64), *deb = Bw.scratch("deb", B, 64);
   fill_zero(ctx, dv, 4 * 64 * N);
