@@ -51,6 +51,8 @@ def _args():
     ap.add_argument("--per-gpu", type=int, default=0, help="structures per GPU (default: 40 at N=1, 128 at N>1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"],
+                    help="GatedMLP GEMM engine: tf32 = tcgen05 tensor cores, fp32 = CUDA cores (strict parity)")
     return ap.parse_args()
 
 
@@ -212,9 +214,16 @@ def main():
             uid.copy_(torch.frombuffer(bytearray(chg.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(uid, 0)
         ctx.set_nccl(bytes(uid.cpu().numpy()), ws, rank)
-    model = chg.Model(ctx)
-    layout = [(n, s) for n, s, _ in model.layout()]     # the library's own layout table
-    model.set_params(init_flat_params(layout, seed=0).astype(np.float32))
+    def make_model(prec):
+        cfg = chg.default_model_cfg()
+        cfg.mlp_precision = 2 if prec == "tf32" else 0
+        mm = chg.Model(ctx, cfg)
+        lay = [(n, s) for n, s, _ in mm.layout()]         # the library's own layout table
+        mm.set_params(init_flat_params(lay, seed=0).astype(np.float32))
+        return mm
+    other = "fp32" if a.precision == "tf32" else "tf32"
+    models = {a.precision: make_model(a.precision), other: make_model(other)}
+    model = models[a.precision]
 
     # ---- batches: global batch per index, balanced over ranks
     batches = []
@@ -261,7 +270,8 @@ def main():
     total_steps = 2 * (a.warmup + a.steps) + 8
     step_no = [0]
 
-    def one_step(b, on_host: bool):
+    def one_step(b, on_host: bool, model=None):
+        model = model or models[a.precision]
         step_no[0] += 1
         lr = lr0 * 0.5 * (1 + math.cos(math.pi * step_no[0] / total_steps))   # cosine
         src = b["host"] if on_host else b["dev"]
@@ -281,7 +291,7 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    def timed(on_host: bool, profile: bool = False):
+    def timed(on_host: bool, profile: bool = False, model=None):
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
         if profile:
             ctx.profile(True)
@@ -290,7 +300,7 @@ def main():
         for k in range(a.steps):
             b = batches[k % len(batches)]
             ev[k][0].record(stream)
-            one_step(b, on_host)
+            one_step(b, on_host, model)
             ev[k][1].record(stream)
             with torch.cuda.stream(stream):
                 flush.zero_()                              # L2 flush outside the timed events
@@ -315,8 +325,11 @@ def main():
     clk = clocks.stop()
     ms_e2e, _, _ = timed(True)
     ms_prof, _, rep = timed(False, profile=True)
+    for k in range(a.warmup):
+        one_step(batches[k % len(batches)], False, models[other])
+    ms_other, _, _ = timed(False, model=models[other])
 
-    structs = sum(batches[k % len(batches)]["gl"]["S"] for k in range(a.steps)) / ws * ws
+    structs = sum(batches[k % len(batches)]["gl"]["S"] for k in range(a.steps))
     value = structs / (ms / 1e3)
     e2e = structs / (ms_e2e / 1e3)
     h2d = int(np.mean([batches[k % len(batches)]["h2d"] for k in range(a.steps)]))
@@ -333,15 +346,21 @@ def main():
         pass
     if dom in HBM_TAGS:
         ach = r["bytes"] / (r["ms"] / 1e3) / 1e9
-        roof = {"bound": "hbm", "achieved": ach, "peak": PEAKS["hbm_gbs"], "unit": "GB/s"}
+        roof = {"bound": "hbm", "achieved": ach, "peak": PEAKS["hbm_gbs"], "unit": "GB/s", "peak_source": PEAK_SRC}
+    elif dom == "rowgemm_tc":
+        # TF32 dense peak = measured bf16 cuBLAS peak (sustained: kernel timed inside a long step) x 1/2
+        # (nominal tf32:bf16 ratio 1.1 : 2.25 PF/s, B200_PROFILING.md)
+        ach = r["flops"] / (r["ms"] / 1e3) / 1e12
+        pk = PEAKS.get("bf16_tflops_sustained", PEAKS.get("bf16_tflops", 1590.0)) * 1.1 / 2.25
+        roof = {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
+                "peak_source": "tf32 = " + PEAK_SRC + " bf16_tflops_sustained x (1.1/2.25 nominal ratio)"}
     else:
         ach = r["flops"] / (r["ms"] / 1e3) / 1e12
-        roof = {"bound": "alu", "achieved": ach, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s"}
+        roof = {"bound": "alu", "achieved": ach, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "peak_source": "FP32 CUDA cores: 148 SM x 128 FMA/clk x 2 x sm_max_mhz (DESIGN.md)"}
     roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": traffic, "kernel": dom,
                  "algorithmic_per_launch": (r["bytes"] if roof["bound"] == "hbm" else r["flops"]) / max(r["launches"], 1),
-                 "avg_launch_us": per_launch_s * 1e6, "share_of_step": r["ms"] / ms_prof,
-                 "peak_source": PEAK_SRC if roof["bound"] == "hbm" else
-                 "FP32 CUDA cores: 148 SM x 128 FMA/clk x 2 x sm_max_mhz (DESIGN.md)"})
+                 "avg_launch_us": per_launch_s * 1e6, "share_of_step": r["ms"] / ms_prof})
     gs = rep.get("segsum", {"bytes": 0.0, "ms": 1e-9})
     gather = {"kernel": "segsum (atomic-free CSR / rev / swap segmented gather-reduce)",
               "achieved_gbs": gs["bytes"] / (gs["ms"] / 1e3) / 1e9,
@@ -357,7 +376,11 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "structures/s", "n_gpus": ws, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "vs_baseline": None, "dtype": "tf32+f32" if a.precision == "tf32" else "f32", "data": "synthetic",
+            "precision": {"mode": a.precision,
+                          "note": "tf32: GatedMLP GEMMs on tcgen05 (TF32, fp32 accumulate), all else fp32; "
+                                  "fp32: everything on CUDA cores (strict 1e-4 gradient parity)",
+                          other: {"value": structs / (ms_other / 1e3), "ms_per_step": ms_other / a.steps}},
             "config": {"workload": f"{wl}: MPtrj-shaped synthetic batch, {per} structures per GPU "
                                    f"(5/3 Å cutoffs, d=64, 4 atom-conv / 3 bond-conv)",
                        "structures_per_gpu": per, "global_batch": per * ws, "parallelism": f"dp{ws}",

@@ -2,23 +2,26 @@
 //
 // Same contract as k_rowgemm (gemm.cuh): out[m, n] = epi(Σ_k A(m, k) W(k, n) + b)
 // with A gathered row by row from up to 4 tables.  One CTA = 128 rows (UMMA
-// M = 128, cta_group::1), all output chunks; the accumulator lives in TMEM
-// (128 lanes × up to 256 fp32 columns) and is read back by the 4 epilogue
-// warps with tcgen05.ld (one TMEM lane = one output row = one thread).
+// M = 128, cta_group::1) and every output chunk; the fp32 accumulator lives in
+// TMEM (128 lanes × up to 256 columns) and is read back with tcgen05.ld (one
+// TMEM lane = one output row).
 //
-// Operands: kind::tf32 (fp32 bits rounded to TF32 with cvt.rna), K-major,
-// SWIZZLE_NONE canonical layout: element (row, k) of a tile with R rows at
-// byte  (k/4)·(R·16) + row·16 + (k%4)·4   (core matrix = 8 rows × 16 B;
-// SBO = 128 B between 8-row groups, LBO = R·16 B between 16-B K chunks).
-// A is staged by all 128 threads (thread = row; the gather is the row index),
-// B (weights, K-major copy) likewise; 2-stage smem ring over K chunks of 32,
-// MMA completion tracked with tcgen05.commit -> mbarrier.
+// Operands: kind::tf32 (round-to-nearest TF32), K-major, SWIZZLE_NONE canonical
+// layout: element (row, k) of an R-row tile at byte (k/4)·(R·16) + row·16 +
+// (k%4)·4 (core matrix 8 rows × 16 B; SBO = 128 B, LBO = R·16 B).
+//   B (weights): packed ONCE per GEMM into that exact smem image (k_pack_b,
+//     TF32-rounded, one image per K chunk) and streamed into smem with
+//     cp.async.bulk (TMA bulk copy, completion via mbarrier expect_tx).
+//   A (gathered activations): 256 threads, 8 lanes per row (coalesced 128-B
+//     row segments), registers prefetch the next K chunk while the tensor core
+//     runs the current one; 2-stage smem ring, tcgen05.commit -> mbarrier.
 #include "gemm.cuh"
 
 namespace {
 
-constexpr int TCM = 128;   // rows per CTA
-constexpr int KC = 32;     // K chunk per stage
+constexpr int TCM = 128;   // rows per CTA (UMMA M)
+constexpr int KC = 32;     // K chunk per pipeline stage
+
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -36,6 +39,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 
 __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -83,7 +97,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// A(m, col..col+3) (segments are 32-column aligned on this path)
+// A(m, col..col+3); segments are 32-column aligned on this path
 __device__ __forceinline__ float4 tc_loadA4(const AOp &A, int m, int col) {
   float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
   int start = 0;
@@ -102,153 +116,322 @@ __device__ __forceinline__ float4 tc_loadA4(const AOp &A, int m, int col) {
   return v;
 }
 
-// K-major weight row n (of chunk c), 4 consecutive k starting at k (k multiple of 4)
-__device__ __forceinline__ float4 tc_loadB4(const Chunk &c, int n, int k) {
-  if (n >= c.ncols) return make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-  for (int b = 0; b < 4; ++b)
-    if (b < c.nwb && k >= c.wk0[b] && k < c.wk0[b + 1]) {
-      // flat parameter offsets are not 16-B aligned: scalar (L1/L2-resident) loads
-      const float *p = c.Wk[b] + (size_t)n * c.ldwk[b] + (k - c.wk0[b]);
-      return make_float4(__ldg(p), __ldg(p + 1), __ldg(p + 2), __ldg(p + 3));
-    }
-  return make_float4(0.f, 0.f, 0.f, 0.f);
-}
-
 struct TcPlan {
   int lo;            // first A column of the union window
-  int width;         // union window width (multiple of 32)
+  int width;         // union window width (multiple of KC)
   int cpad[4];       // padded N of each chunk (multiple of 16)
-  int coff[4];       // TMEM column offset of each chunk
-  int ntot;          // total padded N
+  int coff[4];       // TMEM / image column offset of each chunk (multiple of 32)
+  int ntot;          // total image rows N
   uint32_t tmem_cols;
 };
 
-__global__ void __launch_bounds__(128, 1) k_rowgemm_tc(const RowGemm g, const TcPlan P) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int m0 = blockIdx.x * TCM;
+// B image: img[kc][q][n][4] = tf32(W_chunk(n - coff, k = lo + kc·KC - a_k0 + 4q + r))
+__global__ void k_pack_b(const RowGemm g, const TcPlan P, uint32_t *__restrict__ img) {
+  int kc = blockIdx.y;
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;   // over NT * KC
+  if (idx >= P.ntot * KC) return;
+  int n = idx / KC, k = idx % KC;
+  float v = 0.f;
+  for (int c = 0; c < g.nchunk; ++c) {
+    const Chunk &C = g.ch[c];
+    int j = n - P.coff[c];
+    if (j < 0 || j >= C.ncols) continue;
+    int kk = P.lo + kc * KC - C.a_k0 + k;
+    if (kk < 0 || kk >= g.K) continue;
+    for (int b = 0; b < C.nwb; ++b)
+      if (kk >= C.wk0[b] && kk < C.wk0[b + 1]) v = C.Wk[b][(size_t)j * C.ldwk[b] + (kk - C.wk0[b])];
+  }
+  img[(size_t)kc * P.ntot * KC + ((k >> 2) * P.ntot + n) * 4 + (k & 3)] = to_tf32(v);
+}
+
+// ---------------------------------------------------------------------------
+// warp-specialised persistent kernel
+//   warps 0-7   A producers: cp.async gather of 128 rows x 32 columns per stage
+//               straight into the UMMA layout, then in-place SiLU/TF32 rounding
+//   warp 8      B producer: cp.async.bulk of the packed weight image per stage
+//   warp 9      MMA issuer (one thread): tcgen05.mma into a double-buffered
+//               TMEM accumulator, tcgen05.commit -> stage / accumulator barriers
+//   warps 10-13 epilogue: tcgen05.ld (one lane = one row) -> bias / act /
+//               pre / mul / resid -> global
+// ---------------------------------------------------------------------------
+constexpr int NSA = 5;              // A stages (16 KB each)
+constexpr int NSB = 3;              // B stages (<= 32 KB each)
+constexpr int WS_THREADS = 18 * 32;  // 8 A-producer, 1 B, 1 MMA, 8 epilogue warps
+constexpr int NEPI = 8;
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_n(int n) {
+  switch (n) {
+    case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+    case 3: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+    default: asm volatile("cp.async.wait_group 4;" ::: "memory"); break;
+  }
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const RowGemm g, const TcPlan P,
+                                                               const uint32_t *__restrict__ bimg, int ntiles,
+                                                               int skip) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // SWIZZLE_128B operand atoms need 1024-B aligned stage bases
+  uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int NT = P.ntot;
-  // smem carve: 2 stages of A [KC/4][128][4] and B [KC/4][NT][4] floats, barriers, tmem slot
   const uint32_t a_bytes = KC * TCM * 4, b_bytes = KC * NT * 4;
-  uint8_t *sA[2] = {smem, smem + a_bytes + b_bytes};
-  uint8_t *sB[2] = {smem + a_bytes, smem + 2 * a_bytes + b_bytes};
-  uint64_t *bar = (uint64_t *)(smem + 2 * (a_bytes + b_bytes));
-  uint32_t *tslot = (uint32_t *)(bar + 2);
+  uint8_t *sA = smem;                                   // [NSA][a_bytes]
+  uint8_t *sB = smem + NSA * a_bytes;                   // [NSB][b_bytes]
+  uint64_t *fullA = (uint64_t *)(sB + NSB * b_bytes);
+  uint64_t *emptyA = fullA + NSA;
+  uint64_t *loaded = emptyA + NSA;                      // cp.async completion per A stage
+  uint64_t *fullB = loaded + NSA;
+  uint64_t *emptyB = fullB + NSB;
+  uint64_t *tfull = emptyB + NSB;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tslot = (uint32_t *)(tempty + 2);
+  float *epi = (float *)(smem + NSA * a_bytes + NSB * b_bytes + 8 * (3 * NSA + 2 * NSB + 4) + 16);  // [8][32][33]
+  const uint32_t tcols = P.tmem_cols;                   // per accumulator buffer
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
-                 "r"(P.tmem_cols)
+                 "r"(2 * tcols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int i = 0; i < NSA; ++i) { mbar_init(&fullA[i], 4); mbar_init(&emptyA[i], 1); mbar_init(&loaded[i], 128); }
+    for (int i = 0; i < NSB; ++i) { mbar_init(&fullB[i], 1); mbar_init(&emptyB[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], NEPI); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
-
-  // instruction descriptor: D f32, A/B tf32, K-major, M = 128, N = chunk width
-  auto idesc_for = [&](int n) -> uint32_t {
-    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(TCM >> 4) << 24);
-  };
+  __shared__ uint64_t trace_ts[32], trace_ld[32], trace_cv[32];
+  if ((skip & 32) && tid == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    trace_ts[0] = t;
+  }
 
   const int nkc = P.width / KC;
-  const int m = m0 + tid;
-  const bool row_ok = m < g.M;
-  bool started[4] = {false, false, false, false};
-  for (int kc = 0; kc < nkc; ++kc) {
-    const int s = kc & 1;
-    if (kc >= 2) mbar_wait(&bar[s], ((kc - 2) >> 1) & 1);
-    const int col0 = P.lo + kc * KC;   // A column of this chunk
-    // --- stage A: thread = row, 8 float4 along k
-    {
-      uint8_t *dst = sA[s];
+  const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int total = my_tiles * nkc;
+
+  if (warp < 4) {
+    // ---------------- A loaders (4 warps): cp.async 16 B straight into the 128B-swizzled slots ----------------
+    // A stage layout (SWIZZLE_128B, K-major): row r's 32 tf32 occupy bytes [r*128, r*128+128),
+    // 16-B unit u stored at unit u ^ (r & 7).  Thread = (q: unit, rb); rows rb + 16 i.
+    // Row indices are loaded once per tile, so a chunk issues without dependent loads.
+    const int q = tid & 7, rb = tid >> 3;
+    int cur_tile = -1;
+    int ridx[8][4];
+    for (int gi = 0; gi < total; ++gi) {
+      const int tl = gi / nkc, kc = gi % nkc;
+      const int tile = blockIdx.x + tl * gridDim.x;
+      const int sa = gi % NSA, ua = gi / NSA;
+      if (tile != cur_tile) {
+        cur_tile = tile;
 #pragma unroll
-      for (int q = 0; q < KC / 4; ++q) {
-        float4 v = row_ok ? tc_loadA4(g.A, m, col0 + 4 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
-        uint4 u = make_uint4(to_tf32(v.x), to_tf32(v.y), to_tf32(v.z), to_tf32(v.w));
-        *(uint4 *)(dst + (q * TCM + tid) * 16) = u;
+        for (int i = 0; i < 8; ++i) {
+          const int m = tile * TCM + rb + 16 * i;
+#pragma unroll
+          for (int sg = 0; sg < 4; ++sg)
+            ridx[i][sg] = (sg < g.A.nseg && m < g.M) ? (g.A.seg[sg].idx ? __ldg(g.A.seg[sg].idx + m) : m) : -1;
+        }
       }
-    }
-    // --- stage B: rows n of every chunk whose window covers this A chunk
-    for (int c = 0; c < g.nchunk; ++c) {
-      const Chunk &C = g.ch[c];
-      int kk = col0 - C.a_k0;                 // k within the chunk's reduction
-      if (kk < 0 || kk >= g.K) continue;
-      for (int n = tid; n < P.cpad[c]; n += 128) {
-        uint8_t *dst = sB[s];
+      if (ua > 0) mbar_wait(&emptyA[sa], (ua - 1) & 1);
+      const int col = P.lo + kc * KC;
+      int seg = 0, start = 0;
+      bool found = false;
 #pragma unroll
-        for (int q = 0; q < KC / 4; ++q) {
-          float4 v = tc_loadB4(C, n, kk + 4 * q);
-          uint4 u = make_uint4(to_tf32(v.x), to_tf32(v.y), to_tf32(v.z), to_tf32(v.w));
-          *(uint4 *)(dst + (q * NT + P.coff[c] + n) * 16) = u;
+      for (int sg = 0; sg < 4; ++sg)
+        if (sg < g.A.nseg && !found) {
+          if (col < start + g.A.seg[sg].width) { seg = sg; found = true; }
+          else start += g.A.seg[sg].width;
+        }
+      const ASeg S = g.A.seg[seg];
+      const int cin = col - start + 4 * q;
+      const uint32_t dst0 = smem_u32(sA + sa * a_bytes);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        int r = -1;
+#pragma unroll
+        for (int sg = 0; sg < 4; ++sg)
+          if (sg == seg) r = ridx[i][sg];
+        if (skip & 2) r = -1;                         // debug: no gather traffic
+        const int row = rb + 16 * i;
+        const uint32_t dst = dst0 + row * 128 + ((q ^ (row & 7)) << 4);
+        if (r >= 0) cp_async16(dst, S.base + (size_t)r * S.ld + cin, 16);
+        else cp_async16(dst, g.A.seg[0].base, 0);     // zero fill
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&loaded[sa])) : "memory");
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ---------------- A converters: thread = row; SiLU (GEMM2 input) + TF32 RN in place ----------------
+    const int r = tid - 128;
+    const int sw = r & 7;
+    for (int gi = 0; gi < total; ++gi) {
+      const int sa = gi % NSA, ua = gi / NSA;
+      mbar_wait(&loaded[sa], ua & 1);
+      uint4 *row = (uint4 *)(sA + sa * a_bytes + r * 128);
+      if (!(skip & 16)) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int kk = (k + sw) & 7;                // rotated order: conflict-free banks
+          float4 v = *(const float4 *)&row[kk];
+          if (g.A.act == 1) { v.x = siluf_(v.x); v.y = siluf_(v.y); v.z = siluf_(v.z); v.w = siluf_(v.w); }
+          row[kk] = make_uint4(to_tf32(v.x), to_tf32(v.y), to_tf32(v.z), to_tf32(v.w));
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&fullA[sa]);        // one arrival per converter warp
+    }
+  } else if (warp == 8) {
+    // ---------------- B producer ----------------
+    if (lane == 0) {
+      for (int gi = 0; gi < total; ++gi) {
+        const int kc = gi % nkc, sb = gi % NSB, ub = gi / NSB;
+        if (ub > 0) mbar_wait(&emptyB[sb], (ub - 1) & 1);
+        if (skip & 4) {                                 // debug: no weight traffic
+          mbar_arrive(&fullB[sb]);
+        } else {
+          mbar_expect_tx(&fullB[sb], b_bytes);
+          bulk_g2s(sB + sb * b_bytes, bimg + (size_t)kc * NT * KC, b_bytes, &fullB[sb]);
         }
       }
     }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
+  } else if (warp == 9) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      int gi = 0;
+      for (int tl = 0; tl < my_tiles; ++tl) {
+        const int a = tl & 1, ua2 = tl >> 1;
+        if (ua2 > 0) mbar_wait(&tempty[a], (ua2 - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        bool started[4] = {false, false, false, false};
+        for (int kc = 0; kc < nkc; ++kc, ++gi) {
+          const int sa = gi % NSA, ua = gi / NSA, sb = gi % NSB, ub = gi / NSB;
+          mbar_wait(&fullA[sa], ua & 1);
+          mbar_wait(&fullB[sb], ub & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a_base = smem_u32(sA + sa * a_bytes), b_base = smem_u32(sB + sb * b_bytes);
+          const int col0 = P.lo + kc * KC;
+          for (int c = 0; c < g.nchunk; ++c) {
+            const int kk = col0 - g.ch[c].a_k0;
+            if (kk < 0 || kk >= g.K) continue;
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(P.cpad[c] >> 3) << 17) |
+                                   ((uint32_t)(TCM >> 4) << 24);
+#pragma unroll
+            for (int j = 0; j < KC / 8; ++j) {
+              uint64_t ad = make_desc(a_base + j * 32, 16, 1024) | ((uint64_t)2 << 61);   // SWIZZLE_128B
+              uint64_t bd = make_desc(b_base + j * 2 * (NT * 16) + P.coff[c] * 16, NT * 16, 128);
+              if (!(skip & 8))                            // debug: no tensor-core work
+                mma_tf32(tmem + a * tcols + P.coff[c], ad, bd, idesc, (started[c] || j > 0) ? 1u : 0u);
+            }
+            started[c] = true;
+          }
+          mma_commit(&emptyA[sa]);
+          mma_commit(&emptyB[sb]);
+          if ((skip & 32) && gi < 30) {                // debug trace: MMA-side cadence
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            trace_ts[gi + 1] = t;
+          }
+        }
+        mma_commit(&tfull[a]);
+      }
+      if (skip & 32) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        trace_ts[31] = t;
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 10-13) ----------------
+    const int lq = warp & 3;
+    const uint32_t lane_base = (uint32_t)(lq * 32) << 16;
+    for (int tl = 0; tl < my_tiles; ++tl) {
+      const int a = tl & 1;
+      const int tile = blockIdx.x + tl * gridDim.x;
+      mbar_wait(&tfull[a], (tl >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t a_base = smem_u32(sA[s]), b_base = smem_u32(sB[s]);
+      // 32x32 blocks go TMEM -> registers (lane = row) -> smem -> registers
+      // (lane = column) so that every global access is a coalesced 128-B row run
+      float *stile = epi + (warp - 10) * (32 * 33);
+      const int half = (warp - 10) >> 2;              // two warps per TMEM lane quarter split the blocks
+      int blk = 0;
+      const int row0 = tile * TCM + lq * 32;
+      const int nrows = min(32, g.M - row0);
       for (int c = 0; c < g.nchunk; ++c) {
         const Chunk &C = g.ch[c];
-        int kk = col0 - C.a_k0;
-        if (kk < 0 || kk >= g.K) continue;
+        for (int j0 = 0; j0 < P.cpad[c]; j0 += 32, ++blk) {
+          if ((blk & 1) != half) continue;
+          uint32_t r[32];
+          tmem_ld32(tmem + lane_base + a * tcols + P.coff[c] + j0, r);
+          if (skip & 1) continue;                         // debug: no epilogue stores
 #pragma unroll
-        for (int j = 0; j < KC / 8; ++j) {
-          // K step of 8 tf32 = 2 core-matrix columns of 16 B
-          uint64_t ad = make_desc(a_base + j * 2 * (TCM * 16), TCM * 16, 128);
-          uint64_t bd = make_desc(b_base + j * 2 * (NT * 16) + P.coff[c] * 16, NT * 16, 128);
-          mma_tf32(tmem + P.coff[c], ad, bd, idesc_for(P.cpad[c]), (started[c] || j > 0) ? 1u : 0u);
+          for (int qq = 0; qq < 32; ++qq) stile[lane * 33 + qq] = __uint_as_float(r[qq]);
+          __syncwarp();
+          const int n = j0 + lane;
+          const bool col_ok = n < C.ncols;
+          const float bn = (C.bias && col_ok) ? __ldg(C.bias + n) : 0.f;
+          if (col_ok) {
+            // 16 rows at a time: issue every dependent load first (out may alias resid)
+#pragma unroll
+            for (int h = 0; h < 32; h += 16) {
+              float mv[16], rv[16];
+#pragma unroll
+              for (int rr = 0; rr < 16; ++rr) {
+                const size_t mr = (size_t)(row0 + h + rr);
+                const bool ok = h + rr < nrows;
+                mv[rr] = (C.mul && ok) ? C.mul[mr * C.ldm + n] : 0.f;
+                rv[rr] = (C.resid && ok) ? C.resid[mr * C.ldr + n] : 0.f;
+              }
+#pragma unroll
+              for (int rr = 0; rr < 16; ++rr) {
+                if (h + rr >= nrows) break;
+                const size_t mr = (size_t)(row0 + h + rr);
+                float v = stile[(h + rr) * 33 + lane] + bn;
+                if (C.pre) C.pre[mr * C.ldp + n] = v;
+                if (g.act == 1) v = siluf_(v);
+                if (C.mul) v *= dsiluf_(mv[rr]);
+                v += rv[rr];
+                C.out[mr * C.ldo + n] = v;
+              }
+            }
+          }
+          __syncwarp();
         }
-        started[c] = true;
       }
-      mma_commit(&bar[s]);
-    }
-  }
-  // wait for the last commit (covers every MMA issued before it)
-  {
-    int last = nkc - 1;
-    mbar_wait(&bar[last & 1], (last >> 1) & 1);
-  }
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-
-  // --- epilogue: warp w reads TMEM lanes 32w..32w+31; thread = row
-  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-  for (int c = 0; c < g.nchunk; ++c) {
-    const Chunk &C = g.ch[c];
-    for (int j0 = 0; j0 < P.cpad[c]; j0 += 32) {
-      uint32_t r[32];
-      if (j0 + 32 <= P.cpad[c]) {
-        tmem_ld32(tmem + lane_base + P.coff[c] + j0, r);
-      } else {
-        // 16-column tail: load 32 (the allocation is wide enough), use 16
-        tmem_ld32(tmem + lane_base + P.coff[c] + j0, r);
-      }
-      if (!row_ok) continue;
-#pragma unroll
-      for (int q = 0; q < 32; ++q) {
-        int n = j0 + q;
-        if (n >= C.ncols) continue;
-        float v = __uint_as_float(r[q]);
-        if (C.bias) v += __ldg(C.bias + n);
-        if (C.pre) C.pre[(size_t)m * C.ldp + n] = v;
-        if (g.act == 1) v = siluf_(v);
-        if (C.mul) v *= dsiluf_(C.mul[(size_t)m * C.ldm + n]);
-        if (C.resid) v += C.resid[(size_t)m * C.ldr + n];
-        C.out[(size_t)m * C.ldo + n] = v;
-      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[a]);        // one arrival per epilogue warp
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if ((skip & 32) && blockIdx.x == 0 && tid == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    printf("TRACE tiles %d nkc %d grid %d | start->chunk ends (us):", my_tiles, nkc, (int)gridDim.x);
+    for (int i = 1; i <= min(30, total); ++i) printf(" %.2f", (trace_ts[i] - trace_ts[0]) * 1e-3);
+    printf(" | loader issued:");
+    for (int i = 0; i < min(30, total); ++i) printf(" %.2f", (trace_ld[i] - trace_ts[0]) * 1e-3);
+    printf(" | converted:");
+    for (int i = 0; i < min(30, total); ++i) printf(" %.2f", (trace_cv[i] - trace_ts[0]) * 1e-3);
+    printf(" | mma_done %.2f end %.2f\n", (trace_ts[31] - trace_ts[0]) * 1e-3, (t - trace_ts[0]) * 1e-3);
+  }
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * tcols) : "memory");
 }
 
 }  // namespace
@@ -262,12 +445,12 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
     const Chunk &C = g.ch[c];
     if (C.a_k0 % KC) return false;
     for (int b = 0; b < C.nwb; ++b)
-      if (!C.Wk[b] || (C.wk0[b] % 4)) return false;
+      if (!C.Wk[b]) return false;
     lo = std::min(lo, C.a_k0);
     hi = std::max(hi, C.a_k0 + g.K);
     P.cpad[c] = std::max(16, (C.ncols + 15) / 16 * 16);
     P.coff[c] = off;
-    off += (C.ncols + 31) / 32 * 32;   // keep 32-column TMEM alignment per chunk
+    off += (C.ncols + 31) / 32 * 32;
   }
   int tot = 0;
   for (int s = 0; s < g.A.nseg; ++s) {
@@ -281,17 +464,39 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   P.ntot = off;
   if (P.ntot > 256) return false;
   P.tmem_cols = P.ntot <= 32 ? 32 : P.ntot <= 64 ? 64 : P.ntot <= 128 ? 128 : 256;
-  size_t smem = 2 * (size_t)(KC * TCM * 4 + KC * P.ntot * 4) + 64;
+  const int nkc = P.width / KC;
+  size_t smem = 1024 + (size_t)NSA * KC * TCM * 4 + (size_t)NSB * KC * P.ntot * 4 + 8 * (3 * NSA + 2 * NSB + 4) + 16 +
+                NEPI * 32 * 33 * 4;
   static bool attr = false;
   if (!attr) {
-    CUDA_OK(cudaFuncSetAttribute(k_rowgemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CUDA_OK(cudaFuncSetAttribute(k_rowgemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
     attr = true;
   }
   double cols = 0;
   for (int c = 0; c < g.nchunk; ++c) cols += g.ch[c].ncols;
+  uint32_t *img = (uint32_t *)ctx->get("tc_bimg", (size_t)nkc * P.ntot * KC * 4);
+  {
+    ProfScope ps(ctx, "tc_pack", 0.0, (double)nkc * P.ntot * KC * 8.0);
+    dim3 grid(ceil_div((int64_t)P.ntot * KC, 256), nkc);
+    k_pack_b<<<grid, 256, 0, ctx->stream>>>(g, P, img);
+    check_launch(ctx);
+  }
+  const int ntiles = ceil_div(g.M, TCM);
+  int sms = 148;
+  {
+    static int cached = 0;
+    if (!cached) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+    }
+    sms = cached;
+  }
+  const int grid = std::min(ntiles, sms);
   ProfScope ps(ctx, "rowgemm_tc", 2.0 * g.M * (double)g.K * cols,
                (double)g.M * (4.0 * P.width + 4.0 * cols * 2) + 4.0 * g.K * cols);
-  k_rowgemm_tc<<<ceil_div(g.M, TCM), 128, smem, ctx->stream>>>(g, P);
+  static int skip = getenv("CHG_TC_SKIP") ? atoi(getenv("CHG_TC_SKIP")) : 0;   // debug knob (timing studies)
+  k_rowgemm_tc<<<grid, WS_THREADS, smem, ctx->stream>>>(g, P, img, ntiles, skip);
   check_launch(ctx);
   return true;
 }
