@@ -198,6 +198,16 @@ chg_status chg_profile(chg_ctx *ctx, int mode);
 chg_status chg_profile_query(chg_ctx *ctx, int idx, char *tag, double *ms, int64_t *launches, double *flops,
                              double *bytes);
 
+/* ---- kernel unit tests ---------------------------------------------------------
+ * chg_debug_gemm runs one GEMM engine on dense host matrices (row-major fp32):
+ *   kind 0: out[M,N] = A[M,K] · W[K,N]          (row GEMM; W is also given K-major
+ *           internally for the tensor-core path)
+ *   kind 1: out[K,N] = A[M,K]ᵀ · D[M,N]         (weight-gradient GEMM; `W` = D)
+ * engine 0 = fp32 CUDA cores, 2 = tcgen05 TF32.  Returns CHG_ERR_ARG if the
+ * engine cannot run the shape.  Synchronises. */
+chg_status chg_debug_gemm(chg_ctx *ctx, int kind, int engine, int M, int K, int N, const float *A,
+                          const float *W, float *out);
+
 /* ---- debugging / parity ---------------------------------------------------
  * Copies a named intermediate of the last forward/backward to host memory:
  * names "ea_t","eb_t","a_t" (bases, [rows,32] zero-padded), "v0".."v4",

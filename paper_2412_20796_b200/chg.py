@@ -63,7 +63,7 @@ SYMBOLS = ["chg_ctx_create", "chg_ctx_destroy", "chg_last_error", "chg_sync", "c
            "chg_nccl_unique_id", "chg_ctx_set_nccl", "chg_build_graph", "chg_graph_counts", "chg_graph_export",
            "chg_graph_destroy", "chg_model_create", "chg_model_destroy", "chg_model_layout",
            "chg_model_num_params", "chg_model_set", "chg_model_get", "chg_model_device_ptr", "chg_forward",
-           "chg_backward", "chg_step", "chg_balance", "chg_profile", "chg_profile_query", "chg_debug_get"]
+           "chg_backward", "chg_step", "chg_balance", "chg_profile", "chg_profile_query", "chg_debug_gemm", "chg_debug_get"]
 
 _lib = None
 
@@ -103,6 +103,7 @@ def load(path: str = LIB_PATH):
         "chg_balance": (C.c_int, [vp, i32, i32, vp]),
         "chg_debug_get": (C.c_int, [vp, C.c_char_p, vp, i64, C.POINTER(i64), C.POINTER(i64)]),
         "chg_profile": (C.c_int, [vp, C.c_int]),
+        "chg_debug_gemm": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp]),
         "chg_profile_query": (C.c_int, [vp, C.c_int, C.c_char_p, dp, C.POINTER(i64), dp, dp]),
     }
     for name, (res, args) in sig.items():
@@ -251,6 +252,17 @@ class Context:
                 break
             out[tag.value.decode()] = {"ms": ms.value, "launches": n.value, "flops": fl.value, "bytes": by.value}
             i += 1
+        return out
+
+    def debug_gemm(self, kind: int, engine: int, A: np.ndarray, W: np.ndarray) -> np.ndarray:
+        """Kernel unit test: kind 0 -> A @ W, kind 1 -> A.T @ W (W = D), on the
+        fp32 CUDA-core engine (0) or the tcgen05 TF32 engine (2)."""
+        A = np.ascontiguousarray(A, np.float32)
+        W = np.ascontiguousarray(W, np.float32)
+        M, K = A.shape
+        N = W.shape[1]
+        out = np.zeros((M, N) if kind == 0 else (K, N), np.float32)
+        self._check(self.lib.chg_debug_gemm(self.h, kind, engine, M, K, N, _ptr(A), _ptr(W), _ptr(out)))
         return out
 
     def debug(self, name: str) -> np.ndarray:

@@ -3,7 +3,7 @@
 
 namespace {
 
-constexpr int TM = 128, TN = 64, TK = 32;
+constexpr int TM = 128, TN = 64, TK = 32;   // default rows per CTA, columns per chunk, K step
 
 // A(m, col) for 4 consecutive columns (segment widths are multiples of 4)
 __device__ __forceinline__ float4 loadA4(const AOp &A, int m, int col) {
@@ -51,23 +51,26 @@ __device__ __forceinline__ float loadW(const Chunk &c, int k, int n) {
   return 0.f;
 }
 
-template <bool VEC>
+// TM rows per CTA (128 for large M; 32 when few CTAs would be launched),
+// 256 threads = 16 (x 4 columns) x 16 (x TM/16 rows)
+template <bool VEC, int TM>
 __global__ void __launch_bounds__(256) k_rowgemm(const RowGemm g) {
+  constexpr int RPT = TM / 16;
   __shared__ __align__(16) float As[TK][TM + 4];
   __shared__ __align__(16) float Ws[TK][TN];
   const Chunk &c = g.ch[blockIdx.y];
   const int m0 = blockIdx.x * TM;
   const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
-  float acc[8][4];
+  float acc[RPT][4];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < RPT; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
 
   for (int k0 = 0; k0 < g.K; k0 += TK) {
     if (VEC) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < TM / 32; ++i) {
         int r = (t >> 3) + 32 * i, c4 = t & 7;
         int m = m0 + r, kk = k0 + 4 * c4;
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -91,13 +94,20 @@ __global__ void __launch_bounds__(256) k_rowgemm(const RowGemm g) {
     __syncthreads();
 #pragma unroll 8
     for (int kk = 0; kk < TK; ++kk) {
-      float4 a0 = *(const float4 *)&As[kk][ty * 8];
-      float4 a1 = *(const float4 *)&As[kk][ty * 8 + 4];
+      float a[RPT];
+      if (RPT == 8) {
+        float4 a0 = *(const float4 *)&As[kk][ty * 8];
+        float4 a1 = *(const float4 *)&As[kk][ty * 8 + 4];
+        a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
+        a[RPT > 4 ? 4 : 0] = a1.x; a[RPT > 5 ? 5 : 0] = a1.y; a[RPT > 6 ? 6 : 0] = a1.z; a[RPT > 7 ? 7 : 0] = a1.w;
+      } else {
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) a[i] = As[kk][ty * RPT + i];
+      }
       float4 b = *(const float4 *)&Ws[kk][tx * 4];
-      float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
       float bb[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < RPT; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], bb[j], acc[i][j]);
     }
@@ -105,8 +115,8 @@ __global__ void __launch_bounds__(256) k_rowgemm(const RowGemm g) {
   }
   // epilogue
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    int m = m0 + ty * 8 + i;
+  for (int i = 0; i < RPT; ++i) {
+    int m = m0 + ty * RPT + i;
     if (m >= g.M) continue;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -222,18 +232,31 @@ __global__ void __launch_bounds__(256) k_wgrad(const WGrad g, float *__restrict_
   }
 }
 
-__global__ void k_wgrad_reduce(const WGrad g, const float *__restrict__ partial, int Kp, int splits) {
-  int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= Kp * g.N) return;
-  int k = idx / g.N, n = idx % g.N;
+// Fixed-order reduction of the split-M partials: a block owns 32 consecutive
+// outputs; its 8 warps sum disjoint, interleaved split subsets (warp w: splits
+// w, w+8, ...), then warp 0 adds the 8 subtotals in order (deterministic).
+__global__ void __launch_bounds__(256) k_wgrad_reduce(const WGrad g, const float *__restrict__ partial, int Kp,
+                                                      int splits) {
+  __shared__ float sh[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int idx = blockIdx.x * 32 + lane;
+  const size_t total = (size_t)Kp * g.N;
   float s = 0.f;
-  for (int sp = 0; sp < splits; ++sp) s += partial[(size_t)sp * Kp * g.N + idx];
+  if (idx < total)
+    for (int sp = w; sp < splits; sp += 8) s += partial[(size_t)sp * total + idx];
+  sh[w][lane] = s;
+  __syncthreads();
+  if (w != 0 || idx >= total) return;
+  float t = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) t += sh[k][lane];
+  const int k = idx / g.N, n = idx % g.N;
   const WGradDst &d = g.dst[n / 64];
-  int nn = n % 64;
+  const int nn = n % 64;
   if (k < g.K) {
-    if (d.W) d.W[(size_t)k * d.ldw + nn] += s;
+    if (d.W) d.W[(size_t)k * d.ldw + nn] += t;
   } else if (d.b) {
-    d.b[nn] += s;
+    d.b[nn] += t;
   }
 }
 
@@ -302,19 +325,41 @@ void rowgemm(chg_ctx *ctx, const RowGemm &g) {
   }
   double idxb = 0;
   for (int s = 0; s < g.A.nseg; ++s) idxb += g.A.seg[s].idx ? 4.0 : 0.0;
-  ProfScope ps(ctx, "rowgemm", 2.0 * g.M * (double)g.K * cols,
+  ProfScope ps(ctx, g.tag ? g.tag : "rowgemm", 2.0 * g.M * (double)g.K * cols,
                (double)g.M * (4.0 * std::min(hi - lo, tot) + idxb + 4.0 * outb) + 4.0 * wb);
-  dim3 grid(ceil_div(g.M, TM), g.nchunk);
-  if (vec)
-    k_rowgemm<true><<<grid, 256, 0, ctx->stream>>>(g);
-  else
-    k_rowgemm<false><<<grid, 256, 0, ctx->stream>>>(g);
+  const bool small = (int64_t)ceil_div(g.M, TM) * g.nchunk < 2 * 148;
+  if (small) {
+    dim3 grid(ceil_div(g.M, 32), g.nchunk);
+    if (vec) k_rowgemm<true, 32><<<grid, 256, 0, ctx->stream>>>(g);
+    else k_rowgemm<false, 32><<<grid, 256, 0, ctx->stream>>>(g);
+  } else {
+    dim3 grid(ceil_div(g.M, TM), g.nchunk);
+    if (vec) k_rowgemm<true, TM><<<grid, 256, 0, ctx->stream>>>(g);
+    else k_rowgemm<false, TM><<<grid, 256, 0, ctx->stream>>>(g);
+  }
   check_launch(ctx);
 }
 
 void wgrad(chg_ctx *ctx, const WGrad &g) {
   int Kp = g.K + (g.bias ? 1 : 0);
   if (Kp <= 0 || g.N <= 0) return;
+  if (g.tc && ctx->use_tc && g.M > 0) {
+    float *partial = nullptr;
+    int kp = 0, splits = 0;
+    bool bias_done = false;
+    if (wgrad_tc(ctx, g, &partial, &kp, &splits, &bias_done)) {
+      k_wgrad_reduce<<<ceil_div(kp * g.N, 32), 256, 0, ctx->stream>>>(g, partial, kp, splits);
+      check_launch(ctx);
+      if (!bias_done) {            // K is a multiple of 128: column sums of D on the CUDA cores
+        WGrad b = g;
+        b.A.nseg = 0;
+        b.K = 0;
+        b.tc = 0;
+        wgrad(ctx, b);
+      }
+      return;
+    }
+  }
   int ktiles = ceil_div(Kp, WK), ntiles = ceil_div(g.N, WN);
   int splits = 1;
   if (g.M > 0) {
@@ -325,7 +370,7 @@ void wgrad(chg_ctx *ctx, const WGrad &g) {
   float *partial = ctx->getf("wgrad_partial", (size_t)splits * Kp * g.N);
   double idxb = 0;
   for (int s = 0; s < g.A.nseg; ++s) idxb += g.A.seg[s].idx ? 4.0 : 0.0;
-  ProfScope ps(ctx, "wgrad", 2.0 * g.M * (double)Kp * g.N,
+  ProfScope ps(ctx, g.tag ? g.tag : "wgrad", 2.0 * g.M * (double)Kp * g.N,
                (double)g.M * (4.0 * g.K + idxb + 4.0 * g.N + (g.didx ? 4.0 : 0.0)) + 4.0 * Kp * g.N);
   bool vec = aop_vec(g.A);
   dim3 grid(ktiles, ntiles, splits);
@@ -334,6 +379,63 @@ void wgrad(chg_ctx *ctx, const WGrad &g) {
   else
     k_wgrad<false><<<grid, 256, 0, ctx->stream>>>(g, partial, Kp, rps);
   check_launch(ctx);
-  k_wgrad_reduce<<<ceil_div(Kp * g.N, 256), 256, 0, ctx->stream>>>(g, partial, Kp, splits);
+  k_wgrad_reduce<<<ceil_div(Kp * g.N, 32), 256, 0, ctx->stream>>>(g, partial, Kp, splits);
   check_launch(ctx);
+}
+
+// ---------------------------------------------------------------------------
+// kernel unit-test hook (chg_debug_gemm, include/chg.h)
+// ---------------------------------------------------------------------------
+extern "C" chg_status chg_debug_gemm(chg_ctx *ctx, int kind, int engine, int M, int K, int N, const float *A,
+                                     const float *W, float *out) {
+  if (!ctx || !A || !W || !out || M <= 0 || K <= 0 || N <= 0 || (kind != 0 && kind != 1)) return CHG_ERR_ARG;
+  try {
+    cudaStream_t st = ctx->stream;
+    const size_t na = (size_t)M * K, nw = kind == 0 ? (size_t)K * N : (size_t)M * N;
+    const size_t no = kind == 0 ? (size_t)M * N : (size_t)K * N;
+    float *dA = ctx->getf("dbg_gemm_A", na), *dW = ctx->getf("dbg_gemm_W", nw), *dO = ctx->getf("dbg_gemm_O", no);
+    float *dWk = ctx->getf("dbg_gemm_Wk", kind == 0 ? nw : 1);
+    CUDA_OK(cudaMemcpyAsync(dA, A, 4 * na, cudaMemcpyHostToDevice, st));
+    CUDA_OK(cudaMemcpyAsync(dW, W, 4 * nw, cudaMemcpyHostToDevice, st));
+    CUDA_OK(cudaMemsetAsync(dO, 0, 4 * no, st));
+    const bool old = ctx->use_tc;
+    ctx->use_tc = engine == 2;
+    if (kind == 0) {
+      std::vector<float> wk((size_t)K * N);
+      for (int k = 0; k < K; ++k)
+        for (int n = 0; n < N; ++n) wk[(size_t)n * K + k] = W[(size_t)k * N + n];
+      CUDA_OK(cudaMemcpyAsync(dWk, wk.data(), 4 * nw, cudaMemcpyHostToDevice, st));
+      RowGemm G;
+      G.A.seg[0] = aseg(dA, K, K);
+      G.A.nseg = 1;
+      G.M = M; G.K = K;
+      G.nchunk = (N + 63) / 64;
+      G.tc = 1;
+      if (G.nchunk > 4) CHG_THROW(CHG_ERR_ARG, "N > 256");
+      for (int c = 0; c < G.nchunk; ++c) {
+        G.ch[c] = chunk1(dW + 64 * c, N, K, nullptr, dO + 64 * c, N, std::min(64, N - 64 * c));
+        G.ch[c].Wk[0] = dWk + (size_t)64 * c * K;
+        G.ch[c].ldwk[0] = K;
+      }
+      bool done = engine == 2 ? rowgemm_tc(ctx, G) : false;
+      if (engine == 2 && !done) CHG_THROW(CHG_ERR_ARG, "shape not supported by the tensor-core engine");
+      if (!done) { G.tc = 0; rowgemm(ctx, G); }
+    } else {
+      WGrad g;
+      g.A.seg[0] = aseg(dA, K, K);
+      g.A.nseg = 1;
+      g.M = M; g.K = K;
+      g.D = dW; g.ldd = N; g.N = N; g.bias = 0; g.tc = engine == 2;
+      if (N > 256) CHG_THROW(CHG_ERR_ARG, "N > 256");
+      for (int c = 0; c * 64 < N; ++c) { g.dst[c].W = dO + 64 * c; g.dst[c].ldw = N; }
+      wgrad(ctx, g);
+    }
+    ctx->use_tc = old;
+    CUDA_OK(cudaMemcpyAsync(out, dO, 4 * no, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+  } catch (const ChgError &e) {
+    ctx->err = e.msg;
+    return e.code;
+  }
+  return CHG_OK;
 }

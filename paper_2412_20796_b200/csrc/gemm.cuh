@@ -51,6 +51,7 @@ struct RowGemm {
   int act = 0;                   // 0 none, 1 silu
   int nchunk = 1;
   int tc = 0;                    // 1: a GatedMLP contraction -> tensor cores in TF32 mode (NS)
+  const char *tag = nullptr;     // profiling label (chg_profile)
   Chunk ch[4];
 };
 
@@ -67,12 +68,15 @@ struct WGrad {
   int ldd = 0;
   int N = 0;                     // columns of D (<= 256)
   int bias = 0;                  // 1: also column sums of D -> dst.b
+  int tc = 0;                    // 1: a GatedMLP weight gradient -> tensor cores in TF32 mode
+  const char *tag = nullptr;     // profiling label (chg_profile)
   WGradDst dst[4];               // per 64-column chunk of N
 };
 
 void rowgemm(chg_ctx *ctx, const RowGemm &g);      // tcgen05 when ctx->use_tc and eligible, else SIMT
 bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g);   // false if the shape does not fit the tensor-core path
 void wgrad(chg_ctx *ctx, const WGrad &g);
+bool wgrad_tc(chg_ctx *ctx, const WGrad &g, float **partial, int *Kp, int *splits, bool *bias_done);
 
 // helpers to fill descriptors
 inline ASeg aseg(const float *base, int ld, int width, const int32_t *idx = nullptr) {

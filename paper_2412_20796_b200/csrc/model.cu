@@ -53,6 +53,7 @@ void atom_conv_fwd(Fwd &F, int t, const float *v, const float *e, const float *e
     G.M = (int)E; G.K = 192; G.nchunk = 2; G.tc = 1;
     G.ch[0] = chunk1(m->p(pre + ".core.W1"), 64, 192, m->p(pre + ".core.b1"), z1, 128);
     G.ch[1] = chunk1(m->p(pre + ".gate.W1"), 64, 192, m->p(pre + ".gate.b1"), z1 + 64, 128);
+    G.tag = "ac_f1";
     rowgemm(ctx, G);
   }
   {  // SiLU(z1) · blockdiag(W2_core, W2_gate) + b2
@@ -63,6 +64,7 @@ void atom_conv_fwd(Fwd &F, int t, const float *v, const float *e, const float *e
     G.ch[0] = chunk1(m->p(pre + ".core.W2"), 64, 64, m->p(pre + ".core.b2"), y, 128);
     G.ch[1] = chunk1(m->p(pre + ".gate.W2"), 64, 64, m->p(pre + ".gate.b2"), y + 64, 128);
     G.ch[1].a_k0 = 64;
+    G.tag = "ac_f2";
     rowgemm(ctx, G);
   }
   // m_e = eᵃ_e ⊙ σ(LN_g(y_g)) ⊙ SiLU(LN_c(y_c))
@@ -77,6 +79,7 @@ void atom_conv_fwd(Fwd &F, int t, const float *v, const float *e, const float *e
     G.M = (int)N; G.K = 64; G.nchunk = 1;
     G.ch[0] = chunk1(m->p(pre + ".out.W"), 64, 64, m->p(pre + ".out.b"), v_out, 64);
     G.ch[0].resid = v; G.ch[0].ldr = 64;
+    G.tag = "ac_fout";
     rowgemm(ctx, G);
   }
 }
@@ -110,6 +113,7 @@ void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float
       G.ch[2] = chunk1(m->p(ap + ".core.W"), 64, 256, m->p(ap + ".core.b"), ya, 128);
       G.ch[3] = chunk1(m->p(ap + ".gate.W"), 64, 256, m->p(ap + ".gate.b"), ya + 64, 128);
     }
+    G.tag = "bc_f1";
     rowgemm(ctx, G);
     RowGemm H;
     H.A.seg[0] = aseg(z1, 128, 128);
@@ -118,6 +122,7 @@ void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float
     H.ch[0] = chunk1(m->p(bp + ".core.W2"), 64, 64, m->p(bp + ".core.b2"), yb, 128);
     H.ch[1] = chunk1(m->p(bp + ".gate.W2"), 64, 64, m->p(bp + ".gate.b2"), yb + 64, 128);
     H.ch[1].a_k0 = 64;
+    H.tag = "bc_f2";
     rowgemm(ctx, H);
     // q = eᵇ_ij ⊙ eᵇ_ik ⊙ φ_e
     gate_fwd(ctx, A, yb, 128, F.ln(bp), GATE_MUL_W1W2, eb, g->angle_b1, g->angle_b2, nullptr, q);
@@ -132,6 +137,7 @@ void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float
     G.M = (int)E; G.K = 64; G.nchunk = 1;
     G.ch[0] = chunk1(m->p(bp + ".out.W"), 64, 64, m->p(bp + ".out.b"), e_out, 64);
     G.ch[0].resid = e; G.ch[0].ldr = 64;
+    G.tag = "bc_fout";
     rowgemm(ctx, G);
   }
   if (angle_branch && A > 0)   // a' = a + φ_a
@@ -154,10 +160,12 @@ void mlp_fwd(Fwd &F, const std::string &pre, int nl, const float *x, int64_t row
       G.act = 1;
       G.ch[0] = chunk1(m->p(W), 64, 64, m->p(b), hn, 64);
       G.ch[0].pre = z; G.ch[0].ldp = 64;
+      G.tag = "head_f";
       rowgemm(F.ctx, G);
       h = hn;
     } else {
       G.ch[0] = chunk1(m->p(W), nout, 64, m->p(b), out, ldo, nout);
+      G.tag = "head_f";
       rowgemm(F.ctx, G);
     }
   }
@@ -205,14 +213,17 @@ void forward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, int train, chg_pred 
     G.M = (int)E; G.K = CHG_K; G.nchunk = 2;
     G.ch[0] = chunk1(m->p("proj.W0"), 64, CHG_K, nullptr, e[0], 64);
     G.ch[1] = chunk1(m->p("proj.Wa"), 64, CHG_K, nullptr, ea, 64);
+    G.tag = "proj_f";
     rowgemm(ctx, G);
     G.A.seg[0] = aseg(eb_t, 32, 32);
     G.M = (int)B; G.nchunk = 1;
     G.ch[0] = chunk1(m->p("proj.Wb"), 64, CHG_K, nullptr, eb, 64);
+    G.tag = "proj_f";
     rowgemm(ctx, G);
     G.A.seg[0] = aseg(a_t, 32, 32);
     G.M = (int)A;
     G.ch[0] = chunk1(m->p("proj.Wtheta"), 64, CHG_K, nullptr, a[0], 64);
+    G.tag = "proj_f";
     rowgemm(ctx, G);
   }
   // A4/A5 interaction blocks
@@ -237,6 +248,7 @@ void forward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, int train, chg_pred 
     G.A.nseg = 1;
     G.M = (int)N; G.K = 64;
     G.ch[0] = chunk1(m->p("head_M.W"), 1, 64, m->p("head_M.b"), mag, 1, 1);
+    G.tag = "headM_f";
     rowgemm(ctx, G);
   }
   mlp_fwd(F, "head_F", 3, ef, E, 1, n_e, 1);
@@ -303,6 +315,7 @@ void mlp_bwd(Bwd &Bw, const std::string &pre, int nl, const float *x, int64_t ro
     wg.M = (int)rows; wg.K = 64;
     wg.D = dz; wg.ldd = ncol; wg.N = ncol; wg.bias = 1;
     wg.dst[0].W = Bw.G(W); wg.dst[0].ldw = ncol; wg.dst[0].b = Bw.G(b);
+    wg.tag = "head_wg";
     wgrad(ctx, wg);
     RowGemm G;
     G.A.seg[0] = aseg(dz, ncol, ncol);
@@ -312,12 +325,14 @@ void mlp_bwd(Bwd &Bw, const std::string &pre, int nl, const float *x, int64_t ro
       float *dzn = ctx->getf(pre + "_dz" + std::to_string(k - 1), (size_t)std::max<int64_t>(rows, 1) * 64);
       G.ch[0] = chunk1(Bw.WT(W), 64, ncol, nullptr, dzn, 64);
       G.ch[0].mul = Bw.act(pre + "_z" + std::to_string(k - 1)); G.ch[0].ldm = 64;
+      G.tag = "head_b";
       rowgemm(ctx, G);
       dz = dzn;
       ncol = 64;
     } else {
       G.ch[0] = chunk1(Bw.WT(W), 64, ncol, nullptr, dx, 64);
       G.ch[0].resid = dx; G.ch[0].ldr = 64;
+      G.tag = "head_b";
       rowgemm(ctx, G);
     }
   }
@@ -333,6 +348,7 @@ void ac_bwd_head(Bwd &Bw, int t, const float *dv, float *dagg) {
   G.A.nseg = 1;
   G.M = (int)g->N; G.K = 64;
   G.ch[0] = chunk1(Bw.WT(pre + ".out.W"), 64, 64, nullptr, dagg, 64);
+  G.tag = "ac_dagg";
   rowgemm(Bw.ctx, G);
   WGrad wg;
   wg.A.seg[0] = aseg(agg, 64, 64);
@@ -340,6 +356,7 @@ void ac_bwd_head(Bwd &Bw, int t, const float *dv, float *dagg) {
   wg.M = (int)g->N; wg.K = 64;
   wg.D = dv; wg.ldd = 64; wg.N = 64; wg.bias = 1;
   wg.dst[0].W = Bw.G(pre + ".out.W"); wg.dst[0].ldw = 64; wg.dst[0].b = Bw.G(pre + ".out.b");
+  wg.tag = "ac_out_wg";
   wgrad(Bw.ctx, wg);
 }
 
@@ -352,6 +369,7 @@ void bc_bwd_head(Bwd &Bw, int t, const float *de, float *daggb) {
   G.A.nseg = 1;
   G.M = (int)g->B; G.K = 64;
   G.ch[0] = chunk1(Bw.WT(pre + ".out.W"), 64, 64, nullptr, daggb, 64);
+  G.tag = "bc_daggb";
   rowgemm(Bw.ctx, G);
   WGrad wg;   // dW_out = aggbᵀ · de[bond_edge] (non-bond rows of agg are zero)
   wg.A.seg[0] = aseg(aggb, 64, 64);
@@ -359,12 +377,14 @@ void bc_bwd_head(Bwd &Bw, int t, const float *de, float *daggb) {
   wg.M = (int)g->B; wg.K = 64;
   wg.D = de; wg.didx = g->bond_edge; wg.ldd = 64; wg.N = 64; wg.bias = 0;
   wg.dst[0].W = Bw.G(pre + ".out.W"); wg.dst[0].ldw = 64;
+  wg.tag = "bc_out_wg";
   wgrad(Bw.ctx, wg);
   WGrad wb;   // db_out = Σ over ALL edges of de
   wb.A.nseg = 0;
   wb.M = (int)g->E; wb.K = 0;
   wb.D = de; wb.ldd = 64; wb.N = 64; wb.bias = 1;
   wb.dst[0].b = Bw.G(pre + ".out.b");
+  wb.tag = "bc_outb_wg";
   wgrad(Bw.ctx, wb);
 }
 
@@ -388,6 +408,7 @@ void ac_bwd_body(Bwd &Bw, int t, const float *v, const float *e, const float *ea
     G.ch[0].mul = z1; G.ch[0].ldm = 128;
     G.ch[1] = chunk1(Bw.WT(pre + ".gate.W2"), 64, 64, nullptr, dZ + 64, 128);
     G.ch[1].mul = z1 + 64; G.ch[1].ldm = 128; G.ch[1].a_k0 = 64;
+    G.tag = "ac_dZ";
     rowgemm(ctx, G);
   }
   for (int br = 0; br < 2; ++br) {  // dW2, db2
@@ -395,9 +416,10 @@ void ac_bwd_body(Bwd &Bw, int t, const float *v, const float *e, const float *ea
     WGrad wg;
     wg.A.seg[0] = aseg(z1 + 64 * br, 128, 64);
     wg.A.nseg = 1; wg.A.act = 1;
-    wg.M = (int)E; wg.K = 64;
+    wg.M = (int)E; wg.K = 64; wg.tc = 1;
     wg.D = dY + 64 * br; wg.ldd = 128; wg.N = 64; wg.bias = 1;
     wg.dst[0].W = Bw.G(pre + b + ".W2"); wg.dst[0].ldw = 64; wg.dst[0].b = Bw.G(pre + b + ".b2");
+    wg.tag = "ac_W2_wg";
     wgrad(ctx, wg);
   }
   {  // dX = dZ1 · [W1_coreᵀ ; W1_gateᵀ] -> (v_i part, v_j part, e part)
@@ -414,6 +436,7 @@ void ac_bwd_body(Bwd &Bw, int t, const float *v, const float *e, const float *ea
       C.out = outs[c]; C.ldo = 64;
       if (c == 2) { C.resid = de; C.ldr = 64; }
     }
+    G.tag = "ac_dX";
     rowgemm(ctx, G);
   }
   {  // dW1 = Xᵀ dZ1 with X = [v_i, v_j, e] gathered again
@@ -422,10 +445,11 @@ void ac_bwd_body(Bwd &Bw, int t, const float *v, const float *e, const float *ea
     wg.A.seg[1] = aseg(v, 64, 64, g->nbr);
     wg.A.seg[2] = aseg(e, 64, 64);
     wg.A.nseg = 3;
-    wg.M = (int)E; wg.K = 192;
+    wg.M = (int)E; wg.K = 192; wg.tc = 1;
     wg.D = dZ; wg.ldd = 128; wg.N = 128; wg.bias = 1;
     wg.dst[0].W = Bw.G(pre + ".core.W1"); wg.dst[0].ldw = 64; wg.dst[0].b = Bw.G(pre + ".core.b1");
     wg.dst[1].W = Bw.G(pre + ".gate.W1"); wg.dst[1].ldw = 64; wg.dst[1].b = Bw.G(pre + ".gate.b1");
+    wg.tag = "ac_W1_wg";
     wgrad(ctx, wg);
   }
   // dv_i: CSR row sum; dv_j: rows of j through the reverse-edge map (no atomics)
@@ -460,6 +484,7 @@ void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float 
     G.ch[0].mul = z1; G.ch[0].ldm = 128;
     G.ch[1] = chunk1(Bw.WT(bp + ".gate.W2"), 64, 64, nullptr, dZ + 64, 256);
     G.ch[1].mul = z1 + 64; G.ch[1].ldm = 128; G.ch[1].a_k0 = 64;
+    G.tag = "bc_dZ";
     rowgemm(ctx, G);
   }
   for (int br = 0; br < 2; ++br) {
@@ -467,9 +492,10 @@ void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float 
     WGrad wg;
     wg.A.seg[0] = aseg(z1 + 64 * br, 128, 64);
     wg.A.nseg = 1; wg.A.act = 1;
-    wg.M = (int)A; wg.K = 64;
+    wg.M = (int)A; wg.K = 64; wg.tc = 1;
     wg.D = dYb + 64 * br; wg.ldd = 128; wg.N = 64; wg.bias = 1;
     wg.dst[0].W = Bw.G(bp + b + ".W2"); wg.dst[0].ldw = 64; wg.dst[0].b = Bw.G(bp + b + ".b2");
+    wg.tag = "bc_W2_wg";
     wgrad(ctx, wg);
   }
   const int Kx = angle_branch ? 256 : 128;
@@ -492,6 +518,7 @@ void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float 
       C.out = outs[c]; C.ldo = 64;
       if (c == 3) { C.resid = da; C.ldr = 64; }
     }
+    G.tag = "bc_dX";
     rowgemm(ctx, G);
   }
   {  // dW1 (bond) and dW (angle) = Xᵀ [dZ1 | dY_a]
@@ -501,7 +528,7 @@ void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float 
     wg.A.seg[2] = aseg(e, 64, 64, g->angle_e2);
     wg.A.seg[3] = aseg(a, 64, 64);
     wg.A.nseg = 4;
-    wg.M = (int)A; wg.K = 256;
+    wg.M = (int)A; wg.K = 256; wg.tc = 1;
     wg.D = dZ; wg.ldd = 256; wg.N = Kx; wg.bias = 1;
     wg.dst[0].W = Bw.G(bp + ".core.W1"); wg.dst[0].ldw = 64; wg.dst[0].b = Bw.G(bp + ".core.b1");
     wg.dst[1].W = Bw.G(bp + ".gate.W1"); wg.dst[1].ldw = 64; wg.dst[1].b = Bw.G(bp + ".gate.b1");
@@ -509,6 +536,7 @@ void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float 
       wg.dst[2].W = Bw.G(ap + ".core.W"); wg.dst[2].ldw = 64; wg.dst[2].b = Bw.G(ap + ".core.b");
       wg.dst[3].W = Bw.G(ap + ".gate.W"); wg.dst[3].ldw = 64; wg.dst[3].b = Bw.G(ap + ".gate.b");
     }
+    wg.tag = "bc_W1_wg";
     wgrad(ctx, wg);
   }
   SegSrc s[2];
@@ -575,6 +603,7 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
     wg.M = (int)N; wg.K = 64;
     wg.D = sd.d_mag; wg.ldd = 1; wg.N = 1; wg.bias = 1;
     wg.dst[0].W = Bw.G("head_M.W"); wg.dst[0].ldw = 1; wg.dst[0].b = Bw.G("head_M.b");
+    wg.tag = "headM_wg";
     wgrad(ctx, wg);
     RowGemm G;
     G.A.seg[0] = aseg(sd.d_mag, 1, 1);
@@ -582,6 +611,7 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
     G.M = (int)N; G.K = 1;
     G.ch[0] = chunk1(Bw.WT("head_M.W"), 64, 1, nullptr, dv, 64);
     G.ch[0].resid = dv; G.ch[0].ldr = 64;
+    G.tag = "headM_b";
     rowgemm(ctx, G);
   }
   mlp_bwd(Bw, "head_S", 3, vf, N, sd.d_M9, 9, dv);
@@ -616,6 +646,7 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
     wg.M = (int)rows; wg.K = CHG_K;
     wg.D = d; wg.ldd = 64; wg.N = 64; wg.bias = 0;
     wg.dst[0].W = Bw.G(W); wg.dst[0].ldw = 64;
+    wg.tag = "proj_wg";
     wgrad(ctx, wg);
   };
   const float *ea_t = Bw.act("ea_t"), *eb_t = Bw.act("eb_t"), *a_t = Bw.act("a_t");
@@ -635,6 +666,7 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
     C.W[1] = Bw.WT("proj.Wa"); C.ldw[1] = CHG_K;
     C.wk0[0] = 0; C.wk0[1] = 64; C.wk0[2] = 128; C.nwb = 2;
     C.ncols = CHG_K; C.out = dbt; C.ldo = 32;
+    G.tag = "dbasis";
     rowgemm(ctx, G);
     basis_freq_grad(ctx, E, g->vec64, nullptr, m->p("rbf_a.freq"), g->r_atom, m->cfg.envelope_p, dbt,
                     Bw.G("rbf_a.freq"));
@@ -643,6 +675,7 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
     H.A.nseg = 1;
     H.M = (int)B; H.K = 64;
     H.ch[0] = chunk1(Bw.WT("proj.Wb"), CHG_K, 64, nullptr, dbt, 32, CHG_K);
+    H.tag = "dbasis";
     rowgemm(ctx, H);
     basis_freq_grad(ctx, B, g->vec64, g->bond_edge, m->p("rbf_b.freq"), g->r_bond, m->cfg.envelope_p, dbt,
                     Bw.G("rbf_b.freq"));

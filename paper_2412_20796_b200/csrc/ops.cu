@@ -61,13 +61,23 @@ __global__ void k_basis_freq_grad(int64_t rows, const double4 *__restrict__ vec,
   }
 }
 
-__global__ void k_reduce_cols(int nblocks, int ncols, int stride, const float *__restrict__ partial,
-                              float *__restrict__ grad) {
-  int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= ncols) return;
+// fixed-order column reduction of per-block partials (see k_wgrad_reduce)
+__global__ void __launch_bounds__(256) k_reduce_cols(int nblocks, int ncols, int stride,
+                                                     const float *__restrict__ partial, float *__restrict__ grad) {
+  __shared__ float sh[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + lane;
   float s = 0.f;
-  for (int b = 0; b < nblocks; ++b) s += partial[(size_t)b * stride + j];
-  grad[j] += s;
+  if (j < ncols)
+    for (int b = w; b < nblocks; b += 8) s += partial[(size_t)b * stride + j];
+  sh[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && j < ncols) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += sh[k][lane];
+    grad[j] += t;
+  }
 }
 
 __global__ void k_basis_angle(int64_t A, const double4 *__restrict__ vec, const int32_t *__restrict__ e1,
@@ -208,12 +218,21 @@ __global__ void __launch_bounds__(256) k_gate_bwd(int64_t rows, int64_t rpb, con
   partial[blockIdx.x * 256 + threadIdx.x] = s;
 }
 
-__global__ void k_reduce_ln(int nblocks, const float *__restrict__ partial, GateLNGrad g) {
-  int j = threadIdx.x;   // 256
+__global__ void __launch_bounds__(256) k_reduce_ln(int nblocks, const float *__restrict__ partial, GateLNGrad g) {
+  __shared__ float sh[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + lane;           // 0..255
   float s = 0.f;
-  for (int b = 0; b < nblocks; ++b) s += partial[(size_t)b * 256 + j];
-  float *dst = j < 64 ? g.gc : j < 128 ? g.bc : j < 192 ? g.gg : g.bg;
-  dst[j & 63] += s;
+  for (int b = w; b < nblocks; b += 8) s += partial[(size_t)b * 256 + j];
+  sh[w][lane] = s;
+  __syncthreads();
+  if (w == 0) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += sh[k][lane];
+    float *dst = j < 64 ? g.gc : j < 128 ? g.bc : j < 192 ? g.gg : g.bg;
+    dst[j & 63] += t;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -250,15 +269,16 @@ __global__ void k_segsum(int64_t targets, float *__restrict__ out, int ldo, int 
 // ---------------------------------------------------------------------------
 __global__ void k_heads_forces(int N, const int32_t *__restrict__ row_ptr, const float4 *__restrict__ vec,
                                const float *__restrict__ n_e, float *__restrict__ F) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (i >= N) return;
   float fx = 0.f, fy = 0.f, fz = 0.f;
-  for (int e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+  for (int e = row_ptr[i] + lane; e < row_ptr[i + 1]; e += 32) {
     float4 d = vec[e];
     float s = n_e[e] / d.w;
     fx += s * d.x; fy += s * d.y; fz += s * d.z;
   }
-  F[3 * i] = fx; F[3 * i + 1] = fy; F[3 * i + 2] = fz;
+  fx = warp_sum(fx); fy = warp_sum(fy); fz = warp_sum(fz);
+  if (lane == 0) { F[3 * i] = fx; F[3 * i + 1] = fy; F[3 * i + 2] = fz; }
 }
 
 __device__ __forceinline__ void lattice_G(const float *L, float G[9]) {
@@ -385,13 +405,13 @@ __global__ void k_seed_edge(int64_t E, const int32_t *__restrict__ center, const
 // ---------------------------------------------------------------------------
 __global__ void k_transpose(const int64_t *__restrict__ off, const int32_t *__restrict__ rc, const float *__restrict__ p,
                             float *__restrict__ wt) {
-  int t = blockIdx.x;
-  int64_t o = off[t];
-  int R = rc[2 * t], C = rc[2 * t + 1];
-  for (int idx = threadIdx.x; idx < R * C; idx += blockDim.x) {
-    int i = idx / C, j = idx % C;
-    wt[o + (int64_t)j * R + i] = p[o + idx];
-  }
+  const int t = blockIdx.y;
+  const int64_t o = off[t];
+  const int R = rc[2 * t], C = rc[2 * t + 1];
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= R * C) return;
+  const int i = idx / C, j = idx % C;
+  wt[o + (int64_t)j * R + i] = p[o + idx];
 }
 
 __global__ void k_embed(int64_t N, const int32_t *__restrict__ species, const float *__restrict__ W, float *__restrict__ v) {
@@ -449,7 +469,7 @@ void basis_freq_grad(chg_ctx *ctx, int64_t rows, const double4 *vec64, const int
   ProfScope ps(ctx, "basis_bwd", 0.0, rows * (4.0 + 32.0 + 128.0));
   k_basis_freq_grad<<<nb, 256, 0, ctx->stream>>>(rows, vec64, eor, freq, rc, p, dbasis, part);
   check_launch(ctx);
-  k_reduce_cols<<<1, 32, 0, ctx->stream>>>(nb, CHG_K, 32, part, grad);
+  k_reduce_cols<<<1, 256, 0, ctx->stream>>>(nb, CHG_K, 32, part, grad);
   check_launch(ctx);
 }
 
@@ -473,7 +493,7 @@ void gate_bwd(chg_ctx *ctx, int64_t rows, const float *y, int ldy, GateLN ln, in
   k_gate_bwd<<<nb, 256, 0, ctx->stream>>>(rows, rpb, y, ldy, ln, mode, w, i1, i2, dout, didx, dy, lddy, dw_acc, q1,
                                           q2, part);
   check_launch(ctx);
-  k_reduce_ln<<<1, 256, 0, ctx->stream>>>(nb, part, g);
+  k_reduce_ln<<<8, 256, 0, ctx->stream>>>(nb, part, g);
   check_launch(ctx);
 }
 
@@ -494,7 +514,7 @@ void segsum(chg_ctx *ctx, int64_t targets, float *out, int ldo, int accumulate, 
 void heads_forces(chg_ctx *ctx, const chg_graph *g, const float *n_e, float *forces) {
   if (g->N <= 0) return;
   ProfScope ps(ctx, "heads", 0.0, g->E * 20.0 + g->N * 12.0);
-  k_heads_forces<<<ceil_div(g->N, 128), 128, 0, ctx->stream>>>((int)g->N, g->row_ptr, g->vec, n_e, forces);
+  k_heads_forces<<<ceil_div(g->N * 32, 256), 256, 0, ctx->stream>>>((int)g->N, g->row_ptr, g->vec, n_e, forces);
   check_launch(ctx);
 }
 
@@ -539,7 +559,7 @@ void loss_and_seeds(chg_ctx *ctx, const chg_graph *g, const float *epa, const fl
 void transpose_params(chg_ctx *ctx, const chg_model *m, float *wt) {
   if (m->n2d <= 0) return;
   ProfScope ps(ctx, "transpose", 0.0, 8.0 * m->P);
-  k_transpose<<<m->n2d, 256, 0, ctx->stream>>>(m->d_toff, m->d_trc, m->params, wt);
+  k_transpose<<<dim3(64, m->n2d), 256, 0, ctx->stream>>>(m->d_toff, m->d_trc, m->params, wt);   // <= 16384 per tensor
   check_launch(ctx);
 }
 

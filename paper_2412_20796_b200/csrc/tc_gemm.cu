@@ -434,6 +434,217 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const RowGemm g, c
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * tcols) : "memory");
 }
 
+
+// ---------------------------------------------------------------------------
+// tcgen05 weight-gradient GEMM:  G[k, n] = Σ_m A(m, k) · D(m, n)
+//   UMMA view: D_mma[M = k][N = n] = Σ_{K = m} A_mma[k][m] · B_mma[n][m].  Both
+//   operands are staged K-MAJOR (MN-major tf32 operands read as zeros on this
+//   part, tools/mma_probe.cu): producer lanes own one row m each, load 4
+//   consecutive columns with one ld.global.v4 (gathered row, TF32-rounded in
+//   registers, SiLU for A when act) and scatter them as 4-byte stores into 4
+//   swizzled K-major rows (k or n) at column m — a free transpose, conflict-free.
+//   Stage = 32 rows m: A_T [Kpad rows][128 B], D_T [N rows][128 B], SWIZZLE_128B.
+//   Rows are split across persistent CTAs; each CTA accumulates its k tiles
+//   (M = 128, ≤ 2) × N in TMEM and writes one partial [Kp][N]; partials are
+//   reduced in a fixed order by k_wgrad_reduce (gemm.cu).  When K % 128 != 0 a
+//   constant ones row at k = K yields the bias gradient (column sums of D).
+//   Warps 0-7 produce, warp 8 issues MMAs, warps 0-3 run the epilogue.
+// ---------------------------------------------------------------------------
+constexpr int WG_NST = 3;
+constexpr int WG_THREADS = 9 * 32;
+
+struct WgPlan {
+  int Kpad;        // rows of A_T (multiple of 128)
+  int ktiles;      // Kpad / 128
+  int Npad;        // N
+  int Kp;          // rows written to the partial (K or K+1 with bias)
+  int ones_col;    // K if the bias ones row is used, else -1
+  int rows_per_cta;
+  uint32_t tmem_cols;
+};
+
+__device__ __forceinline__ uint32_t kmaj_swz(int r, int m) {   // byte offset of element (row r, K index m)
+  return (uint32_t)(r * 128 + ((((m >> 2) ^ (r & 7))) << 4) + (m & 3) * 4);
+}
+
+__global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const WGrad g, const WgPlan P, float *__restrict__ partial,
+                                                             int skip) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t a_bytes = P.Kpad * 128, d_bytes = P.Npad * 128;
+  const uint32_t st_bytes = a_bytes + d_bytes;
+  uint64_t *full = (uint64_t *)(smem + WG_NST * st_bytes);
+  uint64_t *empty = full + WG_NST;
+  uint64_t *done = empty + WG_NST;
+  uint32_t *tslot = (uint32_t *)(done + 1);
+  float *epi = (float *)(smem + WG_NST * st_bytes + 8 * (2 * WG_NST + 1) + 16);   // [4][32][33]
+
+  const int r0 = blockIdx.x * P.rows_per_cta;
+  const int r1 = min(g.M, r0 + P.rows_per_cta);
+  const int nchunks = r1 > r0 ? (r1 - r0 + 31) / 32 : 0;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                 "r"(P.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < WG_NST; ++i) { mbar_init(&full[i], 8); mbar_init(&empty[i], 1); }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // constant rows k = K..Kpad of A_T: zeros, and the ones row for the bias
+  for (int s = 0; s < WG_NST; ++s)
+    for (int idx = tid; idx < (P.Kpad - g.K) * 32; idx += blockDim.x) {
+      const int r = g.K + idx / 32, m = idx % 32;
+      *(float *)(smem + s * st_bytes + kmaj_swz(r, m)) = (r == P.ones_col) ? 1.0f : 0.0f;
+    }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+
+  if (warp < 8) {
+    // ---------------- producers: lane = row m of the chunk ----------------
+    // column blocks of 32 over [A columns | D columns]; warp w owns blocks w and w + 8.
+    // Each lane loads its row's whole 128-B block segment (8 x ld.v4), rounds to TF32 and
+    // scatters it into 32 K-major rows at column `lane`.  The next chunk's row indices and
+    // data are loaded while the current chunk is being stored (register double buffer).
+    const int nba = g.K / 32, nbd = g.N / 32, nb = nba + nbd;   // 32-column blocks
+    auto rows_of = [&](int c, int (&ri)[4], int &dr) {
+      const int m = r0 + c * 32 + lane;
+      const bool ok = c < nchunks && m < r1 && !(skip & 2);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ri[q] = (ok && q < g.A.nseg) ? (g.A.seg[q].idx ? __ldg(g.A.seg[q].idx + m) : m) : -1;
+      dr = ok ? (g.didx ? __ldg(g.didx + m) : m) : -1;
+    };
+    auto load = [&](const int (&ri)[4], int dr, float4 (&v)[2][8]) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int b = warp + 8 * h;
+        const float *src = nullptr;
+        if (b < nba) {
+          const int col = 32 * b;
+          int sg = 0, start = 0;
+          bool found = false;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q < g.A.nseg && !found) {
+              if (col < start + g.A.seg[q].width) { sg = q; found = true; }
+              else start += g.A.seg[q].width;
+            }
+          int r = -1;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q == sg) r = ri[q];
+          if (r >= 0) src = g.A.seg[sg].base + (size_t)r * g.A.seg[sg].ld + (col - start);
+        } else if (b < nb && dr >= 0) {
+          src = g.D + (size_t)dr * g.ldd + 32 * (b - nba);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[h][k] = src ? __ldg((const float4 *)src + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    };
+    int ri[4], dr;
+    float4 cur[2][8];
+    rows_of(0, ri, dr);
+    load(ri, dr, cur);
+    for (int c = 0; c < nchunks; ++c) {
+      const int s = c % WG_NST, u = c / WG_NST;
+      float4 nxt[2][8];
+      int nri[4], ndr;
+      rows_of(c + 1, nri, ndr);
+      if (c + 1 < nchunks) load(nri, ndr, nxt);
+      if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+      uint8_t *stA = smem + s * st_bytes, *stD = stA + a_bytes;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int b = warp + 8 * h;
+        if (b >= nb) break;
+        const bool isA = b < nba;
+        uint8_t *base = isA ? stA : stD;
+        const int r0b = isA ? 32 * b : 32 * (b - nba);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          float x[4] = {cur[h][k].x, cur[h][k].y, cur[h][k].z, cur[h][k].w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float t = x[q];
+            if (isA && g.A.act == 1) t = siluf_(t);
+            *(uint32_t *)(base + kmaj_swz(r0b + 4 * k + q, lane)) = to_tf32(t);
+          }
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[s]);
+      if (c + 1 < nchunks) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) cur[h][k] = nxt[h][k];
+      }
+    }
+  } else {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(P.Npad >> 3) << 17) |
+                             ((uint32_t)(128 >> 4) << 24);
+      for (int c = 0; c < nchunks; ++c) {
+        const int s = c % WG_NST, u = c / WG_NST;
+        mbar_wait(&full[s], u & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t baseA = smem_u32(smem + s * st_bytes), baseD = baseA + a_bytes;
+        for (int tt = 0; tt < P.ktiles; ++tt) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint64_t ad = make_desc(baseA + tt * 16384 + j * 32, 16, 1024) | ((uint64_t)2 << 61);
+            uint64_t bd = make_desc(baseD + j * 32, 16, 1024) | ((uint64_t)2 << 61);
+            if (!(skip & 8)) mma_tf32(tmem + tt * P.Npad, ad, bd, idesc, (c > 0 || j > 0) ? 1u : 0u);
+          }
+        }
+        mma_commit(&empty[s]);
+      }
+      mma_commit(done);
+    }
+  }
+
+  // ---------------- epilogue: TMEM -> smem transpose -> coalesced partial rows ----------------
+  if (warp < 4) {
+    if (nchunks > 0) mbar_wait(done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    float *stile = epi + warp * (32 * 33);
+    float *Pout = partial + (size_t)blockIdx.x * P.Kp * g.N;
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    for (int tt = 0; tt < P.ktiles; ++tt) {
+      const int k0 = tt * 128 + warp * 32;
+      for (int j0 = 0; j0 < P.Npad; j0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + lane_base + tt * P.Npad + j0, r);
+#pragma unroll
+        for (int qq = 0; qq < 32; ++qq) stile[lane * 33 + qq] = nchunks > 0 ? __uint_as_float(r[qq]) : 0.f;
+        __syncwarp();
+        const int n = j0 + lane;
+        if (n < g.N) {
+          for (int rr = 0; rr < 32; ++rr) {
+            const int k = k0 + rr;
+            if (k >= P.Kp) break;
+            Pout[(size_t)k * g.N + n] = stile[rr * 33 + lane];
+          }
+        }
+        __syncwarp();
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols) : "memory");
+}
+
 }  // namespace
 
 // Returns false if the GEMM does not fit this path (caller uses the SIMT kernel).
@@ -493,10 +704,59 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
     sms = cached;
   }
   const int grid = std::min(ntiles, sms);
-  ProfScope ps(ctx, "rowgemm_tc", 2.0 * g.M * (double)g.K * cols,
+  ProfScope ps(ctx, g.tag ? g.tag : "rowgemm_tc", 2.0 * g.M * (double)g.K * cols,
                (double)g.M * (4.0 * P.width + 4.0 * cols * 2) + 4.0 * g.K * cols);
   static int skip = getenv("CHG_TC_SKIP") ? atoi(getenv("CHG_TC_SKIP")) : 0;   // debug knob (timing studies)
   k_rowgemm_tc<<<grid, WS_THREADS, smem, ctx->stream>>>(g, P, img, ntiles, skip);
   check_launch(ctx);
+  return true;
+}
+
+// Weight gradient on tcgen05 (TF32).  Returns false when the shape does not fit
+// (caller uses the SIMT kernel).  Writes partials [splits][Kp][N] for k_wgrad_reduce.
+bool wgrad_tc(chg_ctx *ctx, const WGrad &g, float **partial_out, int *Kp_out, int *splits_out, bool *bias_done) {
+  if (g.M <= 0 || g.K <= 0 || g.K % 32 || g.N % 32 || g.N > 256 || g.K > 256 || (g.ldd % 4)) return false;
+  if ((uintptr_t)g.D & 15) return false;
+  for (int s = 0; s < g.A.nseg; ++s) {
+    const ASeg &S = g.A.seg[s];
+    if (S.width % 32 || S.ld % 4 || ((uintptr_t)S.base & 15)) return false;
+  }
+  WgPlan P{};
+  P.Kpad = (g.K + 127) / 128 * 128;
+  P.ktiles = P.Kpad / 128;
+  P.Npad = g.N;
+  const bool ones = g.bias && (g.K % 128 != 0);
+  P.ones_col = ones ? g.K : -1;
+  P.Kp = g.K + (ones ? 1 : 0);
+  const int cols = P.ktiles * P.Npad;
+  if (cols > 512) return false;
+  P.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int chunks = (g.M + 31) / 32;
+  const int grid = std::max(1, std::min(sms, chunks));
+  P.rows_per_cta = (chunks + grid - 1) / grid * 32;
+  const int splits = (g.M + P.rows_per_cta - 1) / P.rows_per_cta;
+  float *partial = ctx->getf("wgrad_partial", (size_t)splits * P.Kp * g.N);
+  const size_t st_bytes = (size_t)(P.Kpad + P.Npad) * 128;
+  const size_t smem = 1024 + WG_NST * st_bytes + 8 * (2 * WG_NST + 1) + 16 + 4 * 32 * 33 * 4;
+  if (smem > 224 * 1024) return false;
+  static bool attr = false;
+  if (!attr) {
+    CUDA_OK(cudaFuncSetAttribute(k_wgrad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
+    attr = true;
+  }
+  static int skip = getenv("CHG_TC_SKIP") ? atoi(getenv("CHG_TC_SKIP")) : 0;
+  ProfScope ps(ctx, g.tag ? g.tag : "wgrad_tc", 2.0 * g.M * (double)P.Kp * g.N, (double)g.M * (4.0 * g.K + 4.0 * g.N));
+  k_wgrad_tc<<<splits, WG_THREADS, smem, ctx->stream>>>(g, P, partial, skip);
+  check_launch(ctx);
+  *partial_out = partial;
+  *Kp_out = P.Kp;
+  *splits_out = splits;
+  *bias_done = !g.bias || ones;
   return true;
 }
