@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(256) k_wgrad_reduce(const WGrad g, const float
   const WGradDst &d = g.dst[n / 64];
   const int nn = n % 64;
   if (k < g.K) {
-    if (d.W) d.W[(size_t)k * d.ldw + nn] += t;
+    if (d.W && k >= d.k0 && (d.kn < 0 || k < d.k0 + d.kn)) d.W[(size_t)(k - d.k0) * d.ldw + nn] += t;
   } else if (d.b) {
     d.b[nn] += t;
   }

@@ -58,6 +58,7 @@ struct RowGemm {
 struct WGradDst {
   float *W = nullptr; int ldw = 0;   // gradient of W columns [n0, n0+64), rows 0..K-1
   float *b = nullptr;                // gradient of bias (column sums), optional
+  int k0 = 0, kn = -1;               // only rows [k0, k0+kn) go to W (kn < 0: all K rows)
 };
 
 struct WGrad {

@@ -411,7 +411,19 @@ void ac_bwd_body(Bwd &Bw, int t, const float *v, const float *e, const float *ea
     G.tag = "ac_dZ";
     rowgemm(ctx, G);
   }
-  for (int br = 0; br < 2; ++br) {  // dW2, db2
+  if (ctx->use_tc) {  // dW2, db2 of both branches in one K = N = 128 launch (diagonal blocks kept)
+    WGrad wg;
+    wg.A.seg[0] = aseg(z1, 128, 128);
+    wg.A.nseg = 1; wg.A.act = 1;
+    wg.M = (int)E; wg.K = 128; wg.tc = 1;
+    wg.D = dY; wg.ldd = 128; wg.N = 128; wg.bias = 1;
+    wg.dst[0].W = Bw.G(pre + ".core.W2"); wg.dst[0].ldw = 64; wg.dst[0].b = Bw.G(pre + ".core.b2");
+    wg.dst[0].k0 = 0; wg.dst[0].kn = 64;
+    wg.dst[1].W = Bw.G(pre + ".gate.W2"); wg.dst[1].ldw = 64; wg.dst[1].b = Bw.G(pre + ".gate.b2");
+    wg.dst[1].k0 = 64; wg.dst[1].kn = 64;
+    wg.tag = "ac_W2_wg";
+    wgrad(ctx, wg);
+  } else for (int br = 0; br < 2; ++br) {  // dW2, db2
     const char *b = br ? ".gate" : ".core";
     WGrad wg;
     wg.A.seg[0] = aseg(z1 + 64 * br, 128, 64);
@@ -487,7 +499,19 @@ void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float 
     G.tag = "bc_dZ";
     rowgemm(ctx, G);
   }
-  for (int br = 0; br < 2; ++br) {
+  if (ctx->use_tc) {  // dW2, db2 of both branches in one K = N = 128 launch (diagonal blocks kept)
+    WGrad wg;
+    wg.A.seg[0] = aseg(z1, 128, 128);
+    wg.A.nseg = 1; wg.A.act = 1;
+    wg.M = (int)A; wg.K = 128; wg.tc = 1;
+    wg.D = dYb; wg.ldd = 128; wg.N = 128; wg.bias = 1;
+    wg.dst[0].W = Bw.G(bp + ".core.W2"); wg.dst[0].ldw = 64; wg.dst[0].b = Bw.G(bp + ".core.b2");
+    wg.dst[0].k0 = 0; wg.dst[0].kn = 64;
+    wg.dst[1].W = Bw.G(bp + ".gate.W2"); wg.dst[1].ldw = 64; wg.dst[1].b = Bw.G(bp + ".gate.b2");
+    wg.dst[1].k0 = 64; wg.dst[1].kn = 64;
+    wg.tag = "bc_W2_wg";
+    wgrad(ctx, wg);
+  } else for (int br = 0; br < 2; ++br) {
     const char *b = br ? ".gate" : ".core";
     WGrad wg;
     wg.A.seg[0] = aseg(z1 + 64 * br, 128, 64);

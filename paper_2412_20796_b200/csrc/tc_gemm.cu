@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const RowGemm g, c
 //   Rows are split across persistent CTAs; each CTA accumulates its k tiles
 //   (M = 128, ≤ 2) × N in TMEM and writes one partial [Kp][N]; partials are
 //   reduced in a fixed order by k_wgrad_reduce (gemm.cu).  When K % 128 != 0 a
-//   constant ones row at k = K yields the bias gradient (column sums of D).
+//   bias (column sums of D) is summed by the producers from the staged K-major D rows.
 //   Warps 0-7 produce, warp 8 issues MMAs, warps 0-3 run the epilogue.
 // ---------------------------------------------------------------------------
 constexpr int WG_NST = 3;
@@ -548,16 +548,19 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const WGrad g, const
         for (int k = 0; k < 8; ++k) v[h][k] = src ? __ldg((const float4 *)src + k) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     };
-    int ri[4], dr;
+    // row indices run two chunks ahead of the data, the data one chunk ahead of the stores
+    int ri[4], dr, ri2[4], dr2;
     float4 cur[2][8];
     rows_of(0, ri, dr);
+    rows_of(1, ri2, dr2);
     load(ri, dr, cur);
+    float bsum[2] = {0.f, 0.f};                         // bias: column sums of D (lane = column)
     for (int c = 0; c < nchunks; ++c) {
       const int s = c % WG_NST, u = c / WG_NST;
       float4 nxt[2][8];
-      int nri[4], ndr;
-      rows_of(c + 1, nri, ndr);
-      if (c + 1 < nchunks) load(nri, ndr, nxt);
+      if (c + 1 < nchunks) load(ri2, dr2, nxt);
+      int ri3[4], dr3;
+      rows_of(c + 2, ri3, dr3);
       if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
       uint8_t *stA = smem + s * st_bytes, *stD = stA + a_bytes;
 #pragma unroll
@@ -577,6 +580,18 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const WGrad g, const
             *(uint32_t *)(base + kmaj_swz(r0b + 4 * k + q, lane)) = to_tf32(t);
           }
         }
+        if (!isA && g.bias) {
+          // lane n sums K-major row r0b + n (the 32 rows m of this chunk), read back from smem
+          __syncwarp();
+          const uint8_t *row = base + (r0b + lane) * 128;
+          float acc = 0.f;
+#pragma unroll
+          for (int uu = 0; uu < 8; ++uu) {
+            float4 v = *(const float4 *)(row + (uu << 4));
+            acc += (v.x + v.y) + (v.z + v.w);
+          }
+          bsum[h] += acc;
+        }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
@@ -586,6 +601,17 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const WGrad g, const
         for (int h = 0; h < 2; ++h)
 #pragma unroll
           for (int k = 0; k < 8; ++k) cur[h][k] = nxt[h][k];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ri2[q] = ri3[q];
+      dr2 = dr3;
+    }
+    if (g.bias) {                                       // bias row K of this CTA's partial
+      float *Pout = partial + (size_t)blockIdx.x * P.Kp * g.N;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int b = warp + 8 * h;
+        if (b >= nba && b < nb) Pout[(size_t)g.K * g.N + 32 * (b - nba) + lane] = bsum[h];
       }
     }
   } else {
@@ -631,7 +657,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const WGrad g, const
         if (n < g.N) {
           for (int rr = 0; rr < 32; ++rr) {
             const int k = k0 + rr;
-            if (k >= P.Kp) break;
+            if (k >= g.K) break;                        // row K (bias) comes from the producers
             Pout[(size_t)k * g.N + n] = stile[rr * 33 + lane];
           }
         }
@@ -725,9 +751,8 @@ bool wgrad_tc(chg_ctx *ctx, const WGrad &g, float **partial_out, int *Kp_out, in
   P.Kpad = (g.K + 127) / 128 * 128;
   P.ktiles = P.Kpad / 128;
   P.Npad = g.N;
-  const bool ones = g.bias && (g.K % 128 != 0);
-  P.ones_col = ones ? g.K : -1;
-  P.Kp = g.K + (ones ? 1 : 0);
+  P.ones_col = -1;                                    // bias is summed by the producers
+  P.Kp = g.K + (g.bias ? 1 : 0);
   const int cols = P.ktiles * P.Npad;
   if (cols > 512) return false;
   P.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
@@ -757,6 +782,6 @@ bool wgrad_tc(chg_ctx *ctx, const WGrad &g, float **partial_out, int *Kp_out, in
   *partial_out = partial;
   *Kp_out = P.Kp;
   *splits_out = splits;
-  *bias_done = !g.bias || ones;
+  *bias_done = true;
   return true;
 }

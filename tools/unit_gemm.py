@@ -15,3 +15,4 @@ for kind in (0, 1):
                 print(kind, eng, (M, K, N), "rel", np.linalg.norm(o - ref) / np.linalg.norm(ref), "max|o|", np.abs(o).max())
             except chg.ChgError as e:
                 print(kind, eng, (M, K, N), "ERR", e)
+# bias path through the gated-MLP weight-gradient call sites is covered by the TF32 parity tests
