@@ -79,6 +79,9 @@ __device__ __forceinline__ void mma_commit(uint64_t *bar) {
                : "memory");
 }
 
+// SiLU with the approximate reciprocal (MUFU.RCP): its error (~2 ulp fp32) is far
+// below the TF32 rounding that follows, and it avoids the IEEE division sequence.
+__device__ __forceinline__ float silu_fast(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
 __device__ __forceinline__ uint32_t to_tf32(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
@@ -287,7 +290,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const RowGemm g, c
         for (int k = 0; k < 8; ++k) {
           const int kk = (k + sw) & 7;                // rotated order: conflict-free banks
           float4 v = *(const float4 *)&row[kk];
-          if (g.A.act == 1) { v.x = siluf_(v.x); v.y = siluf_(v.y); v.z = siluf_(v.z); v.w = siluf_(v.w); }
+          if (g.A.act == 1) { v.x = silu_fast(v.x); v.y = silu_fast(v.y); v.z = silu_fast(v.z); v.w = silu_fast(v.w); }
           row[kk] = make_uint4(to_tf32(v.x), to_tf32(v.y), to_tf32(v.z), to_tf32(v.w));
         }
       }
@@ -448,10 +451,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const RowGemm g, c
 //   (M = 128, ≤ 2) × N in TMEM and writes one partial [Kp][N]; partials are
 //   reduced in a fixed order by k_wgrad_reduce (gemm.cu).  When K % 128 != 0 a
 //   bias (column sums of D) is summed by the producers from the staged K-major D rows.
-//   Warps 0-7 produce, warp 8 issues MMAs, warps 0-3 run the epilogue.
+//   Warps 0-11 produce, warp 12 issues MMAs, warps 0-3 run the epilogue.
 // ---------------------------------------------------------------------------
 constexpr int WG_NST = 3;
-constexpr int WG_THREADS = 9 * 32;
+constexpr int WG_NPW = 12;                 // producer warps
+constexpr int WG_THREADS = (WG_NPW + 1) * 32;
 
 struct WgPlan {
   int Kpad;        // rows of A_T (multiple of 128)
@@ -467,7 +471,7 @@ __device__ __forceinline__ uint32_t kmaj_swz(int r, int m) {   // byte offset of
   return (uint32_t)(r * 128 + ((((m >> 2) ^ (r & 7))) << 4) + (m & 3) * 4);
 }
 
-__global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const WGrad g, const WgPlan P, float *__restrict__ partial,
+__global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constant__ WGrad g, const WgPlan P, float *__restrict__ partial,
                                                              int skip) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -479,6 +483,8 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const WGrad g, const
   uint64_t *done = empty + WG_NST;
   uint32_t *tslot = (uint32_t *)(done + 1);
   float *epi = (float *)(smem + WG_NST * st_bytes + 8 * (2 * WG_NST + 1) + 16);   // [4][32][33]
+  float *sbias = epi + 4 * 32 * 33;                                                 // [WG_NPW][256]
+  __shared__ int s_seg[8], s_col[8];        // A block -> segment, column within the segment
 
   const int r0 = blockIdx.x * P.rows_per_cta;
   const int r1 = min(g.M, r0 + P.rows_per_cta);
@@ -491,10 +497,17 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const WGrad g, const
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (tid == 0) {
-    for (int i = 0; i < WG_NST; ++i) { mbar_init(&full[i], 8); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < WG_NST; ++i) { mbar_init(&full[i], g.K / 32 + g.N / 32); mbar_init(&empty[i], 1); }
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (tid < 8) {
+    int q = 0, start = 0;
+    while (q < g.A.nseg - 1 && 32 * tid >= start + g.A.seg[q].width) start += g.A.seg[q++].width;
+    s_seg[tid] = q;
+    s_col[tid] = 32 * tid - start;
+  }
+  for (int i = tid; i < WG_NPW * 256; i += blockDim.x) sbias[i] = 0.f;
   // constant rows k = K..Kpad of A_T: zeros, and the ones row for the bias
   for (int s = 0; s < WG_NST; ++s)
     for (int idx = tid; idx < (P.Kpad - g.K) * 32; idx += blockDim.x) {
@@ -507,111 +520,94 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const WGrad g, const
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
 
-  if (warp < 8) {
+  if (warp < WG_NPW) {
     // ---------------- producers: lane = row m of the chunk ----------------
-    // column blocks of 32 over [A columns | D columns]; warp w owns blocks w and w + 8.
-    // Each lane loads its row's whole 128-B block segment (8 x ld.v4), rounds to TF32 and
-    // scatters it into 32 K-major rows at column `lane`.  The next chunk's row indices and
-    // data are loaded while the current chunk is being stored (register double buffer).
+    // Jobs are (chunk c, 32-column block b) over [A columns | D columns], j = c·nb + b,
+    // dealt round-robin to the WG_NPW producer warps.  A job loads its lane's 128-B row
+    // segment (8 x ld.v4), rounds to TF32 (SiLU first for A when act) and scatters it
+    // into 32 K-major rows at column `lane`.  The next job's data and the row index of
+    // the one after are loaded while the current job is being stored.
     const int nba = g.K / 32, nbd = g.N / 32, nb = nba + nbd;   // 32-column blocks
-    auto rows_of = [&](int c, int (&ri)[4], int &dr) {
+    const int njobs = nchunks * nb;
+    auto row_of = [&](int j) -> int {
+      if (j >= njobs || (skip & 2)) return -1;
+      const int c = j / nb, b = j - c * nb;
       const int m = r0 + c * 32 + lane;
-      const bool ok = c < nchunks && m < r1 && !(skip & 2);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) ri[q] = (ok && q < g.A.nseg) ? (g.A.seg[q].idx ? __ldg(g.A.seg[q].idx + m) : m) : -1;
-      dr = ok ? (g.didx ? __ldg(g.didx + m) : m) : -1;
-    };
-    auto load = [&](const int (&ri)[4], int dr, float4 (&v)[2][8]) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int b = warp + 8 * h;
-        const float *src = nullptr;
-        if (b < nba) {
-          const int col = 32 * b;
-          int sg = 0, start = 0;
-          bool found = false;
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (q < g.A.nseg && !found) {
-              if (col < start + g.A.seg[q].width) { sg = q; found = true; }
-              else start += g.A.seg[q].width;
-            }
-          int r = -1;
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (q == sg) r = ri[q];
-          if (r >= 0) src = g.A.seg[sg].base + (size_t)r * g.A.seg[sg].ld + (col - start);
-        } else if (b < nb && dr >= 0) {
-          src = g.D + (size_t)dr * g.ldd + 32 * (b - nba);
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v[h][k] = src ? __ldg((const float4 *)src + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (m >= r1) return -1;
+      if (b < nba) {
+        const int32_t *ix = g.A.seg[s_seg[b]].idx;
+        return ix ? __ldg(ix + m) : m;
       }
+      return g.didx ? __ldg(g.didx + m) : m;
     };
-    // row indices run two chunks ahead of the data, the data one chunk ahead of the stores
-    int ri[4], dr, ri2[4], dr2;
-    float4 cur[2][8];
-    rows_of(0, ri, dr);
-    rows_of(1, ri2, dr2);
-    load(ri, dr, cur);
-    float bsum[2] = {0.f, 0.f};                         // bias: column sums of D (lane = column)
-    for (int c = 0; c < nchunks; ++c) {
-      const int s = c % WG_NST, u = c / WG_NST;
-      float4 nxt[2][8];
-      if (c + 1 < nchunks) load(ri2, dr2, nxt);
-      int ri3[4], dr3;
-      rows_of(c + 2, ri3, dr3);
-      if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
-      uint8_t *stA = smem + s * st_bytes, *stD = stA + a_bytes;
+    auto load = [&](int j, int row, float4 (&v)[8]) {
+      const float *src = nullptr;
+      if (j < njobs && row >= 0) {
+        const int b = j % nb;
+        if (b < nba) {
+          const ASeg &S = g.A.seg[s_seg[b]];
+          src = S.base + (size_t)row * S.ld + s_col[b];
+        } else {
+          src = g.D + (size_t)row * g.ldd + 32 * (b - nba);
+        }
+      }
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int b = warp + 8 * h;
-        if (b >= nb) break;
-        const bool isA = b < nba;
-        uint8_t *base = isA ? stA : stD;
-        const int r0b = isA ? 32 * b : 32 * (b - nba);
+      for (int k = 0; k < 8; ++k) v[k] = src ? __ldg((const float4 *)src + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    int j = warp;
+    int row_n = row_of(j + WG_NPW);
+    float4 cur[8];
+    load(j, row_of(j), cur);
+    for (; j < njobs; j += WG_NPW) {
+      float4 nxt[8];
+      load(j + WG_NPW, row_n, nxt);
+      row_n = row_of(j + 2 * WG_NPW);
+      const int c = j / nb, b = j - c * nb, s = c % WG_NST, u = c / WG_NST;
+      if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+      uint8_t *stA = smem + s * st_bytes;
+      const bool isA = b < nba;
+      uint8_t *base = isA ? stA : stA + a_bytes;
+      const int r0b = isA ? 32 * b : 32 * (b - nba);
+      if (isA && g.A.act == 1) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          float x[4] = {cur[h][k].x, cur[h][k].y, cur[h][k].z, cur[h][k].w};
+          const float x[4] = {cur[k].x, cur[k].y, cur[k].z, cur[k].w};
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            float t = x[q];
-            if (isA && g.A.act == 1) t = siluf_(t);
-            *(uint32_t *)(base + kmaj_swz(r0b + 4 * k + q, lane)) = to_tf32(t);
-          }
+          for (int q = 0; q < 4; ++q) *(uint32_t *)(base + kmaj_swz(r0b + 4 * k + q, lane)) = to_tf32(silu_fast(x[q]));
         }
-        if (!isA && g.bias) {
-          // lane n sums K-major row r0b + n (the 32 rows m of this chunk), read back from smem
-          __syncwarp();
-          const uint8_t *row = base + (r0b + lane) * 128;
-          float acc = 0.f;
+      } else {
 #pragma unroll
-          for (int uu = 0; uu < 8; ++uu) {
-            float4 v = *(const float4 *)(row + (uu << 4));
-            acc += (v.x + v.y) + (v.z + v.w);
-          }
-          bsum[h] += acc;
+        for (int k = 0; k < 8; ++k) {
+          const float x[4] = {cur[k].x, cur[k].y, cur[k].z, cur[k].w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) *(uint32_t *)(base + kmaj_swz(r0b + 4 * k + q, lane)) = to_tf32(x[q]);
         }
+      }
+      if (!isA && g.bias) {
+        // lane n sums K-major row r0b + n (the 32 rows m of this chunk), read back from smem
+        __syncwarp();
+        const uint8_t *row = base + (r0b + lane) * 128;
+        float acc = 0.f;
+#pragma unroll
+        for (int uu = 0; uu < 8; ++uu) {
+          float4 v = *(const float4 *)(row + (uu << 4));
+          acc += (v.x + v.y) + (v.z + v.w);
+        }
+        sbias[warp * 256 + r0b + lane] += acc;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[s]);
-      if (c + 1 < nchunks) {
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int k = 0; k < 8; ++k) cur[h][k] = nxt[h][k];
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) ri2[q] = ri3[q];
-      dr2 = dr3;
+      for (int k = 0; k < 8; ++k) cur[k] = nxt[k];
     }
     if (g.bias) {                                       // bias row K of this CTA's partial
+      asm volatile("bar.sync 1, %0;" ::"r"(WG_NPW * 32) : "memory");
       float *Pout = partial + (size_t)blockIdx.x * P.Kp * g.N;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int b = warp + 8 * h;
-        if (b >= nba && b < nb) Pout[(size_t)g.K * g.N + 32 * (b - nba) + lane] = bsum[h];
+      for (int n = tid; n < g.N; n += WG_NPW * 32) {
+        float t = 0.f;
+        for (int w = 0; w < WG_NPW; ++w) t += sbias[w * 256 + n];   // fixed order: deterministic
+        Pout[(size_t)g.K * g.N + n] = t;
       }
     }
   } else {
@@ -768,7 +764,7 @@ bool wgrad_tc(chg_ctx *ctx, const WGrad &g, float **partial_out, int *Kp_out, in
   const int splits = (g.M + P.rows_per_cta - 1) / P.rows_per_cta;
   float *partial = ctx->getf("wgrad_partial", (size_t)splits * P.Kp * g.N);
   const size_t st_bytes = (size_t)(P.Kpad + P.Npad) * 128;
-  const size_t smem = 1024 + WG_NST * st_bytes + 8 * (2 * WG_NST + 1) + 16 + 4 * 32 * 33 * 4;
+  const size_t smem = 1024 + WG_NST * st_bytes + 8 * (2 * WG_NST + 1) + 16 + 4 * 32 * 33 * 4 + WG_NPW * 256 * 4;
   if (smem > 224 * 1024) return false;
   static bool attr = false;
   if (!attr) {
