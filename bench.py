@@ -38,7 +38,36 @@ except Exception:
     PEAK_SRC = "fallback (B200_PROFILING.md)"
 # FP32 CUDA-core peak: 148 SMs x 128 FMA/clk x 2 flop x max SM clock
 FP32_PEAK_TFLOPS = 148 * 128 * 2 * PEAKS.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-HBM_TAGS = {"segsum", "gate_fwd", "gate_bwd", "basis", "basis_bwd", "embed", "adam", "heads", "loss", "transpose"}
+# TF32 dense tensor peak: measured bf16 cuBLAS peak (sustained: kernels timed inside a long step)
+# x the nominal tf32:bf16 ratio 1.1 : 2.25 PF/s (B200_PROFILING.md)
+TF32_PEAK_TFLOPS = PEAKS.get("bf16_tflops_sustained", PEAKS.get("bf16_tflops", 1590.0)) * 1.1 / 2.25
+# profile tags (chg_profile call sites) of the GatedMLP contractions: on tcgen05 in tf32 mode (NS)
+TC_ROW_TAGS = {"ac_f1", "ac_f2", "bc_f1", "bc_f2", "ac_dZ", "ac_dX", "bc_dZ", "bc_dX"}
+TC_WG_TAGS = {"ac_W1_wg", "ac_W2_wg", "bc_W1_wg", "bc_W2_wg"}
+WG_TAGS = TC_WG_TAGS | {"ac_out_wg", "bc_out_wg", "bc_outb_wg", "head_wg", "headM_wg", "proj_wg"}
+ROW_TAGS = TC_ROW_TAGS | {"ac_fout", "bc_fout", "head_f", "proj_f", "headM_f", "ac_dagg", "bc_daggb", "head_b",
+                          "headM_b", "dbasis"}
+
+
+def kernel_of(tag: str, precision: str) -> str:
+    """CUDA kernel (ncu name) that a profile tag times; the roofline is taken per kernel."""
+    if tag.startswith("segsum"):
+        return "k_segsum"
+    if tag.endswith("_red"):
+        return "k_wgrad_reduce"
+    if tag in TC_ROW_TAGS:
+        return "k_rowgemm_tc" if precision == "tf32" else "k_rowgemm"
+    if tag in TC_WG_TAGS:
+        return "k_wgrad_tc" if precision == "tf32" else "k_wgrad"
+    if tag in ROW_TAGS:
+        return "k_rowgemm"
+    if tag in WG_TAGS:
+        return "k_wgrad"
+    if tag in ("head_mlp_f", "head_mlp_b", "head_reduce", "species_grad"):
+        return {"head_mlp_f": "k_head_fwd", "head_mlp_b": "k_head_bwd", "head_reduce": "k_head_reduce",
+                "species_grad": "k_species_grad"}[tag]
+    return {"segsum": "k_segsum", "gate_fwd": "k_gate_fwd", "gate_bwd": "k_gate_bwd", "wgrad_reduce": "k_wgrad_reduce",
+            "tc_pack": "k_pack_b"}.get(tag, tag)
 
 
 def _args():
@@ -334,39 +363,56 @@ def main():
     e2e = structs / (ms_e2e / 1e3)
     h2d = int(np.mean([batches[k % len(batches)]["h2d"] for k in range(a.steps)]))
 
-    # ---- roofline of the dominant op (live CUDA events, profiled pass of the same steps)
-    dom = max(rep, key=lambda t: rep[t]["ms"])
-    r = rep[dom]
+    # ---- roofline of the dominant kernel (live CUDA events, profiled pass of the same steps)
+    kern = {}
+    for t, v in rep.items():
+        k = kernel_of(t, a.precision)
+        d = kern.setdefault(k, {"ms": 0.0, "launches": 0, "flops": 0.0, "bytes": 0.0, "tags": []})
+        for f in ("ms", "launches", "flops", "bytes"):
+            d[f] += v[f]
+        d["tags"].append(t)
+    dom = max(kern, key=lambda k: kern[k]["ms"])
+    r = kern[dom]
     per_launch_s = r["ms"] / 1e3 / max(r["launches"], 1)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(dom)
+            tr = json.load(f).get(a.precision, {}).get(dom)
+            traffic = tr["dram_bytes_per_launch"] if tr else None
     except Exception:
         pass
-    if dom in HBM_TAGS:
-        ach = r["bytes"] / (r["ms"] / 1e3) / 1e9
-        roof = {"bound": "hbm", "achieved": ach, "peak": PEAKS["hbm_gbs"], "unit": "GB/s", "peak_source": PEAK_SRC}
-    elif dom == "rowgemm_tc":
-        # TF32 dense peak = measured bf16 cuBLAS peak (sustained: kernel timed inside a long step) x 1/2
-        # (nominal tf32:bf16 ratio 1.1 : 2.25 PF/s, B200_PROFILING.md)
-        ach = r["flops"] / (r["ms"] / 1e3) / 1e12
-        pk = PEAKS.get("bf16_tflops_sustained", PEAKS.get("bf16_tflops", 1590.0)) * 1.1 / 2.25
-        roof = {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
+    gbs = r["bytes"] / (r["ms"] / 1e3) / 1e9
+    tfs = r["flops"] / (r["ms"] / 1e3) / 1e12
+    on_tc = dom.endswith("_tc")
+    flop_peak = TF32_PEAK_TFLOPS if on_tc else FP32_PEAK_TFLOPS
+    # binding roof by arithmetic intensity: below the ridge flop_peak / hbm_peak the kernel is HBM-bound
+    if r["bytes"] > 0 and (r["flops"] / r["bytes"]) < flop_peak * 1e3 / PEAKS["hbm_gbs"]:
+        roof = {"bound": "hbm", "achieved": gbs, "peak": PEAKS["hbm_gbs"], "unit": "GB/s", "peak_source": PEAK_SRC}
+        per_launch_alg = r["bytes"] / max(r["launches"], 1)
+    elif on_tc:
+        roof = {"bound": "tensor", "achieved": tfs, "peak": flop_peak, "unit": "TFLOP/s",
                 "peak_source": "tf32 = " + PEAK_SRC + " bf16_tflops_sustained x (1.1/2.25 nominal ratio)"}
+        per_launch_alg = r["flops"] / max(r["launches"], 1)
     else:
-        ach = r["flops"] / (r["ms"] / 1e3) / 1e12
-        roof = {"bound": "alu", "achieved": ach, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+        roof = {"bound": "alu", "achieved": tfs, "peak": flop_peak, "unit": "TFLOP/s",
                 "peak_source": "FP32 CUDA cores: 148 SM x 128 FMA/clk x 2 x sm_max_mhz (DESIGN.md)"}
-    roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": traffic, "kernel": dom,
-                 "algorithmic_per_launch": (r["bytes"] if roof["bound"] == "hbm" else r["flops"]) / max(r["launches"], 1),
-                 "avg_launch_us": per_launch_s * 1e6, "share_of_step": r["ms"] / ms_prof})
-    gs = rep.get("segsum", {"bytes": 0.0, "ms": 1e-9})
+        per_launch_alg = r["flops"] / max(r["launches"], 1)
+    roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": traffic, "kernel": dom, "call_sites": sorted(r["tags"]),
+                 "algorithmic_per_launch": per_launch_alg, "algorithmic_unit": "bytes" if roof["bound"] == "hbm" else "flop",
+                 "avg_launch_us": per_launch_s * 1e6, "share_of_step": r["ms"] / ms_prof,
+                 "intensity_flop_per_byte": r["flops"] / max(r["bytes"], 1.0),
+                 "tensor_frac": tfs / TF32_PEAK_TFLOPS if on_tc else None, "hbm_frac": gbs / PEAKS["hbm_gbs"]})
+    gs = {"bytes": sum(v["bytes"] for t, v in rep.items() if t.startswith("segsum")),
+          "ms": sum(v["ms"] for t, v in rep.items() if t.startswith("segsum")) or 1e-9}
     gather = {"kernel": "segsum (atomic-free CSR / rev / swap segmented gather-reduce)",
               "achieved_gbs": gs["bytes"] / (gs["ms"] / 1e3) / 1e9,
               "frac": gs["bytes"] / (gs["ms"] / 1e3) / 1e9 / PEAKS["hbm_gbs"], "peak_gbs": PEAKS["hbm_gbs"]}
     ops = {t: {"ms_per_step": v["ms"] / a.steps, "launches_per_step": v["launches"] / a.steps,
-               "share": v["ms"] / ms_prof} for t, v in sorted(rep.items(), key=lambda kv: -kv[1]["ms"])}
+               "share": v["ms"] / ms_prof, "kernel": kernel_of(t, a.precision)}
+           for t, v in sorted(rep.items(), key=lambda kv: -kv[1]["ms"])}
+    kernels = {k: {"ms_per_step": v["ms"] / a.steps, "share": v["ms"] / ms_prof,
+                   "gbs": v["bytes"] / (v["ms"] / 1e3) / 1e9, "tflops": v["flops"] / (v["ms"] / 1e3) / 1e12}
+               for k, v in sorted(kern.items(), key=lambda kv: -kv[1]["ms"])}
 
     if rank == 0:
         cb = None
@@ -393,6 +439,7 @@ def main():
             "clocks": clk,
             "roofline": roof,
             "gather_scatter": gather,
+            "kernels": kernels,
             "ops": ops,
             "cpu_baseline": cb,
         }

@@ -146,6 +146,7 @@ chg_status chg_ctx_create(int device, void *cuda_stream, chg_ctx **out) {
     uint64_t thr = UINT64_MAX;
     CUDA_OK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     CUDA_OK(cudaMalloc(&ctx->d_flag, 256));
+    CUDA_OK(cudaMemset(ctx->d_flag, 0, 256));
     ctx->d_loss = (double *)((char *)ctx->d_flag + 64);
   } catch (const ChgError &e) {
     delete ctx;
@@ -268,11 +269,13 @@ chg_status chg_model_create(chg_ctx *ctx, const chg_model_cfg *cfg, chg_model **
                              "94 species, mlp_precision 0 (fp32) or 2 (tf32 tcgen05))");
     build_layout(m);
     CUDA_OK(cudaSetDevice(ctx->device));
-    CUDA_OK(cudaMalloc(&m->params, 4 * m->P * 4));
-    m->grads = m->params + m->P;
-    m->m = m->params + 2 * m->P;
-    m->v = m->params + 3 * m->P;
-    CUDA_OK(cudaMemset(m->params, 0, 4 * m->P * 4));
+    // params | grads | adam m | adam v, each segment 256-B aligned (vector loads and stores)
+    const int64_t Ps = (m->P + 63) & ~(int64_t)63;
+    CUDA_OK(cudaMalloc(&m->params, 4 * Ps * 4));
+    m->grads = m->params + Ps;
+    m->m = m->params + 2 * Ps;
+    m->v = m->params + 3 * Ps;
+    CUDA_OK(cudaMemset(m->params, 0, 4 * Ps * 4));
     std::vector<int64_t> toff;
     std::vector<int32_t> trc;
     for (size_t t = 0; t < m->names.size(); ++t) {

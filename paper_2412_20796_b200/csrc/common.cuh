@@ -179,6 +179,13 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 
 // RAII device-time scope: records an event pair around the launches it covers
 // when profiling is on (algorithmic flops / bytes supplied by the caller).
+// stable copy of a composed profile tag (ProfScope keeps the pointer)
+inline const char *prof_tag(const std::string &t) {
+  static std::map<std::string, std::string> pool;
+  auto it = pool.emplace(t, t).first;
+  return it->second.c_str();
+}
+
 struct ProfScope {
   chg_ctx *ctx;
   int ev = -1;
@@ -196,10 +203,15 @@ struct ProfScope {
 };
 
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
-inline void check_launch(chg_ctx *ctx) {
+inline void check_launch(chg_ctx *ctx, const char *file = __builtin_FILE(), int line = __builtin_LINE()) {
   ctx->launched();
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) CHG_THROW(CHG_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+  if (e != cudaSuccess) CHG_THROW(CHG_ERR_CUDA, "kernel launch at %s:%d: %s", file, line, cudaGetErrorString(e));
+  static const bool sync_each = getenv("CHG_SYNC_CHECK") != nullptr;   // debug: attribute async faults to a launch
+  if (sync_each) {
+    e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) CHG_THROW(CHG_ERR_CUDA, "kernel at %s:%d: %s", file, line, cudaGetErrorString(e));
+  }
 }
 
 // graph.cu

@@ -232,6 +232,39 @@ __global__ void __launch_bounds__(256) k_wgrad(const WGrad g, float *__restrict_
   }
 }
 
+// Same reduction on float4 quads (N % 4 == 0): a block owns 32 quads = 128 outputs.
+__global__ void __launch_bounds__(256) k_wgrad_reduce4(const WGrad g, const float4 *__restrict__ partial, int Kp,
+                                                       int splits) {
+  __shared__ float4 sh[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int q = blockIdx.x * 32 + lane;
+  const int nq = Kp * g.N / 4;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (q < nq) {
+#pragma unroll 4
+    for (int sp = w; sp < splits; sp += 8) {
+      const float4 u = __ldcg(partial + (size_t)sp * nq + q);
+      s.x += u.x; s.y += u.y; s.z += u.z; s.w += u.w;
+    }
+  }
+  sh[w][lane] = s;
+  __syncthreads();
+  if (w != 0 || q >= nq) return;
+  float4 t = sh[0][lane];
+#pragma unroll
+  for (int k = 1; k < 8; ++k) { t.x += sh[k][lane].x; t.y += sh[k][lane].y; t.z += sh[k][lane].z; t.w += sh[k][lane].w; }
+  const int k = (4 * q) / g.N, n = (4 * q) % g.N;
+  const WGradDst &d = g.dst[n / 64];
+  const int nn = n % 64;
+  float *dst = nullptr;
+  if (k < g.K) {
+    if (d.W && k >= d.k0 && (d.kn < 0 || k < d.k0 + d.kn)) dst = d.W + (size_t)(k - d.k0) * d.ldw + nn;
+  } else {
+    dst = d.b ? d.b + nn : nullptr;
+  }
+  if (dst) { dst[0] += t.x; dst[1] += t.y; dst[2] += t.z; dst[3] += t.w; }
+}
+
 // Fixed-order reduction of the split-M partials: a block owns 32 consecutive
 // outputs; its 8 warps sum disjoint, interleaved split subsets (warp w: splits
 // w, w+8, ...), then warp 0 adds the 8 subtotals in order (deterministic).
@@ -296,6 +329,20 @@ static bool kmajor_of(const chg_model *m, const float *wt, const float *p, int l
   return false;
 }
 
+double gemm_a_bytes(const AOp &A, int64_t M, int lo, int hi) {
+  double b = 0;
+  int start = 0;
+  for (int s = 0; s < A.nseg; ++s) {
+    const ASeg &S = A.seg[s];
+    const int w = std::max(0, std::min(hi, start + S.width) - std::max(lo, start));
+    start += S.width;
+    if (w <= 0) continue;
+    if (S.idx) b += 4.0 * M + 4.0 * w * (double)(S.rows > 0 ? std::min<int64_t>(S.rows, M) : M);
+    else b += 4.0 * w * (double)M;
+  }
+  return b;
+}
+
 void rowgemm(chg_ctx *ctx, const RowGemm &g) {
   if (g.M <= 0) return;
   if (g.tc && ctx->use_tc && ctx->cur_model && ctx->cur_wt) {
@@ -323,10 +370,8 @@ void rowgemm(chg_ctx *ctx, const RowGemm &g) {
     lo = std::min(lo, C.a_k0);
     hi = std::max(hi, C.a_k0 + g.K);
   }
-  double idxb = 0;
-  for (int s = 0; s < g.A.nseg; ++s) idxb += g.A.seg[s].idx ? 4.0 : 0.0;
   ProfScope ps(ctx, g.tag ? g.tag : "rowgemm", 2.0 * g.M * (double)g.K * cols,
-               (double)g.M * (4.0 * std::min(hi - lo, tot) + idxb + 4.0 * outb) + 4.0 * wb);
+               gemm_a_bytes(g.A, g.M, lo, hi) + (double)g.M * 4.0 * outb + 4.0 * wb);
   const bool small = (int64_t)ceil_div(g.M, TM) * g.nchunk < 2 * 148;
   if (small) {
     dim3 grid(ceil_div(g.M, 32), g.nchunk);
@@ -340,6 +385,14 @@ void rowgemm(chg_ctx *ctx, const RowGemm &g) {
   check_launch(ctx);
 }
 
+static void launch_wgrad_reduce(chg_ctx *ctx, const WGrad &g, const float *partial, int Kp, int splits) {
+  if (g.N % 4 == 0 && ((uintptr_t)partial & 15) == 0)
+    k_wgrad_reduce4<<<ceil_div((int64_t)Kp * g.N / 4, 32), 256, 0, ctx->stream>>>(g, (const float4 *)partial, Kp, splits);
+  else
+    k_wgrad_reduce<<<ceil_div((int64_t)Kp * g.N, 32), 256, 0, ctx->stream>>>(g, partial, Kp, splits);
+  check_launch(ctx);
+}
+
 void wgrad(chg_ctx *ctx, const WGrad &g) {
   int Kp = g.K + (g.bias ? 1 : 0);
   if (Kp <= 0 || g.N <= 0) return;
@@ -348,8 +401,10 @@ void wgrad(chg_ctx *ctx, const WGrad &g) {
     int kp = 0, splits = 0;
     bool bias_done = false;
     if (wgrad_tc(ctx, g, &partial, &kp, &splits, &bias_done)) {
-      k_wgrad_reduce<<<ceil_div(kp * g.N, 32), 256, 0, ctx->stream>>>(g, partial, kp, splits);
-      check_launch(ctx);
+      {
+        ProfScope ps(ctx, prof_tag(std::string(g.tag ? g.tag : "wgrad") + "_red"), 0.0, 4.0 * kp * g.N * (splits + 2.0));
+        launch_wgrad_reduce(ctx, g, partial, kp, splits);
+      }
       if (!bias_done) {            // K is a multiple of 128: column sums of D on the CUDA cores
         WGrad b = g;
         b.A.nseg = 0;
@@ -368,19 +423,19 @@ void wgrad(chg_ctx *ctx, const WGrad &g) {
   int rps = g.M > 0 ? ceil_div(ceil_div(g.M, splits), WM) * WM : WM;
   splits = g.M > 0 ? ceil_div(g.M, rps) : 1;
   float *partial = ctx->getf("wgrad_partial", (size_t)splits * Kp * g.N);
-  double idxb = 0;
-  for (int s = 0; s < g.A.nseg; ++s) idxb += g.A.seg[s].idx ? 4.0 : 0.0;
-  ProfScope ps(ctx, g.tag ? g.tag : "wgrad", 2.0 * g.M * (double)Kp * g.N,
-               (double)g.M * (4.0 * g.K + idxb + 4.0 * g.N + (g.didx ? 4.0 : 0.0)) + 4.0 * Kp * g.N);
-  bool vec = aop_vec(g.A);
-  dim3 grid(ktiles, ntiles, splits);
-  if (vec)
-    k_wgrad<true><<<grid, 256, 0, ctx->stream>>>(g, partial, Kp, rps);
-  else
-    k_wgrad<false><<<grid, 256, 0, ctx->stream>>>(g, partial, Kp, rps);
-  check_launch(ctx);
-  k_wgrad_reduce<<<ceil_div(Kp * g.N, 32), 256, 0, ctx->stream>>>(g, partial, Kp, splits);
-  check_launch(ctx);
+  {
+    ProfScope ps(ctx, g.tag ? g.tag : "wgrad", 2.0 * g.M * (double)Kp * g.N,
+                 gemm_a_bytes(g.A, g.M, 0, g.K) + (double)g.M * (4.0 * g.N + (g.didx ? 4.0 : 0.0)) + 4.0 * Kp * g.N);
+    bool vec = aop_vec(g.A);
+    dim3 grid(ktiles, ntiles, splits);
+    if (vec)
+      k_wgrad<true><<<grid, 256, 0, ctx->stream>>>(g, partial, Kp, rps);
+    else
+      k_wgrad<false><<<grid, 256, 0, ctx->stream>>>(g, partial, Kp, rps);
+    check_launch(ctx);
+  }
+  ProfScope ps(ctx, prof_tag(std::string(g.tag ? g.tag : "wgrad") + "_red"), 0.0, 4.0 * Kp * g.N * (splits + 2.0));
+  launch_wgrad_reduce(ctx, g, partial, Kp, splits);
 }
 
 // ---------------------------------------------------------------------------

@@ -18,6 +18,7 @@ struct ASeg {
   const int32_t *idx = nullptr;  // row index per m (nullptr = m); idx < 0 -> zero row
   int ld = 0;                    // row stride (floats)
   int width = 0;                 // columns contributed by this segment
+  int64_t rows = 0;              // rows of the gathered table (algorithmic bytes: read once); 0 = M
 };
 
 struct AOp {
@@ -80,9 +81,13 @@ void wgrad(chg_ctx *ctx, const WGrad &g);
 bool wgrad_tc(chg_ctx *ctx, const WGrad &g, float **partial, int *Kp, int *splits, bool *bias_done);
 
 // helpers to fill descriptors
-inline ASeg aseg(const float *base, int ld, int width, const int32_t *idx = nullptr) {
-  ASeg s; s.base = base; s.ld = ld; s.width = width; s.idx = idx; return s;
+inline ASeg aseg(const float *base, int ld, int width, const int32_t *idx = nullptr, int64_t table_rows = 0) {
+  ASeg s; s.base = base; s.ld = ld; s.width = width; s.idx = idx; s.rows = table_rows; return s;
 }
+// Algorithmic (compulsory) bytes of reading A columns [lo, hi) for M rows: a direct
+// segment is streamed once (4·w·M); a gathered one costs its indices (4·M) plus its
+// table read once (4·w·min(rows, M)) — repeated gathers of a row are L2 hits.
+double gemm_a_bytes(const AOp &A, int64_t M, int lo, int hi);
 inline Chunk chunk1(const float *W, int ldw, int K, const float *bias, float *out, int ldo, int ncols = 64) {
   Chunk c; c.W[0] = W; c.ldw[0] = ldw; c.wk0[0] = 0; c.wk0[1] = K; c.nwb = 1; c.bias = bias;
   c.out = out; c.ldo = ldo; c.ncols = ncols; return c;

@@ -1,0 +1,401 @@
+// head_mlp.cu — fused readout MLPs (A6 heads and their A8 adjoints).
+//
+// The heads are plain MLPs: hidden layers Linear(64→64)+SiLU, last Linear(64→n_out)
+// (P:141 energy head, Eq. 7 force head on e, Eq. 9 stress head on v).  They are not
+// GatedMLP contractions, so they stay on the fp32 CUDA cores (NS), but each head is
+// one kernel per direction instead of one GEMM launch per layer:
+//
+//   forward  (k_head_fwd):  a CTA keeps every weight of the head in shared memory and
+//            walks 64-row tiles (persistent grid): tile -> Z_k = H_{k-1} W_k + b_k
+//            (stored for the backward), H_k = SiLU(Z_k) in smem -> out = H W_L + b_L.
+//   backward (k_head_bwd):  per tile, dZ runs down the layers in smem; dX += dZ_0 W_0ᵀ is
+//            added into the caller's gradient rows; dW_k, db_k are accumulated in
+//            registers / fixed smem slots across the CTA's tiles and written once as a
+//            per-CTA partial in the flat layout of the head's parameter block, reduced
+//            by k_head_reduce in CTA order (deterministic, no atomics).
+//
+// Register tiling: 256 threads, thread (a = t / 16, b = t % 16) owns a 4 x 4 block.
+// Shared tiles are [64][65] (odd pitch: column walks are conflict-free).
+#include "common.cuh"
+#include "ops.cuh"
+
+namespace {
+
+constexpr int HT = 64;        // rows per tile
+constexpr int HP = 65;        // smem pitch of [64][64] tiles
+constexpr int HMAXL = 4;      // max linear layers per head
+
+struct HeadArgs {
+  const float *X;             // [rows, 64] input (v or e)
+  int64_t rows;
+  const float *P;             // head parameter block: W0 b0 W1 b1 ... (flat layout)
+  float *Z[HMAXL - 1];        // pre-activations of the hidden layers [rows, 64]
+  float *out; int ldo;        // forward output [rows, nout]
+  const float *dout;          // backward seed [rows, nout]
+  float *dX;                  // backward: dX[rows, 64] += ...
+  float *part;                // backward: per-CTA partial [grid][block_size]
+};
+
+__host__ __device__ constexpr int head_block_size(int NL, int NOUT) { return (NL - 1) * (64 * 64 + 64) + 64 * NOUT + NOUT; }
+// per-CTA partial stride (16-B aligned rows for the float4 stores)
+__host__ __device__ constexpr int head_part_stride(int NL, int NOUT) { return (head_block_size(NL, NOUT) + 3) & ~3; }
+
+__device__ __forceinline__ float silu_(float x) { return x / (1.0f + __expf(-x)); }
+__device__ __forceinline__ float dsilu_(float x) {
+  const float s = 1.0f / (1.0f + __expf(-x));
+  return s * (1.0f + x * (1.0f - s));
+}
+
+// smem layout (floats): W hidden [NL-1][64][HP] | b hidden [NL-1][64] | W last [64][NOUT] | b last [NOUT]
+//                       | tiles ...
+template <int NL, int NOUT>
+struct HeadSmem {
+  static constexpr int W = 0;
+  static constexpr int B = W + (NL - 1) * 64 * HP;
+  static constexpr int WL = B + (NL - 1) * 64;
+  static constexpr int BL = WL + 64 * NOUT;
+  static constexpr int T0 = (BL + NOUT + 3) & ~3;
+};
+
+template <int NL, int NOUT>
+__device__ void load_weights(const float *__restrict__ P, float *sm) {
+  using S = HeadSmem<NL, NOUT>;
+  for (int l = 0; l < NL - 1; ++l) {
+    const float *Wg = P + l * (64 * 64 + 64);
+    for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) sm[S::W + l * 64 * HP + (i / 64) * HP + (i % 64)] = Wg[i];
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) sm[S::B + l * 64 + i] = Wg[64 * 64 + i];
+  }
+  const float *Wl = P + (NL - 1) * (64 * 64 + 64);
+  for (int i = threadIdx.x; i < 64 * NOUT; i += blockDim.x) sm[S::WL + i] = Wl[i];
+  for (int i = threadIdx.x; i < NOUT; i += blockDim.x) sm[S::BL + i] = Wl[64 * NOUT + i];
+}
+
+// load a [64][64] row tile of a [rows, 64] matrix into smem [64][HP] (zero rows past the end)
+__device__ __forceinline__ void load_tile(const float *__restrict__ src, int64_t r0, int64_t rows, float *dst) {
+  for (int i = threadIdx.x; i < HT * 16; i += blockDim.x) {
+    const int r = i >> 4, c4 = (i & 15) * 4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r0 + r < rows) v = __ldg((const float4 *)(src + (r0 + r) * 64 + c4));
+    float *d = dst + r * HP + c4;
+    d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+  }
+}
+
+template <int NL, int NOUT>
+__global__ void __launch_bounds__(256) k_head_fwd(const __grid_constant__ HeadArgs a) {
+  extern __shared__ float sm[];
+  using S = HeadSmem<NL, NOUT>;
+  float *sH = sm + S::T0;            // [64][HP] layer input / activation
+  load_weights<NL, NOUT>(a.P, sm);
+  const int t = threadIdx.x, ra = (t >> 4) * 4, cb = (t & 15) * 4;
+  const int64_t ntiles = (a.rows + HT - 1) / HT;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * HT;
+    __syncthreads();
+    load_tile(a.X, r0, a.rows, sH);
+    __syncthreads();
+#pragma unroll 1
+    for (int l = 0; l < NL - 1; ++l) {
+      const float *W = sm + S::W + l * 64 * HP;
+      float acc[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+#pragma unroll 8
+      for (int k = 0; k < 64; ++k) {
+        float h[4], w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h[i] = sH[(ra + i) * HP + k];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) w[j] = W[k * HP + cb + j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(h[i], w[j], acc[i][j]);
+      }
+      __syncthreads();                 // every thread has read sH
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float z[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          z[j] = acc[i][j] + sm[S::B + l * 64 + cb + j];
+          sH[(ra + i) * HP + cb + j] = silu_(z[j]);
+        }
+        if (r0 + ra + i < a.rows) *(float4 *)(a.Z[l] + (r0 + ra + i) * 64 + cb) = make_float4(z[0], z[1], z[2], z[3]);
+      }
+      __syncthreads();
+    }
+    // last layer: out[r][o] = Σ_k H[r][k] W_L[k][o] + b_L[o]
+    for (int p = t; p < HT * NOUT; p += blockDim.x) {
+      const int r = p / NOUT, o = p % NOUT;
+      if (r0 + r >= a.rows) continue;
+      float s = 0.f;
+#pragma unroll 8
+      for (int k = 0; k < 64; ++k) s = fmaf(sH[r * HP + k], sm[S::WL + k * NOUT + o], s);
+      a.out[(r0 + r) * a.ldo + o] = s + sm[S::BL + o];
+    }
+  }
+}
+
+template <int NL, int NOUT>
+__global__ void __launch_bounds__(256) k_head_bwd(const __grid_constant__ HeadArgs a) {
+  extern __shared__ float sm[];
+  using S = HeadSmem<NL, NOUT>;
+  float *sA = sm + S::T0;            // layer input H_{k-1} (or X)
+  float *sZ = sA + HT * HP;          // pre-activation z_{k-1}
+  float *sG = sZ + HT * HP;          // dZ_k
+  float *sD = sG + HT * HP;          // dout tile [64][NOUT]
+  load_weights<NL, NOUT>(a.P, sm);
+  const int t = threadIdx.x, ta = (t >> 4) * 4, tb = (t & 15) * 4;
+  constexpr int NH = NL - 1;
+  // per-thread accumulators: dW_k[ta..ta+3][tb..tb+3] (k = input row, n = output col), db_k[tb..] (ta == 0)
+  float gW[NH][4][4], gb[NH][4];
+#pragma unroll
+  for (int l = 0; l < NH; ++l)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      gb[l][i] = 0.f;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) gW[l][i][j] = 0.f;
+    }
+  constexpr int NLP = (64 * NOUT + 255) / 256;   // last-layer weight grads per thread
+  float gWL[NLP], gbL = 0.f;
+#pragma unroll
+  for (int q = 0; q < NLP; ++q) gWL[q] = 0.f;
+
+  const int64_t ntiles = (a.rows + HT - 1) / HT;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * HT;
+    __syncthreads();
+    for (int p = t; p < HT * NOUT; p += blockDim.x) {
+      const int r = p / NOUT, o = p % NOUT;
+      sD[p] = (r0 + r < a.rows) ? a.dout[(r0 + r) * NOUT + o] : 0.f;
+    }
+    load_tile(a.Z[NH - 1], r0, a.rows, sZ);
+    __syncthreads();
+    for (int i = t; i < HT * 64; i += blockDim.x) {
+      const int r = i >> 6, c = i & 63;
+      sA[r * HP + c] = silu_(sZ[r * HP + c]);
+    }
+    __syncthreads();
+    // last layer: dW_L[k][o] += Σ_r H[r][k] dout[r][o], db_L[o] += Σ_r dout[r][o]
+#pragma unroll
+    for (int q = 0; q < NLP; ++q) {
+      const int p = t + 256 * q;
+      if (p < 64 * NOUT) {
+        const int k = p / NOUT, o = p % NOUT;
+        float s = 0.f;
+        for (int r = 0; r < HT; ++r) s = fmaf(sA[r * HP + k], sD[r * NOUT + o], s);
+        gWL[q] += s;
+      }
+    }
+    if (t < NOUT) {
+      float s = 0.f;
+      for (int r = 0; r < HT; ++r) s += sD[r * NOUT + t];
+      gbL += s;
+    }
+    // dZ_{NH-1}[r][k] = (Σ_o dout[r][o] W_L[k][o]) · SiLU'(z[r][k])
+    for (int i = t; i < HT * 64; i += blockDim.x) {
+      const int r = i >> 6, k = i & 63;
+      float s = 0.f;
+#pragma unroll
+      for (int o = 0; o < NOUT; ++o) s = fmaf(sD[r * NOUT + o], sm[S::WL + k * NOUT + o], s);
+      sG[r * HP + k] = s * dsilu_(sZ[r * HP + k]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int l = NH - 1; l >= 0; --l) {   // unrolled: gW[l] stays in registers
+      // layer input: H_{l-1} = SiLU(z_{l-1}) (z kept in sZ for the next dZ), or X for l = 0
+      if (l > 0) {
+        load_tile(a.Z[l - 1], r0, a.rows, sZ);
+        __syncthreads();
+        for (int i = t; i < HT * 64; i += blockDim.x) {
+          const int r = i >> 6, c = i & 63;
+          sA[r * HP + c] = silu_(sZ[r * HP + c]);
+        }
+      } else {
+        load_tile(a.X, r0, a.rows, sA);
+      }
+      __syncthreads();
+      // dW_l[k][n] += Σ_r A[r][k] G[r][n]; db_l[n] += Σ_r G[r][n]
+      {
+        float acc[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+        float cs[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+        for (int r = 0; r < HT; ++r) {
+          float x[4], gg[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) x[i] = sA[r * HP + ta + i];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) gg[j] = sG[r * HP + tb + j];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(x[i], gg[j], acc[i][j]);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) cs[j] += gg[j];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) gW[l][i][j] += acc[i][j];
+        if (ta == 0)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) gb[l][j] += cs[j];
+      }
+      // dH[r][k] = Σ_n G[r][n] W_l[k][n]: thread owns rows ta.., inputs k = tb..
+      float dh[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dh[i][j] = 0.f;
+      {
+        const float *W = sm + S::W + l * 64 * HP;
+#pragma unroll 8
+        for (int n = 0; n < 64; ++n) {
+          float gg[4], w[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) gg[i] = sG[(ta + i) * HP + n];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) w[j] = W[(tb + j) * HP + n];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dh[i][j] = fmaf(gg[i], w[j], dh[i][j]);
+        }
+      }
+      __syncthreads();                 // all reads of sG / sZ done
+      if (l > 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) sG[(ta + i) * HP + tb + j] = dh[i][j] * dsilu_(sZ[(ta + i) * HP + tb + j]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t r = r0 + ta + i;
+          if (r < a.rows) {
+            float4 *d = (float4 *)(a.dX + r * 64 + tb);
+            float4 v = *d;
+            v.x += dh[i][0]; v.y += dh[i][1]; v.z += dh[i][2]; v.w += dh[i][3];
+            *d = v;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // per-CTA partial in the flat layout of the head block
+  float *pp = a.part + (size_t)blockIdx.x * head_part_stride(NL, NOUT);
+#pragma unroll
+  for (int l = 0; l < NH; ++l) {
+    float *Wp = pp + l * (64 * 64 + 64);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      *(float4 *)(Wp + (ta + i) * 64 + tb) = make_float4(gW[l][i][0], gW[l][i][1], gW[l][i][2], gW[l][i][3]);
+    if (ta == 0) *(float4 *)(Wp + 64 * 64 + tb) = make_float4(gb[l][0], gb[l][1], gb[l][2], gb[l][3]);
+  }
+  float *Lp = pp + NH * (64 * 64 + 64);
+#pragma unroll
+  for (int q = 0; q < NLP; ++q) {
+    const int p = t + 256 * q;
+    if (p < 64 * NOUT) Lp[p] = gWL[q];
+  }
+  if (t < NOUT) Lp[64 * NOUT + t] = gbL;
+}
+
+// G[i] += Σ_c part[c][i] in CTA order (deterministic)
+__global__ void k_head_reduce(const float *__restrict__ part, int nctas, int n, int stride, float *__restrict__ G) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float s = 0.f;
+  for (int c = 0; c < nctas; ++c) s += part[(size_t)c * stride + i];
+  G[i] += s;
+}
+
+template <int NL, int NOUT>
+size_t head_smem_fwd() { return 4 * ((size_t)HeadSmem<NL, NOUT>::T0 + HT * HP); }
+template <int NL, int NOUT>
+size_t head_smem_bwd() { return 4 * ((size_t)HeadSmem<NL, NOUT>::T0 + 3 * HT * HP + HT * NOUT); }
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+template <int NL, int NOUT>
+void run_fwd(chg_ctx *ctx, const HeadArgs &a, const char *tag) {
+  const size_t smem = head_smem_fwd<NL, NOUT>();
+  static bool attr = false;
+  if (!attr) {
+    CUDA_OK(cudaFuncSetAttribute(k_head_fwd<NL, NOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const int64_t ntiles = (a.rows + HT - 1) / HT;
+  const int grid = (int)std::min<int64_t>(ntiles, 2 * sm_count());
+  ProfScope ps(ctx, tag, 2.0 * a.rows * (64.0 * 64 * (NL - 1) + 64.0 * NOUT),
+               a.rows * 4.0 * (64 + 64 * (NL - 1) + NOUT) + 4.0 * head_block_size(NL, NOUT) * grid);
+  k_head_fwd<NL, NOUT><<<grid, 256, smem, ctx->stream>>>(a);
+  check_launch(ctx);
+}
+
+template <int NL, int NOUT>
+void run_bwd(chg_ctx *ctx, HeadArgs a, float *G, const char *tag) {
+  const size_t smem = head_smem_bwd<NL, NOUT>();
+  static bool attr = false;
+  if (!attr) {
+    CUDA_OK(cudaFuncSetAttribute(k_head_bwd<NL, NOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const int64_t ntiles = (a.rows + HT - 1) / HT;
+  const int grid = (int)std::min<int64_t>(ntiles, 2 * sm_count());
+  const int nb = head_block_size(NL, NOUT);
+  const int stride = head_part_stride(NL, NOUT);
+  a.part = ctx->getf("head_part", (size_t)grid * stride);
+  {
+    ProfScope ps(ctx, tag, 2.0 * a.rows * (2.0 * 64 * 64 * (NL - 1) + 2.0 * 64 * NOUT),
+                 a.rows * 4.0 * (64 * 3 + 64 * (NL - 1) + NOUT) + 4.0 * nb * (double)grid * 2);
+    k_head_bwd<NL, NOUT><<<grid, 256, smem, ctx->stream>>>(a);
+    check_launch(ctx);
+  }
+  ProfScope ps(ctx, "head_reduce", 0.0, 4.0 * nb * (grid + 2.0));
+  k_head_reduce<<<ceil_div(nb, 256), 256, 0, ctx->stream>>>(a.part, grid, nb, stride, G);
+  check_launch(ctx);
+}
+
+}  // namespace
+
+void head_mlp_fwd(chg_ctx *ctx, int nl, int nout, const float *X, int64_t rows, const float *P, float *const *Z,
+                  float *out, int ldo) {
+  if (rows <= 0) return;
+  HeadArgs a{};
+  a.X = X; a.rows = rows; a.P = P; a.out = out; a.ldo = ldo;
+  for (int l = 0; l + 1 < nl; ++l) a.Z[l] = Z[l];
+  if (nl == 4 && nout == 1) run_fwd<4, 1>(ctx, a, "head_mlp_f");
+  else if (nl == 3 && nout == 1) run_fwd<3, 1>(ctx, a, "head_mlp_f");
+  else if (nl == 3 && nout == 9) run_fwd<3, 9>(ctx, a, "head_mlp_f");
+  else CHG_THROW(CHG_ERR_ARG, "head_mlp_fwd: unsupported head shape (%d layers, %d outputs)", nl, nout);
+}
+
+void head_mlp_bwd(chg_ctx *ctx, int nl, int nout, const float *X, int64_t rows, const float *P, float *const *Z,
+                  const float *dout, float *G, float *dX) {
+  if (rows <= 0) return;
+  HeadArgs a{};
+  a.X = X; a.rows = rows; a.P = P; a.dout = dout; a.dX = dX;
+  for (int l = 0; l + 1 < nl; ++l) a.Z[l] = Z[l];
+  if (nl == 4 && nout == 1) run_bwd<4, 1>(ctx, a, G, "head_mlp_b");
+  else if (nl == 3 && nout == 1) run_bwd<3, 1>(ctx, a, G, "head_mlp_b");
+  else if (nl == 3 && nout == 9) run_bwd<3, 9>(ctx, a, G, "head_mlp_b");
+  else CHG_THROW(CHG_ERR_ARG, "head_mlp_bwd: unsupported head shape (%d layers, %d outputs)", nl, nout);
+}

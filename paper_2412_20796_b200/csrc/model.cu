@@ -46,8 +46,8 @@ void atom_conv_fwd(Fwd &F, int t, const float *v, const float *e, const float *e
   float *msg = ctx->getf("msg_edge", std::max<int64_t>(E, 1) * 64);
   {  // [v_i, v_j, e_ij] · [W1_core | W1_gate] + b1   (gather fused in the A load)
     RowGemm G;
-    G.A.seg[0] = aseg(v, 64, 64, g->center);
-    G.A.seg[1] = aseg(v, 64, 64, g->nbr);
+    G.A.seg[0] = aseg(v, 64, 64, g->center, N);
+    G.A.seg[1] = aseg(v, 64, 64, g->nbr, N);
     G.A.seg[2] = aseg(e, 64, 64);
     G.A.nseg = 3;
     G.M = (int)E; G.K = 192; G.nchunk = 2; G.tc = 1;
@@ -71,7 +71,7 @@ void atom_conv_fwd(Fwd &F, int t, const float *v, const float *e, const float *e
   gate_fwd(ctx, E, y, 128, F.ln(pre), GATE_MUL_W, ea, nullptr, nullptr, nullptr, msg);
   SegSrc s;
   s.in = msg; s.ptr = g->row_ptr; s.rows = E;
-  segsum(ctx, N, agg, 64, 0, 1, &s);
+  segsum(ctx, N, agg, 64, 0, 1, &s, "segsum_ac");
   {  // v' = v + agg · W_out + b_out
     RowGemm G;
     G.A.seg[0] = aseg(agg, 64, 64);
@@ -101,9 +101,9 @@ void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float
     // shared input [v_i, e_ij, e_ik, a_ijk] against the packed first
     // layers of both modules (Fig. 3a): bond core/gate hidden, angle core/gate
     RowGemm G;
-    G.A.seg[0] = aseg(v, 64, 64, g->angle_ctr);
-    G.A.seg[1] = aseg(e, 64, 64, g->angle_e1);
-    G.A.seg[2] = aseg(e, 64, 64, g->angle_e2);
+    G.A.seg[0] = aseg(v, 64, 64, g->angle_ctr, g->N);
+    G.A.seg[1] = aseg(e, 64, 64, g->angle_e1, E);
+    G.A.seg[2] = aseg(e, 64, 64, g->angle_e2, E);
     G.A.seg[3] = aseg(a, 64, 64);
     G.A.nseg = 4;
     G.M = (int)A; G.K = 256; G.nchunk = angle_branch ? 4 : 2; G.tc = 1;
@@ -129,10 +129,10 @@ void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float
   }
   SegSrc s;
   s.in = q; s.ptr = g->angle_ptr; s.rows = A;
-  segsum(ctx, B, aggb, 64, 0, 1, &s);      // Σ over angles with first bond b (empty -> 0)
+  segsum(ctx, B, aggb, 64, 0, 1, &s, "segsum_bc");      // Σ over angles with first bond b (empty -> 0)
   {  // e' = e + 𝓛_e(agg) on all E edges (non-bond rows gather a zero row, Q16)
     RowGemm G;
-    G.A.seg[0] = aseg(aggb, 64, 64, g->bond_id);
+    G.A.seg[0] = aseg(aggb, 64, 64, g->bond_id, B);
     G.A.nseg = 1;
     G.M = (int)E; G.K = 64; G.nchunk = 1;
     G.ch[0] = chunk1(m->p(bp + ".out.W"), 64, 64, m->p(bp + ".out.b"), e_out, 64);
@@ -144,31 +144,11 @@ void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float
     gate_fwd(ctx, A, ya, 128, F.ln(ap), GATE_RESID, nullptr, nullptr, nullptr, a, a_out);
 }
 
-// --- MLP heads: hidden layers Linear+SiLU, last Linear -------------------------
+// --- MLP heads: hidden layers Linear+SiLU, last Linear (fused, head_mlp.cu) --------
 void mlp_fwd(Fwd &F, const std::string &pre, int nl, const float *x, int64_t rows, int nout, float *out, int ldo) {
-  chg_model *m = F.m;
-  const float *h = x;
-  for (int k = 0; k < nl; ++k) {
-    RowGemm G;
-    G.A.seg[0] = aseg(h, 64, 64);
-    G.A.nseg = 1;
-    G.M = (int)rows; G.K = 64; G.nchunk = 1;
-    std::string W = pre + ".W" + std::to_string(k), b = pre + ".b" + std::to_string(k);
-    if (k + 1 < nl) {
-      float *z = F.buf(pre + "_z" + std::to_string(k), rows, 64);
-      float *hn = F.buf(pre + "_h" + std::to_string(k), rows, 64);
-      G.act = 1;
-      G.ch[0] = chunk1(m->p(W), 64, 64, m->p(b), hn, 64);
-      G.ch[0].pre = z; G.ch[0].ldp = 64;
-      G.tag = "head_f";
-      rowgemm(F.ctx, G);
-      h = hn;
-    } else {
-      G.ch[0] = chunk1(m->p(W), nout, 64, m->p(b), out, ldo, nout);
-      G.tag = "head_f";
-      rowgemm(F.ctx, G);
-    }
-  }
+  float *Z[3] = {nullptr, nullptr, nullptr};
+  for (int k = 0; k + 1 < nl; ++k) Z[k] = F.buf(pre + "_z" + std::to_string(k), rows, 64);
+  head_mlp_fwd(F.ctx, nl, nout, x, rows, F.m->p(pre + ".W0"), Z, out, ldo);
 }
 
 void copy_out(chg_ctx *ctx, float *dst, const float *src, int64_t n, int on_device) {
@@ -299,43 +279,12 @@ struct Bwd {
   }
 };
 
-// dv/dx accumulation through an MLP head (hidden SiLU layers saved as z_k)
+// dx accumulation and parameter gradients through an MLP head (fused, head_mlp.cu)
 void mlp_bwd(Bwd &Bw, const std::string &pre, int nl, const float *x, int64_t rows, const float *dout, int nout,
              float *dx) {
-  chg_ctx *ctx = Bw.ctx;
-  const float *dz = dout;
-  int ncol = nout;
-  for (int k = nl - 1; k >= 0; --k) {
-    std::string W = pre + ".W" + std::to_string(k), b = pre + ".b" + std::to_string(k);
-    const float *in = k == 0 ? x : Bw.act(pre + "_z" + std::to_string(k - 1));
-    WGrad wg;
-    wg.A.seg[0] = aseg(in, 64, 64);
-    wg.A.nseg = 1;
-    wg.A.act = k > 0 ? 1 : 0;
-    wg.M = (int)rows; wg.K = 64;
-    wg.D = dz; wg.ldd = ncol; wg.N = ncol; wg.bias = 1;
-    wg.dst[0].W = Bw.G(W); wg.dst[0].ldw = ncol; wg.dst[0].b = Bw.G(b);
-    wg.tag = "head_wg";
-    wgrad(ctx, wg);
-    RowGemm G;
-    G.A.seg[0] = aseg(dz, ncol, ncol);
-    G.A.nseg = 1;
-    G.M = (int)rows; G.K = ncol;
-    if (k > 0) {
-      float *dzn = ctx->getf(pre + "_dz" + std::to_string(k - 1), (size_t)std::max<int64_t>(rows, 1) * 64);
-      G.ch[0] = chunk1(Bw.WT(W), 64, ncol, nullptr, dzn, 64);
-      G.ch[0].mul = Bw.act(pre + "_z" + std::to_string(k - 1)); G.ch[0].ldm = 64;
-      G.tag = "head_b";
-      rowgemm(ctx, G);
-      dz = dzn;
-      ncol = 64;
-    } else {
-      G.ch[0] = chunk1(Bw.WT(W), 64, ncol, nullptr, dx, 64);
-      G.ch[0].resid = dx; G.ch[0].ldr = 64;
-      G.tag = "head_b";
-      rowgemm(ctx, G);
-    }
-  }
+  float *Z[3] = {nullptr, nullptr, nullptr};
+  for (int k = 0; k + 1 < nl; ++k) Z[k] = const_cast<float *>(Bw.act(pre + "_z" + std::to_string(k)));
+  head_mlp_bwd(Bw.ctx, nl, nout, x, rows, Bw.m->p(pre + ".W0"), Z, dout, Bw.G(pre + ".W0"), dx);
 }
 
 // contributions of the output linear of atom conv t: dagg = dv · W_outᵀ, dW_out, db_out
@@ -365,7 +314,7 @@ void bc_bwd_head(Bwd &Bw, int t, const float *de, float *daggb) {
   std::string pre = "bond" + std::to_string(t);
   const float *aggb = Bw.act("bc_aggb_" + std::to_string(t));
   RowGemm G;
-  G.A.seg[0] = aseg(de, 64, 64, g->bond_edge);
+  G.A.seg[0] = aseg(de, 64, 64, g->bond_edge, g->E);
   G.A.nseg = 1;
   G.M = (int)g->B; G.K = 64;
   G.ch[0] = chunk1(Bw.WT(pre + ".out.W"), 64, 64, nullptr, daggb, 64);
@@ -453,8 +402,8 @@ void ac_bwd_body(Bwd &Bw, int t, const float *v, const float *e, const float *ea
   }
   {  // dW1 = Xᵀ dZ1 with X = [v_i, v_j, e] gathered again
     WGrad wg;
-    wg.A.seg[0] = aseg(v, 64, 64, g->center);
-    wg.A.seg[1] = aseg(v, 64, 64, g->nbr);
+    wg.A.seg[0] = aseg(v, 64, 64, g->center, N);
+    wg.A.seg[1] = aseg(v, 64, 64, g->nbr, N);
     wg.A.seg[2] = aseg(e, 64, 64);
     wg.A.nseg = 3;
     wg.M = (int)E; wg.K = 192; wg.tc = 1;
@@ -468,7 +417,7 @@ void ac_bwd_body(Bwd &Bw, int t, const float *v, const float *e, const float *ea
   SegSrc s[2];
   s[0].in = ti; s[0].ptr = g->row_ptr; s[0].rows = E;
   s[1].in = tj; s[1].ptr = g->row_ptr; s[1].perm = g->rev; s[1].rows = E;
-  segsum(ctx, N, dv, 64, 1, 2, s);
+  segsum(ctx, N, dv, 64, 1, 2, s, "segsum_ac_dv");
 }
 
 void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float *e, const float *a, const float *eb,
@@ -547,9 +496,9 @@ void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float 
   }
   {  // dW1 (bond) and dW (angle) = Xᵀ [dZ1 | dY_a]
     WGrad wg;
-    wg.A.seg[0] = aseg(v, 64, 64, g->angle_ctr);
-    wg.A.seg[1] = aseg(e, 64, 64, g->angle_e1);
-    wg.A.seg[2] = aseg(e, 64, 64, g->angle_e2);
+    wg.A.seg[0] = aseg(v, 64, 64, g->angle_ctr, N);
+    wg.A.seg[1] = aseg(e, 64, 64, g->angle_e1, E);
+    wg.A.seg[2] = aseg(e, 64, 64, g->angle_e2, E);
     wg.A.seg[3] = aseg(a, 64, 64);
     wg.A.nseg = 4;
     wg.M = (int)A; wg.K = 256; wg.tc = 1;
@@ -565,13 +514,13 @@ void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float 
   }
   SegSrc s[2];
  s[0].in = tv; s[0].ptr = g->atom_angle_ptr; s[0].rows = A;                // angles of centre i are contiguous
-  segsum(ctx, N, dv, 64, 1, 1, s);
+  segsum(ctx, N, dv, 64, 1, 1, s, "segsum_bc_dv");
   s[0] = SegSrc(); s[0].in = t1; s[0].ptr = g->angle_ptr; s[0].segmap = g->bond_id; s[0].rows = A;
   s[1] = SegSrc(); s[1].in = t2; s[1].ptr = g->angle_ptr; s[1].segmap = g->bond_id; s[1].perm = g->swap; s[1].rows = A;
-  segsum(ctx, E, de, 64, 1, 2, s);
+  segsum(ctx, E, de, 64, 1, 2, s, "segsum_bc_de");
   s[0] = SegSrc(); s[0].in = q1; s[0].ptr = g->angle_ptr; s[0].rows = A;
   s[1] = SegSrc(); s[1].in = q2; s[1].ptr = g->angle_ptr; s[1].perm = g->swap; s[1].rows = A;
-  segsum(ctx, B, deb, 64, 1, 2, s);
+  segsum(ctx, B, deb, 64, 1, 2, s, "segsum_bc_deb");
 }
 
 const float *labels_dev(chg_ctx *ctx, const void *p, size_t bytes, const char *name, int on_device) {
@@ -657,11 +606,7 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
     bc_bwd_body(Bw, t, ab, V(t), Ef(t), Af(t), eb, daggb, dv, de, da, deb);
   }
   // embedding (rows of W_v gathered by species -> grouped sum, no atomics)
-  {
-    SegSrc s;
-    s.in = dv; s.ptr = g->species_ptr; s.perm = g->species_perm; s.ptr_off = 1; s.rows = N;
-    segsum(ctx, m->cfg.n_species, Bw.G("embed.W"), 64, 1, 1, &s);
-  }
+  species_grad(ctx, N, m->cfg.n_species, g->species_ptr, g->species_perm, dv, Bw.G("embed.W"));
   // projections (Eq. 2) and trainable frequencies
   auto proj_grad = [&](const float *basis, int64_t rows, const float *d, const char *W) {
     WGrad wg;

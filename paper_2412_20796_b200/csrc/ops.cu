@@ -240,28 +240,73 @@ __global__ void __launch_bounds__(256) k_reduce_ln(int nblocks, const float *__r
 // ---------------------------------------------------------------------------
 struct SegArgs { SegSrc s[3]; int n; };
 
-__global__ void k_segsum(int64_t targets, float *__restrict__ out, int ldo, int accumulate, SegArgs a) {
-  int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int l = threadIdx.x & 31;
+// half-warp per target, one float4 (4 columns) per lane: a 256-B row is one
+// 16-lane load.  Row indices are fetched 16 at a time (coalesced) and broadcast by
+// shuffle; four rows are in flight per lane.  Rows are added in segment order, so
+// the result is deterministic.
+__global__ void __launch_bounds__(256) k_segsum(int64_t targets, float *__restrict__ out, int ldo, int accumulate,
+                                                SegArgs a) {
+  const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 4;
+  const int lane = threadIdx.x & 31, hl = lane & 15;
+  const unsigned hmask = 0xffffu << (lane & 16);
   if (t >= targets) return;
-  float2 acc = make_float2(0.f, 0.f);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     if (k >= a.n) break;
     const SegSrc &S = a.s[k];
-    int64_t s = S.segmap ? (int64_t)S.segmap[t] : t + S.ptr_off;
-    if (s < 0) continue;
-    int r0 = S.ptr[s], r1 = S.ptr[s + 1];
-#pragma unroll 4
-    for (int r = r0; r < r1; ++r) {
-      int64_t row = S.perm ? S.perm[r] : r;
-      float2 v = *(const float2 *)(S.in + row * 64 + 2 * l);
-      acc.x += v.x; acc.y += v.y;
+    const int64_t sg = S.segmap ? (int64_t)__ldg(S.segmap + t) : t + S.ptr_off;
+    if (sg < 0) continue;
+    const int r0 = __ldg(S.ptr + sg), r1 = __ldg(S.ptr + sg + 1);
+    const float4 *in = (const float4 *)S.in + hl;
+    for (int base = r0; base < r1; base += 16) {
+      const int n = min(16, r1 - base);
+      const int myrow = hl < n ? (S.perm ? __ldg(S.perm + base + hl) : base + hl) : 0;
+      int j = 0;
+      for (; j + 4 <= n; j += 4) {
+        const int q0 = __shfl_sync(hmask, myrow, j, 16), q1 = __shfl_sync(hmask, myrow, j + 1, 16);
+        const int q2 = __shfl_sync(hmask, myrow, j + 2, 16), q3 = __shfl_sync(hmask, myrow, j + 3, 16);
+        const float4 v0 = __ldg(in + (int64_t)q0 * 16), v1 = __ldg(in + (int64_t)q1 * 16);
+        const float4 v2 = __ldg(in + (int64_t)q2 * 16), v3 = __ldg(in + (int64_t)q3 * 16);
+        acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
+        acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w;
+        acc.x += v2.x; acc.y += v2.y; acc.z += v2.z; acc.w += v2.w;
+        acc.x += v3.x; acc.y += v3.y; acc.z += v3.z; acc.w += v3.w;
+      }
+      for (; j < n; ++j) {
+        const int q = __shfl_sync(hmask, myrow, j, 16);
+        const float4 v = __ldg(in + (int64_t)q * 16);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
     }
   }
-  float2 *o = (float2 *)(out + t * ldo + 2 * l);
-  if (accumulate) { float2 p = *o; acc.x += p.x; acc.y += p.y; }
+  float4 *o = (float4 *)(out + t * ldo) + hl;
+  if (accumulate) { const float4 p = *o; acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w; }
   *o = acc;
+}
+
+// Embedding gradient dW_v[z] += Σ_{i: Z_i = z+1} dv_i (Eq. 2 adjoint) in two fixed-order
+// passes: (1) block (c, z) sums rows [64c, 64c+64) of species z's segment (thread = column),
+// (2) block z adds its chunk partials in chunk order.  Long segments (oxygen) are split
+// across many blocks instead of one serial walk.
+constexpr int SPG_ROWS = 64;
+__global__ void __launch_bounds__(64) k_species_grad1(const int32_t *__restrict__ ptr, const int32_t *__restrict__ perm,
+                                                      const float *__restrict__ dv, float *__restrict__ part, int maxc) {
+  const int c = blockIdx.x, z = blockIdx.y, col = threadIdx.x;
+  const int r0 = ptr[z + 1] + c * SPG_ROWS, r1 = min(r0 + SPG_ROWS, ptr[z + 2]);
+  if (r0 >= r1) return;
+  float acc = 0.f;
+#pragma unroll 8
+  for (int r = r0; r < r1; ++r) acc += dv[(int64_t)perm[r] * 64 + col];
+  part[((int64_t)z * maxc + c) * 64 + col] = acc;
+}
+__global__ void __launch_bounds__(64) k_species_grad2(const int32_t *__restrict__ ptr, const float *__restrict__ part,
+                                                      int maxc, float *__restrict__ dW) {
+  const int z = blockIdx.x, col = threadIdx.x;
+  const int n = ptr[z + 2] - ptr[z + 1], nc = (n + SPG_ROWS - 1) / SPG_ROWS;
+  float acc = 0.f;
+  for (int c = 0; c < nc; ++c) acc += part[((int64_t)z * maxc + c) * 64 + col];
+  dW[(int64_t)z * 64 + col] += acc;
 }
 
 // ---------------------------------------------------------------------------
@@ -497,7 +542,8 @@ void gate_bwd(chg_ctx *ctx, int64_t rows, const float *y, int ldy, GateLN ln, in
   check_launch(ctx);
 }
 
-void segsum(chg_ctx *ctx, int64_t targets, float *out, int ldo, int accumulate, int nsrc, const SegSrc *src) {
+void segsum(chg_ctx *ctx, int64_t targets, float *out, int ldo, int accumulate, int nsrc, const SegSrc *src,
+            const char *tag) {
   if (targets <= 0) return;
   SegArgs a;
   a.n = nsrc;
@@ -506,8 +552,24 @@ void segsum(chg_ctx *ctx, int64_t targets, float *out, int ldo, int accumulate, 
     a.s[k] = src[k];
     bytes += src[k].rows * (256.0 + (src[k].perm ? 4.0 : 0.0)) + targets * (src[k].segmap ? 12.0 : 8.0);
   }
-  ProfScope ps(ctx, "segsum", 0.0, bytes);
-  k_segsum<<<ceil_div(targets * 32, 256), 256, 0, ctx->stream>>>(targets, out, ldo, accumulate, a);
+  for (int k = 0; k < nsrc; ++k)
+    if (((uintptr_t)src[k].in & 15) || ((uintptr_t)out & 15) || (ldo & 3))
+      CHG_THROW(CHG_ERR_STATE, "segsum: 16-byte alignment required (in %p, out %p, ldo %d)", (const void *)src[k].in,
+                (void *)out, ldo);
+  ProfScope ps(ctx, tag, 0.0, bytes);
+  k_segsum<<<ceil_div(targets * 16, 256), 256, 0, ctx->stream>>>(targets, out, ldo, accumulate, a);
+  check_launch(ctx);
+}
+
+void species_grad(chg_ctx *ctx, int64_t N, int n_species, const int32_t *species_ptr, const int32_t *species_perm,
+                  const float *dv, float *dW) {
+  if (N <= 0 || n_species <= 0) return;
+  const int maxc = ceil_div(N, SPG_ROWS);
+  float *part = ctx->getf("species_part", (size_t)n_species * maxc * 64);
+  ProfScope ps(ctx, "species_grad", 0.0, N * 260.0 + n_species * 512.0);
+  k_species_grad1<<<dim3(maxc, n_species), 64, 0, ctx->stream>>>(species_ptr, species_perm, dv, part, maxc);
+  check_launch(ctx);
+  k_species_grad2<<<n_species, 64, 0, ctx->stream>>>(species_ptr, part, maxc, dW);
   check_launch(ctx);
 }
 

@@ -30,7 +30,22 @@ struct SegSrc { const float *in = nullptr; const int32_t *ptr = nullptr; const i
                 const int32_t *segmap = nullptr; int ptr_off = 0;
                 int64_t rows = 0;   // total input rows summed (algorithmic-bytes bookkeeping only)
 };
-void segsum(chg_ctx *ctx, int64_t targets, float *out, int ldo, int accumulate, int nsrc, const SegSrc *src);
+void segsum(chg_ctx *ctx, int64_t targets, float *out, int ldo, int accumulate, int nsrc, const SegSrc *src,
+            const char *tag = "segsum");
+
+// embedding gradient: dW[z] += Σ_{i: Z_i = z+1} dv[i] over the species-sorted atom list
+// (species_ptr has n_species + 2 entries, segment of Z at [ptr[Z], ptr[Z+1])); deterministic
+void species_grad(chg_ctx *ctx, int64_t N, int n_species, const int32_t *species_ptr, const int32_t *species_perm,
+                  const float *dv, float *dW);
+
+// fused readout MLPs (head_mlp.cu): nl linear layers (hidden 64 + SiLU, last 64 -> nout),
+// P / G = the head's parameter / gradient block in the flat layout (W0 b0 W1 b1 ...),
+// Z[k] = hidden pre-activations [rows, 64] (written forward, read backward),
+// dX [rows, 64] accumulates the input gradient.  Supported: (4, 1), (3, 1), (3, 9).
+void head_mlp_fwd(chg_ctx *ctx, int nl, int nout, const float *X, int64_t rows, const float *P, float *const *Z,
+                  float *out, int ldo);
+void head_mlp_bwd(chg_ctx *ctx, int nl, int nout, const float *X, int64_t rows, const float *P, float *const *Z,
+                  const float *dout, float *G, float *dX);
 
 // heads (Eq. 7, Eq. 9)
 void heads_forces(chg_ctx *ctx, const chg_graph *g, const float *n_e, float *forces);

@@ -726,8 +726,13 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
     sms = cached;
   }
   const int grid = std::min(ntiles, sms);
+  double outb = 0;
+  for (int c = 0; c < g.nchunk; ++c) {
+    const Chunk &C = g.ch[c];
+    outb += C.ncols * (1.0 + (C.pre != nullptr) + (C.mul != nullptr) + (C.resid != nullptr));
+  }
   ProfScope ps(ctx, g.tag ? g.tag : "rowgemm_tc", 2.0 * g.M * (double)g.K * cols,
-               (double)g.M * (4.0 * P.width + 4.0 * cols * 2) + 4.0 * g.K * cols);
+               gemm_a_bytes(g.A, g.M, P.lo, P.lo + P.width) + (double)g.M * 4.0 * outb + 4.0 * g.K * cols);
   static int skip = getenv("CHG_TC_SKIP") ? atoi(getenv("CHG_TC_SKIP")) : 0;   // debug knob (timing studies)
   k_rowgemm_tc<<<grid, WS_THREADS, smem, ctx->stream>>>(g, P, img, ntiles, skip);
   check_launch(ctx);
@@ -772,7 +777,8 @@ bool wgrad_tc(chg_ctx *ctx, const WGrad &g, float **partial_out, int *Kp_out, in
     attr = true;
   }
   static int skip = getenv("CHG_TC_SKIP") ? atoi(getenv("CHG_TC_SKIP")) : 0;
-  ProfScope ps(ctx, g.tag ? g.tag : "wgrad_tc", 2.0 * g.M * (double)P.Kp * g.N, (double)g.M * (4.0 * g.K + 4.0 * g.N));
+  ProfScope ps(ctx, g.tag ? g.tag : "wgrad_tc", 2.0 * g.M * (double)P.Kp * g.N,
+               gemm_a_bytes(g.A, g.M, 0, g.K) + (double)g.M * (4.0 * g.N + (g.didx ? 4.0 : 0.0)) + 4.0 * P.Kp * g.N);
   k_wgrad_tc<<<splits, WG_THREADS, smem, ctx->stream>>>(g, P, partial, skip);
   check_launch(ctx);
   *partial_out = partial;
