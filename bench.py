@@ -255,45 +255,49 @@ def main():
     model = models[a.precision]
 
     # ---- batches: global batch per index, balanced over ranks
-    batches = []
-    for bi in range(a.batches):
-        glob = make_config_batch(wl, bi, n_struct=per * ws)
-        if ws > 1:
-            g_all = ctx.build_graph(glob.atom_ptr, glob.positions, glob.lattice, glob.species)
-            ps = g_all.per_struct()
-            g_all.close()
-            loads = ps[:, 0] + ps[:, 1] + ps[:, 3]              # atoms + edges + angles (Q31)
-            rank_of = chg.balance(loads, ws)
-            mine = split_batch(glob, np.nonzero(rank_of == rank)[0].tolist())
-            per_rank_load = np.bincount(rank_of, weights=loads, minlength=ws)
-            contiguous = loads.reshape(ws, -1).sum(1) if glob.n_struct % ws == 0 else per_rank_load
-            cv = (float(per_rank_load.std() / per_rank_load.mean()), float(contiguous.std() / contiguous.mean()))
-        else:
-            mine, cv = glob, (0.0, 0.0)
-        gl = dict(S=glob.n_struct, N=glob.n_atoms, M=int(glob.magmom_mask.sum()))
-        dev = dict(pos=torch.as_tensor(mine.positions, device="cuda"),
-                   lat=torch.as_tensor(mine.lattice, device="cuda"),
-                   spec=torch.as_tensor(mine.species, device="cuda"),
-                   lab=dict(energy_per_atom=torch.as_tensor(mine.energy_per_atom, dtype=torch.float32, device="cuda"),
-                            forces=torch.as_tensor(mine.forces, dtype=torch.float32, device="cuda"),
-                            stress=torch.as_tensor(mine.stress, dtype=torch.float32, device="cuda"),
-                            magmom=torch.as_tensor(mine.magmom, dtype=torch.float32, device="cuda"),
-                            magmom_mask=torch.as_tensor(mine.magmom_mask, device="cuda")))
+    def make_batches(wl, per, nbatches):
+        out = []
+        for bi in range(nbatches):
+            glob = make_config_batch(wl, bi, n_struct=per * ws)
+            if ws > 1:
+                g_all = ctx.build_graph(glob.atom_ptr, glob.positions, glob.lattice, glob.species)
+                ps = g_all.per_struct()
+                g_all.close()
+                loads = ps[:, 0] + ps[:, 1] + ps[:, 3]              # atoms + edges + angles (Q31)
+                rank_of = chg.balance(loads, ws)
+                mine = split_batch(glob, np.nonzero(rank_of == rank)[0].tolist())
+                per_rank_load = np.bincount(rank_of, weights=loads, minlength=ws)
+                contiguous = loads.reshape(ws, -1).sum(1) if glob.n_struct % ws == 0 else per_rank_load
+                cv = (float(per_rank_load.std() / per_rank_load.mean()), float(contiguous.std() / contiguous.mean()))
+            else:
+                mine, cv = glob, (0.0, 0.0)
+            gl = dict(S=glob.n_struct, N=glob.n_atoms, M=int(glob.magmom_mask.sum()))
+            dev = dict(pos=torch.as_tensor(mine.positions, device="cuda"),
+                       lat=torch.as_tensor(mine.lattice, device="cuda"),
+                       spec=torch.as_tensor(mine.species, device="cuda"),
+                       lab=dict(energy_per_atom=torch.as_tensor(mine.energy_per_atom, dtype=torch.float32, device="cuda"),
+                                forces=torch.as_tensor(mine.forces, dtype=torch.float32, device="cuda"),
+                                stress=torch.as_tensor(mine.stress, dtype=torch.float32, device="cuda"),
+                                magmom=torch.as_tensor(mine.magmom, dtype=torch.float32, device="cuda"),
+                                magmom_mask=torch.as_tensor(mine.magmom_mask, device="cuda")))
 
-        def pinned(x, dt):
-            t = torch.empty(x.shape, dtype=dt, pin_memory=True)
-            t.copy_(torch.as_tensor(np.ascontiguousarray(x)).to(dt))
-            return t.numpy()
-        host = dict(pos=pinned(mine.positions, torch.float64), lat=pinned(mine.lattice, torch.float64),
-                    spec=pinned(mine.species, torch.int32),
-                    lab=dict(energy_per_atom=pinned(mine.energy_per_atom, torch.float32),
-                             forces=pinned(mine.forces, torch.float32),
-                             stress=pinned(mine.stress, torch.float32),
-                             magmom=pinned(mine.magmom, torch.float32),
-                             magmom_mask=pinned(mine.magmom_mask, torch.uint8)))
-        h2d = sum(v.nbytes for k, v in host.items() if k != "lab") + sum(v.nbytes for v in host["lab"].values()) \
-            + mine.atom_ptr.nbytes
-        batches.append(dict(ap=mine.atom_ptr, dev=dev, host=host, gl=gl, S=mine.n_struct, cv=cv, h2d=h2d))
+            def pinned(x, dt):
+                t = torch.empty(x.shape, dtype=dt, pin_memory=True)
+                t.copy_(torch.as_tensor(np.ascontiguousarray(x)).to(dt))
+                return t.numpy()
+            host = dict(pos=pinned(mine.positions, torch.float64), lat=pinned(mine.lattice, torch.float64),
+                        spec=pinned(mine.species, torch.int32),
+                        lab=dict(energy_per_atom=pinned(mine.energy_per_atom, torch.float32),
+                                 forces=pinned(mine.forces, torch.float32),
+                                 stress=pinned(mine.stress, torch.float32),
+                                 magmom=pinned(mine.magmom, torch.float32),
+                                 magmom_mask=pinned(mine.magmom_mask, torch.uint8)))
+            h2d = sum(v.nbytes for k, v in host.items() if k != "lab") + sum(v.nbytes for v in host["lab"].values()) \
+                + mine.atom_ptr.nbytes
+            out.append(dict(ap=mine.atom_ptr, dev=dev, host=host, gl=gl, S=mine.n_struct, cv=cv, h2d=h2d))
+        return out
+
+    batches = make_batches(wl, per, a.batches)
 
     lr0 = (per * ws) / 128 * 3e-4                      # Eq. 14
     total_steps = 2 * (a.warmup + a.steps) + 8
@@ -320,14 +324,15 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    def timed(on_host: bool, profile: bool = False, model=None):
+    def timed(on_host: bool, profile: bool = False, model=None, bl=None):
+        bl = bl or batches
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
         if profile:
             ctx.profile(True)
         l0 = ctx.launch_count()
         barrier()
         for k in range(a.steps):
-            b = batches[k % len(batches)]
+            b = bl[k % len(bl)]
             ev[k][0].record(stream)
             one_step(b, on_host, model)
             ev[k][1].record(stream)
@@ -357,6 +362,18 @@ def main():
     for k in range(a.warmup):
         one_step(batches[k % len(batches)], False, models[other])
     ms_other, _, _ = timed(False, model=models[other])
+
+    # weak-scaling base: the per-GPU workload of the N > 1 runs (C3, 128 structures) on this one GPU,
+    # so value(N) / (N * c3_value(1)) compares equal per-GPU work (the headline N = 1 line stays C2)
+    weak_base = None
+    if ws == 1 and wl == "C2":
+        c3 = make_batches("C3", 128, 2)
+        for k in range(a.warmup):
+            one_step(c3[k % len(c3)], False)
+        ms_c3, _, _ = timed(False, bl=c3)
+        s_c3 = sum(c3[k % len(c3)]["gl"]["S"] for k in range(a.steps))
+        weak_base = {"workload": "C3: 128 MPtrj-shaped structures on 1 GPU (the per-GPU work of the N > 1 runs)",
+                     "value": s_c3 / (ms_c3 / 1e3), "unit": "structures/s", "ms_per_step": ms_c3 / a.steps}
 
     structs = sum(batches[k % len(batches)]["gl"]["S"] for k in range(a.steps))
     value = structs / (ms / 1e3)
@@ -436,6 +453,7 @@ def main():
                        "rank0_counts_first_batch": None},
             "e2e": {"value": e2e, "unit": "structures/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 40 + 4},
             "gpu_launches": int(launches),
+            "weak_scaling_base": weak_base,
             "clocks": clk,
             "roofline": roof,
             "gather_scatter": gather,

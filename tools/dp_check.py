@@ -1,0 +1,82 @@
+"""Data-parallel equivalence on N GPUs (torchrun): balanced shards + global loss normalisers +
+the library's NCCL allreduce give the single-GPU full-batch gradient.
+
+Each rank: chg_build_graph / forward / backward on its shard (chg_balance over atoms + edges +
+angles), chg_step(allreduce) with Adam.  After one step Adam's first moment is m = (1 - β1) · g,
+g the allreduced gradient, so m / (1 - β1) is compared with the same quantity from a one-GPU run
+of the full batch (rank 0, separate context, no allreduce).  Also: the updated parameters are
+bit-identical on every rank.  Prints one JSON line on rank 0; exit code 0 iff all checks pass.
+"""
+import json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import torch.distributed as dist
+from chg_inputs import init_flat_params, make_config_batch, split_batch
+from paper_2412_20796_b200 import chg
+
+
+def labels(b):
+    return dict(energy_per_atom=b.energy_per_atom.astype(np.float32), forces=b.forces.astype(np.float32),
+                stress=b.stress.astype(np.float32), magmom=b.magmom.astype(np.float32), magmom_mask=b.magmom_mask)
+
+
+def main():
+    rank, ws, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    prec = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+    glob = make_config_batch("C2", 7, n_struct=8 * ws)
+    ctx = chg.Context(local)
+    uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        uid.copy_(torch.frombuffer(bytearray(chg.nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(uid, 0)
+    ctx.set_nccl(bytes(uid.cpu().numpy()), ws, rank)
+    cfg = chg.default_model_cfg(); cfg.mlp_precision = prec
+    m = chg.Model(ctx, cfg)
+    p0 = init_flat_params([(n, s) for n, s, _ in m.layout()], seed=0).astype(np.float32)
+    m.set_params(p0)
+    g_all = ctx.build_graph(glob.atom_ptr, glob.positions, glob.lattice, glob.species)
+    ps = g_all.per_struct(); g_all.close()
+    rank_of = chg.balance(ps[:, 0] + ps[:, 1] + ps[:, 3], ws)
+    mine = split_batch(glob, np.nonzero(rank_of == rank)[0].tolist())
+    gl = dict(n_struct_global=glob.n_struct, n_atoms_global=glob.n_atoms,
+              n_magmom_global=int(glob.magmom_mask.sum()))
+    g = ctx.build_graph(mine.atom_ptr, mine.positions, mine.lattice, mine.species)
+    ctx.forward(m, g, train=True, host=False)
+    loss = np.asarray(ctx.backward(m, g, labels(mine), **gl), np.float64)
+    ctx.step(m, lr=3e-4, step=1, allreduce=True)
+    g.close()
+    mom = m.get(2).astype(np.float64) / 0.1                 # m = (1 - beta1) * g_allreduced
+    p1 = torch.as_tensor(m.params(), device="cuda")
+    pmax, pmin = p1.clone(), p1.clone()
+    dist.all_reduce(pmax, op=dist.ReduceOp.MAX); dist.all_reduce(pmin, op=dist.ReduceOp.MIN)
+    identical = bool(torch.equal(pmax, pmin))
+    lt = torch.as_tensor(loss, device="cuda"); dist.all_reduce(lt)
+    ok = True
+    if rank == 0:
+        ctx1 = chg.Context(local)
+        m1 = chg.Model(ctx1, cfg); m1.set_params(p0)
+        g1 = ctx1.build_graph(glob.atom_ptr, glob.positions, glob.lattice, glob.species)
+        ctx1.forward(m1, g1, train=True, host=False)
+        loss1 = np.asarray(ctx1.backward(m1, g1, labels(glob)), np.float64)
+        ctx1.step(m1, lr=3e-4, step=1, allreduce=False)
+        mom1 = m1.get(2).astype(np.float64) / 0.1
+        rel = float(np.linalg.norm(mom - mom1) / np.linalg.norm(mom1))
+        lrel = float(abs(lt[0].item() - loss1[0]) / abs(loss1[0]))
+        tol = 1e-4 if prec == 0 else 2e-3
+        ok = identical and rel <= tol and lrel <= 1e-5
+        print(json.dumps({"world_size": ws, "mlp_precision": prec, "structures": glob.n_struct,
+                          "per_rank_structures": np.bincount(rank_of, minlength=ws).tolist(),
+                          "grad_rel_err_vs_1gpu": rel, "loss_rel_err_vs_1gpu": lrel, "tol": tol,
+                          "params_identical_across_ranks": identical, "ok": ok}), flush=True)
+        g1.close(); m1.close(); ctx1.close()
+    okt = torch.tensor([int(ok)], device="cuda"); dist.broadcast(okt, 0)
+    m.close(); ctx.close()
+    dist.destroy_process_group()
+    sys.exit(0 if okt.item() else 1)
+
+
+if __name__ == "__main__":
+    main()
