@@ -9,8 +9,10 @@
 #include <numeric>
 
 #include "common.cuh"
+#include "gemm.cuh"
 
 void destroy_graph_impl(chg_graph *G);
+void graph_fill_counts(chg_graph *G);
 void forward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, int train, chg_pred *out);
 void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *lab,
                    const chg_loss_cfg *cfg, double *loss_out);
@@ -220,7 +222,18 @@ chg_status chg_build_graph(chg_ctx *ctx, int32_t n_struct, const int64_t *atom_p
 chg_status chg_graph_counts(const chg_graph *g, int64_t tot[4], int64_t *per_struct) {
   if (!g || !tot) return CHG_ERR_ARG;
   tot[0] = g->N; tot[1] = g->E; tot[2] = g->B; tot[3] = g->A;
-  if (per_struct) std::copy(g->counts_h.begin(), g->counts_h.end(), per_struct);
+  if (per_struct) {
+    chg_graph *G = const_cast<chg_graph *>(g);    // lazily cached host copy (logically const)
+    if (!G->counts_ready) {
+      try {
+        graph_fill_counts(G);
+      } catch (const ChgError &e) {
+        G->ctx->err = e.msg;
+        return e.code;
+      }
+    }
+    std::copy(g->counts_h.begin(), g->counts_h.end(), per_struct);
+  }
   return CHG_OK;
 }
 
@@ -304,6 +317,8 @@ void chg_model_destroy(chg_model *m) {
   cudaStreamSynchronize(m->ctx->stream);
   cudaFree(m->params);
   if (m->d_toff) cudaFree(m->d_toff);
+  tc_cache_free(m);
+  if (m->wt) cudaFree(m->wt);
   delete m;
 }
 

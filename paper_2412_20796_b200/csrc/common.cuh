@@ -96,7 +96,9 @@ struct chg_graph {
   int64_t N = 0, E = 0, B = 0, A = 0;
   double r_atom = 5.0, r_bond = 3.0;
   std::vector<int64_t> atom_ptr_h;     // [S+1]
-  std::vector<int64_t> counts_h;       // [S*4] N,E,B,A
+  std::vector<int64_t> counts_h;       // [S*4] N,E,B,A (filled on demand: graph_fill_counts)
+  bool counts_ready = false;
+  int *d_flag = nullptr;               // device flags of the build (bit 3: reverse edge missing)
   void *block = nullptr;               // one allocation for all arrays below
   // per atom
   int32_t *atom_ptr = nullptr;         // [S+1]
@@ -147,6 +149,8 @@ struct chg_model {
   int n2d = 0;
   int64_t *d_toff = nullptr;
   int32_t *d_trc = nullptr;
+  void *tc_cache = nullptr;      // tensor-core weight images per call site (tc_gemm.cu)
+  float *wt = nullptr;           // transposed copy of every 2-D weight (same flat offsets)
 
   int64_t off(const std::string &n) const {
     auto it = index.find(n);

@@ -454,7 +454,9 @@ extern "C" chg_status chg_debug_gemm(chg_ctx *ctx, int kind, int engine, int M, 
     CUDA_OK(cudaMemcpyAsync(dW, W, 4 * nw, cudaMemcpyHostToDevice, st));
     CUDA_OK(cudaMemsetAsync(dO, 0, 4 * no, st));
     const bool old = ctx->use_tc;
+    const chg_model *old_model = ctx->cur_model;
     ctx->use_tc = engine == 2;
+    ctx->cur_model = nullptr;                  // no weight-image caching for the hook's scratch operands
     if (kind == 0) {
       std::vector<float> wk((size_t)K * N);
       for (int k = 0; k < K; ++k)
@@ -486,6 +488,7 @@ extern "C" chg_status chg_debug_gemm(chg_ctx *ctx, int kind, int engine, int M, 
       wgrad(ctx, g);
     }
     ctx->use_tc = old;
+    ctx->cur_model = old_model;
     CUDA_OK(cudaMemcpyAsync(out, dO, 4 * no, cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaStreamSynchronize(st));
   } catch (const ChgError &e) {

@@ -75,6 +75,8 @@ struct WGrad {
   WGradDst dst[4];               // per 64-column chunk of N
 };
 
+void tc_repack_all(chg_ctx *ctx, chg_model *m);   // forward start (TF32 mode): refresh cached weight images
+void tc_cache_free(chg_model *m);
 void rowgemm(chg_ctx *ctx, const RowGemm &g);      // tcgen05 when ctx->use_tc and eligible, else SIMT
 bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g);   // false if the shape does not fit the tensor-core path
 void wgrad(chg_ctx *ctx, const WGrad &g);

@@ -99,22 +99,28 @@ __global__ void k_count(int N, const double *__restrict__ pos, const double *__r
 #pragma unroll
   for (int k = 0; k < 9; ++k) L[k] = g.L[k];
   double fi[3] = {frac[3 * i], frac[3 * i + 1], frac[3 * i + 2]};
+  // lanes walk (j, n1) slots: W >= any pair's n1-range width (pair_range: <= 2·rw + 4 values),
+  // so each lane runs only the n2 x n3 loops of one image row (more lanes busy, shorter chains)
+  const int W = (int)floor(2.0 * g.rw[0]) + 4;
+  const int nslot = (a1 - a0) * W;
   int ce = 0, cb = 0, bad = 0;
-  for (int j = a0 + lane; j < a1; j += 32) {
+  for (int p = lane; p < nslot; p += 32) {
+    const int j = a0 + p / W, k = p % W;
     double fj[3] = {frac[3 * j], frac[3 * j + 1], frac[3 * j + 2]};
     Range r = pair_range(fi, fj, g.rw);
-    for (int n1 = r.lo[0]; n1 <= r.hi[0]; ++n1)
-      for (int n2 = r.lo[1]; n2 <= r.hi[1]; ++n2)
-        for (int n3 = r.lo[2]; n3 <= r.hi[2]; ++n3) {
-          if (i == j && n1 == 0 && n2 == 0 && n3 == 0) continue;
-          double dx, dy, dz, q;
-          eval_pair(pos, L, i, j, n1, n2, n3, dx, dy, dz, q);
-          if (q <= ra2) {
-            ++ce;
-            cb += (q <= rb2);
-            bad |= (q < 1e-12);
-          }
+    const int n1 = r.lo[0] + k;
+    if (n1 > r.hi[0]) continue;
+    for (int n2 = r.lo[1]; n2 <= r.hi[1]; ++n2)
+      for (int n3 = r.lo[2]; n3 <= r.hi[2]; ++n3) {
+        if (i == j && n1 == 0 && n2 == 0 && n3 == 0) continue;
+        double dx, dy, dz, q;
+        eval_pair(pos, L, i, j, n1, n2, n3, dx, dy, dz, q);
+        if (q <= ra2) {
+          ++ce;
+          cb += (q <= rb2);
+          bad |= (q < 1e-12);
         }
+      }
   }
   ce = __reduce_add_sync(0xffffffffu, ce);
   cb = __reduce_add_sync(0xffffffffu, cb);
@@ -192,51 +198,58 @@ __global__ void k_fill(int N, const double *__restrict__ pos, const double *__re
   for (int k = 0; k < 9; ++k) L[k] = g.L[k];
   double fi[3] = {frac[3 * i], frac[3 * i + 1], frac[3 * i + 2]};
   int be = row_ptr[i], bb = bond_ptr[i];
-  for (int j0 = a0; j0 < a1; j0 += 32) {
-    int j = j0 + lane;
-    bool act = j < a1;
+  // same (j, n1) slot walk as k_count; slots are in (j, n1) order and each lane's n2, n3
+  // loops are lexicographic, so a warp-ordered scan emits the canonical (j, n1, n2, n3) order
+  const int W = (int)floor(2.0 * g.rw[0]) + 4;
+  const int nslot = (a1 - a0) * W;
+  for (int p0 = 0; p0 < nslot; p0 += 32) {
+    const int p = p0 + lane;
+    int j = 0, n1 = 0, ce = 0, cb = 0;
     Range r;
-    int ce = 0, cb = 0;
+    bool act = p < nslot;
     if (act) {
+      j = a0 + p / W;
       double fj[3] = {frac[3 * j], frac[3 * j + 1], frac[3 * j + 2]};
       r = pair_range(fi, fj, g.rw);
-      for (int n1 = r.lo[0]; n1 <= r.hi[0]; ++n1)
-        for (int n2 = r.lo[1]; n2 <= r.hi[1]; ++n2)
-          for (int n3 = r.lo[2]; n3 <= r.hi[2]; ++n3) {
-            if (i == j && n1 == 0 && n2 == 0 && n3 == 0) continue;
-            double dx, dy, dz, q;
-            eval_pair(pos, L, i, j, n1, n2, n3, dx, dy, dz, q);
-            if (q <= ra2) { ++ce; cb += (q <= rb2); }
-          }
+      n1 = r.lo[0] + p % W;
+      act = n1 <= r.hi[0];
+    }
+    if (act) {
+      for (int n2 = r.lo[1]; n2 <= r.hi[1]; ++n2)
+        for (int n3 = r.lo[2]; n3 <= r.hi[2]; ++n3) {
+          if (i == j && n1 == 0 && n2 == 0 && n3 == 0) continue;
+          double dx, dy, dz, q;
+          eval_pair(pos, L, i, j, n1, n2, n3, dx, dy, dz, q);
+          if (q <= ra2) { ++ce; cb += (q <= rb2); }
+        }
     }
     int te, tb;
     int oe = warp_excl_scan(ce, lane, te);
     int ob = warp_excl_scan(cb, lane, tb);
     if (act && ce > 0) {
       int e = be + oe, b = bb + ob;
-      for (int n1 = r.lo[0]; n1 <= r.hi[0]; ++n1)
-        for (int n2 = r.lo[1]; n2 <= r.hi[1]; ++n2)
-          for (int n3 = r.lo[2]; n3 <= r.hi[2]; ++n3) {
-            if (i == j && n1 == 0 && n2 == 0 && n3 == 0) continue;
-            double dx, dy, dz, q;
-            eval_pair(pos, L, i, j, n1, n2, n3, dx, dy, dz, q);
-            if (q <= ra2) {
-              center[e] = i;
-              nbr[e] = j;
-              img[e] = make_char4((signed char)n1, (signed char)n2, (signed char)n3, 0);
-              double rr = sqrt(q);
-              vec[e] = make_float4((float)dx, (float)dy, (float)dz, (float)rr);
-              vec64[e] = make_double4(dx, dy, dz, rr);
-              if (q <= rb2) {
-                bond_id[e] = b;
-                bond_edge[b] = e;
-                ++b;
-              } else {
-                bond_id[e] = -1;
-              }
-              ++e;
+      for (int n2 = r.lo[1]; n2 <= r.hi[1]; ++n2)
+        for (int n3 = r.lo[2]; n3 <= r.hi[2]; ++n3) {
+          if (i == j && n1 == 0 && n2 == 0 && n3 == 0) continue;
+          double dx, dy, dz, q;
+          eval_pair(pos, L, i, j, n1, n2, n3, dx, dy, dz, q);
+          if (q <= ra2) {
+            center[e] = i;
+            nbr[e] = j;
+            img[e] = make_char4((signed char)n1, (signed char)n2, (signed char)n3, 0);
+            double rr = sqrt(q);
+            vec[e] = make_float4((float)dx, (float)dy, (float)dz, (float)rr);
+            vec64[e] = make_double4(dx, dy, dz, rr);
+            if (q <= rb2) {
+              bond_id[e] = b;
+              bond_edge[b] = e;
+              ++b;
+            } else {
+              bond_id[e] = -1;
             }
+            ++e;
           }
+        }
     }
     be += te;
     bb += tb;
@@ -505,7 +518,7 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
 
     // ---- phase 2 allocation: edge / bond / angle arrays
     size_t sz2 = align_up(4 * E) * 4 + align_up(4 * E) /*img*/ + align_up(16 * E) + align_up(32 * E) + align_up(4 * B) +
-                 align_up(4 * (B + 1)) + align_up(4 * A) * 6 + 256;
+                 align_up(4 * (B + 1)) + align_up(4 * A) * 6 + align_up(16) + 256;
     void *blk2 = nullptr;
     CUDA_OK(cudaMallocAsync(&blk2, sz2, st));
     bl->b = blk2;
@@ -525,6 +538,8 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
     G->angle_e2 = (int32_t *)take(4 * A);
     G->angle_ctr = (int32_t *)take(4 * A);
     G->swap = (int32_t *)take(4 * A);
+    G->d_flag = (int *)take(16);
+    CUDA_OK(cudaMemsetAsync(G->d_flag, 0, 16, st));
 
     ProfScope ps2(ctx, "graph", 0.0, 0.0);
     if (N) {
@@ -538,7 +553,7 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
                                                       G->swap, (int)A);
       check_launch(ctx);
       if (E) {
-        k_rev<<<ceil_div(E, 256), 256, 0, st>>>((int)E, G->center, G->nbr, G->img, G->row_ptr, G->rev, flag);
+        k_rev<<<ceil_div(E, 256), 256, 0, st>>>((int)E, G->center, G->nbr, G->img, G->row_ptr, G->rev, G->d_flag);
         check_launch(ctx);
       }
       k_species<<<1, 32, 4 * (n_species + 1), st>>>((int)N, n_species, G->species, G->species_perm,
@@ -548,24 +563,6 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
       CUDA_OK(cudaMemsetAsync(G->angle_ptr, 0, 4, st));
       CUDA_OK(cudaMemsetAsync(G->species_ptr, 0, 4 * (n_species + 2), st));
     }
-    // per-structure counts on host (from row_ptr etc. at structure boundaries)
-    G->counts_h.assign(4 * (size_t)S, 0);
-    if (S) {
-      int32_t *hrp = (int32_t *)ctx->pinned_get(4 * (N + 1) * 3 + 64);
-      CUDA_OK(cudaMemcpyAsync(hrp, G->row_ptr, 4 * (N + 1), cudaMemcpyDeviceToHost, st));
-      CUDA_OK(cudaMemcpyAsync(hrp + (N + 1), G->bond_ptr, 4 * (N + 1), cudaMemcpyDeviceToHost, st));
-      CUDA_OK(cudaMemcpyAsync(hrp + 2 * (N + 1), G->atom_angle_ptr, 4 * (N + 1), cudaMemcpyDeviceToHost, st));
-      CUDA_OK(cudaMemcpyAsync(hrp + 3 * (N + 1), flag, 4, cudaMemcpyDeviceToHost, st));
-      CUDA_OK(cudaStreamSynchronize(st));
-      if (hrp[3 * (N + 1)] & 8) CHG_THROW(CHG_ERR_GEOMETRY, "internal: reverse edge not found");
-      for (int s = 0; s < S; ++s) {
-        int64_t a0 = atom_ptr[s], a1 = atom_ptr[s + 1];
-        G->counts_h[4 * s + 0] = a1 - a0;
-        G->counts_h[4 * s + 1] = hrp[a1] - hrp[a0];
-        G->counts_h[4 * s + 2] = hrp[N + 1 + a1] - hrp[N + 1 + a0];
-        G->counts_h[4 * s + 3] = hrp[2 * (N + 1) + a1] - hrp[2 * (N + 1) + a0];
-      }
-    }
   } catch (...) {
     if (bl->a) cudaFreeAsync(bl->a, st);
     if (bl->b) cudaFreeAsync(bl->b, st);
@@ -574,6 +571,33 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
     throw;
   }
   return G;
+}
+
+// Per-structure counts (chg_graph_counts) read on demand: the build itself synchronises
+// only once (for the array sizes).  Also surfaces the reverse-edge invariant flag.
+void graph_fill_counts(chg_graph *G) {
+  const int S = G->S;
+  const int64_t N = G->N;
+  chg_ctx *ctx = G->ctx;
+  cudaStream_t st = ctx->stream;
+  G->counts_h.assign(4 * (size_t)S, 0);
+  if (!S) return;
+  int32_t *hrp = (int32_t *)ctx->pinned_get(4 * (N + 1) * 3 + 64);
+  CUDA_OK(cudaMemcpyAsync(hrp, G->row_ptr, 4 * (N + 1), cudaMemcpyDeviceToHost, st));
+  CUDA_OK(cudaMemcpyAsync(hrp + (N + 1), G->bond_ptr, 4 * (N + 1), cudaMemcpyDeviceToHost, st));
+  CUDA_OK(cudaMemcpyAsync(hrp + 2 * (N + 1), G->atom_angle_ptr, 4 * (N + 1), cudaMemcpyDeviceToHost, st));
+  hrp[3 * (N + 1)] = 0;
+  if (G->d_flag) CUDA_OK(cudaMemcpyAsync(hrp + 3 * (N + 1), G->d_flag, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_OK(cudaStreamSynchronize(st));
+  if (hrp[3 * (N + 1)] & 8) CHG_THROW(CHG_ERR_GEOMETRY, "internal: reverse edge not found");
+  for (int s = 0; s < S; ++s) {
+    int64_t a0 = G->atom_ptr_h[s], a1 = G->atom_ptr_h[s + 1];
+    G->counts_h[4 * s + 0] = a1 - a0;
+    G->counts_h[4 * s + 1] = hrp[a1] - hrp[a0];
+    G->counts_h[4 * s + 2] = hrp[N + 1 + a1] - hrp[N + 1 + a0];
+    G->counts_h[4 * s + 3] = hrp[2 * (N + 1) + a1] - hrp[2 * (N + 1) + a0];
+  }
+  G->counts_ready = true;
 }
 
 void destroy_graph_impl(chg_graph *G) {

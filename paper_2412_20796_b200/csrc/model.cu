@@ -170,9 +170,11 @@ void forward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, int train, chg_pred 
   ctx->cur_model = m;
   ctx->cur_wt = nullptr;
   if (ctx->use_tc) {   // K-major weight copy for the tensor-core operands
-    float *wt = ctx->getf("wt", m->P);
+    if (!m->wt) CUDA_OK(cudaMalloc(&m->wt, 4 * (size_t)std::max<int64_t>(m->P, 1)));   // per model: images cache its addresses
+    float *wt = m->wt;
     transpose_params(ctx, m, wt);
     ctx->cur_wt = wt;
+    tc_repack_all(ctx, m);
   }
   // A2 bases (fp64 geometry, fp32 features)
   float *ea_t = F.buf("ea_t", E, 32), *eb_t = F.buf("eb_t", B, 32), *a_t = F.buf("a_t", A, 32);
@@ -554,8 +556,9 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
   sd.d_ne = Bw.scratch("seed_ne", E, 1);
   loss_and_seeds(ctx, g, Bw.act("energy_per_atom"), Bw.act("forces"), Bw.act("stress"), Bw.act("magmom"), lab, *cfg,
                  sd);
-  Bw.wt = ctx->getf("wt", m->P);
-  transpose_params(ctx, m, Bw.wt);
+  if (!m->wt) CUDA_OK(cudaMalloc(&m->wt, 4 * (size_t)std::max<int64_t>(m->P, 1)));
+  Bw.wt = m->wt;
+  if (m->cfg.mlp_precision != 2) transpose_params(ctx, m, Bw.wt);   // TF32 mode: the forward's copy is current
   ctx->use_tc = m->cfg.mlp_precision == 2;
   ctx->cur_model = m;
   ctx->cur_wt = Bw.wt;

@@ -129,11 +129,8 @@ struct TcPlan {
 };
 
 // B image: img[kc][q][n][4] = tf32(W_chunk(n - coff, k = lo + kc·KC - a_k0 + 4q + r))
-__global__ void k_pack_b(const RowGemm g, const TcPlan P, uint32_t *__restrict__ img) {
-  int kc = blockIdx.y;
-  int idx = blockIdx.x * blockDim.x + threadIdx.x;   // over NT * KC
-  if (idx >= P.ntot * KC) return;
-  int n = idx / KC, k = idx % KC;
+__device__ __forceinline__ void pack_elem(const RowGemm &g, const TcPlan &P, uint32_t *__restrict__ img, int kc,
+                                          int n, int k) {
   float v = 0.f;
   for (int c = 0; c < g.nchunk; ++c) {
     const Chunk &C = g.ch[c];
@@ -146,6 +143,31 @@ __global__ void k_pack_b(const RowGemm g, const TcPlan P, uint32_t *__restrict__
   }
   img[(size_t)kc * P.ntot * KC + ((k >> 2) * P.ntot + n) * 4 + (k & 3)] = to_tf32(v);
 }
+
+// every cached image of a model in one launch (blockIdx.y = site), after the weights changed
+struct PackJob {
+  RowGemm g;
+  TcPlan P;
+  uint32_t *img;
+  int nkc;
+};
+__global__ void k_pack_all(const PackJob *__restrict__ jobs) {
+  const PackJob &J = jobs[blockIdx.y];
+  const int per = J.P.ntot * KC, total = J.nkc * per;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const int kc = idx / per, r = idx % per;
+    pack_elem(J.g, J.P, J.img, kc, r / KC, r % KC);
+  }
+}
+
+__global__ void k_pack_b(const RowGemm g, const TcPlan P, uint32_t *__restrict__ img) {
+  int kc = blockIdx.y;
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;   // over NT * KC
+  if (idx >= P.ntot * KC) return;
+  int n = idx / KC, k = idx % KC;
+  pack_elem(g, P, img, kc, n, k);
+}
+
 
 // ---------------------------------------------------------------------------
 // warp-specialised persistent kernel
@@ -667,7 +689,54 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols) : "memory");
 }
 
+struct TcCache {
+  std::map<std::string, int> index;
+  std::vector<PackJob> jobs;
+  std::vector<uint64_t> gen;     // forward generation the image was packed for
+  uint64_t cur_gen = 0;
+  PackJob *d_jobs = nullptr;
+  size_t d_cap = 0;
+  bool dirty = false;
+};
+
 }  // namespace
+
+// start of a forward: new generation; re-pack every cached image of the model in one launch
+void tc_repack_all(chg_ctx *ctx, chg_model *m) {
+  TcCache *c = (TcCache *)m->tc_cache;
+  if (!c) {
+    c = new TcCache();
+    m->tc_cache = c;
+  }
+  ++c->cur_gen;
+  if (c->jobs.empty()) return;
+  if (c->dirty || c->d_cap < c->jobs.size()) {
+    if (c->d_cap < c->jobs.size()) {
+      if (c->d_jobs) CUDA_OK(cudaFree(c->d_jobs));
+      c->d_cap = c->jobs.size() + 8;
+      CUDA_OK(cudaMalloc(&c->d_jobs, c->d_cap * sizeof(PackJob)));
+    }
+    CUDA_OK(cudaMemcpyAsync(c->d_jobs, c->jobs.data(), c->jobs.size() * sizeof(PackJob), cudaMemcpyHostToDevice,
+                            ctx->stream));
+    CUDA_OK(cudaStreamSynchronize(ctx->stream));   // pageable source: keep it simple, happens once per new site
+    c->dirty = false;
+  }
+  double bytes = 0;
+  for (auto &J : c->jobs) bytes += (double)J.nkc * J.P.ntot * KC * 8.0;
+  ProfScope ps(ctx, "tc_pack", 0.0, bytes);
+  k_pack_all<<<dim3(32, (unsigned)c->jobs.size()), 256, 0, ctx->stream>>>(c->d_jobs);
+  check_launch(ctx);
+  for (auto &g : c->gen) g = c->cur_gen;
+}
+
+void tc_cache_free(chg_model *m) {
+  TcCache *c = (TcCache *)m->tc_cache;
+  if (!c) return;
+  for (auto &J : c->jobs) cudaFree(J.img);
+  if (c->d_jobs) cudaFree(c->d_jobs);
+  delete c;
+  m->tc_cache = nullptr;
+}
 
 // Returns false if the GEMM does not fit this path (caller uses the SIMT kernel).
 bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
@@ -707,8 +776,44 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   }
   double cols = 0;
   for (int c = 0; c < g.nchunk; ++c) cols += g.ch[c].ncols;
-  uint32_t *img = (uint32_t *)ctx->get("tc_bimg", (size_t)nkc * P.ntot * KC * 4);
-  {
+  // weight image: cached per (model, call site); all of a model's images are re-packed in
+  // one launch at the start of each forward (tc_repack_all) — only a new site packs here
+  uint32_t *img = nullptr;
+  TcCache *cache = ctx->cur_model ? (TcCache *)ctx->cur_model->tc_cache : nullptr;
+  std::string key;
+  if (cache) {
+    char kb[64];
+    key = g.tag ? g.tag : "";
+    for (int c = 0; c < g.nchunk; ++c)
+      for (int b = 0; b < g.ch[c].nwb; ++b) {
+        snprintf(kb, sizeof(kb), "|%p", (const void *)g.ch[c].Wk[b]);
+        key += kb;
+      }
+    auto it = cache->index.find(key);
+    if (it != cache->index.end() && cache->gen[it->second] == cache->cur_gen) img = cache->jobs[it->second].img;
+  }
+  if (!img) {
+    const size_t bytes = (size_t)nkc * P.ntot * KC * 4;
+    if (cache) {
+      auto it = cache->index.find(key);
+      int id;
+      if (it == cache->index.end()) {
+        id = (int)cache->jobs.size();
+        PackJob J{};
+        J.g = g; J.P = P; J.nkc = nkc;
+        CUDA_OK(cudaMalloc(&J.img, bytes));
+        cache->jobs.push_back(J);
+        cache->gen.push_back(0);
+        cache->index[key] = id;
+        cache->dirty = true;
+      } else {
+        id = it->second;
+      }
+      img = cache->jobs[id].img;
+      cache->gen[id] = cache->cur_gen;
+    } else {
+      img = (uint32_t *)ctx->get("tc_bimg", bytes);
+    }
     ProfScope ps(ctx, "tc_pack", 0.0, (double)nkc * P.ntot * KC * 8.0);
     dim3 grid(ceil_div((int64_t)P.ntot * KC, 256), nkc);
     k_pack_b<<<grid, 256, 0, ctx->stream>>>(g, P, img);
