@@ -201,7 +201,62 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-__global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const RowGemm g, const TcPlan P,
+// epilogue of one 32x32 block (lane = column n, rows row0..row0+nrows): v = acc + b,
+// optional pre-store, SiLU, ·SiLU'(mul), + resid.  Loads of a 16-row half are issued first.
+template <bool PRE, bool MUL, bool RESID, bool ACT>
+__device__ __forceinline__ void epi_rows(const Chunk &C, const float *stile, int lane, int row0, int nrows, int n,
+                                         float bn) {
+#pragma unroll
+  for (int h = 0; h < 32; h += 16) {
+    float mv[16], rv[16];
+    if (MUL || RESID) {
+#pragma unroll
+      for (int rr = 0; rr < 16; ++rr) {
+        const size_t mr = (size_t)(row0 + h + rr);
+        const bool ok = h + rr < nrows;
+        if (MUL) mv[rr] = ok ? C.mul[mr * C.ldm + n] : 0.f;
+        if (RESID) rv[rr] = ok ? C.resid[mr * C.ldr + n] : 0.f;
+      }
+    }
+    if (h + 16 <= nrows) {
+#pragma unroll
+      for (int rr = 0; rr < 16; ++rr) {
+        const size_t mr = (size_t)(row0 + h + rr);
+        float v = stile[(h + rr) * 33 + lane] + bn;
+        if (PRE) C.pre[mr * C.ldp + n] = v;
+        if (ACT) v = siluf_(v);
+        if (MUL) v *= dsiluf_(mv[rr]);
+        if (RESID) v += rv[rr];
+        C.out[mr * C.ldo + n] = v;
+      }
+    } else {
+      for (int rr = 0; rr < 16 && h + rr < nrows; ++rr) {
+        const size_t mr = (size_t)(row0 + h + rr);
+        float v = stile[(h + rr) * 33 + lane] + bn;
+        if (PRE) C.pre[mr * C.ldp + n] = v;
+        if (ACT) v = siluf_(v);
+        if (MUL) v *= dsiluf_(mv[rr]);
+        if (RESID) v += rv[rr];
+        C.out[mr * C.ldo + n] = v;
+      }
+    }
+  }
+}
+
+__device__ __noinline__ void epi_rows_any(const Chunk &C, int act, const float *stile, int lane, int row0, int nrows,
+                                          int n, float bn) {
+  for (int rr = 0; rr < nrows; ++rr) {
+    const size_t mr = (size_t)(row0 + rr);
+    float v = stile[rr * 33 + lane] + bn;
+    if (C.pre) C.pre[mr * C.ldp + n] = v;
+    if (act == 1) v = siluf_(v);
+    if (C.mul) v *= dsiluf_(C.mul[mr * C.ldm + n]);
+    if (C.resid) v += C.resid[mr * C.ldr + n];
+    C.out[mr * C.ldo + n] = v;
+  }
+}
+
+__global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_constant__ RowGemm g, const TcPlan P,
                                                                const uint32_t *__restrict__ bimg, int ntiles,
                                                                int skip) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -407,31 +462,15 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const RowGemm g, c
           for (int qq = 0; qq < 32; ++qq) stile[lane * 33 + qq] = __uint_as_float(r[qq]);
           __syncwarp();
           const int n = j0 + lane;
-          const bool col_ok = n < C.ncols;
-          const float bn = (C.bias && col_ok) ? __ldg(C.bias + n) : 0.f;
-          if (col_ok) {
-            // 16 rows at a time: issue every dependent load first (out may alias resid)
-#pragma unroll
-            for (int h = 0; h < 32; h += 16) {
-              float mv[16], rv[16];
-#pragma unroll
-              for (int rr = 0; rr < 16; ++rr) {
-                const size_t mr = (size_t)(row0 + h + rr);
-                const bool ok = h + rr < nrows;
-                mv[rr] = (C.mul && ok) ? C.mul[mr * C.ldm + n] : 0.f;
-                rv[rr] = (C.resid && ok) ? C.resid[mr * C.ldr + n] : 0.f;
-              }
-#pragma unroll
-              for (int rr = 0; rr < 16; ++rr) {
-                if (h + rr >= nrows) break;
-                const size_t mr = (size_t)(row0 + h + rr);
-                float v = stile[(h + rr) * 33 + lane] + bn;
-                if (C.pre) C.pre[mr * C.ldp + n] = v;
-                if (g.act == 1) v = siluf_(v);
-                if (C.mul) v *= dsiluf_(mv[rr]);
-                v += rv[rr];
-                C.out[mr * C.ldo + n] = v;
-              }
+          if (n < C.ncols) {
+            // flags are uniform per 32x32 block: one specialised row loop per combination
+            const float bn = C.bias ? __ldg(C.bias + n) : 0.f;
+            const int code = (C.pre ? 1 : 0) | (C.mul ? 2 : 0) | (C.resid ? 4 : 0) | (g.act == 1 ? 8 : 0);
+            switch (code) {
+              case 0: epi_rows<false, false, false, false>(C, stile, lane, row0, nrows, n, bn); break;
+              case 2: epi_rows<false, true, false, false>(C, stile, lane, row0, nrows, n, bn); break;
+              case 4: epi_rows<false, false, true, false>(C, stile, lane, row0, nrows, n, bn); break;
+              default: epi_rows_any(C, g.act, stile, lane, row0, nrows, n, bn); break;
             }
           }
           __syncwarp();
