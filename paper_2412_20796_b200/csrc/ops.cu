@@ -123,8 +123,18 @@ __global__ void k_gate_fwd(int64_t rows, const float *__restrict__ y, int ldy, G
   int l = threadIdx.x & 31;
   if (row >= rows) return;
   int c0 = 2 * l;
+  // every operand of the row is requested before any arithmetic (one latency, not three)
   float2 yc = *(const float2 *)(y + row * ldy + c0);
   float2 yg = *(const float2 *)(y + row * ldy + 64 + c0);
+  float2 w1 = make_float2(0.f, 0.f), w2 = make_float2(0.f, 0.f);
+  if (mode == GATE_MUL_W) {
+    w1 = *(const float2 *)(w + row * 64 + c0);
+  } else if (mode == GATE_MUL_W1W2) {
+    w1 = *(const float2 *)(w + (int64_t)i1[row] * 64 + c0);
+    w2 = *(const float2 *)(w + (int64_t)i2[row] * 64 + c0);
+  } else {
+    w1 = *(const float2 *)(resid + row * 64 + c0);
+  }
   RowStats sc = ln_stats(yc.x, yc.y), sg = ln_stats(yg.x, yg.y);
   float2 gc = *(const float2 *)(ln.gc + c0), bc = *(const float2 *)(ln.bc + c0);
   float2 gg = *(const float2 *)(ln.gg + c0), bg = *(const float2 *)(ln.bg + c0);
@@ -133,15 +143,11 @@ __global__ void k_gate_fwd(int64_t rows, const float *__restrict__ y, int ldy, G
   float p0 = sigmoidf_(ng0) * siluf_(nc0), p1 = sigmoidf_(ng1) * siluf_(nc1);
   float2 o;
   if (mode == GATE_MUL_W) {
-    float2 wv = *(const float2 *)(w + row * 64 + c0);
-    o = make_float2(p0 * wv.x, p1 * wv.y);
+    o = make_float2(p0 * w1.x, p1 * w1.y);
   } else if (mode == GATE_MUL_W1W2) {
-    float2 w1 = *(const float2 *)(w + (int64_t)i1[row] * 64 + c0);
-    float2 w2 = *(const float2 *)(w + (int64_t)i2[row] * 64 + c0);
     o = make_float2(p0 * w1.x * w2.x, p1 * w1.y * w2.y);
   } else {
-    float2 r = *(const float2 *)(resid + row * 64 + c0);
-    o = make_float2(r.x + p0, r.y + p1);
+    o = make_float2(w1.x + p0, w1.y + p1);
   }
   *(float2 *)(out + row * 64 + c0) = o;
 }
