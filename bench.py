@@ -63,9 +63,10 @@ def kernel_of(tag: str, precision: str) -> str:
         return "k_rowgemm"
     if tag in WG_TAGS:
         return "k_wgrad"
-    if tag in ("head_mlp_f", "head_mlp_b", "head_reduce", "species_grad"):
+    if tag in ("head_mlp_f", "head_mlp_b", "head_reduce", "species_grad", "proj_basis", "proj_bwd", "proj_reduce"):
         return {"head_mlp_f": "k_head_fwd", "head_mlp_b": "k_head_bwd", "head_reduce": "k_head_reduce",
-                "species_grad": "k_species_grad"}[tag]
+                "species_grad": "k_species_grad", "proj_basis": "k_proj_fwd", "proj_bwd": "k_proj_bwd",
+                "proj_reduce": "k_proj_reduce"}[tag]
     return {"segsum": "k_segsum", "gate_fwd": "k_gate_fwd", "gate_bwd": "k_gate_bwd", "wgrad_reduce": "k_wgrad_reduce",
             "tc_pack": "k_pack_b"}.get(tag, tag)
 

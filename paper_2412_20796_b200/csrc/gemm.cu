@@ -53,8 +53,8 @@ __device__ __forceinline__ float loadW(const Chunk &c, int k, int n) {
 
 // TM rows per CTA (128 for large M; 32 when few CTAs would be launched),
 // 256 threads = 16 (x 4 columns) x 16 (x TM/16 rows)
-template <bool VEC, int TM>
-__global__ void __launch_bounds__(256) k_rowgemm(const RowGemm g) {
+template <bool VEC, int TM, int TK = 32>
+__global__ void __launch_bounds__(256) k_rowgemm(const __grid_constant__ RowGemm g) {
   constexpr int RPT = TM / 16;
   __shared__ __align__(16) float As[TK][TM + 4];
   __shared__ __align__(16) float Ws[TK][TN];
@@ -70,8 +70,10 @@ __global__ void __launch_bounds__(256) k_rowgemm(const RowGemm g) {
   for (int k0 = 0; k0 < g.K; k0 += TK) {
     if (VEC) {
 #pragma unroll
-      for (int i = 0; i < TM / 32; ++i) {
-        int r = (t >> 3) + 32 * i, c4 = t & 7;
+      for (int i = 0; i < (TM * TK / 4 + 255) / 256; ++i) {
+        const int e = t + 256 * i;
+        if (TM * TK / 4 % 256 != 0 && e >= TM * TK / 4) break;
+        int r = e / (TK / 4), c4 = e % (TK / 4);
         int m = m0 + r, kk = k0 + 4 * c4;
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if (m < g.M && kk < g.K) v = loadA4(g.A, m, c.a_k0 + kk);
@@ -373,7 +375,19 @@ void rowgemm(chg_ctx *ctx, const RowGemm &g) {
   ProfScope ps(ctx, g.tag ? g.tag : "rowgemm", 2.0 * g.M * (double)g.K * cols,
                gemm_a_bytes(g.A, g.M, lo, hi) + (double)g.M * 4.0 * outb + 4.0 * wb);
   const bool small = (int64_t)ceil_div(g.M, TM) * g.nchunk < 2 * 148;
-  if (small) {
+  if (small && g.K > 32) {
+    // few rows: short tiles and the whole K = 64 in one smem stage (one load latency, not two)
+    const bool tiny = (int64_t)ceil_div(g.M, 32) * g.nchunk < 148;
+    if (tiny) {
+      dim3 grid(ceil_div(g.M, 16), g.nchunk);
+      if (vec) k_rowgemm<true, 16, 64><<<grid, 256, 0, ctx->stream>>>(g);
+      else k_rowgemm<false, 16, 64><<<grid, 256, 0, ctx->stream>>>(g);
+    } else {
+      dim3 grid(ceil_div(g.M, 32), g.nchunk);
+      if (vec) k_rowgemm<true, 32, 64><<<grid, 256, 0, ctx->stream>>>(g);
+      else k_rowgemm<false, 32, 64><<<grid, 256, 0, ctx->stream>>>(g);
+    }
+  } else if (small) {
     dim3 grid(ceil_div(g.M, 32), g.nchunk);
     if (vec) k_rowgemm<true, 32><<<grid, 256, 0, ctx->stream>>>(g);
     else k_rowgemm<false, 32><<<grid, 256, 0, ctx->stream>>>(g);

@@ -130,15 +130,17 @@ void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float
   SegSrc s;
   s.in = q; s.ptr = g->angle_ptr; s.rows = A;
   segsum(ctx, B, aggb, 64, 0, 1, &s, "segsum_bc");      // Σ over angles with first bond b (empty -> 0)
-  {  // e' = e + 𝓛_e(agg) on all E edges (non-bond rows gather a zero row, Q16)
+  {  // e' = e + 𝓛_e(agg) on all E edges (Q16): the product only for the B bond rows, then every
+     // edge gets its bond row (or nothing) + the bias
+    float *tmp = ctx->getf("bc_out_tmp", (size_t)std::max<int64_t>(B, 1) * 64);
     RowGemm G;
-    G.A.seg[0] = aseg(aggb, 64, 64, g->bond_id, B);
+    G.A.seg[0] = aseg(aggb, 64, 64);
     G.A.nseg = 1;
-    G.M = (int)E; G.K = 64; G.nchunk = 1;
-    G.ch[0] = chunk1(m->p(bp + ".out.W"), 64, 64, m->p(bp + ".out.b"), e_out, 64);
-    G.ch[0].resid = e; G.ch[0].ldr = 64;
+    G.M = (int)B; G.K = 64; G.nchunk = 1;
+    G.ch[0] = chunk1(m->p(bp + ".out.W"), 64, 64, nullptr, tmp, 64);
     G.tag = "bc_fout";
     rowgemm(ctx, G);
+    edge_update(ctx, E, e, m->p(bp + ".out.b"), g->bond_id, tmp, e_out);
   }
   if (angle_branch && A > 0)   // a' = a + φ_a
     gate_fwd(ctx, A, ya, 128, F.ln(ap), GATE_RESID, nullptr, nullptr, nullptr, a, a_out);
@@ -176,38 +178,21 @@ void forward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, int train, chg_pred 
     ctx->cur_wt = wt;
     tc_repack_all(ctx, m);
   }
-  // A2 bases (fp64 geometry, fp32 features)
+  // A2 + A3: fused basis expansion and projection (Eq. 2; no bias, Q5); the bases (and
+  // ∂basis/∂f in train mode) are saved for the backward
   float *ea_t = F.buf("ea_t", E, 32), *eb_t = F.buf("eb_t", B, 32), *a_t = F.buf("a_t", A, 32);
-  basis_radial(ctx, E, g->vec64, nullptr, m->p("rbf_a.freq"), g->r_atom, p, ea_t);
-  basis_radial(ctx, B, g->vec64, g->bond_edge, m->p("rbf_b.freq"), g->r_bond, p, eb_t);
-  basis_angle(ctx, A, g->vec64, g->angle_e1, g->angle_e2, a_t);
-  // A3 embedding and projections (Eq. 2; no bias, Q5)
+  float *ea_g = train ? F.buf("ea_g", E, 32) : nullptr, *eb_g = train ? F.buf("eb_g", B, 32) : nullptr;
   std::vector<float *> v(T + 2), e(T + 1), a(T);
   v[0] = F.buf("v0", N, 64);
   embed_fwd(ctx, N, g->species, m->p("embed.W"), v[0]);
   e[0] = F.buf("e0", E, 64);
   float *ea = F.buf("ea", E, 64), *eb = F.buf("eb", B, 64);
   a[0] = F.buf("a0", A, 64);
-  {
-    RowGemm G;
-    G.A.seg[0] = aseg(ea_t, 32, 32);
-    G.A.nseg = 1;
-    G.M = (int)E; G.K = CHG_K; G.nchunk = 2;
-    G.ch[0] = chunk1(m->p("proj.W0"), 64, CHG_K, nullptr, e[0], 64);
-    G.ch[1] = chunk1(m->p("proj.Wa"), 64, CHG_K, nullptr, ea, 64);
-    G.tag = "proj_f";
-    rowgemm(ctx, G);
-    G.A.seg[0] = aseg(eb_t, 32, 32);
-    G.M = (int)B; G.nchunk = 1;
-    G.ch[0] = chunk1(m->p("proj.Wb"), 64, CHG_K, nullptr, eb, 64);
-    G.tag = "proj_f";
-    rowgemm(ctx, G);
-    G.A.seg[0] = aseg(a_t, 32, 32);
-    G.M = (int)A;
-    G.ch[0] = chunk1(m->p("proj.Wtheta"), 64, CHG_K, nullptr, a[0], 64);
-    G.tag = "proj_f";
-    rowgemm(ctx, G);
-  }
+  proj_radial_fwd(ctx, E, g->vec64, nullptr, m->p("rbf_a.freq"), g->r_atom, p, m->p("proj.W0"), m->p("proj.Wa"),
+                  e[0], ea, ea_t, ea_g);
+  proj_radial_fwd(ctx, B, g->vec64, g->bond_edge, m->p("rbf_b.freq"), g->r_bond, p, m->p("proj.Wb"), nullptr, eb,
+                  nullptr, eb_t, eb_g);
+  proj_angle_fwd(ctx, A, g->vec64, g->angle_e1, g->angle_e2, m->p("proj.Wtheta"), a[0], a_t);
   // A4/A5 interaction blocks
   for (int t = 0; t < T; ++t) {
     v[t + 1] = F.buf("v" + std::to_string(t + 1), N, 64);
@@ -330,13 +315,7 @@ void bc_bwd_head(Bwd &Bw, int t, const float *de, float *daggb) {
   wg.dst[0].W = Bw.G(pre + ".out.W"); wg.dst[0].ldw = 64;
   wg.tag = "bc_out_wg";
   wgrad(Bw.ctx, wg);
-  WGrad wb;   // db_out = Σ over ALL edges of de
-  wb.A.nseg = 0;
-  wb.M = (int)g->E; wb.K = 0;
-  wb.D = de; wb.ldd = 64; wb.N = 64; wb.bias = 1;
-  wb.dst[0].b = Bw.G(pre + ".out.b");
-  wb.tag = "bc_outb_wg";
-  wgrad(Bw.ctx, wb);
+  colsum(Bw.ctx, g->E, de, Bw.G(pre + ".out.b"));   // db_out = Σ over ALL edges of de
 }
 
 void ac_bwd_body(Bwd &Bw, int t, const float *v, const float *e, const float *ea, const float *dagg, float *dv,
@@ -610,48 +589,13 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
   }
   // embedding (rows of W_v gathered by species -> grouped sum, no atomics)
   species_grad(ctx, N, m->cfg.n_species, g->species_ptr, g->species_perm, dv, Bw.G("embed.W"));
-  // projections (Eq. 2) and trainable frequencies
-  auto proj_grad = [&](const float *basis, int64_t rows, const float *d, const char *W) {
-    WGrad wg;
-    wg.A.seg[0] = aseg(basis, 32, 32);
-    wg.A.nseg = 1;
-    wg.M = (int)rows; wg.K = CHG_K;
-    wg.D = d; wg.ldd = 64; wg.N = 64; wg.bias = 0;
-    wg.dst[0].W = Bw.G(W); wg.dst[0].ldw = 64;
-    wg.tag = "proj_wg";
-    wgrad(ctx, wg);
-  };
-  const float *ea_t = Bw.act("ea_t"), *eb_t = Bw.act("eb_t"), *a_t = Bw.act("a_t");
-  proj_grad(ea_t, E, de, "proj.W0");
-  proj_grad(ea_t, E, dea, "proj.Wa");
-  proj_grad(eb_t, B, deb, "proj.Wb");
-  proj_grad(a_t, A, da, "proj.Wtheta");
-  {
-    float *dbt = Bw.scratch("d_basis", std::max(E, B), 32);
-    RowGemm G;
-    G.A.seg[0] = aseg(de, 64, 64);
-    G.A.seg[1] = aseg(dea, 64, 64);
-    G.A.nseg = 2;
-    G.M = (int)E; G.K = 128;
-    Chunk &C = G.ch[0];
-    C.W[0] = Bw.WT("proj.W0"); C.ldw[0] = CHG_K;
-    C.W[1] = Bw.WT("proj.Wa"); C.ldw[1] = CHG_K;
-    C.wk0[0] = 0; C.wk0[1] = 64; C.wk0[2] = 128; C.nwb = 2;
-    C.ncols = CHG_K; C.out = dbt; C.ldo = 32;
-    G.tag = "dbasis";
-    rowgemm(ctx, G);
-    basis_freq_grad(ctx, E, g->vec64, nullptr, m->p("rbf_a.freq"), g->r_atom, m->cfg.envelope_p, dbt,
-                    Bw.G("rbf_a.freq"));
-    RowGemm H;
-    H.A.seg[0] = aseg(deb, 64, 64);
-    H.A.nseg = 1;
-    H.M = (int)B; H.K = 64;
-    H.ch[0] = chunk1(Bw.WT("proj.Wb"), CHG_K, 64, nullptr, dbt, 32, CHG_K);
-    H.tag = "dbasis";
-    rowgemm(ctx, H);
-    basis_freq_grad(ctx, B, g->vec64, g->bond_edge, m->p("rbf_b.freq"), g->r_bond, m->cfg.envelope_p, dbt,
-                    Bw.G("rbf_b.freq"));
-  }
+  // projections (Eq. 2) and trainable frequencies, from the saved bases (proj.cu)
+  proj_bwd(ctx, E, Bw.act("ea_t"), Bw.act("ea_g"), de, dea, m->p("proj.W0"), m->p("proj.Wa"), Bw.G("proj.W0"),
+           Bw.G("proj.Wa"), Bw.G("rbf_a.freq"));
+  proj_bwd(ctx, B, Bw.act("eb_t"), Bw.act("eb_g"), deb, nullptr, m->p("proj.Wb"), nullptr, Bw.G("proj.Wb"), nullptr,
+           Bw.G("rbf_b.freq"));
+  proj_bwd(ctx, A, Bw.act("a_t"), nullptr, da, nullptr, m->p("proj.Wtheta"), nullptr, Bw.G("proj.Wtheta"), nullptr,
+           nullptr);
   if (loss_out) {
     double *h = (double *)ctx->pinned_get(64);
     CUDA_OK(cudaMemcpyAsync(h, ctx->d_loss, 5 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));

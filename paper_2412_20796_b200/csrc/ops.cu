@@ -315,6 +315,45 @@ __global__ void __launch_bounds__(64) k_species_grad2(const int32_t *__restrict_
   dW[(int64_t)z * 64 + col] += acc;
 }
 
+// e' = e + 𝓛_e(agg) for every edge (Eq. 5, Q16): the 64x64 product is computed only for the
+// B bond rows (tmp), non-bond edges get the bias alone; same rounding order as the fused
+// epilogue ((x·W + b) + e).
+__global__ void k_edge_update(int64_t E, const float4 *__restrict__ e, const float *__restrict__ bias,
+                              const int32_t *__restrict__ bond_id, const float4 *__restrict__ tmp,
+                              float4 *__restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;   // float4 index
+  if (i >= E * 16) return;
+  const int64_t row = i >> 4;
+  const int c = (int)(i & 15);
+  const int b = __ldg(bond_id + row);
+  const float4 bb = make_float4(__ldg(bias + 4 * c), __ldg(bias + 4 * c + 1), __ldg(bias + 4 * c + 2),
+                                __ldg(bias + 4 * c + 3));   // flat-parameter offsets need not be 16-B aligned
+  const float4 ev = __ldg(e + i);
+  float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (b >= 0) x = __ldg(tmp + (int64_t)b * 16 + c);
+  out[i] = make_float4((x.x + bb.x) + ev.x, (x.y + bb.y) + ev.y, (x.z + bb.z) + ev.z, (x.w + bb.w) + ev.w);
+}
+
+// column sums of a [rows, 64] matrix: per-block partials (fixed row ranges), reduced in block order
+__global__ void __launch_bounds__(256) k_colsum_partial(int64_t rows, int64_t rpb, const float *__restrict__ D,
+                                                        float *__restrict__ part) {
+  __shared__ float4 sh[16][16];
+  const int t = threadIdx.x, c = t & 15, rl = t >> 4;
+  const int64_t r0 = blockIdx.x * rpb, r1 = min(rows, r0 + rpb);
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t r = r0 + rl; r < r1; r += 16) {
+    const float4 v = __ldg((const float4 *)(D + r * 64) + c);
+    s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+  }
+  sh[rl][c] = s;
+  __syncthreads();
+  if (t < 16) {
+    float4 a = sh[0][t];
+    for (int k = 1; k < 16; ++k) { a.x += sh[k][t].x; a.y += sh[k][t].y; a.z += sh[k][t].z; a.w += sh[k][t].w; }
+    ((float4 *)(part + blockIdx.x * 64))[t] = a;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // heads
 // ---------------------------------------------------------------------------
@@ -576,6 +615,27 @@ void species_grad(chg_ctx *ctx, int64_t N, int n_species, const int32_t *species
   k_species_grad1<<<dim3(maxc, n_species), 64, 0, ctx->stream>>>(species_ptr, species_perm, dv, part, maxc);
   check_launch(ctx);
   k_species_grad2<<<n_species, 64, 0, ctx->stream>>>(species_ptr, part, maxc, dW);
+  check_launch(ctx);
+}
+
+void edge_update(chg_ctx *ctx, int64_t E, const float *e, const float *bias, const int32_t *bond_id, const float *tmp,
+                 float *out) {
+  if (E <= 0) return;
+  ProfScope ps(ctx, "edge_update", 0.0, E * (512.0 + 4.0) + 0.0);
+  k_edge_update<<<ceil_div(E * 16, 256), 256, 0, ctx->stream>>>(E, (const float4 *)e, bias, bond_id,
+                                                                 (const float4 *)tmp, (float4 *)out);
+  check_launch(ctx);
+}
+
+void colsum(chg_ctx *ctx, int64_t rows, const float *D, float *grad) {
+  if (rows <= 0) return;
+  const int64_t rpb = std::max<int64_t>(64, (rows + 295) / 296);
+  const int nb = ceil_div(rows, rpb);
+  float *part = ctx->getf("colsum_part", (size_t)nb * 64);
+  ProfScope ps(ctx, "colsum", 0.0, rows * 256.0 + nb * 512.0);
+  k_colsum_partial<<<nb, 256, 0, ctx->stream>>>(rows, rpb, D, part);
+  check_launch(ctx);
+  k_reduce_cols<<<2, 256, 0, ctx->stream>>>(nb, 64, 64, part, grad);
   check_launch(ctx);
 }
 

@@ -47,6 +47,24 @@ void head_mlp_fwd(chg_ctx *ctx, int nl, int nout, const float *X, int64_t rows, 
 void head_mlp_bwd(chg_ctx *ctx, int nl, int nout, const float *X, int64_t rows, const float *P, float *const *Z,
                   const float *dout, float *G, float *dX);
 
+// fused basis + projection (proj.cu): radial sRBF (one or two 31x64 projections; basis and
+// ∂basis/∂f saved [rows][32]) and Fourier angle basis; backward from the saved bases:
+// dW (+)= basisᵀ·dE into G0/G1 and ∂L/∂f (+)= Σ_c W ⊙ (∂basis/∂f)ᵀ·dE (dbdf == nullptr: no freqs)
+void proj_radial_fwd(chg_ctx *ctx, int64_t rows, const double4 *vec, const int32_t *eor, const float *freq,
+                     double rc, int p, const float *W0, const float *W1, float *out0, float *out1, float *basis,
+                     float *dbdf);
+void proj_angle_fwd(chg_ctx *ctx, int64_t rows, const double4 *vec, const int32_t *e1, const int32_t *e2,
+                    const float *W, float *out, float *basis);
+void proj_bwd(chg_ctx *ctx, int64_t rows, const float *basis, const float *dbdf, const float *dE0, const float *dE1,
+              const float *W0, const float *W1, float *G0, float *G1, float *dfreq);
+
+// e' = e + (tmp[bond_id] or 0) + bias on all E edges (bond-conv output linear, Eq. 5 / Q16);
+// float4 rows (64 floats), tmp holds the product for the B bond rows
+void edge_update(chg_ctx *ctx, int64_t E, const float *e, const float *bias, const int32_t *bond_id, const float *tmp,
+                 float *out);
+// grad[0..63] += column sums of D [rows, 64] (deterministic)
+void colsum(chg_ctx *ctx, int64_t rows, const float *D, float *grad);
+
 // heads (Eq. 7, Eq. 9)
 void heads_forces(chg_ctx *ctx, const chg_graph *g, const float *n_e, float *forces);
 void heads_struct(chg_ctx *ctx, const chg_graph *g, const float *e_atom, const float *M9, float *energy,
