@@ -167,6 +167,9 @@ void chg_ctx_destroy(chg_ctx *ctx) {
   if (ctx->d_flag) cudaFree(ctx->d_flag);
   if (ctx->nccl_comm) ncclCommDestroy((ncclComm_t)ctx->nccl_comm);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }

@@ -47,6 +47,10 @@ struct chg_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  // second stream for the concurrent bond-conv branch of a forward layer (Eq. 11 makes the
+  // atom and bond/angle updates of a layer independent)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::string err;
   int64_t launches = 0;
   // named device workspaces (grow-only, stream-ordered reallocation)

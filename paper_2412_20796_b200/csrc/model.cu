@@ -194,13 +194,39 @@ void forward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, int train, chg_pred 
                   nullptr, eb_t, eb_g);
   proj_angle_fwd(ctx, A, g->vec64, g->angle_e1, g->angle_e2, m->p("proj.Wtheta"), a[0], a_t);
   // A4/A5 interaction blocks
+  // Eq. 11: atom conv (writes v^{t+1}) and bond conv + angle update (write e^{t+1}, a^{t+1})
+  // of a layer read only layer-t features, so they run concurrently: the bond branch on a
+  // second stream forked from / joined into the library stream (CHG_SERIAL=1 disables)
+  static const bool serial = getenv("CHG_SERIAL") != nullptr;
+  if (!serial && !ctx->side) {
+    CUDA_OK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    CUDA_OK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+  }
   for (int t = 0; t < T; ++t) {
     v[t + 1] = F.buf("v" + std::to_string(t + 1), N, 64);
     e[t + 1] = F.buf("e" + std::to_string(t + 1), E, 64);
     bool ab = t + 1 < T;
     if (ab) a[t + 1] = F.buf("a" + std::to_string(t + 1), A, 64);
+    if (serial) {
+      atom_conv_fwd(F, t, v[t], e[t], ea, v[t + 1]);
+      bond_conv_fwd(F, t, ab, v[t], e[t], a[t], eb, e[t + 1], ab ? a[t + 1] : nullptr);
+      continue;
+    }
+    cudaStream_t main_stream = ctx->stream;
+    CUDA_OK(cudaEventRecord(ctx->ev_fork, main_stream));
+    CUDA_OK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+    ctx->stream = ctx->side;
+    try {
+      bond_conv_fwd(F, t, ab, v[t], e[t], a[t], eb, e[t + 1], ab ? a[t + 1] : nullptr);
+    } catch (...) {
+      ctx->stream = main_stream;
+      throw;
+    }
+    ctx->stream = main_stream;
+    CUDA_OK(cudaEventRecord(ctx->ev_join, ctx->side));
     atom_conv_fwd(F, t, v[t], e[t], ea, v[t + 1]);
-    bond_conv_fwd(F, t, ab, v[t], e[t], a[t], eb, e[t + 1], ab ? a[t + 1] : nullptr);
+    CUDA_OK(cudaStreamWaitEvent(main_stream, ctx->ev_join, 0));
   }
   v[T + 1] = F.buf("v" + std::to_string(T + 1), N, 64);
   atom_conv_fwd(F, T, v[T], e[T], ea, v[T + 1]);
