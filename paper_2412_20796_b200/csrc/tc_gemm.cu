@@ -206,39 +206,40 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 template <bool PRE, bool MUL, bool RESID, bool ACT>
 __device__ __forceinline__ void epi_rows(const Chunk &C, const float *stile, int lane, int row0, int nrows, int n,
                                          float bn) {
+  // every dependent load of the block (32 rows) is issued before the first use: one memory
+  // latency per 32x32 block
+  float mv[32], rv[32];
+  if (MUL || RESID) {
 #pragma unroll
-  for (int h = 0; h < 32; h += 16) {
-    float mv[16], rv[16];
-    if (MUL || RESID) {
-#pragma unroll
-      for (int rr = 0; rr < 16; ++rr) {
-        const size_t mr = (size_t)(row0 + h + rr);
-        const bool ok = h + rr < nrows;
-        if (MUL) mv[rr] = ok ? C.mul[mr * C.ldm + n] : 0.f;
-        if (RESID) rv[rr] = ok ? C.resid[mr * C.ldr + n] : 0.f;
-      }
+    for (int rr = 0; rr < 32; ++rr) {
+      const size_t mr = (size_t)(row0 + rr);
+      const bool ok = rr < nrows;
+      if (MUL) mv[rr] = ok ? C.mul[mr * C.ldm + n] : 0.f;
+      if (RESID) rv[rr] = ok ? C.resid[mr * C.ldr + n] : 0.f;
     }
-    if (h + 16 <= nrows) {
+  }
+  if (nrows >= 32) {
 #pragma unroll
-      for (int rr = 0; rr < 16; ++rr) {
-        const size_t mr = (size_t)(row0 + h + rr);
-        float v = stile[(h + rr) * 33 + lane] + bn;
-        if (PRE) C.pre[mr * C.ldp + n] = v;
-        if (ACT) v = siluf_(v);
-        if (MUL) v *= dsiluf_(mv[rr]);
-        if (RESID) v += rv[rr];
-        C.out[mr * C.ldo + n] = v;
-      }
-    } else {
-      for (int rr = 0; rr < 16 && h + rr < nrows; ++rr) {
-        const size_t mr = (size_t)(row0 + h + rr);
-        float v = stile[(h + rr) * 33 + lane] + bn;
-        if (PRE) C.pre[mr * C.ldp + n] = v;
-        if (ACT) v = siluf_(v);
-        if (MUL) v *= dsiluf_(mv[rr]);
-        if (RESID) v += rv[rr];
-        C.out[mr * C.ldo + n] = v;
-      }
+    for (int rr = 0; rr < 32; ++rr) {
+      const size_t mr = (size_t)(row0 + rr);
+      float v = stile[rr * 33 + lane] + bn;
+      if (PRE) C.pre[mr * C.ldp + n] = v;
+      if (ACT) v = siluf_(v);
+      if (MUL) v *= dsiluf_(mv[rr]);
+      if (RESID) v += rv[rr];
+      C.out[mr * C.ldo + n] = v;
+    }
+  } else {
+#pragma unroll
+    for (int rr = 0; rr < 32; ++rr) {
+      if (rr >= nrows) break;
+      const size_t mr = (size_t)(row0 + rr);
+      float v = stile[rr * 33 + lane] + bn;
+      if (PRE) C.pre[mr * C.ldp + n] = v;
+      if (ACT) v = siluf_(v);
+      if (MUL) v *= dsiluf_(mv[rr]);
+      if (RESID) v += rv[rr];
+      C.out[mr * C.ldo + n] = v;
     }
   }
 }
