@@ -84,6 +84,8 @@ struct chg_ctx {
   size_t ev_used = 0;
   cudaEvent_t next_event();
 
+  // scratch shared by kernels that may run on either stream gets a per-stream name
+  std::string ws_name(const char *base) const { return stream == side && side ? std::string(base) + "#side" : base; }
   void *get(const std::string &name, size_t bytes);
   float *getf(const std::string &name, size_t n) { return (float *)get(name, n * sizeof(float)); }
   void *pinned_get(size_t bytes);

@@ -436,7 +436,7 @@ void wgrad(chg_ctx *ctx, const WGrad &g) {
   }
   int rps = g.M > 0 ? ceil_div(ceil_div(g.M, splits), WM) * WM : WM;
   splits = g.M > 0 ? ceil_div(g.M, rps) : 1;
-  float *partial = ctx->getf("wgrad_partial", (size_t)splits * Kp * g.N);
+  float *partial = ctx->getf(ctx->ws_name("wgrad_partial"), (size_t)splits * Kp * g.N);
   {
     ProfScope ps(ctx, g.tag ? g.tag : "wgrad", 2.0 * g.M * (double)Kp * g.N,
                  gemm_a_bytes(g.A, g.M, 0, g.K) + (double)g.M * (4.0 * g.N + (g.didx ? 4.0 : 0.0)) + 4.0 * Kp * g.N);

@@ -427,17 +427,28 @@ void ac_bwd_body(Bwd &Bw, int t, const float *v, const float *e, const float *ea
   segsum(ctx, N, dv, 64, 1, 2, s, "segsum_ac_dv");
 }
 
+// phase 1: everything that touches neither dv nor de (may run concurrently with ac_bwd_body);
+// phase 2: the dv / de segmented adjoint sums (after the atom conv's updates, fixed order)
 void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float *e, const float *a, const float *eb,
-                 const float *daggb, float *dv, float *de, float *da, float *deb) {
+                 const float *daggb, float *dv, float *de, float *da, float *deb, int phase) {
   chg_ctx *ctx = Bw.ctx;
   chg_graph *g = Bw.g;
   const int64_t N = g->N, E = g->E, B = g->B, A = g->A;
   if (A == 0) return;
   std::string bp = "bond" + std::to_string(t), ap = "angle" + std::to_string(t), ts = std::to_string(t);
-  const float *z1 = Bw.act("bc_z1_" + ts), *yb = Bw.act("bc_yb_" + ts);
-  float *dYb = Bw.scratch("bc_dYb", A, 128), *dZ = Bw.scratch("bc_dZ", A, 256);
   float *q1 = Bw.scratch("bc_q1", A, 64), *q2 = Bw.scratch("bc_q2", A, 64);
   float *tv = Bw.scratch("tmp_vi", A, 64), *t1 = Bw.scratch("tmp_e1", A, 64), *t2 = Bw.scratch("tmp_e2", A, 64);
+  if (phase == 2) {
+    SegSrc s[2];
+    s[0].in = tv; s[0].ptr = g->atom_angle_ptr; s[0].rows = A;                // angles of centre i are contiguous
+    segsum(ctx, N, dv, 64, 1, 1, s, "segsum_bc_dv");
+    s[0] = SegSrc(); s[0].in = t1; s[0].ptr = g->angle_ptr; s[0].segmap = g->bond_id; s[0].rows = A;
+    s[1] = SegSrc(); s[1].in = t2; s[1].ptr = g->angle_ptr; s[1].segmap = g->bond_id; s[1].perm = g->swap; s[1].rows = A;
+    segsum(ctx, E, de, 64, 1, 2, s, "segsum_bc_de");
+    return;
+  }
+  const float *z1 = Bw.act("bc_z1_" + ts), *yb = Bw.act("bc_yb_" + ts);
+  float *dYb = Bw.scratch("bc_dYb", A, 128), *dZ = Bw.scratch("bc_dZ", A, 256);
   gate_bwd(ctx, A, yb, 128, Bw.ln(bp), GATE_MUL_W1W2, eb, g->angle_b1, g->angle_b2, daggb, g->angle_b1, dYb, 128,
            nullptr, q1, q2, Bw.lng(bp));
   if (angle_branch)
@@ -520,11 +531,6 @@ void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float 
     wgrad(ctx, wg);
   }
   SegSrc s[2];
- s[0].in = tv; s[0].ptr = g->atom_angle_ptr; s[0].rows = A;                // angles of centre i are contiguous
-  segsum(ctx, N, dv, 64, 1, 1, s, "segsum_bc_dv");
-  s[0] = SegSrc(); s[0].in = t1; s[0].ptr = g->angle_ptr; s[0].segmap = g->bond_id; s[0].rows = A;
-  s[1] = SegSrc(); s[1].in = t2; s[1].ptr = g->angle_ptr; s[1].segmap = g->bond_id; s[1].perm = g->swap; s[1].rows = A;
-  segsum(ctx, E, de, 64, 1, 2, s, "segsum_bc_de");
   s[0] = SegSrc(); s[0].in = q1; s[0].ptr = g->angle_ptr; s[0].rows = A;
   s[1] = SegSrc(); s[1].in = q2; s[1].ptr = g->angle_ptr; s[1].perm = g->swap; s[1].rows = A;
   segsum(ctx, B, deb, 64, 1, 2, s, "segsum_bc_deb");
@@ -610,8 +616,26 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
     // both output linears read the incoming gradients before any update
     ac_bwd_head(Bw, t, dv, dagg);
     bc_bwd_head(Bw, t, de, daggb);
-    ac_bwd_body(Bw, t, V(t), Ef(t), ea, dagg, dv, de, dea);
-    bc_bwd_body(Bw, t, ab, V(t), Ef(t), Af(t), eb, daggb, dv, de, da, deb);
+    if (!ctx->side) {
+      ac_bwd_body(Bw, t, V(t), Ef(t), ea, dagg, dv, de, dea);
+      bc_bwd_body(Bw, t, ab, V(t), Ef(t), Af(t), eb, daggb, dv, de, da, deb, 1);
+    } else {   // the bond/angle adjoints up to their dv/de sums run beside the atom conv's
+      cudaStream_t main_stream = ctx->stream;
+      CUDA_OK(cudaEventRecord(ctx->ev_fork, main_stream));
+      CUDA_OK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+      ctx->stream = ctx->side;
+      try {
+        bc_bwd_body(Bw, t, ab, V(t), Ef(t), Af(t), eb, daggb, dv, de, da, deb, 1);
+      } catch (...) {
+        ctx->stream = main_stream;
+        throw;
+      }
+      ctx->stream = main_stream;
+      CUDA_OK(cudaEventRecord(ctx->ev_join, ctx->side));
+      ac_bwd_body(Bw, t, V(t), Ef(t), ea, dagg, dv, de, dea);
+      CUDA_OK(cudaStreamWaitEvent(main_stream, ctx->ev_join, 0));
+    }
+    bc_bwd_body(Bw, t, ab, V(t), Ef(t), Af(t), eb, daggb, dv, de, da, deb, 2);
   }
   // embedding (rows of W_v gathered by species -> grouped sum, no atomics)
   species_grad(ctx, N, m->cfg.n_species, g->species_ptr, g->species_perm, dv, Bw.G("embed.W"));

@@ -577,7 +577,7 @@ void gate_bwd(chg_ctx *ctx, int64_t rows, const float *y, int ldy, GateLN ln, in
   int64_t rpb = std::max<int64_t>(64, (rows + 591) / 592);
   int nb = rows > 0 ? ceil_div(rows, rpb) : 0;
   if (nb == 0) return;
-  float *part = ctx->getf("ln_partial", (size_t)nb * 256);
+  float *part = ctx->getf(ctx->ws_name("ln_partial"), (size_t)nb * 256);
   ProfScope ps(ctx, "gate_bwd", 0.0,
                rows * (512.0 + 260.0 + 512.0 + (mode == GATE_MUL_W ? 768.0 : mode == GATE_MUL_W1W2 ? 1032.0 : 0.0)));
   k_gate_bwd<<<nb, 256, 0, ctx->stream>>>(rows, rpb, y, ldy, ln, mode, w, i1, i2, dout, didx, dy, lddy, dw_acc, q1,

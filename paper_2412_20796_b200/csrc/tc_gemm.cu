@@ -912,7 +912,7 @@ bool wgrad_tc(chg_ctx *ctx, const WGrad &g, float **partial_out, int *Kp_out, in
   const int grid = std::max(1, std::min(sms, chunks));
   P.rows_per_cta = (chunks + grid - 1) / grid * 32;
   const int splits = (g.M + P.rows_per_cta - 1) / P.rows_per_cta;
-  float *partial = ctx->getf("wgrad_partial", (size_t)splits * P.Kp * g.N);
+  float *partial = ctx->getf(ctx->ws_name("wgrad_partial"), (size_t)splits * P.Kp * g.N);
   const size_t st_bytes = (size_t)(P.Kpad + P.Npad) * 128;
   const size_t smem = 1024 + WG_NST * st_bytes + 8 * (2 * WG_NST + 1) + 16 + 4 * 32 * 33 * 4 + WG_NPW * 256 * 4;
   if (smem > 224 * 1024) return false;
