@@ -362,7 +362,7 @@ void run_bwd(chg_ctx *ctx, HeadArgs a, float *G, const char *tag) {
   const int grid = (int)std::min<int64_t>(ntiles, 2 * sm_count());
   const int nb = head_block_size(NL, NOUT);
   const int stride = head_part_stride(NL, NOUT);
-  a.part = ctx->getf("head_part", (size_t)grid * stride);
+  a.part = ctx->getf(ctx->ws_name("head_part"), (size_t)grid * stride);
   {
     ProfScope ps(ctx, tag, 2.0 * a.rows * (2.0 * 64 * 64 * (NL - 1) + 2.0 * 64 * NOUT),
                  a.rows * 4.0 * (64 * 3 + 64 * (NL - 1) + NOUT) + 4.0 * nb * (double)grid * 2);

@@ -33,6 +33,28 @@ struct Fwd {
   }
 };
 
+// Run f() on the ctx's second stream, forked from the library stream (the caller joins with
+// join_side before consuming f's outputs).  Without a side stream f runs inline.
+template <class Fn>
+void on_side(chg_ctx *ctx, Fn &&f) {
+  if (!ctx->side) { f(); return; }
+  cudaStream_t main_stream = ctx->stream;
+  CUDA_OK(cudaEventRecord(ctx->ev_fork, main_stream));
+  CUDA_OK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+  ctx->stream = ctx->side;
+  try {
+    f();
+  } catch (...) {
+    ctx->stream = main_stream;
+    throw;
+  }
+  ctx->stream = main_stream;
+  CUDA_OK(cudaEventRecord(ctx->ev_join, ctx->side));
+}
+void join_side(chg_ctx *ctx) {
+  if (ctx->side) CUDA_OK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+}
+
 // --- Atom Conv (Eq. 4) ------------------------------------------------------
 void atom_conv_fwd(Fwd &F, int t, const float *v, const float *e, const float *ea, float *v_out) {
   chg_ctx *ctx = F.ctx;
@@ -229,11 +251,13 @@ void forward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, int train, chg_pred 
     CUDA_OK(cudaStreamWaitEvent(main_stream, ctx->ev_join, 0));
   }
   v[T + 1] = F.buf("v" + std::to_string(T + 1), N, 64);
-  atom_conv_fwd(F, T, v[T], e[T], ea, v[T + 1]);
-  // A6 heads
+  // A6 heads: the force head reads e^T only, so it runs beside the final atom conv
   float *vf = v[T + 1], *ef = e[T];
   float *e_atom = F.buf("e_atom", N, 1), *mag = F.buf("magmom", N, 1), *n_e = F.buf("n_e", E, 1);
   float *M9 = F.buf("M9", N, 9);
+  float *Zf[2] = {F.buf("head_F_z0", E, 64), F.buf("head_F_z1", E, 64)};
+  on_side(ctx, [&] { head_mlp_fwd(ctx, 3, 1, ef, E, m->p("head_F.W0"), Zf, n_e, 1); });
+  atom_conv_fwd(F, T, v[T], e[T], ea, v[T + 1]);
   mlp_fwd(F, "head_E", 4, vf, N, 1, e_atom, 1);
   {
     RowGemm G;
@@ -244,8 +268,8 @@ void forward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, int train, chg_pred 
     G.tag = "headM_f";
     rowgemm(ctx, G);
   }
-  mlp_fwd(F, "head_F", 3, ef, E, 1, n_e, 1);
   mlp_fwd(F, "head_S", 3, vf, N, 9, M9, 9);
+  join_side(ctx);
   float *energy = F.buf("energy", g->S, 1), *epa = F.buf("energy_per_atom", g->S, 1);
   float *forces = F.buf("forces", N, 3), *stress = F.buf("stress", g->S, 9);
   heads_forces(ctx, g, n_e, forces);
@@ -581,7 +605,8 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
   fill_zero(ctx, dea, 4 * 64 * E);
   fill_zero(ctx, deb, 4 * 64 * B);
   const float *vf = Bw.act("v" + std::to_string(T + 1)), *ef = Bw.act("e" + std::to_string(T));
-  // heads backward
+  // heads backward: the force head (-> de) beside the atom-side heads (-> dv)
+  on_side(ctx, [&] { mlp_bwd(Bw, "head_F", 3, ef, E, sd.d_ne, 1, de); });
   mlp_bwd(Bw, "head_E", 4, vf, N, sd.d_eatom, 1, dv);
   {
     WGrad wg;
@@ -602,7 +627,6 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
     rowgemm(ctx, G);
   }
   mlp_bwd(Bw, "head_S", 3, vf, N, sd.d_M9, 9, dv);
-  mlp_bwd(Bw, "head_F", 3, ef, E, sd.d_ne, 1, de);
   // A8 interaction blocks, last to first
   const float *ea = Bw.act("ea"), *eb = Bw.act("eb");
   float *dagg = Bw.scratch("dagg", N, 64), *daggb = Bw.scratch("daggb", B, 64);
@@ -610,6 +634,7 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
   auto Ef = [&](int t) { return Bw.act("e" + std::to_string(t)); };
   auto Af = [&](int t) { return Bw.act("a" + std::to_string(t)); };
   ac_bwd_head(Bw, T, dv, dagg);
+  join_side(ctx);                                   // de complete before the atom conv adds to it
   ac_bwd_body(Bw, T, V(T), Ef(T), ea, dagg, dv, de, dea);
   for (int t = T - 1; t >= 0; --t) {
     bool ab = t + 1 < T;
