@@ -84,6 +84,50 @@ __global__ void k_frac(int N, const double *__restrict__ pos, const int32_t *__r
     frac[3 * i + c] = p[0] * g.Linv[0 + c] + p[1] * g.Linv[3 + c] + p[2] * g.Linv[6 + c];
 }
 
+// per-structure geometry on the device (inputs already resident: no host round trip).  Same
+// formulas as the host path; invalid cells set flag bits 16 / 32 / 64 (non-finite, |det| <= 1e-6,
+// too thin) and the smallest offending structure index, and get zero ranges so the later
+// kernels stay bounded; the host raises at the size synchronisation.
+__global__ void k_geo(int S, const double *__restrict__ lat, double r_atom, StructGeo *__restrict__ geo,
+                      float *__restrict__ lat_f, int *flag) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  double l[9];
+  bool finite = true;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    l[k] = lat[9 * s + k];
+    finite = finite && isfinite(l[k]);
+    lat_f[9 * s + k] = (float)l[k];
+  }
+  StructGeo g;
+  int bad = finite ? 0 : 16;
+  const double det = l[0] * (l[4] * l[8] - l[5] * l[7]) - l[1] * (l[3] * l[8] - l[5] * l[6]) +
+                     l[2] * (l[3] * l[7] - l[4] * l[6]);
+  const double V = fabs(det);
+  if (!bad && !(V > 1e-6)) bad = 32;
+  const double inv[9] = {l[4] * l[8] - l[5] * l[7], l[2] * l[7] - l[1] * l[8], l[1] * l[5] - l[2] * l[4],
+                         l[5] * l[6] - l[3] * l[8], l[0] * l[8] - l[2] * l[6], l[2] * l[3] - l[0] * l[5],
+                         l[3] * l[7] - l[4] * l[6], l[1] * l[6] - l[0] * l[7], l[0] * l[4] - l[1] * l[3]};
+#pragma unroll
+  for (int k = 0; k < 9; ++k) { g.L[k] = l[k]; g.Linv[k] = bad ? 0.0 : inv[k] / det; }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double *u = &l[3 * ((k + 1) % 3)], *w = &l[3 * ((k + 2) % 3)];
+    const double cx = u[1] * w[2] - u[2] * w[1], cy = u[2] * w[0] - u[0] * w[2], cz = u[0] * w[1] - u[1] * w[0];
+    const double width = V / sqrt(cx * cx + cy * cy + cz * cz);
+    g.rw[k] = r_atom / width;
+    if (!bad && g.rw[k] > 100.0) bad = 64;
+  }
+  if (bad) {
+    for (int k = 0; k < 3; ++k) g.rw[k] = 0.0;
+    atomicOr(flag, bad);
+    atomicMin(flag + 1, s);
+  }
+  g.pad = 0.0;
+  geo[s] = g;
+}
+
 __global__ void k_count(int N, const double *__restrict__ pos, const double *__restrict__ frac,
                         const int32_t *__restrict__ soa, const int32_t *__restrict__ atom_ptr,
                         const StructGeo *__restrict__ geo, double ra2, double rb2,
@@ -370,18 +414,13 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
   if (N >= (1LL << 31) / 64) CHG_THROW(CHG_ERR_CAPACITY, "too many atoms (%lld)", (long long)N);
   cudaStream_t st = ctx->stream;
 
-  // lattice on host (S*72 B) for validation and per-structure geometry
-  std::vector<double> L(9 * (size_t)S);
-  if (S > 0) {
-    if (on_device) {
-      CUDA_OK(cudaMemcpyAsync(L.data(), lat, 9 * sizeof(double) * S, cudaMemcpyDeviceToHost, st));
-      CUDA_OK(cudaStreamSynchronize(st));
-    } else {
-      std::copy(lat, lat + 9 * (size_t)S, L.begin());
-    }
-  }
+  // per-structure geometry: host inputs are validated here; device inputs by k_geo (no
+  // round trip), its errors surface at the size synchronisation below
+  const bool dev_geo = on_device && S > 0;
+  std::vector<double> L(dev_geo ? 0 : 9 * (size_t)S);
+  if (S > 0 && !dev_geo) std::copy(lat, lat + 9 * (size_t)S, L.begin());
   std::vector<StructGeo> geo(S > 0 ? S : 1);
-  for (int s = 0; s < S; ++s) {
+  for (int s = 0; s < S && !dev_geo; ++s) {
     const double *l = &L[9 * s];
     for (int k = 0; k < 9; ++k)
       if (!std::isfinite(l[k])) CHG_THROW(CHG_ERR_GEOMETRY, "structure %d: non-finite lattice", s);
@@ -458,7 +497,8 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
     for (int s = 0; s <= S; ++s) h_ap[s] = (int32_t)G->atom_ptr_h[s];
     for (int s = 0; s < S; ++s) {
       for (int64_t a = atom_ptr[s]; a < atom_ptr[s + 1]; ++a) h_soa[a] = s;
-      for (int k = 0; k < 9; ++k) h_lat[9 * s + k] = (float)L[9 * s + k];
+      if (!dev_geo)
+        for (int k = 0; k < 9; ++k) h_lat[9 * s + k] = (float)L[9 * s + k];
       int64_t ns = atom_ptr[s + 1] - atom_ptr[s];
       h_inv[s] = ns > 0 ? 1.0f / (float)ns : 0.0f;
     }
@@ -466,10 +506,10 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
     CUDA_OK(cudaMemcpyAsync(G->atom_ptr, h_ap, 4 * (S + 1), cudaMemcpyHostToDevice, st));
     if (N) CUDA_OK(cudaMemcpyAsync(G->struct_of_atom, h_soa, 4 * N, cudaMemcpyHostToDevice, st));
     if (S) {
-      CUDA_OK(cudaMemcpyAsync(G->lattice_f, h_lat, 4 * 9 * (size_t)S, cudaMemcpyHostToDevice, st));
+      if (!dev_geo) CUDA_OK(cudaMemcpyAsync(G->lattice_f, h_lat, 4 * 9 * (size_t)S, cudaMemcpyHostToDevice, st));
       CUDA_OK(cudaMemcpyAsync(G->inv_natoms, h_inv, 4 * (size_t)S, cudaMemcpyHostToDevice, st));
     }
-    CUDA_OK(cudaMemcpyAsync(d_geo, h_geo, sizeof(StructGeo) * geo.size(), cudaMemcpyHostToDevice, st));
+    if (!dev_geo) CUDA_OK(cudaMemcpyAsync(d_geo, h_geo, sizeof(StructGeo) * geo.size(), cudaMemcpyHostToDevice, st));
     if (N) {
       if (on_device) {
         CUDA_OK(cudaMemcpyAsync(d_pos, pos, 8 * 3 * N, cudaMemcpyDeviceToDevice, st));
@@ -486,8 +526,13 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
     int *flag = ctx->d_flag;
     ProfScope ps1(ctx, "graph", 0.0, 0.0);
     CUDA_OK(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    CUDA_OK(cudaMemsetAsync(flag + 1, 0x7f, sizeof(int), st));       // smallest bad structure (k_geo)
     CUDA_OK(cudaMemsetAsync(d_tot, 0, 64, st));
     double ra2 = r_atom * r_atom, rb2 = r_bond * r_bond;
+    if (dev_geo) {
+      k_geo<<<ceil_div(S, 128), 128, 0, st>>>(S, lat, r_atom, d_geo, G->lattice_f, flag);
+      check_launch(ctx);
+    }
     if (N) {
       k_frac<<<ceil_div(N, 256), 256, 0, st>>>((int)N, d_pos, G->struct_of_atom, d_geo, G->species,
                                                 n_species, d_frac, flag);
@@ -505,9 +550,12 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
     // totals + flags to host (the one synchronisation of the build: sizes)
     long long *h_tot = (long long *)ctx->pinned_get(64);
     CUDA_OK(cudaMemcpyAsync(h_tot, d_tot, 32, cudaMemcpyDeviceToHost, st));
-    CUDA_OK(cudaMemcpyAsync(((char *)h_tot) + 32, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaMemcpyAsync(((char *)h_tot) + 32, flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaStreamSynchronize(st));
-    int hflag = *(int *)(((char *)h_tot) + 32);
+    int hflag = *(int *)(((char *)h_tot) + 32), hbad = *(int *)(((char *)h_tot) + 36);
+    if (hflag & 16) CHG_THROW(CHG_ERR_GEOMETRY, "structure %d: non-finite lattice", hbad);
+    if (hflag & 32) CHG_THROW(CHG_ERR_GEOMETRY, "structure %d: |det L| <= 1e-6", hbad);
+    if (hflag & 64) CHG_THROW(CHG_ERR_GEOMETRY, "structure %d: cell too thin for cutoff", hbad);
     if (hflag & 1) CHG_THROW(CHG_ERR_GEOMETRY, "non-finite positions");
     if (hflag & 2) CHG_THROW(CHG_ERR_SPECIES, "species outside 1..%d", n_species);
     if (hflag & 4) CHG_THROW(CHG_ERR_GEOMETRY, "coincident atoms (accepted pair with d^2 < 1e-12)");

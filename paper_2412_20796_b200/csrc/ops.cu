@@ -250,41 +250,66 @@ struct SegArgs { SegSrc s[3]; int n; };
 // 16-lane load.  Row indices are fetched 16 at a time (coalesced) and broadcast by
 // shuffle; four rows are in flight per lane.  Rows are added in segment order, so
 // the result is deterministic.
+// H half-warps per target (H = 1, 2, 4, 8; long segments): half-warp j sums the fixed j-th
+// contiguous part of every source segment, the H partials are added in j order through shared
+// memory — the split points depend only on the segment length, so the result is deterministic.
+template <int H>
 __global__ void __launch_bounds__(256) k_segsum(int64_t targets, float *__restrict__ out, int ldo, int accumulate,
                                                 SegArgs a) {
-  const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 4;
+  __shared__ float4 part[16][16];                   // [half-warp in block][lane]
+  const int hw = threadIdx.x >> 4;                  // half-warp in block (16)
+  const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / (16 * H);
+  const int j = hw % H;                             // part of the segments this half-warp sums
   const int lane = threadIdx.x & 31, hl = lane & 15;
   const unsigned hmask = 0xffffu << (lane & 16);
-  if (t >= targets) return;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (t < targets) {
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    if (k >= a.n) break;
-    const SegSrc &S = a.s[k];
-    const int64_t sg = S.segmap ? (int64_t)__ldg(S.segmap + t) : t + S.ptr_off;
-    if (sg < 0) continue;
-    const int r0 = __ldg(S.ptr + sg), r1 = __ldg(S.ptr + sg + 1);
-    const float4 *in = (const float4 *)S.in + hl;
-    for (int base = r0; base < r1; base += 16) {
-      const int n = min(16, r1 - base);
-      const int myrow = hl < n ? (S.perm ? __ldg(S.perm + base + hl) : base + hl) : 0;
-      int j = 0;
-      for (; j + 4 <= n; j += 4) {
-        const int q0 = __shfl_sync(hmask, myrow, j, 16), q1 = __shfl_sync(hmask, myrow, j + 1, 16);
-        const int q2 = __shfl_sync(hmask, myrow, j + 2, 16), q3 = __shfl_sync(hmask, myrow, j + 3, 16);
-        const float4 v0 = __ldg(in + (int64_t)q0 * 16), v1 = __ldg(in + (int64_t)q1 * 16);
-        const float4 v2 = __ldg(in + (int64_t)q2 * 16), v3 = __ldg(in + (int64_t)q3 * 16);
-        acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
-        acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w;
-        acc.x += v2.x; acc.y += v2.y; acc.z += v2.z; acc.w += v2.w;
-        acc.x += v3.x; acc.y += v3.y; acc.z += v3.z; acc.w += v3.w;
+    for (int k = 0; k < 3; ++k) {
+      if (k >= a.n) break;
+      const SegSrc &S = a.s[k];
+      const int64_t sg = S.segmap ? (int64_t)__ldg(S.segmap + t) : t + S.ptr_off;
+      if (sg < 0) continue;
+      int r0 = __ldg(S.ptr + sg), r1 = __ldg(S.ptr + sg + 1);
+      if (H > 1) {
+        const int len = r1 - r0;
+        const int a0 = r0 + (int)((int64_t)len * j / H), a1 = r0 + (int)((int64_t)len * (j + 1) / H);
+        r0 = a0; r1 = a1;
       }
-      for (; j < n; ++j) {
-        const int q = __shfl_sync(hmask, myrow, j, 16);
-        const float4 v = __ldg(in + (int64_t)q * 16);
-        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      const float4 *in = (const float4 *)S.in + hl;
+      for (int base = r0; base < r1; base += 16) {
+        const int n = min(16, r1 - base);
+        const int myrow = hl < n ? (S.perm ? __ldg(S.perm + base + hl) : base + hl) : 0;
+        int q = 0;
+        for (; q + 4 <= n; q += 4) {
+          const int q0 = __shfl_sync(hmask, myrow, q, 16), q1 = __shfl_sync(hmask, myrow, q + 1, 16);
+          const int q2 = __shfl_sync(hmask, myrow, q + 2, 16), q3 = __shfl_sync(hmask, myrow, q + 3, 16);
+          const float4 v0 = __ldg(in + (int64_t)q0 * 16), v1 = __ldg(in + (int64_t)q1 * 16);
+          const float4 v2 = __ldg(in + (int64_t)q2 * 16), v3 = __ldg(in + (int64_t)q3 * 16);
+          acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
+          acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w;
+          acc.x += v2.x; acc.y += v2.y; acc.z += v2.z; acc.w += v2.w;
+          acc.x += v3.x; acc.y += v3.y; acc.z += v3.z; acc.w += v3.w;
+        }
+        for (; q < n; ++q) {
+          const int qq = __shfl_sync(hmask, myrow, q, 16);
+          const float4 v = __ldg(in + (int64_t)qq * 16);
+          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
       }
     }
+  }
+  if (H > 1) {
+    part[hw][hl] = acc;
+    __syncthreads();
+    if (j != 0 || t >= targets) return;
+#pragma unroll
+    for (int q = 1; q < H; ++q) {
+      const float4 p = part[hw + q][hl];
+      acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w;
+    }
+  } else if (t >= targets) {
+    return;
   }
   float4 *o = (float4 *)(out + t * ldo) + hl;
   if (accumulate) { const float4 p = *o; acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w; }
@@ -601,8 +626,19 @@ void segsum(chg_ctx *ctx, int64_t targets, float *out, int ldo, int accumulate, 
     if (((uintptr_t)src[k].in & 15) || ((uintptr_t)out & 15) || (ldo & 3))
       CHG_THROW(CHG_ERR_STATE, "segsum: 16-byte alignment required (in %p, out %p, ldo %d)", (const void *)src[k].in,
                 (void *)out, ldo);
+  // half-warps per target from the mean segment length (rows per half-warp ~ 16 or more)
+  int64_t rows = 0;
+  for (int k = 0; k < nsrc; ++k) rows += src[k].rows;
+  const int64_t mean = rows / std::max<int64_t>(targets, 1);
+  const int H = mean >= 96 ? 8 : mean >= 48 ? 4 : mean >= 24 ? 2 : 1;
   ProfScope ps(ctx, tag, 0.0, bytes);
-  k_segsum<<<ceil_div(targets * 16, 256), 256, 0, ctx->stream>>>(targets, out, ldo, accumulate, a);
+  const int grid = ceil_div(targets * 16 * H, 256);
+  switch (H) {
+    case 8: k_segsum<8><<<grid, 256, 0, ctx->stream>>>(targets, out, ldo, accumulate, a); break;
+    case 4: k_segsum<4><<<grid, 256, 0, ctx->stream>>>(targets, out, ldo, accumulate, a); break;
+    case 2: k_segsum<2><<<grid, 256, 0, ctx->stream>>>(targets, out, ldo, accumulate, a); break;
+    default: k_segsum<1><<<grid, 256, 0, ctx->stream>>>(targets, out, ldo, accumulate, a); break;
+  }
   check_launch(ctx);
 }
 

@@ -86,6 +86,29 @@ def test_graph_bit_exact(ctx, case):
     np.testing.assert_array_equal(gg.per_struct(), og.counts)
 
 
+def test_graph_device_inputs(ctx):
+    """Device-resident inputs: geometry validated on the GPU (k_geo); same lists as host inputs."""
+    import torch
+    b = make_config_batch("C2")
+    og = build_graph_batch(b)
+    gg = ctx.build_graph(b.atom_ptr, torch.as_tensor(b.positions, device="cuda"),
+                         torch.as_tensor(b.lattice, device="cuda"), torch.as_tensor(b.species, device="cuda"))
+    ex = gg.export()
+    for k, v in og.lists().items():
+        np.testing.assert_array_equal(ex[k], v, err_msg=k)
+    np.testing.assert_array_equal(gg.per_struct(), og.counts)
+    bad = b.lattice.copy(); bad[3] = 0.0
+    with pytest.raises(chg.ChgError) as e:
+        ctx.build_graph(b.atom_ptr, torch.as_tensor(b.positions, device="cuda"), torch.as_tensor(bad, device="cuda"),
+                        torch.as_tensor(b.species, device="cuda"))
+    assert e.value.name == "CHG_ERR_GEOMETRY" and "structure 3" in str(e.value)
+    thin = b.lattice.copy(); thin[5, 2] *= 1e-3
+    with pytest.raises(chg.ChgError) as e:
+        ctx.build_graph(b.atom_ptr, torch.as_tensor(b.positions, device="cuda"), torch.as_tensor(thin, device="cuda"),
+                        torch.as_tensor(b.species, device="cuda"))
+    assert e.value.name == "CHG_ERR_GEOMETRY"
+
+
 def test_graph_errors(ctx):
     b = si_diamond()
     with pytest.raises(chg.ChgError) as e:
