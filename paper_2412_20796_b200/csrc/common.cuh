@@ -41,6 +41,24 @@ struct ChgError {
   } while (0)
 
 // ---------------------------------------------------------------------------
+// deferred split reductions (reduce.cu): every "sum the per-CTA partials into a gradient"
+// step of a backward layer is recorded and executed by ONE launch at the layer's end
+// ---------------------------------------------------------------------------
+struct RedJob {
+  int kind = 0;                 // 0 weight gradient (W/b by 64-col chunk), 1 flat, 2 LayerNorm (4 x 64), 3 projection
+  int n = 0;                    // outputs
+  int splits = 0;               // partial rows
+  int64_t stride = 0;           // floats between partial rows
+  const float *part = nullptr;  // [splits][stride]
+  int K = 0, N = 0;             // kind 0: rows < K -> W, row K -> bias; kind 3: N = columns C
+  float *W[4] = {nullptr, nullptr, nullptr, nullptr};
+  int ldw[4] = {0, 0, 0, 0};
+  float *b[4] = {nullptr, nullptr, nullptr, nullptr};
+  int k0[4] = {0, 0, 0, 0}, kn[4] = {-1, -1, -1, -1};
+  int block0 = 0;               // first block of this job in the batched launch
+};
+
+// ---------------------------------------------------------------------------
 // context
 // ---------------------------------------------------------------------------
 struct chg_ctx {
@@ -86,6 +104,9 @@ struct chg_ctx {
 
   // scratch shared by kernels that may run on either stream gets a per-stream name
   std::string ws_name(const char *base) const { return stream == side && side ? std::string(base) + "#side" : base; }
+  // deferred reductions (reduce.cu): active inside backward layers
+  bool red_on = false;
+  std::vector<RedJob> red_jobs;
   void *get(const std::string &name, size_t bytes);
   float *getf(const std::string &name, size_t n) { return (float *)get(name, n * sizeof(float)); }
   void *pinned_get(size_t bytes);
@@ -223,6 +244,11 @@ inline void check_launch(chg_ctx *ctx, const char *file = __builtin_FILE(), int 
     if (e != cudaSuccess) CHG_THROW(CHG_ERR_CUDA, "kernel at %s:%d: %s", file, line, cudaGetErrorString(e));
   }
 }
+
+// reduce.cu
+float *red_partial(chg_ctx *ctx, size_t floats);       // partial buffer for the next recorded job
+void red_push(chg_ctx *ctx, RedJob j);                 // record (red_on) or launch now
+void red_flush(chg_ctx *ctx);                          // one launch for every recorded job
 
 // graph.cu
 chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const double *pos,

@@ -234,67 +234,6 @@ __global__ void __launch_bounds__(256) k_wgrad(const WGrad g, float *__restrict_
   }
 }
 
-// Same reduction on float4 quads (N % 4 == 0): a block owns 32 quads = 128 outputs.
-__global__ void __launch_bounds__(256) k_wgrad_reduce4(const WGrad g, const float4 *__restrict__ partial, int Kp,
-                                                       int splits) {
-  __shared__ float4 sh[8][32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int q = blockIdx.x * 32 + lane;
-  const int nq = Kp * g.N / 4;
-  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (q < nq) {
-#pragma unroll 4
-    for (int sp = w; sp < splits; sp += 8) {
-      const float4 u = __ldcg(partial + (size_t)sp * nq + q);
-      s.x += u.x; s.y += u.y; s.z += u.z; s.w += u.w;
-    }
-  }
-  sh[w][lane] = s;
-  __syncthreads();
-  if (w != 0 || q >= nq) return;
-  float4 t = sh[0][lane];
-#pragma unroll
-  for (int k = 1; k < 8; ++k) { t.x += sh[k][lane].x; t.y += sh[k][lane].y; t.z += sh[k][lane].z; t.w += sh[k][lane].w; }
-  const int k = (4 * q) / g.N, n = (4 * q) % g.N;
-  const WGradDst &d = g.dst[n / 64];
-  const int nn = n % 64;
-  float *dst = nullptr;
-  if (k < g.K) {
-    if (d.W && k >= d.k0 && (d.kn < 0 || k < d.k0 + d.kn)) dst = d.W + (size_t)(k - d.k0) * d.ldw + nn;
-  } else {
-    dst = d.b ? d.b + nn : nullptr;
-  }
-  if (dst) { dst[0] += t.x; dst[1] += t.y; dst[2] += t.z; dst[3] += t.w; }
-}
-
-// Fixed-order reduction of the split-M partials: a block owns 32 consecutive
-// outputs; its 8 warps sum disjoint, interleaved split subsets (warp w: splits
-// w, w+8, ...), then warp 0 adds the 8 subtotals in order (deterministic).
-__global__ void __launch_bounds__(256) k_wgrad_reduce(const WGrad g, const float *__restrict__ partial, int Kp,
-                                                      int splits) {
-  __shared__ float sh[8][32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int idx = blockIdx.x * 32 + lane;
-  const size_t total = (size_t)Kp * g.N;
-  float s = 0.f;
-  if (idx < total)
-    for (int sp = w; sp < splits; sp += 8) s += partial[(size_t)sp * total + idx];
-  sh[w][lane] = s;
-  __syncthreads();
-  if (w != 0 || idx >= total) return;
-  float t = 0.f;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) t += sh[k][lane];
-  const int k = idx / g.N, n = idx % g.N;
-  const WGradDst &d = g.dst[n / 64];
-  const int nn = n % 64;
-  if (k < g.K) {
-    if (d.W && k >= d.k0 && (d.kn < 0 || k < d.k0 + d.kn)) d.W[(size_t)(k - d.k0) * d.ldw + nn] += t;
-  } else if (d.b) {
-    d.b[nn] += t;
-  }
-}
-
 bool aop_vec(const AOp &A) {
   for (int s = 0; s < A.nseg; ++s) {
     const ASeg &S = A.seg[s];
@@ -399,12 +338,20 @@ void rowgemm(chg_ctx *ctx, const RowGemm &g) {
   check_launch(ctx);
 }
 
+// split partials [splits][Kp][N] -> W / bias of each 64-column chunk (reduce.cu, batched)
 static void launch_wgrad_reduce(chg_ctx *ctx, const WGrad &g, const float *partial, int Kp, int splits) {
-  if (g.N % 4 == 0 && ((uintptr_t)partial & 15) == 0)
-    k_wgrad_reduce4<<<ceil_div((int64_t)Kp * g.N / 4, 32), 256, 0, ctx->stream>>>(g, (const float4 *)partial, Kp, splits);
-  else
-    k_wgrad_reduce<<<ceil_div((int64_t)Kp * g.N, 32), 256, 0, ctx->stream>>>(g, partial, Kp, splits);
-  check_launch(ctx);
+  RedJob j;
+  j.kind = 0;
+  j.n = Kp * g.N;
+  j.splits = splits;
+  j.stride = (int64_t)Kp * g.N;
+  j.part = partial;
+  j.K = g.K;
+  j.N = g.N;
+  for (int c = 0; c < 4; ++c) {
+    j.W[c] = g.dst[c].W; j.ldw[c] = g.dst[c].ldw; j.b[c] = g.dst[c].b; j.k0[c] = g.dst[c].k0; j.kn[c] = g.dst[c].kn;
+  }
+  red_push(ctx, j);
 }
 
 void wgrad(chg_ctx *ctx, const WGrad &g) {
@@ -415,10 +362,7 @@ void wgrad(chg_ctx *ctx, const WGrad &g) {
     int kp = 0, splits = 0;
     bool bias_done = false;
     if (wgrad_tc(ctx, g, &partial, &kp, &splits, &bias_done)) {
-      {
-        ProfScope ps(ctx, prof_tag(std::string(g.tag ? g.tag : "wgrad") + "_red"), 0.0, 4.0 * kp * g.N * (splits + 2.0));
-        launch_wgrad_reduce(ctx, g, partial, kp, splits);
-      }
+      launch_wgrad_reduce(ctx, g, partial, kp, splits);
       if (!bias_done) {            // K is a multiple of 128: column sums of D on the CUDA cores
         WGrad b = g;
         b.A.nseg = 0;
@@ -436,7 +380,7 @@ void wgrad(chg_ctx *ctx, const WGrad &g) {
   }
   int rps = g.M > 0 ? ceil_div(ceil_div(g.M, splits), WM) * WM : WM;
   splits = g.M > 0 ? ceil_div(g.M, rps) : 1;
-  float *partial = ctx->getf(ctx->ws_name("wgrad_partial"), (size_t)splits * Kp * g.N);
+  float *partial = red_partial(ctx, (size_t)splits * Kp * g.N);
   {
     ProfScope ps(ctx, g.tag ? g.tag : "wgrad", 2.0 * g.M * (double)Kp * g.N,
                  gemm_a_bytes(g.A, g.M, 0, g.K) + (double)g.M * (4.0 * g.N + (g.didx ? 4.0 : 0.0)) + 4.0 * Kp * g.N);
@@ -448,7 +392,6 @@ void wgrad(chg_ctx *ctx, const WGrad &g) {
       k_wgrad<false><<<grid, 256, 0, ctx->stream>>>(g, partial, Kp, rps);
     check_launch(ctx);
   }
-  ProfScope ps(ctx, prof_tag(std::string(g.tag ? g.tag : "wgrad") + "_red"), 0.0, 4.0 * Kp * g.N * (splits + 2.0));
   launch_wgrad_reduce(ctx, g, partial, Kp, splits);
 }
 

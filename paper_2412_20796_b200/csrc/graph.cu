@@ -128,51 +128,73 @@ __global__ void k_geo(int S, const double *__restrict__ lat, double r_atom, Stru
   geo[s] = g;
 }
 
-__global__ void k_count(int N, const double *__restrict__ pos, const double *__restrict__ frac,
-                        const int32_t *__restrict__ soa, const int32_t *__restrict__ atom_ptr,
-                        const StructGeo *__restrict__ geo, double ra2, double rb2,
-                        int32_t *__restrict__ cnt_e, int32_t *__restrict__ cnt_b, int *flag) {
-  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  if (warp >= N) return;
-  int i = warp;
-  int s = soa[i];
-  int a0 = atom_ptr[s], a1 = atom_ptr[s + 1];
+// One 128-thread block (4 warps) per centre atom i.  Lanes walk (j, n1) slots: W >= any pair's
+// n1-range width (pair_range: <= 2·rw + 4 values), so a lane runs only the n2 x n3 loops of one
+// image row; the four warps take 32-slot chunks round-robin (more warps in flight per SM).
+constexpr int GWPA = 4;   // warps per atom
+
+__device__ __forceinline__ int slot_count(const double *__restrict__ pos, const double *__restrict__ frac,
+                                          const double *L, const StructGeo &g, const double *fi, int i, int a0,
+                                          int W, int p, double ra2, double rb2, int &cb, int &bad, Range &r,
+                                          int &j, int &n1) {
+  j = a0 + p / W;
+  const int k = p % W;
+  double fj[3] = {frac[3 * j], frac[3 * j + 1], frac[3 * j + 2]};
+  r = pair_range(fi, fj, g.rw);
+  n1 = r.lo[0] + k;
+  int ce = 0;
+  cb = 0;
+  if (n1 > r.hi[0]) return 0;
+  for (int n2 = r.lo[1]; n2 <= r.hi[1]; ++n2)
+    for (int n3 = r.lo[2]; n3 <= r.hi[2]; ++n3) {
+      if (i == j && n1 == 0 && n2 == 0 && n3 == 0) continue;
+      double dx, dy, dz, q;
+      eval_pair(pos, L, i, j, n1, n2, n3, dx, dy, dz, q);
+      if (q <= ra2) {
+        ++ce;
+        cb += (q <= rb2);
+        bad |= (q < 1e-12);
+      }
+    }
+  return ce;
+}
+
+__global__ void __launch_bounds__(32 * GWPA) k_count(int N, const double *__restrict__ pos,
+                                                     const double *__restrict__ frac, const int32_t *__restrict__ soa,
+                                                     const int32_t *__restrict__ atom_ptr,
+                                                     const StructGeo *__restrict__ geo, double ra2, double rb2,
+                                                     int32_t *__restrict__ cnt_e, int32_t *__restrict__ cnt_b,
+                                                     int *flag) {
+  __shared__ int sh[GWPA][2];
+  const int i = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (i >= N) return;
+  const int s = soa[i];
+  const int a0 = atom_ptr[s], a1 = atom_ptr[s + 1];
   const StructGeo &g = geo[s];
   double L[9];
 #pragma unroll
   for (int k = 0; k < 9; ++k) L[k] = g.L[k];
-  double fi[3] = {frac[3 * i], frac[3 * i + 1], frac[3 * i + 2]};
-  // lanes walk (j, n1) slots: W >= any pair's n1-range width (pair_range: <= 2·rw + 4 values),
-  // so each lane runs only the n2 x n3 loops of one image row (more lanes busy, shorter chains)
+  const double fi[3] = {frac[3 * i], frac[3 * i + 1], frac[3 * i + 2]};
   const int W = (int)floor(2.0 * g.rw[0]) + 4;
   const int nslot = (a1 - a0) * W;
-  int ce = 0, cb = 0, bad = 0;
-  for (int p = lane; p < nslot; p += 32) {
-    const int j = a0 + p / W, k = p % W;
-    double fj[3] = {frac[3 * j], frac[3 * j + 1], frac[3 * j + 2]};
-    Range r = pair_range(fi, fj, g.rw);
-    const int n1 = r.lo[0] + k;
-    if (n1 > r.hi[0]) continue;
-    for (int n2 = r.lo[1]; n2 <= r.hi[1]; ++n2)
-      for (int n3 = r.lo[2]; n3 <= r.hi[2]; ++n3) {
-        if (i == j && n1 == 0 && n2 == 0 && n3 == 0) continue;
-        double dx, dy, dz, q;
-        eval_pair(pos, L, i, j, n1, n2, n3, dx, dy, dz, q);
-        if (q <= ra2) {
-          ++ce;
-          cb += (q <= rb2);
-          bad |= (q < 1e-12);
-        }
-      }
+  int ce = 0, cbt = 0, bad = 0;
+  for (int p = w * 32 + lane; p < nslot; p += 32 * GWPA) {
+    int cb, j, n1;
+    Range r;
+    ce += slot_count(pos, frac, L, g, fi, i, a0, W, p, ra2, rb2, cb, bad, r, j, n1);
+    cbt += cb;
   }
   ce = __reduce_add_sync(0xffffffffu, ce);
-  cb = __reduce_add_sync(0xffffffffu, cb);
+  cbt = __reduce_add_sync(0xffffffffu, cbt);
   bad = __any_sync(0xffffffffu, bad);
-  if (lane == 0) {
-    cnt_e[i] = ce;
-    cnt_b[i] = cb;
-    if (bad) atomicOr(flag, 4);
+  if (lane == 0) { sh[w][0] = ce; sh[w][1] = cbt; }
+  if (bad && lane == 0) atomicOr(flag, 4);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int te = 0, tb = 0;
+    for (int k = 0; k < GWPA; ++k) { te += sh[k][0]; tb += sh[k][1]; }
+    cnt_e[i] = te;
+    cnt_b[i] = tb;
   }
 }
 
@@ -223,55 +245,46 @@ __device__ __forceinline__ int warp_excl_scan(int v, int lane, int &total) {
   return x - v;
 }
 
-__global__ void k_fill(int N, const double *__restrict__ pos, const double *__restrict__ frac,
-                       const int32_t *__restrict__ soa, const int32_t *__restrict__ atom_ptr,
-                       const StructGeo *__restrict__ geo, double ra2, double rb2,
-                       const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ bond_ptr,
-                       int32_t *__restrict__ center, int32_t *__restrict__ nbr, char4 *__restrict__ img,
-                       float4 *__restrict__ vec, double4 *__restrict__ vec64, int32_t *__restrict__ bond_id,
-                       int32_t *__restrict__ bond_edge) {
-  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  if (warp >= N) return;
-  int i = warp;
-  int s = soa[i];
-  int a0 = atom_ptr[s], a1 = atom_ptr[s + 1];
+// Ordered emission, one 128-thread block per centre atom: rounds of 4 consecutive 32-slot
+// chunks (one per warp) — count, block-exclusive scan over the chunks in slot order, then the
+// warp-ordered emission of each chunk: the canonical (j, n1, n2, n3) order of the CSR row.
+__global__ void __launch_bounds__(32 * GWPA) k_fill(int N, const double *__restrict__ pos,
+                                                    const double *__restrict__ frac, const int32_t *__restrict__ soa,
+                                                    const int32_t *__restrict__ atom_ptr,
+                                                    const StructGeo *__restrict__ geo, double ra2, double rb2,
+                                                    const int32_t *__restrict__ row_ptr,
+                                                    const int32_t *__restrict__ bond_ptr, int32_t *__restrict__ center,
+                                                    int32_t *__restrict__ nbr, char4 *__restrict__ img,
+                                                    float4 *__restrict__ vec, double4 *__restrict__ vec64,
+                                                    int32_t *__restrict__ bond_id, int32_t *__restrict__ bond_edge) {
+  __shared__ int sh[GWPA][2];
+  const int i = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (i >= N) return;
+  const int s = soa[i];
+  const int a0 = atom_ptr[s], a1 = atom_ptr[s + 1];
   const StructGeo &g = geo[s];
   double L[9];
 #pragma unroll
   for (int k = 0; k < 9; ++k) L[k] = g.L[k];
-  double fi[3] = {frac[3 * i], frac[3 * i + 1], frac[3 * i + 2]};
+  const double fi[3] = {frac[3 * i], frac[3 * i + 1], frac[3 * i + 2]};
   int be = row_ptr[i], bb = bond_ptr[i];
-  // same (j, n1) slot walk as k_count; slots are in (j, n1) order and each lane's n2, n3
-  // loops are lexicographic, so a warp-ordered scan emits the canonical (j, n1, n2, n3) order
   const int W = (int)floor(2.0 * g.rw[0]) + 4;
   const int nslot = (a1 - a0) * W;
-  for (int p0 = 0; p0 < nslot; p0 += 32) {
-    const int p = p0 + lane;
-    int j = 0, n1 = 0, ce = 0, cb = 0;
+  for (int p0 = 0; p0 < nslot; p0 += 32 * GWPA) {
+    const int p = p0 + w * 32 + lane;
+    int j = 0, n1 = 0, ce = 0, cb = 0, bad = 0;
     Range r;
-    bool act = p < nslot;
-    if (act) {
-      j = a0 + p / W;
-      double fj[3] = {frac[3 * j], frac[3 * j + 1], frac[3 * j + 2]};
-      r = pair_range(fi, fj, g.rw);
-      n1 = r.lo[0] + p % W;
-      act = n1 <= r.hi[0];
-    }
-    if (act) {
-      for (int n2 = r.lo[1]; n2 <= r.hi[1]; ++n2)
-        for (int n3 = r.lo[2]; n3 <= r.hi[2]; ++n3) {
-          if (i == j && n1 == 0 && n2 == 0 && n3 == 0) continue;
-          double dx, dy, dz, q;
-          eval_pair(pos, L, i, j, n1, n2, n3, dx, dy, dz, q);
-          if (q <= ra2) { ++ce; cb += (q <= rb2); }
-        }
-    }
+    if (p < nslot) ce = slot_count(pos, frac, L, g, fi, i, a0, W, p, ra2, rb2, cb, bad, r, j, n1);
     int te, tb;
-    int oe = warp_excl_scan(ce, lane, te);
-    int ob = warp_excl_scan(cb, lane, tb);
-    if (act && ce > 0) {
-      int e = be + oe, b = bb + ob;
+    const int oe = warp_excl_scan(ce, lane, te);
+    const int ob = warp_excl_scan(cb, lane, tb);
+    __syncthreads();                                  // previous round's sh reads are done
+    if (lane == 0) { sh[w][0] = te; sh[w][1] = tb; }
+    __syncthreads();
+    int we = be, wb = bb;                             // offsets of this warp's chunk
+    for (int k = 0; k < w; ++k) { we += sh[k][0]; wb += sh[k][1]; }
+    if (ce > 0) {
+      int e = we + oe, b = wb + ob;
       for (int n2 = r.lo[1]; n2 <= r.hi[1]; ++n2)
         for (int n3 = r.lo[2]; n3 <= r.hi[2]; ++n3) {
           if (i == j && n1 == 0 && n2 == 0 && n3 == 0) continue;
@@ -295,8 +308,7 @@ __global__ void k_fill(int N, const double *__restrict__ pos, const double *__re
           }
         }
     }
-    be += te;
-    bb += tb;
+    for (int k = 0; k < GWPA; ++k) { be += sh[k][0]; bb += sh[k][1]; }
   }
 }
 
@@ -537,7 +549,7 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
       k_frac<<<ceil_div(N, 256), 256, 0, st>>>((int)N, d_pos, G->struct_of_atom, d_geo, G->species,
                                                 n_species, d_frac, flag);
       check_launch(ctx);
-      k_count<<<ceil_div(N * 32, 256), 256, 0, st>>>((int)N, d_pos, d_frac, G->struct_of_atom, G->atom_ptr,
+      k_count<<<(unsigned)N, 32 * GWPA, 0, st>>>((int)N, d_pos, d_frac, G->struct_of_atom, G->atom_ptr,
                                                       d_geo, ra2, rb2, cnt_e, cnt_b, flag);
       check_launch(ctx);
       k_scan<<<1, 1024, 0, st>>>((int)N, cnt_e, cnt_b, G->row_ptr, G->bond_ptr, G->atom_angle_ptr, d_tot);
@@ -591,7 +603,7 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
 
     ProfScope ps2(ctx, "graph", 0.0, 0.0);
     if (N) {
-      k_fill<<<ceil_div(N * 32, 256), 256, 0, st>>>((int)N, d_pos, d_frac, G->struct_of_atom, G->atom_ptr,
+      k_fill<<<(unsigned)N, 32 * GWPA, 0, st>>>((int)N, d_pos, d_frac, G->struct_of_atom, G->atom_ptr,
                                                      d_geo, ra2, rb2, G->row_ptr, G->bond_ptr, G->center,
                                                      G->nbr, G->img, G->vec, G->vec64, G->bond_id, G->bond_edge);
       check_launch(ctx);

@@ -12,7 +12,7 @@
 //            added into the caller's gradient rows; dW_k, db_k are accumulated in
 //            registers / fixed smem slots across the CTA's tiles and written once as a
 //            per-CTA partial in the flat layout of the head's parameter block, reduced
-//            by k_head_reduce in CTA order (deterministic, no atomics).
+//            in a fixed order by the batched reduction (reduce.cu; deterministic, no atomics).
 //
 // Register tiling: 256 threads, thread (a = t / 16, b = t % 16) owns a 4 x 4 block.
 // Shared tiles are [64][65] (odd pitch: column walks are conflict-free).
@@ -310,15 +310,6 @@ __global__ void __launch_bounds__(256) k_head_bwd(const __grid_constant__ HeadAr
   if (t < NOUT) Lp[64 * NOUT + t] = gbL;
 }
 
-// G[i] += Σ_c part[c][i] in CTA order (deterministic)
-__global__ void k_head_reduce(const float *__restrict__ part, int nctas, int n, int stride, float *__restrict__ G) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  float s = 0.f;
-  for (int c = 0; c < nctas; ++c) s += part[(size_t)c * stride + i];
-  G[i] += s;
-}
-
 template <int NL, int NOUT>
 size_t head_smem_fwd() { return 4 * ((size_t)HeadSmem<NL, NOUT>::T0 + HT * HP); }
 template <int NL, int NOUT>
@@ -362,16 +353,16 @@ void run_bwd(chg_ctx *ctx, HeadArgs a, float *G, const char *tag) {
   const int grid = (int)std::min<int64_t>(ntiles, 2 * sm_count());
   const int nb = head_block_size(NL, NOUT);
   const int stride = head_part_stride(NL, NOUT);
-  a.part = ctx->getf(ctx->ws_name("head_part"), (size_t)grid * stride);
+  a.part = red_partial(ctx, (size_t)grid * stride);
   {
     ProfScope ps(ctx, tag, 2.0 * a.rows * (2.0 * 64 * 64 * (NL - 1) + 2.0 * 64 * NOUT),
                  a.rows * 4.0 * (64 * 3 + 64 * (NL - 1) + NOUT) + 4.0 * nb * (double)grid * 2);
     k_head_bwd<NL, NOUT><<<grid, 256, smem, ctx->stream>>>(a);
     check_launch(ctx);
   }
-  ProfScope ps(ctx, "head_reduce", 0.0, 4.0 * nb * (grid + 2.0));
-  k_head_reduce<<<ceil_div(nb, 256), 256, 0, ctx->stream>>>(a.part, grid, nb, stride, G);
-  check_launch(ctx);
+  RedJob j;                                        // per-CTA partials -> the head's gradient block
+  j.kind = 1; j.n = nb; j.splits = grid; j.stride = stride; j.part = a.part; j.W[0] = G;
+  red_push(ctx, j);
 }
 
 }  // namespace

@@ -576,6 +576,12 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
   if (!lab_in->energy_per_atom || !lab_in->forces || !lab_in->stress || !lab_in->magmom || !lab_in->magmom_mask)
     CHG_THROW(CHG_ERR_ARG, "all label arrays are required");
   Bwd Bw{ctx, m, g, nullptr};
+  // split-partial reductions of a layer are batched into one launch (reduce.cu)
+  struct RedScope {
+    chg_ctx *c;
+    explicit RedScope(chg_ctx *x) : c(x) { c->red_on = true; c->red_jobs.clear(); }
+    ~RedScope() { c->red_on = false; c->red_jobs.clear(); }
+  } red_scope(ctx);
   chg_labels lab = *lab_in;
   lab.energy_per_atom = labels_dev(ctx, lab_in->energy_per_atom, 4 * S, "lab_epa", lab_in->on_device);
   lab.forces = labels_dev(ctx, lab_in->forces, 12 * N, "lab_f", lab_in->on_device);
@@ -636,6 +642,7 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
   ac_bwd_head(Bw, T, dv, dagg);
   join_side(ctx);                                   // de complete before the atom conv adds to it
   ac_bwd_body(Bw, T, V(T), Ef(T), ea, dagg, dv, de, dea);
+  red_flush(ctx);
   for (int t = T - 1; t >= 0; --t) {
     bool ab = t + 1 < T;
     // both output linears read the incoming gradients before any update
@@ -661,6 +668,7 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
       CUDA_OK(cudaStreamWaitEvent(main_stream, ctx->ev_join, 0));
     }
     bc_bwd_body(Bw, t, ab, V(t), Ef(t), Af(t), eb, daggb, dv, de, da, deb, 2);
+    red_flush(ctx);
   }
   // embedding (rows of W_v gathered by species -> grouped sum, no atomics)
   species_grad(ctx, N, m->cfg.n_species, g->species_ptr, g->species_perm, dv, Bw.G("embed.W"));
@@ -671,6 +679,7 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
            Bw.G("rbf_b.freq"));
   proj_bwd(ctx, A, Bw.act("a_t"), nullptr, da, nullptr, m->p("proj.Wtheta"), nullptr, Bw.G("proj.Wtheta"), nullptr,
            nullptr);
+  red_flush(ctx);
   if (loss_out) {
     double *h = (double *)ctx->pinned_get(64);
     CUDA_OK(cudaMemcpyAsync(h, ctx->d_loss, 5 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));

@@ -61,21 +61,22 @@ __global__ void k_basis_freq_grad(int64_t rows, const double4 *__restrict__ vec,
   }
 }
 
-// fixed-order column reduction of per-block partials (see k_wgrad_reduce)
-__global__ void __launch_bounds__(256) k_reduce_cols(int nblocks, int ncols, int stride,
-                                                     const float *__restrict__ partial, float *__restrict__ grad) {
-  __shared__ float sh[8][32];
+// fixed-order column reduction of per-block partials (same order as reduce.cu)
+__global__ void __launch_bounds__(1024) k_reduce_cols(int nblocks, int ncols, int stride,
+                                                      const float *__restrict__ partial, float *__restrict__ grad) {
+  __shared__ float sh[32][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int j = blockIdx.x * 32 + lane;
   float s = 0.f;
   if (j < ncols)
-    for (int b = w; b < nblocks; b += 8) s += partial[(size_t)b * stride + j];
+#pragma unroll 4
+    for (int b = w; b < nblocks; b += 32) s += partial[(size_t)b * stride + j];
   sh[w][lane] = s;
   __syncthreads();
   if (w == 0 && j < ncols) {
     float t = 0.f;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) t += sh[k][lane];
+    for (int k = 0; k < 32; ++k) t += sh[k][lane];
     grad[j] += t;
   }
 }
@@ -222,23 +223,6 @@ __global__ void __launch_bounds__(256) k_gate_bwd(int64_t rows, int64_t rpb, con
   float s = 0.f;
   for (int k = 0; k < 8; ++k) s += sh[k][threadIdx.x];
   partial[blockIdx.x * 256 + threadIdx.x] = s;
-}
-
-__global__ void __launch_bounds__(256) k_reduce_ln(int nblocks, const float *__restrict__ partial, GateLNGrad g) {
-  __shared__ float sh[8][32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int j = blockIdx.x * 32 + lane;           // 0..255
-  float s = 0.f;
-  for (int b = w; b < nblocks; b += 8) s += partial[(size_t)b * 256 + j];
-  sh[w][lane] = s;
-  __syncthreads();
-  if (w == 0) {
-    float t = 0.f;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) t += sh[k][lane];
-    float *dst = j < 64 ? g.gc : j < 128 ? g.bc : j < 192 ? g.gg : g.bg;
-    dst[j & 63] += t;
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -584,7 +568,7 @@ void basis_freq_grad(chg_ctx *ctx, int64_t rows, const double4 *vec64, const int
   ProfScope ps(ctx, "basis_bwd", 0.0, rows * (4.0 + 32.0 + 128.0));
   k_basis_freq_grad<<<nb, 256, 0, ctx->stream>>>(rows, vec64, eor, freq, rc, p, dbasis, part);
   check_launch(ctx);
-  k_reduce_cols<<<1, 256, 0, ctx->stream>>>(nb, CHG_K, 32, part, grad);
+  k_reduce_cols<<<1, 1024, 0, ctx->stream>>>(nb, CHG_K, 32, part, grad);
   check_launch(ctx);
 }
 
@@ -602,14 +586,16 @@ void gate_bwd(chg_ctx *ctx, int64_t rows, const float *y, int ldy, GateLN ln, in
   int64_t rpb = std::max<int64_t>(64, (rows + 591) / 592);
   int nb = rows > 0 ? ceil_div(rows, rpb) : 0;
   if (nb == 0) return;
-  float *part = ctx->getf(ctx->ws_name("ln_partial"), (size_t)nb * 256);
+  float *part = red_partial(ctx, (size_t)nb * 256);
   ProfScope ps(ctx, "gate_bwd", 0.0,
                rows * (512.0 + 260.0 + 512.0 + (mode == GATE_MUL_W ? 768.0 : mode == GATE_MUL_W1W2 ? 1032.0 : 0.0)));
   k_gate_bwd<<<nb, 256, 0, ctx->stream>>>(rows, rpb, y, ldy, ln, mode, w, i1, i2, dout, didx, dy, lddy, dw_acc, q1,
                                           q2, part);
   check_launch(ctx);
-  k_reduce_ln<<<8, 256, 0, ctx->stream>>>(nb, part, g);
-  check_launch(ctx);
+  RedJob j;                                        // LN affine gradients: batched reduction (reduce.cu)
+  j.kind = 2; j.n = 256; j.splits = nb; j.stride = 256; j.part = part;
+  j.W[0] = g.gc; j.W[1] = g.bc; j.W[2] = g.gg; j.W[3] = g.bg;
+  red_push(ctx, j);
 }
 
 void segsum(chg_ctx *ctx, int64_t targets, float *out, int ldo, int accumulate, int nsrc, const SegSrc *src,
@@ -667,12 +653,15 @@ void colsum(chg_ctx *ctx, int64_t rows, const float *D, float *grad) {
   if (rows <= 0) return;
   const int64_t rpb = std::max<int64_t>(64, (rows + 295) / 296);
   const int nb = ceil_div(rows, rpb);
-  float *part = ctx->getf("colsum_part", (size_t)nb * 64);
-  ProfScope ps(ctx, "colsum", 0.0, rows * 256.0 + nb * 512.0);
-  k_colsum_partial<<<nb, 256, 0, ctx->stream>>>(rows, rpb, D, part);
-  check_launch(ctx);
-  k_reduce_cols<<<2, 256, 0, ctx->stream>>>(nb, 64, 64, part, grad);
-  check_launch(ctx);
+  float *part = red_partial(ctx, (size_t)nb * 64);
+  {
+    ProfScope ps(ctx, "colsum", 0.0, rows * 256.0 + nb * 256.0);
+    k_colsum_partial<<<nb, 256, 0, ctx->stream>>>(rows, rpb, D, part);
+    check_launch(ctx);
+  }
+  RedJob j;
+  j.kind = 1; j.n = 64; j.splits = nb; j.stride = 64; j.part = part; j.W[0] = grad;
+  red_push(ctx, j);
 }
 
 void heads_forces(chg_ctx *ctx, const chg_graph *g, const float *n_e, float *forces) {

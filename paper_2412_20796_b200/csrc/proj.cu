@@ -243,27 +243,6 @@ __global__ void __launch_bounds__(256) k_proj_bwd(const __grid_constant__ ProjBw
     }
 }
 
-// dW[n][c] += Σ_cta partW[cta][n][c] (n < 31): a block owns 32 outputs, warp w sums CTAs
-// w, w+8, ... and warp 0 adds the 8 subtotals in order (deterministic)
-__global__ void __launch_bounds__(256) k_proj_reduce_w(const float *__restrict__ partW, int nctas, int C, float *G0,
-                                                       float *G1) {
-  __shared__ float sh[8][32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int i = blockIdx.x * 32 + lane;
-  float s = 0.f;
-  if (i < CHG_K * C)
-    for (int k = w; k < nctas; k += 8) s += partW[(size_t)k * 32 * C + i];
-  sh[w][lane] = s;
-  __syncthreads();
-  if (w != 0 || i >= CHG_K * C) return;
-  float tsum = 0.f;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) tsum += sh[k][lane];
-  const int n = i / C, c = i % C;
-  float *G = c < 64 ? G0 : G1;
-  G[n * 64 + (c & 63)] += tsum;
-}
-
 // ∂L/∂f_n += Σ_c W[n][c] · Σ_cta partH[cta][n][c]: block n (1024 threads), thread (split, c);
 // splits of the CTA range, combined in order, then a fixed-order tree over c
 __global__ void __launch_bounds__(1024) k_proj_reduce_f(const double *__restrict__ partH, int nctas, int C,
@@ -335,7 +314,7 @@ void proj_bwd(chg_ctx *ctx, int64_t rows, const float *basis, const float *dbdf,
   const int grid = (int)std::min<int64_t>((rows + PTB - 1) / PTB, 2 * sm_count_p());
   ProjBwd a{};
   a.rows = rows; a.basis = basis; a.dbdf = dbdf; a.dE[0] = dE0; a.dE[1] = dE1;
-  a.partW = ctx->getf("proj_partW", (size_t)grid * 32 * C);
+  a.partW = red_partial(ctx, (size_t)grid * 32 * C);
   a.partH = radial ? (double *)ctx->get("proj_partH", (size_t)grid * 32 * C * 8) : nullptr;
   {
     ProfScope ps(ctx, "proj_bwd", 2.0 * rows * CHG_K * C * (radial ? 2 : 1),
@@ -346,10 +325,12 @@ void proj_bwd(chg_ctx *ctx, int64_t rows, const float *basis, const float *dbdf,
     else CHG_THROW(CHG_ERR_ARG, "proj_bwd: unsupported shape");
     check_launch(ctx);
   }
-  ProfScope ps(ctx, "proj_reduce", 0.0, grid * 32.0 * C * (radial ? 12 : 4));
-  k_proj_reduce_w<<<ceil_div(CHG_K * C, 32), 256, 0, ctx->stream>>>(a.partW, grid, C, G0, G1);
-  check_launch(ctx);
+  RedJob j;                                        // dW: batched reduction (reduce.cu)
+  j.kind = 3; j.n = CHG_K * C; j.N = C; j.splits = grid; j.stride = 32 * C; j.part = a.partW;
+  j.W[0] = G0; j.W[1] = G1;
+  red_push(ctx, j);
   if (radial) {
+    ProfScope ps(ctx, "proj_reduce", 0.0, grid * 32.0 * C * 8);
     k_proj_reduce_f<<<CHG_K, 1024, 0, ctx->stream>>>(a.partH, grid, C, W0, W1, dfreq);
     check_launch(ctx);
   }

@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
 //   Stage = 32 rows m: A_T [Kpad rows][128 B], D_T [N rows][128 B], SWIZZLE_128B.
 //   Rows are split across persistent CTAs; each CTA accumulates its k tiles
 //   (M = 128, ≤ 2) × N in TMEM and writes one partial [Kp][N]; partials are
-//   reduced in a fixed order by k_wgrad_reduce (gemm.cu).  When K % 128 != 0 a
+//   reduced in a fixed order by the batched reduction (reduce.cu).  When K % 128 != 0 a
 //   bias (column sums of D) is summed by the producers from the staged K-major D rows.
 //   Warps 0-11 produce, warp 12 issues MMAs, warps 0-3 run the epilogue.
 // ---------------------------------------------------------------------------
@@ -885,7 +885,7 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
 }
 
 // Weight gradient on tcgen05 (TF32).  Returns false when the shape does not fit
-// (caller uses the SIMT kernel).  Writes partials [splits][Kp][N] for k_wgrad_reduce.
+// (caller uses the SIMT kernel).  Writes partials [splits][Kp][N] for the batched reduction (reduce.cu).
 bool wgrad_tc(chg_ctx *ctx, const WGrad &g, float **partial_out, int *Kp_out, int *splits_out, bool *bias_done) {
   if (g.M <= 0 || g.K <= 0 || g.K % 32 || g.N % 32 || g.N > 256 || g.K > 256 || (g.ldd % 4)) return false;
   if ((uintptr_t)g.D & 15) return false;
@@ -912,7 +912,7 @@ bool wgrad_tc(chg_ctx *ctx, const WGrad &g, float **partial_out, int *Kp_out, in
   const int grid = std::max(1, std::min(sms, chunks));
   P.rows_per_cta = (chunks + grid - 1) / grid * 32;
   const int splits = (g.M + P.rows_per_cta - 1) / P.rows_per_cta;
-  float *partial = ctx->getf(ctx->ws_name("wgrad_partial"), (size_t)splits * P.Kp * g.N);
+  float *partial = red_partial(ctx, (size_t)splits * P.Kp * g.N);
   const size_t st_bytes = (size_t)(P.Kpad + P.Npad) * 128;
   const size_t smem = 1024 + WG_NST * st_bytes + 8 * (2 * WG_NST + 1) + 16 + 4 * 32 * 33 * 4 + WG_NPW * 256 * 4;
   if (smem > 224 * 1024) return false;

@@ -19,7 +19,8 @@ for r in rows:
     d = per.setdefault(launch, {"name": name})
     v = float(r["Metric Value"].replace(",", ""))
     unit = r["Metric Unit"]
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3}.get(unit, 1)
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3,
+             "ns": 1e-3, "us": 1, "ms": 1e3}.get(unit, 1)
     d[r["Metric Name"]] = v * scale
 agg = OrderedDict()
 for (_, name), d in per.items():
