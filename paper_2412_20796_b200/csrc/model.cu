@@ -91,19 +91,10 @@ void atom_conv_fwd(Fwd &F, int t, const float *v, const float *e, const float *e
   }
   // m_e = eᵃ_e ⊙ σ(LN_g(y_g)) ⊙ SiLU(LN_c(y_c))
   gate_fwd(ctx, E, y, 128, F.ln(pre), GATE_MUL_W, ea, nullptr, nullptr, nullptr, msg);
+  // agg_i = Σ_{e at centre i} m_e and v' = v + agg · W_out + b_out in one pass
   SegSrc s;
   s.in = msg; s.ptr = g->row_ptr; s.rows = E;
-  segsum(ctx, N, agg, 64, 0, 1, &s, "segsum_ac");
-  {  // v' = v + agg · W_out + b_out
-    RowGemm G;
-    G.A.seg[0] = aseg(agg, 64, 64);
-    G.A.nseg = 1;
-    G.M = (int)N; G.K = 64; G.nchunk = 1;
-    G.ch[0] = chunk1(m->p(pre + ".out.W"), 64, 64, m->p(pre + ".out.b"), v_out, 64);
-    G.ch[0].resid = v; G.ch[0].ldr = 64;
-    G.tag = "ac_fout";
-    rowgemm(ctx, G);
-  }
+  segsum_linear(ctx, N, 1, &s, agg, m->p(pre + ".out.W"), m->p(pre + ".out.b"), v, v_out, "segsum_ac");
 }
 
 // --- Bond Conv (Eq. 5) + Angle Update (Eq. 6) with Eq. 11 inputs ------------
@@ -149,19 +140,12 @@ void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float
     // q = eᵇ_ij ⊙ eᵇ_ik ⊙ φ_e
     gate_fwd(ctx, A, yb, 128, F.ln(bp), GATE_MUL_W1W2, eb, g->angle_b1, g->angle_b2, nullptr, q);
   }
-  SegSrc s;
-  s.in = q; s.ptr = g->angle_ptr; s.rows = A;
-  segsum(ctx, B, aggb, 64, 0, 1, &s, "segsum_bc");      // Σ over angles with first bond b (empty -> 0)
-  {  // e' = e + 𝓛_e(agg) on all E edges (Q16): the product only for the B bond rows, then every
-     // edge gets its bond row (or nothing) + the bias
+  {  // aggb = Σ over angles with first bond b (empty -> 0) fused with its product by W_out (B
+     // bond rows only); then e' = e + 𝓛_e(agg) on all E edges (Q16): bond row (or nothing) + bias
     float *tmp = ctx->getf("bc_out_tmp", (size_t)std::max<int64_t>(B, 1) * 64);
-    RowGemm G;
-    G.A.seg[0] = aseg(aggb, 64, 64);
-    G.A.nseg = 1;
-    G.M = (int)B; G.K = 64; G.nchunk = 1;
-    G.ch[0] = chunk1(m->p(bp + ".out.W"), 64, 64, nullptr, tmp, 64);
-    G.tag = "bc_fout";
-    rowgemm(ctx, G);
+    SegSrc s;
+    s.in = q; s.ptr = g->angle_ptr; s.rows = A;
+    segsum_linear(ctx, B, 1, &s, aggb, m->p(bp + ".out.W"), nullptr, nullptr, tmp, "segsum_bc");
     edge_update(ctx, E, e, m->p(bp + ".out.b"), g->bond_id, tmp, e_out);
   }
   if (angle_branch && A > 0)   // a' = a + φ_a

@@ -300,6 +300,91 @@ __global__ void __launch_bounds__(256) k_segsum(int64_t targets, float *__restri
   *o = acc;
 }
 
+// Segmented sum fused with the 64x64 output linear that consumes it (Eq. 4 𝓛_v, Eq. 5 𝓛_e):
+// agg_t = Σ rows (as k_segsum<H>, stored for the backward), out_t = (agg_t·W + b) + resid_t.
+// W sits in shared memory; the half-warp holding agg_t broadcasts its 64 values by shuffle.
+template <int H>
+__global__ void __launch_bounds__(256) k_segsum_linear(int64_t targets, SegArgs a, float *__restrict__ agg,
+                                                       const float *__restrict__ W, const float *__restrict__ bias,
+                                                       const float *__restrict__ resid, float *__restrict__ out) {
+  __shared__ __align__(16) float sW[64][64];
+  __shared__ float4 part[16][16];
+  for (int i = threadIdx.x; i < 64 * 64; i += 256) sW[i >> 6][i & 63] = W[i];
+  __syncthreads();
+  const int hw = threadIdx.x >> 4;
+  const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / (16 * H);
+  const int j = hw % H;
+  const int lane = threadIdx.x & 31, hl = lane & 15;
+  const unsigned hmask = 0xffffu << (lane & 16);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (t < targets) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (k >= a.n) break;
+      const SegSrc &S = a.s[k];
+      const int64_t sg = S.segmap ? (int64_t)__ldg(S.segmap + t) : t + S.ptr_off;
+      if (sg < 0) continue;
+      int r0 = __ldg(S.ptr + sg), r1 = __ldg(S.ptr + sg + 1);
+      if (H > 1) {
+        const int len = r1 - r0;
+        const int a0 = r0 + (int)((int64_t)len * j / H), a1 = r0 + (int)((int64_t)len * (j + 1) / H);
+        r0 = a0; r1 = a1;
+      }
+      const float4 *in = (const float4 *)S.in + hl;
+      for (int base = r0; base < r1; base += 16) {
+        const int n = min(16, r1 - base);
+        const int myrow = hl < n ? (S.perm ? __ldg(S.perm + base + hl) : base + hl) : 0;
+        int q = 0;
+        for (; q + 4 <= n; q += 4) {
+          const int q0 = __shfl_sync(hmask, myrow, q, 16), q1 = __shfl_sync(hmask, myrow, q + 1, 16);
+          const int q2 = __shfl_sync(hmask, myrow, q + 2, 16), q3 = __shfl_sync(hmask, myrow, q + 3, 16);
+          const float4 v0 = __ldg(in + (int64_t)q0 * 16), v1 = __ldg(in + (int64_t)q1 * 16);
+          const float4 v2 = __ldg(in + (int64_t)q2 * 16), v3 = __ldg(in + (int64_t)q3 * 16);
+          acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
+          acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w;
+          acc.x += v2.x; acc.y += v2.y; acc.z += v2.z; acc.w += v2.w;
+          acc.x += v3.x; acc.y += v3.y; acc.z += v3.z; acc.w += v3.w;
+        }
+        for (; q < n; ++q) {
+          const int qq = __shfl_sync(hmask, myrow, q, 16);
+          const float4 v = __ldg(in + (int64_t)qq * 16);
+          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+      }
+    }
+  }
+  if (H > 1) {
+    part[hw][hl] = acc;
+    __syncthreads();
+    if (j != 0 || t >= targets) return;
+#pragma unroll
+    for (int q = 1; q < H; ++q) {
+      const float4 p = part[hw + q][hl];
+      acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w;
+    }
+  } else if (t >= targets) {
+    return;
+  }
+  ((float4 *)(agg + t * 64))[hl] = acc;
+  float o[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int k = 0; k < 64; ++k) {
+    const float c = (k & 3) == 0 ? acc.x : (k & 3) == 1 ? acc.y : (k & 3) == 2 ? acc.z : acc.w;
+    const float ak = __shfl_sync(hmask, c, k >> 2, 16);
+    const float4 w = *(const float4 *)&sW[k][4 * hl];
+    o[0] = fmaf(ak, w.x, o[0]); o[1] = fmaf(ak, w.y, o[1]); o[2] = fmaf(ak, w.z, o[2]); o[3] = fmaf(ak, w.w, o[3]);
+  }
+  if (bias) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) o[q] += __ldg(bias + 4 * hl + q);
+  }
+  if (resid) {
+    const float4 r = __ldg((const float4 *)(resid + t * 64) + hl);
+    o[0] += r.x; o[1] += r.y; o[2] += r.z; o[3] += r.w;
+  }
+  ((float4 *)(out + t * 64))[hl] = make_float4(o[0], o[1], o[2], o[3]);
+}
+
 // Embedding gradient dW_v[z] += Σ_{i: Z_i = z+1} dv_i (Eq. 2 adjoint) in two fixed-order
 // passes: (1) block (c, z) sums rows [64c, 64c+64) of species z's segment (thread = column),
 // (2) block z adds its chunk partials in chunk order.  Long segments (oxygen) are split
@@ -624,6 +709,32 @@ void segsum(chg_ctx *ctx, int64_t targets, float *out, int ldo, int accumulate, 
     case 4: k_segsum<4><<<grid, 256, 0, ctx->stream>>>(targets, out, ldo, accumulate, a); break;
     case 2: k_segsum<2><<<grid, 256, 0, ctx->stream>>>(targets, out, ldo, accumulate, a); break;
     default: k_segsum<1><<<grid, 256, 0, ctx->stream>>>(targets, out, ldo, accumulate, a); break;
+  }
+  check_launch(ctx);
+}
+
+void segsum_linear(chg_ctx *ctx, int64_t targets, int nsrc, const SegSrc *src, float *agg, const float *W,
+                   const float *bias, const float *resid, float *out, const char *tag) {
+  if (targets <= 0) return;
+  SegArgs a;
+  a.n = nsrc;
+  double bytes = targets * (256.0 * (2 + (resid ? 1 : 0)));
+  int64_t rows = 0;
+  for (int k = 0; k < nsrc; ++k) {
+    a.s[k] = src[k];
+    rows += src[k].rows;
+    bytes += src[k].rows * (256.0 + (src[k].perm ? 4.0 : 0.0)) + targets * (src[k].segmap ? 12.0 : 8.0);
+    if ((uintptr_t)src[k].in & 15) CHG_THROW(CHG_ERR_STATE, "segsum_linear: 16-byte alignment required");
+  }
+  const int64_t mean = rows / std::max<int64_t>(targets, 1);
+  const int H = mean >= 96 ? 8 : mean >= 48 ? 4 : mean >= 24 ? 2 : 1;
+  ProfScope ps(ctx, tag, 2.0 * targets * 64 * 64, bytes);
+  const int grid = ceil_div(targets * 16 * H, 256);
+  switch (H) {
+    case 8: k_segsum_linear<8><<<grid, 256, 0, ctx->stream>>>(targets, a, agg, W, bias, resid, out); break;
+    case 4: k_segsum_linear<4><<<grid, 256, 0, ctx->stream>>>(targets, a, agg, W, bias, resid, out); break;
+    case 2: k_segsum_linear<2><<<grid, 256, 0, ctx->stream>>>(targets, a, agg, W, bias, resid, out); break;
+    default: k_segsum_linear<1><<<grid, 256, 0, ctx->stream>>>(targets, a, agg, W, bias, resid, out); break;
   }
   check_launch(ctx);
 }

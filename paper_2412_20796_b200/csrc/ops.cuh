@@ -33,6 +33,11 @@ struct SegSrc { const float *in = nullptr; const int32_t *ptr = nullptr; const i
 void segsum(chg_ctx *ctx, int64_t targets, float *out, int ldo, int accumulate, int nsrc, const SegSrc *src,
             const char *tag = "segsum");
 
+// segmented sum fused with the 64x64 linear that consumes it: agg = Σ rows (stored),
+// out = (agg·W + bias) + resid (bias / resid optional); W row-major [64][64]
+void segsum_linear(chg_ctx *ctx, int64_t targets, int nsrc, const SegSrc *src, float *agg, const float *W,
+                   const float *bias, const float *resid, float *out, const char *tag);
+
 // embedding gradient: dW[z] += Σ_{i: Z_i = z+1} dv[i] over the species-sorted atom list
 // (species_ptr has n_species + 2 entries, segment of Z at [ptr[Z], ptr[Z+1])); deterministic
 void species_grad(chg_ctx *ctx, int64_t N, int n_species, const int32_t *species_ptr, const int32_t *species_perm,
