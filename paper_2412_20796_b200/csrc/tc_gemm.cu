@@ -15,6 +15,8 @@
 //   A (gathered activations): 256 threads, 8 lanes per row (coalesced 128-B
 //     row segments), registers prefetch the next K chunk while the tensor core
 //     runs the current one; 2-stage smem ring, tcgen05.commit -> mbarrier.
+#include <cuda.h>
+
 #include "gemm.cuh"
 
 namespace {
@@ -119,6 +121,21 @@ __device__ __forceinline__ float4 tc_loadA4(const AOp &A, int m, int col) {
   return v;
 }
 
+// TMA descriptors of the direct (non-gathered) A segments: one 32-column x 128-row box per
+// stage lands, 128B-swizzled, exactly where the UMMA descriptor expects it
+struct TcMaps {
+  CUtensorMap m[4];
+  int use[4];                      // 1: segment s is loaded by TMA
+};
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
 struct TcPlan {
   int lo;            // first A column of the union window
   int width;         // union window width (multiple of KC)
@@ -126,6 +143,9 @@ struct TcPlan {
   int coff[4];       // TMEM / image column offset of each chunk (multiple of 32)
   int ntot;          // total image rows N
   uint32_t tmem_cols;
+  int bst;           // B smem slots: NSB (ring, one K chunk each) or nkc (whole image resident)
+  int nsa;           // A stages
+  int bres;          // 1: the whole weight image is loaded once per CTA (no per-stage B traffic)
 };
 
 // B image: img[kc][q][n][4] = tf32(W_chunk(n - coff, k = lo + kc·KC - a_k0 + 4q + r))
@@ -179,7 +199,7 @@ __global__ void k_pack_b(const RowGemm g, const TcPlan P, uint32_t *__restrict__
 //   warps 10-13 epilogue: tcgen05.ld (one lane = one row) -> bias / act /
 //               pre / mul / resid -> global
 // ---------------------------------------------------------------------------
-constexpr int NSA = 5;              // A stages (16 KB each)
+constexpr int NSA_MAX = 10;         // A stages (16 KB each): P.nsa <= NSA_MAX, as many as shared memory allows
 constexpr int NSB = 3;              // B stages (<= 32 KB each)
 constexpr int WS_THREADS = 18 * 32;  // 8 A-producer, 1 B, 1 MMA, 8 epilogue warps
 constexpr int NEPI = 8;
@@ -259,16 +279,17 @@ __device__ __noinline__ void epi_rows_any(const Chunk &C, int act, const float *
 
 __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_constant__ RowGemm g, const TcPlan P,
                                                                const uint32_t *__restrict__ bimg, int ntiles,
-                                                               int skip) {
+                                                               int skip, const __grid_constant__ TcMaps TM) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // SWIZZLE_128B operand atoms need 1024-B aligned stage bases
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int NT = P.ntot;
   const uint32_t a_bytes = KC * TCM * 4, b_bytes = KC * NT * 4;
+  const int NSA = P.nsa;
   uint8_t *sA = smem;                                   // [NSA][a_bytes]
-  uint8_t *sB = smem + NSA * a_bytes;                   // [NSB][b_bytes]
-  uint64_t *fullA = (uint64_t *)(sB + NSB * b_bytes);
+  uint8_t *sB = smem + NSA * a_bytes;                   // [P.bst][b_bytes]
+  uint64_t *fullA = (uint64_t *)(sB + P.bst * b_bytes);
   uint64_t *emptyA = fullA + NSA;
   uint64_t *loaded = emptyA + NSA;                      // cp.async completion per A stage
   uint64_t *fullB = loaded + NSA;
@@ -276,7 +297,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
   uint64_t *tfull = emptyB + NSB;
   uint64_t *tempty = tfull + 2;
   uint32_t *tslot = (uint32_t *)(tempty + 2);
-  float *epi = (float *)(smem + NSA * a_bytes + NSB * b_bytes + 8 * (3 * NSA + 2 * NSB + 4) + 16);  // [8][32][33]
+  float *epi = (float *)(smem + NSA * a_bytes + P.bst * b_bytes + 8 * (3 * NSA + 2 * NSB + 4) + 16);  // [8][32][33]
   const uint32_t tcols = P.tmem_cols;                   // per accumulator buffer
 
   if (warp == 0) {
@@ -341,6 +362,21 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
       const ASeg S = g.A.seg[seg];
       const int cin = col - start + 4 * q;
       const uint32_t dst0 = smem_u32(sA + sa * a_bytes);
+      bool tma = false;
+#pragma unroll
+      for (int sg = 0; sg < 4; ++sg)
+        if (sg == seg) tma = TM.use[sg] != 0;
+      if (tma) {                                       // one 16 KB box; the other 127 threads just arrive
+        if (tid == 0) {
+          mbar_expect_tx(&loaded[sa], a_bytes);
+#pragma unroll
+          for (int sg = 0; sg < 4; ++sg)
+            if (sg == seg) tma_load_2d(dst0, &TM.m[sg], col - start, tile * TCM, &loaded[sa]);
+        } else {
+          mbar_arrive(&loaded[sa]);
+        }
+        continue;
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         int r = -1;
@@ -354,6 +390,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
         else cp_async16(dst, g.A.seg[0].base, 0);     // zero fill
       }
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&loaded[sa])) : "memory");
+      if ((skip & 32) && tid == 0 && gi < 30) {       // debug trace: loader cadence
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        trace_ld[gi] = t;
+      }
     }
   } else if (warp >= 4 && warp < 8) {
     // ---------------- A converters: thread = row; SiLU (GEMM2 input) + TF32 RN in place ----------------
@@ -372,13 +413,28 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
           row[kk] = make_uint4(to_tf32(v.x), to_tf32(v.y), to_tf32(v.z), to_tf32(v.w));
         }
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (!(skip & 64)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // debug knob 64: no fence
       __syncwarp();
       if (lane == 0) mbar_arrive(&fullA[sa]);        // one arrival per converter warp
+      if ((skip & 32) && tid == 128 && gi < 30) {     // debug trace: converter cadence
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        trace_cv[gi] = t;
+      }
     }
   } else if (warp == 8) {
     // ---------------- B producer ----------------
-    if (lane == 0) {
+    if (lane == 0 && P.bres) {                          // whole image once: one barrier, nkc bulk copies
+      if (total > 0) {
+        if (skip & 4) {
+          mbar_arrive(&fullB[0]);
+        } else {
+          mbar_expect_tx(&fullB[0], b_bytes * nkc);
+          for (int kc = 0; kc < nkc; ++kc)
+            bulk_g2s(sB + kc * b_bytes, bimg + (size_t)kc * NT * KC, b_bytes, &fullB[0]);
+        }
+      }
+    } else if (lane == 0) {
       for (int gi = 0; gi < total; ++gi) {
         const int kc = gi % nkc, sb = gi % NSB, ub = gi / NSB;
         if (ub > 0) mbar_wait(&emptyB[sb], (ub - 1) & 1);
@@ -400,9 +456,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         bool started[4] = {false, false, false, false};
         for (int kc = 0; kc < nkc; ++kc, ++gi) {
-          const int sa = gi % NSA, ua = gi / NSA, sb = gi % NSB, ub = gi / NSB;
+          const int sa = gi % NSA, ua = gi / NSA, sb = P.bres ? kc : gi % NSB, ub = gi / NSB;
           mbar_wait(&fullA[sa], ua & 1);
-          mbar_wait(&fullB[sb], ub & 1);
+          if (!P.bres) mbar_wait(&fullB[sb], ub & 1);
+          else if (gi == 0) mbar_wait(&fullB[0], 0);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t a_base = smem_u32(sA + sa * a_bytes), b_base = smem_u32(sB + sb * b_bytes);
           const int col0 = P.lo + kc * KC;
@@ -421,7 +478,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
             started[c] = true;
           }
           mma_commit(&emptyA[sa]);
-          mma_commit(&emptyB[sb]);
+          if (!P.bres) mma_commit(&emptyB[sb]);
           if ((skip & 32) && gi < 30) {                // debug trace: MMA-side cadence
             uint64_t t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -778,6 +835,37 @@ void tc_cache_free(chg_model *m) {
   m->tc_cache = nullptr;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+// 2-D fp32 map over a row-major [rows][width] table (row stride ld floats): box = 32 columns x
+// 128 rows, SWIZZLE_128B (the K-major UMMA layout), rows past the end read as zeros.
+static int encode_a_map(CUtensorMap *m, const float *base, int width, int rows, int ld) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || rows <= 0 || ((uintptr_t)base & 15) || (ld * 4) % 16) return 0;
+  cuuint64_t dim[2] = {(cuuint64_t)width, (cuuint64_t)rows};
+  cuuint64_t stride[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {KC, TCM}, es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)base, dim, stride, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 1 : 0;
+}
+
 // Returns false if the GEMM does not fit this path (caller uses the SIMT kernel).
 bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   if (g.M <= 0 || g.K % KC != 0 || g.nchunk < 1) return false;
@@ -807,8 +895,19 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   if (P.ntot > 256) return false;
   P.tmem_cols = P.ntot <= 32 ? 32 : P.ntot <= 64 ? 64 : P.ntot <= 128 ? 128 : 256;
   const int nkc = P.width / KC;
-  size_t smem = 1024 + (size_t)NSA * KC * TCM * 4 + (size_t)NSB * KC * P.ntot * 4 + 8 * (3 * NSA + 2 * NSB + 4) + 16 +
-                NEPI * 32 * 33 * 4;
+  const size_t bchunk = (size_t)KC * P.ntot * 4, achunk = (size_t)KC * TCM * 4;
+  auto fixed_of = [&](int nsa) {
+    return 1024 + nsa * achunk + 8 * (3 * nsa + 2 * NSB + 4) + 16 + (size_t)NEPI * 32 * 33 * 4;
+  };
+  // keep the whole weight image resident when it fits (no per-stage B round trips), then as
+  // many A stages as the remaining shared memory holds (the A ring is latency-bound)
+  static const bool no_bres = getenv("CHG_TC_NO_BRES") != nullptr;   // A/B knobs (timing studies)
+  static const int nsa_cap = getenv("CHG_TC_NSA") ? atoi(getenv("CHG_TC_NSA")) : NSA_MAX;
+  P.bres = !no_bres && fixed_of(5) + nkc * bchunk <= 224 * 1024;
+  P.bst = P.bres ? nkc : NSB;
+  P.nsa = 5;
+  while (P.nsa < std::min(nsa_cap, NSA_MAX) && fixed_of(P.nsa + 1) + P.bst * bchunk <= 224 * 1024) ++P.nsa;
+  size_t smem = fixed_of(P.nsa) + P.bst * bchunk;
   static bool attr = false;
   if (!attr) {
     CUDA_OK(cudaFuncSetAttribute(k_rowgemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
@@ -879,7 +978,19 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   ProfScope ps(ctx, g.tag ? g.tag : "rowgemm_tc", 2.0 * g.M * (double)g.K * cols,
                gemm_a_bytes(g.A, g.M, P.lo, P.lo + P.width) + (double)g.M * 4.0 * outb + 4.0 * g.K * cols);
   static int skip = getenv("CHG_TC_SKIP") ? atoi(getenv("CHG_TC_SKIP")) : 0;   // debug knob (timing studies)
-  k_rowgemm_tc<<<grid, WS_THREADS, smem, ctx->stream>>>(g, P, img, ntiles, skip);
+  TcMaps TM;
+  memset(&TM, 0, sizeof(TM));
+  static const bool no_tma = getenv("CHG_TC_NO_TMA") != nullptr;            // A/B knob (timing studies)
+  for (int s = 0; s < g.A.nseg && !no_tma; ++s) {
+    const ASeg &S = g.A.seg[s];
+    if (S.idx) continue;                              // gathered rows stay on cp.async
+    TM.use[s] = encode_a_map(&TM.m[s], S.base, S.width, g.M, S.ld);
+  }
+  static const bool verbose = getenv("CHG_TC_VERBOSE") != nullptr;
+  if (verbose)
+    fprintf(stderr, "rowgemm_tc %s: M %d K %d nseg %d tma %d%d%d%d nsa %d bres %d smem %zu\n", g.tag ? g.tag : "?", g.M,
+            g.K, g.A.nseg, TM.use[0], TM.use[1], TM.use[2], TM.use[3], P.nsa, P.bres, smem);
+  k_rowgemm_tc<<<grid, WS_THREADS, smem, ctx->stream>>>(g, P, img, ntiles, skip, TM);
   check_launch(ctx);
   return true;
 }
