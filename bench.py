@@ -418,6 +418,8 @@ def main():
     roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": traffic, "kernel": dom, "call_sites": sorted(r["tags"]),
                  "algorithmic_per_launch": per_launch_alg, "algorithmic_unit": "bytes" if roof["bound"] == "hbm" else "flop",
                  "avg_launch_us": per_launch_s * 1e6, "share_of_step": r["ms"] / ms_prof,
+                 "profiled_pass": "same steps with per-launch CUDA events; the concurrent branches run serially "
+                                  "while profiling, so each launch's time is its own",
                  "intensity_flop_per_byte": r["flops"] / max(r["bytes"], 1.0),
                  "tensor_frac": tfs / TF32_PEAK_TFLOPS if on_tc else None, "hbm_frac": gbs / PEAKS["hbm_gbs"]})
     gs = {"bytes": sum(v["bytes"] for t, v in rep.items() if t.startswith("segsum")),

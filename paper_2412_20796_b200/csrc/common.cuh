@@ -69,6 +69,9 @@ struct chg_ctx {
   // atom and bond/angle updates of a layer independent)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // the branches run concurrently unless per-op profiling is on (profiled passes are serial so
+  // that every op's CUDA-event time is its own)
+  bool concurrent() const { return side != nullptr && !prof_on; }
   std::string err;
   int64_t launches = 0;
   // named device workspaces (grow-only, stream-ordered reallocation)

@@ -37,7 +37,7 @@ struct Fwd {
 // join_side before consuming f's outputs).  Without a side stream f runs inline.
 template <class Fn>
 void on_side(chg_ctx *ctx, Fn &&f) {
-  if (!ctx->side) { f(); return; }
+  if (!ctx->concurrent()) { f(); return; }
   cudaStream_t main_stream = ctx->stream;
   CUDA_OK(cudaEventRecord(ctx->ev_fork, main_stream));
   CUDA_OK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
@@ -52,7 +52,7 @@ void on_side(chg_ctx *ctx, Fn &&f) {
   CUDA_OK(cudaEventRecord(ctx->ev_join, ctx->side));
 }
 void join_side(chg_ctx *ctx) {
-  if (ctx->side) CUDA_OK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+  if (ctx->concurrent()) CUDA_OK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
 }
 
 // --- Atom Conv (Eq. 4) ------------------------------------------------------
@@ -214,7 +214,7 @@ void forward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, int train, chg_pred 
     e[t + 1] = F.buf("e" + std::to_string(t + 1), E, 64);
     bool ab = t + 1 < T;
     if (ab) a[t + 1] = F.buf("a" + std::to_string(t + 1), A, 64);
-    if (serial) {
+    if (!ctx->concurrent()) {
       atom_conv_fwd(F, t, v[t], e[t], ea, v[t + 1]);
       bond_conv_fwd(F, t, ab, v[t], e[t], a[t], eb, e[t + 1], ab ? a[t + 1] : nullptr);
       continue;
@@ -632,7 +632,7 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
     // both output linears read the incoming gradients before any update
     ac_bwd_head(Bw, t, dv, dagg);
     bc_bwd_head(Bw, t, de, daggb);
-    if (!ctx->side) {
+    if (!ctx->concurrent()) {
       ac_bwd_body(Bw, t, V(t), Ef(t), ea, dagg, dv, de, dea);
       bc_bwd_body(Bw, t, ab, V(t), Ef(t), Af(t), eb, daggb, dv, de, da, deb, 1);
     } else {   // the bond/angle adjoints up to their dv/de sums run beside the atom conv's
