@@ -144,6 +144,8 @@ struct TcPlan {
   int ntot;          // total image rows N
   uint32_t tmem_cols;
   int bst;           // B smem slots: NSB (ring, one K chunk each) or nkc (whole image resident)
+  int ngrp;          // MMA groups: adjacent chunks over the same A window issue ONE MMA of N = gn
+  int gfirst[4], gn[4];
   int nsa;           // A stages
   int bres;          // 1: the whole weight image is loaded once per CTA (no per-stage B traffic)
 };
@@ -316,7 +318,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
-  __shared__ uint64_t trace_ts[32], trace_ld[32], trace_cv[32];
+  __shared__ uint64_t trace_ts[32], trace_ld[32], trace_cv[32], trace_mw[32];
   if ((skip & 32) && tid == 0) {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -460,22 +462,28 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
           mbar_wait(&fullA[sa], ua & 1);
           if (!P.bres) mbar_wait(&fullB[sb], ub & 1);
           else if (gi == 0) mbar_wait(&fullB[0], 0);
+          if ((skip & 32) && gi < 30) {                // debug trace: operands ready
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            trace_mw[gi] = t;
+          }
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t a_base = smem_u32(sA + sa * a_bytes), b_base = smem_u32(sB + sb * b_bytes);
           const int col0 = P.lo + kc * KC;
-          for (int c = 0; c < g.nchunk; ++c) {
+          for (int gr = 0; gr < P.ngrp; ++gr) {
+            const int c = P.gfirst[gr];
             const int kk = col0 - g.ch[c].a_k0;
             if (kk < 0 || kk >= g.K) continue;
-            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(P.cpad[c] >> 3) << 17) |
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(P.gn[gr] >> 3) << 17) |
                                    ((uint32_t)(TCM >> 4) << 24);
 #pragma unroll
             for (int j = 0; j < KC / 8; ++j) {
               uint64_t ad = make_desc(a_base + j * 32, 16, 1024) | ((uint64_t)2 << 61);   // SWIZZLE_128B
               uint64_t bd = make_desc(b_base + j * 2 * (NT * 16) + P.coff[c] * 16, NT * 16, 128);
               if (!(skip & 8))                            // debug: no tensor-core work
-                mma_tf32(tmem + a * tcols + P.coff[c], ad, bd, idesc, (started[c] || j > 0) ? 1u : 0u);
+                mma_tf32(tmem + a * tcols + P.coff[c], ad, bd, idesc, (started[gr] || j > 0) ? 1u : 0u);
             }
-            started[c] = true;
+            started[gr] = true;
           }
           mma_commit(&emptyA[sa]);
           if (!P.bres) mma_commit(&emptyB[sb]);
@@ -550,6 +558,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
     for (int i = 0; i < min(30, total); ++i) printf(" %.2f", (trace_ld[i] - trace_ts[0]) * 1e-3);
     printf(" | converted:");
     for (int i = 0; i < min(30, total); ++i) printf(" %.2f", (trace_cv[i] - trace_ts[0]) * 1e-3);
+    printf(" | mma ready:");
+    for (int i = 0; i < min(30, total); ++i) printf(" %.2f", (trace_mw[i] - trace_ts[0]) * 1e-3);
     printf(" | mma_done %.2f end %.2f\n", (trace_ts[31] - trace_ts[0]) * 1e-3, (t - trace_ts[0]) * 1e-3);
   }
   if (warp == 0)
@@ -892,6 +902,21 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   P.lo = lo;
   P.width = hi - lo;
   P.ntot = off;
+  // adjacent chunks reading the same A window (same a_k0, contiguous TMEM columns) share one
+  // MMA of N = their total width: fewer, wider tensor-core instructions
+  P.ngrp = 0;
+  for (int c = 0; c < g.nchunk; ++c) {
+    const bool join = P.ngrp > 0 && g.ch[c].a_k0 == g.ch[P.gfirst[P.ngrp - 1]].a_k0 &&
+                      P.coff[c] == P.coff[P.gfirst[P.ngrp - 1]] + P.gn[P.ngrp - 1] &&
+                      P.coff[c] - P.coff[P.gfirst[P.ngrp - 1]] + P.cpad[c] <= 256;
+    if (join) {
+      P.gn[P.ngrp - 1] = P.coff[c] - P.coff[P.gfirst[P.ngrp - 1]] + P.cpad[c];
+    } else {
+      P.gfirst[P.ngrp] = c;
+      P.gn[P.ngrp] = P.cpad[c];
+      ++P.ngrp;
+    }
+  }
   if (P.ntot > 256) return false;
   P.tmem_cols = P.ntot <= 32 ? 32 : P.ntot <= 64 ? 64 : P.ntot <= 128 ? 128 : 256;
   const int nkc = P.width / KC;
