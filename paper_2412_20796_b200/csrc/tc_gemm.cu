@@ -126,6 +126,9 @@ __device__ __forceinline__ float4 tc_loadA4(const AOp &A, int m, int col) {
 struct TcMaps {
   CUtensorMap m[4];
   int use[4];                      // 1: segment s is loaded by TMA
+  CUtensorMap e[4];                // epilogue operand (mul or resid) of chunk c: 32 x 32 boxes
+  int use_e[4];
+  int nbuf;                        // operand boxes in flight per epilogue warp (0: plain loads)
 };
 
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
@@ -266,6 +269,21 @@ __device__ __forceinline__ void epi_rows(const Chunk &C, const float *stile, int
   }
 }
 
+// epilogue rows with the mul / resid operand already in shared memory ([32 rows][32 cols], TMA)
+template <bool MUL>
+__device__ __forceinline__ void epi_rows_op(const Chunk &C, const float *stile, const float *ob, int lane, int row0,
+                                            int nrows, int n, float bn) {
+#pragma unroll 8
+  for (int rr = 0; rr < 32; ++rr) {
+    if (rr >= nrows) break;
+    float v = stile[rr * 33 + lane] + bn;
+    const float o = ob[rr * 32 + lane];
+    if (MUL) v *= dsiluf_(o);
+    else v += o;
+    C.out[(size_t)(row0 + rr) * C.ldo + n] = v;
+  }
+}
+
 __device__ __noinline__ void epi_rows_any(const Chunk &C, int act, const float *stile, int lane, int row0, int nrows,
                                           int n, float bn) {
   for (int rr = 0; rr < nrows; ++rr) {
@@ -300,6 +318,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
   uint64_t *tempty = tfull + 2;
   uint32_t *tslot = (uint32_t *)(tempty + 2);
   float *epi = (float *)(smem + NSA * a_bytes + P.bst * b_bytes + 8 * (3 * NSA + 2 * NSB + 4) + 16);  // [8][32][33]
+  // epilogue operand boxes [8 warps][TM.nbuf][32 x 32] (1024-B aligned TMA targets) + their barriers
+  float *obuf0 = (float *)(((uintptr_t)(epi + NEPI * 32 * 33) + 1023) & ~(uintptr_t)1023);
+  uint64_t *ebar = (uint64_t *)(obuf0 + NEPI * TM.nbuf * 1024);
   const uint32_t tcols = P.tmem_cols;                   // per accumulator buffer
 
   if (warp == 0) {
@@ -312,6 +333,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
     for (int i = 0; i < NSA; ++i) { mbar_init(&fullA[i], 4); mbar_init(&emptyA[i], 1); mbar_init(&loaded[i], 128); }
     for (int i = 0; i < NSB; ++i) { mbar_init(&fullB[i], 1); mbar_init(&emptyB[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], NEPI); }
+    for (int i = 0; i < 2 * NEPI; ++i) mbar_init(&ebar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -502,35 +524,67 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
       }
     }
   } else {
-    // ---------------- epilogue (warps 10-13) ----------------
+    // ---------------- epilogue (warps 10-17) ----------------
     const int lq = warp & 3;
     const uint32_t lane_base = (uint32_t)(lq * 32) << 16;
+    float *stile = epi + (warp - 10) * (32 * 33);
+    const int half = (warp - 10) >> 2;                // two warps per TMEM lane quarter split the blocks
+    // this warp's 32x32 blocks (chunk, first column), the same in every tile
+    int nmy = 0, mc[8], mj[8];
+    {
+      int blk = 0;
+      for (int c = 0; c < g.nchunk; ++c)
+        for (int j0 = 0; j0 < P.cpad[c]; j0 += 32, ++blk)
+          if ((blk & 1) == half && nmy < 8) { mc[nmy] = c; mj[nmy] = j0; ++nmy; }
+    }
+    // mul / resid operand boxes arrive by TMA into per-warp buffers, issued ahead of use
+    const int NB = TM.nbuf;
+    float *obuf = obuf0 + (warp - 10) * (NB > 0 ? NB : 1) * 1024;
+    uint64_t *obar = ebar + (warp - 10) * 2;
+    uint32_t ophase = 0;                              // bit s: parity of slot s
+    auto issue_op = [&](int i, int row0) {            // block i of this warp's list -> slot i % NB
+      const int c = mc[i];
+      if (NB == 0 || !TM.use_e[c] || lane != 0) return;
+      const int sl = i % NB;
+      mbar_expect_tx(&obar[sl], 4096);
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc)
+        if (cc == c) tma_load_2d(smem_u32(obuf + sl * 1024), &TM.e[cc], mj[i], row0, &obar[sl]);
+    };
     for (int tl = 0; tl < my_tiles; ++tl) {
       const int a = tl & 1;
       const int tile = blockIdx.x + tl * gridDim.x;
+      const int row0 = tile * TCM + lq * 32;
+      const int nrows = min(32, g.M - row0);
+      for (int i = 0; i < nmy && i < NB; ++i) issue_op(i, row0);   // overlaps the accumulator wait
       mbar_wait(&tfull[a], (tl >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       // 32x32 blocks go TMEM -> registers (lane = row) -> smem -> registers
       // (lane = column) so that every global access is a coalesced 128-B row run
-      float *stile = epi + (warp - 10) * (32 * 33);
-      const int half = (warp - 10) >> 2;              // two warps per TMEM lane quarter split the blocks
-      int blk = 0;
-      const int row0 = tile * TCM + lq * 32;
-      const int nrows = min(32, g.M - row0);
-      for (int c = 0; c < g.nchunk; ++c) {
+      for (int i = 0; i < nmy; ++i) {
+        const int c = mc[i], j0 = mj[i];
         const Chunk &C = g.ch[c];
-        for (int j0 = 0; j0 < P.cpad[c]; j0 += 32, ++blk) {
-          if ((blk & 1) != half) continue;
-          uint32_t r[32];
-          tmem_ld32(tmem + lane_base + a * tcols + P.coff[c] + j0, r);
-          if (skip & 1) continue;                         // debug: no epilogue stores
+        uint32_t r[32];
+        tmem_ld32(tmem + lane_base + a * tcols + P.coff[c] + j0, r);
+        if (skip & 1) continue;                         // debug: no epilogue stores
 #pragma unroll
-          for (int qq = 0; qq < 32; ++qq) stile[lane * 33 + qq] = __uint_as_float(r[qq]);
-          __syncwarp();
-          const int n = j0 + lane;
-          if (n < C.ncols) {
+        for (int qq = 0; qq < 32; ++qq) stile[lane * 33 + qq] = __uint_as_float(r[qq]);
+        __syncwarp();
+        const int n = j0 + lane;
+        const bool opd = NB > 0 && TM.use_e[c];
+        if (opd) {                                    // operand box of this block has landed
+          const int sl = i % NB;
+          mbar_wait(&obar[sl], (ophase >> sl) & 1);
+          ophase ^= 1u << sl;
+        }
+        if (n < C.ncols) {
+          const float bn = C.bias ? __ldg(C.bias + n) : 0.f;
+          if (opd) {
+            const float *ob = obuf + (i % NB) * 1024;
+            if (C.mul) epi_rows_op<true>(C, stile, ob, lane, row0, nrows, n, bn);
+            else epi_rows_op<false>(C, stile, ob, lane, row0, nrows, n, bn);
+          } else {
             // flags are uniform per 32x32 block: one specialised row loop per combination
-            const float bn = C.bias ? __ldg(C.bias + n) : 0.f;
             const int code = (C.pre ? 1 : 0) | (C.mul ? 2 : 0) | (C.resid ? 4 : 0) | (g.act == 1 ? 8 : 0);
             switch (code) {
               case 0: epi_rows<false, false, false, false>(C, stile, lane, row0, nrows, n, bn); break;
@@ -539,8 +593,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
               default: epi_rows_any(C, g.act, stile, lane, row0, nrows, n, bn); break;
             }
           }
-          __syncwarp();
         }
+        __syncwarp();
+        if (opd && i + NB < nmy) issue_op(i + NB, row0);   // slot free again: next box of this tile
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -876,6 +931,19 @@ static int encode_a_map(CUtensorMap *m, const float *base, int width, int rows, 
   return r == CUDA_SUCCESS ? 1 : 0;
 }
 
+// 2-D fp32 map of an epilogue operand [rows][ncols] (row stride ld): 32 x 32 boxes, no swizzle
+static int encode_op_map(CUtensorMap *m, const float *base, int ncols, int rows, int ld) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || rows <= 0 || ncols % 32 || ((uintptr_t)base & 15) || (ld * 4) % 16) return 0;
+  cuuint64_t dim[2] = {(cuuint64_t)ncols, (cuuint64_t)rows};
+  cuuint64_t stride[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {32, 32}, es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)base, dim, stride, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 1 : 0;
+}
+
 // Returns false if the GEMM does not fit this path (caller uses the SIMT kernel).
 bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   if (g.M <= 0 || g.K % KC != 0 || g.nchunk < 1) return false;
@@ -930,9 +998,19 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   static const int nsa_cap = getenv("CHG_TC_NSA") ? atoi(getenv("CHG_TC_NSA")) : NSA_MAX;
   P.bres = !no_bres && fixed_of(5) + nkc * bchunk <= 224 * 1024;
   P.bst = P.bres ? nkc : NSB;
-  P.nsa = 5;
-  while (P.nsa < std::min(nsa_cap, NSA_MAX) && fixed_of(P.nsa + 1) + P.bst * bchunk <= 224 * 1024) ++P.nsa;
-  size_t smem = fixed_of(P.nsa) + P.bst * bchunk;
+  // epilogue operands (mul / resid of a chunk) by TMA when the GEMM has them: 2 boxes in flight
+  // per epilogue warp if shared memory allows (else 1), at the cost of A stages beyond 4
+  static const bool no_etma = getenv("CHG_TC_NO_ETMA") != nullptr;   // A/B knob
+  int has_op = 0;
+  for (int c = 0; c < g.nchunk; ++c) has_op |= ((g.ch[c].mul != nullptr) != (g.ch[c].resid != nullptr)) && !g.ch[c].pre;
+  int nbuf = (has_op && !no_etma) ? 2 : 0;
+  auto opbytes = [&](int nb) { return (size_t)1024 + (size_t)NEPI * nb * 4096 + 2 * NEPI * 8; };
+  if (nbuf == 2 && fixed_of(4) + P.bst * bchunk + opbytes(2) > 224 * 1024) nbuf = 1;
+  if (nbuf == 1 && fixed_of(4) + P.bst * bchunk + opbytes(1) > 224 * 1024) nbuf = 0;
+  P.nsa = 4;
+  while (P.nsa < std::min(nsa_cap, NSA_MAX) && fixed_of(P.nsa + 1) + P.bst * bchunk + opbytes(nbuf) <= 224 * 1024)
+    ++P.nsa;
+  size_t smem = fixed_of(P.nsa) + P.bst * bchunk + opbytes(nbuf);
   static bool attr = false;
   if (!attr) {
     CUDA_OK(cudaFuncSetAttribute(k_rowgemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
@@ -1010,6 +1088,13 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
     const ASeg &S = g.A.seg[s];
     if (S.idx) continue;                              // gathered rows stay on cp.async
     TM.use[s] = encode_a_map(&TM.m[s], S.base, S.width, g.M, S.ld);
+  }
+  TM.nbuf = nbuf;
+  for (int c = 0; c < g.nchunk && nbuf > 0; ++c) {
+    const Chunk &C = g.ch[c];
+    if ((C.mul != nullptr) == (C.resid != nullptr) || C.pre) continue;
+    const float *op = C.mul ? C.mul : C.resid;
+    TM.use_e[c] = encode_op_map(&TM.e[c], op, C.ncols, g.M, C.mul ? C.ldm : C.ldr);
   }
   static const bool verbose = getenv("CHG_TC_VERBOSE") != nullptr;
   if (verbose)
