@@ -19,8 +19,30 @@ struct RedBatch {
   int n;
 };
 
+__device__ __forceinline__ float *red_dst(const RedJob &J, int idx) {
+  switch (J.kind) {
+    case 0: {                               // weight gradient: (k, n) -> W chunk / bias
+      const int k = idx / J.N, n = idx % J.N, c = n >> 6, nn = n & 63;
+      if (k < J.K) {
+        if (J.W[c] && k >= J.k0[c] && (J.kn[c] < 0 || k < J.k0[c] + J.kn[c]))
+          return J.W[c] + (size_t)(k - J.k0[c]) * J.ldw[c] + nn;
+        return nullptr;
+      }
+      return J.b[c] ? J.b[c] + nn : nullptr;
+    }
+    case 1: return J.W[0] + idx;            // flat
+    case 2: return J.W[idx >> 6] + (idx & 63);   // LayerNorm gc | bc | gg | bg
+    default: {                              // projection [31][C]: column c < 64 -> W[0], else W[1]
+      const int n = idx / J.N, c = idx % J.N;
+      return J.W[c >> 6] + n * 64 + (c & 63);
+    }
+  }
+}
+
+// block = 128 consecutive outputs of one job (lane = float4 quad), warp w sums partial rows
+// w, w+8, ... and warp 0 adds the 8 subtotals in order
 __global__ void __launch_bounds__(256) k_reduce_all(const __grid_constant__ RedBatch B) {
-  __shared__ float sh[8][32];
+  __shared__ float4 sh[8][32];
   __shared__ int sj;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
@@ -33,38 +55,42 @@ __global__ void __launch_bounds__(256) k_reduce_all(const __grid_constant__ RedB
   }
   __syncthreads();
   const RedJob &J = B.j[sj];
-  const int idx = ((int)blockIdx.x - J.block0) * 32 + lane;
-  float s = 0.f;
+  const int q = ((int)blockIdx.x - J.block0) * 32 + lane;   // quad index
+  const int idx = 4 * q;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
   if (idx < J.n) {
+    if (J.stride % 4 == 0) {                // 16-B rows: one float4 per partial row
+      const float4 *p = (const float4 *)J.part + q;
+      const int64_t st4 = J.stride / 4;
 #pragma unroll 8
-    for (int sp = w; sp < J.splits; sp += 8) s += __ldcg(J.part + (size_t)sp * J.stride + idx);
+      for (int sp = w; sp < J.splits; sp += 8) {
+        const float4 u = __ldcg(p + (size_t)sp * st4);
+        s.x += u.x; s.y += u.y; s.z += u.z; s.w += u.w;
+      }
+    } else {                                // odd row length (N = 1 or 9 heads): scalar loads
+      const int m = min(4, J.n - idx);
+      for (int sp = w; sp < J.splits; sp += 8) {
+        const float *p = J.part + (size_t)sp * J.stride + idx;
+        s.x += __ldcg(p);
+        if (m > 1) s.y += __ldcg(p + 1);
+        if (m > 2) s.z += __ldcg(p + 2);
+        if (m > 3) s.w += __ldcg(p + 3);
+      }
+    }
   }
   sh[w][lane] = s;
   __syncthreads();
   if (w != 0 || idx >= J.n) return;
-  float t = 0.f;
+  float4 t = sh[0][lane];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) t += sh[k][lane];
-  float *dst = nullptr;
-  switch (J.kind) {
-    case 0: {                               // weight gradient: (k, n) -> W chunk / bias
-      const int k = idx / J.N, n = idx % J.N, c = n >> 6, nn = n & 63;
-      if (k < J.K) {
-        if (J.W[c] && k >= J.k0[c] && (J.kn[c] < 0 || k < J.k0[c] + J.kn[c])) dst = J.W[c] + (size_t)(k - J.k0[c]) * J.ldw[c] + nn;
-      } else {
-        dst = J.b[c] ? J.b[c] + nn : nullptr;
-      }
-      break;
-    }
-    case 1: dst = J.W[0] + idx; break;      // flat
-    case 2: dst = J.W[idx >> 6] + (idx & 63); break;   // LayerNorm gc | bc | gg | bg
-    case 3: {                               // projection [31][C]: column c < 64 -> W[0], else W[1]
-      const int n = idx / J.N, c = idx % J.N;
-      dst = J.W[c >> 6] + n * 64 + (c & 63);
-      break;
-    }
+  for (int k = 1; k < 8; ++k) { t.x += sh[k][lane].x; t.y += sh[k][lane].y; t.z += sh[k][lane].z; t.w += sh[k][lane].w; }
+  const float v[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    if (idx + e >= J.n) break;
+    float *d = red_dst(J, idx + e);
+    if (d) *d += v[e];
   }
-  if (dst) *dst += t;
 }
 
 }  // namespace
@@ -76,6 +102,7 @@ float *red_partial(chg_ctx *ctx, size_t floats) {
 
 void red_push(chg_ctx *ctx, RedJob j) {
   if (j.n <= 0) return;
+  if ((uintptr_t)j.part & 15) CHG_THROW(CHG_ERR_STATE, "red_push: partial buffer must be 16-byte aligned");
   if (ctx->red_on) {
     ctx->red_jobs.push_back(j);
     return;
@@ -96,7 +123,7 @@ void red_flush(chg_ctx *ctx) {
     for (int k = 0; k < B.n; ++k) {
       B.j[k] = ctx->red_jobs[j0 + k];
       B.j[k].block0 = blocks;
-      blocks += ceil_div(B.j[k].n, 32);
+      blocks += ceil_div(B.j[k].n, 128);
       bytes += 4.0 * B.j[k].n * (B.j[k].splits + 2.0);
     }
     ProfScope ps(ctx, "reduce_all", 0.0, bytes);
