@@ -137,8 +137,6 @@ struct chg_graph {
   int32_t *row_ptr = nullptr;          // [N+1] edges by centre
   int32_t *bond_ptr = nullptr;         // [N+1] bonds by centre
   int32_t *atom_angle_ptr = nullptr;   // [N+1] angles by centre
-  int32_t *species_perm = nullptr;     // [N] atoms sorted by species
-  int32_t *species_ptr = nullptr;      // [n_species+1]
   // per edge
   int32_t *center = nullptr;           // [E]
   int32_t *nbr = nullptr;              // [E]

@@ -15,7 +15,6 @@
 //   k_fill      ordered emission with warp ballot/scan                  (G3)
 //   k_angles    angle pairs, swap map, per-angle edge/centre indices    (G4)
 //   k_rev       reverse-edge map by binary search in row j              (G4)
-//   k_species   stable counting sort of atoms by species (embedding grad)
 #include <cmath>
 
 #include "common.cuh"
@@ -368,39 +367,6 @@ __global__ void k_rev(int E, const int32_t *__restrict__ center, const int32_t *
 }
 
 // stable counting sort of atoms by species, one warp (deterministic)
-__global__ void k_species(int N, int n_species, const int32_t *__restrict__ species,
-                          int32_t *__restrict__ perm, int32_t *__restrict__ sptr) {
-  extern __shared__ int cnt[];   // n_species + 1
-  int lane = threadIdx.x;
-  for (int z = lane; z <= n_species; z += 32) cnt[z] = 0;
-  __syncwarp();
-  for (int i0 = 0; i0 < N; i0 += 32) {
-    int i = i0 + lane;
-    int z = i < N ? species[i] : -1;
-    unsigned m = __match_any_sync(0xffffffffu, z);
-    int leader = __ffs(m) - 1;
-    if (i < N && lane == leader) cnt[z] += __popc(m);
-    __syncwarp();
-  }
-  if (lane == 0) {
-    int acc = 0;
-    for (int z = 0; z <= n_species; ++z) { int c = cnt[z]; cnt[z] = acc; sptr[z] = acc; acc += c; }
-    sptr[n_species + 1] = acc;
-  }
-  __syncwarp();
-  for (int i0 = 0; i0 < N; i0 += 32) {
-    int i = i0 + lane;
-    int z = i < N ? species[i] : -1;
-    unsigned m = __match_any_sync(0xffffffffu, z);
-    int rank = __popc(m & ((1u << lane) - 1));
-    int leader = __ffs(m) - 1;
-    if (i < N) perm[cnt[z] + rank] = i;
-    __syncwarp();
-    if (i < N && lane == leader) cnt[z] += __popc(m);
-    __syncwarp();
-  }
-}
-
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct GraphBlocks { void *a = nullptr, *b = nullptr; };
@@ -483,11 +449,9 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
     G->atom_ptr = (int32_t *)take(4 * (S + 1));
     G->struct_of_atom = (int32_t *)take(4 * N);
     G->species = (int32_t *)take(4 * N);
-    G->species_perm = (int32_t *)take(4 * N);
     G->row_ptr = (int32_t *)take(4 * n1);
     G->bond_ptr = (int32_t *)take(4 * n1);
     G->atom_angle_ptr = (int32_t *)take(4 * n1);
-    G->species_ptr = (int32_t *)take(4 * (n_species + 2));
     G->lattice_f = (float *)take(4 * 9 * (size_t)S);
     G->inv_natoms = (float *)take(4 * (size_t)S);
     StructGeo *d_geo = (StructGeo *)take(sizeof(StructGeo) * geo.size());
@@ -616,12 +580,9 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
         k_rev<<<ceil_div(E, 256), 256, 0, st>>>((int)E, G->center, G->nbr, G->img, G->row_ptr, G->rev, G->d_flag);
         check_launch(ctx);
       }
-      k_species<<<1, 32, 4 * (n_species + 1), st>>>((int)N, n_species, G->species, G->species_perm,
-                                                     G->species_ptr);
-      check_launch(ctx);
+
     } else {
       CUDA_OK(cudaMemsetAsync(G->angle_ptr, 0, 4, st));
-      CUDA_OK(cudaMemsetAsync(G->species_ptr, 0, 4 * (n_species + 2), st));
     }
   } catch (...) {
     if (bl->a) cudaFreeAsync(bl->a, st);

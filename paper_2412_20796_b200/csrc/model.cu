@@ -655,7 +655,7 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
     red_flush(ctx);
   }
   // embedding (rows of W_v gathered by species -> grouped sum, no atomics)
-  species_grad(ctx, N, m->cfg.n_species, g->species_ptr, g->species_perm, dv, Bw.G("embed.W"));
+  embed_grad(ctx, N, m->cfg.n_species, g->species, dv, Bw.G("embed.W"));
   // projections (Eq. 2) and trainable frequencies, from the saved bases (proj.cu)
   proj_bwd(ctx, E, Bw.act("ea_t"), Bw.act("ea_g"), de, dea, m->p("proj.W0"), m->p("proj.Wa"), Bw.G("proj.W0"),
            Bw.G("proj.Wa"), Bw.G("rbf_a.freq"));

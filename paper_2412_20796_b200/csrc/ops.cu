@@ -385,28 +385,25 @@ __global__ void __launch_bounds__(256) k_segsum_linear(int64_t targets, SegArgs 
   ((float4 *)(out + t * 64))[hl] = make_float4(o[0], o[1], o[2], o[3]);
 }
 
-// Embedding gradient dW_v[z] += Σ_{i: Z_i = z+1} dv_i (Eq. 2 adjoint) in two fixed-order
-// passes: (1) block (c, z) sums rows [64c, 64c+64) of species z's segment (thread = column),
-// (2) block z adds its chunk partials in chunk order.  Long segments (oxygen) are split
-// across many blocks instead of one serial walk.
-constexpr int SPG_ROWS = 64;
-__global__ void __launch_bounds__(64) k_species_grad1(const int32_t *__restrict__ ptr, const int32_t *__restrict__ perm,
-                                                      const float *__restrict__ dv, float *__restrict__ part, int maxc) {
-  const int c = blockIdx.x, z = blockIdx.y, col = threadIdx.x;
-  const int r0 = ptr[z + 1] + c * SPG_ROWS, r1 = min(r0 + SPG_ROWS, ptr[z + 2]);
-  if (r0 >= r1) return;
-  float acc = 0.f;
-#pragma unroll 8
-  for (int r = r0; r < r1; ++r) acc += dv[(int64_t)perm[r] * 64 + col];
-  part[((int64_t)z * maxc + c) * 64 + col] = acc;
-}
-__global__ void __launch_bounds__(64) k_species_grad2(const int32_t *__restrict__ ptr, const float *__restrict__ part,
-                                                      int maxc, float *__restrict__ dW) {
-  const int z = blockIdx.x, col = threadIdx.x;
-  const int n = ptr[z + 2] - ptr[z + 1], nc = (n + SPG_ROWS - 1) / SPG_ROWS;
-  float acc = 0.f;
-  for (int c = 0; c < nc; ++c) acc += part[((int64_t)z * maxc + c) * 64 + col];
-  dW[(int64_t)z * 64 + col] += acc;
+// Embedding gradient dW_v[z] += Σ_{i: Z_i = z+1} dv_i (Eq. 2 adjoint): block b bins its 64
+// consecutive atoms by species in shared memory (thread = column, atoms in index order), the
+// per-block bins are reduced in block order by the batched reduction (reduce.cu) — no sort,
+// no atomics, deterministic.
+constexpr int EGB = 64;   // atoms per block
+__global__ void __launch_bounds__(64) k_embed_grad(int64_t N, int nz, const int32_t *__restrict__ species,
+                                                   const float *__restrict__ dv, float *__restrict__ part) {
+  extern __shared__ float bins[];                   // [nz][64]
+  const int c = threadIdx.x;
+  for (int i = c; i < nz * 64; i += 64) bins[i] = 0.f;
+  __syncthreads();
+  const int64_t i0 = (int64_t)blockIdx.x * EGB, i1 = min(N, i0 + EGB);
+  for (int64_t i = i0; i < i1; ++i) {
+    const int z = __ldg(species + i) - 1;
+    bins[z * 64 + c] += __ldg(dv + i * 64 + c);
+  }
+  __syncthreads();
+  float *p = part + (size_t)blockIdx.x * nz * 64;
+  for (int i = c; i < nz * 64; i += 64) p[i] = bins[i];
 }
 
 // e' = e + 𝓛_e(agg) for every edge (Eq. 5, Q16): the 64x64 product is computed only for the
@@ -739,16 +736,18 @@ void segsum_linear(chg_ctx *ctx, int64_t targets, int nsrc, const SegSrc *src, f
   check_launch(ctx);
 }
 
-void species_grad(chg_ctx *ctx, int64_t N, int n_species, const int32_t *species_ptr, const int32_t *species_perm,
-                  const float *dv, float *dW) {
+void embed_grad(chg_ctx *ctx, int64_t N, int n_species, const int32_t *species, const float *dv, float *dW) {
   if (N <= 0 || n_species <= 0) return;
-  const int maxc = ceil_div(N, SPG_ROWS);
-  float *part = ctx->getf("species_part", (size_t)n_species * maxc * 64);
-  ProfScope ps(ctx, "species_grad", 0.0, N * 260.0 + n_species * 512.0);
-  k_species_grad1<<<dim3(maxc, n_species), 64, 0, ctx->stream>>>(species_ptr, species_perm, dv, part, maxc);
-  check_launch(ctx);
-  k_species_grad2<<<n_species, 64, 0, ctx->stream>>>(species_ptr, part, maxc, dW);
-  check_launch(ctx);
+  const int nb = ceil_div(N, EGB);
+  float *part = red_partial(ctx, (size_t)nb * n_species * 64);
+  {
+    ProfScope ps(ctx, "embed_grad", 0.0, N * 260.0 + nb * n_species * 256.0);
+    k_embed_grad<<<nb, 64, n_species * 64 * 4, ctx->stream>>>(N, n_species, species, dv, part);
+    check_launch(ctx);
+  }
+  RedJob j;
+  j.kind = 1; j.n = n_species * 64; j.splits = nb; j.stride = n_species * 64; j.part = part; j.W[0] = dW;
+  red_push(ctx, j);
 }
 
 void edge_update(chg_ctx *ctx, int64_t E, const float *e, const float *bias, const int32_t *bond_id, const float *tmp,

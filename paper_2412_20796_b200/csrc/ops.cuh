@@ -38,10 +38,9 @@ void segsum(chg_ctx *ctx, int64_t targets, float *out, int ldo, int accumulate, 
 void segsum_linear(chg_ctx *ctx, int64_t targets, int nsrc, const SegSrc *src, float *agg, const float *W,
                    const float *bias, const float *resid, float *out, const char *tag);
 
-// embedding gradient: dW[z] += Σ_{i: Z_i = z+1} dv[i] over the species-sorted atom list
-// (species_ptr has n_species + 2 entries, segment of Z at [ptr[Z], ptr[Z+1])); deterministic
-void species_grad(chg_ctx *ctx, int64_t N, int n_species, const int32_t *species_ptr, const int32_t *species_perm,
-                  const float *dv, float *dW);
+// embedding gradient: dW[z - 1] += Σ_{i: Z_i = z} dv[i] (species 1..n_species); per-block
+// species bins reduced by the batched reduction (reduce.cu); deterministic
+void embed_grad(chg_ctx *ctx, int64_t N, int n_species, const int32_t *species, const float *dv, float *dW);
 
 // fused readout MLPs (head_mlp.cu): nl linear layers (hidden 64 + SiLU, last 64 -> nout),
 // P / G = the head's parameter / gradient block in the flat layout (W0 b0 W1 b1 ...),
