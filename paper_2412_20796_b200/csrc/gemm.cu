@@ -3,7 +3,7 @@
 
 namespace {
 
-constexpr int TM = 128, TN = 64, TK = 32;   // default rows per CTA, columns per chunk, K step
+constexpr int TM = 128, TN = 64;   // default rows per CTA, columns per chunk (K step: template TK)
 
 // A(m, col) for 4 consecutive columns (segment widths are multiples of 4)
 __device__ __forceinline__ float4 loadA4(const AOp &A, int m, int col) {

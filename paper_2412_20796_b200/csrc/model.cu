@@ -692,14 +692,14 @@ void step_impl(chg_ctx *ctx, chg_model *m, const chg_adam_cfg *cfg) {
   } else if (cfg->allreduce && ctx->nranks > 1) {
     CHG_THROW(CHG_ERR_STATE, "allreduce requested but no NCCL communicator");
   }
-  int bad = finite_check(ctx, m->grads, m->P);
-  if (bad >= 0) {
+  double bc1 = 1.0 - std::pow((double)cfg->beta1, (double)cfg->step);
+  double bc2 = 1.0 - std::pow((double)cfg->beta2, (double)cfg->step);
+  int bad = finite_adam(ctx, m->P, m->params, m->grads, m->m, m->v, cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, bc1,
+                        bc2);
+  if (bad >= 0) {   // nothing was updated (k_adam is guarded by the same flag)
     std::string name = "?";
     for (size_t t = 0; t < m->names.size(); ++t)
       if (m->offsets[t] <= bad) name = m->names[t];
     CHG_THROW(CHG_ERR_NONFINITE, "non-finite gradient in %s (flat index %d)", name.c_str(), bad);
   }
-  double bc1 = 1.0 - std::pow((double)cfg->beta1, (double)cfg->step);
-  double bc2 = 1.0 - std::pow((double)cfg->beta2, (double)cfg->step);
-  adam_update(ctx, m->P, m->params, m->grads, m->m, m->v, cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, bc1, bc2);
 }

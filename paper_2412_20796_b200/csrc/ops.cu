@@ -7,106 +7,6 @@
 namespace {
 
 // ---------------------------------------------------------------------------
-// A2 basis.  Geometry is read in fp64 (vec64 from the graph builder), the
-// envelope is evaluated with ONE ξ^p and a factored quadratic (redundancy
-// removal of Eq. 13, with the DimeNet coefficients of reading Q2),
-// the result is rounded once to fp32.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ double envelope_d(double xi, int p) {
-  double xp = 1.0;
-  for (int k = 0; k < p; ++k) xp *= xi;
-  double a = 0.5 * (p + 1) * (p + 2), b = (double)p * (p + 2), c = 0.5 * p * (p + 1);
-  return 1.0 - xp * (a - xi * (b - c * xi));
-}
-
-__global__ void k_basis_radial(int64_t rows, const double4 *__restrict__ vec, const int32_t *__restrict__ eor,
-                               const float *__restrict__ freq, double rc, int p, float *__restrict__ out) {
-  int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t row = gt >> 5;
-  int n = (int)(gt & 31);
-  if (row >= rows) return;
-  int e = eor ? eor[row] : (int)row;
-  double r = vec[e].w;
-  float val = 0.f;
-  if (n < CHG_K) {
-    double xi = r / rc;
-    double u = envelope_d(xi, p);
-    val = (float)(u * sqrt(2.0 / rc) * sin((double)freq[n] * xi) / r);
-  }
-  out[row * CHG_KP + n] = val;
-}
-
-__global__ void k_basis_freq_grad(int64_t rows, const double4 *__restrict__ vec, const int32_t *__restrict__ eor,
-                                  const float *__restrict__ freq, double rc, int p, const float *__restrict__ db,
-                                  float *__restrict__ partial) {
-  __shared__ float sh[8][32];
-  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int64_t gw = blockIdx.x * 8 + w, nw = (int64_t)gridDim.x * 8;
-  double acc = 0.0;
-  if (lane < CHG_K) {
-    double f = freq[lane];
-    for (int64_t row = gw; row < rows; row += nw) {
-      int e = eor ? eor[row] : (int)row;
-      double r = vec[e].w, xi = r / rc;
-      double u = envelope_d(xi, p);
-      acc += (double)db[row * CHG_KP + lane] * u * sqrt(2.0 / rc) * cos(f * xi) / rc;
-    }
-  }
-  sh[w][lane] = (float)acc;
-  __syncthreads();
-  if (w == 0) {
-    float s = 0.f;
-    for (int k = 0; k < 8; ++k) s += sh[k][lane];
-    partial[blockIdx.x * 32 + lane] = s;
-  }
-}
-
-// fixed-order column reduction of per-block partials (same order as reduce.cu)
-__global__ void __launch_bounds__(1024) k_reduce_cols(int nblocks, int ncols, int stride,
-                                                      const float *__restrict__ partial, float *__restrict__ grad) {
-  __shared__ float sh[32][33];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int j = blockIdx.x * 32 + lane;
-  float s = 0.f;
-  if (j < ncols)
-#pragma unroll 4
-    for (int b = w; b < nblocks; b += 32) s += partial[(size_t)b * stride + j];
-  sh[w][lane] = s;
-  __syncthreads();
-  if (w == 0 && j < ncols) {
-    float t = 0.f;
-#pragma unroll
-    for (int k = 0; k < 32; ++k) t += sh[k][lane];
-    grad[j] += t;
-  }
-}
-
-__global__ void k_basis_angle(int64_t A, const double4 *__restrict__ vec, const int32_t *__restrict__ e1,
-                              const int32_t *__restrict__ e2, float *__restrict__ out) {
-  int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (a >= A) return;
-  double4 d1 = vec[e1[a]], d2 = vec[e2[a]];
-  double c = (d1.x * d2.x + d1.y * d2.y + d1.z * d2.z) / (d1.w * d2.w);
-  c = fmin(1.0, fmax(-1.0, c));
-  double s = sqrt(fmax(0.0, 1.0 - c * c));   // sin θ >= 0 for θ in [0, π]
-  const double isp = 0.56418958354775628695, is2p = 0.39894228040143267794;  // 1/√π, 1/√(2π)
-  float v[32];
-  v[0] = (float)is2p;
-  double ck = c, sk = s;
-#pragma unroll
-  for (int k = 1; k <= 15; ++k) {
-    v[2 * k - 1] = (float)(ck * isp);
-    v[2 * k] = (float)(sk * isp);
-    double cn = ck * c - sk * s, sn = sk * c + ck * s;   // angle addition: (k+1)θ
-    ck = cn; sk = sn;
-  }
-  v[31] = 0.f;
-  float4 *o = (float4 *)(out + a * CHG_KP);
-#pragma unroll
-  for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-}
-
-// ---------------------------------------------------------------------------
 // GatedMLP output stage
 // ---------------------------------------------------------------------------
 struct RowStats { float mu, rstd; };
@@ -608,11 +508,13 @@ __global__ void k_finite(int64_t n, const float *__restrict__ g, int *bad) {
   if (i < n && !isfinite(g[i])) atomicMin(bad, (int)i);
 }
 
+// Adam (PyTorch semantics, Q24), guarded by the finite check's flag: a non-finite gradient
+// leaves params, m, v and the gradients untouched (the host raises after one synchronisation)
 __global__ void k_adam(int64_t n, float *__restrict__ p, float *__restrict__ g, float *__restrict__ m,
                        float *__restrict__ v, float lr, float b1, float b2, float eps, float step_size,
-                       float inv_sqrt_bc2) {
+                       float inv_sqrt_bc2, const int *__restrict__ bad) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  if (i >= n || (bad && *bad != 0x7f7f7f7f)) return;
   float gi = g[i];
   float mi = b1 * m[i] + (1.f - b1) * gi;
   float vi = b2 * v[i] + (1.f - b2) * gi * gi;
@@ -627,33 +529,6 @@ __global__ void k_adam(int64_t n, float *__restrict__ p, float *__restrict__ g, 
 // ---------------------------------------------------------------------------
 // host wrappers
 // ---------------------------------------------------------------------------
-void basis_radial(chg_ctx *ctx, int64_t rows, const double4 *vec64, const int32_t *eor, const float *freq,
-                  double rc, int p, float *out) {
-  if (rows <= 0) return;
-  ProfScope ps(ctx, "basis", 0.0, rows * (4.0 + 32.0 + 128.0));
-  k_basis_radial<<<ceil_div(rows * 32, 256), 256, 0, ctx->stream>>>(rows, vec64, eor, freq, rc, p, out);
-  check_launch(ctx);
-}
-
-void basis_angle(chg_ctx *ctx, int64_t A, const double4 *vec64, const int32_t *e1, const int32_t *e2, float *out) {
-  if (A <= 0) return;
-  ProfScope ps(ctx, "basis", 0.0, A * (8.0 + 64.0 + 128.0));
-  k_basis_angle<<<ceil_div(A, 128), 128, 0, ctx->stream>>>(A, vec64, e1, e2, out);
-  check_launch(ctx);
-}
-
-void basis_freq_grad(chg_ctx *ctx, int64_t rows, const double4 *vec64, const int32_t *eor, const float *freq,
-                     double rc, int p, const float *dbasis, float *grad) {
-  if (rows <= 0) return;
-  int nb = std::min<int64_t>(296, ceil_div(rows, 8));
-  float *part = ctx->getf("freq_partial", (size_t)nb * 32);
-  ProfScope ps(ctx, "basis_bwd", 0.0, rows * (4.0 + 32.0 + 128.0));
-  k_basis_freq_grad<<<nb, 256, 0, ctx->stream>>>(rows, vec64, eor, freq, rc, p, dbasis, part);
-  check_launch(ctx);
-  k_reduce_cols<<<1, 1024, 0, ctx->stream>>>(nb, CHG_K, 32, part, grad);
-  check_launch(ctx);
-}
-
 void gate_fwd(chg_ctx *ctx, int64_t rows, const float *y, int ldy, GateLN ln, int mode, const float *w,
               const int32_t *i1, const int32_t *i2, const float *resid, float *out) {
   if (rows <= 0) return;
@@ -837,23 +712,26 @@ void embed_fwd(chg_ctx *ctx, int64_t N, const int32_t *species, const float *W, 
   check_launch(ctx);
 }
 
-int finite_check(chg_ctx *ctx, const float *g, int64_t n) {
+// finite check and the guarded Adam update back to back, then ONE synchronisation: returns the
+// first non-finite flat index (nothing was updated) or -1
+int finite_adam(chg_ctx *ctx, int64_t n, float *p, float *g, float *m, float *v, float lr, float b1, float b2,
+                float eps, double bc1, double bc2) {
   int *bad = ctx->d_flag;
-  ProfScope ps(ctx, "adam", 0.0, 4.0 * n);
-  CUDA_OK(cudaMemsetAsync(bad, 0x7f, 4, ctx->stream));   // 0x7f7f7f7f means none
-  k_finite<<<ceil_div(n, 256), 256, 0, ctx->stream>>>(n, g, bad);
-  check_launch(ctx);
+  {
+    ProfScope ps(ctx, "adam", 0.0, 4.0 * n);
+    CUDA_OK(cudaMemsetAsync(bad, 0x7f, 4, ctx->stream));   // 0x7f7f7f7f means none
+    k_finite<<<ceil_div(n, 256), 256, 0, ctx->stream>>>(n, g, bad);
+    check_launch(ctx);
+  }
+  {
+    const float step_size = (float)(lr / bc1);
+    const float inv_sqrt_bc2 = (float)(1.0 / std::sqrt(bc2));
+    ProfScope ps(ctx, "adam", 0.0, 28.0 * n);
+    k_adam<<<ceil_div(n, 256), 256, 0, ctx->stream>>>(n, p, g, m, v, lr, b1, b2, eps, step_size, inv_sqrt_bc2, bad);
+    check_launch(ctx);
+  }
   int *h = (int *)ctx->pinned_get(64);
   CUDA_OK(cudaMemcpyAsync(h, bad, 4, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_OK(cudaStreamSynchronize(ctx->stream));
   return *h == 0x7f7f7f7f ? -1 : *h;
-}
-
-void adam_update(chg_ctx *ctx, int64_t n, float *p, float *g, float *m, float *v, float lr, float b1, float b2,
-                 float eps, double bc1, double bc2) {
-  float step_size = (float)(lr / bc1);
-  float inv_sqrt_bc2 = (float)(1.0 / std::sqrt(bc2));
-  ProfScope ps(ctx, "adam", 0.0, 28.0 * n);
-  k_adam<<<ceil_div(n, 256), 256, 0, ctx->stream>>>(n, p, g, m, v, lr, b1, b2, eps, step_size, inv_sqrt_bc2);
-  check_launch(ctx);
 }

@@ -2,15 +2,6 @@
 #pragma once
 #include "common.cuh"
 
-// A2 basis (Eq. 12/13 reading Q2, Alg. 2): out [rows, 32] fp32, col 31 = 0
-void basis_radial(chg_ctx *ctx, int64_t rows, const double4 *vec64, const int32_t *edge_of_row,
-                  const float *freq, double r_cut, int p, float *out);
-void basis_angle(chg_ctx *ctx, int64_t A, const double4 *vec64, const int32_t *e1, const int32_t *e2,
-                 float *out);
-// ∂L/∂f_n = Σ_rows dẽ[row, n] · u · sqrt(2/rc) · cos(f_n r / rc) / rc  (accumulated into grad)
-void basis_freq_grad(chg_ctx *ctx, int64_t rows, const double4 *vec64, const int32_t *edge_of_row,
-                     const float *freq, double r_cut, int p, const float *dbasis, float *grad);
-
 // GatedMLP output stage: φ = σ(LN_g(y_g)) ⊙ SiLU(LN_c(y_c)); y [rows,128] = [core | gate]
 struct GateLN { const float *gc, *bc, *gg, *bg; };
 enum GateMode { GATE_MUL_W = 0, GATE_MUL_W1W2 = 1, GATE_RESID = 2 };
@@ -84,6 +75,5 @@ void transpose_params(chg_ctx *ctx, const chg_model *m, float *wt);
 void fill_zero(chg_ctx *ctx, void *p, size_t bytes);
 void embed_fwd(chg_ctx *ctx, int64_t N, const int32_t *species, const float *W, float *v);
 // Adam (PyTorch semantics) + finite check
-int finite_check(chg_ctx *ctx, const float *g, int64_t n);   // returns first bad index or -1 (syncs)
-void adam_update(chg_ctx *ctx, int64_t n, float *p, float *g, float *m, float *v, float lr, float b1,
-                 float b2, float eps, double bc1, double bc2);
+int finite_adam(chg_ctx *ctx, int64_t n, float *p, float *g, float *m, float *v, float lr, float b1, float b2,
+                float eps, double bc1, double bc2);

@@ -102,25 +102,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// A(m, col..col+3); segments are 32-column aligned on this path
-__device__ __forceinline__ float4 tc_loadA4(const AOp &A, int m, int col) {
-  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-  int start = 0;
-#pragma unroll
-  for (int s = 0; s < 4; ++s) {
-    if (s < A.nseg) {
-      int w = A.seg[s].width;
-      if (col >= start && col < start + w) {
-        int row = A.seg[s].idx ? __ldg(A.seg[s].idx + m) : m;
-        if (row >= 0) v = __ldg((const float4 *)(A.seg[s].base + (size_t)row * A.seg[s].ld + (col - start)));
-      }
-      start += w;
-    }
-  }
-  if (A.act == 1) { v.x = siluf_(v.x); v.y = siluf_(v.y); v.z = siluf_(v.z); v.w = siluf_(v.w); }
-  return v;
-}
-
 // TMA descriptors of the direct (non-gathered) A segments: one 32-column x 128-row box per
 // stage lands, 128B-swizzled, exactly where the UMMA descriptor expects it
 struct TcMaps {
@@ -211,16 +192,6 @@ constexpr int NEPI = 8;
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_n(int n) {
-  switch (n) {
-    case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
-    case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
-    case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
-    case 3: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
-    default: asm volatile("cp.async.wait_group 4;" ::: "memory"); break;
-  }
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
