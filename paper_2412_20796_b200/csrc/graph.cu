@@ -25,8 +25,33 @@ struct StructGeo {
   double L[9];      // rows = lattice vectors
   double Linv[9];
   double rw[3];     // r_atom / perpendicular width
-  double pad;
+  int nc[3];        // cell-list grid (cells per lattice direction), 0 = brute-force image search
+  int pad;
 };
+
+// Cell lists for large structures (>= CELL_MIN atoms, every perpendicular width >= 3 cutoffs):
+// cells of width >= r_atom, at most one cell per atom (so a structure's cells index into its
+// own atom range), 27 neighbour cells per atom.  The accepted pairs are exactly those of the
+// brute-force image search (same canonical evaluation of each (i, j, n)); only the candidate
+// set shrinks from O(n^2) to O(n).
+constexpr int CELL_MIN = 256;
+constexpr int CELL_MAXNB = 1024;   // accepted neighbours per atom sorted in shared memory (else brute force)
+__host__ __device__ inline void cell_grid(const double rw[3], int64_t n_atoms, int nc[3]) {
+  bool ok = n_atoms >= CELL_MIN;
+  for (int k = 0; k < 3; ++k) {
+    nc[k] = rw[k] > 0 ? (int)floor(1.0 / (rw[k] * (1.0 + 1e-6))) : 0;
+    if (nc[k] > 1024) nc[k] = 1024;
+    ok = ok && nc[k] >= 3;
+  }
+  while (ok && (int64_t)nc[0] * nc[1] * nc[2] > n_atoms) {   // larger cells stay valid
+    int kmax = 0;
+    for (int k = 1; k < 3; ++k)
+      if (nc[k] > nc[kmax]) kmax = k;
+    if (nc[kmax] <= 3) ok = false;
+    else --nc[kmax];
+  }
+  if (!ok) nc[0] = nc[1] = nc[2] = 0;
+}
 
 __device__ __forceinline__ bool lexpos(int n1, int n2, int n3) {
   return n1 > 0 || (n1 == 0 && (n2 > 0 || (n2 == 0 && n3 > 0)));
@@ -87,8 +112,8 @@ __global__ void k_frac(int N, const double *__restrict__ pos, const int32_t *__r
 // formulas as the host path; invalid cells set flag bits 16 / 32 / 64 (non-finite, |det| <= 1e-6,
 // too thin) and the smallest offending structure index, and get zero ranges so the later
 // kernels stay bounded; the host raises at the size synchronisation.
-__global__ void k_geo(int S, const double *__restrict__ lat, double r_atom, StructGeo *__restrict__ geo,
-                      float *__restrict__ lat_f, int *flag) {
+__global__ void k_geo(int S, const double *__restrict__ lat, double r_atom, const int32_t *__restrict__ atom_ptr,
+                      StructGeo *__restrict__ geo, float *__restrict__ lat_f, int *flag) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= S) return;
   double l[9];
@@ -123,8 +148,125 @@ __global__ void k_geo(int S, const double *__restrict__ lat, double r_atom, Stru
     atomicOr(flag, bad);
     atomicMin(flag + 1, s);
   }
-  g.pad = 0.0;
+  cell_grid(g.rw, atom_ptr[s + 1] - atom_ptr[s], g.nc);
+  g.pad = 0;
   geo[s] = g;
+}
+
+__device__ __forceinline__ long long edge_key(int nb, char4 im) {
+  return ((long long)nb << 24) | ((long long)((int)im.x + 128) << 16) | ((long long)((int)im.y + 128) << 8) |
+         (long long)((int)im.z + 128);
+}
+
+// ---- cell lists (structures with g.nc[0] > 0) ----
+struct CellArgs {
+  int32_t *atom_cell;       // [N] local cell of the atom's wrapped position, -1 = brute-force structure
+  int32_t *cell_cnt;        // [N] (structure base + cell) -> atoms; also the placement cursor
+  int32_t *cell_start;      // [N + 1]
+  int32_t *cell_atoms;      // [N] atoms grouped by cell
+};
+
+__device__ __forceinline__ int cell_coord(double f, int nc) {
+  const double w = f - floor(f);
+  int c = (int)(w * nc);
+  return c < 0 ? 0 : (c >= nc ? nc - 1 : c);
+}
+
+__global__ void k_cell_assign(int N, const double *__restrict__ frac, const int32_t *__restrict__ soa,
+                              const int32_t *__restrict__ atom_ptr, const StructGeo *__restrict__ geo, CellArgs ca) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const int s = soa[i];
+  const StructGeo &g = geo[s];
+  if (g.nc[0] == 0) { ca.atom_cell[i] = -1; return; }
+  const int c = (cell_coord(frac[3 * i], g.nc[0]) * g.nc[1] + cell_coord(frac[3 * i + 1], g.nc[1])) * g.nc[2] +
+                cell_coord(frac[3 * i + 2], g.nc[2]);
+  ca.atom_cell[i] = c;
+  atomicAdd(&ca.cell_cnt[atom_ptr[s] + c], 1);
+}
+
+// block per structure: exclusive scan of its cell counts -> absolute start positions
+__global__ void k_cell_scan(int S, const int32_t *__restrict__ atom_ptr, const StructGeo *__restrict__ geo,
+                            CellArgs ca) {
+  __shared__ int sh[256];
+  const int s = blockIdx.x;
+  const StructGeo &g = geo[s];
+  if (g.nc[0] == 0) return;
+  const int base = atom_ptr[s], ncell = g.nc[0] * g.nc[1] * g.nc[2];
+  int carry = base;
+  for (int c0 = 0; c0 < ncell; c0 += 256) {
+    const int c = c0 + threadIdx.x;
+    const int v = c < ncell ? ca.cell_cnt[base + c] : 0;
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 1; o < 256; o <<= 1) {
+      const int t = threadIdx.x >= o ? sh[threadIdx.x - o] : 0;
+      __syncthreads();
+      sh[threadIdx.x] += t;
+      __syncthreads();
+    }
+    if (c < ncell) ca.cell_start[base + c] = carry + sh[threadIdx.x] - v;
+    carry += sh[255];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) ca.cell_start[base + ncell] = carry;   // == atom_ptr[s + 1]
+}
+
+__global__ void k_cell_place(int N, const int32_t *__restrict__ soa, const int32_t *__restrict__ atom_ptr,
+                             CellArgs ca, int32_t *__restrict__ cursor) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const int c = ca.atom_cell[i];
+  if (c < 0) return;
+  const int base = atom_ptr[soa[i]];
+  ca.cell_atoms[ca.cell_start[base + c] + atomicAdd(&cursor[base + c], 1)] = i;
+}
+
+// candidate t of atom i's 27 neighbour cells -> (j, n); cnt27 = exclusive prefix of cell sizes
+__device__ __forceinline__ void cell_candidate(const CellArgs &ca, int base, const StructGeo &g, int ci0, int ci1,
+                                               int ci2, const int *cnt27, int t, const double *frac, const int *si,
+                                               int &j, int &n1, int &n2, int &n3) {
+  int d = 0;
+  while (d < 26 && cnt27[d + 1] <= t) ++d;
+  const int dd[3] = {d / 9 - 1, (d / 3) % 3 - 1, d % 3 - 1};
+  const int cc[3] = {ci0, ci1, ci2};
+  int x[3], w[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    x[k] = cc[k] + dd[k];
+    w[k] = 0;
+    if (x[k] < 0) { x[k] += g.nc[k]; w[k] = -1; }
+    else if (x[k] >= g.nc[k]) { x[k] -= g.nc[k]; w[k] = 1; }
+  }
+  const int cell = (x[0] * g.nc[1] + x[1]) * g.nc[2] + x[2];
+  j = ca.cell_atoms[ca.cell_start[base + cell] + (t - cnt27[d])];
+  // d = r_i - (r_j + nL) with wrapped cells: n = shift_i - shift_j + wrap
+  n1 = si[0] - (int)floor(frac[3 * j]) + w[0];
+  n2 = si[1] - (int)floor(frac[3 * j + 1]) + w[1];
+  n3 = si[2] - (int)floor(frac[3 * j + 2]) + w[2];
+}
+
+// sizes of atom i's 27 neighbour cells as an exclusive prefix in smem (threads 0..26)
+__device__ __forceinline__ void cell_prefix(const CellArgs &ca, int base, const StructGeo &g, int ci, int *cnt27,
+                                            int (&cc)[3]) {
+  cc[0] = ci / (g.nc[1] * g.nc[2]);
+  cc[1] = (ci / g.nc[2]) % g.nc[1];
+  cc[2] = ci % g.nc[2];
+  if (threadIdx.x < 27) {
+    const int d = threadIdx.x;
+    const int dd[3] = {d / 9 - 1, (d / 3) % 3 - 1, d % 3 - 1};
+    int x[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) x[k] = (cc[k] + dd[k] + g.nc[k]) % g.nc[k];
+    const int cell = (x[0] * g.nc[1] + x[1]) * g.nc[2] + x[2];
+    cnt27[d + 1] = ca.cell_start[base + cell + 1] - ca.cell_start[base + cell];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    cnt27[0] = 0;
+    for (int d = 0; d < 27; ++d) cnt27[d + 1] += cnt27[d];
+  }
+  __syncthreads();
 }
 
 // One 128-thread block (4 warps) per centre atom i.  Lanes walk (j, n1) slots: W >= any pair's
@@ -163,8 +305,9 @@ __global__ void __launch_bounds__(32 * GWPA) k_count(int N, const double *__rest
                                                      const int32_t *__restrict__ atom_ptr,
                                                      const StructGeo *__restrict__ geo, double ra2, double rb2,
                                                      int32_t *__restrict__ cnt_e, int32_t *__restrict__ cnt_b,
-                                                     int *flag) {
+                                                     int *flag, CellArgs ca) {
   __shared__ int sh[GWPA][2];
+  __shared__ int cnt27[28];
   const int i = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (i >= N) return;
   const int s = soa[i];
@@ -174,14 +317,32 @@ __global__ void __launch_bounds__(32 * GWPA) k_count(int N, const double *__rest
 #pragma unroll
   for (int k = 0; k < 9; ++k) L[k] = g.L[k];
   const double fi[3] = {frac[3 * i], frac[3 * i + 1], frac[3 * i + 2]};
-  const int W = (int)floor(2.0 * g.rw[0]) + 4;
-  const int nslot = (a1 - a0) * W;
   int ce = 0, cbt = 0, bad = 0;
-  for (int p = w * 32 + lane; p < nslot; p += 32 * GWPA) {
-    int cb, j, n1;
-    Range r;
-    ce += slot_count(pos, frac, L, g, fi, i, a0, W, p, ra2, rb2, cb, bad, r, j, n1);
-    cbt += cb;
+  if (g.nc[0] > 0) {                                  // cell list: candidates of the 27 neighbour cells
+    int cc[3];
+    cell_prefix(ca, a0, g, ca.atom_cell[i], cnt27, cc);
+    const int si[3] = {(int)floor(fi[0]), (int)floor(fi[1]), (int)floor(fi[2])};
+    for (int t = threadIdx.x; t < cnt27[27]; t += 32 * GWPA) {
+      int j, n1, n2, n3;
+      cell_candidate(ca, a0, g, cc[0], cc[1], cc[2], cnt27, t, frac, si, j, n1, n2, n3);
+      if (i == j && n1 == 0 && n2 == 0 && n3 == 0) continue;
+      double dx, dy, dz, q;
+      eval_pair(pos, L, i, j, n1, n2, n3, dx, dy, dz, q);
+      if (q <= ra2) {
+        ++ce;
+        cbt += (q <= rb2);
+        bad |= (q < 1e-12);
+      }
+    }
+  } else {
+    const int W = (int)floor(2.0 * g.rw[0]) + 4;
+    const int nslot = (a1 - a0) * W;
+    for (int p = w * 32 + lane; p < nslot; p += 32 * GWPA) {
+      int cb, j, n1;
+      Range r;
+      ce += slot_count(pos, frac, L, g, fi, i, a0, W, p, ra2, rb2, cb, bad, r, j, n1);
+      cbt += cb;
+    }
   }
   ce = __reduce_add_sync(0xffffffffu, ce);
   cbt = __reduce_add_sync(0xffffffffu, cbt);
@@ -255,8 +416,12 @@ __global__ void __launch_bounds__(32 * GWPA) k_fill(int N, const double *__restr
                                                     const int32_t *__restrict__ bond_ptr, int32_t *__restrict__ center,
                                                     int32_t *__restrict__ nbr, char4 *__restrict__ img,
                                                     float4 *__restrict__ vec, double4 *__restrict__ vec64,
-                                                    int32_t *__restrict__ bond_id, int32_t *__restrict__ bond_edge) {
+                                                    int32_t *__restrict__ bond_id, int32_t *__restrict__ bond_edge,
+                                                    CellArgs ca) {
   __shared__ int sh[GWPA][2];
+  __shared__ int cnt27[28];
+  __shared__ long long keys[CELL_MAXNB];
+  __shared__ int nacc, bpre[CELL_MAXNB];
   const int i = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (i >= N) return;
   const int s = soa[i];
@@ -267,6 +432,81 @@ __global__ void __launch_bounds__(32 * GWPA) k_fill(int N, const double *__restr
   for (int k = 0; k < 9; ++k) L[k] = g.L[k];
   const double fi[3] = {frac[3 * i], frac[3 * i + 1], frac[3 * i + 2]};
   int be = row_ptr[i], bb = bond_ptr[i];
+  if (g.nc[0] > 0 && row_ptr[i + 1] - be <= CELL_MAXNB) {
+    // cell list: accepted (j, n) keys collected in any order, sorted (bitonic) into the canonical
+    // (j, n1, n2, n3) order of the CSR row, then written with a block scan for the bond numbers
+    int cc[3];
+    cell_prefix(ca, a0, g, ca.atom_cell[i], cnt27, cc);
+    const int si[3] = {(int)floor(fi[0]), (int)floor(fi[1]), (int)floor(fi[2])};
+    if (threadIdx.x == 0) nacc = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < cnt27[27]; t += 32 * GWPA) {
+      int j, n1, n2, n3;
+      cell_candidate(ca, a0, g, cc[0], cc[1], cc[2], cnt27, t, frac, si, j, n1, n2, n3);
+      if (i == j && n1 == 0 && n2 == 0 && n3 == 0) continue;
+      double dx, dy, dz, q;
+      eval_pair(pos, L, i, j, n1, n2, n3, dx, dy, dz, q);
+      if (q <= ra2) {
+        const int slot = atomicAdd(&nacc, 1);
+        if (slot < CELL_MAXNB) keys[slot] = edge_key(j, make_char4((signed char)n1, (signed char)n2, (signed char)n3, 0));
+      }
+    }
+    __syncthreads();
+    const int na = min(nacc, CELL_MAXNB);
+    int np2 = 1;
+    while (np2 < na) np2 <<= 1;
+    for (int k = na + threadIdx.x; k < np2; k += 32 * GWPA) keys[k] = 0x7fffffffffffffffLL;
+    __syncthreads();
+    for (int size = 2; size <= np2; size <<= 1)       // bitonic sort, ascending
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int k = threadIdx.x; k < np2; k += 32 * GWPA) {
+          const int o = k ^ stride;
+          if (o > k) {
+            const bool up = (k & size) == 0;
+            const long long x = keys[k], y = keys[o];
+            if ((x > y) == up) { keys[k] = y; keys[o] = x; }
+          }
+        }
+        __syncthreads();
+      }
+    // bond flags -> exclusive prefix (single thread: <= CELL_MAXNB entries, off the hot path)
+    for (int k = threadIdx.x; k < na; k += 32 * GWPA) {
+      const long long key = keys[k];
+      const int j = (int)(key >> 24);
+      const int n1 = (int)((key >> 16) & 255) - 128, n2 = (int)((key >> 8) & 255) - 128, n3 = (int)(key & 255) - 128;
+      double dx, dy, dz, q;
+      eval_pair(pos, L, i, j, n1, n2, n3, dx, dy, dz, q);
+      bpre[k] = q <= rb2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      for (int k = 0; k < na; ++k) { const int f = bpre[k]; bpre[k] = acc; acc += f; }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < na; k += 32 * GWPA) {
+      const long long key = keys[k];
+      const int j = (int)(key >> 24);
+      const int n1 = (int)((key >> 16) & 255) - 128, n2 = (int)((key >> 8) & 255) - 128, n3 = (int)(key & 255) - 128;
+      double dx, dy, dz, q;
+      eval_pair(pos, L, i, j, n1, n2, n3, dx, dy, dz, q);
+      const int e = be + k;
+      center[e] = i;
+      nbr[e] = j;
+      img[e] = make_char4((signed char)n1, (signed char)n2, (signed char)n3, 0);
+      const double rr = sqrt(q);
+      vec[e] = make_float4((float)dx, (float)dy, (float)dz, (float)rr);
+      vec64[e] = make_double4(dx, dy, dz, rr);
+      if (q <= rb2) {
+        const int b = bb + bpre[k];
+        bond_id[e] = b;
+        bond_edge[b] = e;
+      } else {
+        bond_id[e] = -1;
+      }
+    }
+    return;
+  }
   const int W = (int)floor(2.0 * g.rw[0]) + 4;
   const int nslot = (a1 - a0) * W;
   for (int p0 = 0; p0 < nslot; p0 += 32 * GWPA) {
@@ -341,10 +581,6 @@ __global__ void k_angles(int B, const int32_t *__restrict__ bond_edge, const int
   }
 }
 
-__device__ __forceinline__ long long edge_key(int nb, char4 im) {
-  return ((long long)nb << 24) | ((long long)((int)im.x + 128) << 16) | ((long long)((int)im.y + 128) << 8) |
-         (long long)((int)im.z + 128);
-}
 
 __global__ void k_rev(int E, const int32_t *__restrict__ center, const int32_t *__restrict__ nbr,
                       const char4 *__restrict__ img, const int32_t *__restrict__ row_ptr,
@@ -420,6 +656,8 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
       g.rw[k] = r_atom / width;
       if (g.rw[k] > 100.0) CHG_THROW(CHG_ERR_GEOMETRY, "structure %d: cell too thin for cutoff", s);
     }
+    cell_grid(g.rw, atom_ptr[s + 1] - atom_ptr[s], g.nc);
+    g.pad = 0;
   }
 
   chg_graph *G = new chg_graph();
@@ -441,6 +679,10 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
                      align_up(4 * (size_t)(n_species + 2)) + align_up(4 * 9 * (size_t)S) +
                      align_up(4 * (size_t)S) + align_up(sizeof(StructGeo) * geo.size()) +
                      align_up(8 * 3 * N) * 2 + align_up(4 * N) * 2 + align_up(64);
+    // cell lists only when some structure is large enough to use them (host knows the sizes)
+    bool any_cells = false;
+    for (int ss = 0; ss < S; ++ss) any_cells = any_cells || atom_ptr[ss + 1] - atom_ptr[ss] >= CELL_MIN;
+    if (any_cells) sz_atom += align_up(4 * N) * 4 + align_up(4 * (N + 1));
     void *blk1 = nullptr;
     CUDA_OK(cudaMallocAsync(&blk1, sz_atom, st));
     bl->a = blk1;
@@ -460,6 +702,15 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
     int32_t *cnt_e = (int32_t *)take(4 * N);
     int32_t *cnt_b = (int32_t *)take(4 * N);
     long long *d_tot = (long long *)take(64);
+    CellArgs ca{};
+    int32_t *cell_cursor = nullptr;
+    if (any_cells) {
+      ca.atom_cell = (int32_t *)take(4 * N);
+      ca.cell_cnt = (int32_t *)take(4 * N);
+      ca.cell_start = (int32_t *)take(4 * (N + 1));
+      ca.cell_atoms = (int32_t *)take(4 * N);
+      cell_cursor = (int32_t *)take(4 * N);
+    }
 
     // host-side per-atom/per-structure arrays via pinned staging
     size_t hbytes = 4 * (S + 1) + 4 * N + 4 * 9 * (size_t)S + 4 * (size_t)S + sizeof(StructGeo) * geo.size();
@@ -506,15 +757,25 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
     CUDA_OK(cudaMemsetAsync(d_tot, 0, 64, st));
     double ra2 = r_atom * r_atom, rb2 = r_bond * r_bond;
     if (dev_geo) {
-      k_geo<<<ceil_div(S, 128), 128, 0, st>>>(S, lat, r_atom, d_geo, G->lattice_f, flag);
+      k_geo<<<ceil_div(S, 128), 128, 0, st>>>(S, lat, r_atom, G->atom_ptr, d_geo, G->lattice_f, flag);
       check_launch(ctx);
     }
     if (N) {
       k_frac<<<ceil_div(N, 256), 256, 0, st>>>((int)N, d_pos, G->struct_of_atom, d_geo, G->species,
                                                 n_species, d_frac, flag);
       check_launch(ctx);
+      if (any_cells) {
+        CUDA_OK(cudaMemsetAsync(ca.cell_cnt, 0, 4 * N, st));
+        CUDA_OK(cudaMemsetAsync(cell_cursor, 0, 4 * N, st));
+        k_cell_assign<<<ceil_div(N, 256), 256, 0, st>>>((int)N, d_frac, G->struct_of_atom, G->atom_ptr, d_geo, ca);
+        check_launch(ctx);
+        k_cell_scan<<<S, 256, 0, st>>>(S, G->atom_ptr, d_geo, ca);
+        check_launch(ctx);
+        k_cell_place<<<ceil_div(N, 256), 256, 0, st>>>((int)N, G->struct_of_atom, G->atom_ptr, ca, cell_cursor);
+        check_launch(ctx);
+      }
       k_count<<<(unsigned)N, 32 * GWPA, 0, st>>>((int)N, d_pos, d_frac, G->struct_of_atom, G->atom_ptr,
-                                                      d_geo, ra2, rb2, cnt_e, cnt_b, flag);
+                                                      d_geo, ra2, rb2, cnt_e, cnt_b, flag, ca);
       check_launch(ctx);
       k_scan<<<1, 1024, 0, st>>>((int)N, cnt_e, cnt_b, G->row_ptr, G->bond_ptr, G->atom_angle_ptr, d_tot);
       check_launch(ctx);
@@ -569,7 +830,7 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
     if (N) {
       k_fill<<<(unsigned)N, 32 * GWPA, 0, st>>>((int)N, d_pos, d_frac, G->struct_of_atom, G->atom_ptr,
                                                      d_geo, ra2, rb2, G->row_ptr, G->bond_ptr, G->center,
-                                                     G->nbr, G->img, G->vec, G->vec64, G->bond_id, G->bond_edge);
+                                                     G->nbr, G->img, G->vec, G->vec64, G->bond_id, G->bond_edge, ca);
       check_launch(ctx);
       k_angles<<<ceil_div(B + 1, 256), 256, 0, st>>>((int)B, G->bond_edge, G->center, G->bond_ptr,
                                                       G->atom_angle_ptr, G->angle_ptr, G->angle_b1,

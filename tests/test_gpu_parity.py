@@ -10,7 +10,8 @@ Parameters and labels are rounded to fp32 once and given to BOTH sides.
 import numpy as np
 import pytest
 
-from chg_inputs import (Batch, concat_batches, dimer, init_flat_params, make_config_batch, mptrj_like_batch,
+from chg_inputs import (Batch, concat_batches, dimer, init_flat_params, lifepo4_like_cell, make_config_batch,
+                        mptrj_like_batch,
                         si_diamond, simple_cubic, skewed_oxide_batch)
 
 pytestmark = pytest.mark.gpu
@@ -58,7 +59,27 @@ def _labels64(b):
                  magmom=lb["magmom"].astype(np.float64), magmom_mask=lb["magmom_mask"])
 
 
+def _large_cell(n, edge, shear=0.0, shift=False, seed=3001):
+    """A >= 256-atom cell with every width >= 3 cutoffs (cell-list path of the builder);
+    optional shear (triclinic) and atoms moved by whole lattice vectors (wrapping)."""
+    b = lifepo4_like_cell(n_atoms=n, edge=edge, seed=seed)
+    L = b.lattice[0].copy()
+    f = b.positions @ np.linalg.inv(L)
+    if shear:
+        L[1] += shear * L[0]
+        L[2] += 0.5 * shear * L[1]
+    if shift:
+        rng = np.random.default_rng(seed)
+        f = f + rng.integers(-1, 2, size=f.shape)
+    pos = f @ L
+    return Batch(atom_ptr=b.atom_ptr, positions=pos, lattice=L[None], species=b.species,
+                 energy_per_atom=b.energy_per_atom, forces=b.forces, stress=b.stress, magmom=b.magmom,
+                 magmom_mask=b.magmom_mask)
+
+
 GRAPH_CASES = {
+    "cells_300": lambda: _large_cell(300, 16.0),
+    "cells_300_triclinic_shifted": lambda: _large_cell(300, 17.5, shear=0.12, shift=True),
     "si_diamond": lambda: si_diamond(),
     "si_diamond_r6": lambda: si_diamond(),
     "simple_cubic_r6": lambda: simple_cubic(3.0),
