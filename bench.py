@@ -376,6 +376,33 @@ def main():
         weak_base = {"workload": "C3: 128 MPtrj-shaped structures on 1 GPU (the per-GPU work of the N > 1 runs)",
                      "value": s_c3 / (ms_c3 / 1e3), "unit": "structures/s", "ms_per_step": ms_c3 / a.steps}
 
+    # C5 (BASELINE configs[4]): one 4,096-atom LiFePO4-like cell, graph build + forward with the
+    # force / stress readout (inference path), device-timed latency
+    c5 = None
+    if ws == 1 and wl == "C2":
+        b5 = make_config_batch("C5")
+        d5 = (torch.as_tensor(b5.positions, device="cuda"), torch.as_tensor(b5.lattice, device="cuda"),
+              torch.as_tensor(b5.species, device="cuda"))
+        model5 = models[a.precision]
+
+        def inf5():
+            g5 = ctx.build_graph(b5.atom_ptr, d5[0], d5[1], d5[2], 5.0, 3.0)
+            ctx.forward(model5, g5, train=False, host=False)
+            return g5
+        for _ in range(a.warmup):
+            inf5().close()
+        ev5 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+        barrier()
+        for k in range(a.steps):
+            ev5[k][0].record(stream)
+            g5 = inf5()
+            ev5[k][1].record(stream)
+            g5.close()
+        barrier()
+        t5 = sorted(s.elapsed_time(e) for s, e in ev5)
+        c5 = {"workload": "C5: one 4,096-atom LiFePO4-like cell (graph build + forward + force/stress readout)",
+              "atoms": int(b5.n_atoms), "latency_ms_median": t5[len(t5) // 2], "latency_ms_min": t5[0]}
+
     structs = sum(batches[k % len(batches)]["gl"]["S"] for k in range(a.steps))
     value = structs / (ms / 1e3)
     e2e = structs / (ms_e2e / 1e3)
@@ -457,6 +484,7 @@ def main():
             "e2e": {"value": e2e, "unit": "structures/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 40 + 4},
             "gpu_launches": int(launches),
             "weak_scaling_base": weak_base,
+            "c5_inference": c5,
             "clocks": clk,
             "roofline": roof,
             "gather_scatter": gather,
