@@ -164,6 +164,16 @@ void *chg_model_device_ptr(chg_model *m, int which);
  * workspace (valid until the next chg_forward on ctx). */
 chg_status chg_forward(chg_ctx *ctx, chg_model *m, chg_graph *g, int train, chg_pred *out);
 
+/* ---- conservative forces (the reference-CHGNet output) --
+ * Same outputs as chg_forward except forces and stress, which are the derivatives of the
+ * energy head instead of the decomposed heads (Eq. 7 / Eq. 9):
+ *   forces[i] = −∂E/∂r_i (eV/Å),  stress[s] = (160.21766208 / V_s)·∂E_s/∂ε_s (GPa, reading Q27,
+ *   r → r(I+ε), L → L(I+ε), graph fixed); energy, energy_per_atom, magmom as in chg_forward.
+ * One forward pass plus a first-order backward seeded with ∂E/∂e_atom = 1 (parameter
+ * gradients untouched) and analytic basis derivatives (fp64 geometry).  Consumes the
+ * train-mode activations: a following chg_backward needs a new chg_forward (CHG_ERR_STATE). */
+chg_status chg_forward_conservative(chg_ctx *ctx, chg_model *m, chg_graph *g, chg_pred *out);
+
 /* ---- A7-A8 loss + backward (first-order only) ---------
  * Computes the Huber loss of the last train-mode forward and ACCUMULATES
  * dL/dθ into the model's gradient vector.  loss_out (host, optional) =

@@ -63,6 +63,7 @@ SYMBOLS = ["chg_ctx_create", "chg_ctx_destroy", "chg_last_error", "chg_sync", "c
            "chg_nccl_unique_id", "chg_ctx_set_nccl", "chg_build_graph", "chg_graph_counts", "chg_graph_export",
            "chg_graph_destroy", "chg_model_create", "chg_model_destroy", "chg_model_layout",
            "chg_model_num_params", "chg_model_set", "chg_model_get", "chg_model_device_ptr", "chg_forward",
+           "chg_forward_conservative",
            "chg_backward", "chg_step", "chg_balance", "chg_profile", "chg_profile_query", "chg_debug_gemm", "chg_debug_get"]
 
 _lib = None
@@ -98,6 +99,7 @@ def load(path: str = LIB_PATH):
         "chg_model_get": (C.c_int, [vp, C.c_int, vp, i64]),
         "chg_model_device_ptr": (vp, [vp, C.c_int]),
         "chg_forward": (C.c_int, [vp, vp, vp, C.c_int, C.POINTER(Pred)]),
+        "chg_forward_conservative": (C.c_int, [vp, vp, vp, C.POINTER(Pred)]),
         "chg_backward": (C.c_int, [vp, vp, vp, C.POINTER(Labels), C.POINTER(LossCfg), dp]),
         "chg_step": (C.c_int, [vp, vp, C.POINTER(AdamCfg)]),
         "chg_balance": (C.c_int, [vp, i32, i32, vp]),
@@ -209,6 +211,18 @@ class Context:
         else:
             self._check(self.lib.chg_forward(self.h, model.h, graph.h, int(train), None))
         return None
+
+    def forward_conservative(self, model: "Model", graph: "Graph") -> Dict[str, np.ndarray]:
+        """chg_forward_conservative: energy-head forces F = -dE/dr and stress (160.2/V) dE/deps
+        (the reference-CHGNet output) plus energy / magmom, as numpy arrays."""
+        N, E, B, A = graph.counts()
+        S = graph.n_struct
+        res = {"energy": np.zeros(S, np.float32), "energy_per_atom": np.zeros(S, np.float32),
+               "forces": np.zeros((N, 3), np.float32), "stress": np.zeros((S, 3, 3), np.float32),
+               "magmom": np.zeros(N, np.float32)}
+        p = Pred(*(_ptr(res[k]) for k in ("energy", "energy_per_atom", "forces", "stress", "magmom")), 0)
+        self._check(self.lib.chg_forward_conservative(self.h, model.h, graph.h, C.byref(p)))
+        return res
 
     def backward(self, model: "Model", graph: "Graph", labels: Dict, w=(2.0, 1.5, 0.1, 0.1), delta: float = 0.1,
                  n_struct_global: int = 0, n_atoms_global: int = 0, n_magmom_global: int = 0,

@@ -17,6 +17,7 @@ void forward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, int train, chg_pred 
 void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *lab,
                    const chg_loss_cfg *cfg, double *loss_out);
 void step_impl(chg_ctx *ctx, chg_model *m, const chg_adam_cfg *cfg);
+void derivative_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, chg_pred *out);
 
 // ---------------------------------------------------------------------------
 // ctx helpers
@@ -371,6 +372,15 @@ chg_status chg_forward(chg_ctx *ctx, chg_model *m, chg_graph *g, int train, chg_
   ABI_GUARD(ctx, {
     CUDA_OK(cudaSetDevice(ctx->device));
     forward_impl(ctx, m, g, train, out);
+  });
+}
+
+chg_status chg_forward_conservative(chg_ctx *ctx, chg_model *m, chg_graph *g, chg_pred *out) {
+  if (!ctx || !m || !g) return CHG_ERR_ARG;
+  if (m->ctx != ctx || g->ctx != ctx) { ctx->err = "model/graph bound to another ctx"; return CHG_ERR_ARG; }
+  ABI_GUARD(ctx, {
+    CUDA_OK(cudaSetDevice(ctx->device));
+    derivative_impl(ctx, m, g, out);
   });
 }
 

@@ -109,6 +109,8 @@ struct chg_ctx {
   std::string ws_name(const char *base) const { return stream == side && side ? std::string(base) + "#side" : base; }
   // deferred reductions (reduce.cu): active inside backward layers
   bool red_on = false;
+  // conservative-force pass (deriv.cu): the backward runs without parameter gradients
+  bool no_param_grads = false;
   std::vector<RedJob> red_jobs;
   void *get(const std::string &name, size_t bytes);
   float *getf(const std::string &name, size_t n) { return (float *)get(name, n * sizeof(float)); }

@@ -355,6 +355,7 @@ static void launch_wgrad_reduce(chg_ctx *ctx, const WGrad &g, const float *parti
 }
 
 void wgrad(chg_ctx *ctx, const WGrad &g) {
+  if (ctx->no_param_grads) return;
   int Kp = g.K + (g.bias ? 1 : 0);
   if (Kp <= 0 || g.N <= 0) return;
   if (g.tc && ctx->use_tc && g.M > 0) {

@@ -553,34 +553,15 @@ const float *labels_dev(chg_ctx *ctx, const void *p, size_t bytes, const char *n
 
 }  // namespace
 
-void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *lab_in, const chg_loss_cfg *cfg,
-                   double *loss_out) {
+// Everything after the loss seeds: head adjoints, interaction blocks (last to first), and —
+// for training — the embedding / projection / frequency gradients.  deriv = 1: the
+// conservative-force pass (seed ∂E/∂e_atom = 1 only, no parameter gradients): the force,
+// stress and magmom heads are skipped and dE/d(e⁰, eᵃ, eᵇ, a⁰) are left in the de, dea, deb,
+// da scratch rows for the geometry kernels (deriv.cu).
+static void backward_core(chg_ctx *ctx, chg_model *m, chg_graph *g, const LossSeeds &sd, bool deriv) {
   const int64_t N = g->N, E = g->E, B = g->B, A = g->A;
-  const int S = g->S, T = m->cfg.n_bond_conv;
-  if (!lab_in->energy_per_atom || !lab_in->forces || !lab_in->stress || !lab_in->magmom || !lab_in->magmom_mask)
-    CHG_THROW(CHG_ERR_ARG, "all label arrays are required");
+  const int T = m->cfg.n_bond_conv;
   Bwd Bw{ctx, m, g, nullptr};
-  // split-partial reductions of a layer are batched into one launch (reduce.cu)
-  struct RedScope {
-    chg_ctx *c;
-    explicit RedScope(chg_ctx *x) : c(x) { c->red_on = true; c->red_jobs.clear(); }
-    ~RedScope() { c->red_on = false; c->red_jobs.clear(); }
-  } red_scope(ctx);
-  chg_labels lab = *lab_in;
-  lab.energy_per_atom = labels_dev(ctx, lab_in->energy_per_atom, 4 * S, "lab_epa", lab_in->on_device);
-  lab.forces = labels_dev(ctx, lab_in->forces, 12 * N, "lab_f", lab_in->on_device);
-  lab.stress = labels_dev(ctx, lab_in->stress, 36 * (size_t)S, "lab_s", lab_in->on_device);
-  lab.magmom = labels_dev(ctx, lab_in->magmom, 4 * N, "lab_m", lab_in->on_device);
-  lab.magmom_mask = (const uint8_t *)labels_dev(ctx, lab_in->magmom_mask, N, "lab_mask", lab_in->on_device);
-  lab.on_device = 1;
-  // A7 loss + seeds
-  LossSeeds sd;
-  sd.d_eatom = Bw.scratch("seed_eatom", N, 1);
-  sd.d_M9 = Bw.scratch("seed_M9", N, 9);
-  sd.d_mag = Bw.scratch("seed_mag", N, 1);
-  sd.d_ne = Bw.scratch("seed_ne", E, 1);
-  loss_and_seeds(ctx, g, Bw.act("energy_per_atom"), Bw.act("forces"), Bw.act("stress"), Bw.act("magmom"), lab, *cfg,
-                 sd);
   if (!m->wt) CUDA_OK(cudaMalloc(&m->wt, 4 * (size_t)std::max<int64_t>(m->P, 1)));
   Bw.wt = m->wt;
   if (m->cfg.mlp_precision != 2) transpose_params(ctx, m, Bw.wt);   // TF32 mode: the forward's copy is current
@@ -596,9 +577,9 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
   fill_zero(ctx, deb, 4 * 64 * B);
   const float *vf = Bw.act("v" + std::to_string(T + 1)), *ef = Bw.act("e" + std::to_string(T));
   // heads backward: the force head (-> de) beside the atom-side heads (-> dv)
-  on_side(ctx, [&] { mlp_bwd(Bw, "head_F", 3, ef, E, sd.d_ne, 1, de); });
+  if (!deriv) on_side(ctx, [&] { mlp_bwd(Bw, "head_F", 3, ef, E, sd.d_ne, 1, de); });
   mlp_bwd(Bw, "head_E", 4, vf, N, sd.d_eatom, 1, dv);
-  {
+  if (!deriv) {
     WGrad wg;
     wg.A.seg[0] = aseg(vf, 64, 64);
     wg.A.nseg = 1;
@@ -616,7 +597,7 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
     G.tag = "headM_b";
     rowgemm(ctx, G);
   }
-  mlp_bwd(Bw, "head_S", 3, vf, N, sd.d_M9, 9, dv);
+  if (!deriv) mlp_bwd(Bw, "head_S", 3, vf, N, sd.d_M9, 9, dv);
   // A8 interaction blocks, last to first
   const float *ea = Bw.act("ea"), *eb = Bw.act("eb");
   float *dagg = Bw.scratch("dagg", N, 64), *daggb = Bw.scratch("daggb", B, 64);
@@ -654,6 +635,10 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
     bc_bwd_body(Bw, t, ab, V(t), Ef(t), Af(t), eb, daggb, dv, de, da, deb, 2);
     red_flush(ctx);
   }
+  if (deriv) {                                      // no parameter gradients on this pass
+    red_flush(ctx);
+    return;
+  }
   // embedding (rows of W_v gathered by species -> grouped sum, no atomics)
   embed_grad(ctx, N, m->cfg.n_species, g->species, dv, Bw.G("embed.W"));
   // projections (Eq. 2) and trainable frequencies, from the saved bases (proj.cu)
@@ -664,18 +649,82 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
   proj_bwd(ctx, A, Bw.act("a_t"), nullptr, da, nullptr, m->p("proj.Wtheta"), nullptr, Bw.G("proj.Wtheta"), nullptr,
            nullptr);
   red_flush(ctx);
+  ctx->dbg["dv0"] = {dv, N, 64, 64};
+  ctx->dbg["de0"] = {de, E, 64, 64};
+  ctx->dbg["da0"] = {da, A, 64, 64};
+  ctx->dbg["dea"] = {dea, E, 64, 64};
+  ctx->dbg["deb"] = {deb, B, 64, 64};
+}
+
+void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *lab_in, const chg_loss_cfg *cfg,
+                   double *loss_out) {
+  const int64_t N = g->N, E = g->E, B = g->B, A = g->A;
+  const int S = g->S, T = m->cfg.n_bond_conv;
+  if (!lab_in->energy_per_atom || !lab_in->forces || !lab_in->stress || !lab_in->magmom || !lab_in->magmom_mask)
+    CHG_THROW(CHG_ERR_ARG, "all label arrays are required");
+  Bwd Bw{ctx, m, g, nullptr};
+  // split-partial reductions of a layer are batched into one launch (reduce.cu)
+  struct RedScope {
+    chg_ctx *c;
+    explicit RedScope(chg_ctx *x) : c(x) { c->red_on = true; c->red_jobs.clear(); }
+    ~RedScope() { c->red_on = false; c->red_jobs.clear(); }
+  } red_scope(ctx);
+  chg_labels lab = *lab_in;
+  lab.energy_per_atom = labels_dev(ctx, lab_in->energy_per_atom, 4 * S, "lab_epa", lab_in->on_device);
+  lab.forces = labels_dev(ctx, lab_in->forces, 12 * N, "lab_f", lab_in->on_device);
+  lab.stress = labels_dev(ctx, lab_in->stress, 36 * (size_t)S, "lab_s", lab_in->on_device);
+  lab.magmom = labels_dev(ctx, lab_in->magmom, 4 * N, "lab_m", lab_in->on_device);
+  lab.magmom_mask = (const uint8_t *)labels_dev(ctx, lab_in->magmom_mask, N, "lab_mask", lab_in->on_device);
+  lab.on_device = 1;
+  // A7 loss + seeds
+  LossSeeds sd;
+  sd.d_eatom = Bw.scratch("seed_eatom", N, 1);
+  sd.d_M9 = Bw.scratch("seed_M9", N, 9);
+  sd.d_mag = Bw.scratch("seed_mag", N, 1);
+  sd.d_ne = Bw.scratch("seed_ne", E, 1);
+  loss_and_seeds(ctx, g, Bw.act("energy_per_atom"), Bw.act("forces"), Bw.act("stress"), Bw.act("magmom"), lab, *cfg,
+                 sd);
+  backward_core(ctx, m, g, sd, false);
   if (loss_out) {
     double *h = (double *)ctx->pinned_get(64);
     CUDA_OK(cudaMemcpyAsync(h, ctx->d_loss, 5 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_OK(cudaStreamSynchronize(ctx->stream));
     for (int k = 0; k < 5; ++k) loss_out[k] = h[k];
   }
-  // debug views of the main gradients
-  ctx->dbg["dv0"] = {dv, N, 64, 64};
-  ctx->dbg["de0"] = {de, E, 64, 64};
-  ctx->dbg["da0"] = {da, A, 64, 64};
-  ctx->dbg["dea"] = {dea, E, 64, 64};
-  ctx->dbg["deb"] = {deb, B, 64, 64};
+}
+
+// ===========================================================================
+// conservative forces and stress: F = −∂E/∂r, σ = (160.2/V)·∂E/∂ε
+// ===========================================================================
+void derivative_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, chg_pred *out) {
+  const int64_t N = g->N, E = g->E, B = g->B, A = g->A;
+  forward_impl(ctx, m, g, 1, nullptr);
+  struct Scope {
+    chg_ctx *c;
+    explicit Scope(chg_ctx *x) : c(x) { c->red_on = true; c->red_jobs.clear(); c->no_param_grads = true; }
+    ~Scope() { c->red_on = false; c->red_jobs.clear(); c->no_param_grads = false; }
+  } scope(ctx);
+  Bwd Bw{ctx, m, g, nullptr};
+  LossSeeds sd;                                      // ∂E/∂e_atom = 1 (E = Σ_s E_s); the other heads off
+  sd.d_eatom = Bw.scratch("seed_eatom", N, 1);
+  sd.d_M9 = Bw.scratch("seed_M9", N, 9);
+  sd.d_mag = Bw.scratch("seed_mag", N, 1);
+  sd.d_ne = Bw.scratch("seed_ne", E, 1);
+  fill_value(ctx, sd.d_eatom, N, 1.0f);
+  backward_core(ctx, m, g, sd, true);
+  float *forces = Bw.scratch("dforces", N, 3), *stress = Bw.scratch("dstress", g->S, 9);
+  deriv_geometry(ctx, g, m->p("rbf_a.freq"), m->p("rbf_b.freq"), m->cfg.envelope_p, m->p("proj.W0"), m->p("proj.Wa"),
+                 m->p("proj.Wb"), m->p("proj.Wtheta"), Bw.scratch("de", E, 64), Bw.scratch("dea", E, 64),
+                 Bw.scratch("deb", B, 64), Bw.scratch("da", A, 64), forces, stress);
+  ctx->fwd_train = false;                            // the activations were consumed by this pass
+  if (out) {
+    copy_out(ctx, out->energy, Bw.act("energy"), g->S, out->on_device);
+    copy_out(ctx, out->energy_per_atom, Bw.act("energy_per_atom"), g->S, out->on_device);
+    copy_out(ctx, out->forces, forces, 3 * N, out->on_device);
+    copy_out(ctx, out->stress, stress, 9 * (int64_t)g->S, out->on_device);
+    copy_out(ctx, out->magmom, Bw.act("magmom"), N, out->on_device);
+    if (!out->on_device) CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  }
 }
 
 // ===========================================================================

@@ -635,7 +635,7 @@ void edge_update(chg_ctx *ctx, int64_t E, const float *e, const float *bias, con
 }
 
 void colsum(chg_ctx *ctx, int64_t rows, const float *D, float *grad) {
-  if (rows <= 0) return;
+  if (rows <= 0 || ctx->no_param_grads) return;
   const int64_t rpb = std::max<int64_t>(64, (rows + 295) / 296);
   const int nb = ceil_div(rows, rpb);
   float *part = red_partial(ctx, (size_t)nb * 64);

@@ -60,6 +60,12 @@ void edge_update(chg_ctx *ctx, int64_t E, const float *e, const float *bias, con
 // grad[0..63] += column sums of D [rows, 64] (deterministic)
 void colsum(chg_ctx *ctx, int64_t rows, const float *D, float *grad);
 
+// conservative forces / stress (deriv.cu): from dE/d(e⁰, eᵃ, eᵇ, a⁰) of an energy-seeded backward
+void deriv_geometry(chg_ctx *ctx, const chg_graph *g, const float *freq_a, const float *freq_b, int p,
+                    const float *W0, const float *Wa, const float *Wb, const float *Wth, const float *de,
+                    const float *dea, const float *deb, const float *da, float *forces, float *stress);
+void fill_value(chg_ctx *ctx, float *x, int64_t n, float v);
+
 // heads (Eq. 7, Eq. 9)
 void heads_forces(chg_ctx *ctx, const chg_graph *g, const float *n_e, float *forces);
 void heads_struct(chg_ctx *ctx, const chg_graph *g, const float *e_atom, const float *M9, float *energy,

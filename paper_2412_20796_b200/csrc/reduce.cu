@@ -101,7 +101,7 @@ float *red_partial(chg_ctx *ctx, size_t floats) {
 }
 
 void red_push(chg_ctx *ctx, RedJob j) {
-  if (j.n <= 0) return;
+  if (j.n <= 0 || ctx->no_param_grads) return;
   if ((uintptr_t)j.part & 15) CHG_THROW(CHG_ERR_STATE, "red_push: partial buffer must be 16-byte aligned");
   if (ctx->red_on) {
     ctx->red_jobs.push_back(j);
