@@ -20,3 +20,4 @@ from .structures import (  # noqa: F401
     random_rotation,
 )
 from .params import init_flat_params  # noqa: F401
+from .lj import lj_dataset, lj_labels  # noqa: F401
