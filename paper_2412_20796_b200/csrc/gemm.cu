@@ -130,7 +130,8 @@ __global__ void __launch_bounds__(256) k_rowgemm(const __grid_constant__ RowGemm
       if (g.act == 1) v = siluf_(v);
       if (c.mul) v *= dsiluf_(c.mul[(size_t)m * c.ldm + n]);
       if (c.resid) v += c.resid[(size_t)m * c.ldr + n];
-      c.out[(size_t)m * c.ldo + n] = v;
+      if (c.sout) c.sout[(size_t)m * c.ldso + n] = tf32_round(silu_fast(v));
+      c.out[(size_t)m * c.ldo + n] = c.round_out ? tf32_round(v) : v;
     }
   }
 }
@@ -306,7 +307,7 @@ void rowgemm(chg_ctx *ctx, const RowGemm &g) {
   for (int c = 0; c < g.nchunk; ++c) {
     const Chunk &C = g.ch[c];
     cols += C.ncols;
-    outb += C.ncols * (1.0 + (C.pre != nullptr) + (C.mul != nullptr) + (C.resid != nullptr));
+    outb += C.ncols * (1.0 + (C.pre != nullptr) + (C.mul != nullptr) + (C.resid != nullptr) + (C.sout != nullptr));
     wb += (double)g.K * C.ncols;
     lo = std::min(lo, C.a_k0);
     hi = std::max(hi, C.a_k0 + g.K);

@@ -25,6 +25,7 @@ struct AOp {
   ASeg seg[4];
   int nseg = 0;
   int act = 0;                   // 0: identity, 1: silu applied on load
+  int rounded = 0;               // 1: values are already TF32-rounded (tcgen05 path: no conversion pass)
 };
 
 struct Chunk {
@@ -39,6 +40,8 @@ struct Chunk {
   const float *resid = nullptr; int ldr = 0;   // added after activation
   float *pre = nullptr; int ldp = 0;           // pre-activation store
   const float *mul = nullptr; int ldm = 0;     // v *= dsilu(mul) (backward of silu)
+  float *sout = nullptr; int ldso = 0;         // second output tf32(SiLU(v)) (the next GEMM's operand)
+  int round_out = 0;                           // 1: out is stored TF32-rounded (consumed by tcgen05 only)
   // K-major view of the same weight blocks (element (n, k) at Wk[b][n*ldwk[b] + k - wk0[b]]),
   // filled by the orchestration for the tensor-core path (tc_gemm.cu)
   const float *Wk[4] = {nullptr, nullptr, nullptr, nullptr};

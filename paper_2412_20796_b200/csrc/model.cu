@@ -366,12 +366,12 @@ void ac_bwd_body(Bwd &Bw, int t, const float *v, const float *e, const float *ea
   {  // dZ1 = (dY · blockdiag(W2ᵀ)) ⊙ SiLU'(z1)
     RowGemm G;
     G.A.seg[0] = aseg(dY, 128, 128);
-    G.A.nseg = 1;
+    G.A.nseg = 1; G.A.rounded = ctx->use_tc;       // gate_bwd rounds dY in TF32 mode
     G.M = (int)E; G.K = 64; G.nchunk = 2; G.tc = 1;
     G.ch[0] = chunk1(Bw.WT(pre + ".core.W2"), 64, 64, nullptr, dZ, 128);
-    G.ch[0].mul = z1; G.ch[0].ldm = 128;
+    G.ch[0].mul = z1; G.ch[0].ldm = 128; G.ch[0].round_out = ctx->use_tc;
     G.ch[1] = chunk1(Bw.WT(pre + ".gate.W2"), 64, 64, nullptr, dZ + 64, 128);
-    G.ch[1].mul = z1 + 64; G.ch[1].ldm = 128; G.ch[1].a_k0 = 64;
+    G.ch[1].mul = z1 + 64; G.ch[1].ldm = 128; G.ch[1].a_k0 = 64; G.ch[1].round_out = ctx->use_tc;
     G.tag = "ac_dZ";
     rowgemm(ctx, G);
   }
@@ -401,7 +401,7 @@ void ac_bwd_body(Bwd &Bw, int t, const float *v, const float *e, const float *ea
   {  // dX = dZ1 · [W1_coreᵀ ; W1_gateᵀ] -> (v_i part, v_j part, e part)
     RowGemm G;
     G.A.seg[0] = aseg(dZ, 128, 128);
-    G.A.nseg = 1;
+    G.A.nseg = 1; G.A.rounded = ctx->use_tc;
     G.M = (int)E; G.K = 128; G.nchunk = 3; G.tc = 1;
     float *outs[3] = {ti, tj, de};
     for (int c = 0; c < 3; ++c) {
@@ -465,12 +465,12 @@ void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float 
   {
     RowGemm G;
     G.A.seg[0] = aseg(dYb, 128, 128);
-    G.A.nseg = 1;
+    G.A.nseg = 1; G.A.rounded = ctx->use_tc;
     G.M = (int)A; G.K = 64; G.nchunk = 2; G.tc = 1;
     G.ch[0] = chunk1(Bw.WT(bp + ".core.W2"), 64, 64, nullptr, dZ, 256);
-    G.ch[0].mul = z1; G.ch[0].ldm = 128;
+    G.ch[0].mul = z1; G.ch[0].ldm = 128; G.ch[0].round_out = ctx->use_tc;
     G.ch[1] = chunk1(Bw.WT(bp + ".gate.W2"), 64, 64, nullptr, dZ + 64, 256);
-    G.ch[1].mul = z1 + 64; G.ch[1].ldm = 128; G.ch[1].a_k0 = 64;
+    G.ch[1].mul = z1 + 64; G.ch[1].ldm = 128; G.ch[1].a_k0 = 64; G.ch[1].round_out = ctx->use_tc;
     G.tag = "bc_dZ";
     rowgemm(ctx, G);
   }
@@ -501,7 +501,7 @@ void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float 
   {  // dX = [dZ1_bond | dY_angle] · [W1_bcᵀ; W1_bgᵀ; W_acᵀ; W_agᵀ] -> (v_i, e_ij, e_ik, a)
     RowGemm G;
     G.A.seg[0] = aseg(dZ, 256, Kx);
-    G.A.nseg = 1;
+    G.A.nseg = 1; G.A.rounded = ctx->use_tc;
     G.M = (int)A; G.K = Kx; G.nchunk = 4; G.tc = 1;
     float *outs[4] = {tv, t1, t2, da};
     for (int c = 0; c < 4; ++c) {

@@ -53,13 +53,13 @@ __global__ void k_gate_fwd(int64_t rows, const float *__restrict__ y, int ldy, G
   *(float2 *)(out + row * 64 + c0) = o;
 }
 
-__global__ void __launch_bounds__(256) k_gate_bwd(int64_t rows, int64_t rpb, const float *__restrict__ y, int ldy,
+__global__ void __launch_bounds__(256, 4) k_gate_bwd(int64_t rows, int64_t rpb, const float *__restrict__ y, int ldy,
                                                   GateLN ln, int mode, const float *__restrict__ w,
                                                   const int32_t *__restrict__ i1, const int32_t *__restrict__ i2,
                                                   const float *__restrict__ dout, const int32_t *__restrict__ didx,
                                                   float *__restrict__ dy, int lddy, float *__restrict__ dw_acc,
                                                   float *__restrict__ q1, float *__restrict__ q2,
-                                                  float *__restrict__ partial) {
+                                                  float *__restrict__ partial, int rnd) {
   __shared__ float sh[8][256];
   int l = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int c0 = 2 * l;
@@ -110,10 +110,13 @@ __global__ void __launch_bounds__(256) k_gate_bwd(int64_t rows, int64_t rpb, con
     float m2c = warp_sum(gdc[0] * xc[0] + gdc[1] * xc[1]) * (1.0f / 64.0f);
     float m1g = warp_sum(gdg[0] + gdg[1]) * (1.0f / 64.0f);
     float m2g = warp_sum(gdg[0] * xg[0] + gdg[1] * xg[1]) * (1.0f / 64.0f);
-    *(float2 *)(dy + row * lddy + c0) =
-        make_float2(sc.rstd * (gdc[0] - m1c - xc[0] * m2c), sc.rstd * (gdc[1] - m1c - xc[1] * m2c));
-    *(float2 *)(dy + row * lddy + 64 + c0) =
-        make_float2(sg.rstd * (gdg[0] - m1g - xg[0] * m2g), sg.rstd * (gdg[1] - m1g - xg[1] * m2g));
+    float2 oc = make_float2(sc.rstd * (gdc[0] - m1c - xc[0] * m2c), sc.rstd * (gdc[1] - m1c - xc[1] * m2c));
+    float2 og = make_float2(sg.rstd * (gdg[0] - m1g - xg[0] * m2g), sg.rstd * (gdg[1] - m1g - xg[1] * m2g));
+    if (rnd) {                                       // dY feeds only tensor-core GEMMs (TF32 mode)
+      oc.x = tf32_round(oc.x); oc.y = tf32_round(oc.y); og.x = tf32_round(og.x); og.y = tf32_round(og.y);
+    }
+    *(float2 *)(dy + row * lddy + c0) = oc;
+    *(float2 *)(dy + row * lddy + 64 + c0) = og;
   }
   sh[wid][c0] = a_gc[0]; sh[wid][c0 + 1] = a_gc[1];
   sh[wid][64 + c0] = a_bc[0]; sh[wid][64 + c0 + 1] = a_bc[1];
@@ -547,7 +550,7 @@ void gate_bwd(chg_ctx *ctx, int64_t rows, const float *y, int ldy, GateLN ln, in
   ProfScope ps(ctx, "gate_bwd", 0.0,
                rows * (512.0 + 260.0 + 512.0 + (mode == GATE_MUL_W ? 768.0 : mode == GATE_MUL_W1W2 ? 1032.0 : 0.0)));
   k_gate_bwd<<<nb, 256, 0, ctx->stream>>>(rows, rpb, y, ldy, ln, mode, w, i1, i2, dout, didx, dy, lddy, dw_acc, q1,
-                                          q2, part);
+                                          q2, part, ctx->use_tc ? 1 : 0);
   check_launch(ctx);
   RedJob j;                                        // LN affine gradients: batched reduction (reduce.cu)
   j.kind = 2; j.n = 256; j.splits = nb; j.stride = 256; j.part = part;

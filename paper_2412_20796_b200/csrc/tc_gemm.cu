@@ -83,7 +83,6 @@ __device__ __forceinline__ void mma_commit(uint64_t *bar) {
 
 // SiLU with the approximate reciprocal (MUFU.RCP): its error (~2 ulp fp32) is far
 // below the TF32 rounding that follows, and it avoids the IEEE division sequence.
-__device__ __forceinline__ float silu_fast(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
 __device__ __forceinline__ uint32_t to_tf32(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
@@ -110,7 +109,32 @@ struct TcMaps {
   CUtensorMap e[4];                // epilogue operand (mul or resid) of chunk c: 32 x 32 boxes
   int use_e[4];
   int nbuf;                        // operand boxes in flight per epilogue warp (0: plain loads)
+  CUtensorMap o[4];                // output of chunk c (TMA-store epilogue): 32 x 32 boxes, SWIZZLE_128B
+  CUtensorMap o2[4];               // second output (sout) of chunk c
+  int tstore;                      // 1: lane = row epilogue, results leave through TMA stores
+  int radd[4];                     // chunk c accumulates into its output (resid == out): TMA reduce-add store
+  int nst;                         // staging boxes per epilogue warp (tstore)
 };
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(src)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// out[box] += smem box (element-wise fp32 add at L2; one writer per element -> deterministic)
+__device__ __forceinline__ void tma_store_add_2d(const CUtensorMap *map, uint32_t src, int c0, int c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(src)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ float dsilu_fast(float x) {
+  const float s = __fdividef(1.0f, 1.0f + __expf(-x));
+  return s * (1.0f + x * (1.0f - s));
+}
 
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
   asm volatile(
@@ -132,6 +156,7 @@ struct TcPlan {
   int gfirst[4], gn[4];
   int nsa;           // A stages
   int bres;          // 1: the whole weight image is loaded once per CTA (no per-stage B traffic)
+  int noconv;        // 1: A arrives TF32-rounded by TMA: no conversion pass, the MMA waits on the load
 };
 
 // B image: img[kc][q][n][4] = tf32(W_chunk(n - coff, k = lo + kc·KC - a_k0 + 4q + r))
@@ -290,8 +315,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
   uint32_t *tslot = (uint32_t *)(tempty + 2);
   float *epi = (float *)(smem + NSA * a_bytes + P.bst * b_bytes + 8 * (3 * NSA + 2 * NSB + 4) + 16);  // [8][32][33]
   // epilogue operand boxes [8 warps][TM.nbuf][32 x 32] (1024-B aligned TMA targets) + their barriers
-  float *obuf0 = (float *)(((uintptr_t)(epi + NEPI * 32 * 33) + 1023) & ~(uintptr_t)1023);
-  uint64_t *ebar = (uint64_t *)(obuf0 + NEPI * TM.nbuf * 1024);
+  float *obuf0 = (float *)(((uintptr_t)(epi + (TM.tstore ? 0 : NEPI * 32 * 33)) + 1023) & ~(uintptr_t)1023);
+  float *stg0 = obuf0 + NEPI * TM.nbuf * 1024;          // TMA-store staging [8 warps][TM.nst][32 x 32]
+  uint64_t *ebar = (uint64_t *)(stg0 + (TM.tstore ? NEPI * TM.nst * 1024 : 0));
   const uint32_t tcols = P.tmem_cols;                   // per accumulator buffer
 
   if (warp == 0) {
@@ -300,6 +326,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
+  __shared__ uint64_t trace_ts[32], trace_ld[32], trace_cv[32], trace_mw[32], trace_ep[48];
+  int nep = 0;
+  if ((skip & 32) && tid < 48) trace_ep[tid] = 0;
   if (tid == 0) {
     for (int i = 0; i < NSA; ++i) { mbar_init(&fullA[i], 4); mbar_init(&emptyA[i], 1); mbar_init(&loaded[i], 128); }
     for (int i = 0; i < NSB; ++i) { mbar_init(&fullB[i], 1); mbar_init(&emptyB[i], 1); }
@@ -311,7 +340,6 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
-  __shared__ uint64_t trace_ts[32], trace_ld[32], trace_cv[32], trace_mw[32];
   if ((skip & 32) && tid == 0) {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -395,7 +423,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
     // ---------------- A converters: thread = row; SiLU (GEMM2 input) + TF32 RN in place ----------------
     const int r = tid - 128;
     const int sw = r & 7;
-    for (int gi = 0; gi < total; ++gi) {
+    for (int gi = 0; gi < (P.noconv ? 0 : total); ++gi) {
       const int sa = gi % NSA, ua = gi / NSA;
       mbar_wait(&loaded[sa], ua & 1);
       uint4 *row = (uint4 *)(sA + sa * a_bytes + r * 128);
@@ -452,7 +480,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
         bool started[4] = {false, false, false, false};
         for (int kc = 0; kc < nkc; ++kc, ++gi) {
           const int sa = gi % NSA, ua = gi / NSA, sb = P.bres ? kc : gi % NSB, ub = gi / NSB;
-          mbar_wait(&fullA[sa], ua & 1);
+          mbar_wait(P.noconv ? &loaded[sa] : &fullA[sa], ua & 1);
           if (!P.bres) mbar_wait(&fullB[sb], ub & 1);
           else if (gi == 0) mbar_wait(&fullB[0], 0);
           if ((skip & 32) && gi < 30) {                // debug trace: operands ready
@@ -513,23 +541,129 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
     float *obuf = obuf0 + (warp - 10) * (NB > 0 ? NB : 1) * 1024;
     uint64_t *obar = ebar + (warp - 10) * 2;
     uint32_t ophase = 0;                              // bit s: parity of slot s
-    auto issue_op = [&](int i, int row0) {            // block i of this warp's list -> slot i % NB
-      const int c = mc[i];
-      if (NB == 0 || !TM.use_e[c] || lane != 0) return;
-      const int sl = i % NB;
+    // blocks with a TMA operand, in list order: operand k of a tile uses slot k % NB
+    int nop = 0, oi[8], kord[8];
+    for (int i = 0; i < nmy; ++i) {
+      kord[i] = -1;
+      if (NB > 0 && TM.use_e[mc[i]]) { kord[i] = nop; oi[nop++] = i; }
+    }
+    auto issue_op = [&](int k, int row0) {            // operand k of this warp's list -> slot k % NB
+      if (k >= nop || lane != 0) return;
+      const int i = oi[k], c = mc[i], sl = k % NB;
       mbar_expect_tx(&obar[sl], 4096);
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc)
         if (cc == c) tma_load_2d(smem_u32(obuf + sl * 1024), &TM.e[cc], mj[i], row0, &obar[sl]);
     };
+    auto ep_mark = [&]() {
+      if ((skip & 32) && warp == 10 && lane == 0 && nep < 48) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        trace_ep[nep++] = t;
+      }
+    };
+    if (TM.tstore) {
+      // lane = row: the accumulator row as tcgen05.ld leaves it, bias / dSiLU(mul) / resid in
+      // registers (operand box 128B-swizzled, conflict-free row reads), result written to a
+      // swizzled staging box and stored by TMA (one bulk store per 32 x 32 block)
+      float *stg = stg0 + (warp - 10) * TM.nst * 1024;
+      int sc = 0;
+      const int sw = lane & 7;
+      for (int tl = 0; tl < my_tiles; ++tl) {
+        const int a = tl & 1;
+        const int tile = blockIdx.x + tl * gridDim.x;
+        const int row0 = tile * TCM + lq * 32;
+        for (int k = 0; k < NB; ++k) issue_op(k, row0);
+        mbar_wait(&tfull[a], (tl >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        ep_mark();
+        for (int i = 0; i < nmy; ++i) {
+          const int c = mc[i], j0 = mj[i];
+          const Chunk &C = g.ch[c];
+          uint32_t r[32];
+          tmem_ld32(tmem + lane_base + a * tcols + P.coff[c] + j0, r);
+          float *v = reinterpret_cast<float *>(r);
+          if (C.bias) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) v[q] += __ldg(C.bias + j0 + q);
+          }
+          const int m = row0 + lane;
+          if (kord[i] >= 0) {
+            const int sl = kord[i] % NB;
+            mbar_wait(&obar[sl], (ophase >> sl) & 1);
+            ophase ^= 1u << sl;
+            const float4 *ob = reinterpret_cast<const float4 *>(obuf + sl * 1024) + lane * 8;
+#pragma unroll
+            for (int q4 = 0; q4 < 8; ++q4) {
+              const float4 u = ob[q4 ^ sw];
+              if (C.mul) {
+                v[4 * q4] *= dsilu_fast(u.x); v[4 * q4 + 1] *= dsilu_fast(u.y);
+                v[4 * q4 + 2] *= dsilu_fast(u.z); v[4 * q4 + 3] *= dsilu_fast(u.w);
+              } else {
+                v[4 * q4] += u.x; v[4 * q4 + 1] += u.y; v[4 * q4 + 2] += u.z; v[4 * q4 + 3] += u.w;
+              }
+            }
+            __syncwarp();
+            issue_op(kord[i] + NB, row0);                // slot consumed: next box of this tile
+          } else if ((C.mul || C.resid) && !TM.radd[c] && m < g.M) {   // operand without a TMA map: own row
+            const float *op = C.mul ? C.mul + (size_t)m * C.ldm + j0 : C.resid + (size_t)m * C.ldr + j0;
+#pragma unroll
+            for (int q = 0; q < 32; ++q) v[q] = C.mul ? v[q] * dsilu_fast(__ldg(op + q)) : v[q] + __ldg(op + q);
+          }
+          if (skip & 1) continue;                       // debug: no epilogue stores
+          // pass 0: out (TF32-rounded if round_out); pass 1: sout = tf32(SiLU(v))
+          for (int pass = 0; pass < (C.sout ? 2 : 1); ++pass) {
+            float *st = stg + (sc % TM.nst) * 1024;
+            if (lane == 0) {                            // staging box free (its previous store has read it)
+              if (TM.nst > 1) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+              else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            }
+            __syncwarp();
+            float4 *srow = reinterpret_cast<float4 *>(st) + lane * 8;
+            if (pass == 0 && C.round_out) {
+#pragma unroll
+              for (int q4 = 0; q4 < 8; ++q4)
+                srow[q4 ^ sw] = make_float4(tf32_round(v[4 * q4]), tf32_round(v[4 * q4 + 1]), tf32_round(v[4 * q4 + 2]),
+                                            tf32_round(v[4 * q4 + 3]));
+            } else if (pass == 0) {
+#pragma unroll
+              for (int q4 = 0; q4 < 8; ++q4) srow[q4 ^ sw] = make_float4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
+            } else {
+#pragma unroll
+              for (int q4 = 0; q4 < 8; ++q4)
+                srow[q4 ^ sw] = make_float4(tf32_round(silu_fast(v[4 * q4])), tf32_round(silu_fast(v[4 * q4 + 1])),
+                                            tf32_round(silu_fast(v[4 * q4 + 2])), tf32_round(silu_fast(v[4 * q4 + 3])));
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0 && row0 < g.M) {
+#pragma unroll
+              for (int cc = 0; cc < 4; ++cc)
+                if (cc == c) {
+                  if (TM.radd[cc]) tma_store_add_2d(&TM.o[cc], smem_u32(st), j0, row0);
+                  else tma_store_2d(pass ? &TM.o2[cc] : &TM.o[cc], smem_u32(st), j0, row0);
+                }
+            }
+            ++sc;
+          }
+          ep_mark();
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[a]);
+      }
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      __syncwarp();
+    } else
     for (int tl = 0; tl < my_tiles; ++tl) {
       const int a = tl & 1;
       const int tile = blockIdx.x + tl * gridDim.x;
       const int row0 = tile * TCM + lq * 32;
       const int nrows = min(32, g.M - row0);
-      for (int i = 0; i < nmy && i < NB; ++i) issue_op(i, row0);   // overlaps the accumulator wait
+      for (int k = 0; k < NB; ++k) issue_op(k, row0);   // overlaps the accumulator wait
       mbar_wait(&tfull[a], (tl >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      ep_mark();
       // 32x32 blocks go TMEM -> registers (lane = row) -> smem -> registers
       // (lane = column) so that every global access is a coalesced 128-B row run
       for (int i = 0; i < nmy; ++i) {
@@ -542,16 +676,17 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
         for (int qq = 0; qq < 32; ++qq) stile[lane * 33 + qq] = __uint_as_float(r[qq]);
         __syncwarp();
         const int n = j0 + lane;
-        const bool opd = NB > 0 && TM.use_e[c];
+        const bool opd = kord[i] >= 0;
         if (opd) {                                    // operand box of this block has landed
-          const int sl = i % NB;
+          const int sl = kord[i] % NB;
           mbar_wait(&obar[sl], (ophase >> sl) & 1);
           ophase ^= 1u << sl;
         }
+        ep_mark();
         if (n < C.ncols) {
           const float bn = C.bias ? __ldg(C.bias + n) : 0.f;
           if (opd) {
-            const float *ob = obuf + (i % NB) * 1024;
+            const float *ob = obuf + (kord[i] % NB) * 1024;
             if (C.mul) epi_rows_op<true>(C, stile, ob, lane, row0, nrows, n, bn);
             else epi_rows_op<false>(C, stile, ob, lane, row0, nrows, n, bn);
           } else {
@@ -566,7 +701,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
           }
         }
         __syncwarp();
-        if (opd && i + NB < nmy) issue_op(i + NB, row0);   // slot free again: next box of this tile
+        ep_mark();
+        if (opd) issue_op(kord[i] + NB, row0);          // slot free again: next box of this tile
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -586,7 +722,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
     for (int i = 0; i < min(30, total); ++i) printf(" %.2f", (trace_cv[i] - trace_ts[0]) * 1e-3);
     printf(" | mma ready:");
     for (int i = 0; i < min(30, total); ++i) printf(" %.2f", (trace_mw[i] - trace_ts[0]) * 1e-3);
-    printf(" | mma_done %.2f end %.2f\n", (trace_ts[31] - trace_ts[0]) * 1e-3, (t - trace_ts[0]) * 1e-3);
+    printf(" | mma_done %.2f end %.2f", (trace_ts[31] - trace_ts[0]) * 1e-3, (t - trace_ts[0]) * 1e-3);
+    printf(" | epi(w10):");
+    for (int i = 0; i < 48 && trace_ep[i] > trace_ts[0]; ++i) printf(" %.2f", (trace_ep[i] - trace_ts[0]) * 1e-3);
+    printf("\n");
   }
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * tcols) : "memory");
@@ -903,15 +1042,15 @@ static int encode_a_map(CUtensorMap *m, const float *base, int width, int rows, 
 }
 
 // 2-D fp32 map of an epilogue operand [rows][ncols] (row stride ld): 32 x 32 boxes, no swizzle
-static int encode_op_map(CUtensorMap *m, const float *base, int ncols, int rows, int ld) {
+static int encode_op_map(CUtensorMap *m, const float *base, int ncols, int rows, int ld, bool swz = false) {
   EncodeTiledFn fn = encode_fn();
   if (!fn || rows <= 0 || ncols % 32 || ((uintptr_t)base & 15) || (ld * 4) % 16) return 0;
   cuuint64_t dim[2] = {(cuuint64_t)ncols, (cuuint64_t)rows};
   cuuint64_t stride[1] = {(cuuint64_t)ld * 4};
   cuuint32_t box[2] = {32, 32}, es[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)base, dim, stride, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 1 : 0;
 }
 
@@ -960,28 +1099,55 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   P.tmem_cols = P.ntot <= 32 ? 32 : P.ntot <= 64 ? 64 : P.ntot <= 128 ? 128 : 256;
   const int nkc = P.width / KC;
   const size_t bchunk = (size_t)KC * P.ntot * 4, achunk = (size_t)KC * TCM * 4;
+  // TMA-store epilogue (lane = row) when every chunk's output is a plain [M][32k] table
+  static const bool no_tstore = getenv("CHG_TC_NO_TSTORE") != nullptr;   // A/B knob
+  TcMaps TM;
+  memset(&TM, 0, sizeof(TM));
+  TM.tstore = !no_tstore && g.act == 0 && encode_fn() != nullptr;
+  for (int c = 0; c < g.nchunk && TM.tstore; ++c) {
+    const Chunk &C = g.ch[c];
+    if (C.pre || C.ncols % 32 || !C.out) TM.tstore = 0;
+    else if (!encode_op_map(&TM.o[c], C.out, C.ncols, g.M, C.ldo, true)) TM.tstore = 0;
+    else if (C.sout && !encode_op_map(&TM.o2[c], C.sout, C.ncols, g.M, C.ldso, true)) TM.tstore = 0;
+  }
+  for (int c = 0; c < g.nchunk && TM.tstore; ++c)
+    TM.radd[c] = g.ch[c].resid == g.ch[c].out && g.ch[c].ldr == g.ch[c].ldo && !g.ch[c].mul;
+  bool has_sout = false, has_round = false;
+  for (int c = 0; c < g.nchunk; ++c) { has_sout |= g.ch[c].sout != nullptr; has_round |= g.ch[c].round_out != 0; }
+  if ((has_sout || has_round) && !TM.tstore) return false;          // only the TMA-store epilogue writes sout / rounded out
+  const size_t epi_b = TM.tstore ? 0 : (size_t)NEPI * 32 * 33 * 4;
   auto fixed_of = [&](int nsa) {
-    return 1024 + nsa * achunk + 8 * (3 * nsa + 2 * NSB + 4) + 16 + (size_t)NEPI * 32 * 33 * 4;
+    return 1024 + nsa * achunk + 8 * (3 * nsa + 2 * NSB + 4) + 16 + epi_b;
   };
   // keep the whole weight image resident when it fits (no per-stage B round trips), then as
   // many A stages as the remaining shared memory holds (the A ring is latency-bound)
   static const bool no_bres = getenv("CHG_TC_NO_BRES") != nullptr;   // A/B knobs (timing studies)
   static const int nsa_cap = getenv("CHG_TC_NSA") ? atoi(getenv("CHG_TC_NSA")) : NSA_MAX;
-  P.bres = !no_bres && fixed_of(5) + nkc * bchunk <= 224 * 1024;
-  P.bst = P.bres ? nkc : NSB;
   // epilogue operands (mul / resid of a chunk) by TMA when the GEMM has them: 2 boxes in flight
-  // per epilogue warp if shared memory allows (else 1), at the cost of A stages beyond 4
+  // per epilogue warp if shared memory allows (else 1); with the TMA-store epilogue one
+  // operand box and one staging box per warp take precedence over a resident weight image
   static const bool no_etma = getenv("CHG_TC_NO_ETMA") != nullptr;   // A/B knob
   int has_op = 0;
-  for (int c = 0; c < g.nchunk; ++c) has_op |= ((g.ch[c].mul != nullptr) != (g.ch[c].resid != nullptr)) && !g.ch[c].pre;
+  for (int c = 0; c < g.nchunk; ++c)
+    has_op |= ((g.ch[c].mul != nullptr) != (g.ch[c].resid != nullptr)) && !g.ch[c].pre && !TM.radd[c];
   int nbuf = (has_op && !no_etma) ? 2 : 0;
-  auto opbytes = [&](int nb) { return (size_t)1024 + (size_t)NEPI * nb * 4096 + 2 * NEPI * 8; };
+  static const int nst_cap = getenv("CHG_TC_NST") ? atoi(getenv("CHG_TC_NST")) : 1;
+  TM.nst = TM.tstore ? ((has_sout || nst_cap >= 2) ? 2 : 1) : 0;
+  auto opbytes = [&](int nb) { return (size_t)1024 + (size_t)NEPI * (nb + TM.nst) * 4096 + 2 * NEPI * 8; };
+  const int nb_min = TM.tstore ? std::min(nbuf, 1) : 0;
+  P.bres = !no_bres && fixed_of(5) + nkc * bchunk + (TM.tstore ? opbytes(nb_min) : 0) <= 224 * 1024;
+  P.bst = P.bres ? nkc : NSB;
   if (nbuf == 2 && fixed_of(4) + P.bst * bchunk + opbytes(2) > 224 * 1024) nbuf = 1;
   if (nbuf == 1 && fixed_of(4) + P.bst * bchunk + opbytes(1) > 224 * 1024) nbuf = 0;
+  if (TM.nst == 2 && fixed_of(4) + P.bst * bchunk + opbytes(nbuf) > 224 * 1024) TM.nst = 1;
   P.nsa = 4;
   while (P.nsa < std::min(nsa_cap, NSA_MAX) && fixed_of(P.nsa + 1) + P.bst * bchunk + opbytes(nbuf) <= 224 * 1024)
     ++P.nsa;
   size_t smem = fixed_of(P.nsa) + P.bst * bchunk + opbytes(nbuf);
+  if (smem > 224 * 1024) {
+    fprintf(stderr, "rowgemm_tc %s: shared memory plan %zu B exceeds 224 KB\n", g.tag ? g.tag : "?", smem);
+    return false;
+  }
   static bool attr = false;
   if (!attr) {
     CUDA_OK(cudaFuncSetAttribute(k_rowgemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
@@ -1047,30 +1213,32 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   double outb = 0;
   for (int c = 0; c < g.nchunk; ++c) {
     const Chunk &C = g.ch[c];
-    outb += C.ncols * (1.0 + (C.pre != nullptr) + (C.mul != nullptr) + (C.resid != nullptr));
+    outb += C.ncols * (1.0 + (C.pre != nullptr) + (C.mul != nullptr) + (C.resid != nullptr) + (C.sout != nullptr));
   }
   ProfScope ps(ctx, g.tag ? g.tag : "rowgemm_tc", 2.0 * g.M * (double)g.K * cols,
                gemm_a_bytes(g.A, g.M, P.lo, P.lo + P.width) + (double)g.M * 4.0 * outb + 4.0 * g.K * cols);
   static int skip = getenv("CHG_TC_SKIP") ? atoi(getenv("CHG_TC_SKIP")) : 0;   // debug knob (timing studies)
-  TcMaps TM;
-  memset(&TM, 0, sizeof(TM));
   static const bool no_tma = getenv("CHG_TC_NO_TMA") != nullptr;            // A/B knob (timing studies)
   for (int s = 0; s < g.A.nseg && !no_tma; ++s) {
     const ASeg &S = g.A.seg[s];
     if (S.idx) continue;                              // gathered rows stay on cp.async
     TM.use[s] = encode_a_map(&TM.m[s], S.base, S.width, g.M, S.ld);
   }
+  static const bool no_noconv = getenv("CHG_TC_NO_NOCONV") != nullptr;    // A/B knob
+  P.noconv = g.A.rounded && g.A.act == 0 && !no_noconv;
+  for (int s = 0; s < g.A.nseg; ++s) P.noconv &= TM.use[s];
   TM.nbuf = nbuf;
   for (int c = 0; c < g.nchunk && nbuf > 0; ++c) {
     const Chunk &C = g.ch[c];
-    if ((C.mul != nullptr) == (C.resid != nullptr) || C.pre) continue;
+    if ((C.mul != nullptr) == (C.resid != nullptr) || C.pre || TM.radd[c]) continue;
     const float *op = C.mul ? C.mul : C.resid;
-    TM.use_e[c] = encode_op_map(&TM.e[c], op, C.ncols, g.M, C.mul ? C.ldm : C.ldr);
+    TM.use_e[c] = encode_op_map(&TM.e[c], op, C.ncols, g.M, C.mul ? C.ldm : C.ldr, TM.tstore != 0);
   }
   static const bool verbose = getenv("CHG_TC_VERBOSE") != nullptr;
   if (verbose)
-    fprintf(stderr, "rowgemm_tc %s: M %d K %d nseg %d tma %d%d%d%d nsa %d bres %d smem %zu\n", g.tag ? g.tag : "?", g.M,
-            g.K, g.A.nseg, TM.use[0], TM.use[1], TM.use[2], TM.use[3], P.nsa, P.bres, smem);
+    fprintf(stderr, "rowgemm_tc %s: M %d K %d nseg %d tma %d%d%d%d nsa %d bres %d tstore %d nst %d nbuf %d noconv %d smem %zu\n",
+            g.tag ? g.tag : "?", g.M, g.K, g.A.nseg, TM.use[0], TM.use[1], TM.use[2], TM.use[3], P.nsa, P.bres,
+            TM.tstore, TM.nst, nbuf, P.noconv, smem);
   k_rowgemm_tc<<<grid, WS_THREADS, smem, ctx->stream>>>(g, P, img, ntiles, skip, TM);
   check_launch(ctx);
   return true;
