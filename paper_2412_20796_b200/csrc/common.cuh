@@ -56,6 +56,7 @@ struct RedJob {
   float *b[4] = {nullptr, nullptr, nullptr, nullptr};
   int k0[4] = {0, 0, 0, 0}, kn[4] = {-1, -1, -1, -1};
   int block0 = 0;               // first block of this job in the batched launch
+  int qpb = 32;                 // float4 quads per block (set by red_flush from n and splits)
 };
 
 // ---------------------------------------------------------------------------

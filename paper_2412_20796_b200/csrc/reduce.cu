@@ -5,10 +5,9 @@
 // the fused readout heads, the basis projections and the output-linear biases — used to
 // need its own small reduction launch (~10 µs of latency each, ~50 per step).  Inside a
 // backward layer they are recorded instead (red_push) and red_flush runs them all in ONE
-// launch at the layer's end: block b serves 32 outputs of job j (found by binary search over
-// the jobs' first blocks), warp w sums partial rows w, w+8, ..., warp 0 adds the 8
-// subtotals in order — the same fixed order as a per-job reduction, so results are
-// bit-identical and deterministic.
+// launch at the layer's end: block b serves a run of outputs of job j (found by binary search
+// over the jobs' first blocks); the partial rows are summed in a fixed order that depends only
+// on the job's shape, so results are deterministic.
 #include "common.cuh"
 
 namespace {
@@ -39,12 +38,15 @@ __device__ __forceinline__ float *red_dst(const RedJob &J, int idx) {
   }
 }
 
-// block = 128 consecutive outputs of one job (lane = float4 quad), warp w sums partial rows
-// w, w+8, ... and warp 0 adds the 8 subtotals in order
+// block = qpb consecutive float4 quads of one job; its 256 threads are (quad q, group r),
+// G = 256 / qpb groups: group r sums partial rows r, r + G, ... (fixed), then the G group
+// sums of a quad are added in group order.  qpb depends only on the job's (n, splits), so
+// the summation order — and the result — is the same on every run.  Tall jobs (few outputs,
+// hundreds of splits: LayerNorm / bias / head partials) get many groups instead of one
+// long serial chain per lane.
 __global__ void __launch_bounds__(256) k_reduce_all(const __grid_constant__ RedBatch B) {
-  __shared__ float4 sh[8][32];
+  __shared__ float4 sh[256];
   __shared__ int sj;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     int lo = 0, hi = B.n - 1;
     while (lo < hi) {                       // last job with block0 <= blockIdx.x
@@ -55,21 +57,23 @@ __global__ void __launch_bounds__(256) k_reduce_all(const __grid_constant__ RedB
   }
   __syncthreads();
   const RedJob &J = B.j[sj];
-  const int q = ((int)blockIdx.x - J.block0) * 32 + lane;   // quad index
+  const int qpb = J.qpb, G = 256 / qpb;
+  const int ql = threadIdx.x % qpb, grp = threadIdx.x / qpb;
+  const int q = ((int)blockIdx.x - J.block0) * qpb + ql;   // quad index
   const int idx = 4 * q;
   float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
   if (idx < J.n) {
     if (J.stride % 4 == 0) {                // 16-B rows: one float4 per partial row
       const float4 *p = (const float4 *)J.part + q;
       const int64_t st4 = J.stride / 4;
-#pragma unroll 8
-      for (int sp = w; sp < J.splits; sp += 8) {
+#pragma unroll 4
+      for (int sp = grp; sp < J.splits; sp += G) {
         const float4 u = __ldcg(p + (size_t)sp * st4);
         s.x += u.x; s.y += u.y; s.z += u.z; s.w += u.w;
       }
     } else {                                // odd row length (N = 1 or 9 heads): scalar loads
       const int m = min(4, J.n - idx);
-      for (int sp = w; sp < J.splits; sp += 8) {
+      for (int sp = grp; sp < J.splits; sp += G) {
         const float *p = J.part + (size_t)sp * J.stride + idx;
         s.x += __ldcg(p);
         if (m > 1) s.y += __ldcg(p + 1);
@@ -78,12 +82,14 @@ __global__ void __launch_bounds__(256) k_reduce_all(const __grid_constant__ RedB
       }
     }
   }
-  sh[w][lane] = s;
+  sh[threadIdx.x] = s;
   __syncthreads();
-  if (w != 0 || idx >= J.n) return;
-  float4 t = sh[0][lane];
-#pragma unroll
-  for (int k = 1; k < 8; ++k) { t.x += sh[k][lane].x; t.y += sh[k][lane].y; t.z += sh[k][lane].z; t.w += sh[k][lane].w; }
+  if (grp != 0 || idx >= J.n) return;
+  float4 t = sh[ql];
+  for (int k = 1; k < G; ++k) {
+    const float4 u = sh[k * qpb + ql];
+    t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
+  }
   const float v[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
@@ -123,7 +129,11 @@ void red_flush(chg_ctx *ctx) {
     for (int k = 0; k < B.n; ++k) {
       B.j[k] = ctx->red_jobs[j0 + k];
       B.j[k].block0 = blocks;
-      blocks += ceil_div(B.j[k].n, 128);
+      // ~4-8 partial rows per thread: G = 256 / qpb split groups (8..64, a power of two)
+      int G = 8;
+      while (G < 64 && G * 8 < B.j[k].splits) G *= 2;
+      B.j[k].qpb = 256 / G;
+      blocks += ceil_div(ceil_div(B.j[k].n, 4), B.j[k].qpb);
       bytes += 4.0 * B.j[k].n * (B.j[k].splits + 2.0);
     }
     ProfScope ps(ctx, "reduce_all", 0.0, bytes);
