@@ -78,6 +78,10 @@ def _args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batches", type=int, default=4, help="distinct pre-generated batches cycled through")
+    ap.add_argument("--prefetch", default="off", choices=["e2e", "all", "off"],
+                    help="graph prefetch on a builder context (SURVEY NEXT-3) in the e2e pass, in every pass, "
+                         "or never (default: measured at C2, the builder's small kernels share SMs with the "
+                         "persistent GEMMs and the overlap gains nothing; DESIGN.md §12)")
     ap.add_argument("--per-gpu", type=int, default=0, help="structures per GPU (default: 40 at N=1, 128 at N>1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -304,18 +308,38 @@ def main():
     total_steps = 2 * (a.warmup + a.steps) + 8
     step_no = [0]
 
-    def one_step(b, on_host: bool, model=None):
+    # graph prefetch: a builder context builds the next step's graph on its own
+    # stream while this step's forward / backward run; the step's end waits for that build, so
+    # every build stays inside a timed step window (the first step builds its own inline)
+    # (high-priority stream: its short kernels are scheduled first whenever SMs free up)
+    bstream = None if a.prefetch == "off" else torch.cuda.Stream(device=local, priority=-5)
+    builder = None if a.prefetch == "off" else chg.Context(local, stream=bstream.cuda_stream)
+
+    def build(b, on_host: bool, bctx=None):
+        src = b["host"] if on_host else b["dev"]
+        return (bctx or ctx).build_graph(b["ap"], src["pos"], src["lat"], src["spec"], 5.0, 3.0)
+
+    def one_step(b, on_host: bool, model=None, g=None, nxt=None):
         model = model or models[a.precision]
         step_no[0] += 1
         lr = lr0 * 0.5 * (1 + math.cos(math.pi * step_no[0] / total_steps))   # cosine
         src = b["host"] if on_host else b["dev"]
-        g = ctx.build_graph(b["ap"], src["pos"], src["lat"], src["spec"], 5.0, 3.0)
+        if g is None:
+            g = build(b, on_host)
         ctx.forward(model, g, train=True, host=False)
+        # the build's host part (count readback on the builder stream) is issued once this
+        # step's work is queued: after the forward when the loss readback blocks the host
+        # (e2e), after the Adam step otherwise — the training stream never runs dry
+        gn = build(nxt, on_host, builder) if (nxt is not None and on_host) else None
         loss = ctx.backward(model, g, src["lab"], n_struct_global=b["gl"]["S"], n_atoms_global=b["gl"]["N"],
                             n_magmom_global=b["gl"]["M"], sync_loss=on_host)
         ctx.step(model, lr=lr, step=step_no[0], allreduce=ws > 1)
+        if nxt is not None and not on_host:
+            gn = build(nxt, on_host, builder)
+        if gn is not None:
+            ctx.wait_graph(gn)
         g.close()
-        return loss
+        return loss, gn
 
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")     # 256 MiB > 126 MB L2
 
@@ -331,16 +355,20 @@ def main():
         if profile:
             ctx.profile(True)
         l0 = ctx.launch_count()
+        lb0 = builder.launch_count() if builder else 0
         barrier()
+        gnext = None
         for k in range(a.steps):
             b = bl[k % len(bl)]
+            use = builder is not None and not profile and (on_host or a.prefetch == "all")
+            nxt = bl[(k + 1) % len(bl)] if (use and k + 1 < a.steps) else None
             ev[k][0].record(stream)
-            one_step(b, on_host, model)
+            _, gnext = one_step(b, on_host, model, g=gnext, nxt=nxt)
             ev[k][1].record(stream)
             with torch.cuda.stream(stream):
                 flush.zero_()                              # L2 flush outside the timed events
         barrier()
-        launches = ctx.launch_count() - l0
+        launches = ctx.launch_count() - l0 + ((builder.launch_count() - lb0) if builder else 0)
         ms = sum(s.elapsed_time(e) for s, e in ev)
         rep = ctx.profile_report() if profile else None
         if profile:
@@ -441,7 +469,8 @@ def main():
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            tr = json.load(f).get(a.precision, {}).get(dom)
+            tj = json.load(f)
+            tr = tj.get(f"{a.precision}_{wl}", tj.get(a.precision, {})).get(dom)
             traffic = tr["dram_bytes_per_launch"] if tr else None
     except Exception:
         pass
@@ -497,6 +526,10 @@ def main():
                                    f"(5/3 Å cutoffs, d=64, 4 atom-conv / 3 bond-conv)",
                        "structures_per_gpu": per, "global_batch": per * ws, "parallelism": f"dp{ws}",
                        "step": "build_graph + forward + backward + allreduce + Adam",
+                       "graph_build": {"value": "prefetched on a builder context during the previous step" if a.prefetch == "all"
+                                       else "inline",
+                                       "e2e": "inline" if a.prefetch == "off" else
+                                       "prefetched on a builder context during the previous step"},
                        "l2": "flushed between steps (256 MiB write, outside the timed events)",
                        "batches_cycled": len(batches), "cv_balanced_vs_contiguous": b0["cv"],
                        "rank0_counts_first_batch": None},

@@ -12,7 +12,12 @@
  *     Device pointers (flag `*_on_device` = 1) must stay valid until the work
  *     enqueued on the ctx stream has finished.
  *   - Handles are owned by the caller and released with the *_destroy calls.
- *     A graph / model is bound to the ctx (device) that created it.
+ *     A model is bound to the ctx (device) that created it.  A graph may be
+ *     used by another ctx of the same device (graph prefetch: a builder ctx
+ *     builds batch i+1 on its own stream while the training ctx runs batch i):
+ *     the using ctx's stream waits for the build, and chg_graph_destroy
+ *     releases the arrays only after the user's enqueued work (one user ctx
+ *     per graph besides its builder; CHG_ERR_ARG otherwise).
  *   - A ctx is not thread-safe; use one per (thread, device).
  *   - Determinism: same inputs -> bit-identical outputs, gradients and
  *     parameters on a given GPU count (no atomics on the feature path, fixed
@@ -142,6 +147,10 @@ chg_status chg_graph_export(const chg_graph *g, int32_t *row_ptr, int32_t *nbr, 
                             int32_t *angle_ptr, int32_t *angle_b1, int32_t *angle_b2,
                             int32_t *rev, int32_t *swap);
 void chg_graph_destroy(chg_graph *g);
+/* Make ctx's stream wait for the build of g (built by ctx or by another ctx of the same
+ * device — graph prefetch, see the conventions above); chg_forward does this implicitly.
+ * Registers ctx as the graph's user.  CHG_ERR_ARG for another device or a third ctx. */
+chg_status chg_graph_wait(chg_ctx *ctx, chg_graph *g);
 
 /* ---- model ------------------------------------------------------------- */
 chg_status chg_model_create(chg_ctx *ctx, const chg_model_cfg *cfg, chg_model **out);

@@ -61,7 +61,7 @@ class AdamCfg(C.Structure):
 # every symbol include/chg.h declares (checked by tests/test_abi_symbols.py)
 SYMBOLS = ["chg_ctx_create", "chg_ctx_destroy", "chg_last_error", "chg_sync", "chg_launch_count",
            "chg_nccl_unique_id", "chg_ctx_set_nccl", "chg_build_graph", "chg_graph_counts", "chg_graph_export",
-           "chg_graph_destroy", "chg_model_create", "chg_model_destroy", "chg_model_layout",
+           "chg_graph_destroy", "chg_graph_wait", "chg_model_create", "chg_model_destroy", "chg_model_layout",
            "chg_model_num_params", "chg_model_set", "chg_model_get", "chg_model_device_ptr", "chg_forward",
            "chg_forward_conservative",
            "chg_backward", "chg_step", "chg_balance", "chg_profile", "chg_profile_query", "chg_debug_gemm", "chg_debug_get"]
@@ -90,6 +90,7 @@ def load(path: str = LIB_PATH):
         "chg_graph_counts": (C.c_int, [vp, vp, vp]),
         "chg_graph_export": (C.c_int, [vp] + [vp] * 11),
         "chg_graph_destroy": (None, [vp]),
+        "chg_graph_wait": (C.c_int, [vp, vp]),
         "chg_model_create": (C.c_int, [vp, C.POINTER(ModelCfg), C.POINTER(vp)]),
         "chg_model_destroy": (None, [vp]),
         "chg_model_layout": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.POINTER(C.c_char_p)),
@@ -179,6 +180,11 @@ class Context:
         self._check(self.lib.chg_ctx_set_nccl(self.h, buf, nranks, rank))
 
     # ---- graph
+    def wait_graph(self, graph: "Graph"):
+        """This context's stream waits for `graph`'s build (graph prefetch: built by another
+        Context of the same device on its own stream; chg_forward also waits implicitly)."""
+        self._check(self.lib.chg_graph_wait(self.h, graph.h))
+
     def build_graph(self, atom_ptr, positions, lattice, species, r_atom: float = 5.0, r_bond: float = 3.0) -> "Graph":
         ap = np.ascontiguousarray(np.asarray(atom_ptr, np.int64))
         dev = _on_device(positions)

@@ -366,20 +366,40 @@ chg_status chg_model_get(const chg_model *m, int which, float *host, int64_t n) 
 
 void *chg_model_device_ptr(chg_model *m, int which) { return m ? which_ptr(m, which) : nullptr; }
 
-chg_status chg_forward(chg_ctx *ctx, chg_model *m, chg_graph *g, int train, chg_pred *out) {
-  if (!ctx || !m || !g) return CHG_ERR_ARG;
-  if (m->ctx != ctx || g->ctx != ctx) { ctx->err = "model/graph bound to another ctx"; return CHG_ERR_ARG; }
+// a graph built by another context (e.g. a prefetching builder) of the same device: this
+// context's stream waits for the build; the graph frees its arrays after this stream's work
+static void graph_use(chg_ctx *ctx, chg_graph *g) {
+  if (g->ctx == ctx) return;
+  if (g->ctx->device != ctx->device) CHG_THROW(CHG_ERR_ARG, "graph built on device %d, used on %d", g->ctx->device, ctx->device);
+  if (g->user && g->user != ctx) CHG_THROW(CHG_ERR_ARG, "graph already used by a third context");
+  CUDA_OK(cudaStreamWaitEvent(ctx->stream, g->ready, 0));
+  g->user = ctx;
+}
+
+chg_status chg_graph_wait(chg_ctx *ctx, chg_graph *g) {
+  if (!ctx || !g) return CHG_ERR_ARG;
   ABI_GUARD(ctx, {
     CUDA_OK(cudaSetDevice(ctx->device));
+    graph_use(ctx, g);
+  });
+}
+
+chg_status chg_forward(chg_ctx *ctx, chg_model *m, chg_graph *g, int train, chg_pred *out) {
+  if (!ctx || !m || !g) return CHG_ERR_ARG;
+  if (m->ctx != ctx) { ctx->err = "model bound to another ctx"; return CHG_ERR_ARG; }
+  ABI_GUARD(ctx, {
+    CUDA_OK(cudaSetDevice(ctx->device));
+    graph_use(ctx, g);
     forward_impl(ctx, m, g, train, out);
   });
 }
 
 chg_status chg_forward_conservative(chg_ctx *ctx, chg_model *m, chg_graph *g, chg_pred *out) {
   if (!ctx || !m || !g) return CHG_ERR_ARG;
-  if (m->ctx != ctx || g->ctx != ctx) { ctx->err = "model/graph bound to another ctx"; return CHG_ERR_ARG; }
+  if (m->ctx != ctx) { ctx->err = "model bound to another ctx"; return CHG_ERR_ARG; }
   ABI_GUARD(ctx, {
     CUDA_OK(cudaSetDevice(ctx->device));
+    graph_use(ctx, g);
     derivative_impl(ctx, m, g, out);
   });
 }

@@ -161,6 +161,10 @@ struct chg_graph {
   // per structure
   float *lattice_f = nullptr;          // [S*9]
   float *inv_natoms = nullptr;         // [S]
+  // built on ctx's stream; another context of the same device may use it (graph prefetch):
+  // its stream waits on `ready`, and the arrays are freed only after that user's work
+  cudaEvent_t ready = nullptr;
+  chg_ctx *user = nullptr;
 };
 
 // ---------------------------------------------------------------------------

@@ -852,6 +852,8 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
     delete G;
     throw;
   }
+  CUDA_OK(cudaEventCreateWithFlags(&G->ready, cudaEventDisableTiming));
+  CUDA_OK(cudaEventRecord(G->ready, st));
   return G;
 }
 
@@ -884,6 +886,15 @@ void graph_fill_counts(chg_graph *G) {
 
 void destroy_graph_impl(chg_graph *G) {
   if (!G) return;
+  if (G->user && G->user != G->ctx) {          // used on another context's stream: free after its work
+    cudaEvent_t done;
+    if (cudaEventCreateWithFlags(&done, cudaEventDisableTiming) == cudaSuccess) {
+      cudaEventRecord(done, G->user->stream);
+      cudaStreamWaitEvent(G->ctx->stream, done, 0);
+      cudaEventDestroy(done);
+    }
+  }
+  if (G->ready) cudaEventDestroy(G->ready);
   if (G->block) {
     GraphBlocks *bl = (GraphBlocks *)G->block;
     if (bl->a) cudaFreeAsync(bl->a, G->ctx->stream);

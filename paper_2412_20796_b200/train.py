@@ -9,7 +9,9 @@ chg_build_graph → chg_forward(train) → chg_backward (global loss normalisers
 * epochs over a list of structures, reshuffled per epoch with a seeded generator; with
   world_size > 1 each global batch is dealt to ranks with chg_balance (P:330-331);
 * checkpoints: parameters, Adam m / v, the step counter and the shuffle generator state in
-  one .npz — resuming reproduces the uninterrupted run bit for bit (the step is deterministic).
+  one .npz — resuming reproduces the uninterrupted run bit for bit (the step is deterministic);
+* graph prefetch (`prefetch=True`): the next global batch's graph is built
+  on a builder context's stream while this step's backward runs (chg_graph_wait orders it).
 """
 from __future__ import annotations
 
@@ -62,7 +64,7 @@ class Trainer:
 
     def __init__(self, ctx: chg.Context, model: chg.Model, global_batch: int, total_steps: int,
                  rank: int = 0, world_size: int = 1, seed: int = 0, r_atom: float = 5.0, r_bond: float = 3.0,
-                 loss_weights=(2.0, 1.5, 0.1, 0.1), huber_delta: float = 0.1):
+                 loss_weights=(2.0, 1.5, 0.1, 0.1), huber_delta: float = 0.1, prefetch: bool = False):
         self.ctx, self.model = ctx, model
         self.global_batch, self.total_steps = global_batch, total_steps
         self.rank, self.world_size = rank, world_size
@@ -73,31 +75,47 @@ class Trainer:
         self.state = TrainState()
         self._order: Optional[np.ndarray] = None      # current epoch's shuffled structure order
         self._pos = 0                                 # next global batch in it
+        self.builder = chg.Context(ctx.device) if prefetch else None
+        self._pending = None                          # (struct ids, local batch, graph) built ahead
 
-    # ---- one optimizer step on one global batch (whole structures) -------------
-    def train_step(self, batch, struct_ids) -> Dict[str, float]:
+    def _local(self, batch, struct_ids, gctx):
+        """This rank's share of a global batch (whole structures, chg_balance over ranks)."""
         glob = _take(batch, struct_ids)
-        n_atoms = int(glob["atom_ptr"][-1])
-        n_mag = int(glob["labels"]["magmom_mask"].sum())
         if self.world_size > 1:
-            g_all = self.ctx.build_graph(glob["atom_ptr"], glob["positions"], glob["lattice"], glob["species"],
-                                         self.r_atom, self.r_bond)
+            g_all = gctx.build_graph(glob["atom_ptr"], glob["positions"], glob["lattice"], glob["species"],
+                                     self.r_atom, self.r_bond)
             ps = g_all.per_struct()
             g_all.close()
             owner = chg.balance(ps[:, 0] + ps[:, 1] + ps[:, 3], self.world_size)
             mine = [struct_ids[k] for k in range(len(struct_ids)) if owner[k] == self.rank]
-            local = _take(batch, mine)
+            return glob, _take(batch, mine)
+        return glob, glob
+
+    # ---- one optimizer step on one global batch (whole structures) -------------
+    def train_step(self, batch, struct_ids, next_ids=None) -> Dict[str, float]:
+        if self._pending is not None and self._pending[0] == list(struct_ids):
+            _, glob, local, g = self._pending
         else:
-            local = glob
-        g = self.ctx.build_graph(local["atom_ptr"], local["positions"], local["lattice"], local["species"],
-                                 self.r_atom, self.r_bond)
+            glob, local = self._local(batch, struct_ids, self.ctx)
+            g = self.ctx.build_graph(local["atom_ptr"], local["positions"], local["lattice"], local["species"],
+                                     self.r_atom, self.r_bond)
+        self._pending = None
+        n_atoms = int(glob["atom_ptr"][-1])
+        n_mag = int(glob["labels"]["magmom_mask"].sum())
         self.ctx.forward(self.model, g, train=True, host=False)
+        if self.builder is not None and next_ids is not None:    # next step's graph, built meanwhile
+            nglob, nloc = self._local(batch, next_ids, self.builder)
+            ng = self.builder.build_graph(nloc["atom_ptr"], nloc["positions"], nloc["lattice"], nloc["species"],
+                                          self.r_atom, self.r_bond)
+            self._pending = (list(next_ids), nglob, nloc, ng)
         loss = self.ctx.backward(self.model, g, local["labels"], w=self.w, delta=self.delta,
                                  n_struct_global=len(struct_ids), n_atoms_global=n_atoms,
                                  n_magmom_global=n_mag, sync_loss=True)
         self.state.step += 1
         lr = cosine_lr(self.state.step, self.total_steps, self.lr0)
         self.ctx.step(self.model, lr=lr, step=self.state.step, allreduce=self.world_size > 1)
+        if self._pending is not None:
+            self.ctx.wait_graph(self._pending[3])
         g.close()
         rec = {"step": self.state.step, "lr": lr, "loss": float(loss[0]), "loss_E": float(loss[1]),
                "loss_F": float(loss[2]), "loss_S": float(loss[3]), "loss_M": float(loss[4])}
@@ -119,7 +137,10 @@ class Trainer:
                     return self.state
                 ids = self._order[self._pos:self._pos + self.global_batch].tolist()
                 self._pos += self.global_batch
-                rec = self.train_step(batch, ids)
+                nxt = None
+                if self._pos + self.global_batch <= S and (max_steps is None or self.state.step + 1 < max_steps):
+                    nxt = self._order[self._pos:self._pos + self.global_batch].tolist()
+                rec = self.train_step(batch, ids, nxt)
                 if log:
                     log(rec)
             self._order = None

@@ -66,3 +66,18 @@ def test_checkpoint_resume_is_bit_exact(ctx):
         assert t1.state.step == t2.state.step == 11
         np.testing.assert_array_equal(a, b)
         m1.close(); m2.close()
+
+
+def test_prefetch_is_bit_exact(ctx):
+    data = lj_dataset(16, seed=13)
+    out = []
+    for pf in (False, True):
+        m = _model(ctx, 2)
+        tr = Trainer(ctx, m, global_batch=4, total_steps=12, seed=3, prefetch=pf)
+        tr.fit(data, epochs=3)
+        out.append((m.params(), [r["loss"] for r in tr.state.history]))
+        m.close()
+        if tr.builder is not None:
+            tr.builder.close()
+    np.testing.assert_array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]
