@@ -128,6 +128,15 @@ __global__ void __launch_bounds__(256, 4) k_gate_bwd(int64_t rows, int64_t rpb, 
   partial[blockIdx.x * 256 + threadIdx.x] = s;
 }
 
+// half-warps per target: enough for ~16+ rows each on long segments, and enough in total to
+// fill the GPU (~75K threads) when there are few targets (atoms of a small batch); the split
+// depends only on (mean length, targets), so the summation order is fixed for a given batch
+static int seg_split(int64_t mean, int64_t targets) {
+  int H = mean >= 96 ? 8 : mean >= 48 ? 4 : mean >= 24 ? 2 : 1;
+  while (H < 8 && targets * 16 * H < 75000 && mean >= 2 * H) H *= 2;
+  return H;
+}
+
 // ---------------------------------------------------------------------------
 // segmented sums (warp per target row, 2 columns per lane, fixed order)
 // ---------------------------------------------------------------------------
@@ -212,8 +221,6 @@ __global__ void __launch_bounds__(256) k_segsum_linear(int64_t targets, SegArgs 
                                                        const float *__restrict__ resid, float *__restrict__ out) {
   __shared__ __align__(16) float sW[64][64];
   __shared__ float4 part[16][16];
-  for (int i = threadIdx.x; i < 64 * 64; i += 256) sW[i >> 6][i & 63] = W[i];
-  __syncthreads();
   const int hw = threadIdx.x >> 4;
   const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / (16 * H);
   const int j = hw % H;
@@ -256,9 +263,11 @@ __global__ void __launch_bounds__(256) k_segsum_linear(int64_t targets, SegArgs 
       }
     }
   }
+  // W_out is staged after the gather loop (its load latency overlaps the row loads)
+  for (int i = threadIdx.x; i < 64 * 64; i += 256) sW[i >> 6][i & 63] = W[i];
+  if (H > 1) part[hw][hl] = acc;
+  __syncthreads();
   if (H > 1) {
-    part[hw][hl] = acc;
-    __syncthreads();
     if (j != 0 || t >= targets) return;
 #pragma unroll
     for (int q = 1; q < H; ++q) {
@@ -576,7 +585,7 @@ void segsum(chg_ctx *ctx, int64_t targets, float *out, int ldo, int accumulate, 
   int64_t rows = 0;
   for (int k = 0; k < nsrc; ++k) rows += src[k].rows;
   const int64_t mean = rows / std::max<int64_t>(targets, 1);
-  const int H = mean >= 96 ? 8 : mean >= 48 ? 4 : mean >= 24 ? 2 : 1;
+  const int H = seg_split(mean, targets);
   ProfScope ps(ctx, tag, 0.0, bytes);
   const int grid = ceil_div(targets * 16 * H, 256);
   switch (H) {
@@ -602,7 +611,7 @@ void segsum_linear(chg_ctx *ctx, int64_t targets, int nsrc, const SegSrc *src, f
     if ((uintptr_t)src[k].in & 15) CHG_THROW(CHG_ERR_STATE, "segsum_linear: 16-byte alignment required");
   }
   const int64_t mean = rows / std::max<int64_t>(targets, 1);
-  const int H = mean >= 96 ? 8 : mean >= 48 ? 4 : mean >= 24 ? 2 : 1;
+  const int H = seg_split(mean, targets);
   ProfScope ps(ctx, tag, 2.0 * targets * 64 * 64, bytes);
   const int grid = ceil_div(targets * 16 * H, 256);
   switch (H) {
