@@ -262,6 +262,33 @@ inline void check_launch(chg_ctx *ctx, const char *file = __builtin_FILE(), int 
   }
 }
 
+// Programmatic dependent launch: every kernel is launched with the PDL attribute and starts
+// with pdl_begin() — it waits for the preceding kernel of the stream (completion + memory
+// flush) and lets the next kernel's CTAs be scheduled as soon as its own CTAs are resident, so
+// launch processing and CTA ramp overlap the predecessor's tail.  Nothing is read before the
+// wait, so the ordering of the stream is unchanged (CHG_NO_PDL=1: plain launches).
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+template <typename... KArgs, typename... Args>
+inline void launch_k(chg_ctx *ctx, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     Args &&...args) {
+  static const bool no_pdl = getenv("CHG_NO_PDL") != nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  (void)ctx;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);   // errors: check_launch (cudaGetLastError)
+}
+
 // reduce.cu
 float *red_partial(chg_ctx *ctx, size_t floats);       // partial buffer for the next recorded job
 void red_push(chg_ctx *ctx, RedJob j);                 // record (red_on) or launch now

@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(256) k_dgeom_radial(int64_t rows, const double
                                                       const float *__restrict__ W1, const float *__restrict__ dE0,
                                                       const float *__restrict__ dE1, float4 *__restrict__ g,
                                                       int accumulate) {
+  pdl_begin();
   __shared__ float Wt[NC * 64][33];
   __shared__ float rowbuf[8][NC * 64];
   for (int i = threadIdx.x; i < NC * 64 * 32; i += blockDim.x) {
@@ -88,6 +89,7 @@ __global__ void __launch_bounds__(256) k_dgeom_angle(int64_t A, const double4 *_
                                                      const int32_t *__restrict__ e1, const int32_t *__restrict__ e2,
                                                      const float *__restrict__ Wth, const float *__restrict__ da,
                                                      float4 *__restrict__ ga1, float4 *__restrict__ ga2) {
+  pdl_begin();
   __shared__ float Wt[64][33];
   __shared__ float rowbuf[8][64];
   for (int i = threadIdx.x; i < 64 * 32; i += blockDim.x) {
@@ -133,6 +135,7 @@ __global__ void __launch_bounds__(256) k_dgeom_angle(int64_t A, const double4 *_
 __global__ void k_angle_to_edge(int64_t E, const int32_t *__restrict__ bond_id, const int32_t *__restrict__ angle_ptr,
                                 const int32_t *__restrict__ swp, const float4 *__restrict__ ga1,
                                 const float4 *__restrict__ ga2, float4 *__restrict__ g) {
+  pdl_begin();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= E) return;
   const int b = bond_id[e];
@@ -148,6 +151,7 @@ __global__ void k_angle_to_edge(int64_t E, const int32_t *__restrict__ bond_id, 
 // F_i = −Σ_{e out of i} (g_e − g_rev(e)), warp per atom (fixed tree)
 __global__ void k_dforce(int64_t N, const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ rev,
                          const float4 *__restrict__ g, float *__restrict__ F) {
+  pdl_begin();
   const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (i >= N) return;
@@ -164,6 +168,7 @@ __global__ void k_dforce(int64_t N, const int32_t *__restrict__ row_ptr, const i
 __global__ void k_dstress(const int32_t *__restrict__ atom_ptr, const int32_t *__restrict__ row_ptr,
                           const double4 *__restrict__ vec, const float4 *__restrict__ g, const float *__restrict__ lat,
                           float *__restrict__ stress) {
+  pdl_begin();
   __shared__ double sh[9][128];
   const int s = blockIdx.x, t = threadIdx.x;
   const int e0 = row_ptr[atom_ptr[s]], e1 = row_ptr[atom_ptr[s + 1]];
@@ -196,6 +201,7 @@ __global__ void k_dstress(const int32_t *__restrict__ atom_ptr, const int32_t *_
 }
 
 __global__ void k_fill_value(int64_t n, float v, float *__restrict__ x) {
+  pdl_begin();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) x[i] = v;
 }
@@ -212,34 +218,34 @@ void deriv_geometry(chg_ctx *ctx, const chg_graph *g, const float *freq_a, const
   float4 *gv = (float4 *)ctx->get("dgeom_g", 16 * (size_t)std::max<int64_t>(E, 1));
   ProfScope ps(ctx, "deriv_geom", 0.0, E * (512.0 + 48.0) + B * 300.0 + A * 400.0 + N * 12.0);
   if (E > 0) {
-    k_dgeom_radial<2><<<grid_rows(E), 256, 0, ctx->stream>>>(E, g->vec64, nullptr, freq_a, g->r_atom, p, W0, Wa, de,
+    launch_k(ctx, k_dgeom_radial<2>, grid_rows(E), 256, 0, ctx->stream, E, g->vec64, nullptr, freq_a, g->r_atom, p, W0, Wa, de,
                                                              dea, gv, 0);
     check_launch(ctx);
   }
   if (B > 0) {
-    k_dgeom_radial<1><<<grid_rows(B), 256, 0, ctx->stream>>>(B, g->vec64, g->bond_edge, freq_b, g->r_bond, p, Wb,
+    launch_k(ctx, k_dgeom_radial<1>, grid_rows(B), 256, 0, ctx->stream, B, g->vec64, g->bond_edge, freq_b, g->r_bond, p, Wb,
                                                              nullptr, deb, nullptr, gv, 1);
     check_launch(ctx);
   }
   if (A > 0) {
     float4 *ga1 = (float4 *)ctx->get("dgeom_a1", 16 * (size_t)A), *ga2 = (float4 *)ctx->get("dgeom_a2", 16 * (size_t)A);
-    k_dgeom_angle<<<grid_rows(A), 256, 0, ctx->stream>>>(A, g->vec64, g->angle_e1, g->angle_e2, Wth, da, ga1, ga2);
+    launch_k(ctx, k_dgeom_angle, grid_rows(A), 256, 0, ctx->stream, A, g->vec64, g->angle_e1, g->angle_e2, Wth, da, ga1, ga2);
     check_launch(ctx);
-    k_angle_to_edge<<<ceil_div(E, 256), 256, 0, ctx->stream>>>(E, g->bond_id, g->angle_ptr, g->swap, ga1, ga2, gv);
+    launch_k(ctx, k_angle_to_edge, ceil_div(E, 256), 256, 0, ctx->stream, E, g->bond_id, g->angle_ptr, g->swap, ga1, ga2, gv);
     check_launch(ctx);
   }
   if (N > 0) {
-    k_dforce<<<ceil_div(N * 32, 256), 256, 0, ctx->stream>>>(N, g->row_ptr, g->rev, gv, forces);
+    launch_k(ctx, k_dforce, ceil_div(N * 32, 256), 256, 0, ctx->stream, N, g->row_ptr, g->rev, gv, forces);
     check_launch(ctx);
   }
   if (g->S > 0) {
-    k_dstress<<<g->S, 128, 0, ctx->stream>>>(g->atom_ptr, g->row_ptr, g->vec64, gv, g->lattice_f, stress);
+    launch_k(ctx, k_dstress, g->S, 128, 0, ctx->stream, g->atom_ptr, g->row_ptr, g->vec64, gv, g->lattice_f, stress);
     check_launch(ctx);
   }
 }
 
 void fill_value(chg_ctx *ctx, float *x, int64_t n, float v) {
   if (n <= 0) return;
-  k_fill_value<<<ceil_div(n, 256), 256, 0, ctx->stream>>>(n, v, x);
+  launch_k(ctx, k_fill_value, ceil_div(n, 256), 256, 0, ctx->stream, n, v, x);
   check_launch(ctx);
 }

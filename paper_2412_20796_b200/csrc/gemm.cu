@@ -55,6 +55,7 @@ __device__ __forceinline__ float loadW(const Chunk &c, int k, int n) {
 // 256 threads = 16 (x 4 columns) x 16 (x TM/16 rows)
 template <bool VEC, int TM, int TK = 32>
 __global__ void __launch_bounds__(256) k_rowgemm(const __grid_constant__ RowGemm g) {
+  pdl_begin();
   constexpr int RPT = TM / 16;
   __shared__ __align__(16) float As[TK][TM + 4];
   __shared__ __align__(16) float Ws[TK][TN];
@@ -140,6 +141,7 @@ constexpr int WK = 64, WN = 64, WM = 32;
 
 template <bool VEC>
 __global__ void __launch_bounds__(256) k_wgrad(const WGrad g, float *__restrict__ partial, int Kp, int rows_per_split) {
+  pdl_begin();
   __shared__ __align__(16) float As[WM][WK + 4];
   __shared__ __align__(16) float Ds[WM][WN + 4];
   const int kt = blockIdx.x, nt = blockIdx.y, sp = blockIdx.z;
@@ -320,21 +322,21 @@ void rowgemm(chg_ctx *ctx, const RowGemm &g) {
     const bool tiny = (int64_t)ceil_div(g.M, 32) * g.nchunk < 148;
     if (tiny) {
       dim3 grid(ceil_div(g.M, 16), g.nchunk);
-      if (vec) k_rowgemm<true, 16, 64><<<grid, 256, 0, ctx->stream>>>(g);
-      else k_rowgemm<false, 16, 64><<<grid, 256, 0, ctx->stream>>>(g);
+      if (vec) launch_k(ctx, k_rowgemm<true, 16, 64>, grid, 256, 0, ctx->stream, g);
+      else launch_k(ctx, k_rowgemm<false, 16, 64>, grid, 256, 0, ctx->stream, g);
     } else {
       dim3 grid(ceil_div(g.M, 32), g.nchunk);
-      if (vec) k_rowgemm<true, 32, 64><<<grid, 256, 0, ctx->stream>>>(g);
-      else k_rowgemm<false, 32, 64><<<grid, 256, 0, ctx->stream>>>(g);
+      if (vec) launch_k(ctx, k_rowgemm<true, 32, 64>, grid, 256, 0, ctx->stream, g);
+      else launch_k(ctx, k_rowgemm<false, 32, 64>, grid, 256, 0, ctx->stream, g);
     }
   } else if (small) {
     dim3 grid(ceil_div(g.M, 32), g.nchunk);
-    if (vec) k_rowgemm<true, 32><<<grid, 256, 0, ctx->stream>>>(g);
-    else k_rowgemm<false, 32><<<grid, 256, 0, ctx->stream>>>(g);
+    if (vec) launch_k(ctx, k_rowgemm<true, 32>, grid, 256, 0, ctx->stream, g);
+    else launch_k(ctx, k_rowgemm<false, 32>, grid, 256, 0, ctx->stream, g);
   } else {
     dim3 grid(ceil_div(g.M, TM), g.nchunk);
-    if (vec) k_rowgemm<true, TM><<<grid, 256, 0, ctx->stream>>>(g);
-    else k_rowgemm<false, TM><<<grid, 256, 0, ctx->stream>>>(g);
+    if (vec) launch_k(ctx, k_rowgemm<true, TM>, grid, 256, 0, ctx->stream, g);
+    else launch_k(ctx, k_rowgemm<false, TM>, grid, 256, 0, ctx->stream, g);
   }
   check_launch(ctx);
 }
@@ -389,9 +391,9 @@ void wgrad(chg_ctx *ctx, const WGrad &g) {
     bool vec = aop_vec(g.A);
     dim3 grid(ktiles, ntiles, splits);
     if (vec)
-      k_wgrad<true><<<grid, 256, 0, ctx->stream>>>(g, partial, Kp, rps);
+      launch_k(ctx, k_wgrad<true>, grid, 256, 0, ctx->stream, g, partial, Kp, rps);
     else
-      k_wgrad<false><<<grid, 256, 0, ctx->stream>>>(g, partial, Kp, rps);
+      launch_k(ctx, k_wgrad<false>, grid, 256, 0, ctx->stream, g, partial, Kp, rps);
     check_launch(ctx);
   }
   launch_wgrad_reduce(ctx, g, partial, Kp, splits);

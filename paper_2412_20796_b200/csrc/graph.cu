@@ -96,6 +96,7 @@ __device__ __forceinline__ Range pair_range(const double *fi, const double *fj, 
 __global__ void k_frac(int N, const double *__restrict__ pos, const int32_t *__restrict__ soa,
                        const StructGeo *__restrict__ geo, const int32_t *__restrict__ species,
                        int n_species, double *__restrict__ frac, int *flag) {
+  pdl_begin();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
   const StructGeo &g = geo[soa[i]];
@@ -114,6 +115,7 @@ __global__ void k_frac(int N, const double *__restrict__ pos, const int32_t *__r
 // kernels stay bounded; the host raises at the size synchronisation.
 __global__ void k_geo(int S, const double *__restrict__ lat, double r_atom, const int32_t *__restrict__ atom_ptr,
                       StructGeo *__restrict__ geo, float *__restrict__ lat_f, int *flag) {
+  pdl_begin();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= S) return;
   double l[9];
@@ -174,6 +176,7 @@ __device__ __forceinline__ int cell_coord(double f, int nc) {
 
 __global__ void k_cell_assign(int N, const double *__restrict__ frac, const int32_t *__restrict__ soa,
                               const int32_t *__restrict__ atom_ptr, const StructGeo *__restrict__ geo, CellArgs ca) {
+  pdl_begin();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
   const int s = soa[i];
@@ -188,6 +191,7 @@ __global__ void k_cell_assign(int N, const double *__restrict__ frac, const int3
 // block per structure: exclusive scan of its cell counts -> absolute start positions
 __global__ void k_cell_scan(int S, const int32_t *__restrict__ atom_ptr, const StructGeo *__restrict__ geo,
                             CellArgs ca) {
+  pdl_begin();
   __shared__ int sh[256];
   const int s = blockIdx.x;
   const StructGeo &g = geo[s];
@@ -214,6 +218,7 @@ __global__ void k_cell_scan(int S, const int32_t *__restrict__ atom_ptr, const S
 
 __global__ void k_cell_place(int N, const int32_t *__restrict__ soa, const int32_t *__restrict__ atom_ptr,
                              CellArgs ca, int32_t *__restrict__ cursor) {
+  pdl_begin();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
   const int c = ca.atom_cell[i];
@@ -306,6 +311,7 @@ __global__ void __launch_bounds__(32 * GWPA) k_count(int N, const double *__rest
                                                      const StructGeo *__restrict__ geo, double ra2, double rb2,
                                                      int32_t *__restrict__ cnt_e, int32_t *__restrict__ cnt_b,
                                                      int *flag, CellArgs ca) {
+  pdl_begin();
   __shared__ int sh[GWPA][2];
   __shared__ int cnt27[28];
   const int i = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -362,6 +368,7 @@ __global__ void __launch_bounds__(32 * GWPA) k_count(int N, const double *__rest
 __global__ void k_scan(int N, const int32_t *__restrict__ cnt_e, const int32_t *__restrict__ cnt_b,
                        int32_t *__restrict__ row_ptr, int32_t *__restrict__ bond_ptr,
                        int32_t *__restrict__ ang_ptr, long long *tot) {
+  pdl_begin();
   __shared__ long long sh[3][1024];
   int t = threadIdx.x;
   int per = (N + blockDim.x - 1) / blockDim.x;
@@ -418,6 +425,7 @@ __global__ void __launch_bounds__(32 * GWPA) k_fill(int N, const double *__restr
                                                     float4 *__restrict__ vec, double4 *__restrict__ vec64,
                                                     int32_t *__restrict__ bond_id, int32_t *__restrict__ bond_edge,
                                                     CellArgs ca) {
+  pdl_begin();
   __shared__ int sh[GWPA][2];
   __shared__ int cnt27[28];
   __shared__ long long keys[CELL_MAXNB];
@@ -556,6 +564,7 @@ __global__ void k_angles(int B, const int32_t *__restrict__ bond_edge, const int
                          int32_t *__restrict__ angle_ptr, int32_t *__restrict__ ab1,
                          int32_t *__restrict__ ab2, int32_t *__restrict__ ae1, int32_t *__restrict__ ae2,
                          int32_t *__restrict__ actr, int32_t *__restrict__ swp, int A) {
+  pdl_begin();
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) {
     if (b == B) angle_ptr[B] = A;
@@ -585,6 +594,7 @@ __global__ void k_angles(int B, const int32_t *__restrict__ bond_edge, const int
 __global__ void k_rev(int E, const int32_t *__restrict__ center, const int32_t *__restrict__ nbr,
                       const char4 *__restrict__ img, const int32_t *__restrict__ row_ptr,
                       int32_t *__restrict__ rev, int *flag) {
+  pdl_begin();
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E) return;
   int i = center[e], j = nbr[e];
@@ -757,27 +767,27 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
     CUDA_OK(cudaMemsetAsync(d_tot, 0, 64, st));
     double ra2 = r_atom * r_atom, rb2 = r_bond * r_bond;
     if (dev_geo) {
-      k_geo<<<ceil_div(S, 128), 128, 0, st>>>(S, lat, r_atom, G->atom_ptr, d_geo, G->lattice_f, flag);
+      launch_k(ctx, k_geo, ceil_div(S, 128), 128, 0, st, S, lat, r_atom, G->atom_ptr, d_geo, G->lattice_f, flag);
       check_launch(ctx);
     }
     if (N) {
-      k_frac<<<ceil_div(N, 256), 256, 0, st>>>((int)N, d_pos, G->struct_of_atom, d_geo, G->species,
+      launch_k(ctx, k_frac, ceil_div(N, 256), 256, 0, st, (int)N, d_pos, G->struct_of_atom, d_geo, G->species,
                                                 n_species, d_frac, flag);
       check_launch(ctx);
       if (any_cells) {
         CUDA_OK(cudaMemsetAsync(ca.cell_cnt, 0, 4 * N, st));
         CUDA_OK(cudaMemsetAsync(cell_cursor, 0, 4 * N, st));
-        k_cell_assign<<<ceil_div(N, 256), 256, 0, st>>>((int)N, d_frac, G->struct_of_atom, G->atom_ptr, d_geo, ca);
+        launch_k(ctx, k_cell_assign, ceil_div(N, 256), 256, 0, st, (int)N, d_frac, G->struct_of_atom, G->atom_ptr, d_geo, ca);
         check_launch(ctx);
-        k_cell_scan<<<S, 256, 0, st>>>(S, G->atom_ptr, d_geo, ca);
+        launch_k(ctx, k_cell_scan, S, 256, 0, st, S, G->atom_ptr, d_geo, ca);
         check_launch(ctx);
-        k_cell_place<<<ceil_div(N, 256), 256, 0, st>>>((int)N, G->struct_of_atom, G->atom_ptr, ca, cell_cursor);
+        launch_k(ctx, k_cell_place, ceil_div(N, 256), 256, 0, st, (int)N, G->struct_of_atom, G->atom_ptr, ca, cell_cursor);
         check_launch(ctx);
       }
-      k_count<<<(unsigned)N, 32 * GWPA, 0, st>>>((int)N, d_pos, d_frac, G->struct_of_atom, G->atom_ptr,
+      launch_k(ctx, k_count, (unsigned)N, 32 * GWPA, 0, st, (int)N, d_pos, d_frac, G->struct_of_atom, G->atom_ptr,
                                                       d_geo, ra2, rb2, cnt_e, cnt_b, flag, ca);
       check_launch(ctx);
-      k_scan<<<1, 1024, 0, st>>>((int)N, cnt_e, cnt_b, G->row_ptr, G->bond_ptr, G->atom_angle_ptr, d_tot);
+      launch_k(ctx, k_scan, 1, 1024, 0, st, (int)N, cnt_e, cnt_b, G->row_ptr, G->bond_ptr, G->atom_angle_ptr, d_tot);
       check_launch(ctx);
     } else {
       CUDA_OK(cudaMemsetAsync(G->row_ptr, 0, 4, st));
@@ -828,17 +838,17 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
 
     ProfScope ps2(ctx, "graph", 0.0, 0.0);
     if (N) {
-      k_fill<<<(unsigned)N, 32 * GWPA, 0, st>>>((int)N, d_pos, d_frac, G->struct_of_atom, G->atom_ptr,
+      launch_k(ctx, k_fill, (unsigned)N, 32 * GWPA, 0, st, (int)N, d_pos, d_frac, G->struct_of_atom, G->atom_ptr,
                                                      d_geo, ra2, rb2, G->row_ptr, G->bond_ptr, G->center,
                                                      G->nbr, G->img, G->vec, G->vec64, G->bond_id, G->bond_edge, ca);
       check_launch(ctx);
-      k_angles<<<ceil_div(B + 1, 256), 256, 0, st>>>((int)B, G->bond_edge, G->center, G->bond_ptr,
+      launch_k(ctx, k_angles, ceil_div(B + 1, 256), 256, 0, st, (int)B, G->bond_edge, G->center, G->bond_ptr,
                                                       G->atom_angle_ptr, G->angle_ptr, G->angle_b1,
                                                       G->angle_b2, G->angle_e1, G->angle_e2, G->angle_ctr,
                                                       G->swap, (int)A);
       check_launch(ctx);
       if (E) {
-        k_rev<<<ceil_div(E, 256), 256, 0, st>>>((int)E, G->center, G->nbr, G->img, G->row_ptr, G->rev, G->d_flag);
+        launch_k(ctx, k_rev, ceil_div(E, 256), 256, 0, st, (int)E, G->center, G->nbr, G->img, G->row_ptr, G->rev, G->d_flag);
         check_launch(ctx);
       }
 

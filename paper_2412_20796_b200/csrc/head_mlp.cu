@@ -83,6 +83,7 @@ __device__ __forceinline__ void load_tile(const float *__restrict__ src, int64_t
 
 template <int NL, int NOUT>
 __global__ void __launch_bounds__(256) k_head_fwd(const __grid_constant__ HeadArgs a) {
+  pdl_begin();
   extern __shared__ float sm[];
   using S = HeadSmem<NL, NOUT>;
   float *sH = sm + S::T0;            // [64][HP] layer input / activation
@@ -141,6 +142,7 @@ __global__ void __launch_bounds__(256) k_head_fwd(const __grid_constant__ HeadAr
 
 template <int NL, int NOUT>
 __global__ void __launch_bounds__(256) k_head_bwd(const __grid_constant__ HeadArgs a) {
+  pdl_begin();
   extern __shared__ float sm[];
   using S = HeadSmem<NL, NOUT>;
   float *sA = sm + S::T0;            // layer input H_{k-1} (or X)
@@ -337,7 +339,7 @@ void run_fwd(chg_ctx *ctx, const HeadArgs &a, const char *tag) {
   const int grid = (int)std::min<int64_t>(ntiles, 2 * sm_count());
   ProfScope ps(ctx, tag, 2.0 * a.rows * (64.0 * 64 * (NL - 1) + 64.0 * NOUT),
                a.rows * 4.0 * (64 + 64 * (NL - 1) + NOUT) + 4.0 * head_block_size(NL, NOUT) * grid);
-  k_head_fwd<NL, NOUT><<<grid, 256, smem, ctx->stream>>>(a);
+  launch_k(ctx, k_head_fwd<NL, NOUT>, grid, 256, smem, ctx->stream, a);
   check_launch(ctx);
 }
 
@@ -357,7 +359,7 @@ void run_bwd(chg_ctx *ctx, HeadArgs a, float *G, const char *tag) {
   {
     ProfScope ps(ctx, tag, 2.0 * a.rows * (2.0 * 64 * 64 * (NL - 1) + 2.0 * 64 * NOUT),
                  a.rows * 4.0 * (64 * 3 + 64 * (NL - 1) + NOUT) + 4.0 * nb * (double)grid * 2);
-    k_head_bwd<NL, NOUT><<<grid, 256, smem, ctx->stream>>>(a);
+    launch_k(ctx, k_head_bwd<NL, NOUT>, grid, 256, smem, ctx->stream, a);
     check_launch(ctx);
   }
   RedJob j;                                        // per-CTA partials -> the head's gradient block

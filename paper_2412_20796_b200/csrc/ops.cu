@@ -20,6 +20,7 @@ __device__ __forceinline__ RowStats ln_stats(float a, float b) {
 __global__ void k_gate_fwd(int64_t rows, const float *__restrict__ y, int ldy, GateLN ln, int mode,
                            const float *__restrict__ w, const int32_t *__restrict__ i1, const int32_t *__restrict__ i2,
                            const float *__restrict__ resid, float *__restrict__ out) {
+  pdl_begin();
   int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int l = threadIdx.x & 31;
   if (row >= rows) return;
@@ -60,6 +61,7 @@ __global__ void __launch_bounds__(256, 4) k_gate_bwd(int64_t rows, int64_t rpb, 
                                                   float *__restrict__ dy, int lddy, float *__restrict__ dw_acc,
                                                   float *__restrict__ q1, float *__restrict__ q2,
                                                   float *__restrict__ partial, int rnd) {
+  pdl_begin();
   __shared__ float sh[8][256];
   int l = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int c0 = 2 * l;
@@ -67,9 +69,23 @@ __global__ void __launch_bounds__(256, 4) k_gate_bwd(int64_t rows, int64_t rpb, 
   float2 gc = *(const float2 *)(ln.gc + c0), bc = *(const float2 *)(ln.bc + c0);
   float2 gg = *(const float2 *)(ln.gg + c0), bg = *(const float2 *)(ln.bg + c0);
   float a_gc[2] = {0, 0}, a_bc[2] = {0, 0}, a_gg[2] = {0, 0}, a_bg[2] = {0, 0};
+  // software pipeline: the next row's y (and its seed-row index) are in flight while this
+  // row's LayerNorm adjoint runs
+  float2 nyc = make_float2(0.f, 0.f), nyg = nyc;
+  int64_t ndrow = 0;
+  if (r0 + wid < r1) {
+    nyc = __ldg((const float2 *)(y + (r0 + wid) * ldy + c0));
+    nyg = __ldg((const float2 *)(y + (r0 + wid) * ldy + 64 + c0));
+    ndrow = didx ? __ldg(didx + r0 + wid) : r0 + wid;
+  }
   for (int64_t row = r0 + wid; row < r1; row += 8) {
-    float2 yc = *(const float2 *)(y + row * ldy + c0);
-    float2 yg = *(const float2 *)(y + row * ldy + 64 + c0);
+    const float2 yc = nyc, yg = nyg;
+    const int64_t drow = ndrow;
+    if (row + 8 < r1) {
+      nyc = __ldg((const float2 *)(y + (row + 8) * ldy + c0));
+      nyg = __ldg((const float2 *)(y + (row + 8) * ldy + 64 + c0));
+      ndrow = didx ? __ldg(didx + row + 8) : row + 8;
+    }
     RowStats sc = ln_stats(yc.x, yc.y), sg = ln_stats(yg.x, yg.y);
     float xc[2] = {(yc.x - sc.mu) * sc.rstd, (yc.y - sc.mu) * sc.rstd};
     float xg[2] = {(yg.x - sg.mu) * sg.rstd, (yg.y - sg.mu) * sg.rstd};
@@ -78,7 +94,6 @@ __global__ void __launch_bounds__(256, 4) k_gate_bwd(int64_t rows, int64_t rpb, 
     float s_g[2] = {sigmoidf_(ng[0]), sigmoidf_(ng[1])};
     float s_c[2] = {siluf_(nc[0]), siluf_(nc[1])};
     float phi[2] = {s_g[0] * s_c[0], s_g[1] * s_c[1]};
-    int64_t drow = didx ? didx[row] : row;
     float2 d2 = *(const float2 *)(dout + drow * 64 + c0);
     float d[2] = {d2.x, d2.y};
     float dphi[2];
@@ -152,6 +167,7 @@ struct SegArgs { SegSrc s[3]; int n; };
 template <int H>
 __global__ void __launch_bounds__(256) k_segsum(int64_t targets, float *__restrict__ out, int ldo, int accumulate,
                                                 SegArgs a) {
+  pdl_begin();
   __shared__ float4 part[16][16];                   // [half-warp in block][lane]
   const int hw = threadIdx.x >> 4;                  // half-warp in block (16)
   const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / (16 * H);
@@ -219,6 +235,7 @@ template <int H>
 __global__ void __launch_bounds__(256) k_segsum_linear(int64_t targets, SegArgs a, float *__restrict__ agg,
                                                        const float *__restrict__ W, const float *__restrict__ bias,
                                                        const float *__restrict__ resid, float *__restrict__ out) {
+  pdl_begin();
   __shared__ __align__(16) float sW[64][64];
   __shared__ float4 part[16][16];
   const int hw = threadIdx.x >> 4;
@@ -304,6 +321,7 @@ __global__ void __launch_bounds__(256) k_segsum_linear(int64_t targets, SegArgs 
 constexpr int EGB = 64;   // atoms per block
 __global__ void __launch_bounds__(64) k_embed_grad(int64_t N, int nz, const int32_t *__restrict__ species,
                                                    const float *__restrict__ dv, float *__restrict__ part) {
+  pdl_begin();
   extern __shared__ float bins[];                   // [nz][64]
   const int c = threadIdx.x;
   for (int i = c; i < nz * 64; i += 64) bins[i] = 0.f;
@@ -324,6 +342,7 @@ __global__ void __launch_bounds__(64) k_embed_grad(int64_t N, int nz, const int3
 __global__ void k_edge_update(int64_t E, const float4 *__restrict__ e, const float *__restrict__ bias,
                               const int32_t *__restrict__ bond_id, const float4 *__restrict__ tmp,
                               float4 *__restrict__ out) {
+  pdl_begin();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;   // float4 index
   if (i >= E * 16) return;
   const int64_t row = i >> 4;
@@ -340,6 +359,7 @@ __global__ void k_edge_update(int64_t E, const float4 *__restrict__ e, const flo
 // column sums of a [rows, 64] matrix: per-block partials (fixed row ranges), reduced in block order
 __global__ void __launch_bounds__(256) k_colsum_partial(int64_t rows, int64_t rpb, const float *__restrict__ D,
                                                         float *__restrict__ part) {
+  pdl_begin();
   __shared__ float4 sh[16][16];
   const int t = threadIdx.x, c = t & 15, rl = t >> 4;
   const int64_t r0 = blockIdx.x * rpb, r1 = min(rows, r0 + rpb);
@@ -362,6 +382,7 @@ __global__ void __launch_bounds__(256) k_colsum_partial(int64_t rows, int64_t rp
 // ---------------------------------------------------------------------------
 __global__ void k_heads_forces(int N, const int32_t *__restrict__ row_ptr, const float4 *__restrict__ vec,
                                const float *__restrict__ n_e, float *__restrict__ F) {
+  pdl_begin();
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (i >= N) return;
   float fx = 0.f, fy = 0.f, fz = 0.f;
@@ -389,6 +410,7 @@ __global__ void k_heads_struct(const int32_t *__restrict__ atom_ptr, const float
                                const float *__restrict__ inv_n, const float *__restrict__ e_atom,
                                const float *__restrict__ M9, float *__restrict__ energy, float *__restrict__ epa,
                                float *__restrict__ stress) {
+  pdl_begin();
   __shared__ double sh[10][128];
   int s = blockIdx.x, t = threadIdx.x;
   int a0 = atom_ptr[s], a1 = atom_ptr[s + 1];
@@ -436,6 +458,7 @@ struct LossArgs {
 };
 
 __global__ void k_loss(LossArgs a, double *out) {
+  pdl_begin();
   __shared__ double sh[5][1024];
   int t = threadIdx.x;
   double le = 0, lf = 0, ls = 0, lm = 0, cm = 0;
@@ -465,6 +488,7 @@ __global__ void k_loss(LossArgs a, double *out) {
 
 __global__ void k_seed_atom(LossArgs a, const double *lossbuf, float *__restrict__ d_eatom, float *__restrict__ dM9,
                             float *__restrict__ d_mag, float *__restrict__ seedF) {
+  pdl_begin();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.N) return;
   int s = a.soa[i];
@@ -486,6 +510,7 @@ __global__ void k_seed_atom(LossArgs a, const double *lossbuf, float *__restrict
 
 __global__ void k_seed_edge(int64_t E, const int32_t *__restrict__ center, const float4 *__restrict__ vec,
                             const float *__restrict__ seedF, float *__restrict__ dn) {
+  pdl_begin();
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= E) return;
   float4 d = vec[e];
@@ -498,6 +523,7 @@ __global__ void k_seed_edge(int64_t E, const int32_t *__restrict__ center, const
 // ---------------------------------------------------------------------------
 __global__ void k_transpose(const int64_t *__restrict__ off, const int32_t *__restrict__ rc, const float *__restrict__ p,
                             float *__restrict__ wt) {
+  pdl_begin();
   const int t = blockIdx.y;
   const int64_t o = off[t];
   const int R = rc[2 * t], C = rc[2 * t + 1];
@@ -508,6 +534,7 @@ __global__ void k_transpose(const int64_t *__restrict__ off, const int32_t *__re
 }
 
 __global__ void k_embed(int64_t N, const int32_t *__restrict__ species, const float *__restrict__ W, float *__restrict__ v) {
+  pdl_begin();
   int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t i = gt >> 4;
   int c4 = (int)(gt & 15);
@@ -516,6 +543,7 @@ __global__ void k_embed(int64_t N, const int32_t *__restrict__ species, const fl
 }
 
 __global__ void k_finite(int64_t n, const float *__restrict__ g, int *bad) {
+  pdl_begin();
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n && !isfinite(g[i])) atomicMin(bad, (int)i);
 }
@@ -525,6 +553,7 @@ __global__ void k_finite(int64_t n, const float *__restrict__ g, int *bad) {
 __global__ void k_adam(int64_t n, float *__restrict__ p, float *__restrict__ g, float *__restrict__ m,
                        float *__restrict__ v, float lr, float b1, float b2, float eps, float step_size,
                        float inv_sqrt_bc2, const int *__restrict__ bad) {
+  pdl_begin();
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n || (bad && *bad != 0x7f7f7f7f)) return;
   float gi = g[i];
@@ -545,7 +574,7 @@ void gate_fwd(chg_ctx *ctx, int64_t rows, const float *y, int ldy, GateLN ln, in
               const int32_t *i1, const int32_t *i2, const float *resid, float *out) {
   if (rows <= 0) return;
   ProfScope ps(ctx, "gate_fwd", 0.0, rows * (512.0 + 256.0 + (mode == GATE_MUL_W1W2 ? 520.0 : 256.0)));
-  k_gate_fwd<<<ceil_div(rows * 32, 256), 256, 0, ctx->stream>>>(rows, y, ldy, ln, mode, w, i1, i2, resid, out);
+  launch_k(ctx, k_gate_fwd, ceil_div(rows * 32, 256), 256, 0, ctx->stream, rows, y, ldy, ln, mode, w, i1, i2, resid, out);
   check_launch(ctx);
 }
 
@@ -558,7 +587,7 @@ void gate_bwd(chg_ctx *ctx, int64_t rows, const float *y, int ldy, GateLN ln, in
   float *part = red_partial(ctx, (size_t)nb * 256);
   ProfScope ps(ctx, "gate_bwd", 0.0,
                rows * (512.0 + 260.0 + 512.0 + (mode == GATE_MUL_W ? 768.0 : mode == GATE_MUL_W1W2 ? 1032.0 : 0.0)));
-  k_gate_bwd<<<nb, 256, 0, ctx->stream>>>(rows, rpb, y, ldy, ln, mode, w, i1, i2, dout, didx, dy, lddy, dw_acc, q1,
+  launch_k(ctx, k_gate_bwd, nb, 256, 0, ctx->stream, rows, rpb, y, ldy, ln, mode, w, i1, i2, dout, didx, dy, lddy, dw_acc, q1,
                                           q2, part, ctx->use_tc ? 1 : 0);
   check_launch(ctx);
   RedJob j;                                        // LN affine gradients: batched reduction (reduce.cu)
@@ -589,10 +618,10 @@ void segsum(chg_ctx *ctx, int64_t targets, float *out, int ldo, int accumulate, 
   ProfScope ps(ctx, tag, 0.0, bytes);
   const int grid = ceil_div(targets * 16 * H, 256);
   switch (H) {
-    case 8: k_segsum<8><<<grid, 256, 0, ctx->stream>>>(targets, out, ldo, accumulate, a); break;
-    case 4: k_segsum<4><<<grid, 256, 0, ctx->stream>>>(targets, out, ldo, accumulate, a); break;
-    case 2: k_segsum<2><<<grid, 256, 0, ctx->stream>>>(targets, out, ldo, accumulate, a); break;
-    default: k_segsum<1><<<grid, 256, 0, ctx->stream>>>(targets, out, ldo, accumulate, a); break;
+    case 8: launch_k(ctx, k_segsum<8>, grid, 256, 0, ctx->stream, targets, out, ldo, accumulate, a); break;
+    case 4: launch_k(ctx, k_segsum<4>, grid, 256, 0, ctx->stream, targets, out, ldo, accumulate, a); break;
+    case 2: launch_k(ctx, k_segsum<2>, grid, 256, 0, ctx->stream, targets, out, ldo, accumulate, a); break;
+    default: launch_k(ctx, k_segsum<1>, grid, 256, 0, ctx->stream, targets, out, ldo, accumulate, a); break;
   }
   check_launch(ctx);
 }
@@ -615,10 +644,10 @@ void segsum_linear(chg_ctx *ctx, int64_t targets, int nsrc, const SegSrc *src, f
   ProfScope ps(ctx, tag, 2.0 * targets * 64 * 64, bytes);
   const int grid = ceil_div(targets * 16 * H, 256);
   switch (H) {
-    case 8: k_segsum_linear<8><<<grid, 256, 0, ctx->stream>>>(targets, a, agg, W, bias, resid, out); break;
-    case 4: k_segsum_linear<4><<<grid, 256, 0, ctx->stream>>>(targets, a, agg, W, bias, resid, out); break;
-    case 2: k_segsum_linear<2><<<grid, 256, 0, ctx->stream>>>(targets, a, agg, W, bias, resid, out); break;
-    default: k_segsum_linear<1><<<grid, 256, 0, ctx->stream>>>(targets, a, agg, W, bias, resid, out); break;
+    case 8: launch_k(ctx, k_segsum_linear<8>, grid, 256, 0, ctx->stream, targets, a, agg, W, bias, resid, out); break;
+    case 4: launch_k(ctx, k_segsum_linear<4>, grid, 256, 0, ctx->stream, targets, a, agg, W, bias, resid, out); break;
+    case 2: launch_k(ctx, k_segsum_linear<2>, grid, 256, 0, ctx->stream, targets, a, agg, W, bias, resid, out); break;
+    default: launch_k(ctx, k_segsum_linear<1>, grid, 256, 0, ctx->stream, targets, a, agg, W, bias, resid, out); break;
   }
   check_launch(ctx);
 }
@@ -629,7 +658,7 @@ void embed_grad(chg_ctx *ctx, int64_t N, int n_species, const int32_t *species, 
   float *part = red_partial(ctx, (size_t)nb * n_species * 64);
   {
     ProfScope ps(ctx, "embed_grad", 0.0, N * 260.0 + nb * n_species * 256.0);
-    k_embed_grad<<<nb, 64, n_species * 64 * 4, ctx->stream>>>(N, n_species, species, dv, part);
+    launch_k(ctx, k_embed_grad, nb, 64, n_species * 64 * 4, ctx->stream, N, n_species, species, dv, part);
     check_launch(ctx);
   }
   RedJob j;
@@ -641,7 +670,7 @@ void edge_update(chg_ctx *ctx, int64_t E, const float *e, const float *bias, con
                  float *out) {
   if (E <= 0) return;
   ProfScope ps(ctx, "edge_update", 0.0, E * (512.0 + 4.0) + 0.0);
-  k_edge_update<<<ceil_div(E * 16, 256), 256, 0, ctx->stream>>>(E, (const float4 *)e, bias, bond_id,
+  launch_k(ctx, k_edge_update, ceil_div(E * 16, 256), 256, 0, ctx->stream, E, (const float4 *)e, bias, bond_id,
                                                                  (const float4 *)tmp, (float4 *)out);
   check_launch(ctx);
 }
@@ -653,7 +682,7 @@ void colsum(chg_ctx *ctx, int64_t rows, const float *D, float *grad) {
   float *part = red_partial(ctx, (size_t)nb * 64);
   {
     ProfScope ps(ctx, "colsum", 0.0, rows * 256.0 + nb * 256.0);
-    k_colsum_partial<<<nb, 256, 0, ctx->stream>>>(rows, rpb, D, part);
+    launch_k(ctx, k_colsum_partial, nb, 256, 0, ctx->stream, rows, rpb, D, part);
     check_launch(ctx);
   }
   RedJob j;
@@ -664,7 +693,7 @@ void colsum(chg_ctx *ctx, int64_t rows, const float *D, float *grad) {
 void heads_forces(chg_ctx *ctx, const chg_graph *g, const float *n_e, float *forces) {
   if (g->N <= 0) return;
   ProfScope ps(ctx, "heads", 0.0, g->E * 20.0 + g->N * 12.0);
-  k_heads_forces<<<ceil_div(g->N * 32, 256), 256, 0, ctx->stream>>>((int)g->N, g->row_ptr, g->vec, n_e, forces);
+  launch_k(ctx, k_heads_forces, ceil_div(g->N * 32, 256), 256, 0, ctx->stream, (int)g->N, g->row_ptr, g->vec, n_e, forces);
   check_launch(ctx);
 }
 
@@ -672,7 +701,7 @@ void heads_struct(chg_ctx *ctx, const chg_graph *g, const float *e_atom, const f
                   float *stress) {
   if (g->S <= 0) return;
   ProfScope ps(ctx, "heads", 0.0, g->N * 40.0 + g->S * 48.0);
-  k_heads_struct<<<g->S, 128, 0, ctx->stream>>>(g->atom_ptr, g->lattice_f, g->inv_natoms, e_atom, M9, energy, epa,
+  launch_k(ctx, k_heads_struct, g->S, 128, 0, ctx->stream, g->atom_ptr, g->lattice_f, g->inv_natoms, e_atom, M9, energy, epa,
                                                 stress);
   check_launch(ctx);
 }
@@ -692,15 +721,15 @@ void loss_and_seeds(chg_ctx *ctx, const chg_graph *g, const float *epa, const fl
   if (a.Sg <= 0) a.Sg = 1;
   if (a.Ng <= 0) a.Ng = 1;
   ProfScope ps(ctx, "loss", 0.0, g->N * 60.0 + g->S * 80.0 + g->E * 24.0);
-  k_loss<<<1, 1024, 0, ctx->stream>>>(a, ctx->d_loss);
+  launch_k(ctx, k_loss, 1, 1024, 0, ctx->stream, a, ctx->d_loss);
   check_launch(ctx);
   if (g->N > 0) {
     float *seedF = ctx->getf("seedF", 3 * g->N);
-    k_seed_atom<<<ceil_div(g->N, 128), 128, 0, ctx->stream>>>(a, ctx->d_loss, seeds.d_eatom, seeds.d_M9, seeds.d_mag,
+    launch_k(ctx, k_seed_atom, ceil_div(g->N, 128), 128, 0, ctx->stream, a, ctx->d_loss, seeds.d_eatom, seeds.d_M9, seeds.d_mag,
                                                               seedF);
     check_launch(ctx);
     if (g->E > 0) {
-      k_seed_edge<<<ceil_div(g->E, 256), 256, 0, ctx->stream>>>(g->E, g->center, g->vec, seedF, seeds.d_ne);
+      launch_k(ctx, k_seed_edge, ceil_div(g->E, 256), 256, 0, ctx->stream, g->E, g->center, g->vec, seedF, seeds.d_ne);
       check_launch(ctx);
     }
   }
@@ -709,7 +738,7 @@ void loss_and_seeds(chg_ctx *ctx, const chg_graph *g, const float *epa, const fl
 void transpose_params(chg_ctx *ctx, const chg_model *m, float *wt) {
   if (m->n2d <= 0) return;
   ProfScope ps(ctx, "transpose", 0.0, 8.0 * m->P);
-  k_transpose<<<dim3(64, m->n2d), 256, 0, ctx->stream>>>(m->d_toff, m->d_trc, m->params, wt);   // <= 16384 per tensor
+  launch_k(ctx, k_transpose, dim3(64, m->n2d), 256, 0, ctx->stream, m->d_toff, m->d_trc, m->params, wt);   // <= 16384 per tensor
   check_launch(ctx);
 }
 
@@ -720,7 +749,7 @@ void fill_zero(chg_ctx *ctx, void *p, size_t bytes) {
 void embed_fwd(chg_ctx *ctx, int64_t N, const int32_t *species, const float *W, float *v) {
   if (N <= 0) return;
   ProfScope ps(ctx, "embed", 0.0, N * 260.0);
-  k_embed<<<ceil_div(N * 16, 256), 256, 0, ctx->stream>>>(N, species, W, v);
+  launch_k(ctx, k_embed, ceil_div(N * 16, 256), 256, 0, ctx->stream, N, species, W, v);
   check_launch(ctx);
 }
 
@@ -732,14 +761,14 @@ int finite_adam(chg_ctx *ctx, int64_t n, float *p, float *g, float *m, float *v,
   {
     ProfScope ps(ctx, "adam", 0.0, 4.0 * n);
     CUDA_OK(cudaMemsetAsync(bad, 0x7f, 4, ctx->stream));   // 0x7f7f7f7f means none
-    k_finite<<<ceil_div(n, 256), 256, 0, ctx->stream>>>(n, g, bad);
+    launch_k(ctx, k_finite, ceil_div(n, 256), 256, 0, ctx->stream, n, g, bad);
     check_launch(ctx);
   }
   {
     const float step_size = (float)(lr / bc1);
     const float inv_sqrt_bc2 = (float)(1.0 / std::sqrt(bc2));
     ProfScope ps(ctx, "adam", 0.0, 28.0 * n);
-    k_adam<<<ceil_div(n, 256), 256, 0, ctx->stream>>>(n, p, g, m, v, lr, b1, b2, eps, step_size, inv_sqrt_bc2, bad);
+    launch_k(ctx, k_adam, ceil_div(n, 256), 256, 0, ctx->stream, n, p, g, m, v, lr, b1, b2, eps, step_size, inv_sqrt_bc2, bad);
     check_launch(ctx);
   }
   int *h = (int *)ctx->pinned_get(64);

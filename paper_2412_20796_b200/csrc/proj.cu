@@ -45,6 +45,7 @@ struct ProjFwd {
 // KIND 0: radial (sRBF with envelope), 1: angle (Fourier)
 template <int NC, int KIND>
 __global__ void __launch_bounds__(256) k_proj_fwd(const __grid_constant__ ProjFwd a) {
+  pdl_begin();
   __shared__ float sW[32][NC * 64];
   __shared__ float sB[PT][PBP];
   const int t = threadIdx.x;
@@ -165,6 +166,7 @@ constexpr int PTB = 32;           // rows per backward tile (static smem < 48 KB
 
 template <int NC, bool RADIAL>
 __global__ void __launch_bounds__(256) k_proj_bwd(const __grid_constant__ ProjBwd a) {
+  pdl_begin();
   constexpr int C = NC * 64;
   __shared__ float sB[PTB][PBP];
   __shared__ float sG[RADIAL ? PTB : 1][PBP];
@@ -247,6 +249,7 @@ __global__ void __launch_bounds__(256) k_proj_bwd(const __grid_constant__ ProjBw
 // splits of the CTA range, combined in order, then a fixed-order tree over c
 __global__ void __launch_bounds__(1024) k_proj_reduce_f(const double *__restrict__ partH, int nctas, int C,
                                                         const float *W0, const float *W1, float *dfreq) {
+  pdl_begin();
   __shared__ double sh[1024];
   const int n = blockIdx.x, t = threadIdx.x, c = t % C, sp = t / C, nsp = 1024 / C;
   double h = 0.0;
@@ -290,8 +293,8 @@ void proj_radial_fwd(chg_ctx *ctx, int64_t rows, const double4 *vec, const int32
   const int grid = (int)std::min<int64_t>((rows + PT - 1) / PT, 4 * sm_count_p());
   ProfScope ps(ctx, "proj_basis", 2.0 * rows * CHG_K * 64 * nc,
                rows * (32.0 + (eor ? 4 : 0) + 128.0 * (dbdf ? 2 : 1) + 256.0 * nc));
-  if (nc == 2) k_proj_fwd<2, 0><<<grid, 256, 0, ctx->stream>>>(a);
-  else k_proj_fwd<1, 0><<<grid, 256, 0, ctx->stream>>>(a);
+  if (nc == 2) launch_k(ctx, k_proj_fwd<2, 0>, grid, 256, 0, ctx->stream, a);
+  else launch_k(ctx, k_proj_fwd<1, 0>, grid, 256, 0, ctx->stream, a);
   check_launch(ctx);
 }
 
@@ -302,7 +305,7 @@ void proj_angle_fwd(chg_ctx *ctx, int64_t rows, const double4 *vec, const int32_
   a.rows = rows; a.vec = vec; a.e1 = e1; a.e2 = e2; a.W[0] = W; a.out[0] = out; a.basis = basis;
   const int grid = (int)std::min<int64_t>((rows + PT - 1) / PT, 4 * sm_count_p());
   ProfScope ps(ctx, "proj_basis", 2.0 * rows * CHG_K * 64, rows * (8.0 + 64.0 + 128.0 + 256.0));
-  k_proj_fwd<1, 1><<<grid, 256, 0, ctx->stream>>>(a);
+  launch_k(ctx, k_proj_fwd<1, 1>, grid, 256, 0, ctx->stream, a);
   check_launch(ctx);
 }
 
@@ -319,9 +322,9 @@ void proj_bwd(chg_ctx *ctx, int64_t rows, const float *basis, const float *dbdf,
   {
     ProfScope ps(ctx, "proj_bwd", 2.0 * rows * CHG_K * C * (radial ? 2 : 1),
                  rows * (128.0 * (radial ? 2 : 1) + 256.0 * nc) + grid * 32.0 * C * (radial ? 12 : 4));
-    if (nc == 2 && radial) k_proj_bwd<2, true><<<grid, 256, 0, ctx->stream>>>(a);
-    else if (nc == 1 && radial) k_proj_bwd<1, true><<<grid, 256, 0, ctx->stream>>>(a);
-    else if (nc == 1) k_proj_bwd<1, false><<<grid, 256, 0, ctx->stream>>>(a);
+    if (nc == 2 && radial) launch_k(ctx, k_proj_bwd<2, true>, grid, 256, 0, ctx->stream, a);
+    else if (nc == 1 && radial) launch_k(ctx, k_proj_bwd<1, true>, grid, 256, 0, ctx->stream, a);
+    else if (nc == 1) launch_k(ctx, k_proj_bwd<1, false>, grid, 256, 0, ctx->stream, a);
     else CHG_THROW(CHG_ERR_ARG, "proj_bwd: unsupported shape");
     check_launch(ctx);
   }
@@ -331,7 +334,7 @@ void proj_bwd(chg_ctx *ctx, int64_t rows, const float *basis, const float *dbdf,
   red_push(ctx, j);
   if (radial) {
     ProfScope ps(ctx, "proj_reduce", 0.0, grid * 32.0 * C * 8);
-    k_proj_reduce_f<<<CHG_K, 1024, 0, ctx->stream>>>(a.partH, grid, C, W0, W1, dfreq);
+    launch_k(ctx, k_proj_reduce_f, CHG_K, 1024, 0, ctx->stream, a.partH, grid, C, W0, W1, dfreq);
     check_launch(ctx);
   }
 }

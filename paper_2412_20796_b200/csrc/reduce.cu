@@ -45,6 +45,7 @@ __device__ __forceinline__ float *red_dst(const RedJob &J, int idx) {
 // hundreds of splits: LayerNorm / bias / head partials) get many groups instead of one
 // long serial chain per lane.
 __global__ void __launch_bounds__(256) k_reduce_all(const __grid_constant__ RedBatch B) {
+  pdl_begin();
   __shared__ float4 sh[256];
   __shared__ int sj;
   if (threadIdx.x == 0) {
@@ -137,7 +138,7 @@ void red_flush(chg_ctx *ctx) {
       bytes += 4.0 * B.j[k].n * (B.j[k].splits + 2.0);
     }
     ProfScope ps(ctx, "reduce_all", 0.0, bytes);
-    k_reduce_all<<<blocks, 256, 0, ctx->stream>>>(B);
+    launch_k(ctx, k_reduce_all, blocks, 256, 0, ctx->stream, B);
     check_launch(ctx);
   }
   ctx->red_jobs.clear();

@@ -196,6 +196,7 @@ struct PackJob {
   int nkc;
 };
 __global__ void k_pack_all(const PackJob *__restrict__ jobs) {
+  pdl_begin();
   const PackJob &J = jobs[blockIdx.y];
   const int per = J.P.ntot * KC, total = J.nkc * per;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
@@ -205,6 +206,7 @@ __global__ void k_pack_all(const PackJob *__restrict__ jobs) {
 }
 
 __global__ void k_pack_b(const RowGemm g, const TcPlan P, uint32_t *__restrict__ img) {
+  pdl_begin();
   int kc = blockIdx.y;
   int idx = blockIdx.x * blockDim.x + threadIdx.x;   // over NT * KC
   if (idx >= P.ntot * KC) return;
@@ -352,6 +354,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  pdl_begin();                                    // the setup above overlaps the predecessor's tail
   const uint32_t tmem = *tslot;
   if ((skip & 32) && tid == 0) {
     uint64_t t;
@@ -857,6 +860,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  pdl_begin();                                    // the setup above overlaps the predecessor's tail
   const uint32_t tmem = *tslot;
 
   if (warp < WG_NPW) {
@@ -1041,7 +1045,7 @@ void tc_repack_all(chg_ctx *ctx, chg_model *m) {
   double bytes = 0;
   for (auto &J : c->jobs) bytes += (double)J.nkc * J.P.ntot * KC * 8.0;
   ProfScope ps(ctx, "tc_pack", 0.0, bytes);
-  k_pack_all<<<dim3(32, (unsigned)c->jobs.size()), 256, 0, ctx->stream>>>(c->d_jobs);
+  launch_k(ctx, k_pack_all, dim3(32, (unsigned)c->jobs.size()), 256, 0, ctx->stream, c->d_jobs);
   check_launch(ctx);
   for (auto &g : c->gen) g = c->cur_gen;
 }
@@ -1254,7 +1258,7 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
     }
     ProfScope ps(ctx, "tc_pack", 0.0, (double)nkc * P.ntot * KC * 8.0);
     dim3 grid(ceil_div((int64_t)P.ntot * KC, 256), nkc);
-    k_pack_b<<<grid, 256, 0, ctx->stream>>>(g, P, img);
+    launch_k(ctx, k_pack_b, grid, 256, 0, ctx->stream, g, P, img);
     check_launch(ctx);
   }
   const int ntiles = ceil_div(g.M, TCM);
@@ -1308,7 +1312,7 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
             g.tag ? g.tag : "?", g.M, g.K, g.A.nseg, TM.use_g[0], TM.use_g[1], TM.use_g[2], TM.use_g[3], TM.use[0],
             TM.use[1], TM.use[2], TM.use[3], P.nsa, P.bres,
             TM.tstore, TM.nst, nbuf, P.noconv, smem);
-  k_rowgemm_tc<<<grid, WS_THREADS, smem, ctx->stream>>>(g, P, img, ntiles, skip, TM);
+  launch_k(ctx, k_rowgemm_tc, grid, WS_THREADS, smem, ctx->stream, g, P, img, ntiles, skip, TM);
   check_launch(ctx);
   return true;
 }
@@ -1353,7 +1357,7 @@ bool wgrad_tc(chg_ctx *ctx, const WGrad &g, float **partial_out, int *Kp_out, in
   static int skip = getenv("CHG_TC_SKIP") ? atoi(getenv("CHG_TC_SKIP")) : 0;
   ProfScope ps(ctx, g.tag ? g.tag : "wgrad_tc", 2.0 * g.M * (double)P.Kp * g.N,
                gemm_a_bytes(g.A, g.M, 0, g.K) + (double)g.M * (4.0 * g.N + (g.didx ? 4.0 : 0.0)) + 4.0 * P.Kp * g.N);
-  k_wgrad_tc<<<splits, WG_THREADS, smem, ctx->stream>>>(g, P, partial, skip);
+  launch_k(ctx, k_wgrad_tc, splits, WG_THREADS, smem, ctx->stream, g, P, partial, skip);
   check_launch(ctx);
   *partial_out = partial;
   *Kp_out = P.Kp;
