@@ -14,7 +14,7 @@ from typing import Dict, Optional, Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libchg.so")
+LIB_PATH = os.environ.get("CHG_LIB_PATH") or os.path.join(_PKG, "libchg.so")   # override: A/B timing builds
 
 CHG_OK = 0
 STATUS = {0: "CHG_OK", 1: "CHG_ERR_ARG", 2: "CHG_ERR_GEOMETRY", 3: "CHG_ERR_SPECIES", 4: "CHG_ERR_CAPACITY",

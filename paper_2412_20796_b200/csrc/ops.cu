@@ -157,14 +157,37 @@ static int seg_split(int64_t mean, int64_t targets) {
 // ---------------------------------------------------------------------------
 struct SegArgs { SegSrc s[3]; int n; };
 
+// rows [r0, r1) of S (through S.perm) added in order into acc (lane hl = float4 column quad of a
+// 256-B row): row indices are fetched 16 at a time (coalesced) and broadcast by shuffle; U rows
+// are in flight per lane (all loads of a group issued, predicated, before the in-order adds)
+template <int U>
+__device__ __forceinline__ void seg_rows(const SegSrc &S, int r0, int r1, int hl, unsigned hmask, float4 &acc) {
+  const float4 *in = (const float4 *)S.in + hl;
+  for (int base = r0; base < r1; base += 16) {
+    const int n = min(16, r1 - base);
+    const int myrow = hl < n ? (S.perm ? __ldg(S.perm + base + hl) : base + hl) : 0;
+    for (int q = 0; q < n; q += U) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int qq = __shfl_sync(hmask, myrow, (q + u) & 15, 16);
+        v[u] = (q + u < n) ? __ldg(in + (int64_t)qq * 16) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (q + u < n) { acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w; }
+    }
+  }
+}
+
 // half-warp per target, one float4 (4 columns) per lane: a 256-B row is one
 // 16-lane load.  Row indices are fetched 16 at a time (coalesced) and broadcast by
-// shuffle; four rows are in flight per lane.  Rows are added in segment order, so
-// the result is deterministic.
+// shuffle; 4 or 8 rows are in flight per lane (seg_rows).  Rows are added in segment order,
+// so the result is deterministic.
 // H half-warps per target (H = 1, 2, 4, 8; long segments): half-warp j sums the fixed j-th
 // contiguous part of every source segment, the H partials are added in j order through shared
 // memory — the split points depend only on the segment length, so the result is deterministic.
-template <int H>
+template <int H, int U>
 __global__ void __launch_bounds__(256) k_segsum(int64_t targets, float *__restrict__ out, int ldo, int accumulate,
                                                 SegArgs a) {
   pdl_begin();
@@ -188,27 +211,7 @@ __global__ void __launch_bounds__(256) k_segsum(int64_t targets, float *__restri
         const int a0 = r0 + (int)((int64_t)len * j / H), a1 = r0 + (int)((int64_t)len * (j + 1) / H);
         r0 = a0; r1 = a1;
       }
-      const float4 *in = (const float4 *)S.in + hl;
-      for (int base = r0; base < r1; base += 16) {
-        const int n = min(16, r1 - base);
-        const int myrow = hl < n ? (S.perm ? __ldg(S.perm + base + hl) : base + hl) : 0;
-        int q = 0;
-        for (; q + 4 <= n; q += 4) {
-          const int q0 = __shfl_sync(hmask, myrow, q, 16), q1 = __shfl_sync(hmask, myrow, q + 1, 16);
-          const int q2 = __shfl_sync(hmask, myrow, q + 2, 16), q3 = __shfl_sync(hmask, myrow, q + 3, 16);
-          const float4 v0 = __ldg(in + (int64_t)q0 * 16), v1 = __ldg(in + (int64_t)q1 * 16);
-          const float4 v2 = __ldg(in + (int64_t)q2 * 16), v3 = __ldg(in + (int64_t)q3 * 16);
-          acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
-          acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w;
-          acc.x += v2.x; acc.y += v2.y; acc.z += v2.z; acc.w += v2.w;
-          acc.x += v3.x; acc.y += v3.y; acc.z += v3.z; acc.w += v3.w;
-        }
-        for (; q < n; ++q) {
-          const int qq = __shfl_sync(hmask, myrow, q, 16);
-          const float4 v = __ldg(in + (int64_t)qq * 16);
-          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-        }
-      }
+      seg_rows<U>(S, r0, r1, hl, hmask, acc);
     }
   }
   if (H > 1) {
@@ -231,7 +234,7 @@ __global__ void __launch_bounds__(256) k_segsum(int64_t targets, float *__restri
 // Segmented sum fused with the 64x64 output linear that consumes it (Eq. 4 𝓛_v, Eq. 5 𝓛_e):
 // agg_t = Σ rows (as k_segsum<H>, stored for the backward), out_t = (agg_t·W + b) + resid_t.
 // W sits in shared memory; the half-warp holding agg_t broadcasts its 64 values by shuffle.
-template <int H>
+template <int H, int U>
 __global__ void __launch_bounds__(256) k_segsum_linear(int64_t targets, SegArgs a, float *__restrict__ agg,
                                                        const float *__restrict__ W, const float *__restrict__ bias,
                                                        const float *__restrict__ resid, float *__restrict__ out) {
@@ -257,27 +260,7 @@ __global__ void __launch_bounds__(256) k_segsum_linear(int64_t targets, SegArgs 
         const int a0 = r0 + (int)((int64_t)len * j / H), a1 = r0 + (int)((int64_t)len * (j + 1) / H);
         r0 = a0; r1 = a1;
       }
-      const float4 *in = (const float4 *)S.in + hl;
-      for (int base = r0; base < r1; base += 16) {
-        const int n = min(16, r1 - base);
-        const int myrow = hl < n ? (S.perm ? __ldg(S.perm + base + hl) : base + hl) : 0;
-        int q = 0;
-        for (; q + 4 <= n; q += 4) {
-          const int q0 = __shfl_sync(hmask, myrow, q, 16), q1 = __shfl_sync(hmask, myrow, q + 1, 16);
-          const int q2 = __shfl_sync(hmask, myrow, q + 2, 16), q3 = __shfl_sync(hmask, myrow, q + 3, 16);
-          const float4 v0 = __ldg(in + (int64_t)q0 * 16), v1 = __ldg(in + (int64_t)q1 * 16);
-          const float4 v2 = __ldg(in + (int64_t)q2 * 16), v3 = __ldg(in + (int64_t)q3 * 16);
-          acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
-          acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w;
-          acc.x += v2.x; acc.y += v2.y; acc.z += v2.z; acc.w += v2.w;
-          acc.x += v3.x; acc.y += v3.y; acc.z += v3.z; acc.w += v3.w;
-        }
-        for (; q < n; ++q) {
-          const int qq = __shfl_sync(hmask, myrow, q, 16);
-          const float4 v = __ldg(in + (int64_t)qq * 16);
-          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-        }
-      }
+      seg_rows<U>(S, r0, r1, hl, hmask, acc);
     }
   }
   // W_out is staged after the gather loop (its load latency overlaps the row loads)
@@ -617,11 +600,14 @@ void segsum(chg_ctx *ctx, int64_t targets, float *out, int ldo, int accumulate, 
   const int H = seg_split(mean, targets);
   ProfScope ps(ctx, tag, 0.0, bytes);
   const int grid = ceil_div(targets * 16 * H, 256);
+  // 8 rows in flight per lane on long segments; 4 on short ones (fewer registers, more warps)
+  auto go = [&](auto kern) { launch_k(ctx, kern, grid, 256, 0, ctx->stream, targets, out, ldo, accumulate, a); };
+  const bool deep = mean >= 16;
   switch (H) {
-    case 8: launch_k(ctx, k_segsum<8>, grid, 256, 0, ctx->stream, targets, out, ldo, accumulate, a); break;
-    case 4: launch_k(ctx, k_segsum<4>, grid, 256, 0, ctx->stream, targets, out, ldo, accumulate, a); break;
-    case 2: launch_k(ctx, k_segsum<2>, grid, 256, 0, ctx->stream, targets, out, ldo, accumulate, a); break;
-    default: launch_k(ctx, k_segsum<1>, grid, 256, 0, ctx->stream, targets, out, ldo, accumulate, a); break;
+    case 8: deep ? go(k_segsum<8, 8>) : go(k_segsum<8, 4>); break;
+    case 4: deep ? go(k_segsum<4, 8>) : go(k_segsum<4, 4>); break;
+    case 2: deep ? go(k_segsum<2, 8>) : go(k_segsum<2, 4>); break;
+    default: deep ? go(k_segsum<1, 8>) : go(k_segsum<1, 4>); break;
   }
   check_launch(ctx);
 }
@@ -643,11 +629,13 @@ void segsum_linear(chg_ctx *ctx, int64_t targets, int nsrc, const SegSrc *src, f
   const int H = seg_split(mean, targets);
   ProfScope ps(ctx, tag, 2.0 * targets * 64 * 64, bytes);
   const int grid = ceil_div(targets * 16 * H, 256);
+  auto go = [&](auto kern) { launch_k(ctx, kern, grid, 256, 0, ctx->stream, targets, a, agg, W, bias, resid, out); };
+  const bool deep = mean >= 16;
   switch (H) {
-    case 8: launch_k(ctx, k_segsum_linear<8>, grid, 256, 0, ctx->stream, targets, a, agg, W, bias, resid, out); break;
-    case 4: launch_k(ctx, k_segsum_linear<4>, grid, 256, 0, ctx->stream, targets, a, agg, W, bias, resid, out); break;
-    case 2: launch_k(ctx, k_segsum_linear<2>, grid, 256, 0, ctx->stream, targets, a, agg, W, bias, resid, out); break;
-    default: launch_k(ctx, k_segsum_linear<1>, grid, 256, 0, ctx->stream, targets, a, agg, W, bias, resid, out); break;
+    case 8: deep ? go(k_segsum_linear<8, 8>) : go(k_segsum_linear<8, 4>); break;
+    case 4: deep ? go(k_segsum_linear<4, 8>) : go(k_segsum_linear<4, 4>); break;
+    case 2: deep ? go(k_segsum_linear<2, 8>) : go(k_segsum_linear<2, 4>); break;
+    default: deep ? go(k_segsum_linear<1, 8>) : go(k_segsum_linear<1, 4>); break;
   }
   check_launch(ctx);
 }
