@@ -41,6 +41,7 @@ void on_side(chg_ctx *ctx, Fn &&f) {
   cudaStream_t main_stream = ctx->stream;
   CUDA_OK(cudaEventRecord(ctx->ev_fork, main_stream));
   CUDA_OK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+  ctx->forked = true;
   ctx->stream = ctx->side;
   try {
     f();
@@ -53,6 +54,7 @@ void on_side(chg_ctx *ctx, Fn &&f) {
 }
 void join_side(chg_ctx *ctx) {
   if (ctx->concurrent()) CUDA_OK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+  ctx->forked = false;
 }
 
 // --- Atom Conv (Eq. 4) ------------------------------------------------------
@@ -222,6 +224,7 @@ void forward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, int train, chg_pred 
     cudaStream_t main_stream = ctx->stream;
     CUDA_OK(cudaEventRecord(ctx->ev_fork, main_stream));
     CUDA_OK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+    ctx->forked = true;
     ctx->stream = ctx->side;
     try {
       bond_conv_fwd(F, t, ab, v[t], e[t], a[t], eb, e[t + 1], ab ? a[t + 1] : nullptr);
@@ -233,6 +236,7 @@ void forward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, int train, chg_pred 
     CUDA_OK(cudaEventRecord(ctx->ev_join, ctx->side));
     atom_conv_fwd(F, t, v[t], e[t], ea, v[t + 1]);
     CUDA_OK(cudaStreamWaitEvent(main_stream, ctx->ev_join, 0));
+    ctx->forked = false;
   }
   v[T + 1] = F.buf("v" + std::to_string(T + 1), N, 64);
   // A6 heads: the force head reads e^T only, so it runs beside the final atom conv
@@ -620,6 +624,7 @@ static void backward_core(chg_ctx *ctx, chg_model *m, chg_graph *g, const LossSe
       cudaStream_t main_stream = ctx->stream;
       CUDA_OK(cudaEventRecord(ctx->ev_fork, main_stream));
       CUDA_OK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+      ctx->forked = true;
       ctx->stream = ctx->side;
       try {
         bc_bwd_body(Bw, t, ab, V(t), Ef(t), Af(t), eb, daggb, dv, de, da, deb, 1);
@@ -631,6 +636,7 @@ static void backward_core(chg_ctx *ctx, chg_model *m, chg_graph *g, const LossSe
       CUDA_OK(cudaEventRecord(ctx->ev_join, ctx->side));
       ac_bwd_body(Bw, t, V(t), Ef(t), ea, dagg, dv, de, dea);
       CUDA_OK(cudaStreamWaitEvent(main_stream, ctx->ev_join, 0));
+      ctx->forked = false;
     }
     bc_bwd_body(Bw, t, ab, V(t), Ef(t), Af(t), eb, daggb, dv, de, da, deb, 2);
     red_flush(ctx);
