@@ -42,13 +42,22 @@ __device__ __forceinline__ float loadA1(const AOp &A, int m, int col) {
   return v;
 }
 
-__device__ __forceinline__ float loadW(const Chunk &c, int k, int n) {
-  if (n >= c.ncols) return 0.f;
+
+// W(k, n..n+3) as one 16-B load when aligned (else per element; zeros past ncols)
+__device__ __forceinline__ float4 loadW4(const Chunk &c, int k, int n) {
 #pragma unroll
   for (int b = 0; b < 4; ++b)
-    if (b < c.nwb && k >= c.wk0[b] && k < c.wk0[b + 1])
-      return __ldg(c.W[b] + (size_t)(k - c.wk0[b]) * c.ldw[b] + n);
-  return 0.f;
+    if (b < c.nwb && k >= c.wk0[b] && k < c.wk0[b + 1]) {
+      const float *p = c.W[b] + (size_t)(k - c.wk0[b]) * c.ldw[b] + n;
+      if (n + 3 < c.ncols && ((uintptr_t)p & 15) == 0) return __ldg((const float4 *)p);
+      float4 v;
+      v.x = n < c.ncols ? __ldg(p) : 0.f;
+      v.y = n + 1 < c.ncols ? __ldg(p + 1) : 0.f;
+      v.z = n + 2 < c.ncols ? __ldg(p + 2) : 0.f;
+      v.w = n + 3 < c.ncols ? __ldg(p + 3) : 0.f;
+      return v;
+    }
+  return make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 // TM rows per CTA (128 for large M; 32 when few CTAs would be launched),
@@ -89,10 +98,10 @@ __global__ void __launch_bounds__(256) k_rowgemm(const __grid_constant__ RowGemm
       }
     }
 #pragma unroll
-    for (int i = 0; i < (TK * TN) / 256; ++i) {
-      int e = t + 256 * i, kr = e / TN, n = e % TN;
-      int k = k0 + kr;
-      Ws[kr][n] = (k < g.K) ? loadW(c, k, n) : 0.f;
+    for (int i = 0; i < (TK * TN) / 1024; ++i) {       // independent 16-B weight loads (one latency)
+      const int e = t + 256 * i, kr = e / (TN / 4), n = (e % (TN / 4)) * 4;
+      const int k = k0 + kr;
+      *(float4 *)&Ws[kr][n] = (k < g.K) ? loadW4(c, k, n) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     __syncthreads();
 #pragma unroll 8

@@ -62,6 +62,7 @@ __device__ void load_weights(const float *__restrict__ P, float *sm) {
   using S = HeadSmem<NL, NOUT>;
   for (int l = 0; l < NL - 1; ++l) {
     const float *Wg = P + l * (64 * 64 + 64);
+    #pragma unroll 8   // independent loads in flight (one latency, not one per iteration)
     for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) sm[S::W + l * 64 * HP + (i / 64) * HP + (i % 64)] = Wg[i];
     for (int i = threadIdx.x; i < 64; i += blockDim.x) sm[S::B + l * 64 + i] = Wg[64 * 64 + i];
   }
@@ -72,6 +73,7 @@ __device__ void load_weights(const float *__restrict__ P, float *sm) {
 
 // load a [64][64] row tile of a [rows, 64] matrix into smem [64][HP] (zero rows past the end)
 __device__ __forceinline__ void load_tile(const float *__restrict__ src, int64_t r0, int64_t rows, float *dst) {
+  #pragma unroll 8   // independent loads in flight (one latency, not one per iteration)
   for (int i = threadIdx.x; i < HT * 16; i += blockDim.x) {
     const int r = i >> 4, c4 = (i & 15) * 4;
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
