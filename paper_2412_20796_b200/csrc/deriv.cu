@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(256) k_dgeom_radial(int64_t rows, const double
   pdl_begin();
   __shared__ float Wt[NC * 64][33];
   __shared__ float rowbuf[8][NC * 64];
-  #pragma unroll 8   // independent loads in flight (one latency, not one per iteration)
+#pragma unroll 8   // independent loads in flight (one latency, not one per iteration)
   for (int i = threadIdx.x; i < NC * 64 * 32; i += blockDim.x) {
     const int c = i / 32, n = i % 32;
     Wt[c][n] = n < CHG_K ? (c < 64 ? W0 : W1)[n * 64 + (c & 63)] : 0.f;
@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(256) k_dgeom_angle(int64_t A, const double4 *_
   pdl_begin();
   __shared__ float Wt[64][33];
   __shared__ float rowbuf[8][64];
-  #pragma unroll 8   // independent loads in flight (one latency, not one per iteration)
+#pragma unroll 8   // independent loads in flight (one latency, not one per iteration)
   for (int i = threadIdx.x; i < 64 * 32; i += blockDim.x) {
     const int c = i / 32, n = i % 32;
     Wt[c][n] = n < CHG_K ? Wth[n * 64 + c] : 0.f;

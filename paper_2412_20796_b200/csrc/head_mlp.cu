@@ -22,7 +22,8 @@
 namespace {
 
 constexpr int HT = 64;        // rows per tile
-constexpr int HP = 65;        // smem pitch of [64][64] tiles
+constexpr int HP = 65;        // smem pitch of the forward activation tile (odd: row walks across lanes are conflict-free)
+constexpr int TPB = 68;       // smem pitch of the backward tiles (16-B rows: float4 row reads in the dW loop)
 constexpr int HMAXL = 4;      // max linear layers per head
 
 struct HeadArgs {
@@ -46,24 +47,27 @@ __device__ __forceinline__ float dsilu_(float x) {
   return s * (1.0f + x * (1.0f - s));
 }
 
-// smem layout (floats): W hidden [NL-1][64][HP] | b hidden [NL-1][64] | W last [64][NOUT] | b last [NOUT]
+// smem layout (floats): W hidden [NL-1][64][64] (forward: W[k][n]; backward: transposed W[n][k], so
+// both kernels read 4 consecutive outputs as one float4) | b hidden [NL-1][64] | W last [64][NOUT]
+// | b last [NOUT]
 //                       | tiles ...
 template <int NL, int NOUT>
 struct HeadSmem {
   static constexpr int W = 0;
-  static constexpr int B = W + (NL - 1) * 64 * HP;
+  static constexpr int B = W + (NL - 1) * 64 * 64;
   static constexpr int WL = B + (NL - 1) * 64;
   static constexpr int BL = WL + 64 * NOUT;
   static constexpr int T0 = (BL + NOUT + 3) & ~3;
 };
 
-template <int NL, int NOUT>
+template <int NL, int NOUT, bool TRANS>
 __device__ void load_weights(const float *__restrict__ P, float *sm) {
   using S = HeadSmem<NL, NOUT>;
   for (int l = 0; l < NL - 1; ++l) {
     const float *Wg = P + l * (64 * 64 + 64);
-    #pragma unroll 8   // independent loads in flight (one latency, not one per iteration)
-    for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) sm[S::W + l * 64 * HP + (i / 64) * HP + (i % 64)] = Wg[i];
+#pragma unroll 8   // independent loads in flight (one latency, not one per iteration)
+    for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x)
+      sm[S::W + l * 64 * 64 + (TRANS ? (i % 64) * 64 + i / 64 : i)] = Wg[i];
     for (int i = threadIdx.x; i < 64; i += blockDim.x) sm[S::B + l * 64 + i] = Wg[64 * 64 + i];
   }
   const float *Wl = P + (NL - 1) * (64 * 64 + 64);
@@ -71,14 +75,15 @@ __device__ void load_weights(const float *__restrict__ P, float *sm) {
   for (int i = threadIdx.x; i < NOUT; i += blockDim.x) sm[S::BL + i] = Wl[64 * NOUT + i];
 }
 
-// load a [64][64] row tile of a [rows, 64] matrix into smem [64][HP] (zero rows past the end)
+// load a [64][64] row tile of a [rows, 64] matrix into smem [64][P] (zero rows past the end)
+template <int P>
 __device__ __forceinline__ void load_tile(const float *__restrict__ src, int64_t r0, int64_t rows, float *dst) {
-  #pragma unroll 8   // independent loads in flight (one latency, not one per iteration)
+#pragma unroll 8   // independent loads in flight (one latency, not one per iteration)
   for (int i = threadIdx.x; i < HT * 16; i += blockDim.x) {
     const int r = i >> 4, c4 = (i & 15) * 4;
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     if (r0 + r < rows) v = __ldg((const float4 *)(src + (r0 + r) * 64 + c4));
-    float *d = dst + r * HP + c4;
+    float *d = dst + r * P + c4;
     d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
   }
 }
@@ -89,17 +94,17 @@ __global__ void __launch_bounds__(256) k_head_fwd(const __grid_constant__ HeadAr
   extern __shared__ float sm[];
   using S = HeadSmem<NL, NOUT>;
   float *sH = sm + S::T0;            // [64][HP] layer input / activation
-  load_weights<NL, NOUT>(a.P, sm);
+  load_weights<NL, NOUT, false>(a.P, sm);
   const int t = threadIdx.x, ra = (t >> 4) * 4, cb = (t & 15) * 4;
   const int64_t ntiles = (a.rows + HT - 1) / HT;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t r0 = tile * HT;
     __syncthreads();
-    load_tile(a.X, r0, a.rows, sH);
+    load_tile<HP>(a.X, r0, a.rows, sH);
     __syncthreads();
 #pragma unroll 1
     for (int l = 0; l < NL - 1; ++l) {
-      const float *W = sm + S::W + l * 64 * HP;
+      const float *W = sm + S::W + l * 64 * 64;
       float acc[4][4];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
@@ -110,8 +115,8 @@ __global__ void __launch_bounds__(256) k_head_fwd(const __grid_constant__ HeadAr
         float h[4], w[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) h[i] = sH[(ra + i) * HP + k];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) w[j] = W[k * HP + cb + j];
+        const float4 w4 = *(const float4 *)&W[k * 64 + cb];
+        w[0] = w4.x; w[1] = w4.y; w[2] = w4.z; w[3] = w4.w;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -148,10 +153,10 @@ __global__ void __launch_bounds__(256) k_head_bwd(const __grid_constant__ HeadAr
   extern __shared__ float sm[];
   using S = HeadSmem<NL, NOUT>;
   float *sA = sm + S::T0;            // layer input H_{k-1} (or X)
-  float *sZ = sA + HT * HP;          // pre-activation z_{k-1}
-  float *sG = sZ + HT * HP;          // dZ_k
-  float *sD = sG + HT * HP;          // dout tile [64][NOUT]
-  load_weights<NL, NOUT>(a.P, sm);
+  float *sZ = sA + HT * TPB;         // pre-activation z_{k-1}
+  float *sG = sZ + HT * TPB;         // dZ_k
+  float *sD = sG + HT * TPB;         // dout tile [64][NOUT]
+  load_weights<NL, NOUT, true>(a.P, sm);
   const int t = threadIdx.x, ta = (t >> 4) * 4, tb = (t & 15) * 4;
   constexpr int NH = NL - 1;
   // per-thread accumulators: dW_k[ta..ta+3][tb..tb+3] (k = input row, n = output col), db_k[tb..] (ta == 0)
@@ -177,11 +182,11 @@ __global__ void __launch_bounds__(256) k_head_bwd(const __grid_constant__ HeadAr
       const int r = p / NOUT, o = p % NOUT;
       sD[p] = (r0 + r < a.rows) ? a.dout[(r0 + r) * NOUT + o] : 0.f;
     }
-    load_tile(a.Z[NH - 1], r0, a.rows, sZ);
+    load_tile<TPB>(a.Z[NH - 1], r0, a.rows, sZ);
     __syncthreads();
     for (int i = t; i < HT * 64; i += blockDim.x) {
       const int r = i >> 6, c = i & 63;
-      sA[r * HP + c] = silu_(sZ[r * HP + c]);
+      sA[r * TPB + c] = silu_(sZ[r * TPB + c]);
     }
     __syncthreads();
     // last layer: dW_L[k][o] += Σ_r H[r][k] dout[r][o], db_L[o] += Σ_r dout[r][o]
@@ -191,7 +196,7 @@ __global__ void __launch_bounds__(256) k_head_bwd(const __grid_constant__ HeadAr
       if (p < 64 * NOUT) {
         const int k = p / NOUT, o = p % NOUT;
         float s = 0.f;
-        for (int r = 0; r < HT; ++r) s = fmaf(sA[r * HP + k], sD[r * NOUT + o], s);
+        for (int r = 0; r < HT; ++r) s = fmaf(sA[r * TPB + k], sD[r * NOUT + o], s);
         gWL[q] += s;
       }
     }
@@ -206,21 +211,21 @@ __global__ void __launch_bounds__(256) k_head_bwd(const __grid_constant__ HeadAr
       float s = 0.f;
 #pragma unroll
       for (int o = 0; o < NOUT; ++o) s = fmaf(sD[r * NOUT + o], sm[S::WL + k * NOUT + o], s);
-      sG[r * HP + k] = s * dsilu_(sZ[r * HP + k]);
+      sG[r * TPB + k] = s * dsilu_(sZ[r * TPB + k]);
     }
     __syncthreads();
 #pragma unroll
     for (int l = NH - 1; l >= 0; --l) {   // unrolled: gW[l] stays in registers
       // layer input: H_{l-1} = SiLU(z_{l-1}) (z kept in sZ for the next dZ), or X for l = 0
       if (l > 0) {
-        load_tile(a.Z[l - 1], r0, a.rows, sZ);
+        load_tile<TPB>(a.Z[l - 1], r0, a.rows, sZ);
         __syncthreads();
         for (int i = t; i < HT * 64; i += blockDim.x) {
           const int r = i >> 6, c = i & 63;
-          sA[r * HP + c] = silu_(sZ[r * HP + c]);
+          sA[r * TPB + c] = silu_(sZ[r * TPB + c]);
         }
       } else {
-        load_tile(a.X, r0, a.rows, sA);
+        load_tile<TPB>(a.X, r0, a.rows, sA);
       }
       __syncthreads();
       // dW_l[k][n] += Σ_r A[r][k] G[r][n]; db_l[n] += Σ_r G[r][n]
@@ -233,11 +238,8 @@ __global__ void __launch_bounds__(256) k_head_bwd(const __grid_constant__ HeadAr
         float cs[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 4
         for (int r = 0; r < HT; ++r) {
-          float x[4], gg[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) x[i] = sA[r * HP + ta + i];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) gg[j] = sG[r * HP + tb + j];
+          const float4 x4 = *(const float4 *)&sA[r * TPB + ta], g4 = *(const float4 *)&sG[r * TPB + tb];
+          const float x[4] = {x4.x, x4.y, x4.z, x4.w}, gg[4] = {g4.x, g4.y, g4.z, g4.w};
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -260,14 +262,14 @@ __global__ void __launch_bounds__(256) k_head_bwd(const __grid_constant__ HeadAr
 #pragma unroll
         for (int j = 0; j < 4; ++j) dh[i][j] = 0.f;
       {
-        const float *W = sm + S::W + l * 64 * HP;
+        const float *WT = sm + S::W + l * 64 * 64;     // WT[n][k] = W[k][n]
 #pragma unroll 8
         for (int n = 0; n < 64; ++n) {
-          float gg[4], w[4];
+          float gg[4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) gg[i] = sG[(ta + i) * HP + n];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) w[j] = W[(tb + j) * HP + n];
+          for (int i = 0; i < 4; ++i) gg[i] = sG[(ta + i) * TPB + n];
+          const float4 w4 = *(const float4 *)&WT[n * 64 + tb];
+          const float w[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(256) k_head_bwd(const __grid_constant__ HeadAr
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) sG[(ta + i) * HP + tb + j] = dh[i][j] * dsilu_(sZ[(ta + i) * HP + tb + j]);
+          for (int j = 0; j < 4; ++j) sG[(ta + i) * TPB + tb + j] = dh[i][j] * dsilu_(sZ[(ta + i) * TPB + tb + j]);
       } else {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -317,7 +319,7 @@ __global__ void __launch_bounds__(256) k_head_bwd(const __grid_constant__ HeadAr
 template <int NL, int NOUT>
 size_t head_smem_fwd() { return 4 * ((size_t)HeadSmem<NL, NOUT>::T0 + HT * HP); }
 template <int NL, int NOUT>
-size_t head_smem_bwd() { return 4 * ((size_t)HeadSmem<NL, NOUT>::T0 + 3 * HT * HP + HT * NOUT); }
+size_t head_smem_bwd() { return 4 * ((size_t)HeadSmem<NL, NOUT>::T0 + 3 * HT * TPB + HT * NOUT); }
 
 int sm_count() {
   static int n = 0;

@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(256) k_segsum_linear(int64_t targets, SegArgs 
     }
   }
   // W_out is staged after the gather loop (its load latency overlaps the row loads)
-  #pragma unroll 8   // independent loads in flight (one latency, not one per iteration)
+#pragma unroll 8   // independent loads in flight (one latency, not one per iteration)
   for (int i = threadIdx.x; i < 64 * 64; i += 256) sW[i >> 6][i & 63] = W[i];
   if (H > 1) part[hw][hl] = acc;
   __syncthreads();

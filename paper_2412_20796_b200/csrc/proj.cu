@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(256) k_proj_fwd(const __grid_constant__ ProjFw
   __shared__ float sW[32][NC * 64];
   __shared__ float sB[PT][PBP];
   const int t = threadIdx.x;
-  #pragma unroll 4
+#pragma unroll 4
   for (int i = t; i < 32 * NC * 64; i += 256) {
     const int k = i / (NC * 64), c = i % (NC * 64);
     sW[k][c] = k < CHG_K ? a.W[c >> 6][k * 64 + (c & 63)] : 0.f;
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(256) k_proj_bwd(const __grid_constant__ ProjBw
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t r0 = tile * PTB;
     __syncthreads();
-    #pragma unroll 4
+#pragma unroll 4
     for (int i = t; i < PTB * 8; i += 256) {         // basis (and derivative) tiles: float4 per thread
       const int r = i >> 3, q = (i & 7) * 4;
       float4 b = make_float4(0.f, 0.f, 0.f, 0.f), g = b;
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(256) k_proj_bwd(const __grid_constant__ ProjBw
       sB[r][q] = b.x; sB[r][q + 1] = b.y; sB[r][q + 2] = b.z; sB[r][q + 3] = b.w;
       if (RADIAL) { sG[r][q] = g.x; sG[r][q + 1] = g.y; sG[r][q + 2] = g.z; sG[r][q + 3] = g.w; }
     }
-    #pragma unroll 4
+#pragma unroll 4
     for (int i = t; i < PTB * C / 4; i += 256) {
       const int r = i / (C / 4), c = (i % (C / 4)) * 4;
       float4 d = make_float4(0.f, 0.f, 0.f, 0.f);
