@@ -444,11 +444,33 @@ def main():
             g5.close()
         barrier()
         t6 = sorted(s.elapsed_time(e) for s, e in ev6)
+        # NEXT-2 MD loop: one velocity-Verlet NVE step (kick+drift, graph rebuild, conservative
+        # forces on device, kick), device-timed, for the C5 cell and an 8-atom cell (Table II size)
+        from paper_2412_20796_b200.md import NVE, maxwell_boltzmann
+
+        def md_ms(b, mass):
+            md = NVE(ctx, model5, b.atom_ptr, b.positions, b.lattice, b.species, mass,
+                     maxwell_boltzmann(mass, 300.0, 0), dt_fs=0.5)
+            md.step(a.warmup)
+            evm = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+            barrier()
+            for k in range(a.steps):
+                evm[k][0].record(stream)
+                md.step(1)
+                evm[k][1].record(stream)
+            barrier()
+            tm = sorted(s.elapsed_time(e) for s, e in evm)
+            return tm[len(tm) // 2]
+        b8 = make_config_batch("C1")
         c5 = {"workload": "C5: one 4,096-atom LiFePO4-like cell (graph build + forward + force/stress readout)",
               "atoms": int(b5.n_atoms), "latency_ms_median": t5[len(t5) // 2], "latency_ms_min": t5[0],
               "conservative_latency_ms_median": t6[len(t6) // 2],
               "conservative_note": "chg_forward_conservative: forward + energy-seeded backward + basis derivatives "
-                                   "(includes the host copy of the outputs)"}
+                                   "(includes the host copy of the outputs)",
+              "md_step_ms_median": {"C5_4096_atoms": md_ms(b5, np.full(b5.n_atoms, 30.0)),
+                                    "C1_Si8": md_ms(b8, np.full(b8.n_atoms, 28.0855))},
+              "md_note": "NEXT-2 velocity-Verlet NVE step: chg_md_verlet kick+drift, graph rebuild from device "
+                         "positions, chg_forward_conservative (device outputs), kick; dt 0.5 fs"}
 
     structs = sum(batches[k % len(batches)]["gl"]["S"] for k in range(a.steps))
     value = structs / (ms / 1e3)

@@ -183,6 +183,18 @@ chg_status chg_forward(chg_ctx *ctx, chg_model *m, chg_graph *g, int train, chg_
  * train-mode activations: a following chg_backward needs a new chg_forward (CHG_ERR_STATE). */
 chg_status chg_forward_conservative(chg_ctx *ctx, chg_model *m, chg_graph *g, chg_pred *out);
 
+/* ---- MD inference loop (Table II regime) ----------------
+ * One half of a velocity-Verlet NVE step on device arrays (all DEVICE pointers, enqueued on
+ * the ctx stream; units eV, Å, amu, fs):
+ *   drift = 1:  v += (dt/2)·F/m·c, then r += dt·v     (call before rebuilding the graph)
+ *   drift = 0:  v += (dt/2)·F/m·c                     (call with the new forces)
+ * c = 9.648533212e-3 Å/fs² per eV/(Å·amu).  positions / velocities: fp64 [n,3]; forces: fp32
+ * [n,3] (e.g. chg_forward_conservative with on_device outputs); inv_mass: fp64 [n] (1/amu).
+ * Periodic wrapping is not applied (the graph builder accepts any Cartesian positions).
+ * Errors: CHG_ERR_ARG for null pointers with n > 0. */
+chg_status chg_md_verlet(chg_ctx *ctx, int64_t n_atoms, double *positions, double *velocities, const float *forces,
+                         const double *inv_mass, double dt_fs, int drift);
+
 /* ---- A7-A8 loss + backward (first-order only) ---------
  * Computes the Huber loss of the last train-mode forward and ACCUMULATES
  * dL/dθ into the model's gradient vector.  loss_out (host, optional) =

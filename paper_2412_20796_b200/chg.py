@@ -61,7 +61,7 @@ class AdamCfg(C.Structure):
 # every symbol include/chg.h declares (checked by tests/test_abi_symbols.py)
 SYMBOLS = ["chg_ctx_create", "chg_ctx_destroy", "chg_last_error", "chg_sync", "chg_launch_count",
            "chg_nccl_unique_id", "chg_ctx_set_nccl", "chg_build_graph", "chg_graph_counts", "chg_graph_export",
-           "chg_graph_destroy", "chg_graph_wait", "chg_model_create", "chg_model_destroy", "chg_model_layout",
+           "chg_graph_destroy", "chg_graph_wait", "chg_md_verlet", "chg_model_create", "chg_model_destroy", "chg_model_layout",
            "chg_model_num_params", "chg_model_set", "chg_model_get", "chg_model_device_ptr", "chg_forward",
            "chg_forward_conservative",
            "chg_backward", "chg_step", "chg_balance", "chg_profile", "chg_profile_query", "chg_debug_gemm", "chg_debug_get"]
@@ -91,6 +91,7 @@ def load(path: str = LIB_PATH):
         "chg_graph_export": (C.c_int, [vp] + [vp] * 11),
         "chg_graph_destroy": (None, [vp]),
         "chg_graph_wait": (C.c_int, [vp, vp]),
+        "chg_md_verlet": (C.c_int, [vp, i64, vp, vp, vp, vp, C.c_double, C.c_int]),
         "chg_model_create": (C.c_int, [vp, C.POINTER(ModelCfg), C.POINTER(vp)]),
         "chg_model_destroy": (None, [vp]),
         "chg_model_layout": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.POINTER(C.c_char_p)),
@@ -185,6 +186,13 @@ class Context:
         Context of the same device on its own stream; chg_forward also waits implicitly)."""
         self._check(self.lib.chg_graph_wait(self.h, graph.h))
 
+    def md_verlet(self, positions, velocities, forces, inv_mass, dt_fs: float, drift: bool):
+        """chg_md_verlet: one velocity-Verlet half step on device tensors (fp64 positions /
+        velocities [n,3], fp32 forces [n,3], fp64 inverse masses [n]; eV, Å, amu, fs)."""
+        n = int(positions.shape[0])
+        self._check(self.lib.chg_md_verlet(self.h, n, _ptr(positions), _ptr(velocities), _ptr(forces), _ptr(inv_mass),
+                                           float(dt_fs), int(bool(drift))))
+
     def build_graph(self, atom_ptr, positions, lattice, species, r_atom: float = 5.0, r_bond: float = 3.0) -> "Graph":
         ap = np.ascontiguousarray(np.asarray(atom_ptr, np.int64))
         dev = _on_device(positions)
@@ -218,9 +226,14 @@ class Context:
             self._check(self.lib.chg_forward(self.h, model.h, graph.h, int(train), None))
         return None
 
-    def forward_conservative(self, model: "Model", graph: "Graph") -> Dict[str, np.ndarray]:
+    def forward_conservative(self, model: "Model", graph: "Graph", out: Optional[Dict] = None):
         """chg_forward_conservative: energy-head forces F = -dE/dr and stress (160.2/V) dE/deps
-        (the reference-CHGNet output) plus energy / magmom, as numpy arrays."""
+        (the reference-CHGNet output) plus energy / magmom, as numpy arrays — or written into
+        `out` (dict of device tensors, nothing returned)."""
+        if out is not None:
+            p = Pred(*(_ptr(out.get(k)) for k in ("energy", "energy_per_atom", "forces", "stress", "magmom")), 1)
+            self._check(self.lib.chg_forward_conservative(self.h, model.h, graph.h, C.byref(p)))
+            return None
         N, E, B, A = graph.counts()
         S = graph.n_struct
         res = {"energy": np.zeros(S, np.float32), "energy_per_atom": np.zeros(S, np.float32),

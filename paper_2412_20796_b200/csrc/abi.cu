@@ -18,6 +18,8 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
                    const chg_loss_cfg *cfg, double *loss_out);
 void step_impl(chg_ctx *ctx, chg_model *m, const chg_adam_cfg *cfg);
 void derivative_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, chg_pred *out);
+void md_verlet(chg_ctx *ctx, int64_t n, double *pos, double *vel, const float *F, const double *inv_mass, double dt,
+               int drift);
 
 // ---------------------------------------------------------------------------
 // ctx helpers
@@ -401,6 +403,15 @@ chg_status chg_forward_conservative(chg_ctx *ctx, chg_model *m, chg_graph *g, ch
     CUDA_OK(cudaSetDevice(ctx->device));
     graph_use(ctx, g);
     derivative_impl(ctx, m, g, out);
+  });
+}
+
+chg_status chg_md_verlet(chg_ctx *ctx, int64_t n_atoms, double *positions, double *velocities, const float *forces,
+                         const double *inv_mass, double dt_fs, int drift) {
+  if (!ctx || n_atoms < 0 || (n_atoms > 0 && (!positions || !velocities || !forces || !inv_mass))) return CHG_ERR_ARG;
+  ABI_GUARD(ctx, {
+    CUDA_OK(cudaSetDevice(ctx->device));
+    md_verlet(ctx, n_atoms, positions, velocities, forces, inv_mass, dt_fs, drift);
   });
 }
 

@@ -65,6 +65,9 @@ void deriv_geometry(chg_ctx *ctx, const chg_graph *g, const float *freq_a, const
                     const float *W0, const float *Wa, const float *Wb, const float *Wth, const float *de,
                     const float *dea, const float *deb, const float *da, float *forces, float *stress);
 void fill_value(chg_ctx *ctx, float *x, int64_t n, float v);
+// md.cu: velocity-Verlet half step (chg_md_verlet)
+void md_verlet(chg_ctx *ctx, int64_t n, double *pos, double *vel, const float *F, const double *inv_mass, double dt,
+               int drift);
 
 // heads (Eq. 7, Eq. 9)
 void heads_forces(chg_ctx *ctx, const chg_graph *g, const float *n_e, float *forces);
