@@ -17,41 +17,50 @@ __device__ __forceinline__ RowStats ln_stats(float a, float b) {
   return {mu, rsqrtf(var + 1e-5f)};
 }
 
-__global__ void k_gate_fwd(int64_t rows, const float *__restrict__ y, int ldy, GateLN ln, int mode,
-                           const float *__restrict__ w, const int32_t *__restrict__ i1, const int32_t *__restrict__ i2,
-                           const float *__restrict__ resid, float *__restrict__ out) {
+__global__ void __launch_bounds__(256, 4) k_gate_fwd(int64_t rows, const float *__restrict__ y, int ldy, GateLN ln,
+                                                  int mode, const float *__restrict__ w,
+                                                  const int32_t *__restrict__ i1, const int32_t *__restrict__ i2,
+                                                  const float *__restrict__ resid, float *__restrict__ out) {
   pdl_begin();
+  const int l = threadIdx.x & 31, c0 = 2 * l;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int l = threadIdx.x & 31;
-  if (row >= rows) return;
-  int c0 = 2 * l;
-  // every operand of the row is requested before any arithmetic (one latency, not three)
-  float2 yc = *(const float2 *)(y + row * ldy + c0);
-  float2 yg = *(const float2 *)(y + row * ldy + 64 + c0);
-  float2 w1 = make_float2(0.f, 0.f), w2 = make_float2(0.f, 0.f);
-  if (mode == GATE_MUL_W) {
-    w1 = *(const float2 *)(w + row * 64 + c0);
-  } else if (mode == GATE_MUL_W1W2) {
-    w1 = *(const float2 *)(w + (int64_t)i1[row] * 64 + c0);
-    w2 = *(const float2 *)(w + (int64_t)i2[row] * 64 + c0);
-  } else {
-    w1 = *(const float2 *)(resid + row * 64 + c0);
+  const float2 gc = *(const float2 *)(ln.gc + c0), bc = *(const float2 *)(ln.bc + c0);
+  const float2 gg = *(const float2 *)(ln.gg + c0), bg = *(const float2 *)(ln.bg + c0);
+  // grid-stride over rows (a warp per row); every operand of the next row is requested before
+  // this row's arithmetic, so two rows' loads are in flight per warp
+  auto load = [&](int64_t r, float2 &yc, float2 &yg, float2 &w1, float2 &w2) {
+    yc = __ldg((const float2 *)(y + r * ldy + c0));
+    yg = __ldg((const float2 *)(y + r * ldy + 64 + c0));
+    w2 = make_float2(0.f, 0.f);
+    if (mode == GATE_MUL_W) {
+      w1 = __ldg((const float2 *)(w + r * 64 + c0));
+    } else if (mode == GATE_MUL_W1W2) {
+      w1 = __ldg((const float2 *)(w + (int64_t)__ldg(i1 + r) * 64 + c0));
+      w2 = __ldg((const float2 *)(w + (int64_t)__ldg(i2 + r) * 64 + c0));
+    } else {
+      w1 = __ldg((const float2 *)(resid + r * 64 + c0));
+    }
+  };
+  float2 nyc, nyg, nw1, nw2;
+  if (row < rows) load(row, nyc, nyg, nw1, nw2);
+  for (; row < rows; row += warps) {
+    const float2 yc = nyc, yg = nyg, w1 = nw1, w2 = nw2;
+    if (row + warps < rows) load(row + warps, nyc, nyg, nw1, nw2);
+    RowStats sc = ln_stats(yc.x, yc.y), sg = ln_stats(yg.x, yg.y);
+    float nc0 = gc.x * (yc.x - sc.mu) * sc.rstd + bc.x, nc1 = gc.y * (yc.y - sc.mu) * sc.rstd + bc.y;
+    float ng0 = gg.x * (yg.x - sg.mu) * sg.rstd + bg.x, ng1 = gg.y * (yg.y - sg.mu) * sg.rstd + bg.y;
+    float p0 = sigmoidf_(ng0) * siluf_(nc0), p1 = sigmoidf_(ng1) * siluf_(nc1);
+    float2 o;
+    if (mode == GATE_MUL_W) {
+      o = make_float2(p0 * w1.x, p1 * w1.y);
+    } else if (mode == GATE_MUL_W1W2) {
+      o = make_float2(p0 * w1.x * w2.x, p1 * w1.y * w2.y);
+    } else {
+      o = make_float2(w1.x + p0, w1.y + p1);
+    }
+    *(float2 *)(out + row * 64 + c0) = o;
   }
-  RowStats sc = ln_stats(yc.x, yc.y), sg = ln_stats(yg.x, yg.y);
-  float2 gc = *(const float2 *)(ln.gc + c0), bc = *(const float2 *)(ln.bc + c0);
-  float2 gg = *(const float2 *)(ln.gg + c0), bg = *(const float2 *)(ln.bg + c0);
-  float nc0 = gc.x * (yc.x - sc.mu) * sc.rstd + bc.x, nc1 = gc.y * (yc.y - sc.mu) * sc.rstd + bc.y;
-  float ng0 = gg.x * (yg.x - sg.mu) * sg.rstd + bg.x, ng1 = gg.y * (yg.y - sg.mu) * sg.rstd + bg.y;
-  float p0 = sigmoidf_(ng0) * siluf_(nc0), p1 = sigmoidf_(ng1) * siluf_(nc1);
-  float2 o;
-  if (mode == GATE_MUL_W) {
-    o = make_float2(p0 * w1.x, p1 * w1.y);
-  } else if (mode == GATE_MUL_W1W2) {
-    o = make_float2(p0 * w1.x * w2.x, p1 * w1.y * w2.y);
-  } else {
-    o = make_float2(w1.x + p0, w1.y + p1);
-  }
-  *(float2 *)(out + row * 64 + c0) = o;
 }
 
 __global__ void __launch_bounds__(256, 4) k_gate_bwd(int64_t rows, int64_t rpb, const float *__restrict__ y, int ldy,
@@ -558,7 +567,8 @@ void gate_fwd(chg_ctx *ctx, int64_t rows, const float *y, int ldy, GateLN ln, in
               const int32_t *i1, const int32_t *i2, const float *resid, float *out) {
   if (rows <= 0) return;
   ProfScope ps(ctx, "gate_fwd", 0.0, rows * (512.0 + 256.0 + (mode == GATE_MUL_W1W2 ? 520.0 : 256.0)));
-  launch_k(ctx, k_gate_fwd, ceil_div(rows * 32, 256), 256, 0, ctx->stream, rows, y, ldy, ln, mode, w, i1, i2, resid, out);
+  const int grid = (int)std::min<int64_t>(ceil_div(rows * 32, 256), 148 * 4);   // persistent: 4 CTAs / SM
+  launch_k(ctx, k_gate_fwd, grid, 256, 0, ctx->stream, rows, y, ldy, ln, mode, w, i1, i2, resid, out);
   check_launch(ctx);
 }
 
