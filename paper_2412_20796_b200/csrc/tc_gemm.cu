@@ -790,10 +790,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
 //   swizzled K-major rows (k or n) at column m — a free transpose, conflict-free.
 //   Stage = 32 rows m: A_T [Kpad rows][128 B], D_T [N rows][128 B], SWIZZLE_128B.
 //   Rows are split across persistent CTAs; each CTA accumulates its k tiles
-//   (M = 128, ≤ 2) × N in TMEM and writes one partial [Kp][N]; partials are
-//   reduced in a fixed order by the batched reduction (reduce.cu).  When K % 128 != 0 a
-//   bias (column sums of D) is summed by the producers from the staged K-major D rows.
-//   Warps 0-11 produce, warp 12 issues MMAs, warps 0-3 run the epilogue.
+//   (M = 128, ≤ 2) × N in TMEM and writes one partial [Kp][N] (TMA bulk stores of 32 x 32
+//   blocks staged in the idle stage buffers); partials are reduced in a fixed order by the
+//   batched reduction (reduce.cu).  The bias (column sums of D) is summed by the producers
+//   from the staged K-major D rows.  Warps 0-11 produce, warp 12 issues MMAs, warps 0-3 run
+//   the epilogue.
 // ---------------------------------------------------------------------------
 constexpr int WG_NST = 3;
 constexpr int WG_NPW = 12;                 // producer warps
@@ -814,7 +815,7 @@ __device__ __forceinline__ uint32_t kmaj_swz(int r, int m) {   // byte offset of
 }
 
 __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constant__ WGrad g, const WgPlan P, float *__restrict__ partial,
-                                                             int skip) {
+                                                             int skip, const __grid_constant__ CUtensorMap pmap) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -824,8 +825,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
   uint64_t *empty = full + WG_NST;
   uint64_t *done = empty + WG_NST;
   uint32_t *tslot = (uint32_t *)(done + 1);
-  float *epi = (float *)(smem + WG_NST * st_bytes + 8 * (2 * WG_NST + 1) + 16);   // [4][32][33]
-  float *sbias = epi + 4 * 32 * 33;                                                 // [WG_NPW][256]
+  float *sbias = (float *)(smem + WG_NST * st_bytes + 8 * (2 * WG_NST + 1) + 16);   // [WG_NPW][256]
   __shared__ int s_seg[8], s_col[8];        // A block -> segment, column within the segment
 
   const int r0 = blockIdx.x * P.rows_per_cta;
@@ -977,32 +977,43 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
     }
   }
 
-  // ---------------- epilogue: TMEM -> smem transpose -> coalesced partial rows ----------------
+  // ---------------- epilogue: TMEM -> partial rows ----------------
+  // thread = gradient row k (as tcgen05.ld leaves it): each 32 x 32 block goes to a swizzled
+  // staging box in the now idle stage buffers and leaves by one TMA bulk store (rows >= K are
+  // clipped by the map, so the producers' bias row K is untouched)
   if (warp < 4) {
     if (nchunks > 0) mbar_wait(done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    float *stile = epi + warp * (32 * 33);
-    float *Pout = partial + (size_t)blockIdx.x * P.Kp * g.N;
+    float *stg = (float *)(smem + warp * 4096);
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const int sw = lane & 7;
     for (int tt = 0; tt < P.ktiles; ++tt) {
       const int k0 = tt * 128 + warp * 32;
       for (int j0 = 0; j0 < P.Npad; j0 += 32) {
         uint32_t r[32];
         tmem_ld32(tmem + lane_base + tt * P.Npad + j0, r);
+        if (k0 >= g.K) continue;
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+        float4 *srow = reinterpret_cast<float4 *>(stg) + lane * 8;
 #pragma unroll
-        for (int qq = 0; qq < 32; ++qq) stile[lane * 33 + qq] = nchunks > 0 ? __uint_as_float(r[qq]) : 0.f;
+        for (int q = 0; q < 8; ++q)
+          srow[q ^ sw] = nchunks > 0 ? make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                                   __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        const int n = j0 + lane;
-        if (n < g.N) {
-          for (int rr = 0; rr < 32; ++rr) {
-            const int k = k0 + rr;
-            if (k >= g.K) break;                        // row K (bias) comes from the producers
-            Pout[(size_t)k * g.N + n] = stile[rr * 33 + lane];
-          }
+        if (lane == 0) {
+          asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                           reinterpret_cast<uint64_t>(&pmap)),
+                       "r"(j0), "r"(k0), "r"((int)blockIdx.x), "r"(smem_u32(stg))
+                       : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
-        __syncwarp();
       }
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -1347,7 +1358,7 @@ bool wgrad_tc(chg_ctx *ctx, const WGrad &g, float **partial_out, int *Kp_out, in
   const int splits = (g.M + P.rows_per_cta - 1) / P.rows_per_cta;
   float *partial = red_partial(ctx, (size_t)splits * P.Kp * g.N);
   const size_t st_bytes = (size_t)(P.Kpad + P.Npad) * 128;
-  const size_t smem = 1024 + WG_NST * st_bytes + 8 * (2 * WG_NST + 1) + 16 + 4 * 32 * 33 * 4 + WG_NPW * 256 * 4;
+  const size_t smem = 1024 + WG_NST * st_bytes + 8 * (2 * WG_NST + 1) + 16 + WG_NPW * 256 * 4;
   if (smem > 224 * 1024) return false;
   static bool attr = false;
   if (!attr) {
@@ -1357,7 +1368,20 @@ bool wgrad_tc(chg_ctx *ctx, const WGrad &g, float **partial_out, int *Kp_out, in
   static int skip = getenv("CHG_TC_SKIP") ? atoi(getenv("CHG_TC_SKIP")) : 0;
   ProfScope ps(ctx, g.tag ? g.tag : "wgrad_tc", 2.0 * g.M * (double)P.Kp * g.N,
                gemm_a_bytes(g.A, g.M, 0, g.K) + (double)g.M * (4.0 * g.N + (g.didx ? 4.0 : 0.0)) + 4.0 * P.Kp * g.N);
-  launch_k(ctx, k_wgrad_tc, splits, WG_THREADS, smem, ctx->stream, g, P, partial, skip);
+  // partial as a 3-D tensor [splits][K][N] (row stride N, split stride Kp·N): TMA-store epilogue
+  CUtensorMap pmap;
+  memset(&pmap, 0, sizeof(pmap));
+  int use_pmap = 0;
+  if (EncodeTiledFn fn = encode_fn(); fn && ((uintptr_t)partial & 15) == 0) {
+    cuuint64_t dim[3] = {(cuuint64_t)g.N, (cuuint64_t)g.K, (cuuint64_t)splits};
+    cuuint64_t stride[2] = {(cuuint64_t)g.N * 4, (cuuint64_t)P.Kp * g.N * 4};
+    cuuint32_t box[3] = {32, 32, 1}, es[3] = {1, 1, 1};
+    use_pmap = fn(&pmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, partial, dim, stride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  if (!use_pmap) return false;                        // SIMT weight gradient instead
+  launch_k(ctx, k_wgrad_tc, splits, WG_THREADS, smem, ctx->stream, g, P, partial, skip, pmap);
   check_launch(ctx);
   *partial_out = partial;
   *Kp_out = P.Kp;
