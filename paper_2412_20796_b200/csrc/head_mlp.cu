@@ -6,7 +6,8 @@
 // one kernel per direction instead of one GEMM launch per layer:
 //
 //   forward  (k_head_fwd):  a CTA keeps every weight of the head in shared memory and
-//            walks 64-row tiles (persistent grid): tile -> Z_k = H_{k-1} W_k + b_k
+//            walks R-row tiles (persistent grid; R = 64, or 16 when the rows — a small batch's
+//            atoms — would leave most SMs idle): tile -> Z_k = H_{k-1} W_k + b_k
 //            (stored for the backward), H_k = SiLU(Z_k) in smem -> out = H W_L + b_L.
 //   backward (k_head_bwd):  per tile, dZ runs down the layers in smem; dX += dZ_0 W_0ᵀ is
 //            added into the caller's gradient rows; dW_k, db_k are accumulated in
@@ -14,14 +15,15 @@
 //            per-CTA partial in the flat layout of the head's parameter block, reduced
 //            in a fixed order by the batched reduction (reduce.cu; deterministic, no atomics).
 //
-// Register tiling: 256 threads, thread (a = t / 16, b = t % 16) owns a 4 x 4 block.
+// Register tiling: 256 threads, thread (a = t / 16, b = t % 16) owns R/16 rows x 4 columns of
+// a layer output (4 x 4 input x output entries of a weight gradient).
 // Shared tiles are [64][65] (odd pitch: column walks are conflict-free).
 #include "common.cuh"
 #include "ops.cuh"
 
 namespace {
 
-constexpr int HT = 64;        // rows per tile
+constexpr int HT = 64;        // rows per tile (16 when the rows would give fewer than 2 tiles per SM)
 constexpr int HP = 65;        // smem pitch of the forward activation tile (odd: row walks across lanes are conflict-free)
 constexpr int TPB = 68;       // smem pitch of the backward tiles (16-B rows: float4 row reads in the dW loop)
 constexpr int HMAXL = 4;      // max linear layers per head
@@ -76,10 +78,10 @@ __device__ void load_weights(const float *__restrict__ P, float *sm) {
 }
 
 // load a [64][64] row tile of a [rows, 64] matrix into smem [64][P] (zero rows past the end)
-template <int P>
+template <int P, int R>
 __device__ __forceinline__ void load_tile(const float *__restrict__ src, int64_t r0, int64_t rows, float *dst) {
 #pragma unroll 8   // independent loads in flight (one latency, not one per iteration)
-  for (int i = threadIdx.x; i < HT * 16; i += blockDim.x) {
+  for (int i = threadIdx.x; i < R * 16; i += blockDim.x) {
     const int r = i >> 4, c4 = (i & 15) * 4;
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     if (r0 + r < rows) v = __ldg((const float4 *)(src + (r0 + r) * 64 + c4));
@@ -88,43 +90,44 @@ __device__ __forceinline__ void load_tile(const float *__restrict__ src, int64_t
   }
 }
 
-template <int NL, int NOUT>
+template <int NL, int NOUT, int R>
 __global__ void __launch_bounds__(256) k_head_fwd(const __grid_constant__ HeadArgs a) {
   pdl_begin();
   extern __shared__ float sm[];
   using S = HeadSmem<NL, NOUT>;
   float *sH = sm + S::T0;            // [64][HP] layer input / activation
   load_weights<NL, NOUT, false>(a.P, sm);
-  const int t = threadIdx.x, ra = (t >> 4) * 4, cb = (t & 15) * 4;
-  const int64_t ntiles = (a.rows + HT - 1) / HT;
+  constexpr int RPT = R / 16;        // rows per thread
+  const int t = threadIdx.x, ra = (t >> 4) * RPT, cb = (t & 15) * 4;
+  const int64_t ntiles = (a.rows + R - 1) / R;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t r0 = tile * HT;
+    const int64_t r0 = tile * R;
     __syncthreads();
-    load_tile<HP>(a.X, r0, a.rows, sH);
+    load_tile<HP, R>(a.X, r0, a.rows, sH);
     __syncthreads();
 #pragma unroll 1
     for (int l = 0; l < NL - 1; ++l) {
       const float *W = sm + S::W + l * 64 * 64;
-      float acc[4][4];
+      float acc[RPT][4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < RPT; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
 #pragma unroll 8
       for (int k = 0; k < 64; ++k) {
-        float h[4], w[4];
+        float h[RPT], w[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) h[i] = sH[(ra + i) * HP + k];
+        for (int i = 0; i < RPT; ++i) h[i] = sH[(ra + i) * HP + k];
         const float4 w4 = *(const float4 *)&W[k * 64 + cb];
         w[0] = w4.x; w[1] = w4.y; w[2] = w4.z; w[3] = w4.w;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < RPT; ++i)
 #pragma unroll
           for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(h[i], w[j], acc[i][j]);
       }
       __syncthreads();                 // every thread has read sH
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < RPT; ++i) {
         float z[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -136,7 +139,7 @@ __global__ void __launch_bounds__(256) k_head_fwd(const __grid_constant__ HeadAr
       __syncthreads();
     }
     // last layer: out[r][o] = Σ_k H[r][k] W_L[k][o] + b_L[o]
-    for (int p = t; p < HT * NOUT; p += blockDim.x) {
+    for (int p = t; p < R * NOUT; p += blockDim.x) {
       const int r = p / NOUT, o = p % NOUT;
       if (r0 + r >= a.rows) continue;
       float s = 0.f;
@@ -147,17 +150,18 @@ __global__ void __launch_bounds__(256) k_head_fwd(const __grid_constant__ HeadAr
   }
 }
 
-template <int NL, int NOUT>
+template <int NL, int NOUT, int R>
 __global__ void __launch_bounds__(256) k_head_bwd(const __grid_constant__ HeadArgs a) {
   pdl_begin();
   extern __shared__ float sm[];
   using S = HeadSmem<NL, NOUT>;
   float *sA = sm + S::T0;            // layer input H_{k-1} (or X)
-  float *sZ = sA + HT * TPB;         // pre-activation z_{k-1}
-  float *sG = sZ + HT * TPB;         // dZ_k
-  float *sD = sG + HT * TPB;         // dout tile [64][NOUT]
+  float *sZ = sA + R * TPB;          // pre-activation z_{k-1}
+  float *sG = sZ + R * TPB;          // dZ_k
+  float *sD = sG + R * TPB;          // dout tile [R][NOUT]
   load_weights<NL, NOUT, true>(a.P, sm);
-  const int t = threadIdx.x, ta = (t >> 4) * 4, tb = (t & 15) * 4;
+  constexpr int RPT = R / 16;        // tile rows per thread (dH); ta indexes inputs k in dW
+  const int t = threadIdx.x, ta = (t >> 4) * 4, tr = (t >> 4) * RPT, tb = (t & 15) * 4;
   constexpr int NH = NL - 1;
   // per-thread accumulators: dW_k[ta..ta+3][tb..tb+3] (k = input row, n = output col), db_k[tb..] (ta == 0)
   float gW[NH][4][4], gb[NH][4];
@@ -174,17 +178,17 @@ __global__ void __launch_bounds__(256) k_head_bwd(const __grid_constant__ HeadAr
 #pragma unroll
   for (int q = 0; q < NLP; ++q) gWL[q] = 0.f;
 
-  const int64_t ntiles = (a.rows + HT - 1) / HT;
+  const int64_t ntiles = (a.rows + R - 1) / R;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t r0 = tile * HT;
+    const int64_t r0 = tile * R;
     __syncthreads();
-    for (int p = t; p < HT * NOUT; p += blockDim.x) {
+    for (int p = t; p < R * NOUT; p += blockDim.x) {
       const int r = p / NOUT, o = p % NOUT;
       sD[p] = (r0 + r < a.rows) ? a.dout[(r0 + r) * NOUT + o] : 0.f;
     }
-    load_tile<TPB>(a.Z[NH - 1], r0, a.rows, sZ);
+    load_tile<TPB, R>(a.Z[NH - 1], r0, a.rows, sZ);
     __syncthreads();
-    for (int i = t; i < HT * 64; i += blockDim.x) {
+    for (int i = t; i < R * 64; i += blockDim.x) {
       const int r = i >> 6, c = i & 63;
       sA[r * TPB + c] = silu_(sZ[r * TPB + c]);
     }
@@ -196,17 +200,17 @@ __global__ void __launch_bounds__(256) k_head_bwd(const __grid_constant__ HeadAr
       if (p < 64 * NOUT) {
         const int k = p / NOUT, o = p % NOUT;
         float s = 0.f;
-        for (int r = 0; r < HT; ++r) s = fmaf(sA[r * TPB + k], sD[r * NOUT + o], s);
+        for (int r = 0; r < R; ++r) s = fmaf(sA[r * TPB + k], sD[r * NOUT + o], s);
         gWL[q] += s;
       }
     }
     if (t < NOUT) {
       float s = 0.f;
-      for (int r = 0; r < HT; ++r) s += sD[r * NOUT + t];
+      for (int r = 0; r < R; ++r) s += sD[r * NOUT + t];
       gbL += s;
     }
     // dZ_{NH-1}[r][k] = (Σ_o dout[r][o] W_L[k][o]) · SiLU'(z[r][k])
-    for (int i = t; i < HT * 64; i += blockDim.x) {
+    for (int i = t; i < R * 64; i += blockDim.x) {
       const int r = i >> 6, k = i & 63;
       float s = 0.f;
 #pragma unroll
@@ -218,14 +222,14 @@ __global__ void __launch_bounds__(256) k_head_bwd(const __grid_constant__ HeadAr
     for (int l = NH - 1; l >= 0; --l) {   // unrolled: gW[l] stays in registers
       // layer input: H_{l-1} = SiLU(z_{l-1}) (z kept in sZ for the next dZ), or X for l = 0
       if (l > 0) {
-        load_tile<TPB>(a.Z[l - 1], r0, a.rows, sZ);
+        load_tile<TPB, R>(a.Z[l - 1], r0, a.rows, sZ);
         __syncthreads();
-        for (int i = t; i < HT * 64; i += blockDim.x) {
+        for (int i = t; i < R * 64; i += blockDim.x) {
           const int r = i >> 6, c = i & 63;
           sA[r * TPB + c] = silu_(sZ[r * TPB + c]);
         }
       } else {
-        load_tile<TPB>(a.X, r0, a.rows, sA);
+        load_tile<TPB, R>(a.X, r0, a.rows, sA);
       }
       __syncthreads();
       // dW_l[k][n] += Σ_r A[r][k] G[r][n]; db_l[n] += Σ_r G[r][n]
@@ -237,7 +241,7 @@ __global__ void __launch_bounds__(256) k_head_bwd(const __grid_constant__ HeadAr
           for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
         float cs[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 4
-        for (int r = 0; r < HT; ++r) {
+        for (int r = 0; r < R; ++r) {
           const float4 x4 = *(const float4 *)&sA[r * TPB + ta], g4 = *(const float4 *)&sG[r * TPB + tb];
           const float x[4] = {x4.x, x4.y, x4.z, x4.w}, gg[4] = {g4.x, g4.y, g4.z, g4.w};
 #pragma unroll
@@ -255,23 +259,23 @@ __global__ void __launch_bounds__(256) k_head_bwd(const __grid_constant__ HeadAr
 #pragma unroll
           for (int j = 0; j < 4; ++j) gb[l][j] += cs[j];
       }
-      // dH[r][k] = Σ_n G[r][n] W_l[k][n]: thread owns rows ta.., inputs k = tb..
-      float dh[4][4];
+      // dH[r][k] = Σ_n G[r][n] W_l[k][n]: thread owns rows tr.., inputs k = tb..
+      float dh[RPT][4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < RPT; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dh[i][j] = 0.f;
       {
         const float *WT = sm + S::W + l * 64 * 64;     // WT[n][k] = W[k][n]
 #pragma unroll 8
         for (int n = 0; n < 64; ++n) {
-          float gg[4];
+          float gg[RPT];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) gg[i] = sG[(ta + i) * TPB + n];
+          for (int i = 0; i < RPT; ++i) gg[i] = sG[(tr + i) * TPB + n];
           const float4 w4 = *(const float4 *)&WT[n * 64 + tb];
           const float w[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
+          for (int i = 0; i < RPT; ++i)
 #pragma unroll
             for (int j = 0; j < 4; ++j) dh[i][j] = fmaf(gg[i], w[j], dh[i][j]);
         }
@@ -279,13 +283,13 @@ __global__ void __launch_bounds__(256) k_head_bwd(const __grid_constant__ HeadAr
       __syncthreads();                 // all reads of sG / sZ done
       if (l > 0) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < RPT; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) sG[(ta + i) * TPB + tb + j] = dh[i][j] * dsilu_(sZ[(ta + i) * TPB + tb + j]);
+          for (int j = 0; j < 4; ++j) sG[(tr + i) * TPB + tb + j] = dh[i][j] * dsilu_(sZ[(tr + i) * TPB + tb + j]);
       } else {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int64_t r = r0 + ta + i;
+        for (int i = 0; i < RPT; ++i) {
+          const int64_t r = r0 + tr + i;
           if (r < a.rows) {
             float4 *d = (float4 *)(a.dX + r * 64 + tb);
             float4 v = *d;
@@ -316,10 +320,10 @@ __global__ void __launch_bounds__(256) k_head_bwd(const __grid_constant__ HeadAr
   if (t < NOUT) Lp[64 * NOUT + t] = gbL;
 }
 
-template <int NL, int NOUT>
-size_t head_smem_fwd() { return 4 * ((size_t)HeadSmem<NL, NOUT>::T0 + HT * HP); }
-template <int NL, int NOUT>
-size_t head_smem_bwd() { return 4 * ((size_t)HeadSmem<NL, NOUT>::T0 + 3 * HT * TPB + HT * NOUT); }
+template <int NL, int NOUT, int R>
+size_t head_smem_fwd() { return 4 * ((size_t)HeadSmem<NL, NOUT>::T0 + R * HP); }
+template <int NL, int NOUT, int R>
+size_t head_smem_bwd() { return 4 * ((size_t)HeadSmem<NL, NOUT>::T0 + 3 * R * TPB + R * NOUT); }
 
 int sm_count() {
   static int n = 0;
@@ -331,31 +335,38 @@ int sm_count() {
   return n;
 }
 
-template <int NL, int NOUT>
-void run_fwd(chg_ctx *ctx, const HeadArgs &a, const char *tag) {
-  const size_t smem = head_smem_fwd<NL, NOUT>();
+template <int NL, int NOUT, int R>
+void run_fwd_r(chg_ctx *ctx, const HeadArgs &a, const char *tag) {
+  const size_t smem = head_smem_fwd<NL, NOUT, R>();
   static bool attr = false;
   if (!attr) {
-    CUDA_OK(cudaFuncSetAttribute(k_head_fwd<NL, NOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_OK(cudaFuncSetAttribute(k_head_fwd<NL, NOUT, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  const int64_t ntiles = (a.rows + HT - 1) / HT;
+  const int64_t ntiles = (a.rows + R - 1) / R;
   const int grid = (int)std::min<int64_t>(ntiles, 2 * sm_count());
   ProfScope ps(ctx, tag, 2.0 * a.rows * (64.0 * 64 * (NL - 1) + 64.0 * NOUT),
                a.rows * 4.0 * (64 + 64 * (NL - 1) + NOUT) + 4.0 * head_block_size(NL, NOUT) * grid);
-  launch_k(ctx, k_head_fwd<NL, NOUT>, grid, 256, smem, ctx->stream, a);
+  launch_k(ctx, k_head_fwd<NL, NOUT, R>, grid, 256, smem, ctx->stream, a);
   check_launch(ctx);
 }
 
+// 64-row tiles; 16-row tiles when the rows (e.g. a small batch's atoms) would leave most SMs idle
 template <int NL, int NOUT>
-void run_bwd(chg_ctx *ctx, HeadArgs a, float *G, const char *tag) {
-  const size_t smem = head_smem_bwd<NL, NOUT>();
+void run_fwd(chg_ctx *ctx, const HeadArgs &a, const char *tag) {
+  if ((a.rows + HT - 1) / HT < 2 * sm_count()) run_fwd_r<NL, NOUT, 16>(ctx, a, tag);
+  else run_fwd_r<NL, NOUT, HT>(ctx, a, tag);
+}
+
+template <int NL, int NOUT, int R>
+void run_bwd_r(chg_ctx *ctx, HeadArgs a, float *G, const char *tag) {
+  const size_t smem = head_smem_bwd<NL, NOUT, R>();
   static bool attr = false;
   if (!attr) {
-    CUDA_OK(cudaFuncSetAttribute(k_head_bwd<NL, NOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_OK(cudaFuncSetAttribute(k_head_bwd<NL, NOUT, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  const int64_t ntiles = (a.rows + HT - 1) / HT;
+  const int64_t ntiles = (a.rows + R - 1) / R;
   const int grid = (int)std::min<int64_t>(ntiles, 2 * sm_count());
   const int nb = head_block_size(NL, NOUT);
   const int stride = head_part_stride(NL, NOUT);
@@ -363,12 +374,18 @@ void run_bwd(chg_ctx *ctx, HeadArgs a, float *G, const char *tag) {
   {
     ProfScope ps(ctx, tag, 2.0 * a.rows * (2.0 * 64 * 64 * (NL - 1) + 2.0 * 64 * NOUT),
                  a.rows * 4.0 * (64 * 3 + 64 * (NL - 1) + NOUT) + 4.0 * nb * (double)grid * 2);
-    launch_k(ctx, k_head_bwd<NL, NOUT>, grid, 256, smem, ctx->stream, a);
+    launch_k(ctx, k_head_bwd<NL, NOUT, R>, grid, 256, smem, ctx->stream, a);
     check_launch(ctx);
   }
   RedJob j;                                        // per-CTA partials -> the head's gradient block
   j.kind = 1; j.n = nb; j.splits = grid; j.stride = stride; j.part = a.part; j.W[0] = G;
   red_push(ctx, j);
+}
+
+template <int NL, int NOUT>
+void run_bwd(chg_ctx *ctx, HeadArgs a, float *G, const char *tag) {
+  if ((a.rows + HT - 1) / HT < 2 * sm_count()) run_bwd_r<NL, NOUT, 16>(ctx, a, G, tag);
+  else run_bwd_r<NL, NOUT, HT>(ctx, a, G, tag);
 }
 
 }  // namespace
