@@ -1056,7 +1056,7 @@ void tc_repack_all(chg_ctx *ctx, chg_model *m) {
   double bytes = 0;
   for (auto &J : c->jobs) bytes += (double)J.nkc * J.P.ntot * KC * 8.0;
   ProfScope ps(ctx, "tc_pack", 0.0, bytes);
-  launch_k(ctx, k_pack_all, dim3(32, (unsigned)c->jobs.size()), 256, 0, ctx->stream, c->d_jobs);
+  launch_k(ctx, k_pack_all, dim3(148, (unsigned)c->jobs.size()), 256, 0, ctx->stream, c->d_jobs);
   check_launch(ctx);
   for (auto &g : c->gen) g = c->cur_gen;
 }
