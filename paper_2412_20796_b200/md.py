@@ -12,7 +12,7 @@ import numpy as np
 
 from . import chg
 
-EV_PER_AMU_A2_FS2 = 103.642691      # 1 amu·Å²/fs² in eV (kinetic energy, monitoring only)
+EV_PER_AMU_A2_FS2 = 103.6426965     # 1 amu·Å²/fs² in eV (kinetic energy, monitoring only)
 KB_EV = 8.617333262e-5               # Boltzmann constant, eV/K
 
 
