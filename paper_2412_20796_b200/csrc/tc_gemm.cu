@@ -793,11 +793,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
 //   (M = 128, ≤ 2) × N in TMEM and writes one partial [Kp][N] (TMA bulk stores of 32 x 32
 //   blocks staged in the idle stage buffers); partials are reduced in a fixed order by the
 //   batched reduction (reduce.cu).  The bias (column sums of D) is summed by the producers
-//   from the staged K-major D rows.  Warps 0-11 produce, warp 12 issues MMAs, warps 0-3 run
+//   from the staged K-major D rows.  Warps 0-14 produce, warp 15 issues MMAs, warps 0-3 run
 //   the epilogue.
 // ---------------------------------------------------------------------------
 constexpr int WG_NST = 3;
-constexpr int WG_NPW = 12;                 // producer warps
+constexpr int WG_NPW = 15;                 // producer warps
 constexpr int WG_THREADS = (WG_NPW + 1) * 32;
 
 struct WgPlan {
