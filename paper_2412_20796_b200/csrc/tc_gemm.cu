@@ -106,9 +106,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 struct TcMaps {
   CUtensorMap m[4];
   int use[4];                      // 1: segment s is loaded by TMA
-  CUtensorMap gm[4];               // gathered segment s: 32 x 1 boxes for tile::gather4 (4 rows / instruction)
-  int use_g[4];
-  int grows[4];                    // table rows of gathered segment s (index >= grows: zero-filled row)
   CUtensorMap e[4];                // epilogue operand (mul or resid) of chunk c: 32 x 32 boxes
   int use_e[4];
   int nbuf;                        // operand boxes in flight per epilogue warp (0: plain loads)
@@ -137,16 +134,6 @@ __device__ __forceinline__ void tma_store_add_2d(const CUtensorMap *map, uint32_
 __device__ __forceinline__ float dsilu_fast(float x) {
   const float s = __fdividef(1.0f, 1.0f + __expf(-x));
   return s * (1.0f + x * (1.0f - s));
-}
-
-// 4 gathered rows (r0..r3) x 32 columns -> 512 B at dst (rows past the table: zero fill)
-__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *map, int c0, int r0, int r1, int r2,
-                                            int r3, uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
-      : "memory");
 }
 
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
@@ -374,7 +361,6 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
     const int q = tid & 7, rb = tid >> 3;
     int cur_tile = -1;
     int ridx[8][4];
-    int gidx[4][4];                                     // gather4 rows 4·lane .. 4·lane+3 (warp 0)
     for (int gi = 0; gi < total; ++gi) {
       const int tl = gi / nkc, kc = gi % nkc;
       const int tile = blockIdx.x + tl * gridDim.x;
@@ -386,22 +372,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
           const int m = tile * TCM + rb + 16 * i;
 #pragma unroll
           for (int sg = 0; sg < 4; ++sg)
-            ridx[i][sg] = (sg < g.A.nseg && m < g.M && !TM.use_g[sg]) ? (g.A.seg[sg].idx ? __ldg(g.A.seg[sg].idx + m) : m)
-                                                                       : -1;
-        }
-        if (warp == 0) {
-#pragma unroll
-          for (int sg = 0; sg < 4; ++sg)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int m = tile * TCM + 4 * lane + u;
-              int r = TM.grows[sg];                     // out of the table: zero row
-              if (TM.use_g[sg] && m < g.M) {
-                const int x = __ldg(g.A.seg[sg].idx + m);
-                if (x >= 0) r = x;
-              }
-              gidx[sg][u] = r;
-            }
+            ridx[i][sg] = (sg < g.A.nseg && m < g.M) ? (g.A.seg[sg].idx ? __ldg(g.A.seg[sg].idx + m) : m) : -1;
         }
       }
       if (ua > 0) mbar_wait(&emptyA[sa], (ua - 1) & 1);
@@ -421,22 +392,6 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
 #pragma unroll
       for (int sg = 0; sg < 4; ++sg)
         if (sg == seg) tma = TM.use[sg] != 0;
-      bool g4 = false;
-#pragma unroll
-      for (int sg = 0; sg < 4; ++sg)
-        if (sg == seg) g4 = TM.use_g[sg] != 0;
-      if (g4) {                                        // warp 0: 32 gather4 boxes (4 rows each); others arrive
-        if (tid == 0) mbar_expect_tx(&loaded[sa], a_bytes);
-        else mbar_arrive(&loaded[sa]);
-        if (warp == 0) {
-#pragma unroll
-          for (int sg = 0; sg < 4; ++sg)
-            if (sg == seg)
-              tma_gather4(dst0 + lane * 512, &TM.gm[sg], col - start, gidx[sg][0], gidx[sg][1], gidx[sg][2],
-                          gidx[sg][3], &loaded[sa]);
-        }
-        continue;
-      }
       if (tma) {                                       // one 16 KB box; the other 127 threads just arrive
         if (tid == 0) {
           mbar_expect_tx(&loaded[sa], a_bytes);
@@ -1101,20 +1056,6 @@ static int encode_a_map(CUtensorMap *m, const float *base, int width, int rows, 
   return r == CUDA_SUCCESS ? 1 : 0;
 }
 
-// 2-D fp32 map of a gathered row table [rows][width]: 32-column x 1-row boxes, SWIZZLE_128B —
-// tile::gather4 fetches 4 rows per instruction into consecutive 128-B rows of the UMMA layout
-static int encode_g4_map(CUtensorMap *m, const float *base, int width, int rows, int ld) {
-  EncodeTiledFn fn = encode_fn();
-  if (!fn || rows <= 0 || ((uintptr_t)base & 15) || (ld * 4) % 16) return 0;
-  cuuint64_t dim[2] = {(cuuint64_t)width, (cuuint64_t)rows};
-  cuuint64_t stride[1] = {(cuuint64_t)ld * 4};
-  cuuint32_t box[2] = {KC, 1}, es[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)base, dim, stride, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? 1 : 0;
-}
-
 // 2-D fp32 map of an epilogue operand [rows][ncols] (row stride ld): 32 x 32 boxes, no swizzle
 static int encode_op_map(CUtensorMap *m, const float *base, int ncols, int rows, int ld, bool swz = false) {
   EncodeTiledFn fn = encode_fn();
@@ -1293,18 +1234,9 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
                gemm_a_bytes(g.A, g.M, P.lo, P.lo + P.width) + (double)g.M * 4.0 * outb + 4.0 * g.K * cols);
   static int skip = getenv("CHG_TC_SKIP") ? atoi(getenv("CHG_TC_SKIP")) : 0;   // debug knob (timing studies)
   static const bool no_tma = getenv("CHG_TC_NO_TMA") != nullptr;            // A/B knob (timing studies)
-  // tile::gather4 for the gathered segments: opt-in (measured slower than the 4-warp cp.async
-  // gather at C2 / C3: ac_f1 25.9 -> 32.6 us, bc_f1 41.7 -> 56.6 us)
-  static const bool no_g4 = getenv("CHG_TC_G4") == nullptr;
   for (int s = 0; s < g.A.nseg && !no_tma; ++s) {
     const ASeg &S = g.A.seg[s];
-    if (S.idx) {                                      // gathered rows: TMA tile::gather4 when the table is known
-      if (!no_g4 && S.rows > 0 && S.rows < (int64_t)INT32_MAX) {
-        TM.use_g[s] = encode_g4_map(&TM.gm[s], S.base, S.width, (int)S.rows, S.ld);
-        TM.grows[s] = (int)S.rows;
-      }
-      continue;
-    }
+    if (S.idx) continue;                              // gathered rows stay on cp.async (tile::gather4 measured slower)
     TM.use[s] = encode_a_map(&TM.m[s], S.base, S.width, g.M, S.ld);
   }
   static const bool no_noconv = getenv("CHG_TC_NO_NOCONV") != nullptr;    // A/B knob
@@ -1319,9 +1251,8 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   }
   static const bool verbose = getenv("CHG_TC_VERBOSE") != nullptr;
   if (verbose)
-    fprintf(stderr, "rowgemm_tc %s: M %d K %d nseg %d g4 %d%d%d%d tma %d%d%d%d nsa %d bres %d tstore %d nst %d nbuf %d noconv %d smem %zu\n",
-            g.tag ? g.tag : "?", g.M, g.K, g.A.nseg, TM.use_g[0], TM.use_g[1], TM.use_g[2], TM.use_g[3], TM.use[0],
-            TM.use[1], TM.use[2], TM.use[3], P.nsa, P.bres,
+    fprintf(stderr, "rowgemm_tc %s: M %d K %d nseg %d tma %d%d%d%d nsa %d bres %d tstore %d nst %d nbuf %d noconv %d smem %zu\n",
+            g.tag ? g.tag : "?", g.M, g.K, g.A.nseg, TM.use[0], TM.use[1], TM.use[2], TM.use[3], P.nsa, P.bres,
             TM.tstore, TM.nst, nbuf, P.noconv, smem);
   launch_k(ctx, k_rowgemm_tc, grid, WS_THREADS, smem, ctx->stream, g, P, img, ntiles, skip, TM);
   check_launch(ctx);
