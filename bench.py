@@ -82,6 +82,8 @@ def _args():
                     help="graph prefetch on a builder context (SURVEY NEXT-3) in the e2e pass, in every pass, "
                          "or never (default: measured at C2, the builder's small kernels share SMs with the "
                          "persistent GEMMs and the overlap gains nothing; DESIGN.md §12)")
+    ap.add_argument("--workload", default="auto", choices=["auto", "C2", "C3", "C4"],
+                    help="auto: C2 at N=1, C3 at N>1; C4: skewed 4-400-atom oxides (BASELINE configs[3])")
     ap.add_argument("--per-gpu", type=int, default=0, help="structures per GPU (default: 40 at N=1, 128 at N>1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -97,7 +99,13 @@ def _dist():
     return ws, rank, local
 
 
-def _workload(n_gpus: int, per_gpu: int):
+WL_DESC = {"C2": "MPtrj-shaped synthetic batch", "C3": "MPtrj-shaped synthetic batch",
+           "C4": "skewed synthetic oxides (4-400 atoms, O/Li/Mn/Fe/Co/Ni)"}
+
+
+def _workload(n_gpus: int, per_gpu: int, name: str = "auto"):
+    if name != "auto":
+        return name, per_gpu or (40 if name == "C2" else 128)
     if n_gpus == 1 and per_gpu in (0, 40):
         return "C2", 40
     return "C3", per_gpu or 128
@@ -201,7 +209,7 @@ def cpu_baseline(wl: str, per: int, seconds: float):
 def run_reference(a, ws, rank):
     if rank != 0:
         return
-    wl, per = _workload(ws, a.per_gpu)
+    wl, per = _workload(ws, a.per_gpu, a.workload)
     sample, params, cfg, lc, cores = _oracle_sample(wl, per, 8.0)
     state = {"t": 0, "m": np.zeros_like(params), "v": np.zeros_like(params)}
     for _ in range(a.warmup):
@@ -239,7 +247,7 @@ def main():
     torch.cuda.set_device(local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    wl, per = _workload(ws, a.per_gpu)
+    wl, per = _workload(ws, a.per_gpu, a.workload)
     stream = torch.cuda.Stream()
     ctx = chg.Context(local, stream=stream.cuda_stream)
     if ws > 1:
@@ -274,8 +282,9 @@ def main():
                 per_rank_load = np.bincount(rank_of, weights=loads, minlength=ws)
                 contiguous = loads.reshape(ws, -1).sum(1) if glob.n_struct % ws == 0 else per_rank_load
                 cv = (float(per_rank_load.std() / per_rank_load.mean()), float(contiguous.std() / contiguous.mean()))
+                imb = (float(per_rank_load.max() / per_rank_load.mean()), float(contiguous.max() / contiguous.mean()))
             else:
-                mine, cv = glob, (0.0, 0.0)
+                mine, cv, imb = glob, (0.0, 0.0), (1.0, 1.0)
             gl = dict(S=glob.n_struct, N=glob.n_atoms, M=int(glob.magmom_mask.sum()))
             dev = dict(pos=torch.as_tensor(mine.positions, device="cuda"),
                        lat=torch.as_tensor(mine.lattice, device="cuda"),
@@ -299,7 +308,7 @@ def main():
                                  magmom_mask=pinned(mine.magmom_mask, torch.uint8)))
             h2d = sum(v.nbytes for k, v in host.items() if k != "lab") + sum(v.nbytes for v in host["lab"].values()) \
                 + mine.atom_ptr.nbytes
-            out.append(dict(ap=mine.atom_ptr, dev=dev, host=host, gl=gl, S=mine.n_struct, cv=cv, h2d=h2d))
+            out.append(dict(ap=mine.atom_ptr, dev=dev, host=host, gl=gl, S=mine.n_struct, cv=cv, imb=imb, h2d=h2d))
         return out
 
     batches = make_batches(wl, per, a.batches)
@@ -544,7 +553,7 @@ def main():
                           "note": "tf32: GatedMLP GEMMs on tcgen05 (TF32, fp32 accumulate), all else fp32; "
                                   "fp32: everything on CUDA cores (strict 1e-4 gradient parity)",
                           other: {"value": structs / (ms_other / 1e3), "ms_per_step": ms_other / a.steps}},
-            "config": {"workload": f"{wl}: MPtrj-shaped synthetic batch, {per} structures per GPU "
+            "config": {"workload": f"{wl}: {WL_DESC[wl]}, {per} structures per GPU "
                                    f"(5/3 Å cutoffs, d=64, 4 atom-conv / 3 bond-conv)",
                        "structures_per_gpu": per, "global_batch": per * ws, "parallelism": f"dp{ws}",
                        "step": "build_graph + forward + backward + allreduce + Adam",
@@ -554,6 +563,7 @@ def main():
                                        "prefetched on a builder context during the previous step"},
                        "l2": "flushed between steps (256 MiB write, outside the timed events)",
                        "batches_cycled": len(batches), "cv_balanced_vs_contiguous": b0["cv"],
+                       "max_over_mean_rank_load_balanced_vs_contiguous": b0["imb"],
                        "rank0_counts_first_batch": None},
             "e2e": {"value": e2e, "unit": "structures/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 40 + 4},
             "gpu_launches": int(launches),

@@ -15,6 +15,7 @@
 //   k_fill      ordered emission with warp ballot/scan                  (G3)
 //   k_angles    angle pairs, swap map, per-angle edge/centre indices    (G4)
 //   k_rev       reverse-edge map by binary search in row j              (G4)
+#include <optional>
 #include <cmath>
 
 #include "common.cuh"
@@ -761,7 +762,8 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
       }
     }
     int *flag = ctx->d_flag;
-    ProfScope ps1(ctx, "graph", 0.0, 0.0);
+    std::optional<ProfScope> ps1;        // device work only: closed before the host synchronisation
+    ps1.emplace(ctx, "graph", 0.0, 0.0);
     CUDA_OK(cudaMemsetAsync(flag, 0, sizeof(int), st));
     CUDA_OK(cudaMemsetAsync(flag + 1, 0x7f, sizeof(int), st));       // smallest bad structure (k_geo)
     CUDA_OK(cudaMemsetAsync(d_tot, 0, 64, st));
@@ -794,6 +796,7 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
       CUDA_OK(cudaMemsetAsync(G->bond_ptr, 0, 4, st));
       CUDA_OK(cudaMemsetAsync(G->atom_angle_ptr, 0, 4, st));
     }
+    ps1.reset();
     // totals + flags to host (the one synchronisation of the build: sizes)
     long long *h_tot = (long long *)ctx->pinned_get(64);
     CUDA_OK(cudaMemcpyAsync(h_tot, d_tot, 32, cudaMemcpyDeviceToHost, st));

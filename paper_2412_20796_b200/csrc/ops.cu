@@ -357,6 +357,7 @@ __global__ void __launch_bounds__(256) k_colsum_partial(int64_t rows, int64_t rp
   const int t = threadIdx.x, c = t & 15, rl = t >> 4;
   const int64_t r0 = blockIdx.x * rpb, r1 = min(rows, r0 + rpb);
   float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4   // 4 independent row loads in flight per thread
   for (int64_t r = r0 + rl; r < r1; r += 16) {
     const float4 v = __ldg((const float4 *)(D + r * 64) + c);
     s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
@@ -676,7 +677,8 @@ void edge_update(chg_ctx *ctx, int64_t E, const float *e, const float *bias, con
 
 void colsum(chg_ctx *ctx, int64_t rows, const float *D, float *grad) {
   if (rows <= 0 || ctx->no_param_grads) return;
-  const int64_t rpb = std::max<int64_t>(64, (rows + 295) / 296);
+  // 4 blocks per SM (296 blocks: 14.7 us, 592: 12.8 us per launch at C3; 1184 no better)
+  const int64_t rpb = std::max<int64_t>(64, (rows + 591) / 592);
   const int nb = ceil_div(rows, rpb);
   float *part = red_partial(ctx, (size_t)nb * 64);
   {
