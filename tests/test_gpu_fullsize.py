@@ -1,0 +1,116 @@
+"""GPU parity at BASELINE.json's full sizes, in the configuration bench.py times: the first
+batch of C3 (128 MPtrj-shaped structures) and of C4 (128 skewed oxides, BASELINE configs[3]),
+built and run as ONE batch on the GPU.
+
+* C3 graph: every list bit-exact against the oracle's graph of the whole batch (~15 s).
+* C4 graph (the oracle needs minutes for the whole batch): sampled structures — the slice of
+  the full-batch lists belonging to structure s, re-based to local indices, is bit-exact
+  against the oracle's graph of s alone (structures are independent).
+* Forward (fp32 strict and TF32 bench mode): the per-structure outputs of sampled structures
+  of the full batch equal the oracle run on each structure alone, within the DESIGN §6 bars.
+"""
+import numpy as np
+import pytest
+
+from chg_inputs import init_flat_params, make_config_batch, split_batch
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle.graph import build_graph_batch  # noqa: E402
+from oracle.model import ModelConfig, param_layout, run_forward  # noqa: E402
+from paper_2412_20796_b200 import chg  # noqa: E402
+
+CFG = ModelConfig()
+_BATCHES = {}
+
+
+def _batch(wl):
+    if wl not in _BATCHES:
+        _BATCHES[wl] = make_config_batch(wl, 0, n_struct=128)
+    return _BATCHES[wl]
+
+
+def _samples(b):
+    """Smallest, median and 90th-percentile structure by atom count (deterministic)."""
+    n = np.diff(b.atom_ptr)
+    o = np.argsort(n, kind="stable")
+    return sorted({int(o[0]), int(o[len(o) // 2]), int(o[int(len(o) * 0.9)])})
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = chg.Context(0)
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module")
+def params():
+    return init_flat_params(param_layout(CFG), seed=0, bias_scale=0.1).astype(np.float32).astype(np.float64)
+
+
+def test_fullsize_c3_graph_bit_exact(ctx):
+    b = _batch("C3")
+    og = build_graph_batch(b)
+    gg = ctx.build_graph(b.atom_ptr, b.positions, b.lattice, b.species)
+    assert tuple(gg.counts()) == (og.n_atoms, og.n_edges, og.n_bonds, og.n_angles)
+    ex = gg.export()
+    for k, v in og.lists().items():
+        np.testing.assert_array_equal(ex[k], v, err_msg=k)
+    np.testing.assert_array_equal(ex["vec"][:, :3], og.d.astype(np.float32))
+    np.testing.assert_array_equal(gg.per_struct(), og.counts)
+
+
+def test_fullsize_c4_graph_sampled(ctx):
+    b = _batch("C4")
+    gg = ctx.build_graph(b.atom_ptr, b.positions, b.lattice, b.species)
+    ps = gg.per_struct()
+    ex = gg.export()
+    N, E, B, A = gg.counts()
+    assert (ps[:, 0].sum(), ps[:, 1].sum(), ps[:, 2].sum(), ps[:, 3].sum()) == (N, E, B, A)
+    for s in _samples(b):
+        og = build_graph_batch(split_batch(b, [s]))
+        np.testing.assert_array_equal(ps[s], og.counts[0])
+        a0, a1 = int(b.atom_ptr[s]), int(b.atom_ptr[s + 1])
+        e0, e1 = int(ex["row_ptr"][a0]), int(ex["row_ptr"][a1])
+        b0, q0 = int(ps[:s, 2].sum()), int(ps[:s, 3].sum())
+        q1 = q0 + int(ps[s, 3])
+        np.testing.assert_array_equal(ex["row_ptr"][a0:a1 + 1] - e0, og.row_ptr)
+        np.testing.assert_array_equal(ex["nbr"][e0:e1] - a0, og.nbr)
+        np.testing.assert_array_equal(ex["img"][e0:e1], og.img)
+        np.testing.assert_array_equal(ex["rev"][e0:e1] - e0, og.rev)
+        np.testing.assert_array_equal(ex["vec"][e0:e1, :3], og.d.astype(np.float32))
+        bid = ex["bond_id"][e0:e1]
+        np.testing.assert_array_equal(np.where(bid >= 0, bid - b0, -1), og.bond_id)
+        np.testing.assert_array_equal(ex["bond_edge"][b0:b0 + int(ps[s, 2])] - e0, og.bond_edge)
+        np.testing.assert_array_equal(ex["angle_ptr"][b0:b0 + int(ps[s, 2]) + 1] - q0, og.angle_ptr)
+        for k in ("angle_b1", "angle_b2"):
+            np.testing.assert_array_equal(ex[k][q0:q1] - b0, getattr(og, k), err_msg=k)
+        np.testing.assert_array_equal(ex["swap"][q0:q1] - q0, og.swap)
+
+
+@pytest.mark.parametrize("wl", ["C3", "C4"])
+@pytest.mark.parametrize("prec", [0, 2])
+def test_fullsize_forward_sampled(ctx, params, wl, prec):
+    b = _batch(wl)
+    cfg = chg.default_model_cfg()
+    cfg.mlp_precision = prec
+    m = chg.Model(ctx, cfg)
+    m.set_params(params.astype(np.float32))
+    gg = ctx.build_graph(b.atom_ptr, b.positions, b.lattice, b.species)
+    out = ctx.forward(m, gg, train=True)
+    tol = 1e-5 if prec == 0 else 2e-3          # fp32 strict / TF32 loosened
+    ftol = 1e-4 if prec == 0 else 2e-3
+    for s in _samples(b):
+        sb = split_batch(b, [s])
+        ref = run_forward(build_graph_batch(sb), sb.species, sb.lattice, params, CFG)
+        a0, a1 = int(b.atom_ptr[s]), int(b.atom_ptr[s + 1])
+        eps = float(ref["energy_per_atom"].detach().numpy()[0])
+        assert abs(out["energy_per_atom"][s] - eps) <= tol * max(abs(eps), 1.0), (s, out["energy_per_atom"][s], eps)
+        assert np.max(np.abs(out["forces"][a0:a1] - ref["forces"].detach().numpy())) <= ftol, s
+        assert np.max(np.abs(out["stress"][s] - ref["stress"].detach().numpy()[0])) <= ftol, s
+        assert np.max(np.abs(out["magmom"][a0:a1] - ref["magmom"].detach().numpy())) <= (1e-5 if prec == 0 else 2e-3), s
+    m.close()
