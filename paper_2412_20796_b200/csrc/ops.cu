@@ -78,22 +78,25 @@ __global__ void __launch_bounds__(256, 4) k_gate_bwd(int64_t rows, int64_t rpb, 
   float2 gc = *(const float2 *)(ln.gc + c0), bc = *(const float2 *)(ln.bc + c0);
   float2 gg = *(const float2 *)(ln.gg + c0), bg = *(const float2 *)(ln.bg + c0);
   float a_gc[2] = {0, 0}, a_bc[2] = {0, 0}, a_gg[2] = {0, 0}, a_bg[2] = {0, 0};
-  // software pipeline: the next row's y (and its seed-row index) are in flight while this
-  // row's LayerNorm adjoint runs
-  float2 nyc = make_float2(0.f, 0.f), nyg = nyc;
+  // software pipeline: the next row's y and seed row dout are in flight while this row's
+  // LayerNorm adjoint runs; the seed-row index is fetched one row further ahead so the dout
+  // load does not wait on it
+  float2 nyc = make_float2(0.f, 0.f), nyg = nyc, nd = nyc;
   int64_t ndrow = 0;
   if (r0 + wid < r1) {
-    nyc = __ldg((const float2 *)(y + (r0 + wid) * ldy + c0));
-    nyg = __ldg((const float2 *)(y + (r0 + wid) * ldy + 64 + c0));
-    ndrow = didx ? __ldg(didx + r0 + wid) : r0 + wid;
+    const int64_t r = r0 + wid;
+    nyc = __ldg((const float2 *)(y + r * ldy + c0));
+    nyg = __ldg((const float2 *)(y + r * ldy + 64 + c0));
+    nd = *(const float2 *)(dout + (didx ? (int64_t)__ldg(didx + r) : r) * 64 + c0);
+    if (r + 8 < r1) ndrow = didx ? __ldg(didx + r + 8) : r + 8;
   }
   for (int64_t row = r0 + wid; row < r1; row += 8) {
-    const float2 yc = nyc, yg = nyg;
-    const int64_t drow = ndrow;
+    const float2 yc = nyc, yg = nyg, d2 = nd;
     if (row + 8 < r1) {
       nyc = __ldg((const float2 *)(y + (row + 8) * ldy + c0));
       nyg = __ldg((const float2 *)(y + (row + 8) * ldy + 64 + c0));
-      ndrow = didx ? __ldg(didx + row + 8) : row + 8;
+      nd = *(const float2 *)(dout + ndrow * 64 + c0);
+      if (row + 16 < r1) ndrow = didx ? __ldg(didx + row + 16) : row + 16;
     }
     RowStats sc = ln_stats(yc.x, yc.y), sg = ln_stats(yg.x, yg.y);
     float xc[2] = {(yc.x - sc.mu) * sc.rstd, (yc.y - sc.mu) * sc.rstd};
@@ -103,7 +106,6 @@ __global__ void __launch_bounds__(256, 4) k_gate_bwd(int64_t rows, int64_t rpb, 
     float s_g[2] = {sigmoidf_(ng[0]), sigmoidf_(ng[1])};
     float s_c[2] = {siluf_(nc[0]), siluf_(nc[1])};
     float phi[2] = {s_g[0] * s_c[0], s_g[1] * s_c[1]};
-    float2 d2 = *(const float2 *)(dout + drow * 64 + c0);
     float d[2] = {d2.x, d2.y};
     float dphi[2];
     if (mode == GATE_MUL_W) {
