@@ -82,21 +82,25 @@ __global__ void __launch_bounds__(256, 4) k_gate_bwd(int64_t rows, int64_t rpb, 
   // LayerNorm adjoint runs; the seed-row index is fetched one row further ahead so the dout
   // load does not wait on it
   float2 nyc = make_float2(0.f, 0.f), nyg = nyc, nd = nyc;
-  int64_t ndrow = 0;
+  int ndrow = 0;                                     // row indices fit int32 (didx is int32)
+  int ni1 = 0, ni2 = 0;                              // GATE_MUL_W1W2: next row's bond indices
   if (r0 + wid < r1) {
     const int64_t r = r0 + wid;
+    if (mode == GATE_MUL_W1W2) { ni1 = __ldg(i1 + r); ni2 = __ldg(i2 + r); }
     nyc = __ldg((const float2 *)(y + r * ldy + c0));
     nyg = __ldg((const float2 *)(y + r * ldy + 64 + c0));
     nd = *(const float2 *)(dout + (didx ? (int64_t)__ldg(didx + r) : r) * 64 + c0);
-    if (r + 8 < r1) ndrow = didx ? __ldg(didx + r + 8) : r + 8;
+    if (r + 8 < r1) ndrow = didx ? __ldg(didx + r + 8) : (int)(r + 8);
   }
   for (int64_t row = r0 + wid; row < r1; row += 8) {
     const float2 yc = nyc, yg = nyg, d2 = nd;
+    const int ci1 = ni1, ci2 = ni2;
     if (row + 8 < r1) {
+      if (mode == GATE_MUL_W1W2) { ni1 = __ldg(i1 + row + 8); ni2 = __ldg(i2 + row + 8); }
       nyc = __ldg((const float2 *)(y + (row + 8) * ldy + c0));
       nyg = __ldg((const float2 *)(y + (row + 8) * ldy + 64 + c0));
-      nd = *(const float2 *)(dout + ndrow * 64 + c0);
-      if (row + 16 < r1) ndrow = didx ? __ldg(didx + row + 16) : row + 16;
+      nd = *(const float2 *)(dout + (int64_t)ndrow * 64 + c0);
+      if (row + 16 < r1) ndrow = didx ? __ldg(didx + row + 16) : (int)(row + 16);
     }
     RowStats sc = ln_stats(yc.x, yc.y), sg = ln_stats(yg.x, yg.y);
     float xc[2] = {(yc.x - sc.mu) * sc.rstd, (yc.y - sc.mu) * sc.rstd};
@@ -115,8 +119,8 @@ __global__ void __launch_bounds__(256, 4) k_gate_bwd(int64_t rows, int64_t rpb, 
       acc.x += d[0] * phi[0]; acc.y += d[1] * phi[1];
       *(float2 *)(dw_acc + row * 64 + c0) = acc;
     } else if (mode == GATE_MUL_W1W2) {
-      float2 w1 = *(const float2 *)(w + (int64_t)i1[row] * 64 + c0);
-      float2 w2 = *(const float2 *)(w + (int64_t)i2[row] * 64 + c0);
+      float2 w1 = *(const float2 *)(w + (int64_t)ci1 * 64 + c0);
+      float2 w2 = *(const float2 *)(w + (int64_t)ci2 * 64 + c0);
       dphi[0] = d[0] * w1.x * w2.x; dphi[1] = d[1] * w1.y * w2.y;
       *(float2 *)(q1 + row * 64 + c0) = make_float2(d[0] * phi[0] * w2.x, d[1] * phi[1] * w2.y);
       *(float2 *)(q2 + row * 64 + c0) = make_float2(d[0] * phi[0] * w1.x, d[1] * phi[1] * w1.y);
