@@ -201,7 +201,7 @@ def cpu_baseline(wl: str, per: int, seconds: float):
         if time.time() - t0 >= seconds / 2:
             break
     dt = time.time() - t0
-    return {"value": done / dt, "unit": "structures/s", "cores": cores, "kind": "oracle",
+    return {"value": done / dt, "unit": "structures/s", "cores": cores, "host_cores": os.cpu_count(), "kind": "oracle",
             "sample": f"{sample.n_struct} of the {wl} batch's {per} structures, fp64 torch CPU oracle fwd+bwd+Adam "
                       f"({done} structure-steps in {dt:.1f} s)"}
 
@@ -219,7 +219,7 @@ def run_reference(a, ws, rank):
         params = _oracle_step(sample, params, cfg, lc, state)
     dt = time.time() - t0
     v = sample.n_struct * a.steps / dt
-    cb = {"value": v, "unit": "structures/s", "cores": cores, "kind": "oracle",
+    cb = {"value": v, "unit": "structures/s", "cores": cores, "host_cores": os.cpu_count(), "kind": "oracle",
           "sample": f"{sample.n_struct} structures of the {wl} batch per step (fp64 torch CPU oracle fwd+bwd+Adam)"}
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "structures/s", "n_gpus": ws, "steps": a.steps,

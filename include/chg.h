@@ -76,7 +76,10 @@ typedef struct {
 } chg_pred;
 
 /* Labels for the loss.  energy_per_atom [S], forces [N*3],
- * stress [S*9], magmom [N], magmom_mask [N] (1 = labelled).  All required. */
+ * stress [S*9], magmom [N], magmom_mask [N] (1 = labelled).  A NULL array
+ * skips that task (its loss term and seeds are 0); a NULL
+ * magmom_mask with magmom given means every atom is labelled.  All four
+ * label arrays NULL is CHG_ERR_ARG (chg_backward). */
 typedef struct {
   const float *energy_per_atom, *forces, *stress, *magmom;
   const uint8_t *magmom_mask;
@@ -199,7 +202,8 @@ chg_status chg_md_verlet(chg_ctx *ctx, int64_t n_atoms, double *positions, doubl
  * Computes the Huber loss of the last train-mode forward and ACCUMULATES
  * dL/dθ into the model's gradient vector.  loss_out (host, optional) =
  * {total, E, F, S, M}; NULL = no host synchronisation.
- * Errors: CHG_ERR_STATE if the last forward on ctx was not train-mode on g. */
+ * Errors: CHG_ERR_STATE if the last forward on ctx was not train-mode on g;
+ * CHG_ERR_ARG if every label array is NULL. */
 chg_status chg_backward(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *labels,
                         const chg_loss_cfg *cfg, double loss_out[5]);
 
@@ -207,7 +211,9 @@ chg_status chg_backward(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labe
  * [ncclAllReduce(sum) of the gradients if cfg->allreduce] -> finite check ->
  * Adam update of params/m/v -> gradients zeroed.  On a non-finite gradient
  * returns CHG_ERR_NONFINITE naming the first offending tensor and leaves
- * params, m and v untouched (gradients are kept).  Synchronises once (the
+ * params, m and v untouched (gradients are kept — with allreduce they already
+ * hold the cross-rank sum, so every rank sees the same non-finite entry and
+ * takes the same decision; do not reduce them again).  Synchronises once (the
  * finite flag). */
 chg_status chg_step(chg_ctx *ctx, chg_model *m, const chg_adam_cfg *cfg);
 

@@ -247,17 +247,16 @@ class Context:
                  n_struct_global: int = 0, n_atoms_global: int = 0, n_magmom_global: int = 0,
                  sync_loss: bool = True):
         """labels: dict energy_per_atom [S], forces [N,3], stress [S,3,3], magmom [N],
-        magmom_mask [N] (numpy → host copy, or CUDA tensors)."""
-        dev = _on_device(labels["forces"])
+        magmom_mask [N] (numpy → host copy, or CUDA tensors).  A missing / None entry
+        skips that task (chg_labels NULL field)."""
+        names = ("energy_per_atom", "forces", "stress", "magmom", "magmom_mask")
+        present = [labels[k] for k in names if labels.get(k) is not None]
+        dev = _on_device(present[0]) if present else False
         keep = {}
-        if not dev:
-            for k, dt in (("energy_per_atom", np.float32), ("forces", np.float32), ("stress", np.float32),
-                          ("magmom", np.float32), ("magmom_mask", np.uint8)):
-                keep[k] = np.ascontiguousarray(np.asarray(labels[k], dt))
-        else:
-            keep = labels
-        lab = Labels(_ptr(keep["energy_per_atom"]), _ptr(keep["forces"]), _ptr(keep["stress"]),
-                     _ptr(keep["magmom"]), _ptr(keep["magmom_mask"]), int(dev))
+        for k, dt in zip(names, (np.float32, np.float32, np.float32, np.float32, np.uint8)):
+            x = labels.get(k)
+            keep[k] = None if x is None else (x if dev else np.ascontiguousarray(np.asarray(x, dt)))
+        lab = Labels(*(_ptr(keep[k]) for k in names), int(dev))
         cfg = LossCfg(w[0], w[1], w[2], w[3], delta, n_struct_global, n_atoms_global, n_magmom_global)
         out = (C.c_double * 5)()
         self._check(self.lib.chg_backward(self.h, model.h, graph.h, C.byref(lab), C.byref(cfg),

@@ -1,6 +1,7 @@
 // abi.cu — C ABI entry points of libchg (include/chg.h): context, graph and
 // model handles, canonical parameter layout, load-balance sampler, NCCL
 // bootstrap.  Compute lives in graph.cu / model.cu.
+#include <mutex>
 #include <nccl.h>
 
 #include <algorithm>
@@ -131,6 +132,32 @@ static void build_layout(chg_model *m) {
 }
 
 // ---------------------------------------------------------------------------
+int device_sm_count() {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  cache[dev] = n;
+  return n;
+}
+
+void smem_optin(const void *func, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void *, int>, int> done;   // (kernel, device) -> bytes opted in
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  int &have = done[{func, dev}];
+  if (have >= bytes) return;
+  CUDA_OK(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  have = bytes;
+}
+
 extern "C" {
 
 chg_status chg_ctx_create(int device, void *cuda_stream, chg_ctx **out) {

@@ -292,6 +292,11 @@ inline void launch_k(chg_ctx *ctx, void (*kern)(KArgs...), dim3 grid, dim3 block
   cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);   // errors: check_launch (cudaGetLastError)
 }
 
+// per-device facts and opt-ins (abi.cu): thread-safe, cached per CUDA device, so one process
+// may run ctxs on several GPUs (the attribute is per device context)
+int device_sm_count();                                  // SMs of the current device
+void smem_optin(const void *func, int bytes);           // MaxDynamicSharedMemorySize once per (func, device)
+
 // reduce.cu
 float *red_partial(chg_ctx *ctx, size_t floats);       // partial buffer for the next recorded job
 void red_push(chg_ctx *ctx, RedJob j);                 // record (red_on) or launch now

@@ -325,24 +325,12 @@ size_t head_smem_fwd() { return 4 * ((size_t)HeadSmem<NL, NOUT>::T0 + R * HP); }
 template <int NL, int NOUT, int R>
 size_t head_smem_bwd() { return 4 * ((size_t)HeadSmem<NL, NOUT>::T0 + 3 * R * TPB + R * NOUT); }
 
-int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return n;
-}
+int sm_count() { return device_sm_count(); }
 
 template <int NL, int NOUT, int R>
 void run_fwd_r(chg_ctx *ctx, const HeadArgs &a, const char *tag) {
   const size_t smem = head_smem_fwd<NL, NOUT, R>();
-  static bool attr = false;
-  if (!attr) {
-    CUDA_OK(cudaFuncSetAttribute(k_head_fwd<NL, NOUT, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  smem_optin((const void *)k_head_fwd<NL, NOUT, R>, (int)smem);
   const int64_t ntiles = (a.rows + R - 1) / R;
   const int grid = (int)std::min<int64_t>(ntiles, 2 * sm_count());
   ProfScope ps(ctx, tag, 2.0 * a.rows * (64.0 * 64 * (NL - 1) + 64.0 * NOUT),
@@ -361,11 +349,7 @@ void run_fwd(chg_ctx *ctx, const HeadArgs &a, const char *tag) {
 template <int NL, int NOUT, int R>
 void run_bwd_r(chg_ctx *ctx, HeadArgs a, float *G, const char *tag) {
   const size_t smem = head_smem_bwd<NL, NOUT, R>();
-  static bool attr = false;
-  if (!attr) {
-    CUDA_OK(cudaFuncSetAttribute(k_head_bwd<NL, NOUT, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  smem_optin((const void *)k_head_bwd<NL, NOUT, R>, (int)smem);
   const int64_t ntiles = (a.rows + R - 1) / R;
   const int grid = (int)std::min<int64_t>(ntiles, 2 * sm_count());
   const int nb = head_block_size(NL, NOUT);

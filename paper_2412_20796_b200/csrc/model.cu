@@ -549,7 +549,7 @@ void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float 
 }
 
 const float *labels_dev(chg_ctx *ctx, const void *p, size_t bytes, const char *name, int on_device) {
-  if (on_device) return (const float *)p;
+  if (on_device || !p) return (const float *)p;   // NULL = task skipped
   void *d = ctx->get(name, bytes);
   if (bytes) CUDA_OK(cudaMemcpyAsync(d, p, bytes, cudaMemcpyHostToDevice, ctx->stream));
   return (const float *)d;
@@ -666,8 +666,9 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
                    double *loss_out) {
   const int64_t N = g->N, E = g->E, B = g->B, A = g->A;
   const int S = g->S, T = m->cfg.n_bond_conv;
-  if (!lab_in->energy_per_atom || !lab_in->forces || !lab_in->stress || !lab_in->magmom || !lab_in->magmom_mask)
-    CHG_THROW(CHG_ERR_ARG, "all label arrays are required");
+  // a NULL label array skips that task; all four missing is a contract error
+  if (!lab_in->energy_per_atom && !lab_in->forces && !lab_in->stress && !lab_in->magmom)
+    CHG_THROW(CHG_ERR_ARG, "no labels: energy_per_atom, forces, stress and magmom are all NULL");
   Bwd Bw{ctx, m, g, nullptr};
   // split-partial reductions of a layer are batched into one launch (reduce.cu)
   struct RedScope {

@@ -462,13 +462,16 @@ __global__ void k_loss(LossArgs a, double *out) {
   __shared__ double sh[5][1024];
   int t = threadIdx.x;
   double le = 0, lf = 0, ls = 0, lm = 0, cm = 0;
+  // a NULL label array skips that task; a NULL mask with magmoms = all labelled
   for (int s = t; s < a.S; s += blockDim.x) {
-    le += huber_d((double)a.epa[s] - a.l_epa[s], a.delta);
-    for (int k = 0; k < 9; ++k) ls += huber_d((double)a.stress[9 * s + k] - a.l_stress[9 * s + k], a.delta);
+    if (a.l_epa) le += huber_d((double)a.epa[s] - a.l_epa[s], a.delta);
+    if (a.l_stress)
+      for (int k = 0; k < 9; ++k) ls += huber_d((double)a.stress[9 * s + k] - a.l_stress[9 * s + k], a.delta);
   }
   for (int i = t; i < a.N; i += blockDim.x) {
-    for (int c = 0; c < 3; ++c) lf += huber_d((double)a.forces[3 * i + c] - a.l_forces[3 * i + c], a.delta);
-    if (a.l_mask[i]) { lm += huber_d((double)a.mag[i] - a.l_mag[i], a.delta); cm += 1.0; }
+    if (a.l_forces)
+      for (int c = 0; c < 3; ++c) lf += huber_d((double)a.forces[3 * i + c] - a.l_forces[3 * i + c], a.delta);
+    if (a.l_mag && (!a.l_mask || a.l_mask[i])) { lm += huber_d((double)a.mag[i] - a.l_mag[i], a.delta); cm += 1.0; }
   }
   sh[0][t] = le; sh[1][t] = lf; sh[2][t] = ls; sh[3][t] = lm; sh[4][t] = cm;
   __syncthreads();
@@ -493,19 +496,21 @@ __global__ void k_seed_atom(LossArgs a, const double *lossbuf, float *__restrict
   if (i >= a.N) return;
   int s = a.soa[i];
   float in = a.inv_n[s];
-  d_eatom[i] = (float)(a.w_e / a.Sg) * dhuber(a.epa[s] - a.l_epa[s], a.delta) * in;
+  d_eatom[i] = a.l_epa ? (float)(a.w_e / a.Sg) * dhuber(a.epa[s] - a.l_epa[s], a.delta) * in : 0.f;
   float G[9];
   lattice_G(a.lat + 9 * s, G);
   float cs = (float)(a.w_s / (9.0 * a.Sg));
   float ds[9];
-  for (int k = 0; k < 9; ++k) ds[k] = cs * dhuber(a.stress[9 * s + k] - a.l_stress[9 * s + k], a.delta);
+  for (int k = 0; k < 9; ++k) ds[k] = a.l_stress ? cs * dhuber(a.stress[9 * s + k] - a.l_stress[9 * s + k], a.delta) : 0.f;
   for (int p = 0; p < 3; ++p)
     for (int q = 0; q < 3; ++q)
       dM9[(int64_t)i * 9 + 3 * p + q] = in * 0.5f * (ds[3 * p + q] * G[3 * p + q] + ds[3 * q + p] * G[3 * q + p]);
   float cf = (float)(a.w_f / (3.0 * a.Ng));
-  for (int c = 0; c < 3; ++c) seedF[3 * i + c] = cf * dhuber(a.forces[3 * i + c] - a.l_forces[3 * i + c], a.delta);
+  for (int c = 0; c < 3; ++c)
+    seedF[3 * i + c] = a.l_forces ? cf * dhuber(a.forces[3 * i + c] - a.l_forces[3 * i + c], a.delta) : 0.f;
   double Mg = lossbuf[5];
-  d_mag[i] = (Mg > 0 && a.l_mask[i]) ? (float)(a.w_m / Mg) * dhuber(a.mag[i] - a.l_mag[i], a.delta) : 0.f;
+  d_mag[i] = (Mg > 0 && a.l_mag && (!a.l_mask || a.l_mask[i]))
+                 ? (float)(a.w_m / Mg) * dhuber(a.mag[i] - a.l_mag[i], a.delta) : 0.f;
 }
 
 __global__ void k_seed_edge(int64_t E, const int32_t *__restrict__ center, const float4 *__restrict__ vec,

@@ -273,15 +273,7 @@ __global__ void __launch_bounds__(1024) k_proj_reduce_f(const double *__restrict
   if (t == 0) dfreq[n] += (float)sh[0];
 }
 
-int sm_count_p() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return n;
-}
+int sm_count_p() { return device_sm_count(); }
 
 }  // namespace
 

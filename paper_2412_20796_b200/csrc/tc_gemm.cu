@@ -1,23 +1,32 @@
-// tc_gemm.cu — tcgen05 (5th-gen tensor core) version of the gathered row GEMM.
+// tc_gemm.cu — tcgen05 (5th-gen tensor core) GEMM engines of the GatedMLP contractions.
 //
-// Same contract as k_rowgemm (gemm.cuh): out[m, n] = epi(Σ_k A(m, k) W(k, n) + b)
-// with A gathered row by row from up to 4 tables.  One CTA = 128 rows (UMMA
-// M = 128, cta_group::1) and every output chunk; the fp32 accumulator lives in
-// TMEM (128 lanes × up to 256 columns) and is read back with tcgen05.ld (one
-// TMEM lane = one output row).
-//
-// Operands: kind::tf32 (round-to-nearest TF32), K-major, SWIZZLE_NONE canonical
-// layout: element (row, k) of an R-row tile at byte (k/4)·(R·16) + row·16 +
-// (k%4)·4 (core matrix 8 rows × 16 B; SBO = 128 B, LBO = R·16 B).
-//   B (weights): packed ONCE per GEMM into that exact smem image (k_pack_b,
-//     TF32-rounded, one image per K chunk) and streamed into smem with
-//     cp.async.bulk (TMA bulk copy, completion via mbarrier expect_tx).
-//   A (gathered activations): 256 threads, 8 lanes per row (coalesced 128-B
-//     row segments), registers prefetch the next K chunk while the tensor core
-//     runs the current one; 2-stage smem ring, tcgen05.commit -> mbarrier.
+// k_rowgemm_tc: out[m, n] = epi(Σ_k A(m, k) W(k, n) + b) with A gathered row by row from up to
+// 4 tables (the concatenations of Eq. 4 / Eq. 5-6 are never materialised).  Persistent, one CTA
+// per SM, 128-row tiles (UMMA M = 128, cta_group::1), fp32 accumulators double-buffered in TMEM.
+// Warp roles (18 warps):
+//   warps 0-3   A loaders: gathered rows by 16-B cp.async straight into SWIZZLE_128B K-major
+//               stage slots (row r's 32 tf32 at bytes [128r, 128r+128), 16-B unit u stored at
+//               u ^ (r & 7)); direct (non-gathered) segments by one TMA 2-D box per stage
+//   warps 4-7   converters: thread = row, SiLU (second GatedMLP layer) + TF32 rounding in place,
+//               fence.proxy.async, one mbarrier arrival per warp (skipped when the operand was
+//               written TF32-rounded by its producer: the MMA then waits on the TMA barrier)
+//   warp 8      weight image: cp.async.bulk of the packed K-major TF32 image (resident when it
+//               fits, else a 3-slot ring)
+//   warp 9      one thread issues tcgen05.mma.kind::tf32 and tcgen05.commit
+//   warps 10-17 epilogue: tcgen05.ld (lane = row) -> bias / dSiLU(mul) / residual in registers ->
+//               swizzled staging box -> TMA bulk tensor store (or TMA reduce-add store)
+// k_wgrad_tc: weight gradients Σ_m A(m, k) D(m, n), rows m as the MMA K dimension, per-CTA
+// partials reduced in a fixed order (reduce.cu).  See DESIGN.md §5.
+// Debug / timing knobs (CHG_TC_SKIP, per-CTA trace) exist only in -DCHG_TC_DEBUG builds.
 #include <cuda.h>
 
 #include "gemm.cuh"
+
+#ifdef CHG_TC_DEBUG
+#define TC_SKIP(bit) ((skip & (bit)) != 0)
+#else
+#define TC_SKIP(bit) (false)
+#endif
 
 namespace {
 
@@ -203,18 +212,11 @@ __global__ void k_pack_b(const RowGemm g, const TcPlan P, uint32_t *__restrict__
 
 
 // ---------------------------------------------------------------------------
-// warp-specialised persistent kernel
-//   warps 0-7   A producers: cp.async gather of 128 rows x 32 columns per stage
-//               straight into the UMMA layout, then in-place SiLU/TF32 rounding
-//   warp 8      B producer: cp.async.bulk of the packed weight image per stage
-//   warp 9      MMA issuer (one thread): tcgen05.mma into a double-buffered
-//               TMEM accumulator, tcgen05.commit -> stage / accumulator barriers
-//   warps 10-13 epilogue: tcgen05.ld (one lane = one row) -> bias / act /
-//               pre / mul / resid -> global
+// warp-specialised persistent row GEMM (warp roles: file header)
 // ---------------------------------------------------------------------------
 constexpr int NSA_MAX = 10;         // A stages (16 KB each): P.nsa <= NSA_MAX, as many as shared memory allows
 constexpr int NSB = 3;              // B stages (<= 32 KB each)
-constexpr int WS_THREADS = 18 * 32;  // 8 A-producer, 1 B, 1 MMA, 8 epilogue warps
+constexpr int WS_THREADS = 18 * 32;  // 4 loader, 4 converter, 1 B, 1 MMA, 8 epilogue warps
 constexpr int NEPI = 8;
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32_t src_bytes) {
@@ -330,7 +332,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
   }
   __shared__ uint64_t trace_ts[32], trace_ld[32], trace_cv[32], trace_mw[32], trace_ep[48];
   int nep = 0;
-  if ((skip & 32) && tid < 48) trace_ep[tid] = 0;
+  if (TC_SKIP(32) && tid < 48) trace_ep[tid] = 0;
   if (tid == 0) {
     for (int i = 0; i < NSA; ++i) { mbar_init(&fullA[i], 4); mbar_init(&emptyA[i], 1); mbar_init(&loaded[i], 128); }
     for (int i = 0; i < NSB; ++i) { mbar_init(&fullB[i], 1); mbar_init(&emptyB[i], 1); }
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   pdl_begin();                                    // the setup above overlaps the predecessor's tail
   const uint32_t tmem = *tslot;
-  if ((skip & 32) && tid == 0) {
+  if (TC_SKIP(32) && tid == 0) {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     trace_ts[0] = t;
@@ -409,14 +411,14 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
 #pragma unroll
         for (int sg = 0; sg < 4; ++sg)
           if (sg == seg) r = ridx[i][sg];
-        if (skip & 2) r = -1;                         // debug: no gather traffic
+        if TC_SKIP(2) r = -1;                         // debug: no gather traffic
         const int row = rb + 16 * i;
         const uint32_t dst = dst0 + row * 128 + ((q ^ (row & 7)) << 4);
         if (r >= 0) cp_async16(dst, S.base + (size_t)r * S.ld + cin, 16);
         else cp_async16(dst, g.A.seg[0].base, 0);     // zero fill
       }
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&loaded[sa])) : "memory");
-      if ((skip & 32) && tid == 0 && gi < 30) {       // debug trace: loader cadence
+      if (TC_SKIP(32) && tid == 0 && gi < 30) {       // debug trace: loader cadence
         uint64_t t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         trace_ld[gi] = t;
@@ -430,7 +432,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
       const int sa = gi % NSA, ua = gi / NSA;
       mbar_wait(&loaded[sa], ua & 1);
       uint4 *row = (uint4 *)(sA + sa * a_bytes + r * 128);
-      if (!(skip & 16)) {
+      if (!TC_SKIP(16)) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const int kk = (k + sw) & 7;                // rotated order: conflict-free banks
@@ -439,10 +441,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
           row[kk] = make_uint4(to_tf32(v.x), to_tf32(v.y), to_tf32(v.z), to_tf32(v.w));
         }
       }
-      if (!(skip & 64)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // debug knob 64: no fence
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic-proxy writes -> async proxy (MMA)
       __syncwarp();
       if (lane == 0) mbar_arrive(&fullA[sa]);        // one arrival per converter warp
-      if ((skip & 32) && tid == 128 && gi < 30) {     // debug trace: converter cadence
+      if (TC_SKIP(32) && tid == 128 && gi < 30) {     // debug trace: converter cadence
         uint64_t t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         trace_cv[gi] = t;
@@ -452,7 +454,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
     // ---------------- B producer ----------------
     if (lane == 0 && P.bres) {                          // whole image once: one barrier, nkc bulk copies
       if (total > 0) {
-        if (skip & 4) {
+        if TC_SKIP(4) {
           mbar_arrive(&fullB[0]);
         } else {
           mbar_expect_tx(&fullB[0], b_bytes * nkc);
@@ -464,7 +466,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
       for (int gi = 0; gi < total; ++gi) {
         const int kc = gi % nkc, sb = gi % NSB, ub = gi / NSB;
         if (ub > 0) mbar_wait(&emptyB[sb], (ub - 1) & 1);
-        if (skip & 4) {                                 // debug: no weight traffic
+        if TC_SKIP(4) {                                 // debug: no weight traffic
           mbar_arrive(&fullB[sb]);
         } else {
           mbar_expect_tx(&fullB[sb], b_bytes);
@@ -486,7 +488,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
           mbar_wait(P.noconv ? &loaded[sa] : &fullA[sa], ua & 1);
           if (!P.bres) mbar_wait(&fullB[sb], ub & 1);
           else if (gi == 0) mbar_wait(&fullB[0], 0);
-          if ((skip & 32) && gi < 30) {                // debug trace: operands ready
+          if (TC_SKIP(32) && gi < 30) {                // debug trace: operands ready
             uint64_t t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
             trace_mw[gi] = t;
@@ -504,14 +506,14 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
             for (int j = 0; j < KC / 8; ++j) {
               uint64_t ad = make_desc(a_base + j * 32, 16, 1024) | ((uint64_t)2 << 61);   // SWIZZLE_128B
               uint64_t bd = make_desc(b_base + j * 2 * (NT * 16) + P.coff[c] * 16, NT * 16, 128);
-              if (!(skip & 8))                            // debug: no tensor-core work
+              if (!TC_SKIP(8))                            // debug: no tensor-core work
                 mma_tf32(tmem + a * tcols + P.coff[c], ad, bd, idesc, (started[gr] || j > 0) ? 1u : 0u);
             }
             started[gr] = true;
           }
           mma_commit(&emptyA[sa]);
           if (!P.bres) mma_commit(&emptyB[sb]);
-          if ((skip & 32) && gi < 30) {                // debug trace: MMA-side cadence
+          if (TC_SKIP(32) && gi < 30) {                // debug trace: MMA-side cadence
             uint64_t t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
             trace_ts[gi + 1] = t;
@@ -519,7 +521,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
         }
         mma_commit(&tfull[a]);
       }
-      if (skip & 32) {
+      if TC_SKIP(32) {
         uint64_t t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         trace_ts[31] = t;
@@ -559,7 +561,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
         if (cc == c) tma_load_2d(smem_u32(obuf + sl * 1024), &TM.e[cc], mj[i], row0, &obar[sl]);
     };
     auto ep_mark = [&]() {
-      if ((skip & 32) && warp == 10 && lane == 0 && nep < 48) {
+      if (TC_SKIP(32) && warp == 10 && lane == 0 && nep < 48) {
         uint64_t t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         trace_ep[nep++] = t;
@@ -613,7 +615,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
 #pragma unroll
             for (int q = 0; q < 32; ++q) v[q] = C.mul ? v[q] * dsilu_fast(__ldg(op + q)) : v[q] + __ldg(op + q);
           }
-          if (skip & 1) continue;                       // debug: no epilogue stores
+          if TC_SKIP(1) continue;                       // debug: no epilogue stores
           // pass 0: out (TF32-rounded if round_out); pass 1: sout = tf32(SiLU(v))
           for (int pass = 0; pass < (C.sout ? 2 : 1); ++pass) {
             float *st = stg + (sc % TM.nst) * 1024;
@@ -674,7 +676,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
         const Chunk &C = g.ch[c];
         uint32_t r[32];
         tmem_ld32(tmem + lane_base + a * tcols + P.coff[c] + j0, r);
-        if (skip & 1) continue;                         // debug: no epilogue stores
+        if TC_SKIP(1) continue;                         // debug: no epilogue stores
 #pragma unroll
         for (int qq = 0; qq < 32; ++qq) stile[lane * 33 + qq] = __uint_as_float(r[qq]);
         __syncwarp();
@@ -714,7 +716,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if ((skip & 32) && blockIdx.x == 0 && tid == 0) {
+  if (TC_SKIP(32) && blockIdx.x == 0 && tid == 0) {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     printf("TRACE tiles %d nkc %d grid %d | start->chunk ends (us):", my_tiles, nkc, (int)gridDim.x);
@@ -828,7 +830,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
     const int nba = g.K / 32, nbd = g.N / 32, nb = nba + nbd;   // 32-column blocks
     const int njobs = nchunks * nb;
     auto row_of = [&](int j) -> int {
-      if (j >= njobs || (skip & 2)) return -1;
+      if (j >= njobs || TC_SKIP(2)) return -1;
       const int c = j / nb, b = j - c * nb;
       const int m = r0 + c * 32 + lane;
       if (m >= r1) return -1;
@@ -923,7 +925,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
           for (int j = 0; j < 4; ++j) {
             uint64_t ad = make_desc(baseA + tt * 16384 + j * 32, 16, 1024) | ((uint64_t)2 << 61);
             uint64_t bd = make_desc(baseD + j * 32, 16, 1024) | ((uint64_t)2 << 61);
-            if (!(skip & 8)) mma_tf32(tmem + tt * P.Npad, ad, bd, idesc, (c > 0 || j > 0) ? 1u : 0u);
+            if (!TC_SKIP(8)) mma_tf32(tmem + tt * P.Npad, ad, bd, idesc, (c > 0 || j > 0) ? 1u : 0u);
           }
         }
         mma_commit(&empty[s]);
@@ -1163,11 +1165,7 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
     fprintf(stderr, "rowgemm_tc %s: shared memory plan %zu B exceeds 224 KB\n", g.tag ? g.tag : "?", smem);
     return false;
   }
-  static bool attr = false;
-  if (!attr) {
-    CUDA_OK(cudaFuncSetAttribute(k_rowgemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
-    attr = true;
-  }
+  smem_optin((const void *)k_rowgemm_tc, 224 * 1024);
   double cols = 0;
   for (int c = 0; c < g.nchunk; ++c) cols += g.ch[c].ncols;
   // weight image: cached per (model, call site); all of a model's images are re-packed in
@@ -1214,16 +1212,7 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
     check_launch(ctx);
   }
   const int ntiles = ceil_div(g.M, TCM);
-  int sms = 148;
-  {
-    static int cached = 0;
-    if (!cached) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
-    }
-    sms = cached;
-  }
+  const int sms = device_sm_count();
   const int grid = std::min(ntiles, sms);
   double outb = 0;
   for (int c = 0; c < g.nchunk; ++c) {
@@ -1232,7 +1221,11 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   }
   ProfScope ps(ctx, g.tag ? g.tag : "rowgemm_tc", 2.0 * g.M * (double)g.K * cols,
                gemm_a_bytes(g.A, g.M, P.lo, P.lo + P.width) + (double)g.M * 4.0 * outb + 4.0 * g.K * cols);
+#ifdef CHG_TC_DEBUG
   static int skip = getenv("CHG_TC_SKIP") ? atoi(getenv("CHG_TC_SKIP")) : 0;   // debug knob (timing studies)
+#else
+  const int skip = 0;
+#endif
   static const bool no_tma = getenv("CHG_TC_NO_TMA") != nullptr;            // A/B knob (timing studies)
   for (int s = 0; s < g.A.nseg && !no_tma; ++s) {
     const ASeg &S = g.A.seg[s];
@@ -1277,12 +1270,7 @@ bool wgrad_tc(chg_ctx *ctx, const WGrad &g, float **partial_out, int *Kp_out, in
   const int cols = P.ktiles * P.Npad;
   if (cols > 512) return false;
   P.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = device_sm_count();
   const int chunks = (g.M + 31) / 32;
   const int grid = std::max(1, std::min(sms, chunks));
   P.rows_per_cta = (chunks + grid - 1) / grid * 32;
@@ -1291,12 +1279,12 @@ bool wgrad_tc(chg_ctx *ctx, const WGrad &g, float **partial_out, int *Kp_out, in
   const size_t st_bytes = (size_t)(P.Kpad + P.Npad) * 128;
   const size_t smem = 1024 + WG_NST * st_bytes + 8 * (2 * WG_NST + 1) + 16 + WG_NPW * 256 * 4;
   if (smem > 224 * 1024) return false;
-  static bool attr = false;
-  if (!attr) {
-    CUDA_OK(cudaFuncSetAttribute(k_wgrad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
-    attr = true;
-  }
+  smem_optin((const void *)k_wgrad_tc, 224 * 1024);
+#ifdef CHG_TC_DEBUG
   static int skip = getenv("CHG_TC_SKIP") ? atoi(getenv("CHG_TC_SKIP")) : 0;
+#else
+  const int skip = 0;
+#endif
   ProfScope ps(ctx, g.tag ? g.tag : "wgrad_tc", 2.0 * g.M * (double)P.Kp * g.N,
                gemm_a_bytes(g.A, g.M, 0, g.K) + (double)g.M * (4.0 * g.N + (g.didx ? 4.0 : 0.0)) + 4.0 * P.Kp * g.N);
   // partial as a 3-D tensor [splits][K][N] (row stride N, split stride Kp·N): TMA-store epilogue

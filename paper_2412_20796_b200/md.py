@@ -38,7 +38,9 @@ class NVE:
                     "forces": torch.zeros(n, 3, **f32), "stress": torch.zeros(S, 3, 3, **f32),
                     "magmom": torch.zeros(n, **f32)}
         self.steps = 0
+        torch.cuda.current_stream(dev).synchronize()   # state tensors written on torch's stream
         self._forces()
+        self.ctx.sync()
 
     def _forces(self):
         g = self.ctx.build_graph(self.ap, self.pos, self.lat, self.spec, self.r_atom, self.r_bond)
@@ -46,18 +48,22 @@ class NVE:
         g.close()
 
     def step(self, n: int = 1):
-        """n velocity-Verlet steps (graph rebuilt every step)."""
+        """n velocity-Verlet steps (graph rebuilt every step).  Returns after the work on the
+        ctx stream has finished, so pos / vel / out may be read or edited on any stream."""
         for _ in range(n):
             self.ctx.md_verlet(self.pos, self.vel, self.out["forces"], self.inv_m, self.dt, drift=True)
             self._forces()
             self.ctx.md_verlet(self.pos, self.vel, self.out["forces"], self.inv_m, self.dt, drift=False)
             self.steps += 1
+        self.ctx.sync()
 
-    # ---- observation (host copies) -------------------------------------------------
+    # ---- observation (host copies; wait for the ctx stream first) -------------------
     def potential_energy(self) -> np.ndarray:
+        self.ctx.sync()
         return self.out["energy"].double().cpu().numpy()
 
     def kinetic_energy(self) -> np.ndarray:
+        self.ctx.sync()
         v = self.vel.cpu().numpy()
         ke = 0.5 * self.mass[:, None] * v * v * EV_PER_AMU_A2_FS2
         return np.add.reduceat(ke.sum(1), self.ap[:-1]) if len(self.ap) > 1 else np.zeros(0)

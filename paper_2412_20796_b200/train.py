@@ -77,16 +77,24 @@ class Trainer:
         self._pos = 0                                 # next global batch in it
         self.builder = chg.Context(ctx.device) if prefetch else None
         self._pending = None                          # (struct ids, local batch, graph) built ahead
+        self._loads: Dict[int, int] = {}              # structure id -> atoms + edges + angles (static)
 
     def _local(self, batch, struct_ids, gctx):
         """This rank's share of a global batch (whole structures, chg_balance over ranks)."""
         glob = _take(batch, struct_ids)
         if self.world_size > 1:
-            g_all = gctx.build_graph(glob["atom_ptr"], glob["positions"], glob["lattice"], glob["species"],
-                                     self.r_atom, self.r_bond)
-            ps = g_all.per_struct()
-            g_all.close()
-            owner = chg.balance(ps[:, 0] + ps[:, 1] + ps[:, 3], self.world_size)
+            # the balancer's load (N + E + A, P:425) is a property of the structure: counted once per
+            # structure of the dataset (one graph build of the not-yet-seen ones), then cached
+            missing = sorted({int(k) for k in struct_ids if int(k) not in self._loads})
+            if missing:
+                part = _take(batch, missing)
+                g_new = gctx.build_graph(part["atom_ptr"], part["positions"], part["lattice"], part["species"],
+                                         self.r_atom, self.r_bond)
+                ps = g_new.per_struct()
+                g_new.close()
+                for k, sid in enumerate(missing):
+                    self._loads[sid] = int(ps[k, 0] + ps[k, 1] + ps[k, 3])
+            owner = chg.balance(np.array([self._loads[int(k)] for k in struct_ids], np.int64), self.world_size)
             mine = [struct_ids[k] for k in range(len(struct_ids)) if owner[k] == self.rank]
             return glob, _take(batch, mine)
         return glob, glob
