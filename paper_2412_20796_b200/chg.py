@@ -135,6 +135,10 @@ def _on_device(x) -> bool:
     return hasattr(x, "is_cuda") and bool(x.is_cuda)
 
 
+# chg_model_cfg.mlp_precision values this build implements (include/chg.h)
+PRECISION_MODES = {0: "fp32", 2: "tf32"}
+
+
 def default_model_cfg() -> ModelCfg:
     """d = 64, 31 radial / angular bases, p = 8; three interaction blocks
     plus a final atom conv (reading Q17); GatedMLP hidden 64 (Q12); 94 species (Q28)."""

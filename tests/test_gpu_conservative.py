@@ -49,7 +49,7 @@ def _rel(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-12)
 
 
-@pytest.mark.parametrize("prec", [0, 2])
+@pytest.mark.parametrize("prec", sorted(chg.PRECISION_MODES))
 @pytest.mark.parametrize("case", list(CASES))
 def test_conservative_forces_stress(ctx, params, case, prec):
     b = CASES[case]()
@@ -63,7 +63,8 @@ def test_conservative_forces_stress(ctx, params, case, prec):
     F, S = ref["forces"].detach().numpy(), ref["stress"].detach().numpy()
     E = ref["energy"].detach().numpy()
     natoms = np.diff(b.atom_ptr)
-    if prec == 0:
+    if prec != 2:      # fp32 strict and 3xTF32: the NS F / sigma / E bars
+                       # (TF32: F and sigma are position / strain GRADIENTS: NS-loosened 2e-3 relative)
         assert np.max(np.abs(out["forces"] - F)) <= 1e-4, np.max(np.abs(out["forces"] - F))
         assert np.max(np.abs(out["stress"] - S)) <= 1e-4, np.max(np.abs(out["stress"] - S))
         epa = E / natoms

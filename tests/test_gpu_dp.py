@@ -36,6 +36,10 @@ def test_dp_allreduce_matches_single_gpu(prec):
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert lines, r.stdout[-2000:] + r.stderr[-2000:]
     res = json.loads(lines[-1])
+    out = os.path.join(ROOT, "gpurun_out")
+    if os.path.isdir(out):                    # kept under profiles/ as the multi-GPU evidence
+        with open(os.path.join(out, f"dp_check_ws{ws}_prec{prec}.json"), "w") as f:
+            json.dump(res, f)
     assert res["params_identical_across_ranks"], res
     assert res["grad_rel_err_vs_1gpu"] <= res["tol"], res
     assert res["loss_rel_err_vs_1gpu"] <= 1e-5, res

@@ -1,8 +1,9 @@
 """GPU parity of the TF32 tensor-core mode (mlp_precision = 2, tcgen05) against
 the fp64 oracle.  NS: gradients relative <= 2e-3 when TF32/BF16 MLPs are
-enabled (reported separately).  Forward bars for this mode (DESIGN.md
-"Tolerances"): features ‖Δ‖/‖ref‖ <= 2e-3, E/atom |Δ| <= 2e-3·max(|ε|, 1 eV),
-F <= 2e-3 eV/Å, σ <= 2e-3 GPa, m <= 2e-3 μB."""
+enabled (reported separately).  NS loosens only the gradients: the outputs keep the
+strict bars E/atom |Δ| <= 1e-5·max(|ε|, 1 eV), F <= 1e-4 eV/Å, σ <= 1e-4 GPa; magmom
+<= 2e-4 μB (stated for this mode: m is a linear map of v⁴, whose TF32 feature error is
+~1e-5 relative; measured 5.9e-5).  Intermediate features ‖Δ‖/‖ref‖ <= 2e-3."""
 import json
 import os
 
@@ -76,8 +77,8 @@ def test_tf32_forward(ctx, params, case):
     rep["stress_abs"] = float(np.max(np.abs(out["stress"] - ref["stress"].detach().numpy())))
     rep["magmom_abs"] = float(np.max(np.abs(out["magmom"] - ref["magmom"].detach().numpy())))
     REPORT[f"forward_{case}"] = rep
-    assert rep["epa_abs"] <= 2e-3 and rep["forces_abs"] <= 2e-3
-    assert rep["stress_abs"] <= 2e-3 and rep["magmom_abs"] <= 2e-3
+    assert rep["epa_abs"] <= 1e-5 and rep["forces_abs"] <= 1e-4
+    assert rep["stress_abs"] <= 1e-4 and rep["magmom_abs"] <= 2e-4
 
 
 @pytest.mark.parametrize("case", list(CASES))
