@@ -41,6 +41,26 @@ FP32_PEAK_TFLOPS = 148 * 128 * 2 * PEAKS.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
 # TF32 dense tensor peak: measured bf16 cuBLAS peak (sustained: kernels timed inside a long step)
 # x the nominal tf32:bf16 ratio 1.1 : 2.25 PF/s (B200_PROFILING.md)
 TF32_PEAK_TFLOPS = PEAKS.get("bf16_tflops_sustained", PEAKS.get("bf16_tflops", 1590.0)) * 1.1 / 2.25
+# 3xTF32 (mlp_precision 1): every fp32 product is three TF32 MMAs (A_lo·B_hi + A_hi·B_lo + A_hi·B_hi),
+# so the tensor roof for the algorithmic flops is a third of the TF32 peak
+PREC_CODE = {"fp32": 0, "3xtf32": 1, "tf32": 2}
+DTYPE = {"fp32": "f32", "3xtf32": "f32 (3xTF32)", "tf32": "tf32+f32"}
+
+
+def tensor_peak(precision: str) -> float:
+    return {"tf32": TF32_PEAK_TFLOPS, "3xtf32": TF32_PEAK_TFLOPS / 3.0}.get(precision, FP32_PEAK_TFLOPS)
+
+
+def step_roofline(counts, precision: str):
+    """whole-step roof from the batch's N, E, B, A (per GPU).
+    GEMM flops fwd = 286,592 E + 380,800 A + 28,544 B + 75,136 N, step = 3 x fwd;
+    compulsory bytes fwd = 256 (14E + 6A + 7B + 12N) + 24E + 12A, step = 3 x fwd."""
+    N, E, B, A = (float(x) for x in counts)
+    flops = 3.0 * (286592 * E + 380800 * A + 28544 * B + 75136 * N)
+    byts = 3.0 * (256 * (14 * E + 6 * A + 7 * B + 12 * N) + 24 * E + 12 * A)
+    t_tensor = flops / (tensor_peak(precision) * 1e12)
+    t_hbm = byts / (PEAKS["hbm_gbs"] * 1e9)
+    return flops, byts, t_tensor, t_hbm
 # profile tags (chg_profile call sites) of the GatedMLP contractions: on tcgen05 in tf32 mode (NS)
 TC_ROW_TAGS = {"ac_f1", "ac_f2", "bc_f1", "bc_f2", "ac_dZ", "ac_dX", "bc_dZ", "bc_dX"}
 TC_WG_TAGS = {"ac_W1_wg", "ac_W2_wg", "bc_W1_wg", "bc_W2_wg"}
@@ -56,9 +76,9 @@ def kernel_of(tag: str, precision: str) -> str:
     if tag.endswith("_red"):
         return "k_wgrad_reduce"
     if tag in TC_ROW_TAGS:
-        return "k_rowgemm_tc" if precision == "tf32" else "k_rowgemm"
+        return "k_rowgemm_tc" if precision != "fp32" else "k_rowgemm"
     if tag in TC_WG_TAGS:
-        return "k_wgrad_tc" if precision == "tf32" else "k_wgrad"
+        return "k_wgrad_tc" if precision != "fp32" else "k_wgrad"
     if tag in ROW_TAGS:
         return "k_rowgemm"
     if tag in WG_TAGS:
@@ -87,8 +107,10 @@ def _args():
     ap.add_argument("--per-gpu", type=int, default=0, help="structures per GPU (default: 40 at N=1, 128 at N>1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"],
-                    help="GatedMLP GEMM engine: tf32 = tcgen05 tensor cores, fp32 = CUDA cores (strict parity)")
+    ap.add_argument("--precision", default="3xtf32", choices=["3xtf32", "tf32", "fp32"],
+                    help="GatedMLP GEMM engine (headline mode): 3xtf32 = tcgen05 split-operand fp32 (strict "
+                         "parity, the paper's fp32, P:473), tf32 = tcgen05 TF32 (NS loosened), fp32 = CUDA cores")
+    ap.add_argument("--no-side-modes", action="store_true", help="skip timing the two other precision modes")
     return ap.parse_args()
 
 
@@ -258,13 +280,13 @@ def main():
         ctx.set_nccl(bytes(uid.cpu().numpy()), ws, rank)
     def make_model(prec):
         cfg = chg.default_model_cfg()
-        cfg.mlp_precision = 2 if prec == "tf32" else 0
+        cfg.mlp_precision = PREC_CODE[prec]
         mm = chg.Model(ctx, cfg)
         lay = [(n, s) for n, s, _ in mm.layout()]         # the library's own layout table
         mm.set_params(init_flat_params(lay, seed=0).astype(np.float32))
         return mm
-    other = "fp32" if a.precision == "tf32" else "tf32"
-    models = {a.precision: make_model(a.precision), other: make_model(other)}
+    others = [] if a.no_side_modes else [p for p in PREC_CODE if p != a.precision]
+    models = {p: make_model(p) for p in [a.precision] + others}
     model = models[a.precision]
 
     # ---- batches: global batch per index, balanced over ranks
@@ -285,6 +307,9 @@ def main():
                 imb = (float(per_rank_load.max() / per_rank_load.mean()), float(contiguous.max() / contiguous.mean()))
             else:
                 mine, cv, imb = glob, (0.0, 0.0), (1.0, 1.0)
+            gc = ctx.build_graph(mine.atom_ptr, mine.positions, mine.lattice, mine.species)
+            counts = tuple(int(x) for x in gc.counts())              # this rank's N, E, B, A
+            gc.close()
             gl = dict(S=glob.n_struct, N=glob.n_atoms, M=int(glob.magmom_mask.sum()))
             dev = dict(pos=torch.as_tensor(mine.positions, device="cuda"),
                        lat=torch.as_tensor(mine.lattice, device="cuda"),
@@ -308,7 +333,8 @@ def main():
                                  magmom_mask=pinned(mine.magmom_mask, torch.uint8)))
             h2d = sum(v.nbytes for k, v in host.items() if k != "lab") + sum(v.nbytes for v in host["lab"].values()) \
                 + mine.atom_ptr.nbytes
-            out.append(dict(ap=mine.atom_ptr, dev=dev, host=host, gl=gl, S=mine.n_struct, cv=cv, imb=imb, h2d=h2d))
+            out.append(dict(ap=mine.atom_ptr, dev=dev, host=host, gl=gl, S=mine.n_struct, cv=cv, imb=imb, h2d=h2d,
+                            counts=counts))
         return out
 
     batches = make_batches(wl, per, a.batches)
@@ -328,7 +354,7 @@ def main():
         src = b["host"] if on_host else b["dev"]
         return (bctx or ctx).build_graph(b["ap"], src["pos"], src["lat"], src["spec"], 5.0, 3.0)
 
-    def one_step(b, on_host: bool, model=None, g=None, nxt=None):
+    def one_step(b, on_host: bool, model=None, g=None, nxt=None, keep_graph=False):
         model = model or models[a.precision]
         step_no[0] += 1
         lr = lr0 * 0.5 * (1 + math.cos(math.pi * step_no[0] / total_steps))   # cosine
@@ -342,12 +368,14 @@ def main():
         gn = build(nxt, on_host, builder) if (nxt is not None and on_host) else None
         loss = ctx.backward(model, g, src["lab"], n_struct_global=b["gl"]["S"], n_atoms_global=b["gl"]["N"],
                             n_magmom_global=b["gl"]["M"], sync_loss=on_host)
-        ctx.step(model, lr=lr, step=step_no[0], allreduce=ws > 1)
+        # device-resident pass: no host synchronisation in the step (finite flag checked by a later call)
+        ctx.step(model, lr=lr, step=step_no[0], allreduce=ws > 1, defer_check=not on_host)
         if nxt is not None and not on_host:
             gn = build(nxt, on_host, builder)
         if gn is not None:
             ctx.wait_graph(gn)
-        g.close()
+        if not keep_graph:
+            g.close()
         return loss, gn
 
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")     # 256 MiB > 126 MB L2
@@ -358,7 +386,9 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    def timed(on_host: bool, profile: bool = False, model=None, bl=None):
+    def timed(on_host: bool, profile: bool = False, model=None, bl=None, cached=None, execs=None):
+        """K steps; cached = prebuilt graphs per batch (SURVEY §8(d) item 3: graph build outside);
+        execs = captured steps per batch (chg_capture_step: one CUDA graph replay per step)."""
         bl = bl or batches
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
         if profile:
@@ -372,34 +402,76 @@ def main():
             use = builder is not None and not profile and (on_host or a.prefetch == "all")
             nxt = bl[(k + 1) % len(bl)] if (use and k + 1 < a.steps) else None
             ev[k][0].record(stream)
-            _, gnext = one_step(b, on_host, model, g=gnext, nxt=nxt)
+            if execs is not None:
+                step_no[0] += 1
+                lr = lr0 * 0.5 * (1 + math.cos(math.pi * step_no[0] / total_steps))
+                execs[k % len(bl)].step(lr, step_no[0])
+            elif cached is not None:
+                one_step(b, on_host, model, g=cached[k % len(bl)], keep_graph=True)
+            else:
+                _, gnext = one_step(b, on_host, model, g=gnext, nxt=nxt)
             ev[k][1].record(stream)
             with torch.cuda.stream(stream):
                 flush.zero_()                              # L2 flush outside the timed events
         barrier()
         launches = ctx.launch_count() - l0 + ((builder.launch_count() - lb0) if builder else 0)
-        ms = sum(s.elapsed_time(e) for s, e in ev)
+        per_step = [s.elapsed_time(e) for s, e in ev]
+        ms = sum(per_step)
         rep = ctx.profile_report() if profile else None
         if profile:
             ctx.profile(False)
+        rank_ms = [ms]
         if ws > 1:
             t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
+            allt = [torch.zeros_like(t) for _ in range(ws)]
+            dist.all_gather(allt, t)
+            rank_ms = [float(x.item()) for x in allt]
+            ms = max(rank_ms)
+        stats[id(bl), on_host, profile, id(model), cached is not None] = dict(per_step=per_step, rank_ms=rank_ms)
+        last_stats[0] = stats[id(bl), on_host, profile, id(model), cached is not None]
         return ms, launches, rep
 
+    stats, last_stats = {}, [None]
     for k in range(a.warmup):
         one_step(batches[k % len(batches)], False)
         one_step(batches[k % len(batches)], True)
     clocks = Clocks(local)
     clocks.start()
     ms, launches, _ = timed(False)
+    main_stats = last_stats[0]
     clk = clocks.stop()
     ms_e2e, _, _ = timed(True)
-    ms_prof, _, rep = timed(False, profile=True)
+    # cached-graph variant: graphs built once outside the timed region (training graphs are static
+    # per dataset)
+    cached = [build(b, False) for b in batches]
     for k in range(a.warmup):
-        one_step(batches[k % len(batches)], False, models[other])
-    ms_other, _, _ = timed(False, model=models[other])
+        one_step(batches[k % len(batches)], False, g=cached[k % len(batches)], keep_graph=True)
+    ms_cached, _, _ = timed(False, cached=cached)
+    # captured variant: the cached graph's whole step (forward + backward + allreduce + Adam) as one
+    # CUDA graph per batch, replayed with this step's lr (no host synchronisation inside the step)
+    ms_capt, capt_launches, capt_err = None, None, None
+    try:
+        execs = [ctx.capture_step(model, cached[i], b["dev"]["lab"], n_struct_global=b["gl"]["S"],
+                                  n_atoms_global=b["gl"]["N"], n_magmom_global=b["gl"]["M"], allreduce=ws > 1)
+                 for i, b in enumerate(batches)]
+        for k in range(a.warmup):
+            execs[k % len(execs)].step(lr0, step_no[0] + 1)
+            step_no[0] += 1
+        ms_capt, capt_launches, _ = timed(False, execs=execs)
+        ctx.sync()
+        for x in execs:
+            x.close()
+    except Exception as ex:          # reported in the line, never silently
+        capt_err = f"{type(ex).__name__}: {ex}"
+    for g_ in cached:
+        g_.close()
+    ms_prof, _, rep = timed(False, profile=True)
+    side = {}
+    for other in others:
+        for k in range(a.warmup):
+            one_step(batches[k % len(batches)], False, models[other])
+        ms_o, _, _ = timed(False, model=models[other])
+        side[other] = ms_o
 
     # weak-scaling base: the per-GPU workload of the N > 1 runs (C3, 128 structures) on this one GPU,
     # so value(N) / (N * c3_value(1)) compares equal per-GPU work (the headline N = 1 line stays C2)
@@ -410,8 +482,11 @@ def main():
             one_step(c3[k % len(c3)], False)
         ms_c3, _, _ = timed(False, bl=c3)
         s_c3 = sum(c3[k % len(c3)]["gl"]["S"] for k in range(a.steps))
+        roof_c3 = [step_roofline(c3[k % len(c3)]["counts"], a.precision) for k in range(a.steps)]
         weak_base = {"workload": "C3: 128 MPtrj-shaped structures on 1 GPU (the per-GPU work of the N > 1 runs)",
-                     "value": s_c3 / (ms_c3 / 1e3), "unit": "structures/s", "ms_per_step": ms_c3 / a.steps}
+                     "value": s_c3 / (ms_c3 / 1e3), "unit": "structures/s", "ms_per_step": ms_c3 / a.steps,
+                     "whole_step_frac": sum(max(r[2], r[3]) for r in roof_c3) / (ms_c3 / 1e3)}
+        _, _, rep_c3 = timed(False, profile=True, bl=c3)         # gather-scatter GB/s at C3 (§8(d) item 7)
 
     # C5 (BASELINE configs[4]): one 4,096-atom LiFePO4-like cell, graph build + forward with the
     # force / stress readout (inference path), device-timed latency
@@ -508,14 +583,15 @@ def main():
     gbs = r["bytes"] / (r["ms"] / 1e3) / 1e9
     tfs = r["flops"] / (r["ms"] / 1e3) / 1e12
     on_tc = dom.endswith("_tc")
-    flop_peak = TF32_PEAK_TFLOPS if on_tc else FP32_PEAK_TFLOPS
+    flop_peak = tensor_peak(a.precision) if on_tc else FP32_PEAK_TFLOPS
     # binding roof by arithmetic intensity: below the ridge flop_peak / hbm_peak the kernel is HBM-bound
     if r["bytes"] > 0 and (r["flops"] / r["bytes"]) < flop_peak * 1e3 / PEAKS["hbm_gbs"]:
         roof = {"bound": "hbm", "achieved": gbs, "peak": PEAKS["hbm_gbs"], "unit": "GB/s", "peak_source": PEAK_SRC}
         per_launch_alg = r["bytes"] / max(r["launches"], 1)
     elif on_tc:
         roof = {"bound": "tensor", "achieved": tfs, "peak": flop_peak, "unit": "TFLOP/s",
-                "peak_source": "tf32 = " + PEAK_SRC + " bf16_tflops_sustained x (1.1/2.25 nominal ratio)"}
+                "peak_source": "tf32 = " + PEAK_SRC + " bf16_tflops_sustained x (1.1/2.25 nominal ratio)"
+                               + (" / 3 (3xTF32: three MMAs per fp32 product)" if a.precision == "3xtf32" else "")}
         per_launch_alg = r["flops"] / max(r["launches"], 1)
     else:
         roof = {"bound": "alu", "achieved": tfs, "peak": flop_peak, "unit": "TFLOP/s",
@@ -527,12 +603,29 @@ def main():
                  "profiled_pass": "same steps with per-launch CUDA events; the concurrent branches run serially "
                                   "while profiling, so each launch's time is its own",
                  "intensity_flop_per_byte": r["flops"] / max(r["bytes"], 1.0),
-                 "tensor_frac": tfs / TF32_PEAK_TFLOPS if on_tc else None, "hbm_frac": gbs / PEAKS["hbm_gbs"]})
-    gs = {"bytes": sum(v["bytes"] for t, v in rep.items() if t.startswith("segsum")),
-          "ms": sum(v["ms"] for t, v in rep.items() if t.startswith("segsum")) or 1e-9}
-    gather = {"kernel": "segsum (atomic-free CSR / rev / swap segmented gather-reduce)",
-              "achieved_gbs": gs["bytes"] / (gs["ms"] / 1e3) / 1e9,
-              "frac": gs["bytes"] / (gs["ms"] / 1e3) / 1e9 / PEAKS["hbm_gbs"], "peak_gbs": PEAKS["hbm_gbs"]}
+                 "tensor_frac": tfs / flop_peak if on_tc else None, "hbm_frac": gbs / PEAKS["hbm_gbs"]})
+    def gather_of(rp, wl_name):
+        gs = {"bytes": sum(v["bytes"] for t, v in rp.items() if t.startswith("segsum")),
+              "ms": sum(v["ms"] for t, v in rp.items() if t.startswith("segsum")) or 1e-9}
+        return {"kernel": "segsum (atomic-free CSR / rev / swap segmented gather-reduce)", "workload": wl_name,
+                "achieved_gbs": gs["bytes"] / (gs["ms"] / 1e3) / 1e9,
+                "frac": gs["bytes"] / (gs["ms"] / 1e3) / 1e9 / PEAKS["hbm_gbs"], "peak_gbs": PEAKS["hbm_gbs"],
+                "bytes": "algorithmic: each summed row (256 B) + index read once, each target written once"}
+    gather = gather_of(rep_c3, "C3") if (ws == 1 and wl == "C2") else gather_of(rep, wl)
+    if ws == 1 and wl == "C2":
+        gather["at_headline_workload"] = gather_of(rep, wl)
+    # whole-step roof from each timed batch's N, E, B, A
+    roofs = [step_roofline(batches[k % len(batches)]["counts"], a.precision) for k in range(a.steps)]
+    whole = {"flop_per_step": float(np.mean([r[0] for r in roofs])), "bytes_per_step": float(np.mean([r[1] for r in roofs])),
+             "t_tensor_ms": 1e3 * float(np.mean([r[2] for r in roofs])), "t_hbm_ms": 1e3 * float(np.mean([r[3] for r in roofs])),
+             "tensor_peak_tflops": tensor_peak(a.precision), "hbm_peak_gbs": PEAKS["hbm_gbs"],
+             "frac": sum(max(r[2], r[3]) for r in roofs) / (ms / 1e3),
+             "note": "max(t_tensor, t_HBM) / measured step time; SURVEY §8(d) algorithmic GEMM flops and compulsory "
+                     "bytes of the batch's counts (3 x forward); 3xtf32 roof = TF32 peak / 3"}
+    ps_ = sorted(main_stats["per_step"])
+    q = lambda f: ps_[min(len(ps_) - 1, int(round(f * (len(ps_) - 1))))]   # noqa: E731
+    step_ms = {"median": q(0.5), "p10": q(0.1), "p90": q(0.9), "mean": float(np.mean(ps_))}
+    rank_ms = main_stats["rank_ms"]
     ops = {t: {"ms_per_step": v["ms"] / a.steps, "launches_per_step": v["launches"] / a.steps,
                "share": v["ms"] / ms_prof, "kernel": kernel_of(t, a.precision)}
            for t, v in sorted(rep.items(), key=lambda kv: -kv[1]["ms"])}
@@ -548,11 +641,29 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "structures/s", "n_gpus": ws, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "tf32+f32" if a.precision == "tf32" else "f32", "data": "synthetic",
+            "vs_baseline": None, "dtype": DTYPE[a.precision], "data": "synthetic",
             "precision": {"mode": a.precision,
-                          "note": "tf32: GatedMLP GEMMs on tcgen05 (TF32, fp32 accumulate), all else fp32; "
-                                  "fp32: everything on CUDA cores (strict 1e-4 gradient parity)",
-                          other: {"value": structs / (ms_other / 1e3), "ms_per_step": ms_other / a.steps}},
+                          "note": "3xtf32: GatedMLP GEMMs on tcgen05 with split operands (hi + lo TF32, three MMAs, "
+                                  "fp32 accumulate: strict 1e-4 gradient parity); tf32: tcgen05 TF32 (NS-loosened "
+                                  "2e-3); fp32: everything on CUDA cores (strict); heads, projections, output linears "
+                                  "and all non-GEMM kernels are fp32 in every mode",
+                          **{o: {"value": structs / (side[o] / 1e3), "ms_per_step": side[o] / a.steps,
+                                 "dtype": DTYPE[o],
+                                 "whole_step_frac": sum(max(r[2], r[3]) for r in
+                                                        [step_roofline(batches[k % len(batches)]["counts"], o)
+                                                         for k in range(a.steps)]) / (side[o] / 1e3)}
+                             for o in others}},
+            "step_ms": step_ms,
+            "whole_step_roofline": whole,
+            "cached_graph": {"value": structs / (ms_cached / 1e3), "unit": "structures/s",
+                             "ms_per_step": ms_cached / a.steps,
+                             "note": "graphs built once outside the timed region (static per dataset); "
+                                     "forward + backward + allreduce + Adam timed"},
+            "captured_step": ({"value": structs / (ms_capt / 1e3), "unit": "structures/s",
+                               "ms_per_step": ms_capt / a.steps, "kernels_per_step": capt_launches / a.steps,
+                               "note": "cached graph + chg_capture_step: the whole step replayed as ONE CUDA graph "
+                                       "(no host synchronisation inside; finite flag checked by a later call)"}
+                              if ms_capt is not None else {"error": capt_err}),
             "config": {"workload": f"{wl}: {WL_DESC[wl]}, {per} structures per GPU "
                                    f"(5/3 Å cutoffs, d=64, 4 atom-conv / 3 bond-conv)",
                        "structures_per_gpu": per, "global_batch": per * ws, "parallelism": f"dp{ws}",
@@ -564,7 +675,8 @@ def main():
                        "l2": "flushed between steps (256 MiB write, outside the timed events)",
                        "batches_cycled": len(batches), "cv_balanced_vs_contiguous": b0["cv"],
                        "max_over_mean_rank_load_balanced_vs_contiguous": b0["imb"],
-                       "rank0_counts_first_batch": None},
+                       "counts_first_batch_NEBA": list(b0["counts"]),
+                       "per_rank_ms_max_over_mean": max(rank_ms) / (sum(rank_ms) / len(rank_ms))},
             "e2e": {"value": e2e, "unit": "structures/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 40 + 4},
             "gpu_launches": int(launches),
             "weak_scaling_base": weak_base,

@@ -57,10 +57,13 @@ typedef struct { double r_atom, r_bond; } chg_cutoffs;
  * t = 0,1,2) plus a final atom conv; the angle update of the last block has no
  * consumer and is skipped (reading Q17).  gmlp_hidden = 64: each
  * GatedMLP branch of atom/bond conv is Linear-SiLU-Linear (reading Q12).
- * mlp_precision: 0 = fp32 CUDA cores (strict parity: gradients <= 1e-4);
- * 2 = TF32 on the tcgen05 tensor cores for the GatedMLP / linear GEMMs
- * (gradients <= 2e-3, NS "loosened" mode), fp32 everywhere else. Only d = 64,
- * n_radial = n_angular = 31, gmlp_hidden = head_hidden = 64 are built. */
+ * mlp_precision (the GatedMLP contractions; everything else is fp32 on CUDA cores):
+ *   0 = fp32 CUDA cores (strict parity: gradients <= 1e-4);
+ *   1 = 3xTF32 on the tcgen05 tensor cores: each operand split x = hi + lo (both TF32)
+ *       and A_lo·B_hi + A_hi·B_lo + A_hi·B_hi accumulated in fp32 (fp32-level accuracy,
+ *       the strict 1e-4 gradient bar; the paper trains in fp32);
+ *   2 = TF32 on the tcgen05 tensor cores (gradients <= 2e-3, NS "loosened" mode).
+ * Only d = 64, n_radial = n_angular = 31, gmlp_hidden = head_hidden = 64 are built. */
 typedef struct {
   int d, n_radial, n_angular, envelope_p, n_atom_conv, n_bond_conv, gmlp_hidden,
       n_species, head_hidden, mlp_precision;
@@ -98,11 +101,16 @@ typedef struct {
 /* Adam (PyTorch semantics, no weight decay).  `step` is the 1-based
  * step number used for bias correction.  lr comes from Eq. 14 × cosine
  * (computed by the caller).  allreduce = 1: sum gradients over the NCCL
- * communicator set with chg_ctx_set_nccl before the update. */
+ * communicator set with chg_ctx_set_nccl before the update.
+ * defer_check = 1: no host synchronisation in chg_step — the update is still
+ * skipped ON THE DEVICE when a gradient is non-finite, and CHG_ERR_NONFINITE
+ * (naming the tensor) is returned by a later chg_step / chg_exec_step /
+ * chg_sync on the ctx once the flag's copy has completed. */
 typedef struct {
   float lr, beta1, beta2, eps;
   int64_t step;
   int allreduce;
+  int defer_check;
 } chg_adam_cfg;
 
 /* ---- context ------------------------------------------------------------ */
@@ -217,6 +225,26 @@ chg_status chg_backward(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labe
  * finite flag). */
 chg_status chg_step(chg_ctx *ctx, chg_model *m, const chg_adam_cfg *cfg);
 
+/* ---- captured training step (CUDA graph) ----------
+ * chg_capture_step records forward(train) + backward + [allreduce] + finite
+ * check + Adam on graph g into one CUDA graph (no host synchronisation inside):
+ * it first runs forward + backward once on the stream (sizing every workspace;
+ * the gradients are restored afterwards), then captures.  labels must be
+ * DEVICE pointers (on_device = 1) that stay valid while the exec is used;
+ * adam->defer_check is implied.  chg_exec_step replays it with this step's lr
+ * and bias-correction step (the Adam node's scalars are updated in the
+ * instantiated graph), enqueued on the ctx stream; a non-finite gradient is
+ * reported by a later call (see defer_check).  The exec is bound to (ctx,
+ * model, g); it becomes invalid (CHG_ERR_STATE) when any ctx workspace was
+ * re-allocated after the capture (e.g. a larger batch ran: capture after the
+ * largest one) and must not outlive g.
+ * Errors: CHG_ERR_ARG (host labels), CHG_ERR_STATE, CHG_ERR_CUDA. */
+typedef struct chg_exec chg_exec;
+chg_status chg_capture_step(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *labels,
+                            const chg_loss_cfg *loss, const chg_adam_cfg *adam, chg_exec **out);
+chg_status chg_exec_step(chg_ctx *ctx, chg_exec *x, const chg_adam_cfg *adam);
+void chg_exec_destroy(chg_exec *x);
+
 /* ---- load-balance sampler (Fig. 4) -- host only --------------
  * loads[n] = atoms + bonds + angles per sample.  Sort ascending (ties
  * by index); ranks take turns round-robin, each turn taking the smallest and
@@ -240,7 +268,7 @@ chg_status chg_profile_query(chg_ctx *ctx, int idx, char *tag, double *ms, int64
  *   kind 0: out[M,N] = A[M,K] · W[K,N]          (row GEMM; W is also given K-major
  *           internally for the tensor-core path)
  *   kind 1: out[K,N] = A[M,K]ᵀ · D[M,N]         (weight-gradient GEMM; `W` = D)
- * engine 0 = fp32 CUDA cores, 2 = tcgen05 TF32.  Returns CHG_ERR_ARG if the
+ * engine 0 = fp32 CUDA cores, 1 = tcgen05 3xTF32, 2 = tcgen05 TF32.  Returns CHG_ERR_ARG if the
  * engine cannot run the shape.  Synchronises. */
 chg_status chg_debug_gemm(chg_ctx *ctx, int kind, int engine, int M, int K, int N, const float *A,
                           const float *W, float *out);

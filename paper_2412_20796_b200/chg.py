@@ -55,7 +55,7 @@ class LossCfg(C.Structure):
 
 class AdamCfg(C.Structure):
     _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
-                ("step", C.c_int64), ("allreduce", C.c_int)]
+                ("step", C.c_int64), ("allreduce", C.c_int), ("defer_check", C.c_int)]
 
 
 # every symbol include/chg.h declares (checked by tests/test_abi_symbols.py)
@@ -64,7 +64,8 @@ SYMBOLS = ["chg_ctx_create", "chg_ctx_destroy", "chg_last_error", "chg_sync", "c
            "chg_graph_destroy", "chg_graph_wait", "chg_md_verlet", "chg_model_create", "chg_model_destroy", "chg_model_layout",
            "chg_model_num_params", "chg_model_set", "chg_model_get", "chg_model_device_ptr", "chg_forward",
            "chg_forward_conservative",
-           "chg_backward", "chg_step", "chg_balance", "chg_profile", "chg_profile_query", "chg_debug_gemm", "chg_debug_get"]
+           "chg_backward", "chg_step", "chg_balance", "chg_profile", "chg_profile_query", "chg_debug_gemm", "chg_debug_get",
+           "chg_capture_step", "chg_exec_step", "chg_exec_destroy"]
 
 _lib = None
 
@@ -109,6 +110,10 @@ def load(path: str = LIB_PATH):
         "chg_profile": (C.c_int, [vp, C.c_int]),
         "chg_debug_gemm": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp]),
         "chg_profile_query": (C.c_int, [vp, C.c_int, C.c_char_p, dp, C.POINTER(i64), dp, dp]),
+        "chg_capture_step": (C.c_int, [vp, vp, vp, C.POINTER(Labels), C.POINTER(LossCfg), C.POINTER(AdamCfg),
+                                       C.POINTER(vp)]),
+        "chg_exec_step": (C.c_int, [vp, vp, C.POINTER(AdamCfg)]),
+        "chg_exec_destroy": (None, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -136,7 +141,7 @@ def _on_device(x) -> bool:
 
 
 # chg_model_cfg.mlp_precision values this build implements (include/chg.h)
-PRECISION_MODES = {0: "fp32", 2: "tf32"}
+PRECISION_MODES = {0: "fp32", 1: "3xtf32", 2: "tf32"}
 
 
 def default_model_cfg() -> ModelCfg:
@@ -253,6 +258,19 @@ class Context:
         """labels: dict energy_per_atom [S], forces [N,3], stress [S,3,3], magmom [N],
         magmom_mask [N] (numpy → host copy, or CUDA tensors).  A missing / None entry
         skips that task (chg_labels NULL field)."""
+        lab, keep = self._labels(labels)
+        cfg = LossCfg(w[0], w[1], w[2], w[3], delta, n_struct_global, n_atoms_global, n_magmom_global)
+        out = (C.c_double * 5)()
+        self._check(self.lib.chg_backward(self.h, model.h, graph.h, C.byref(lab), C.byref(cfg),
+                                          out if sync_loss else None))
+        return list(out) if sync_loss else None
+
+    def step(self, model: "Model", lr: float, step: int, allreduce: bool = False, beta1=0.9, beta2=0.999, eps=1e-8,
+             defer_check: bool = False):
+        cfg = AdamCfg(lr, beta1, beta2, eps, step, int(allreduce), int(defer_check))
+        self._check(self.lib.chg_step(self.h, model.h, C.byref(cfg)))
+
+    def _labels(self, labels: Dict):
         names = ("energy_per_atom", "forces", "stress", "magmom", "magmom_mask")
         present = [labels[k] for k in names if labels.get(k) is not None]
         dev = _on_device(present[0]) if present else False
@@ -260,16 +278,20 @@ class Context:
         for k, dt in zip(names, (np.float32, np.float32, np.float32, np.float32, np.uint8)):
             x = labels.get(k)
             keep[k] = None if x is None else (x if dev else np.ascontiguousarray(np.asarray(x, dt)))
-        lab = Labels(*(_ptr(keep[k]) for k in names), int(dev))
-        cfg = LossCfg(w[0], w[1], w[2], w[3], delta, n_struct_global, n_atoms_global, n_magmom_global)
-        out = (C.c_double * 5)()
-        self._check(self.lib.chg_backward(self.h, model.h, graph.h, C.byref(lab), C.byref(cfg),
-                                          out if sync_loss else None))
-        return list(out) if sync_loss else None
+        return Labels(*(_ptr(keep[k]) for k in names), int(dev)), keep
 
-    def step(self, model: "Model", lr: float, step: int, allreduce: bool = False, beta1=0.9, beta2=0.999, eps=1e-8):
-        cfg = AdamCfg(lr, beta1, beta2, eps, step, int(allreduce))
-        self._check(self.lib.chg_step(self.h, model.h, C.byref(cfg)))
+    def capture_step(self, model: "Model", graph: "Graph", labels: Dict, w=(2.0, 1.5, 0.1, 0.1), delta: float = 0.1,
+                     n_struct_global: int = 0, n_atoms_global: int = 0, n_magmom_global: int = 0,
+                     allreduce: bool = False, beta1=0.9, beta2=0.999, eps=1e-8) -> "Exec":
+        """chg_capture_step: forward + backward + [allreduce] + Adam on `graph` as one CUDA graph.
+        labels: CUDA tensors (kept alive by the returned Exec)."""
+        lab, keep = self._labels(labels)
+        cfg = LossCfg(w[0], w[1], w[2], w[3], delta, n_struct_global, n_atoms_global, n_magmom_global)
+        acfg = AdamCfg(1e-3, beta1, beta2, eps, 1, int(allreduce), 1)
+        h = C.c_void_p()
+        self._check(self.lib.chg_capture_step(self.h, model.h, graph.h, C.byref(lab), C.byref(cfg), C.byref(acfg),
+                                              C.byref(h)))
+        return Exec(self, h, (keep, graph, model), (beta1, beta2, eps, allreduce))
 
     def profile(self, on: bool):
         """Clear and enable/disable per-op device timing (chg_profile)."""
@@ -344,6 +366,29 @@ class Graph:
         if getattr(self, "h", None) and getattr(self.ctx, "h", None):
             self.ctx.lib.chg_graph_destroy(self.h)
         self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Exec:
+    """A captured training step (chg_exec); .step(lr, step) replays it on the ctx stream."""
+
+    def __init__(self, ctx: "Context", h, keep, adam):
+        self.ctx, self.h, self._keep, self._adam = ctx, h, keep, adam
+
+    def step(self, lr: float, step: int):
+        b1, b2, eps, ar = self._adam
+        cfg = AdamCfg(lr, b1, b2, eps, step, int(ar), 1)
+        self.ctx._check(self.ctx.lib.chg_exec_step(self.ctx.h, self.h, C.byref(cfg)))
+
+    def close(self):
+        if self.h:
+            self.ctx.lib.chg_exec_destroy(self.h)
+            self.h = None
 
     def __del__(self):
         try:

@@ -14,10 +14,6 @@
 
 void destroy_graph_impl(chg_graph *G);
 void graph_fill_counts(chg_graph *G);
-void forward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, int train, chg_pred *out);
-void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *lab,
-                   const chg_loss_cfg *cfg, double *loss_out);
-void step_impl(chg_ctx *ctx, chg_model *m, const chg_adam_cfg *cfg);
 void derivative_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, chg_pred *out);
 void md_verlet(chg_ctx *ctx, int64_t n, double *pos, double *vel, const float *F, const double *inv_mass, double dt,
                int drift);
@@ -29,6 +25,8 @@ void *chg_ctx::get(const std::string &name, size_t bytes) {
   if (bytes == 0) bytes = 16;
   auto it = ws.find(name);
   if (it != ws.end() && it->second.second >= bytes) return it->second.first;
+  if (capturing) CHG_THROW(CHG_ERR_STATE, "workspace %s would grow inside a captured step", name.c_str());
+  ++ws_gen;
   if (it != ws.end()) CUDA_OK(cudaFreeAsync(it->second.first, stream));
   size_t cap = bytes + bytes / 4 + 256;
   void *p = nullptr;
@@ -179,6 +177,8 @@ chg_status chg_ctx_create(int device, void *cuda_stream, chg_ctx **out) {
     CUDA_OK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     CUDA_OK(cudaMalloc(&ctx->d_flag, 256));
     CUDA_OK(cudaMemset(ctx->d_flag, 0, 256));
+    CUDA_OK(cudaMallocHost(&ctx->h_flags, sizeof(int) * chg_ctx::NFLAG));
+    for (int i = 0; i < chg_ctx::NFLAG; ++i) ctx->h_flags[i] = 0x7f7f7f7f;
     ctx->d_loss = (double *)((char *)ctx->d_flag + 64);
   } catch (const ChgError &e) {
     delete ctx;
@@ -195,6 +195,9 @@ void chg_ctx_destroy(chg_ctx *ctx) {
   for (auto &kv : ctx->ws) cudaFree(kv.second.first);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->d_flag) cudaFree(ctx->d_flag);
+  if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
+  for (auto &p : ctx->pending) cudaEventDestroy(p.ev);
+  for (auto e : ctx->flag_ev_pool) cudaEventDestroy(e);
   if (ctx->nccl_comm) ncclCommDestroy((ncclComm_t)ctx->nccl_comm);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->side) cudaStreamDestroy(ctx->side);
@@ -211,6 +214,7 @@ chg_status chg_sync(chg_ctx *ctx) {
   ABI_GUARD(ctx, {
     CUDA_OK(cudaStreamSynchronize(ctx->stream));
     CUDA_OK(cudaGetLastError());
+    check_pending(ctx, true);
   });
 }
 
@@ -310,9 +314,9 @@ chg_status chg_model_create(chg_ctx *ctx, const chg_model_cfg *cfg, chg_model **
     const chg_model_cfg &c = *cfg;
     if (c.d != 64 || c.n_radial != 31 || c.n_angular != 31 || c.gmlp_hidden != 64 || c.head_hidden != 64 ||
         c.n_atom_conv != c.n_bond_conv + 1 || c.n_bond_conv < 1 || c.n_species != 94 || c.envelope_p < 2 ||
-        (c.mlp_precision != 0 && c.mlp_precision != 2))
+        c.mlp_precision < 0 || c.mlp_precision > 2)
       CHG_THROW(CHG_ERR_ARG, "unsupported model config (built: d=64, K=31, hidden 64, n_atom_conv = n_bond_conv+1, "
-                             "94 species, mlp_precision 0 (fp32) or 2 (tf32 tcgen05))");
+                             "94 species, mlp_precision 0 (fp32), 1 (3xTF32 tcgen05) or 2 (TF32 tcgen05))");
     build_layout(m);
     CUDA_OK(cudaSetDevice(ctx->device));
     // params | grads | adam m | adam v, each segment 256-B aligned (vector loads and stores)
@@ -348,6 +352,8 @@ void chg_model_destroy(chg_model *m) {
   if (!m) return;
   cudaSetDevice(m->ctx->device);
   cudaStreamSynchronize(m->ctx->stream);
+  for (auto &p : m->ctx->pending)                  // deferred checks of this model report no name
+    if (p.m == m) p.m = nullptr;
   cudaFree(m->params);
   if (m->d_toff) cudaFree(m->d_toff);
   tc_cache_free(m);
@@ -397,7 +403,7 @@ void *chg_model_device_ptr(chg_model *m, int which) { return m ? which_ptr(m, wh
 
 // a graph built by another context (e.g. a prefetching builder) of the same device: this
 // context's stream waits for the build; the graph frees its arrays after this stream's work
-static void graph_use(chg_ctx *ctx, chg_graph *g) {
+void graph_use(chg_ctx *ctx, chg_graph *g) {
   if (g->ctx == ctx) return;
   if (g->ctx->device != ctx->device) CHG_THROW(CHG_ERR_ARG, "graph built on device %d, used on %d", g->ctx->device, ctx->device);
   if (g->user && g->user != ctx) CHG_THROW(CHG_ERR_ARG, "graph already used by a third context");
@@ -459,7 +465,7 @@ chg_status chg_step(chg_ctx *ctx, chg_model *m, const chg_adam_cfg *cfg) {
   if (!ctx || !m || !cfg) return CHG_ERR_ARG;
   ABI_GUARD(ctx, {
     CUDA_OK(cudaSetDevice(ctx->device));
-    step_impl(ctx, m, cfg);
+    step_impl(ctx, m, cfg, -1);
   });
 }
 

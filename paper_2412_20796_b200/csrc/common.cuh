@@ -87,8 +87,12 @@ struct chg_ctx {
   const chg_graph *fwd_graph = nullptr;
   uint64_t fwd_graph_id = 0;
   bool fwd_train = false;
-  // GEMM engine for the current call: false = fp32 CUDA cores, true = tcgen05 TF32
+  // GEMM engine for the current call: false = fp32 CUDA cores, true = tcgen05 (TF32, or
+  // 3xTF32 split operands when tc_split: mlp_precision 1)
   bool use_tc = false;
+  bool tc_split = false;
+  // producers may write tensor-core-only operands already TF32-rounded (plain TF32 mode only)
+  bool tc_round() const { return use_tc && !tc_split; }
   bool forked = false;           // a side-stream branch is in flight: plain launches (no PDL)
   const struct chg_model *cur_model = nullptr;   // model of the current forward/backward
   const float *cur_wt = nullptr;                 // its transposed weight copy (same flat offsets)
@@ -98,6 +102,18 @@ struct chg_ctx {
   // device scratch for flags / loss
   int *d_flag = nullptr;
   double *d_loss = nullptr;
+  // finite flags of chg_step copied to pinned host slots; a deferred check (defer_check or a
+  // captured step) is resolved by a later call once its event has completed
+  static constexpr int NFLAG = 64;
+  int *h_flags = nullptr;                       // pinned [NFLAG]
+  int flag_next = 0;
+  struct Pending { cudaEvent_t ev; int slot; const struct chg_model *m; };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> flag_ev_pool;
+  // CUDA-graph capture of a training step (chg_capture_step): no workspace may grow while
+  // capturing; every (re)allocation bumps ws_gen so stale captures are refused
+  bool capturing = false;
+  uint64_t ws_gen = 0;
 
   // optional per-op device timing (chg_profile_*): CUDA events on the ctx stream
   struct ProfRec { const char *tag; int ev; double flops, bytes; };
@@ -296,6 +312,15 @@ inline void launch_k(chg_ctx *ctx, void (*kern)(KArgs...), dim3 grid, dim3 block
 // may run ctxs on several GPUs (the attribute is per device context)
 int device_sm_count();                                  // SMs of the current device
 void smem_optin(const void *func, int bytes);           // MaxDynamicSharedMemorySize once per (func, device)
+
+// model.cu: the step's phases (also used by the captured step, capture.cu)
+void forward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, int train, chg_pred *out);
+void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *lab, const chg_loss_cfg *cfg,
+                   double *loss_out);
+void step_impl(chg_ctx *ctx, chg_model *m, const chg_adam_cfg *cfg, int flag_slot /* -1: next free */);
+void check_pending(chg_ctx *ctx, bool block);       // deferred finite checks (CHG_ERR_NONFINITE)
+void push_pending(chg_ctx *ctx, int slot, const chg_model *m);
+int next_flag_slot(chg_ctx *ctx);
 
 // reduce.cu
 float *red_partial(chg_ctx *ctx, size_t floats);       // partial buffer for the next recorded job

@@ -385,6 +385,34 @@ void wgrad(chg_ctx *ctx, const WGrad &g) {
       }
       return;
     }
+    bool plain_dst = true;
+    for (int c = 0; c < 4; ++c) plain_dst &= g.dst[c].k0 == 0 && g.dst[c].kn < 0;
+    if (ctx->tc_split && g.K > 128 && plain_dst) {
+      // 3xTF32 stages ([hi | lo] operands) are twice as large: the rows k of the gradient (the
+      // A columns) are split into pieces of 128, each a launch over the same D; a piece takes the
+      // column ranges of the A segments it overlaps (a segment's columns are base + offset)
+      for (int k0 = 0; k0 < g.K; k0 += 128) {
+        const int k1 = std::min(g.K, k0 + 128);
+        WGrad h = g;
+        h.A.nseg = 0;
+        for (int sg = 0, c0 = 0; sg < g.A.nseg; c0 += g.A.seg[sg].width, ++sg) {
+          const int lo = std::max(k0, c0), hi = std::min(k1, c0 + g.A.seg[sg].width);
+          if (lo >= hi) continue;
+          ASeg piece = g.A.seg[sg];
+          piece.base += lo - c0;
+          piece.width = hi - lo;
+          h.A.seg[h.A.nseg++] = piece;
+        }
+        h.K = k1 - k0;
+        h.bias = (k0 == 0) ? g.bias : 0;
+        for (int c = 0; c < 4; ++c) {
+          h.dst[c].W = g.dst[c].W ? g.dst[c].W + (size_t)k0 * g.dst[c].ldw : nullptr;
+          if (k0 != 0) h.dst[c].b = nullptr;
+        }
+        wgrad(ctx, h);
+      }
+      return;
+    }
   }
   int ktiles = ceil_div(Kp, WK), ntiles = ceil_div(g.N, WN);
   int splits = 1;
@@ -423,9 +451,10 @@ extern "C" chg_status chg_debug_gemm(chg_ctx *ctx, int kind, int engine, int M, 
     CUDA_OK(cudaMemcpyAsync(dA, A, 4 * na, cudaMemcpyHostToDevice, st));
     CUDA_OK(cudaMemcpyAsync(dW, W, 4 * nw, cudaMemcpyHostToDevice, st));
     CUDA_OK(cudaMemsetAsync(dO, 0, 4 * no, st));
-    const bool old = ctx->use_tc;
+    const bool old = ctx->use_tc, old_split = ctx->tc_split;
     const chg_model *old_model = ctx->cur_model;
-    ctx->use_tc = engine == 2;
+    ctx->use_tc = engine == 1 || engine == 2;
+    ctx->tc_split = engine == 1;
     ctx->cur_model = nullptr;                  // no weight-image caching for the hook's scratch operands
     if (kind == 0) {
       std::vector<float> wk((size_t)K * N);
@@ -444,20 +473,21 @@ extern "C" chg_status chg_debug_gemm(chg_ctx *ctx, int kind, int engine, int M, 
         G.ch[c].Wk[0] = dWk + (size_t)64 * c * K;
         G.ch[c].ldwk[0] = K;
       }
-      bool done = engine == 2 ? rowgemm_tc(ctx, G) : false;
-      if (engine == 2 && !done) CHG_THROW(CHG_ERR_ARG, "shape not supported by the tensor-core engine");
+      bool done = engine != 0 ? rowgemm_tc(ctx, G) : false;
+      if (engine != 0 && !done) CHG_THROW(CHG_ERR_ARG, "shape not supported by the tensor-core engine");
       if (!done) { G.tc = 0; rowgemm(ctx, G); }
     } else {
       WGrad g;
       g.A.seg[0] = aseg(dA, K, K);
       g.A.nseg = 1;
       g.M = M; g.K = K;
-      g.D = dW; g.ldd = N; g.N = N; g.bias = 0; g.tc = engine == 2;
+      g.D = dW; g.ldd = N; g.N = N; g.bias = 0; g.tc = engine != 0;
       if (N > 256) CHG_THROW(CHG_ERR_ARG, "N > 256");
       for (int c = 0; c * 64 < N; ++c) { g.dst[c].W = dO + 64 * c; g.dst[c].ldw = N; }
       wgrad(ctx, g);
     }
     ctx->use_tc = old;
+    ctx->tc_split = old_split;
     ctx->cur_model = old_model;
     CUDA_OK(cudaMemcpyAsync(out, dO, 4 * no, cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaStreamSynchronize(st));

@@ -176,7 +176,8 @@ void forward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, int train, chg_pred 
   const int p = m->cfg.envelope_p;
   ctx->dbg.clear();
   ctx->fwd_train = false;
-  ctx->use_tc = m->cfg.mlp_precision == 2;
+  ctx->use_tc = m->cfg.mlp_precision == 1 || m->cfg.mlp_precision == 2;
+  ctx->tc_split = m->cfg.mlp_precision == 1;
   ctx->cur_model = m;
   ctx->cur_wt = nullptr;
   if (ctx->use_tc) {   // K-major weight copy for the tensor-core operands
@@ -370,12 +371,12 @@ void ac_bwd_body(Bwd &Bw, int t, const float *v, const float *e, const float *ea
   {  // dZ1 = (dY · blockdiag(W2ᵀ)) ⊙ SiLU'(z1)
     RowGemm G;
     G.A.seg[0] = aseg(dY, 128, 128);
-    G.A.nseg = 1; G.A.rounded = ctx->use_tc;       // gate_bwd rounds dY in TF32 mode
+    G.A.nseg = 1; G.A.rounded = ctx->tc_round();       // gate_bwd rounds dY in TF32 mode
     G.M = (int)E; G.K = 64; G.nchunk = 2; G.tc = 1;
     G.ch[0] = chunk1(Bw.WT(pre + ".core.W2"), 64, 64, nullptr, dZ, 128);
-    G.ch[0].mul = z1; G.ch[0].ldm = 128; G.ch[0].round_out = ctx->use_tc;
+    G.ch[0].mul = z1; G.ch[0].ldm = 128; G.ch[0].round_out = ctx->tc_round();
     G.ch[1] = chunk1(Bw.WT(pre + ".gate.W2"), 64, 64, nullptr, dZ + 64, 128);
-    G.ch[1].mul = z1 + 64; G.ch[1].ldm = 128; G.ch[1].a_k0 = 64; G.ch[1].round_out = ctx->use_tc;
+    G.ch[1].mul = z1 + 64; G.ch[1].ldm = 128; G.ch[1].a_k0 = 64; G.ch[1].round_out = ctx->tc_round();
     G.tag = "ac_dZ";
     rowgemm(ctx, G);
   }
@@ -405,7 +406,7 @@ void ac_bwd_body(Bwd &Bw, int t, const float *v, const float *e, const float *ea
   {  // dX = dZ1 · [W1_coreᵀ ; W1_gateᵀ] -> (v_i part, v_j part, e part)
     RowGemm G;
     G.A.seg[0] = aseg(dZ, 128, 128);
-    G.A.nseg = 1; G.A.rounded = ctx->use_tc;
+    G.A.nseg = 1; G.A.rounded = ctx->tc_round();
     G.M = (int)E; G.K = 128; G.nchunk = 3; G.tc = 1;
     float *outs[3] = {ti, tj, de};
     for (int c = 0; c < 3; ++c) {
@@ -469,12 +470,12 @@ void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float 
   {
     RowGemm G;
     G.A.seg[0] = aseg(dYb, 128, 128);
-    G.A.nseg = 1; G.A.rounded = ctx->use_tc;
+    G.A.nseg = 1; G.A.rounded = ctx->tc_round();
     G.M = (int)A; G.K = 64; G.nchunk = 2; G.tc = 1;
     G.ch[0] = chunk1(Bw.WT(bp + ".core.W2"), 64, 64, nullptr, dZ, 256);
-    G.ch[0].mul = z1; G.ch[0].ldm = 128; G.ch[0].round_out = ctx->use_tc;
+    G.ch[0].mul = z1; G.ch[0].ldm = 128; G.ch[0].round_out = ctx->tc_round();
     G.ch[1] = chunk1(Bw.WT(bp + ".gate.W2"), 64, 64, nullptr, dZ + 64, 256);
-    G.ch[1].mul = z1 + 64; G.ch[1].ldm = 128; G.ch[1].a_k0 = 64; G.ch[1].round_out = ctx->use_tc;
+    G.ch[1].mul = z1 + 64; G.ch[1].ldm = 128; G.ch[1].a_k0 = 64; G.ch[1].round_out = ctx->tc_round();
     G.tag = "bc_dZ";
     rowgemm(ctx, G);
   }
@@ -505,7 +506,7 @@ void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float 
   {  // dX = [dZ1_bond | dY_angle] · [W1_bcᵀ; W1_bgᵀ; W_acᵀ; W_agᵀ] -> (v_i, e_ij, e_ik, a)
     RowGemm G;
     G.A.seg[0] = aseg(dZ, 256, Kx);
-    G.A.nseg = 1; G.A.rounded = ctx->use_tc;
+    G.A.nseg = 1; G.A.rounded = ctx->tc_round();
     G.M = (int)A; G.K = Kx; G.nchunk = 4; G.tc = 1;
     float *outs[4] = {tv, t1, t2, da};
     for (int c = 0; c < 4; ++c) {
@@ -568,8 +569,9 @@ static void backward_core(chg_ctx *ctx, chg_model *m, chg_graph *g, const LossSe
   Bwd Bw{ctx, m, g, nullptr};
   if (!m->wt) CUDA_OK(cudaMalloc(&m->wt, 4 * (size_t)std::max<int64_t>(m->P, 1)));
   Bw.wt = m->wt;
-  if (m->cfg.mlp_precision != 2) transpose_params(ctx, m, Bw.wt);   // TF32 mode: the forward's copy is current
-  ctx->use_tc = m->cfg.mlp_precision == 2;
+  ctx->use_tc = m->cfg.mlp_precision == 1 || m->cfg.mlp_precision == 2;
+  ctx->tc_split = m->cfg.mlp_precision == 1;
+  if (!ctx->use_tc) transpose_params(ctx, m, Bw.wt);   // tensor-core modes: the forward's copy is current
   ctx->cur_model = m;
   ctx->cur_wt = Bw.wt;
   float *dv = Bw.scratch("dv", N, 64), *de = Bw.scratch("de", E, 64), *da = Bw.scratch("da", A, 64);
@@ -738,8 +740,53 @@ void derivative_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, chg_pred *out) {
 // A9 allreduce + Adam
 // ===========================================================================
 
-void step_impl(chg_ctx *ctx, chg_model *m, const chg_adam_cfg *cfg) {
+static std::string param_name_at(const chg_model *m, int flat) {
+  std::string name = "?";
+  for (size_t t = 0; t < m->names.size(); ++t)
+    if (m->offsets[t] <= flat) name = m->names[t];
+  return name;
+}
+
+// deferred finite checks (defer_check / captured steps): resolve every pending flag whose
+// event has completed (all of them when block); the first non-finite one is reported
+void check_pending(chg_ctx *ctx, bool block) {
+  size_t k = 0;
+  for (; k < ctx->pending.size(); ++k) {
+    chg_ctx::Pending &p = ctx->pending[k];
+    if (block) CUDA_OK(cudaEventSynchronize(p.ev));
+    else if (cudaEventQuery(p.ev) != cudaSuccess) break;
+    const int bad = ctx->h_flags[p.slot];
+    ctx->flag_ev_pool.push_back(p.ev);
+    if (bad != 0x7f7f7f7f) {
+      const std::string name = p.m ? param_name_at(p.m, bad) : "?";
+      for (size_t r = k + 1; r < ctx->pending.size(); ++r) ctx->flag_ev_pool.push_back(ctx->pending[r].ev);
+      ctx->pending.clear();
+      CHG_THROW(CHG_ERR_NONFINITE, "non-finite gradient in %s (flat index %d) at a deferred step: that update "
+                "and the following ones were skipped on the device", name.c_str(), bad);
+    }
+  }
+  ctx->pending.erase(ctx->pending.begin(), ctx->pending.begin() + k);
+}
+
+// a pinned flag slot and a completion event for a deferred check
+void push_pending(chg_ctx *ctx, int slot, const chg_model *m) {
+  cudaEvent_t ev;
+  if (!ctx->flag_ev_pool.empty()) { ev = ctx->flag_ev_pool.back(); ctx->flag_ev_pool.pop_back(); }
+  else CUDA_OK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CUDA_OK(cudaEventRecord(ev, ctx->stream));
+  ctx->pending.push_back({ev, slot, m});
+  if (ctx->pending.size() > chg_ctx::NFLAG / 2) check_pending(ctx, true);   // bounded: oldest are long done
+}
+
+int next_flag_slot(chg_ctx *ctx) {
+  const int s = ctx->flag_next;
+  ctx->flag_next = (ctx->flag_next + 1) % chg_ctx::NFLAG;
+  return s;
+}
+
+void step_impl(chg_ctx *ctx, chg_model *m, const chg_adam_cfg *cfg, int slot) {
   if (cfg->step < 1) CHG_THROW(CHG_ERR_ARG, "adam step must be >= 1");
+  if (!ctx->capturing) check_pending(ctx, false);
   if (cfg->allreduce && ctx->nccl_comm && ctx->nranks > 1) {
     ProfScope ps(ctx, "allreduce", 0.0, 4.0 * m->P);
     ncclResult_t r = ncclAllReduce(m->grads, m->grads, (size_t)m->P, ncclFloat32, ncclSum,
@@ -750,12 +797,16 @@ void step_impl(chg_ctx *ctx, chg_model *m, const chg_adam_cfg *cfg) {
   }
   double bc1 = 1.0 - std::pow((double)cfg->beta1, (double)cfg->step);
   double bc2 = 1.0 - std::pow((double)cfg->beta2, (double)cfg->step);
-  int bad = finite_adam(ctx, m->P, m->params, m->grads, m->m, m->v, cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, bc1,
-                        bc2);
-  if (bad >= 0) {   // nothing was updated (k_adam is guarded by the same flag)
-    std::string name = "?";
-    for (size_t t = 0; t < m->names.size(); ++t)
-      if (m->offsets[t] <= bad) name = m->names[t];
-    CHG_THROW(CHG_ERR_NONFINITE, "non-finite gradient in %s (flat index %d)", name.c_str(), bad);
+  if (slot < 0) slot = next_flag_slot(ctx);
+  finite_adam(ctx, m->P, m->params, m->grads, m->m, m->v, cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, bc1, bc2,
+              ctx->h_flags + slot);
+  if (ctx->capturing) return;                       // the replay records the check (chg_exec_step)
+  if (cfg->defer_check) {                           // no host synchronisation: resolved by a later call
+    push_pending(ctx, slot, m);
+    return;
   }
+  CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  const int bad = ctx->h_flags[slot];
+  if (bad != 0x7f7f7f7f)   // nothing was updated (k_adam is guarded by the same flag)
+    CHG_THROW(CHG_ERR_NONFINITE, "non-finite gradient in %s (flat index %d)", param_name_at(m, bad).c_str(), bad);
 }

@@ -594,7 +594,7 @@ void gate_bwd(chg_ctx *ctx, int64_t rows, const float *y, int ldy, GateLN ln, in
   ProfScope ps(ctx, "gate_bwd", 0.0,
                rows * (512.0 + 260.0 + 512.0 + (mode == GATE_MUL_W ? 768.0 : mode == GATE_MUL_W1W2 ? 1032.0 : 0.0)));
   launch_k(ctx, k_gate_bwd, nb, 256, 0, ctx->stream, rows, rpb, y, ldy, ln, mode, w, i1, i2, dout, didx, dy, lddy, dw_acc, q1,
-                                          q2, part, ctx->use_tc ? 1 : 0);
+                                          q2, part, ctx->tc_round() ? 1 : 0);
   check_launch(ctx);
   RedJob j;                                        // LN affine gradients: batched reduction (reduce.cu)
   j.kind = 2; j.n = 256; j.splits = nb; j.stride = 256; j.part = part;
@@ -765,10 +765,13 @@ void embed_fwd(chg_ctx *ctx, int64_t N, const int32_t *species, const float *W, 
   check_launch(ctx);
 }
 
-// finite check and the guarded Adam update back to back, then ONE synchronisation: returns the
-// first non-finite flat index (nothing was updated) or -1
-int finite_adam(chg_ctx *ctx, int64_t n, float *p, float *g, float *m, float *v, float lr, float b1, float b2,
-                float eps, double bc1, double bc2) {
+const void *adam_kernel() { return (const void *)k_adam; }
+
+// finite check and the guarded Adam update back to back; the first non-finite flat index
+// (0x7f7f7f7f = none; nothing is updated otherwise) is copied to the pinned host_flag on the
+// stream — no synchronisation here (the caller checks it now or later)
+void finite_adam(chg_ctx *ctx, int64_t n, float *p, float *g, float *m, float *v, float lr, float b1, float b2,
+                 float eps, double bc1, double bc2, int *host_flag) {
   int *bad = ctx->d_flag;
   {
     ProfScope ps(ctx, "adam", 0.0, 4.0 * n);
@@ -783,8 +786,5 @@ int finite_adam(chg_ctx *ctx, int64_t n, float *p, float *g, float *m, float *v,
     launch_k(ctx, k_adam, ceil_div(n, 256), 256, 0, ctx->stream, n, p, g, m, v, lr, b1, b2, eps, step_size, inv_sqrt_bc2, bad);
     check_launch(ctx);
   }
-  int *h = (int *)ctx->pinned_get(64);
-  CUDA_OK(cudaMemcpyAsync(h, bad, 4, cudaMemcpyDeviceToHost, ctx->stream));
-  CUDA_OK(cudaStreamSynchronize(ctx->stream));
-  return *h == 0x7f7f7f7f ? -1 : *h;
+  CUDA_OK(cudaMemcpyAsync(host_flag, bad, 4, cudaMemcpyDeviceToHost, ctx->stream));
 }

@@ -84,5 +84,6 @@ void transpose_params(chg_ctx *ctx, const chg_model *m, float *wt);
 void fill_zero(chg_ctx *ctx, void *p, size_t bytes);
 void embed_fwd(chg_ctx *ctx, int64_t N, const int32_t *species, const float *W, float *v);
 // Adam (PyTorch semantics) + finite check
-int finite_adam(chg_ctx *ctx, int64_t n, float *p, float *g, float *m, float *v, float lr, float b1, float b2,
-                float eps, double bc1, double bc2);
+const void *adam_kernel();                        // k_adam (captured-step parameter updates)
+void finite_adam(chg_ctx *ctx, int64_t n, float *p, float *g, float *m, float *v, float lr, float b1, float b2,
+                 float eps, double bc1, double bc2, int *host_flag);

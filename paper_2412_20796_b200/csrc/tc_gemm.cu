@@ -166,6 +166,9 @@ struct TcPlan {
   int nsa;           // A stages
   int bres;          // 1: the whole weight image is loaded once per CTA (no per-stage B traffic)
   int noconv;        // 1: A arrives TF32-rounded by TMA: no conversion pass, the MMA waits on the load
+  int split;         // 1: 3xTF32 (mlp_precision 1): operands split x = hi + lo (both TF32), three MMAs
+                     //    A_lo·B_hi + A_hi·B_lo + A_hi·B_hi per K step; stages hold [hi | lo]
+  int nsb;           // B ring slots (<= NSB) when the image is not resident
 };
 
 // B image: img[kc][q][n][4] = tf32(W_chunk(n - coff, k = lo + kc·KC - a_k0 + 4q + r))
@@ -181,7 +184,11 @@ __device__ __forceinline__ void pack_elem(const RowGemm &g, const TcPlan &P, uin
     for (int b = 0; b < C.nwb; ++b)
       if (kk >= C.wk0[b] && kk < C.wk0[b + 1]) v = C.Wk[b][(size_t)j * C.ldwk[b] + (kk - C.wk0[b])];
   }
-  img[(size_t)kc * P.ntot * KC + ((k >> 2) * P.ntot + n) * 4 + (k & 3)] = to_tf32(v);
+  const size_t at = (size_t)kc * P.ntot * KC + ((k >> 2) * P.ntot + n) * 4 + (k & 3);
+  const uint32_t hi = to_tf32(v);
+  img[at] = hi;
+  if (P.split)                                   // lo image: the TF32 rounding of the remainder
+    img[(size_t)(P.width / KC) * P.ntot * KC + at] = to_tf32(v - __uint_as_float(hi));
 }
 
 // every cached image of a model in one launch (blockIdx.y = site), after the weights changed
@@ -306,10 +313,12 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int NT = P.ntot;
   const uint32_t a_bytes = KC * TCM * 4, b_bytes = KC * NT * 4;
-  const int NSA = P.nsa;
-  uint8_t *sA = smem;                                   // [NSA][a_bytes]
-  uint8_t *sB = smem + NSA * a_bytes;                   // [P.bst][b_bytes]
-  uint64_t *fullA = (uint64_t *)(sB + P.bst * b_bytes);
+  const uint32_t a_stage = a_bytes << P.split, b_stage = b_bytes << P.split;   // [hi | lo] in split mode
+  const int NSA = P.nsa, NSBr = P.nsb;
+  const uint32_t *bimg_lo = bimg + (size_t)(P.width / KC) * NT * KC;
+  uint8_t *sA = smem;                                   // [NSA][a_stage]
+  uint8_t *sB = smem + NSA * a_stage;                   // [P.bst][b_stage]
+  uint64_t *fullA = (uint64_t *)(sB + P.bst * b_stage);
   uint64_t *emptyA = fullA + NSA;
   uint64_t *loaded = emptyA + NSA;                      // cp.async completion per A stage
   uint64_t *fullB = loaded + NSA;
@@ -317,7 +326,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
   uint64_t *tfull = emptyB + NSB;
   uint64_t *tempty = tfull + 2;
   uint32_t *tslot = (uint32_t *)(tempty + 2);
-  float *epi = (float *)(smem + NSA * a_bytes + P.bst * b_bytes + 8 * (3 * NSA + 2 * NSB + 4) + 16);  // [8][32][33]
+  float *epi = (float *)(smem + NSA * a_stage + P.bst * b_stage + 8 * (3 * NSA + 2 * NSB + 4) + 16);  // [8][32][33]
   // epilogue operand boxes [8 warps][TM.nbuf][32 x 32] (1024-B aligned TMA targets) + their barriers
   float *obuf0 = (float *)(((uintptr_t)(epi + (TM.tstore ? 0 : NEPI * 32 * 33)) + 1023) & ~(uintptr_t)1023);
   float *stg0 = obuf0 + NEPI * TM.nbuf * 1024;          // TMA-store staging [8 warps][TM.nst][32 x 32]
@@ -389,7 +398,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
         }
       const ASeg S = g.A.seg[seg];
       const int cin = col - start + 4 * q;
-      const uint32_t dst0 = smem_u32(sA + sa * a_bytes);
+      const uint32_t dst0 = smem_u32(sA + sa * a_stage);
       bool tma = false;
 #pragma unroll
       for (int sg = 0; sg < 4; ++sg)
@@ -431,14 +440,19 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
     for (int gi = 0; gi < (P.noconv ? 0 : total); ++gi) {
       const int sa = gi % NSA, ua = gi / NSA;
       mbar_wait(&loaded[sa], ua & 1);
-      uint4 *row = (uint4 *)(sA + sa * a_bytes + r * 128);
+      uint4 *row = (uint4 *)(sA + sa * a_stage + r * 128);
+      uint4 *row_lo = (uint4 *)(sA + sa * a_stage + a_bytes + r * 128);
       if (!TC_SKIP(16)) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const int kk = (k + sw) & 7;                // rotated order: conflict-free banks
           float4 v = *(const float4 *)&row[kk];
           if (g.A.act == 1) { v.x = silu_fast(v.x); v.y = silu_fast(v.y); v.z = silu_fast(v.z); v.w = silu_fast(v.w); }
-          row[kk] = make_uint4(to_tf32(v.x), to_tf32(v.y), to_tf32(v.z), to_tf32(v.w));
+          const uint4 h = make_uint4(to_tf32(v.x), to_tf32(v.y), to_tf32(v.z), to_tf32(v.w));
+          row[kk] = h;
+          if (P.split)                                // exact remainder, rounded to TF32 again
+            row_lo[kk] = make_uint4(to_tf32(v.x - __uint_as_float(h.x)), to_tf32(v.y - __uint_as_float(h.y)),
+                                    to_tf32(v.z - __uint_as_float(h.z)), to_tf32(v.w - __uint_as_float(h.w)));
         }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic-proxy writes -> async proxy (MMA)
@@ -457,20 +471,23 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
         if TC_SKIP(4) {
           mbar_arrive(&fullB[0]);
         } else {
-          mbar_expect_tx(&fullB[0], b_bytes * nkc);
-          for (int kc = 0; kc < nkc; ++kc)
-            bulk_g2s(sB + kc * b_bytes, bimg + (size_t)kc * NT * KC, b_bytes, &fullB[0]);
+          mbar_expect_tx(&fullB[0], b_stage * nkc);
+          for (int kc = 0; kc < nkc; ++kc) {
+            bulk_g2s(sB + kc * b_stage, bimg + (size_t)kc * NT * KC, b_bytes, &fullB[0]);
+            if (P.split) bulk_g2s(sB + kc * b_stage + b_bytes, bimg_lo + (size_t)kc * NT * KC, b_bytes, &fullB[0]);
+          }
         }
       }
     } else if (lane == 0) {
       for (int gi = 0; gi < total; ++gi) {
-        const int kc = gi % nkc, sb = gi % NSB, ub = gi / NSB;
+        const int kc = gi % nkc, sb = gi % NSBr, ub = gi / NSBr;
         if (ub > 0) mbar_wait(&emptyB[sb], (ub - 1) & 1);
         if TC_SKIP(4) {                                 // debug: no weight traffic
           mbar_arrive(&fullB[sb]);
         } else {
-          mbar_expect_tx(&fullB[sb], b_bytes);
-          bulk_g2s(sB + sb * b_bytes, bimg + (size_t)kc * NT * KC, b_bytes, &fullB[sb]);
+          mbar_expect_tx(&fullB[sb], b_stage);
+          bulk_g2s(sB + sb * b_stage, bimg + (size_t)kc * NT * KC, b_bytes, &fullB[sb]);
+          if (P.split) bulk_g2s(sB + sb * b_stage + b_bytes, bimg_lo + (size_t)kc * NT * KC, b_bytes, &fullB[sb]);
         }
       }
     }
@@ -484,7 +501,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         bool started[4] = {false, false, false, false};
         for (int kc = 0; kc < nkc; ++kc, ++gi) {
-          const int sa = gi % NSA, ua = gi / NSA, sb = P.bres ? kc : gi % NSB, ub = gi / NSB;
+          const int sa = gi % NSA, ua = gi / NSA, sb = P.bres ? kc : gi % NSBr, ub = gi / NSBr;
           mbar_wait(P.noconv ? &loaded[sa] : &fullA[sa], ua & 1);
           if (!P.bres) mbar_wait(&fullB[sb], ub & 1);
           else if (gi == 0) mbar_wait(&fullB[0], 0);
@@ -494,7 +511,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
             trace_mw[gi] = t;
           }
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t a_base = smem_u32(sA + sa * a_bytes), b_base = smem_u32(sB + sb * b_bytes);
+          const uint32_t a_base = smem_u32(sA + sa * a_stage), b_base = smem_u32(sB + sb * b_stage);
           const int col0 = P.lo + kc * KC;
           for (int gr = 0; gr < P.ngrp; ++gr) {
             const int c = P.gfirst[gr];
@@ -506,8 +523,17 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
             for (int j = 0; j < KC / 8; ++j) {
               uint64_t ad = make_desc(a_base + j * 32, 16, 1024) | ((uint64_t)2 << 61);   // SWIZZLE_128B
               uint64_t bd = make_desc(b_base + j * 2 * (NT * 16) + P.coff[c] * 16, NT * 16, 128);
-              if (!TC_SKIP(8))                            // debug: no tensor-core work
-                mma_tf32(tmem + a * tcols + P.coff[c], ad, bd, idesc, (started[gr] || j > 0) ? 1u : 0u);
+              const uint32_t acc = (started[gr] || j > 0) ? 1u : 0u;
+              if (TC_SKIP(8)) continue;                   // debug: no tensor-core work
+              if (P.split) {                              // 3xTF32: small terms first, then hi·hi
+                const uint64_t ad_lo = make_desc(a_base + a_bytes + j * 32, 16, 1024) | ((uint64_t)2 << 61);
+                const uint64_t bd_lo = make_desc(b_base + b_bytes + j * 2 * (NT * 16) + P.coff[c] * 16, NT * 16, 128);
+                mma_tf32(tmem + a * tcols + P.coff[c], ad_lo, bd, idesc, acc);
+                mma_tf32(tmem + a * tcols + P.coff[c], ad, bd_lo, idesc, 1u);
+                mma_tf32(tmem + a * tcols + P.coff[c], ad, bd, idesc, 1u);
+              } else {
+                mma_tf32(tmem + a * tcols + P.coff[c], ad, bd, idesc, acc);
+              }
             }
             started[gr] = true;
           }
@@ -765,6 +791,8 @@ struct WgPlan {
   int ones_col;    // K if the bias ones row is used, else -1
   int rows_per_cta;
   uint32_t tmem_cols;
+  int split;       // 1: 3xTF32 — stage = [A_T hi | D_T hi | A_T lo | D_T lo], three MMAs per K step
+  int nst;         // stages in the ring (<= WG_NST)
 };
 
 __device__ __forceinline__ uint32_t kmaj_swz(int r, int m) {   // byte offset of element (row r, K index m)
@@ -777,12 +805,14 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t a_bytes = P.Kpad * 128, d_bytes = P.Npad * 128;
-  const uint32_t st_bytes = a_bytes + d_bytes;
-  uint64_t *full = (uint64_t *)(smem + WG_NST * st_bytes);
+  const uint32_t lo_off = a_bytes + d_bytes;                  // split: lo half of a stage
+  const uint32_t st_bytes = lo_off << P.split;
+  const int NST = P.nst;
+  uint64_t *full = (uint64_t *)(smem + NST * st_bytes);
   uint64_t *empty = full + WG_NST;
   uint64_t *done = empty + WG_NST;
   uint32_t *tslot = (uint32_t *)(done + 1);
-  float *sbias = (float *)(smem + WG_NST * st_bytes + 8 * (2 * WG_NST + 1) + 16);   // [WG_NPW][256]
+  float *sbias = (float *)(smem + NST * st_bytes + 8 * (2 * WG_NST + 1) + 16);   // [WG_NPW][256]
   __shared__ int s_seg[8], s_col[8];        // A block -> segment, column within the segment
 
   const int r0 = blockIdx.x * P.rows_per_cta;
@@ -796,7 +826,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (tid == 0) {
-    for (int i = 0; i < WG_NST; ++i) { mbar_init(&full[i], g.K / 32 + g.N / 32); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < NST; ++i) { mbar_init(&full[i], g.K / 32 + g.N / 32); mbar_init(&empty[i], 1); }
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -808,10 +838,11 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
   }
   for (int i = tid; i < WG_NPW * 256; i += blockDim.x) sbias[i] = 0.f;
   // constant rows k = K..Kpad of A_T: zeros, and the ones row for the bias
-  for (int s = 0; s < WG_NST; ++s)
+  for (int s = 0; s < NST; ++s)
     for (int idx = tid; idx < (P.Kpad - g.K) * 32; idx += blockDim.x) {
       const int r = g.K + idx / 32, m = idx % 32;
       *(float *)(smem + s * st_bytes + kmaj_swz(r, m)) = (r == P.ones_col) ? 1.0f : 0.0f;
+      if (P.split) *(float *)(smem + s * st_bytes + lo_off + kmaj_swz(r, m)) = 0.0f;
     }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -862,13 +893,27 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
       float4 nxt[8];
       load(j + WG_NPW, row_n, nxt);
       row_n = row_of(j + 2 * WG_NPW);
-      const int c = j / nb, b = j - c * nb, s = c % WG_NST, u = c / WG_NST;
+      const int c = j / nb, b = j - c * nb, s = c % NST, u = c / NST;
       if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
       uint8_t *stA = smem + s * st_bytes;
       const bool isA = b < nba;
       uint8_t *base = isA ? stA : stA + a_bytes;
       const int r0b = isA ? 32 * b : 32 * (b - nba);
-      if (isA && g.A.act == 1) {
+      const bool act = isA && g.A.act == 1;
+      if (P.split) {                                   // 3xTF32: hi and the rounded remainder lo
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float x[4] = {cur[k].x, cur[k].y, cur[k].z, cur[k].w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float v = act ? silu_fast(x[q]) : x[q];
+            const uint32_t h = to_tf32(v);
+            const uint32_t o = kmaj_swz(r0b + 4 * k + q, lane);
+            *(uint32_t *)(base + o) = h;
+            *(uint32_t *)(base + lo_off + o) = to_tf32(v - __uint_as_float(h));
+          }
+        }
+      } else if (act) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const float x[4] = {cur[k].x, cur[k].y, cur[k].z, cur[k].w};
@@ -891,6 +936,10 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
 #pragma unroll
         for (int uu = 0; uu < 8; ++uu) {
           float4 v = *(const float4 *)(row + (uu << 4));
+          if (P.split) {                               // hi + lo: the value to 22 bits
+            const float4 w = *(const float4 *)(row + lo_off + (uu << 4));
+            v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
+          }
           acc += (v.x + v.y) + (v.z + v.w);
         }
         sbias[warp * 256 + r0b + lane] += acc;
@@ -916,7 +965,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(P.Npad >> 3) << 17) |
                              ((uint32_t)(128 >> 4) << 24);
       for (int c = 0; c < nchunks; ++c) {
-        const int s = c % WG_NST, u = c / WG_NST;
+        const int s = c % NST, u = c / NST;
         mbar_wait(&full[s], u & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t baseA = smem_u32(smem + s * st_bytes), baseD = baseA + a_bytes;
@@ -925,7 +974,17 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
           for (int j = 0; j < 4; ++j) {
             uint64_t ad = make_desc(baseA + tt * 16384 + j * 32, 16, 1024) | ((uint64_t)2 << 61);
             uint64_t bd = make_desc(baseD + j * 32, 16, 1024) | ((uint64_t)2 << 61);
-            if (!TC_SKIP(8)) mma_tf32(tmem + tt * P.Npad, ad, bd, idesc, (c > 0 || j > 0) ? 1u : 0u);
+            const uint32_t acc = (c > 0 || j > 0) ? 1u : 0u;
+            if (TC_SKIP(8)) continue;
+            if (P.split) {                             // 3xTF32: A_lo·D_hi + A_hi·D_lo + A_hi·D_hi
+              const uint64_t ad_lo = make_desc(baseA + lo_off + tt * 16384 + j * 32, 16, 1024) | ((uint64_t)2 << 61);
+              const uint64_t bd_lo = make_desc(baseD + lo_off + j * 32, 16, 1024) | ((uint64_t)2 << 61);
+              mma_tf32(tmem + tt * P.Npad, ad_lo, bd, idesc, acc);
+              mma_tf32(tmem + tt * P.Npad, ad, bd_lo, idesc, 1u);
+              mma_tf32(tmem + tt * P.Npad, ad, bd, idesc, 1u);
+            } else {
+              mma_tf32(tmem + tt * P.Npad, ad, bd, idesc, acc);
+            }
           }
         }
         mma_commit(&empty[s]);
@@ -1011,7 +1070,7 @@ void tc_repack_all(chg_ctx *ctx, chg_model *m) {
     c->dirty = false;
   }
   double bytes = 0;
-  for (auto &J : c->jobs) bytes += (double)J.nkc * J.P.ntot * KC * 8.0;
+  for (auto &J : c->jobs) bytes += (double)J.nkc * J.P.ntot * KC * 8.0 * (1 + J.P.split);
   ProfScope ps(ctx, "tc_pack", 0.0, bytes);
   launch_k(ctx, k_pack_all, dim3(148, (unsigned)c->jobs.size()), 256, 0, ctx->stream, c->d_jobs);
   check_launch(ctx);
@@ -1074,7 +1133,31 @@ static int encode_op_map(CUtensorMap *m, const float *base, int ncols, int rows,
 // Returns false if the GEMM does not fit this path (caller uses the SIMT kernel).
 bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   if (g.M <= 0 || g.K % KC != 0 || g.nchunk < 1) return false;
+  const int split = ctx->tc_split ? 1 : 0;
+  if (split && g.nchunk > 1) {
+    // 3xTF32 stages hold [hi | lo] operands: at most 128 output columns per launch, so wider
+    // GEMMs (bc_f1, bc_dX, ac_dX) run as launches over groups of their output chunks
+    int cols = 0;
+    for (int c = 0; c < g.nchunk; ++c) cols += (g.ch[c].ncols + 31) / 32 * 32;
+    if (cols > 128) {
+      int c0 = 0;
+      while (c0 < g.nchunk) {
+        RowGemm h = g;
+        int w = 0, n = 0;
+        while (c0 + n < g.nchunk && w + (g.ch[c0 + n].ncols + 31) / 32 * 32 <= 128) {
+          h.ch[n] = g.ch[c0 + n];
+          w += (g.ch[c0 + n].ncols + 31) / 32 * 32;
+          ++n;
+        }
+        h.nchunk = n;
+        if (!rowgemm_tc(ctx, h)) CHG_THROW(CHG_ERR_STATE, "rowgemm_tc %s: 3xTF32 column group does not fit", g.tag);
+        c0 += n;
+      }
+      return true;
+    }
+  }
   TcPlan P{};
+  P.split = split;
   int lo = 1 << 30, hi = 0, off = 0;
   for (int c = 0; c < g.nchunk; ++c) {
     const Chunk &C = g.ch[c];
@@ -1115,7 +1198,8 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   if (P.ntot > 256) return false;
   P.tmem_cols = P.ntot <= 32 ? 32 : P.ntot <= 64 ? 64 : P.ntot <= 128 ? 128 : 256;
   const int nkc = P.width / KC;
-  const size_t bchunk = (size_t)KC * P.ntot * 4, achunk = (size_t)KC * TCM * 4;
+  const size_t bchunk = ((size_t)KC * P.ntot * 4) << split, achunk = ((size_t)KC * TCM * 4) << split;
+  const int nsa_min = split ? 2 : 4;
   // TMA-store epilogue (lane = row) when every chunk's output is a plain [M][32k] table
   static const bool no_tstore = getenv("CHG_TC_NO_TSTORE") != nullptr;   // A/B knob
   TcMaps TM;
@@ -1152,12 +1236,13 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   TM.nst = TM.tstore ? ((has_sout || nst_cap >= 2) ? 2 : 1) : 0;
   auto opbytes = [&](int nb) { return (size_t)1024 + (size_t)NEPI * (nb + TM.nst) * 4096 + 2 * NEPI * 8; };
   const int nb_min = TM.tstore ? std::min(nbuf, 1) : 0;
-  P.bres = !no_bres && fixed_of(5) + nkc * bchunk + (TM.tstore ? opbytes(nb_min) : 0) <= 224 * 1024;
-  P.bst = P.bres ? nkc : NSB;
-  if (nbuf == 2 && fixed_of(4) + P.bst * bchunk + opbytes(2) > 224 * 1024) nbuf = 1;
-  if (nbuf == 1 && fixed_of(4) + P.bst * bchunk + opbytes(1) > 224 * 1024) nbuf = 0;
-  if (TM.nst == 2 && fixed_of(4) + P.bst * bchunk + opbytes(nbuf) > 224 * 1024) TM.nst = 1;
-  P.nsa = 4;
+  P.bres = !no_bres && fixed_of(nsa_min + 1) + nkc * bchunk + (TM.tstore ? opbytes(nb_min) : 0) <= 224 * 1024;
+  P.nsb = split ? 2 : NSB;
+  P.bst = P.bres ? nkc : P.nsb;
+  if (nbuf == 2 && fixed_of(nsa_min) + P.bst * bchunk + opbytes(2) > 224 * 1024) nbuf = 1;
+  if (nbuf == 1 && fixed_of(nsa_min) + P.bst * bchunk + opbytes(1) > 224 * 1024) nbuf = 0;
+  if (TM.nst == 2 && fixed_of(nsa_min) + P.bst * bchunk + opbytes(nbuf) > 224 * 1024) TM.nst = 1;
+  P.nsa = nsa_min;
   while (P.nsa < std::min(nsa_cap, NSA_MAX) && fixed_of(P.nsa + 1) + P.bst * bchunk + opbytes(nbuf) <= 224 * 1024)
     ++P.nsa;
   size_t smem = fixed_of(P.nsa) + P.bst * bchunk + opbytes(nbuf);
@@ -1185,7 +1270,7 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
     if (it != cache->index.end() && cache->gen[it->second] == cache->cur_gen) img = cache->jobs[it->second].img;
   }
   if (!img) {
-    const size_t bytes = (size_t)nkc * P.ntot * KC * 4;
+    const size_t bytes = ((size_t)nkc * P.ntot * KC * 4) << split;   // hi image (+ lo image)
     if (cache) {
       auto it = cache->index.find(key);
       int id;
@@ -1233,7 +1318,7 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
     TM.use[s] = encode_a_map(&TM.m[s], S.base, S.width, g.M, S.ld);
   }
   static const bool no_noconv = getenv("CHG_TC_NO_NOCONV") != nullptr;    // A/B knob
-  P.noconv = g.A.rounded && g.A.act == 0 && !no_noconv;
+  P.noconv = g.A.rounded && g.A.act == 0 && !no_noconv && !split;
   for (int s = 0; s < g.A.nseg; ++s) P.noconv &= TM.use[s];
   TM.nbuf = nbuf;
   for (int c = 0; c < g.nchunk && nbuf > 0; ++c) {
@@ -1276,9 +1361,12 @@ bool wgrad_tc(chg_ctx *ctx, const WGrad &g, float **partial_out, int *Kp_out, in
   P.rows_per_cta = (chunks + grid - 1) / grid * 32;
   const int splits = (g.M + P.rows_per_cta - 1) / P.rows_per_cta;
   float *partial = red_partial(ctx, (size_t)splits * P.Kp * g.N);
-  const size_t st_bytes = (size_t)(P.Kpad + P.Npad) * 128;
-  const size_t smem = 1024 + WG_NST * st_bytes + 8 * (2 * WG_NST + 1) + 16 + WG_NPW * 256 * 4;
-  if (smem > 224 * 1024) return false;
+  P.split = ctx->tc_split ? 1 : 0;
+  const size_t st_bytes = ((size_t)(P.Kpad + P.Npad) * 128) << P.split;
+  const size_t fixed = 1024 + 8 * (2 * WG_NST + 1) + 16 + WG_NPW * 256 * 4;
+  P.nst = (int)std::min<size_t>(WG_NST, (224 * 1024 - fixed) / st_bytes);
+  if (P.nst < (P.split ? 2 : 1)) return false;        // caller splits K (3xTF32) or uses the SIMT kernel
+  const size_t smem = fixed + P.nst * st_bytes;
   smem_optin((const void *)k_wgrad_tc, 224 * 1024);
 #ifdef CHG_TC_DEBUG
   static int skip = getenv("CHG_TC_SKIP") ? atoi(getenv("CHG_TC_SKIP")) : 0;

@@ -23,7 +23,7 @@ def _ngpu():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("prec", [0, 2])
+@pytest.mark.parametrize("prec", [0, 1, 2])
 def test_dp_allreduce_matches_single_gpu(prec):
     n = _ngpu()
     if n < 2:
