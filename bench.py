@@ -111,6 +111,8 @@ def _args():
                     help="GatedMLP GEMM engine (headline mode): 3xtf32 = tcgen05 split-operand fp32 (strict "
                          "parity, the paper's fp32, P:473), tf32 = tcgen05 TF32 (NS loosened), fp32 = CUDA cores")
     ap.add_argument("--no-side-modes", action="store_true", help="skip timing the two other precision modes")
+    ap.add_argument("--grad-overlap", default="on", choices=["on", "off"],
+                    help="N > 1: bucketed gradient allreduce during the backward (SURVEY NEXT-3, P:353)")
     return ap.parse_args()
 
 
@@ -278,6 +280,7 @@ def main():
             uid.copy_(torch.frombuffer(bytearray(chg.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(uid, 0)
         ctx.set_nccl(bytes(uid.cpu().numpy()), ws, rank)
+        ctx.set_grad_overlap(a.grad_overlap == "on")
     def make_model(prec):
         cfg = chg.default_model_cfg()
         cfg.mlp_precision = PREC_CODE[prec]
@@ -668,6 +671,8 @@ def main():
                                    f"(5/3 Å cutoffs, d=64, 4 atom-conv / 3 bond-conv)",
                        "structures_per_gpu": per, "global_batch": per * ws, "parallelism": f"dp{ws}",
                        "step": "build_graph + forward + backward + allreduce + Adam",
+                       "allreduce": ("bucketed during the backward (NEXT-3)" if a.grad_overlap == "on" else
+                                     "one call before Adam") if ws > 1 else "none (1 GPU)",
                        "graph_build": {"value": "prefetched on a builder context during the previous step" if a.prefetch == "all"
                                        else "inline",
                                        "e2e": "inline" if a.prefetch == "off" else

@@ -129,6 +129,14 @@ int64_t chg_launch_count(const chg_ctx *ctx);
  * chg_nccl_unique_id on rank 0, broadcast by the caller. */
 chg_status chg_nccl_unique_id(void *uid128);
 chg_status chg_ctx_set_nccl(chg_ctx *ctx, const void *uid128, int nranks, int rank);
+/* SURVEY §8(f) NEXT-3 ("perform all-reduce once after the gradient calculation of a
+ * part of parameters is completed"): on = 1 makes every chg_backward on a multi-rank ctx sum
+ * the gradients over the ranks in buckets while it runs — the heads + last atom conv, then
+ * each (atom, bond, angle) layer, then embedding / bases — one grouped ncclAllReduce per
+ * bucket on a communication stream, overlapping the backward of the earlier layers; the
+ * following chg_step only waits for them (its own allreduce is skipped).  Exactly one
+ * chg_backward per chg_step while on (a second one would add to already-summed gradients). */
+chg_status chg_ctx_set_grad_overlap(chg_ctx *ctx, int on);
 
 /* ---- A1 graph build (Alg. 2; reading Q8-Q11) ------------
  * Builds, for S structures, the atom graph (all (i, j, n) with

@@ -14,8 +14,11 @@ from concurrent.futures import ThreadPoolExecutor
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(PKG, "build")
-LIB = os.path.join(PKG, "libchg.so")
+# CHG_BUILD_DEBUG=1: a separate timing/debug build (-DCHG_TC_DEBUG: CHG_TC_SKIP knobs, per-CTA
+# trace) into libchg_dbg.so, loaded with CHG_LIB_PATH; the product library never has the knobs
+DEBUG = os.environ.get("CHG_BUILD_DEBUG") == "1"
+OBJ = os.path.join(PKG, "build_dbg" if DEBUG else "build")
+LIB = os.path.join(PKG, "libchg_dbg.so" if DEBUG else "libchg.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -33,6 +36,10 @@ def _nccl_dirs():
 
 
 def _flags():
+    return _flags_base() + (["-DCHG_TC_DEBUG"] if DEBUG else [])
+
+
+def _flags_base():
     inc, _ = _nccl_dirs()
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + inc,
                    "-I" + os.path.join(ROOT, "include"), "--expt-relaxed-constexpr", "-Xptxas", "-v"] \

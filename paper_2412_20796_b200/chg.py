@@ -65,7 +65,7 @@ SYMBOLS = ["chg_ctx_create", "chg_ctx_destroy", "chg_last_error", "chg_sync", "c
            "chg_model_num_params", "chg_model_set", "chg_model_get", "chg_model_device_ptr", "chg_forward",
            "chg_forward_conservative",
            "chg_backward", "chg_step", "chg_balance", "chg_profile", "chg_profile_query", "chg_debug_gemm", "chg_debug_get",
-           "chg_capture_step", "chg_exec_step", "chg_exec_destroy"]
+           "chg_capture_step", "chg_exec_step", "chg_exec_destroy", "chg_ctx_set_grad_overlap"]
 
 _lib = None
 
@@ -114,6 +114,7 @@ def load(path: str = LIB_PATH):
                                        C.POINTER(vp)]),
         "chg_exec_step": (C.c_int, [vp, vp, C.POINTER(AdamCfg)]),
         "chg_exec_destroy": (None, [vp]),
+        "chg_ctx_set_grad_overlap": (C.c_int, [vp, C.c_int]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -188,6 +189,10 @@ class Context:
     def set_nccl(self, uid: bytes, nranks: int, rank: int):
         buf = C.create_string_buffer(uid, 128)
         self._check(self.lib.chg_ctx_set_nccl(self.h, buf, nranks, rank))
+
+    def set_grad_overlap(self, on: bool = True):
+        """chg_ctx_set_grad_overlap: bucketed gradient allreduce during the backward (NEXT-3)."""
+        self._check(self.lib.chg_ctx_set_grad_overlap(self.h, int(on)))
 
     # ---- graph
     def wait_graph(self, graph: "Graph"):

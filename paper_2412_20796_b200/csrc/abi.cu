@@ -201,6 +201,9 @@ void chg_ctx_destroy(chg_ctx *ctx) {
   if (ctx->nccl_comm) ncclCommDestroy((ncclComm_t)ctx->nccl_comm);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->comm) cudaStreamDestroy(ctx->comm);
+  if (ctx->ev_comm_in) cudaEventDestroy(ctx->ev_comm_in);
+  if (ctx->ev_comm_done) cudaEventDestroy(ctx->ev_comm_done);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -243,6 +246,12 @@ chg_status chg_ctx_set_nccl(chg_ctx *ctx, const void *uid128, int nranks, int ra
     ctx->nranks = nranks;
     ctx->rank = rank;
   });
+}
+
+chg_status chg_ctx_set_grad_overlap(chg_ctx *ctx, int on) {
+  if (!ctx) return CHG_ERR_ARG;
+  ctx->grad_overlap = on != 0;
+  return CHG_OK;
 }
 
 chg_status chg_build_graph(chg_ctx *ctx, int32_t n_struct, const int64_t *atom_ptr, const double *positions,

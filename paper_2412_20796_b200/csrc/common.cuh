@@ -83,6 +83,13 @@ struct chg_ctx {
   // NCCL
   void *nccl_comm = nullptr;
   int nranks = 1, rank = 0;
+  // NEXT-3: gradient allreduce in buckets issued during the backward on `comm`, as soon
+  // as a layer's gradients are final; chg_step then only waits for them (ev_comm)
+  bool grad_overlap = false;
+  cudaStream_t comm = nullptr;
+  cudaEvent_t ev_comm_in = nullptr, ev_comm_done = nullptr;
+  bool ar_pending = false;
+  int ar_buckets = 0;                           // buckets issued by the last backward (bookkeeping)
   // forward bookkeeping for backward
   const chg_graph *fwd_graph = nullptr;
   uint64_t fwd_graph_id = 0;

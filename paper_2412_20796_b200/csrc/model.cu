@@ -558,6 +558,48 @@ const float *labels_dev(chg_ctx *ctx, const void *p, size_t bytes, const char *n
 
 }  // namespace
 
+// NEXT-3 ("perform all-reduce once after the gradient calculation of a part of parameters
+// is completed"): the flat gradient ranges of the parameter groups whose gradients are final are
+// summed over the ranks on the comm stream while the backward of the earlier layers continues.
+// Groups are contiguous ranges of the canonical layout (prefix match: "atom2.", "bond2.", ...).
+static std::pair<int64_t, int64_t> group_range(const chg_model *m, const std::vector<std::string> &prefixes) {
+  int64_t lo = -1, hi = -1;
+  for (size_t t = 0; t < m->names.size(); ++t) {
+    bool in = false;
+    for (auto &p : prefixes) in |= m->names[t].compare(0, p.size(), p) == 0;
+    if (!in) continue;
+    const int64_t end = t + 1 < m->names.size() ? m->offsets[t + 1] : m->P;
+    if (lo < 0) lo = m->offsets[t];
+    else if (m->offsets[t] != hi) CHG_THROW(CHG_ERR_STATE, "gradient bucket %s is not contiguous", prefixes[0].c_str());
+    hi = end;
+  }
+  return {lo, hi};
+}
+
+static void grad_bucket(chg_ctx *ctx, chg_model *m, const std::vector<std::vector<std::string>> &groups) {
+  if (!ctx->grad_overlap || !ctx->nccl_comm || ctx->nranks <= 1 || ctx->no_param_grads) return;
+  if (!ctx->comm) {
+    CUDA_OK(cudaStreamCreateWithFlags(&ctx->comm, cudaStreamNonBlocking));
+    CUDA_OK(cudaEventCreateWithFlags(&ctx->ev_comm_in, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&ctx->ev_comm_done, cudaEventDisableTiming));
+  }
+  CUDA_OK(cudaEventRecord(ctx->ev_comm_in, ctx->stream));        // the group's reductions are queued
+  CUDA_OK(cudaStreamWaitEvent(ctx->comm, ctx->ev_comm_in, 0));
+  ncclGroupStart();
+  for (auto &g : groups) {
+    auto r = group_range(m, g);
+    if (r.first < 0 || r.second <= r.first) continue;
+    ncclResult_t e = ncclAllReduce(m->grads + r.first, m->grads + r.first, (size_t)(r.second - r.first), ncclFloat32,
+                                   ncclSum, (ncclComm_t)ctx->nccl_comm, ctx->comm);
+    if (e != ncclSuccess) { ncclGroupEnd(); CHG_THROW(CHG_ERR_NCCL, "ncclAllReduce (bucket): %s", ncclGetErrorString(e)); }
+    ++ctx->ar_buckets;
+  }
+  ncclResult_t e = ncclGroupEnd();
+  if (e != ncclSuccess) CHG_THROW(CHG_ERR_NCCL, "ncclGroupEnd: %s", ncclGetErrorString(e));
+  CUDA_OK(cudaEventRecord(ctx->ev_comm_done, ctx->comm));
+  ctx->ar_pending = true;
+}
+
 // Everything after the loss seeds: head adjoints, interaction blocks (last to first), and —
 // for training — the embedding / projection / frequency gradients.  deriv = 1: the
 // conservative-force pass (seed ∂E/∂e_atom = 1 only, no parameter gradients): the force,
@@ -614,6 +656,8 @@ static void backward_core(chg_ctx *ctx, chg_model *m, chg_graph *g, const LossSe
   join_side(ctx);                                   // de complete before the atom conv adds to it
   ac_bwd_body(Bw, T, V(T), Ef(T), ea, dagg, dv, de, dea);
   red_flush(ctx);
+  ctx->ar_buckets = 0;
+  grad_bucket(ctx, m, {{"head_"}, {"atom" + std::to_string(T) + "."}});
   for (int t = T - 1; t >= 0; --t) {
     bool ab = t + 1 < T;
     // both output linears read the incoming gradients before any update
@@ -642,6 +686,8 @@ static void backward_core(chg_ctx *ctx, chg_model *m, chg_graph *g, const LossSe
     }
     bc_bwd_body(Bw, t, ab, V(t), Ef(t), Af(t), eb, daggb, dv, de, da, deb, 2);
     red_flush(ctx);
+    const std::string ts = std::to_string(t);
+    grad_bucket(ctx, m, {{"atom" + ts + "."}, {"bond" + ts + "."}, {"angle" + ts + "."}});
   }
   if (deriv) {                                      // no parameter gradients on this pass
     red_flush(ctx);
@@ -657,6 +703,7 @@ static void backward_core(chg_ctx *ctx, chg_model *m, chg_graph *g, const LossSe
   proj_bwd(ctx, A, Bw.act("a_t"), nullptr, da, nullptr, m->p("proj.Wtheta"), nullptr, Bw.G("proj.Wtheta"), nullptr,
            nullptr);
   red_flush(ctx);
+  grad_bucket(ctx, m, {{"embed.", "rbf_a.", "rbf_b.", "proj."}});
   ctx->dbg["dv0"] = {dv, N, 64, 64};
   ctx->dbg["de0"] = {de, E, 64, 64};
   ctx->dbg["da0"] = {da, A, 64, 64};
@@ -787,7 +834,10 @@ int next_flag_slot(chg_ctx *ctx) {
 void step_impl(chg_ctx *ctx, chg_model *m, const chg_adam_cfg *cfg, int slot) {
   if (cfg->step < 1) CHG_THROW(CHG_ERR_ARG, "adam step must be >= 1");
   if (!ctx->capturing) check_pending(ctx, false);
-  if (cfg->allreduce && ctx->nccl_comm && ctx->nranks > 1) {
+  if (ctx->ar_pending) {                            // bucketed during the backward (NEXT-3)
+    CUDA_OK(cudaStreamWaitEvent(ctx->stream, ctx->ev_comm_done, 0));
+    ctx->ar_pending = false;
+  } else if (cfg->allreduce && ctx->nccl_comm && ctx->nranks > 1) {
     ProfScope ps(ctx, "allreduce", 0.0, 4.0 * m->P);
     ncclResult_t r = ncclAllReduce(m->grads, m->grads, (size_t)m->P, ncclFloat32, ncclSum,
                                    (ncclComm_t)ctx->nccl_comm, ctx->stream);

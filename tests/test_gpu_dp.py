@@ -23,22 +23,23 @@ def _ngpu():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("overlap", [False, True])
 @pytest.mark.parametrize("prec", [0, 1, 2])
-def test_dp_allreduce_matches_single_gpu(prec):
+def test_dp_allreduce_matches_single_gpu(prec, overlap):
     n = _ngpu()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     ws = 4 if n >= 4 else 2
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={ws}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29600 + prec), os.path.join(ROOT, "tools", "dp_check.py"),
-           str(prec)]
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + 2 * prec + int(overlap)),
+           os.path.join(ROOT, "tools", "dp_check.py"), str(prec)] + (["overlap"] if overlap else [])
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert lines, r.stdout[-2000:] + r.stderr[-2000:]
     res = json.loads(lines[-1])
     out = os.path.join(ROOT, "gpurun_out")
     if os.path.isdir(out):                    # kept under profiles/ as the multi-GPU evidence
-        with open(os.path.join(out, f"dp_check_ws{ws}_prec{prec}.json"), "w") as f:
+        with open(os.path.join(out, f"dp_check_ws{ws}_prec{prec}{'_overlap' if overlap else ''}.json"), "w") as f:
             json.dump(res, f)
     assert res["params_identical_across_ranks"], res
     assert res["grad_rel_err_vs_1gpu"] <= res["tol"], res

@@ -26,6 +26,7 @@ def main():
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     prec = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+    overlap = len(sys.argv) > 2 and sys.argv[2] == "overlap"   # bucketed allreduce during backward (NEXT-3)
     glob = make_config_batch("C2", 7, n_struct=8 * ws)
     ctx = chg.Context(local)
     uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
@@ -33,6 +34,7 @@ def main():
         uid.copy_(torch.frombuffer(bytearray(chg.nccl_unique_id()), dtype=torch.uint8))
     dist.broadcast(uid, 0)
     ctx.set_nccl(bytes(uid.cpu().numpy()), ws, rank)
+    ctx.set_grad_overlap(overlap)
     cfg = chg.default_model_cfg(); cfg.mlp_precision = prec
     m = chg.Model(ctx, cfg)
     p0 = init_flat_params([(n, s) for n, s, _ in m.layout()], seed=0).astype(np.float32)
@@ -67,7 +69,7 @@ def main():
         lrel = float(abs(lt[0].item() - loss1[0]) / abs(loss1[0]))
         tol = 2e-3 if prec == 2 else 1e-4
         ok = identical and rel <= tol and lrel <= 1e-5
-        print(json.dumps({"world_size": ws, "mlp_precision": prec, "structures": glob.n_struct,
+        print(json.dumps({"world_size": ws, "mlp_precision": prec, "grad_overlap": overlap, "structures": glob.n_struct,
                           "per_rank_structures": np.bincount(rank_of, minlength=ws).tolist(),
                           "grad_rel_err_vs_1gpu": rel, "loss_rel_err_vs_1gpu": lrel, "tol": tol,
                           "params_identical_across_ranks": identical, "ok": ok}), flush=True)
