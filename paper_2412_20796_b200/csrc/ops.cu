@@ -17,53 +17,82 @@ __device__ __forceinline__ RowStats ln_stats(float a, float b) {
   return {mu, rsqrtf(var + 1e-5f)};
 }
 
-__global__ void __launch_bounds__(256, 4) k_gate_fwd(int64_t rows, const float *__restrict__ y, int ldy, GateLN ln,
+// 16 lanes per row, 2 rows per warp: lane j = lane & 15 of row slot rs = lane >> 4 owns columns
+// 4j..4j+3 of each 64-wide branch (one float4: a row is one coalesced 256-B access).  LayerNorm
+// statistics are 4-step shuffle reductions inside the half-warp, and a warp carries 2
+// independent rows through every dependent chain (the row loop is latency-bound, not HBM-bound).
+typedef float4 G8;                                   // a lane's 4 columns of one 64-wide row
+__device__ __forceinline__ G8 ld8(const float *row, int j) { return __ldg((const float4 *)(row + 4 * j)); }
+__device__ __forceinline__ G8 ld8p(const float *row, int j) { return *(const float4 *)(row + 4 * j); }
+__device__ __forceinline__ void st8(float *row, int j, const float (&v)[4]) {
+  *(float4 *)(row + 4 * j) = make_float4(v[0], v[1], v[2], v[3]);
+}
+__device__ __forceinline__ void un8(const G8 &g, float (&v)[4]) { v[0] = g.x; v[1] = g.y; v[2] = g.z; v[3] = g.w; }
+__device__ __forceinline__ float sum8(float v) {     // over the 16 lanes of a row group
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
+  v += __shfl_xor_sync(0xffffffffu, v, 8);
+  return v;
+}
+__device__ __forceinline__ RowStats ln_stats8(const float (&v)[4]) {
+  float s = 0.f;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) s += v[q];
+  const float mu = sum8(s) * (1.0f / 64.0f);
+  float s2 = 0.f;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) s2 += (v[q] - mu) * (v[q] - mu);
+  return {mu, rsqrtf(sum8(s2) * (1.0f / 64.0f) + 1e-5f)};
+}
+
+__global__ void __launch_bounds__(256) k_gate_fwd(int64_t rows, const float *__restrict__ y, int ldy, GateLN ln,
                                                   int mode, const float *__restrict__ w,
                                                   const int32_t *__restrict__ i1, const int32_t *__restrict__ i2,
                                                   const float *__restrict__ resid, float *__restrict__ out) {
   pdl_begin();
-  const int l = threadIdx.x & 31, c0 = 2 * l;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const float2 gc = *(const float2 *)(ln.gc + c0), bc = *(const float2 *)(ln.bc + c0);
-  const float2 gg = *(const float2 *)(ln.gg + c0), bg = *(const float2 *)(ln.bg + c0);
-  // grid-stride over rows (a warp per row); every operand of the next row is requested before
-  // this row's arithmetic, so two rows' loads are in flight per warp
-  auto load = [&](int64_t r, float2 &yc, float2 &yg, float2 &w1, float2 &w2) {
-    yc = __ldg((const float2 *)(y + r * ldy + c0));
-    yg = __ldg((const float2 *)(y + r * ldy + 64 + c0));
-    w2 = make_float2(0.f, 0.f);
+  const int lane = threadIdx.x & 31, j = lane & 15, rs = lane >> 4;
+  const int64_t step = (int64_t)gridDim.x * (blockDim.x >> 5) * 2;
+  float gc[4], bc[4], gg[4], bg[4];
+  un8(ld8(ln.gc, j), gc); un8(ld8(ln.bc, j), bc); un8(ld8(ln.gg, j), gg); un8(ld8(ln.bg, j), bg);
+  struct Ops { G8 yc, yg, w1, w2; };
+  auto load = [&](int64_t r, Ops &o) {
+    o.yc = ld8(y + r * ldy, j);
+    o.yg = ld8(y + r * ldy + 64, j);
     if (mode == GATE_MUL_W) {
-      w1 = __ldg((const float2 *)(w + r * 64 + c0));
+      o.w1 = ld8(w + r * 64, j);
     } else if (mode == GATE_MUL_W1W2) {
-      w1 = __ldg((const float2 *)(w + (int64_t)__ldg(i1 + r) * 64 + c0));
-      w2 = __ldg((const float2 *)(w + (int64_t)__ldg(i2 + r) * 64 + c0));
+      o.w1 = ld8(w + (int64_t)__ldg(i1 + r) * 64, j);
+      o.w2 = ld8(w + (int64_t)__ldg(i2 + r) * 64, j);
     } else {
-      w1 = __ldg((const float2 *)(resid + r * 64 + c0));
+      o.w1 = ld8(resid + r * 64, j);
     }
   };
-  float2 nyc, nyg, nw1, nw2;
-  if (row < rows) load(row, nyc, nyg, nw1, nw2);
-  for (; row < rows; row += warps) {
-    const float2 yc = nyc, yg = nyg, w1 = nw1, w2 = nw2;
-    if (row + warps < rows) load(row + warps, nyc, nyg, nw1, nw2);
-    RowStats sc = ln_stats(yc.x, yc.y), sg = ln_stats(yg.x, yg.y);
-    float nc0 = gc.x * (yc.x - sc.mu) * sc.rstd + bc.x, nc1 = gc.y * (yc.y - sc.mu) * sc.rstd + bc.y;
-    float ng0 = gg.x * (yg.x - sg.mu) * sg.rstd + bg.x, ng1 = gg.y * (yg.y - sg.mu) * sg.rstd + bg.y;
-    float p0 = sigmoidf_(ng0) * siluf_(nc0), p1 = sigmoidf_(ng1) * siluf_(nc1);
-    float2 o;
-    if (mode == GATE_MUL_W) {
-      o = make_float2(p0 * w1.x, p1 * w1.y);
-    } else if (mode == GATE_MUL_W1W2) {
-      o = make_float2(p0 * w1.x * w2.x, p1 * w1.y * w2.y);
-    } else {
-      o = make_float2(w1.x + p0, w1.y + p1);
+  int64_t base = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 2;
+  Ops nx;
+  if (base + rs < rows) load(base + rs, nx);
+  for (; base < rows; base += step) {
+    const int64_t r = base + rs;
+    const bool ok = r < rows;
+    const Ops cu = nx;
+    if (base + step + rs < rows) load(base + step + rs, nx);      // next rows in flight
+    float yc[4], yg[4], w1[4], w2[4];
+    un8(cu.yc, yc); un8(cu.yg, yg); un8(cu.w1, w1);
+    if (mode == GATE_MUL_W1W2) un8(cu.w2, w2);
+    const RowStats sc = ln_stats8(yc), sg = ln_stats8(yg);
+    float o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float nc = gc[q] * (yc[q] - sc.mu) * sc.rstd + bc[q];
+      const float ng = gg[q] * (yg[q] - sg.mu) * sg.rstd + bg[q];
+      const float p = sigmoidf_(ng) * siluf_(nc);
+      o[q] = mode == GATE_MUL_W ? p * w1[q] : mode == GATE_MUL_W1W2 ? p * w1[q] * w2[q] : w1[q] + p;
     }
-    *(float2 *)(out + row * 64 + c0) = o;
+    if (ok) st8(out + r * 64, j, o);
   }
 }
 
-__global__ void __launch_bounds__(256, 4) k_gate_bwd(int64_t rows, int64_t rpb, const float *__restrict__ y, int ldy,
+__global__ void __launch_bounds__(256) k_gate_bwd(int64_t rows, int64_t rpb, const float *__restrict__ y, int ldy,
                                                   GateLN ln, int mode, const float *__restrict__ w,
                                                   const int32_t *__restrict__ i1, const int32_t *__restrict__ i2,
                                                   const float *__restrict__ dout, const int32_t *__restrict__ didx,
@@ -72,86 +101,105 @@ __global__ void __launch_bounds__(256, 4) k_gate_bwd(int64_t rows, int64_t rpb, 
                                                   float *__restrict__ partial, int rnd) {
   pdl_begin();
   __shared__ float sh[8][256];
-  int l = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int c0 = 2 * l;
-  int64_t r0 = blockIdx.x * rpb, r1 = min(rows, r0 + rpb);
-  float2 gc = *(const float2 *)(ln.gc + c0), bc = *(const float2 *)(ln.bc + c0);
-  float2 gg = *(const float2 *)(ln.gg + c0), bg = *(const float2 *)(ln.bg + c0);
-  float a_gc[2] = {0, 0}, a_bc[2] = {0, 0}, a_gg[2] = {0, 0}, a_bg[2] = {0, 0};
-  // software pipeline: the next row's y and seed row dout are in flight while this row's
-  // LayerNorm adjoint runs; the seed-row index is fetched one row further ahead so the dout
-  // load does not wait on it
-  float2 nyc = make_float2(0.f, 0.f), nyg = nyc, nd = nyc;
-  int ndrow = 0;                                     // row indices fit int32 (didx is int32)
-  int ni1 = 0, ni2 = 0;                              // GATE_MUL_W1W2: next row's bond indices
-  if (r0 + wid < r1) {
-    const int64_t r = r0 + wid;
-    if (mode == GATE_MUL_W1W2) { ni1 = __ldg(i1 + r); ni2 = __ldg(i2 + r); }
-    nyc = __ldg((const float2 *)(y + r * ldy + c0));
-    nyg = __ldg((const float2 *)(y + r * ldy + 64 + c0));
-    nd = *(const float2 *)(dout + (didx ? (int64_t)__ldg(didx + r) : r) * 64 + c0);
-    if (r + 8 < r1) ndrow = didx ? __ldg(didx + r + 8) : (int)(r + 8);
-  }
-  for (int64_t row = r0 + wid; row < r1; row += 8) {
-    const float2 yc = nyc, yg = nyg, d2 = nd;
-    const int ci1 = ni1, ci2 = ni2;
-    if (row + 8 < r1) {
-      if (mode == GATE_MUL_W1W2) { ni1 = __ldg(i1 + row + 8); ni2 = __ldg(i2 + row + 8); }
-      nyc = __ldg((const float2 *)(y + (row + 8) * ldy + c0));
-      nyg = __ldg((const float2 *)(y + (row + 8) * ldy + 64 + c0));
-      nd = *(const float2 *)(dout + (int64_t)ndrow * 64 + c0);
-      if (row + 16 < r1) ndrow = didx ? __ldg(didx + row + 16) : (int)(row + 16);
-    }
-    RowStats sc = ln_stats(yc.x, yc.y), sg = ln_stats(yg.x, yg.y);
-    float xc[2] = {(yc.x - sc.mu) * sc.rstd, (yc.y - sc.mu) * sc.rstd};
-    float xg[2] = {(yg.x - sg.mu) * sg.rstd, (yg.y - sg.mu) * sg.rstd};
-    float nc[2] = {gc.x * xc[0] + bc.x, gc.y * xc[1] + bc.y};
-    float ng[2] = {gg.x * xg[0] + bg.x, gg.y * xg[1] + bg.y};
-    float s_g[2] = {sigmoidf_(ng[0]), sigmoidf_(ng[1])};
-    float s_c[2] = {siluf_(nc[0]), siluf_(nc[1])};
-    float phi[2] = {s_g[0] * s_c[0], s_g[1] * s_c[1]};
-    float d[2] = {d2.x, d2.y};
-    float dphi[2];
-    if (mode == GATE_MUL_W) {
-      float2 wv = *(const float2 *)(w + row * 64 + c0);
-      dphi[0] = d[0] * wv.x; dphi[1] = d[1] * wv.y;
-      float2 acc = *(float2 *)(dw_acc + row * 64 + c0);
-      acc.x += d[0] * phi[0]; acc.y += d[1] * phi[1];
-      *(float2 *)(dw_acc + row * 64 + c0) = acc;
-    } else if (mode == GATE_MUL_W1W2) {
-      float2 w1 = *(const float2 *)(w + (int64_t)ci1 * 64 + c0);
-      float2 w2 = *(const float2 *)(w + (int64_t)ci2 * 64 + c0);
-      dphi[0] = d[0] * w1.x * w2.x; dphi[1] = d[1] * w1.y * w2.y;
-      *(float2 *)(q1 + row * 64 + c0) = make_float2(d[0] * phi[0] * w2.x, d[1] * phi[1] * w2.y);
-      *(float2 *)(q2 + row * 64 + c0) = make_float2(d[0] * phi[0] * w1.x, d[1] * phi[1] * w1.y);
-    } else {
-      dphi[0] = d[0]; dphi[1] = d[1];
-    }
-    float dnc[2], dng[2];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, j = lane & 15, rs = lane >> 4;
+  const int64_t r0 = blockIdx.x * rpb, r1 = min(rows, r0 + rpb);
+  float gc[4], bc[4], gg[4], bg[4];
+  un8(ld8(ln.gc, j), gc); un8(ld8(ln.bc, j), bc); un8(ld8(ln.gg, j), gg); un8(ld8(ln.bg, j), bg);
+  float a_gc[4], a_bc[4], a_gg[4], a_bg[4];
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      dnc[q] = dphi[q] * s_g[q] * dsiluf_(nc[q]);
-      dng[q] = dphi[q] * s_c[q] * s_g[q] * (1.0f - s_g[q]);
+  for (int q = 0; q < 4; ++q) a_gc[q] = a_bc[q] = a_gg[q] = a_bg[q] = 0.f;
+  struct Ops { G8 yc, yg, d, w1, w2; };
+  auto load = [&](int64_t r, Ops &o) {
+    o.yc = ld8(y + r * ldy, j);
+    o.yg = ld8(y + r * ldy + 64, j);
+    o.d = ld8p(dout + (didx ? (int64_t)__ldg(didx + r) : r) * 64, j);
+    if (mode == GATE_MUL_W) {
+      o.w1 = ld8(w + r * 64, j);
+    } else if (mode == GATE_MUL_W1W2) {
+      o.w1 = ld8(w + (int64_t)__ldg(i1 + r) * 64, j);
+      o.w2 = ld8(w + (int64_t)__ldg(i2 + r) * 64, j);
+    }
+  };
+  // block = rpb contiguous rows; warp w takes row pairs r0 + 2 (w + 8 i) + rs
+  int64_t base = r0 + 2 * wid;
+  Ops nx;
+  if (base + rs < r1) load(base + rs, nx);
+  for (; base < r1; base += 16) {
+    const int64_t r = base + rs;
+    const bool ok = r < r1;
+    const Ops cu = nx;
+    if (base + 16 + rs < r1) load(base + 16 + rs, nx);
+    float yc[4], yg[4], d[4], w1[4], w2[4];
+    un8(cu.yc, yc); un8(cu.yg, yg); un8(cu.d, d);
+    if (mode != GATE_RESID) un8(cu.w1, w1);
+    if (mode == GATE_MUL_W1W2) un8(cu.w2, w2);
+    if (!ok) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) d[q] = 0.f;               // padding rows contribute nothing
+    }
+    const RowStats sc = ln_stats8(yc), sg = ln_stats8(yg);
+    float xc[4], xg[4], dnc[4], dng[4], phi[4], dphi[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      xc[q] = (yc[q] - sc.mu) * sc.rstd;
+      xg[q] = (yg[q] - sg.mu) * sg.rstd;
+      const float nc = gc[q] * xc[q] + bc[q], ng = gg[q] * xg[q] + bg[q];
+      const float s_g = sigmoidf_(ng), s_c = siluf_(nc);
+      phi[q] = s_g * s_c;
+      dphi[q] = mode == GATE_MUL_W ? d[q] * w1[q] : mode == GATE_MUL_W1W2 ? d[q] * w1[q] * w2[q] : d[q];
+      dnc[q] = dphi[q] * s_g * dsiluf_(nc);
+      dng[q] = dphi[q] * s_c * s_g * (1.0f - s_g);
       a_gc[q] += dnc[q] * xc[q]; a_bc[q] += dnc[q];
       a_gg[q] += dng[q] * xg[q]; a_bg[q] += dng[q];
     }
-    float gdc[2] = {gc.x * dnc[0], gc.y * dnc[1]}, gdg[2] = {gg.x * dng[0], gg.y * dng[1]};
-    float m1c = warp_sum(gdc[0] + gdc[1]) * (1.0f / 64.0f);
-    float m2c = warp_sum(gdc[0] * xc[0] + gdc[1] * xc[1]) * (1.0f / 64.0f);
-    float m1g = warp_sum(gdg[0] + gdg[1]) * (1.0f / 64.0f);
-    float m2g = warp_sum(gdg[0] * xg[0] + gdg[1] * xg[1]) * (1.0f / 64.0f);
-    float2 oc = make_float2(sc.rstd * (gdc[0] - m1c - xc[0] * m2c), sc.rstd * (gdc[1] - m1c - xc[1] * m2c));
-    float2 og = make_float2(sg.rstd * (gdg[0] - m1g - xg[0] * m2g), sg.rstd * (gdg[1] - m1g - xg[1] * m2g));
-    if (rnd) {                                       // dY feeds only tensor-core GEMMs (TF32 mode)
-      oc.x = tf32_round(oc.x); oc.y = tf32_round(oc.y); og.x = tf32_round(og.x); og.y = tf32_round(og.y);
+    float m1c = 0.f, m2c = 0.f, m1g = 0.f, m2g = 0.f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      m1c += gc[q] * dnc[q]; m2c += gc[q] * dnc[q] * xc[q];
+      m1g += gg[q] * dng[q]; m2g += gg[q] * dng[q] * xg[q];
     }
-    *(float2 *)(dy + row * lddy + c0) = oc;
-    *(float2 *)(dy + row * lddy + 64 + c0) = og;
+    m1c = sum8(m1c) * (1.0f / 64.0f); m2c = sum8(m2c) * (1.0f / 64.0f);
+    m1g = sum8(m1g) * (1.0f / 64.0f); m2g = sum8(m2g) * (1.0f / 64.0f);
+    if (!ok) continue;
+    float oc[4], og[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      oc[q] = sc.rstd * (gc[q] * dnc[q] - m1c - xc[q] * m2c);
+      og[q] = sg.rstd * (gg[q] * dng[q] - m1g - xg[q] * m2g);
+      if (rnd) { oc[q] = tf32_round(oc[q]); og[q] = tf32_round(og[q]); }   // dY feeds only TF32 GEMMs
+    }
+    st8(dy + r * lddy, j, oc);
+    st8(dy + r * lddy + 64, j, og);
+    if (mode == GATE_MUL_W) {
+      float acc[4];
+      un8(ld8p(dw_acc + r * 64, j), acc);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] += d[q] * phi[q];
+      st8(dw_acc + r * 64, j, acc);
+    } else if (mode == GATE_MUL_W1W2) {
+      float t1[4], t2[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { t1[q] = d[q] * phi[q] * w2[q]; t2[q] = d[q] * phi[q] * w1[q]; }
+      st8(q1 + r * 64, j, t1);
+      st8(q2 + r * 64, j, t2);
+    }
   }
-  sh[wid][c0] = a_gc[0]; sh[wid][c0 + 1] = a_gc[1];
-  sh[wid][64 + c0] = a_bc[0]; sh[wid][64 + c0 + 1] = a_bc[1];
-  sh[wid][128 + c0] = a_gg[0]; sh[wid][128 + c0 + 1] = a_gg[1];
-  sh[wid][192 + c0] = a_bg[0]; sh[wid][192 + c0 + 1] = a_bg[1];
+  // LN affine partials: the 2 row slots of a warp hold the same columns (xor 16), then warps
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    a_gc[q] += __shfl_xor_sync(0xffffffffu, a_gc[q], 16);
+    a_bc[q] += __shfl_xor_sync(0xffffffffu, a_bc[q], 16);
+    a_gg[q] += __shfl_xor_sync(0xffffffffu, a_gg[q], 16);
+    a_bg[q] += __shfl_xor_sync(0xffffffffu, a_bg[q], 16);
+  }
+  if (rs == 0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int col = 4 * j + q;
+      sh[wid][col] = a_gc[q]; sh[wid][64 + col] = a_bc[q];
+      sh[wid][128 + col] = a_gg[q]; sh[wid][192 + col] = a_bg[q];
+    }
+  }
   __syncthreads();
   float s = 0.f;
   for (int k = 0; k < 8; ++k) s += sh[k][threadIdx.x];
@@ -579,7 +627,7 @@ void gate_fwd(chg_ctx *ctx, int64_t rows, const float *y, int ldy, GateLN ln, in
               const int32_t *i1, const int32_t *i2, const float *resid, float *out) {
   if (rows <= 0) return;
   ProfScope ps(ctx, "gate_fwd", 0.0, rows * (512.0 + 256.0 + (mode == GATE_MUL_W1W2 ? 520.0 : 256.0)));
-  const int grid = (int)std::min<int64_t>(ceil_div(rows * 32, 256), 148 * 4);   // persistent: 4 CTAs / SM
+  const int grid = (int)std::min<int64_t>(ceil_div(rows * 16, 256), 148 * 8);   // 2 rows per warp, grid-stride
   launch_k(ctx, k_gate_fwd, grid, 256, 0, ctx->stream, rows, y, ldy, ln, mode, w, i1, i2, resid, out);
   check_launch(ctx);
 }
