@@ -139,44 +139,60 @@ def _workload(n_gpus: int, per_gpu: int, name: str = "auto"):
 # clocks sampled during the timed region
 # ---------------------------------------------------------------------------
 class Clocks:
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """nvidia-smi sampled every 25 ms from before the timed passes to after them; only samples
+    whose timestamp falls inside a timed window (mark_begin / mark_end) are kept."""
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device: int):
         self.device = device
         self.p = None
+        self.windows = []
 
     def start(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                       "-lms", "100", "-i", str(self.device)], stdout=subprocess.PIPE,
+                                       "-lms", "25", "-i", str(self.device)], stdout=subprocess.PIPE,
                                       stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.p = None
 
+    def mark_begin(self):
+        self.windows.append([time.time(), None])
+
+    def mark_end(self):
+        self.windows[-1][1] = time.time()
+
     def stop(self):
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": PEAKS.get("sm_max_mhz"), "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
+        time.sleep(0.1)
         self.p.terminate()
         out, _ = self.p.communicate(timeout=5)
-        sm, mx, reasons = [], None, set()
+        import datetime
+        sm, mx, reasons, total = [], None, set(), 0
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
             f = [x.strip() for x in line.split(",")]
-            if len(f) < 9:
+            if len(f) < 10:
                 continue
             try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                clk, mxv = float(f[2]), float(f[3])
             except ValueError:
                 continue
-            for k, v in zip(names, f[5:9]):
+            total += 1
+            if not any(w0 - 0.03 <= ts <= (w1 or w0) + 0.03 for w0, w1 in self.windows):
+                continue
+            sm.append(clk)
+            mx = mxv
+            for k, v in zip(names, f[6:10]):
                 if v.lower().startswith("active"):
                     reasons.add(k)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "samples": len(sm),
-                "reasons": sorted(reasons)}
+                "samples_total": total, "reasons": sorted(reasons),
+                "window": "samples inside the timed passes (device-resident + e2e), 25 ms period"}
 
 
 # ---------------------------------------------------------------------------
@@ -440,10 +456,15 @@ def main():
         one_step(batches[k % len(batches)], True)
     clocks = Clocks(local)
     clocks.start()
+    time.sleep(0.3)                                   # nvidia-smi's first sample lands before the timing
+    clocks.mark_begin()
     ms, launches, _ = timed(False)
+    clocks.mark_end()
     main_stats = last_stats[0]
+    clocks.mark_begin()
+    ms_e2e, _, _ = timed(True)                        # clocks sampled across both timed passes
+    clocks.mark_end()
     clk = clocks.stop()
-    ms_e2e, _, _ = timed(True)
     # cached-graph variant: graphs built once outside the timed region (training graphs are static
     # per dataset)
     cached = [build(b, False) for b in batches]

@@ -73,6 +73,7 @@ chg_status chg_capture_step(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_
     x->ctx = ctx; x->m = m;
     x->slot = next_flag_slot(ctx);
     const int64_t l0 = ctx->launches;
+    cudaGetLastError();                              // a stale (already reported) error must not fail the capture
     CUDA_OK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
     began = true;
     ctx->capturing = true;

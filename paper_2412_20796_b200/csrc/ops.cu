@@ -28,6 +28,11 @@ __device__ __forceinline__ void st8(float *row, int j, const float (&v)[4]) {
   *(float4 *)(row + 4 * j) = make_float4(v[0], v[1], v[2], v[3]);
 }
 __device__ __forceinline__ void un8(const G8 &g, float (&v)[4]) { v[0] = g.x; v[1] = g.y; v[2] = g.z; v[3] = g.w; }
+// LayerNorm affine vectors sit at canonical flat offsets (only 8-B aligned): two float2 loads
+__device__ __forceinline__ G8 ldp8(const float *p, int j) {
+  const float2 a = __ldg((const float2 *)(p + 4 * j)), b = __ldg((const float2 *)(p + 4 * j + 2));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
 __device__ __forceinline__ float sum8(float v) {     // over the 16 lanes of a row group
   v += __shfl_xor_sync(0xffffffffu, v, 1);
   v += __shfl_xor_sync(0xffffffffu, v, 2);
@@ -54,7 +59,7 @@ __global__ void __launch_bounds__(256) k_gate_fwd(int64_t rows, const float *__r
   const int lane = threadIdx.x & 31, j = lane & 15, rs = lane >> 4;
   const int64_t step = (int64_t)gridDim.x * (blockDim.x >> 5) * 2;
   float gc[4], bc[4], gg[4], bg[4];
-  un8(ld8(ln.gc, j), gc); un8(ld8(ln.bc, j), bc); un8(ld8(ln.gg, j), gg); un8(ld8(ln.bg, j), bg);
+  un8(ldp8(ln.gc, j), gc); un8(ldp8(ln.bc, j), bc); un8(ldp8(ln.gg, j), gg); un8(ldp8(ln.bg, j), bg);
   struct Ops { G8 yc, yg, w1, w2; };
   auto load = [&](int64_t r, Ops &o) {
     o.yc = ld8(y + r * ldy, j);
@@ -104,7 +109,7 @@ __global__ void __launch_bounds__(256) k_gate_bwd(int64_t rows, int64_t rpb, con
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, j = lane & 15, rs = lane >> 4;
   const int64_t r0 = blockIdx.x * rpb, r1 = min(rows, r0 + rpb);
   float gc[4], bc[4], gg[4], bg[4];
-  un8(ld8(ln.gc, j), gc); un8(ld8(ln.bc, j), bc); un8(ld8(ln.gg, j), gg); un8(ld8(ln.bg, j), bg);
+  un8(ldp8(ln.gc, j), gc); un8(ldp8(ln.bc, j), bc); un8(ldp8(ln.gg, j), gg); un8(ldp8(ln.bg, j), bg);
   float a_gc[4], a_bc[4], a_gg[4], a_bg[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) a_gc[q] = a_bc[q] = a_gg[q] = a_bg[q] = 0.f;
