@@ -62,8 +62,9 @@ def step_roofline(counts, precision: str):
     t_hbm = byts / (PEAKS["hbm_gbs"] * 1e9)
     return flops, byts, t_tensor, t_hbm
 # profile tags (chg_profile call sites) of the GatedMLP contractions: on tcgen05 in tf32 mode (NS)
-TC_ROW_TAGS = {"ac_f1", "ac_f2", "bc_f1", "bc_f2", "ac_dZ", "ac_dX", "bc_dZ", "bc_dX"}
-TC_WG_TAGS = {"ac_W1_wg", "ac_W2_wg", "bc_W1_wg", "bc_W2_wg"}
+TC_ROW_TAGS = {"ac_f1", "ac_f2", "bc_f1", "bc_f2", "ac_dZ", "ac_dX", "bc_dZ", "bc_dX", "ac_P", "bc_P", "ac_dvS",
+               "bc_dvS", "bc_deS"}
+TC_WG_TAGS = {"ac_W1_wg", "ac_W2_wg", "bc_W1_wg", "bc_W2_wg", "ac_W1v_wg", "bc_W1p_wg"}
 WG_TAGS = TC_WG_TAGS | {"ac_out_wg", "bc_out_wg", "bc_outb_wg", "head_wg", "headM_wg", "proj_wg"}
 ROW_TAGS = TC_ROW_TAGS | {"ac_fout", "bc_fout", "head_f", "proj_f", "headM_f", "ac_dagg", "bc_daggb", "head_b",
                           "headM_b", "dbasis"}
@@ -88,7 +89,7 @@ def kernel_of(tag: str, precision: str) -> str:
                 "species_grad": "k_species_grad", "proj_basis": "k_proj_fwd", "proj_bwd": "k_proj_bwd",
                 "proj_reduce": "k_proj_reduce"}[tag]
     return {"segsum": "k_segsum", "gate_fwd": "k_gate_fwd", "gate_bwd": "k_gate_bwd", "wgrad_reduce": "k_wgrad_reduce",
-            "tc_pack": "k_pack_b"}.get(tag, tag)
+            "tc_pack": "k_pack_b", "rows_add": "k_rows_add"}.get(tag, tag)
 
 
 def _args():

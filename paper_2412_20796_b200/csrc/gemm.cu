@@ -136,6 +136,10 @@ __global__ void __launch_bounds__(256) k_rowgemm(const __grid_constant__ RowGemm
       if (n >= c.ncols) continue;
       float v = acc[i][j];
       if (c.bias) v += __ldg(c.bias + n);
+      for (int k = 0; k < c.ngadd; ++k) {
+        const int r = c.gidx[k] ? __ldg(c.gidx[k] + m) : m;
+        v += __ldg(c.gadd[k] + (size_t)r * c.ldga[k] + n);
+      }
       if (c.pre) c.pre[(size_t)m * c.ldp + n] = v;
       if (g.act == 1) v = siluf_(v);
       if (c.mul) v *= dsiluf_(c.mul[(size_t)m * c.ldm + n]);
@@ -298,7 +302,10 @@ double gemm_a_bytes(const AOp &A, int64_t M, int lo, int hi) {
 
 void rowgemm(chg_ctx *ctx, const RowGemm &g) {
   if (g.M <= 0) return;
-  if (g.tc && ctx->use_tc && ctx->cur_model && ctx->cur_wt) {
+  // small problems (per-atom / per-bond products of the factorised layer 1): the persistent
+  // tensor-core kernel's fixed cost (TMEM, barriers, resident weight image) outweighs the math
+  static const int tc_min_rows = getenv("CHG_TC_MIN_ROWS") ? atoi(getenv("CHG_TC_MIN_ROWS")) : 0;
+  if (g.tc && ctx->use_tc && ctx->cur_model && ctx->cur_wt && g.M >= tc_min_rows) {
     RowGemm h = g;
     bool ok = true;
     for (int c = 0; c < h.nchunk && ok; ++c)
@@ -370,7 +377,8 @@ void wgrad(chg_ctx *ctx, const WGrad &g) {
   if (ctx->no_param_grads) return;
   int Kp = g.K + (g.bias ? 1 : 0);
   if (Kp <= 0 || g.N <= 0) return;
-  if (g.tc && ctx->use_tc && g.M > 0) {
+  static const int tc_min_rows = getenv("CHG_TC_MIN_ROWS") ? atoi(getenv("CHG_TC_MIN_ROWS")) : 0;
+  if (g.tc && ctx->use_tc && g.M > 0 && g.M >= tc_min_rows) {
     float *partial = nullptr;
     int kp = 0, splits = 0;
     bool bias_done = false;

@@ -42,6 +42,12 @@ struct Chunk {
   const float *mul = nullptr; int ldm = 0;     // v *= dsilu(mul) (backward of silu)
   float *sout = nullptr; int ldso = 0;         // second output tf32(SiLU(v)) (the next GEMM's operand)
   int round_out = 0;                           // 1: out is stored TF32-rounded (consumed by tcgen05 only)
+  // gathered row additions before the activation: v += gadd[k][gidx[k][m] * ldga[k] + n]
+  // (the per-atom / per-bond products of the factorised first GatedMLP layer)
+  const float *gadd[3] = {nullptr, nullptr, nullptr};
+  const int32_t *gidx[3] = {nullptr, nullptr, nullptr};
+  int ldga[3] = {0, 0, 0};
+  int ngadd = 0;
   // K-major view of the same weight blocks (element (n, k) at Wk[b][n*ldwk[b] + k - wk0[b]]),
   // filled by the orchestration for the tensor-core path (tc_gemm.cu)
   const float *Wk[4] = {nullptr, nullptr, nullptr, nullptr};

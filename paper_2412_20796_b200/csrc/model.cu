@@ -57,6 +57,24 @@ void join_side(chg_ctx *ctx) {
   ctx->forked = false;
 }
 
+// First GatedMLP layer, factorised: the input rows are concatenations of per-atom,
+// per-bond and per-row features, so x·W1 = Σ_parts part·W1[part rows]: the per-atom / per-bond
+// products are computed once per atom / bond (P tables) and added by the per-row GEMM's
+// epilogue through the gather indices — the per-row GEMM contracts only the row's own part
+// (K = 64: e_ij for atom conv, a_ijk for bond conv / angle update).  Exact up to rounding order.
+// P[rows, 64·nw] = X · [W_0[r0:r0+64] | W_1[r0:r0+64] | ...] (one 64-column chunk per weight)
+static void part_product(chg_ctx *ctx, const ASeg &x, int64_t rows, const float *const *W, int nw, int r0, float *P,
+                         int ldP, const char *tag) {
+  if (rows <= 0) return;
+  RowGemm G;
+  G.A.seg[0] = x;
+  G.A.nseg = 1;
+  G.M = (int)rows; G.K = 64; G.nchunk = nw; G.tc = 1;
+  for (int c = 0; c < nw; ++c) G.ch[c] = chunk1(W[c] + (size_t)r0 * 64, 64, 64, nullptr, P + 64 * c, ldP);
+  G.tag = tag;
+  rowgemm(ctx, G);
+}
+
 // --- Atom Conv (Eq. 4) ------------------------------------------------------
 void atom_conv_fwd(Fwd &F, int t, const float *v, const float *e, const float *ea, float *v_out) {
   chg_ctx *ctx = F.ctx;
@@ -68,15 +86,25 @@ void atom_conv_fwd(Fwd &F, int t, const float *v, const float *e, const float *e
   float *y = F.buf("ac_y_" + std::to_string(t), E, 128);
   float *agg = F.buf("ac_agg_" + std::to_string(t), N, 64);
   float *msg = ctx->getf("msg_edge", std::max<int64_t>(E, 1) * 64);
-  {  // [v_i, v_j, e_ij] · [W1_core | W1_gate] + b1   (gather fused in the A load)
+  const float *W1c = m->p(pre + ".core.W1"), *W1g = m->p(pre + ".gate.W1");
+  {  // per atom: Pa = v · [W1c_i | W1g_i | W1c_j | W1g_j]  (rows 0..63: v_i part, 64..127: v_j part)
+    float *Pa = ctx->getf(ctx->ws_name("ac_P"), (size_t)std::max<int64_t>(N, 1) * 256);
+    const float *Wi[2] = {W1c, W1g};
+    part_product(ctx, aseg(v, 64, 64), N, Wi, 2, 0, Pa, 256, "ac_P");
+    part_product(ctx, aseg(v, 64, 64), N, Wi, 2, 64, Pa + 128, 256, "ac_P");
+    // per edge: z1 = e·W1[128:192] + b1 + Pa[i] (v_i part) + Pa[j] (v_j part)
     RowGemm G;
-    G.A.seg[0] = aseg(v, 64, 64, g->center, N);
-    G.A.seg[1] = aseg(v, 64, 64, g->nbr, N);
-    G.A.seg[2] = aseg(e, 64, 64);
-    G.A.nseg = 3;
-    G.M = (int)E; G.K = 192; G.nchunk = 2; G.tc = 1;
-    G.ch[0] = chunk1(m->p(pre + ".core.W1"), 64, 192, m->p(pre + ".core.b1"), z1, 128);
-    G.ch[1] = chunk1(m->p(pre + ".gate.W1"), 64, 192, m->p(pre + ".gate.b1"), z1 + 64, 128);
+    G.A.seg[0] = aseg(e, 64, 64);
+    G.A.nseg = 1;
+    G.M = (int)E; G.K = 64; G.nchunk = 2; G.tc = 1;
+    G.ch[0] = chunk1(W1c + 128 * 64, 64, 64, m->p(pre + ".core.b1"), z1, 128);
+    G.ch[1] = chunk1(W1g + 128 * 64, 64, 64, m->p(pre + ".gate.b1"), z1 + 64, 128);
+    for (int c = 0; c < 2; ++c) {
+      Chunk &C = G.ch[c];
+      C.gadd[0] = Pa + 64 * c; C.gidx[0] = g->center; C.ldga[0] = 256;
+      C.gadd[1] = Pa + 128 + 64 * c; C.gidx[1] = g->nbr; C.ldga[1] = 256;
+      C.ngadd = 2;
+    }
     G.tag = "ac_f1";
     rowgemm(ctx, G);
   }
@@ -100,12 +128,24 @@ void atom_conv_fwd(Fwd &F, int t, const float *v, const float *e, const float *e
 }
 
 // --- Bond Conv (Eq. 5) + Angle Update (Eq. 6) with Eq. 11 inputs ------------
+// first-layer weights of the shared input [v_i, e_ij, e_ik, a_ijk] (Fig. 3a packing):
+// bond core / gate hidden, angle core / gate (rows 0..63 v_i, 64..127 e_ij, 128..191 e_ik, 192..255 a)
+static int bc_first_weights(chg_model *m, int t, bool angle_branch, const float **W, const float **b) {
+  const std::string bp = "bond" + std::to_string(t), ap = "angle" + std::to_string(t);
+  W[0] = m->p(bp + ".core.W1"); b[0] = m->p(bp + ".core.b1");
+  W[1] = m->p(bp + ".gate.W1"); b[1] = m->p(bp + ".gate.b1");
+  if (!angle_branch) return 2;
+  W[2] = m->p(ap + ".core.W"); b[2] = m->p(ap + ".core.b");
+  W[3] = m->p(ap + ".gate.W"); b[3] = m->p(ap + ".gate.b");
+  return 4;
+}
+
 void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float *e, const float *a, const float *eb,
                    float *e_out, float *a_out) {
   chg_ctx *ctx = F.ctx;
   chg_model *m = F.m;
   chg_graph *g = F.g;
-  const int64_t E = g->E, B = g->B, A = g->A;
+  const int64_t N = g->N, E = g->E, B = g->B, A = g->A;
   std::string bp = "bond" + std::to_string(t), ap = "angle" + std::to_string(t), ts = std::to_string(t);
   float *z1 = F.buf("bc_z1_" + ts, A, 128);
   float *yb = F.buf("bc_yb_" + ts, A, 128);
@@ -113,20 +153,29 @@ void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float
   float *aggb = F.buf("bc_aggb_" + ts, B, 64);
   float *q = ctx->getf("msg_angle", std::max<int64_t>(A, 1) * 64);
   if (A > 0) {
-    // shared input [v_i, e_ij, e_ik, a_ijk] against the packed first
-    // layers of both modules (Fig. 3a): bond core/gate hidden, angle core/gate
+    const float *W[4], *bias[4];
+    const int nw = bc_first_weights(m, t, angle_branch, W, bias);
+    const int ldP = 64 * nw;
+    // per atom (v_i part) and per bond (e_ij, e_ik parts) products of the packed first layers
+    float *Pv = ctx->getf(ctx->ws_name("bc_Pv"), (size_t)std::max<int64_t>(N, 1) * ldP);
+    float *P1 = ctx->getf(ctx->ws_name("bc_P1"), (size_t)std::max<int64_t>(B, 1) * ldP);
+    float *P2 = ctx->getf(ctx->ws_name("bc_P2"), (size_t)std::max<int64_t>(B, 1) * ldP);
+    part_product(ctx, aseg(v, 64, 64), N, W, nw, 0, Pv, ldP, "bc_P");
+    part_product(ctx, aseg(e, 64, 64, g->bond_edge, E), B, W, nw, 64, P1, ldP, "bc_P");
+    part_product(ctx, aseg(e, 64, 64, g->bond_edge, E), B, W, nw, 128, P2, ldP, "bc_P");
+    // per angle: [z1_bond | y_angle] = a·W[192:256] + b + Pv[i] + P1[b1] + P2[b2]
     RowGemm G;
-    G.A.seg[0] = aseg(v, 64, 64, g->angle_ctr, g->N);
-    G.A.seg[1] = aseg(e, 64, 64, g->angle_e1, E);
-    G.A.seg[2] = aseg(e, 64, 64, g->angle_e2, E);
-    G.A.seg[3] = aseg(a, 64, 64);
-    G.A.nseg = 4;
-    G.M = (int)A; G.K = 256; G.nchunk = angle_branch ? 4 : 2; G.tc = 1;
-    G.ch[0] = chunk1(m->p(bp + ".core.W1"), 64, 256, m->p(bp + ".core.b1"), z1, 128);
-    G.ch[1] = chunk1(m->p(bp + ".gate.W1"), 64, 256, m->p(bp + ".gate.b1"), z1 + 64, 128);
-    if (angle_branch) {
-      G.ch[2] = chunk1(m->p(ap + ".core.W"), 64, 256, m->p(ap + ".core.b"), ya, 128);
-      G.ch[3] = chunk1(m->p(ap + ".gate.W"), 64, 256, m->p(ap + ".gate.b"), ya + 64, 128);
+    G.A.seg[0] = aseg(a, 64, 64);
+    G.A.nseg = 1;
+    G.M = (int)A; G.K = 64; G.nchunk = nw; G.tc = 1;
+    for (int c = 0; c < nw; ++c) {
+      float *dst = c < 2 ? z1 + 64 * c : ya + 64 * (c - 2);
+      G.ch[c] = chunk1(W[c] + 192 * 64, 64, 64, bias[c], dst, 128);
+      Chunk &C = G.ch[c];
+      C.gadd[0] = Pv + 64 * c; C.gidx[0] = g->angle_ctr; C.ldga[0] = ldP;
+      C.gadd[1] = P1 + 64 * c; C.gidx[1] = g->angle_b1; C.ldga[1] = ldP;
+      C.gadd[2] = P2 + 64 * c; C.gidx[2] = g->angle_b2; C.ldga[2] = ldP;
+      C.ngadd = 3;
     }
     G.tag = "bc_f1";
     rowgemm(ctx, G);
@@ -357,6 +406,12 @@ void bc_bwd_head(Bwd &Bw, int t, const float *de, float *daggb) {
   colsum(Bw.ctx, g->E, de, Bw.G(pre + ".out.b"));   // db_out = Σ over ALL edges of de
 }
 
+// Backward of the factorised first layer.  With z = Σ_parts x_part·W1[part] the
+// per-row adjoint dZ (the GatedMLP's layer-1 pre-activation gradient) gives
+//   d(own part)  = dZ · W1[own]ᵀ                        (per-row GEMM, K = width of dZ, N = 64)
+//   d(part p)    = (Σ_{rows using index i in part p} dZ) · W1[p]ᵀ  (segmented sums, then per-atom /
+//                   per-bond GEMMs; the gather adjoints follow the CSR / rev / swap orders: no atomics)
+//   dW1[part p]  = Σ_i x_p,iᵀ · (Σ_{rows of i} dZ)             (weight gradients over atoms / bonds)
 void ac_bwd_body(Bwd &Bw, int t, const float *v, const float *e, const float *ea, const float *dagg, float *dv,
                  float *de, float *dea) {
   chg_ctx *ctx = Bw.ctx;
@@ -365,7 +420,7 @@ void ac_bwd_body(Bwd &Bw, int t, const float *v, const float *e, const float *ea
   std::string pre = "atom" + std::to_string(t), ts = std::to_string(t);
   const float *z1 = Bw.act("ac_z1_" + ts), *y = Bw.act("ac_y_" + ts);
   float *dY = Bw.scratch("ac_dY", E, 128), *dZ = Bw.scratch("ac_dZ", E, 128);
-  float *ti = Bw.scratch("tmp_i", E, 64), *tj = Bw.scratch("tmp_j", E, 64);
+  float *S = Bw.scratch("ac_S", N, 256);
   gate_bwd(ctx, E, y, 128, Bw.ln(pre), GATE_MUL_W, ea, nullptr, nullptr, dagg, g->center, dY, 128, dea, nullptr,
            nullptr, Bw.lng(pre));
   {  // dZ1 = (dY · blockdiag(W2ᵀ)) ⊙ SiLU'(z1)
@@ -403,45 +458,67 @@ void ac_bwd_body(Bwd &Bw, int t, const float *v, const float *e, const float *ea
     wg.tag = "ac_W2_wg";
     wgrad(ctx, wg);
   }
-  {  // dX = dZ1 · [W1_coreᵀ ; W1_gateᵀ] -> (v_i part, v_j part, e part)
+  {  // de += dZ1 · [W1_core[128:192]ᵀ ; W1_gate[128:192]ᵀ]  (the row's own part e_ij)
     RowGemm G;
     G.A.seg[0] = aseg(dZ, 128, 128);
     G.A.nseg = 1; G.A.rounded = ctx->tc_round();
-    G.M = (int)E; G.K = 128; G.nchunk = 3; G.tc = 1;
-    float *outs[3] = {ti, tj, de};
-    for (int c = 0; c < 3; ++c) {
-      Chunk &C = G.ch[c];
-      C.W[0] = Bw.WT(pre + ".core.W1") + 64 * c; C.ldw[0] = 192;
-      C.W[1] = Bw.WT(pre + ".gate.W1") + 64 * c; C.ldw[1] = 192;
-      C.wk0[0] = 0; C.wk0[1] = 64; C.wk0[2] = 128; C.nwb = 2;
-      C.out = outs[c]; C.ldo = 64;
-      if (c == 2) { C.resid = de; C.ldr = 64; }
-    }
+    G.M = (int)E; G.K = 128; G.nchunk = 1; G.tc = 1;
+    Chunk &C = G.ch[0];
+    C.W[0] = Bw.WT(pre + ".core.W1") + 128; C.ldw[0] = 192;
+    C.W[1] = Bw.WT(pre + ".gate.W1") + 128; C.ldw[1] = 192;
+    C.wk0[0] = 0; C.wk0[1] = 64; C.wk0[2] = 128; C.nwb = 2;
+    C.out = de; C.ldo = 64; C.resid = de; C.ldr = 64;
     G.tag = "ac_dX";
     rowgemm(ctx, G);
   }
-  {  // dW1 = Xᵀ dZ1 with X = [v_i, v_j, e] gathered again
+  {  // S_i = Σ_{e: centre i} dZ_e (CSR rows), S_j = Σ_{e: neighbour j} dZ_e (rows of j through rev)
+    SegSrc s;
+    s.in = dZ; s.ld = 128; s.ptr = g->row_ptr; s.rows = E;
+    segsum(ctx, N, S, 256, 0, 1, &s, "segsum_ac_S", 128);
+    s.perm = g->rev;
+    segsum(ctx, N, S + 128, 256, 0, 1, &s, "segsum_ac_S", 128);
+  }
+  {  // dW1: e part over edges (with db1), v_i / v_j parts over atoms
     WGrad wg;
-    wg.A.seg[0] = aseg(v, 64, 64, g->center, N);
-    wg.A.seg[1] = aseg(v, 64, 64, g->nbr, N);
-    wg.A.seg[2] = aseg(e, 64, 64);
-    wg.A.nseg = 3;
-    wg.M = (int)E; wg.K = 192; wg.tc = 1;
+    wg.A.seg[0] = aseg(e, 64, 64);
+    wg.A.nseg = 1;
+    wg.M = (int)E; wg.K = 64; wg.tc = 1;
     wg.D = dZ; wg.ldd = 128; wg.N = 128; wg.bias = 1;
-    wg.dst[0].W = Bw.G(pre + ".core.W1"); wg.dst[0].ldw = 64; wg.dst[0].b = Bw.G(pre + ".core.b1");
-    wg.dst[1].W = Bw.G(pre + ".gate.W1"); wg.dst[1].ldw = 64; wg.dst[1].b = Bw.G(pre + ".gate.b1");
+    wg.dst[0].W = Bw.G(pre + ".core.W1") + 128 * 64; wg.dst[0].ldw = 64; wg.dst[0].b = Bw.G(pre + ".core.b1");
+    wg.dst[1].W = Bw.G(pre + ".gate.W1") + 128 * 64; wg.dst[1].ldw = 64; wg.dst[1].b = Bw.G(pre + ".gate.b1");
     wg.tag = "ac_W1_wg";
     wgrad(ctx, wg);
+    WGrad wv;
+    wv.A.seg[0] = aseg(v, 64, 64);
+    wv.A.nseg = 1;
+    wv.M = (int)N; wv.K = 64; wv.tc = 1;
+    wv.D = S; wv.ldd = 256; wv.N = 256; wv.bias = 0;
+    wv.dst[0].W = Bw.G(pre + ".core.W1"); wv.dst[0].ldw = 64;
+    wv.dst[1].W = Bw.G(pre + ".gate.W1"); wv.dst[1].ldw = 64;
+    wv.dst[2].W = Bw.G(pre + ".core.W1") + 64 * 64; wv.dst[2].ldw = 64;
+    wv.dst[3].W = Bw.G(pre + ".gate.W1") + 64 * 64; wv.dst[3].ldw = 64;
+    wv.tag = "ac_W1v_wg";
+    wgrad(ctx, wv);
   }
-  // dv_i: CSR row sum; dv_j: rows of j through the reverse-edge map (no atomics)
-  SegSrc s[2];
-  s[0].in = ti; s[0].ptr = g->row_ptr; s[0].rows = E;
-  s[1].in = tj; s[1].ptr = g->row_ptr; s[1].perm = g->rev; s[1].rows = E;
-  segsum(ctx, N, dv, 64, 1, 2, s, "segsum_ac_dv");
+  {  // dv += [S_i | S_j] · [W1_c[0:64]ᵀ ; W1_g[0:64]ᵀ ; W1_c[64:128]ᵀ ; W1_g[64:128]ᵀ]
+    RowGemm G;
+    G.A.seg[0] = aseg(S, 256, 256);
+    G.A.nseg = 1;
+    G.M = (int)N; G.K = 256; G.nchunk = 1; G.tc = 1;
+    Chunk &C = G.ch[0];
+    C.W[0] = Bw.WT(pre + ".core.W1"); C.ldw[0] = 192;
+    C.W[1] = Bw.WT(pre + ".gate.W1"); C.ldw[1] = 192;
+    C.W[2] = Bw.WT(pre + ".core.W1") + 64; C.ldw[2] = 192;
+    C.W[3] = Bw.WT(pre + ".gate.W1") + 64; C.ldw[3] = 192;
+    C.wk0[0] = 0; C.wk0[1] = 64; C.wk0[2] = 128; C.wk0[3] = 192; C.wk0[4] = 256; C.nwb = 4;
+    C.out = dv; C.ldo = 64; C.resid = dv; C.ldr = 64;
+    G.tag = "ac_dvS";
+    rowgemm(ctx, G);
+  }
 }
 
 // phase 1: everything that touches neither dv nor de (may run concurrently with ac_bwd_body);
-// phase 2: the dv / de segmented adjoint sums (after the atom conv's updates, fixed order)
+// phase 2: the dv / de updates (after the atom conv's updates, fixed order)
 void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float *e, const float *a, const float *eb,
                  const float *daggb, float *dv, float *de, float *da, float *deb, int phase) {
   chg_ctx *ctx = Bw.ctx;
@@ -449,19 +526,38 @@ void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float 
   const int64_t N = g->N, E = g->E, B = g->B, A = g->A;
   if (A == 0) return;
   std::string bp = "bond" + std::to_string(t), ap = "angle" + std::to_string(t), ts = std::to_string(t);
-  float *q1 = Bw.scratch("bc_q1", A, 64), *q2 = Bw.scratch("bc_q2", A, 64);
-  float *tv = Bw.scratch("tmp_vi", A, 64), *t1 = Bw.scratch("tmp_e1", A, 64), *t2 = Bw.scratch("tmp_e2", A, 64);
+  const float *W[4], *bias[4];
+  const int nw = bc_first_weights(Bw.m, t, angle_branch, W, bias);
+  const int Kx = 64 * nw;                           // width of dZ used: bond hidden (+ angle pre-LN)
+  float *S1 = Bw.scratch("bc_S1", B, 256), *S2 = Bw.scratch("bc_S2", B, 256), *Sv = Bw.scratch("bc_Sv", N, 256);
+  float *tb = Bw.scratch("bc_tb", B, 64);
+  auto WTp = [&](int c) { return Bw.WT(c < 2 ? bp + (c ? ".gate.W1" : ".core.W1") : ap + (c == 3 ? ".gate.W" : ".core.W")); };
+  auto Gp = [&](int c) { return Bw.G(c < 2 ? bp + (c ? ".gate.W1" : ".core.W1") : ap + (c == 3 ? ".gate.W" : ".core.W")); };
+  // d(part) GEMM: out (+)= Src · [W_c[r0:r0+64]ᵀ]_c   (Src [rows, Kx], ld 256)
+  auto part_adjoint = [&](const float *Src, int lds, int64_t rows, int r0, float *out, bool accumulate, const char *tag) {
+    if (rows <= 0) return;
+    RowGemm G;
+    G.A.seg[0] = aseg(Src, lds, Kx);
+    G.A.nseg = 1;                                    // fp32 sums (not TF32-rounded)
+    G.M = (int)rows; G.K = Kx; G.nchunk = 1; G.tc = 1;
+    Chunk &C = G.ch[0];
+    for (int c = 0; c < nw; ++c) { C.W[c] = WTp(c) + r0; C.ldw[c] = 256; C.wk0[c] = 64 * c; }
+    C.wk0[nw] = Kx; C.nwb = nw;
+    C.out = out; C.ldo = 64;
+    if (accumulate) { C.resid = out; C.ldr = 64; }
+    G.tag = tag;
+    rowgemm(ctx, G);
+  };
   if (phase == 2) {
-    SegSrc s[2];
-    s[0].in = tv; s[0].ptr = g->atom_angle_ptr; s[0].rows = A;                // angles of centre i are contiguous
-    segsum(ctx, N, dv, 64, 1, 1, s, "segsum_bc_dv");
-    s[0] = SegSrc(); s[0].in = t1; s[0].ptr = g->angle_ptr; s[0].segmap = g->bond_id; s[0].rows = A;
-    s[1] = SegSrc(); s[1].in = t2; s[1].ptr = g->angle_ptr; s[1].segmap = g->bond_id; s[1].perm = g->swap; s[1].rows = A;
-    segsum(ctx, E, de, 64, 1, 2, s, "segsum_bc_de");
+    part_adjoint(Sv, 256, N, 0, dv, true, "bc_dvS");                 // v_i part
+    part_adjoint(S1, 256, B, 64, tb, false, "bc_deS");                // e_ij part (first bond)
+    part_adjoint(S2, 256, B, 128, tb, true, "bc_deS");                // e_ik part (second bond)
+    rows_add(ctx, B, g->bond_edge, tb, de);                          // bond rows -> their edges
     return;
   }
   const float *z1 = Bw.act("bc_z1_" + ts), *yb = Bw.act("bc_yb_" + ts);
   float *dYb = Bw.scratch("bc_dYb", A, 128), *dZ = Bw.scratch("bc_dZ", A, 256);
+  float *q1 = Bw.scratch("bc_q1", A, 64), *q2 = Bw.scratch("bc_q2", A, 64);
   gate_bwd(ctx, A, yb, 128, Bw.ln(bp), GATE_MUL_W1W2, eb, g->angle_b1, g->angle_b2, daggb, g->angle_b1, dYb, 128,
            nullptr, q1, q2, Bw.lng(bp));
   if (angle_branch)
@@ -502,46 +598,50 @@ void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float 
     wg.tag = "bc_W2_wg";
     wgrad(ctx, wg);
   }
-  const int Kx = angle_branch ? 256 : 128;
-  {  // dX = [dZ1_bond | dY_angle] · [W1_bcᵀ; W1_bgᵀ; W_acᵀ; W_agᵀ] -> (v_i, e_ij, e_ik, a)
+  // da += [dZ1_bond | dY_angle] · [W_c[192:256]ᵀ]_c   (the row's own part a_ijk)
+  {
     RowGemm G;
     G.A.seg[0] = aseg(dZ, 256, Kx);
     G.A.nseg = 1; G.A.rounded = ctx->tc_round();
-    G.M = (int)A; G.K = Kx; G.nchunk = 4; G.tc = 1;
-    float *outs[4] = {tv, t1, t2, da};
-    for (int c = 0; c < 4; ++c) {
-      Chunk &C = G.ch[c];
-      C.W[0] = Bw.WT(bp + ".core.W1") + 64 * c; C.ldw[0] = 256;
-      C.W[1] = Bw.WT(bp + ".gate.W1") + 64 * c; C.ldw[1] = 256;
-      C.wk0[0] = 0; C.wk0[1] = 64; C.wk0[2] = 128; C.nwb = 2;
-      if (angle_branch) {
-        C.W[2] = Bw.WT(ap + ".core.W") + 64 * c; C.ldw[2] = 256;
-        C.W[3] = Bw.WT(ap + ".gate.W") + 64 * c; C.ldw[3] = 256;
-        C.wk0[3] = 192; C.wk0[4] = 256; C.nwb = 4;
-      }
-      C.out = outs[c]; C.ldo = 64;
-      if (c == 3) { C.resid = da; C.ldr = 64; }
-    }
+    G.M = (int)A; G.K = Kx; G.nchunk = 1; G.tc = 1;
+    Chunk &C = G.ch[0];
+    for (int c = 0; c < nw; ++c) { C.W[c] = WTp(c) + 192; C.ldw[c] = 256; C.wk0[c] = 64 * c; }
+    C.wk0[nw] = Kx; C.nwb = nw;
+    C.out = da; C.ldo = 64; C.resid = da; C.ldr = 64;
     G.tag = "bc_dX";
     rowgemm(ctx, G);
   }
-  {  // dW1 (bond) and dW (angle) = Xᵀ [dZ1 | dY_a]
-    WGrad wg;
-    wg.A.seg[0] = aseg(v, 64, 64, g->angle_ctr, N);
-    wg.A.seg[1] = aseg(e, 64, 64, g->angle_e1, E);
-    wg.A.seg[2] = aseg(e, 64, 64, g->angle_e2, E);
-    wg.A.seg[3] = aseg(a, 64, 64);
-    wg.A.nseg = 4;
-    wg.M = (int)A; wg.K = 256; wg.tc = 1;
-    wg.D = dZ; wg.ldd = 256; wg.N = Kx; wg.bias = 1;
-    wg.dst[0].W = Bw.G(bp + ".core.W1"); wg.dst[0].ldw = 64; wg.dst[0].b = Bw.G(bp + ".core.b1");
-    wg.dst[1].W = Bw.G(bp + ".gate.W1"); wg.dst[1].ldw = 64; wg.dst[1].b = Bw.G(bp + ".gate.b1");
-    if (angle_branch) {
-      wg.dst[2].W = Bw.G(ap + ".core.W"); wg.dst[2].ldw = 64; wg.dst[2].b = Bw.G(ap + ".core.b");
-      wg.dst[3].W = Bw.G(ap + ".gate.W"); wg.dst[3].ldw = 64; wg.dst[3].b = Bw.G(ap + ".gate.b");
-    }
-    wg.tag = "bc_W1_wg";
-    wgrad(ctx, wg);
+  {  // S1[b] = Σ_{angles with first bond b} dZ, S2[b] = Σ_{angles with second bond b} dZ (swap
+     // order), Sv[i] = Σ_{bonds b at centre i} S1[b]
+    SegSrc s;
+    s.in = dZ; s.ld = 256; s.ptr = g->angle_ptr; s.rows = A;
+    segsum(ctx, B, S1, 256, 0, 1, &s, "segsum_bc_S", Kx);
+    s.perm = g->swap;
+    segsum(ctx, B, S2, 256, 0, 1, &s, "segsum_bc_S", Kx);
+    SegSrc u;
+    u.in = S1; u.ld = 256; u.ptr = g->bond_ptr; u.rows = B;
+    segsum(ctx, N, Sv, 256, 0, 1, &u, "segsum_bc_S", Kx);
+  }
+  {  // dW (bond W1 and angle W): a part over angles (with the biases), v / e_ij / e_ik parts over
+     // atoms and bonds
+    auto wpart = [&](const ASeg &x, int64_t rows, const float *D, int r0, int with_bias, const char *tag) {
+      if (rows <= 0) return;
+      WGrad wg;
+      wg.A.seg[0] = x;
+      wg.A.nseg = 1;
+      wg.M = (int)rows; wg.K = 64; wg.tc = 1;
+      wg.D = D; wg.ldd = 256; wg.N = Kx; wg.bias = with_bias;
+      for (int c = 0; c < nw; ++c) {
+        wg.dst[c].W = Gp(c) + (size_t)r0 * 64; wg.dst[c].ldw = 64;
+        if (with_bias) wg.dst[c].b = Bw.G(c < 2 ? bp + (c ? ".gate.b1" : ".core.b1") : ap + (c == 3 ? ".gate.b" : ".core.b"));
+      }
+      wg.tag = tag;
+      wgrad(ctx, wg);
+    };
+    wpart(aseg(a, 64, 64), A, dZ, 192, 1, "bc_W1_wg");
+    wpart(aseg(v, 64, 64), N, Sv, 0, 0, "bc_W1p_wg");
+    wpart(aseg(e, 64, 64, g->bond_edge, E), B, S1, 64, 0, "bc_W1p_wg");
+    wpart(aseg(e, 64, 64, g->bond_edge, E), B, S2, 128, 0, "bc_W1p_wg");
   }
   SegSrc s[2];
   s[0] = SegSrc(); s[0].in = q1; s[0].ptr = g->angle_ptr; s[0].rows = A;

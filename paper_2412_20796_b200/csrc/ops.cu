@@ -229,8 +229,10 @@ struct SegArgs { SegSrc s[3]; int n; };
 // 256-B row): row indices are fetched 16 at a time (coalesced) and broadcast by shuffle; U rows
 // are in flight per lane (all loads of a group issued, predicated, before the in-order adds)
 template <int U>
-__device__ __forceinline__ void seg_rows(const SegSrc &S, int r0, int r1, int hl, unsigned hmask, float4 &acc) {
-  const float4 *in = (const float4 *)S.in + hl;
+__device__ __forceinline__ void seg_rows(const SegSrc &S, int r0, int r1, int hl, unsigned hmask, float4 &acc,
+                                         int col0 = 0) {
+  const float4 *in = (const float4 *)(S.in + col0) + hl;
+  const int64_t st4 = S.ld >> 2;
   for (int base = r0; base < r1; base += 16) {
     const int n = min(16, r1 - base);
     const int myrow = hl < n ? (S.perm ? __ldg(S.perm + base + hl) : base + hl) : 0;
@@ -239,7 +241,7 @@ __device__ __forceinline__ void seg_rows(const SegSrc &S, int r0, int r1, int hl
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int qq = __shfl_sync(hmask, myrow, (q + u) & 15, 16);
-        v[u] = (q + u < n) ? __ldg(in + (int64_t)qq * 16) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[u] = (q + u < n) ? __ldg(in + (int64_t)qq * st4) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u)
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(256) k_segsum(int64_t targets, float *__restri
         const int a0 = r0 + (int)((int64_t)len * j / H), a1 = r0 + (int)((int64_t)len * (j + 1) / H);
         r0 = a0; r1 = a1;
       }
-      seg_rows<U>(S, r0, r1, hl, hmask, acc);
+      seg_rows<U>(S, r0, r1, hl, hmask, acc, 64 * (int)blockIdx.y);
     }
   }
   if (H > 1) {
@@ -294,7 +296,7 @@ __global__ void __launch_bounds__(256) k_segsum(int64_t targets, float *__restri
   } else if (t >= targets) {
     return;
   }
-  float4 *o = (float4 *)(out + t * ldo) + hl;
+  float4 *o = (float4 *)(out + t * ldo + 64 * blockIdx.y) + hl;
   if (accumulate) { const float4 p = *o; acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w; }
   *o = acc;
 }
@@ -656,17 +658,19 @@ void gate_bwd(chg_ctx *ctx, int64_t rows, const float *y, int ldy, GateLN ln, in
 }
 
 void segsum(chg_ctx *ctx, int64_t targets, float *out, int ldo, int accumulate, int nsrc, const SegSrc *src,
-            const char *tag) {
+            const char *tag, int ncols) {
   if (targets <= 0) return;
+  if (ncols % 64 || ncols <= 0) CHG_THROW(CHG_ERR_STATE, "segsum: ncols %d not a multiple of 64", ncols);
+  const int ng = ncols / 64;
   SegArgs a;
   a.n = nsrc;
-  double bytes = targets * 256.0 * (1 + accumulate);
+  double bytes = targets * 256.0 * ng * (1 + accumulate);
   for (int k = 0; k < nsrc; ++k) {
     a.s[k] = src[k];
-    bytes += src[k].rows * (256.0 + (src[k].perm ? 4.0 : 0.0)) + targets * (src[k].segmap ? 12.0 : 8.0);
+    bytes += src[k].rows * (256.0 * ng + (src[k].perm ? 4.0 : 0.0)) + targets * (src[k].segmap ? 12.0 : 8.0);
   }
   for (int k = 0; k < nsrc; ++k)
-    if (((uintptr_t)src[k].in & 15) || ((uintptr_t)out & 15) || (ldo & 3))
+    if (((uintptr_t)src[k].in & 15) || ((uintptr_t)out & 15) || (ldo & 3) || (src[k].ld & 3))
       CHG_THROW(CHG_ERR_STATE, "segsum: 16-byte alignment required (in %p, out %p, ldo %d)", (const void *)src[k].in,
                 (void *)out, ldo);
   // half-warps per target from the mean segment length (rows per half-warp ~ 16 or more)
@@ -675,7 +679,7 @@ void segsum(chg_ctx *ctx, int64_t targets, float *out, int ldo, int accumulate, 
   const int64_t mean = rows / std::max<int64_t>(targets, 1);
   const int H = seg_split(mean, targets);
   ProfScope ps(ctx, tag, 0.0, bytes);
-  const int grid = ceil_div(targets * 16 * H, 256);
+  const dim3 grid(ceil_div(targets * 16 * H, 256), ng);
   // 8 rows in flight per lane on long segments; 4 on short ones (fewer registers, more warps)
   auto go = [&](auto kern) { launch_k(ctx, kern, grid, 256, 0, ctx->stream, targets, out, ldo, accumulate, a); };
   const bool deep = mean >= 16;
@@ -840,4 +844,26 @@ void finite_adam(chg_ctx *ctx, int64_t n, float *p, float *g, float *m, float *v
     check_launch(ctx);
   }
   CUDA_OK(cudaMemcpyAsync(host_flag, bad, 4, cudaMemcpyDeviceToHost, ctx->stream));
+}
+
+// dst[idx[r]] += src[r] for 64-float rows (idx injective: deterministic, no atomics)
+namespace {
+__global__ void k_rows_add(int64_t rows, const int32_t *__restrict__ idx, const float4 *__restrict__ src,
+                           float4 *__restrict__ dst) {
+  pdl_begin();
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;   // float4 index
+  if (i >= rows * 16) return;
+  const int64_t r = i >> 4;
+  const int c = (int)(i & 15);
+  float4 *d = dst + (int64_t)__ldg(idx + r) * 16 + c;
+  const float4 s = __ldg(src + i), o = *d;
+  *d = make_float4(o.x + s.x, o.y + s.y, o.z + s.z, o.w + s.w);
+}
+}  // namespace
+
+void rows_add(chg_ctx *ctx, int64_t rows, const int32_t *idx, const float *src, float *dst) {
+  if (rows <= 0) return;
+  ProfScope ps(ctx, "rows_add", 0.0, rows * (256.0 * 3 + 4.0));
+  launch_k(ctx, k_rows_add, ceil_div(rows * 16, 256), 256, 0, ctx->stream, rows, idx, (const float4 *)src, (float4 *)dst);
+  check_launch(ctx);
 }

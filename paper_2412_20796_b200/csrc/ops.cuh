@@ -19,10 +19,12 @@ void gate_bwd(chg_ctx *ctx, int64_t rows, const float *y, int ldy, GateLN ln, in
 // with s = segmap ? segmap[t] : t + ptr_off (segmap < 0 -> nothing).  64 columns.
 struct SegSrc { const float *in = nullptr; const int32_t *ptr = nullptr; const int32_t *perm = nullptr;
                 const int32_t *segmap = nullptr; int ptr_off = 0;
+                int ld = 64;        // row stride of `in` (floats, multiple of 4)
                 int64_t rows = 0;   // total input rows summed (algorithmic-bytes bookkeeping only)
 };
+// ncols (multiple of 64): column groups of 64 summed by grid.y (input column 64·y of every source)
 void segsum(chg_ctx *ctx, int64_t targets, float *out, int ldo, int accumulate, int nsrc, const SegSrc *src,
-            const char *tag = "segsum");
+            const char *tag = "segsum", int ncols = 64);
 
 // segmented sum fused with the 64x64 linear that consumes it: agg = Σ rows (stored),
 // out = (agg·W + bias) + resid (bias / resid optional); W row-major [64][64]
@@ -57,6 +59,8 @@ void proj_bwd(chg_ctx *ctx, int64_t rows, const float *basis, const float *dbdf,
 // float4 rows (64 floats), tmp holds the product for the B bond rows
 void edge_update(chg_ctx *ctx, int64_t E, const float *e, const float *bias, const int32_t *bond_id, const float *tmp,
                  float *out);
+// dst[idx[r]] += src[r], 64-float rows, idx injective (bond rows -> their atom-graph edges)
+void rows_add(chg_ctx *ctx, int64_t rows, const int32_t *idx, const float *src, float *dst);
 // grad[0..63] += column sums of D [rows, 64] (deterministic)
 void colsum(chg_ctx *ctx, int64_t rows, const float *D, float *grad);
 

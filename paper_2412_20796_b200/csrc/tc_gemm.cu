@@ -169,26 +169,32 @@ struct TcPlan {
   int split;         // 1: 3xTF32 (mlp_precision 1): operands split x = hi + lo (both TF32), three MMAs
                      //    A_lo·B_hi + A_hi·B_lo + A_hi·B_hi per K step; stages hold [hi | lo]
   int nsb;           // B ring slots (<= NSB) when the image is not resident
+  // compact weight image: K chunk kc holds only the chunks whose A window covers it (block-
+  // diagonal GEMMs — the second GatedMLP layer, its adjoint — store half the columns), bnt
+  // columns per K chunk, chunk c at column bcoff[kc][c] (-1: not active in kc)
+  int bnt;
+  int16_t bcoff[16][4];
 };
 
-// B image: img[kc][q][n][4] = tf32(W_chunk(n - coff, k = lo + kc·KC - a_k0 + 4q + r))
+// B image: img[kc][q][n][4] = tf32(W_chunk(n - bcoff[kc][c], k = lo + kc·KC - a_k0 + 4q + r))
 __device__ __forceinline__ void pack_elem(const RowGemm &g, const TcPlan &P, uint32_t *__restrict__ img, int kc,
                                           int n, int k) {
   float v = 0.f;
   for (int c = 0; c < g.nchunk; ++c) {
     const Chunk &C = g.ch[c];
-    int j = n - P.coff[c];
+    if (P.bcoff[kc][c] < 0) continue;
+    int j = n - P.bcoff[kc][c];
     if (j < 0 || j >= C.ncols) continue;
     int kk = P.lo + kc * KC - C.a_k0 + k;
     if (kk < 0 || kk >= g.K) continue;
     for (int b = 0; b < C.nwb; ++b)
       if (kk >= C.wk0[b] && kk < C.wk0[b + 1]) v = C.Wk[b][(size_t)j * C.ldwk[b] + (kk - C.wk0[b])];
   }
-  const size_t at = (size_t)kc * P.ntot * KC + ((k >> 2) * P.ntot + n) * 4 + (k & 3);
+  const size_t at = (size_t)kc * P.bnt * KC + ((k >> 2) * P.bnt + n) * 4 + (k & 3);
   const uint32_t hi = to_tf32(v);
   img[at] = hi;
   if (P.split)                                   // lo image: the TF32 rounding of the remainder
-    img[(size_t)(P.width / KC) * P.ntot * KC + at] = to_tf32(v - __uint_as_float(hi));
+    img[(size_t)(P.width / KC) * P.bnt * KC + at] = to_tf32(v - __uint_as_float(hi));
 }
 
 // every cached image of a model in one launch (blockIdx.y = site), after the weights changed
@@ -201,7 +207,7 @@ struct PackJob {
 __global__ void k_pack_all(const PackJob *__restrict__ jobs) {
   pdl_begin();
   const PackJob &J = jobs[blockIdx.y];
-  const int per = J.P.ntot * KC, total = J.nkc * per;
+  const int per = J.P.bnt * KC, total = J.nkc * per;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
     const int kc = idx / per, r = idx % per;
     pack_elem(J.g, J.P, J.img, kc, r / KC, r % KC);
@@ -211,8 +217,8 @@ __global__ void k_pack_all(const PackJob *__restrict__ jobs) {
 __global__ void k_pack_b(const RowGemm g, const TcPlan P, uint32_t *__restrict__ img) {
   pdl_begin();
   int kc = blockIdx.y;
-  int idx = blockIdx.x * blockDim.x + threadIdx.x;   // over NT * KC
-  if (idx >= P.ntot * KC) return;
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;   // over bnt * KC
+  if (idx >= P.bnt * KC) return;
   int n = idx / KC, k = idx % KC;
   pack_elem(g, P, img, kc, n, k);
 }
@@ -296,6 +302,10 @@ __device__ __noinline__ void epi_rows_any(const Chunk &C, int act, const float *
   for (int rr = 0; rr < nrows; ++rr) {
     const size_t mr = (size_t)(row0 + rr);
     float v = stile[rr * 33 + lane] + bn;
+    for (int k = 0; k < C.ngadd; ++k) {
+      const int r = C.gidx[k] ? __ldg(C.gidx[k] + mr) : (int)mr;
+      v += __ldg(C.gadd[k] + (size_t)r * C.ldga[k] + n);
+    }
     if (C.pre) C.pre[mr * C.ldp + n] = v;
     if (act == 1) v = siluf_(v);
     if (C.mul) v *= dsiluf_(C.mul[mr * C.ldm + n]);
@@ -311,7 +321,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
   // SWIZZLE_128B operand atoms need 1024-B aligned stage bases
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int NT = P.ntot;
+  const int NT = P.bnt;                                 // weight-image columns per K chunk
   const uint32_t a_bytes = KC * TCM * 4, b_bytes = KC * NT * 4;
   const uint32_t a_stage = a_bytes << P.split, b_stage = b_bytes << P.split;   // [hi | lo] in split mode
   const int NSA = P.nsa, NSBr = P.nsb;
@@ -522,12 +532,12 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
 #pragma unroll
             for (int j = 0; j < KC / 8; ++j) {
               uint64_t ad = make_desc(a_base + j * 32, 16, 1024) | ((uint64_t)2 << 61);   // SWIZZLE_128B
-              uint64_t bd = make_desc(b_base + j * 2 * (NT * 16) + P.coff[c] * 16, NT * 16, 128);
+              uint64_t bd = make_desc(b_base + j * 2 * (NT * 16) + P.bcoff[kc][c] * 16, NT * 16, 128);
               const uint32_t acc = (started[gr] || j > 0) ? 1u : 0u;
               if (TC_SKIP(8)) continue;                   // debug: no tensor-core work
               if (P.split) {                              // 3xTF32: small terms first, then hi·hi
                 const uint64_t ad_lo = make_desc(a_base + a_bytes + j * 32, 16, 1024) | ((uint64_t)2 << 61);
-                const uint64_t bd_lo = make_desc(b_base + b_bytes + j * 2 * (NT * 16) + P.coff[c] * 16, NT * 16, 128);
+                const uint64_t bd_lo = make_desc(b_base + b_bytes + j * 2 * (NT * 16) + P.bcoff[kc][c] * 16, NT * 16, 128);
                 mma_tf32(tmem + a * tcols + P.coff[c], ad_lo, bd, idesc, acc);
                 mma_tf32(tmem + a * tcols + P.coff[c], ad, bd_lo, idesc, 1u);
                 mma_tf32(tmem + a * tcols + P.coff[c], ad, bd, idesc, 1u);
@@ -619,6 +629,20 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
             for (int q = 0; q < 32; ++q) v[q] += __ldg(C.bias + j0 + q);
           }
           const int m = row0 + lane;
+          if (C.ngadd && m < g.M) {                     // gathered row additions (factorised layer 1)
+#pragma unroll 1
+            for (int k = 0; k < C.ngadd; ++k) {
+              const int r = C.gidx[k] ? __ldg(C.gidx[k] + m) : m;
+              const float4 *src = reinterpret_cast<const float4 *>(C.gadd[k] + (size_t)r * C.ldga[k] + j0);
+              float4 u[8];
+#pragma unroll
+              for (int q4 = 0; q4 < 8; ++q4) u[q4] = __ldg(src + q4);
+#pragma unroll
+              for (int q4 = 0; q4 < 8; ++q4) {
+                v[4 * q4] += u[q4].x; v[4 * q4 + 1] += u[q4].y; v[4 * q4 + 2] += u[q4].z; v[4 * q4 + 3] += u[q4].w;
+              }
+            }
+          }
           if (kord[i] >= 0) {
             const int sl = kord[i] % NB;
             mbar_wait(&obar[sl], (ophase >> sl) & 1);
@@ -722,7 +746,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
             else epi_rows_op<false>(C, stile, ob, lane, row0, nrows, n, bn);
           } else {
             // flags are uniform per 32x32 block: one specialised row loop per combination
-            const int code = (C.pre ? 1 : 0) | (C.mul ? 2 : 0) | (C.resid ? 4 : 0) | (g.act == 1 ? 8 : 0);
+            const int code = (C.pre ? 1 : 0) | (C.mul ? 2 : 0) | (C.resid ? 4 : 0) | (g.act == 1 ? 8 : 0) |
+                             (C.ngadd ? 16 : 0);
             switch (code) {
               case 0: epi_rows<false, false, false, false>(C, stile, lane, row0, nrows, n, bn); break;
               case 2: epi_rows<false, true, false, false>(C, stile, lane, row0, nrows, n, bn); break;
@@ -1070,7 +1095,7 @@ void tc_repack_all(chg_ctx *ctx, chg_model *m) {
     c->dirty = false;
   }
   double bytes = 0;
-  for (auto &J : c->jobs) bytes += (double)J.nkc * J.P.ntot * KC * 8.0 * (1 + J.P.split);
+  for (auto &J : c->jobs) bytes += (double)J.nkc * J.P.bnt * KC * 8.0 * (1 + J.P.split);
   ProfScope ps(ctx, "tc_pack", 0.0, bytes);
   launch_k(ctx, k_pack_all, dim3(148, (unsigned)c->jobs.size()), 256, 0, ctx->stream, c->d_jobs);
   check_launch(ctx);
@@ -1177,6 +1202,9 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
     tot += S.width;
   }
   if (hi > tot) return false;
+  for (int c = 0; c < g.nchunk; ++c)                  // gathered additions: 16-B rows, no TMA-operand chunk
+    for (int k = 0; k < g.ch[c].ngadd; ++k)
+      if (((uintptr_t)g.ch[c].gadd[k] & 15) || (g.ch[c].ldga[k] & 3) || g.ch[c].mul || g.ch[c].resid) return false;
   P.lo = lo;
   P.width = hi - lo;
   P.ntot = off;
@@ -1197,8 +1225,24 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   }
   if (P.ntot > 256) return false;
   P.tmem_cols = P.ntot <= 32 ? 32 : P.ntot <= 64 ? 64 : P.ntot <= 128 ? 128 : 256;
+  {  // compact weight image: per K chunk only the chunks whose window covers it
+    const int nkc0 = P.width / KC;
+    if (nkc0 > 16) return false;
+    P.bnt = 0;
+    for (int kc = 0; kc < nkc0; ++kc) {
+      int w = 0;
+      for (int c = 0; c < 4; ++c) P.bcoff[kc][c] = -1;
+      for (int c = 0; c < g.nchunk; ++c) {
+        const int kk = P.lo + kc * KC - g.ch[c].a_k0;
+        if (kk < 0 || kk >= g.K) continue;
+        P.bcoff[kc][c] = (int16_t)w;
+        w += (g.ch[c].ncols + 31) / 32 * 32;
+      }
+      P.bnt = std::max(P.bnt, w);
+    }
+  }
   const int nkc = P.width / KC;
-  const size_t bchunk = ((size_t)KC * P.ntot * 4) << split, achunk = ((size_t)KC * TCM * 4) << split;
+  const size_t bchunk = ((size_t)KC * P.bnt * 4) << split, achunk = ((size_t)KC * TCM * 4) << split;
   const int nsa_min = split ? 2 : 4;
   // TMA-store epilogue (lane = row) when every chunk's output is a plain [M][32k] table
   static const bool no_tstore = getenv("CHG_TC_NO_TSTORE") != nullptr;   // A/B knob
@@ -1270,7 +1314,7 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
     if (it != cache->index.end() && cache->gen[it->second] == cache->cur_gen) img = cache->jobs[it->second].img;
   }
   if (!img) {
-    const size_t bytes = ((size_t)nkc * P.ntot * KC * 4) << split;   // hi image (+ lo image)
+    const size_t bytes = ((size_t)nkc * P.bnt * KC * 4) << split;    // hi image (+ lo image)
     if (cache) {
       auto it = cache->index.find(key);
       int id;
@@ -1291,8 +1335,8 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
     } else {
       img = (uint32_t *)ctx->get("tc_bimg", bytes);
     }
-    ProfScope ps(ctx, "tc_pack", 0.0, (double)nkc * P.ntot * KC * 8.0);
-    dim3 grid(ceil_div((int64_t)P.ntot * KC, 256), nkc);
+    ProfScope ps(ctx, "tc_pack", 0.0, (double)nkc * P.bnt * KC * 8.0);
+    dim3 grid(ceil_div((int64_t)P.bnt * KC, 256), nkc);
     launch_k(ctx, k_pack_b, grid, 256, 0, ctx->stream, g, P, img);
     check_launch(ctx);
   }
