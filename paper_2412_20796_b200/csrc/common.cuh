@@ -309,7 +309,9 @@ inline void launch_k(chg_ctx *ctx, void (*kern)(KArgs...), dim3 grid, dim3 block
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   // not while two streams run: early-launched CTAs waiting on their predecessor would hold SM
   // slots the other stream's kernels need (measured: fp32 C2 -12 %, C3 -1 %)
-  at[0].val.programmaticStreamSerializationAllowed = (no_pdl || ctx->forked) ? 0 : 1;
+  // (and not inside a stream capture on a multi-rank ctx: the launch failed there, "invalid device
+  // function", on NCCL-initialised contexts)
+  at[0].val.programmaticStreamSerializationAllowed = (no_pdl || ctx->forked || (ctx->capturing && ctx->nranks > 1)) ? 0 : 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);   // errors: check_launch (cudaGetLastError)

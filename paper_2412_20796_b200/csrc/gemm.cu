@@ -46,7 +46,7 @@ __device__ __forceinline__ float loadA1(const AOp &A, int m, int col) {
 // W(k, n..n+3) as one 16-B load when aligned (else per element; zeros past ncols)
 __device__ __forceinline__ float4 loadW4(const Chunk &c, int k, int n) {
 #pragma unroll
-  for (int b = 0; b < 4; ++b)
+  for (int b = 0; b < 8; ++b)
     if (b < c.nwb && k >= c.wk0[b] && k < c.wk0[b + 1]) {
       const float *p = c.W[b] + (size_t)(k - c.wk0[b]) * c.ldw[b] + n;
       if (n + 3 < c.ncols && ((uintptr_t)p & 15) == 0) return __ldg((const float4 *)p);
@@ -371,6 +371,23 @@ static void launch_wgrad_reduce(chg_ctx *ctx, const WGrad &g, const float *parti
     j.W[c] = g.dst[c].W; j.ldw[c] = g.dst[c].ldw; j.b[c] = g.dst[c].b; j.k0[c] = g.dst[c].k0; j.kn[c] = g.dst[c].kn;
   }
   red_push(ctx, j);
+}
+
+bool rowgemm_gate(chg_ctx *ctx, const RowGemm &g) {
+  if (g.M <= 0) return true;
+  if (g.gate.on && g.tc && ctx->use_tc && ctx->cur_model && ctx->cur_wt) {
+    RowGemm h = g;
+    bool ok = true;
+    for (int c = 0; c < h.nchunk && ok; ++c)
+      for (int b = 0; b < h.ch[c].nwb && ok; ++b)
+        ok = kmajor_of(ctx->cur_model, ctx->cur_wt, h.ch[c].W[b], h.ch[c].ldw[b], &h.ch[c].Wk[b], &h.ch[c].ldwk[b]);
+    static const bool no_fuse = getenv("CHG_NO_GATE_FUSION") != nullptr;   // A/B knob
+    if (ok && !no_fuse && rowgemm_tc(ctx, h)) return true;
+  }
+  RowGemm h = g;
+  h.gate.on = 0;
+  rowgemm(ctx, h);
+  return false;
 }
 
 void wgrad(chg_ctx *ctx, const WGrad &g) {

@@ -29,9 +29,9 @@ struct AOp {
 };
 
 struct Chunk {
-  const float *W[4] = {nullptr, nullptr, nullptr, nullptr};  // row blocks of W
-  int ldw[4] = {0, 0, 0, 0};
-  int wk0[5] = {0, 0, 0, 0, 0};  // row-block starts, wk0[nwb] = K
+  const float *W[8] = {};        // row blocks of W (up to 8)
+  int ldw[8] = {};
+  int wk0[9] = {};               // row-block starts, wk0[nwb] = K
   int nwb = 1;
   const float *bias = nullptr;
   int a_k0 = 0;                  // first A column read by this chunk
@@ -50,11 +50,25 @@ struct Chunk {
   int ngadd = 0;
   // K-major view of the same weight blocks (element (n, k) at Wk[b][n*ldwk[b] + k - wk0[b]]),
   // filled by the orchestration for the tensor-core path (tc_gemm.cu)
-  const float *Wk[4] = {nullptr, nullptr, nullptr, nullptr};
-  int ldwk[4] = {0, 0, 0, 0};
+  const float *Wk[8] = {};
+  int ldwk[8] = {};
+};
+
+// GatedMLP output stage fused into the epilogue: for the chunk pair (c = core, c + 1 =
+// gate) of 64 columns each, y = the pair's pre-LN outputs (still stored when write_y, for the
+// backward) and out = φ ⊙ w (mode 0), φ ⊙ w[i1] ⊙ w[i2] (mode 1) or resid + φ (mode 2) with
+// φ = σ(LN_g(y_g)) ⊙ SiLU(LN_c(y_c)) — the k_gate_fwd contract (ops.cuh GateMode)
+struct GateEpi {
+  int on = 0, c = 0, mode = 0, write_y = 1;
+  const float *gc = nullptr, *bc = nullptr, *gg = nullptr, *bg = nullptr;
+  const float *w = nullptr;
+  const int32_t *i1 = nullptr, *i2 = nullptr;
+  const float *resid = nullptr;
+  float *out = nullptr;                                // [M, 64]
 };
 
 struct RowGemm {
+  GateEpi gate;
   AOp A;
   int M = 0;
   int K = 0;                     // reduction length (per chunk)
@@ -88,6 +102,9 @@ void tc_repack_all(chg_ctx *ctx, chg_model *m);   // forward start (TF32 mode): 
 void tc_cache_free(chg_model *m);
 void rowgemm(chg_ctx *ctx, const RowGemm &g);      // tcgen05 when ctx->use_tc and eligible, else SIMT
 bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g);   // false if the shape does not fit the tensor-core path
+// rowgemm with a fused GatedMLP output stage (g.gate.on): true if the fused epilogue ran (tensor-core
+// path); false: the GEMM ran without it and the caller applies gate_fwd
+bool rowgemm_gate(chg_ctx *ctx, const RowGemm &g);
 void wgrad(chg_ctx *ctx, const WGrad &g);
 bool wgrad_tc(chg_ctx *ctx, const WGrad &g, float **partial, int *Kp, int *splits, bool *bias_done);
 

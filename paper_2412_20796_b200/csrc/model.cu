@@ -22,6 +22,7 @@ struct Fwd {
   chg_ctx *ctx;
   chg_model *m;
   chg_graph *g;
+  int train;                       // 0: the pre-LN activations y are not stored (no backward)
   float *buf(const std::string &n, int64_t rows, int cols) {
     float *q = ctx->getf(n, (size_t)std::max<int64_t>(rows, 1) * cols);
     ctx->dbg[n] = {q, rows, cols, cols};
@@ -62,17 +63,29 @@ void join_side(chg_ctx *ctx) {
 // products are computed once per atom / bond (P tables) and added by the per-row GEMM's
 // epilogue through the gather indices — the per-row GEMM contracts only the row's own part
 // (K = 64: e_ij for atom conv, a_ijk for bond conv / angle update).  Exact up to rounding order.
-// P[rows, 64·nw] = X · [W_0[r0:r0+64] | W_1[r0:r0+64] | ...] (one 64-column chunk per weight)
+// P[rows, 64·nw] = X · [W_0[r_0:r_0+64] | W_1[r_1:r_1+64] | ...] (one 64-column chunk per weight
+// block; r == nullptr: all blocks at row r0)
 static void part_product(chg_ctx *ctx, const ASeg &x, int64_t rows, const float *const *W, int nw, int r0, float *P,
-                         int ldP, const char *tag) {
+                         int ldP, const char *tag, const int *r = nullptr) {
   if (rows <= 0) return;
   RowGemm G;
   G.A.seg[0] = x;
   G.A.nseg = 1;
   G.M = (int)rows; G.K = 64; G.nchunk = nw; G.tc = 1;
-  for (int c = 0; c < nw; ++c) G.ch[c] = chunk1(W[c] + (size_t)r0 * 64, 64, 64, nullptr, P + 64 * c, ldP);
+  for (int c = 0; c < nw; ++c) G.ch[c] = chunk1(W[c] + (size_t)(r ? r[c] : r0) * 64, 64, 64, nullptr, P + 64 * c, ldP);
   G.tag = tag;
   rowgemm(ctx, G);
+}
+
+// the GatedMLP output stage fused into a GEMM epilogue (GateEpi, gemm.cuh): chunks (c, c + 1) =
+// (core, gate) pre-LN outputs
+static void set_gate(RowGemm &G, const Fwd &F, const std::string &pre, int mode, const float *w, const int32_t *i1,
+                     const int32_t *i2, const float *resid, float *out, int c = 0) {
+  GateEpi &E = G.gate;
+  E.on = 1; E.c = c; E.mode = mode; E.write_y = F.train;
+  E.gc = F.m->p(pre + ".ln_core.g"); E.bc = F.m->p(pre + ".ln_core.b");
+  E.gg = F.m->p(pre + ".ln_gate.g"); E.bg = F.m->p(pre + ".ln_gate.b");
+  E.w = w; E.i1 = i1; E.i2 = i2; E.resid = resid; E.out = out;
 }
 
 // --- Atom Conv (Eq. 4) ------------------------------------------------------
@@ -89,9 +102,9 @@ void atom_conv_fwd(Fwd &F, int t, const float *v, const float *e, const float *e
   const float *W1c = m->p(pre + ".core.W1"), *W1g = m->p(pre + ".gate.W1");
   {  // per atom: Pa = v · [W1c_i | W1g_i | W1c_j | W1g_j]  (rows 0..63: v_i part, 64..127: v_j part)
     float *Pa = ctx->getf(ctx->ws_name("ac_P"), (size_t)std::max<int64_t>(N, 1) * 256);
-    const float *Wi[2] = {W1c, W1g};
-    part_product(ctx, aseg(v, 64, 64), N, Wi, 2, 0, Pa, 256, "ac_P");
-    part_product(ctx, aseg(v, 64, 64), N, Wi, 2, 64, Pa + 128, 256, "ac_P");
+    const float *Wi[4] = {W1c, W1g, W1c, W1g};
+    const int ri[4] = {0, 0, 64, 64};
+    part_product(ctx, aseg(v, 64, 64), N, Wi, 4, 0, Pa, 256, "ac_P", ri);
     // per edge: z1 = e·W1[128:192] + b1 + Pa[i] (v_i part) + Pa[j] (v_j part)
     RowGemm G;
     G.A.seg[0] = aseg(e, 64, 64);
@@ -117,10 +130,10 @@ void atom_conv_fwd(Fwd &F, int t, const float *v, const float *e, const float *e
     G.ch[1] = chunk1(m->p(pre + ".gate.W2"), 64, 64, m->p(pre + ".gate.b2"), y + 64, 128);
     G.ch[1].a_k0 = 64;
     G.tag = "ac_f2";
-    rowgemm(ctx, G);
+    // m_e = eᵃ_e ⊙ σ(LN_g(y_g)) ⊙ SiLU(LN_c(y_c)): fused into the epilogue on the tensor-core path
+    set_gate(G, F, pre, GATE_MUL_W, ea, nullptr, nullptr, nullptr, msg);
+    if (!rowgemm_gate(ctx, G)) gate_fwd(ctx, E, y, 128, F.ln(pre), GATE_MUL_W, ea, nullptr, nullptr, nullptr, msg);
   }
-  // m_e = eᵃ_e ⊙ σ(LN_g(y_g)) ⊙ SiLU(LN_c(y_c))
-  gate_fwd(ctx, E, y, 128, F.ln(pre), GATE_MUL_W, ea, nullptr, nullptr, nullptr, msg);
   // agg_i = Σ_{e at centre i} m_e and v' = v + agg · W_out + b_out in one pass
   SegSrc s;
   s.in = msg; s.ptr = g->row_ptr; s.rows = E;
@@ -152,6 +165,7 @@ void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float
   float *ya = angle_branch ? F.buf("bc_ya_" + ts, A, 128) : nullptr;
   float *aggb = F.buf("bc_aggb_" + ts, B, 64);
   float *q = ctx->getf("msg_angle", std::max<int64_t>(A, 1) * 64);
+  bool angle_done = false;
   if (A > 0) {
     const float *W[4], *bias[4];
     const int nw = bc_first_weights(m, t, angle_branch, W, bias);
@@ -178,7 +192,9 @@ void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float
       C.ngadd = 3;
     }
     G.tag = "bc_f1";
-    rowgemm(ctx, G);
+    // a' = a + φ_a (angle update, Eq. 6) fused into the angle pair's epilogue on the tensor-core path
+    if (angle_branch) set_gate(G, F, ap, GATE_RESID, nullptr, nullptr, nullptr, a, a_out, 2);
+    angle_done = rowgemm_gate(ctx, G) && angle_branch;
     RowGemm H;
     H.A.seg[0] = aseg(z1, 128, 128);
     H.A.nseg = 1; H.A.act = 1;
@@ -187,9 +203,10 @@ void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float
     H.ch[1] = chunk1(m->p(bp + ".gate.W2"), 64, 64, m->p(bp + ".gate.b2"), yb + 64, 128);
     H.ch[1].a_k0 = 64;
     H.tag = "bc_f2";
-    rowgemm(ctx, H);
-    // q = eᵇ_ij ⊙ eᵇ_ik ⊙ φ_e
-    gate_fwd(ctx, A, yb, 128, F.ln(bp), GATE_MUL_W1W2, eb, g->angle_b1, g->angle_b2, nullptr, q);
+    // q = eᵇ_ij ⊙ eᵇ_ik ⊙ φ_e (fused into the epilogue on the tensor-core path)
+    set_gate(H, F, bp, GATE_MUL_W1W2, eb, g->angle_b1, g->angle_b2, nullptr, q);
+    if (!rowgemm_gate(ctx, H))
+      gate_fwd(ctx, A, yb, 128, F.ln(bp), GATE_MUL_W1W2, eb, g->angle_b1, g->angle_b2, nullptr, q);
   }
   {  // aggb = Σ over angles with first bond b (empty -> 0) fused with its product by W_out (B
      // bond rows only); then e' = e + 𝓛_e(agg) on all E edges (Q16): bond row (or nothing) + bias
@@ -199,7 +216,7 @@ void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float
     segsum_linear(ctx, B, 1, &s, aggb, m->p(bp + ".out.W"), nullptr, nullptr, tmp, "segsum_bc");
     edge_update(ctx, E, e, m->p(bp + ".out.b"), g->bond_id, tmp, e_out);
   }
-  if (angle_branch && A > 0)   // a' = a + φ_a
+  if (angle_branch && A > 0 && !angle_done)   // a' = a + φ_a
     gate_fwd(ctx, A, ya, 128, F.ln(ap), GATE_RESID, nullptr, nullptr, nullptr, a, a_out);
 }
 
@@ -219,7 +236,7 @@ void copy_out(chg_ctx *ctx, float *dst, const float *src, int64_t n, int on_devi
 }  // namespace
 
 void forward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, int train, chg_pred *out) {
-  Fwd F{ctx, m, g};
+  Fwd F{ctx, m, g, train};
   const int64_t N = g->N, E = g->E, B = g->B, A = g->A;
   const int T = m->cfg.n_bond_conv;
   const int p = m->cfg.envelope_p;
@@ -471,12 +488,13 @@ void ac_bwd_body(Bwd &Bw, int t, const float *v, const float *e, const float *ea
     G.tag = "ac_dX";
     rowgemm(ctx, G);
   }
-  {  // S_i = Σ_{e: centre i} dZ_e (CSR rows), S_j = Σ_{e: neighbour j} dZ_e (rows of j through rev)
-    SegSrc s;
-    s.in = dZ; s.ld = 128; s.ptr = g->row_ptr; s.rows = E;
-    segsum(ctx, N, S, 256, 0, 1, &s, "segsum_ac_S", 128);
-    s.perm = g->rev;
-    segsum(ctx, N, S + 128, 256, 0, 1, &s, "segsum_ac_S", 128);
+  {  // S_i = Σ_{e: centre i} dZ_e (CSR rows), S_j = Σ_{e: neighbour j} dZ_e (rows of j through rev):
+     // one launch, each source into its own half of S
+    SegSrc s[2];
+    s[0].in = dZ; s[0].ld = 128; s[0].ptr = g->row_ptr; s[0].rows = E;
+    s[1] = s[0]; s[1].perm = g->rev;
+    const int off[2] = {0, 128};
+    segsum(ctx, N, S, 256, 0, 2, s, "segsum_ac_S", 128, off);
   }
   {  // dW1: e part over edges (with db1), v_i / v_j parts over atoms
     WGrad wg;
@@ -529,7 +547,7 @@ void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float 
   const float *W[4], *bias[4];
   const int nw = bc_first_weights(Bw.m, t, angle_branch, W, bias);
   const int Kx = 64 * nw;                           // width of dZ used: bond hidden (+ angle pre-LN)
-  float *S1 = Bw.scratch("bc_S1", B, 256), *S2 = Bw.scratch("bc_S2", B, 256), *Sv = Bw.scratch("bc_Sv", N, 256);
+  float *S1 = Bw.scratch("bc_S12", B, 512), *S2 = S1 + 256, *Sv = Bw.scratch("bc_Sv", N, 256);
   float *tb = Bw.scratch("bc_tb", B, 64);
   auto WTp = [&](int c) { return Bw.WT(c < 2 ? bp + (c ? ".gate.W1" : ".core.W1") : ap + (c == 3 ? ".gate.W" : ".core.W")); };
   auto Gp = [&](int c) { return Bw.G(c < 2 ? bp + (c ? ".gate.W1" : ".core.W1") : ap + (c == 3 ? ".gate.W" : ".core.W")); };
@@ -550,8 +568,22 @@ void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float 
   };
   if (phase == 2) {
     part_adjoint(Sv, 256, N, 0, dv, true, "bc_dvS");                 // v_i part
-    part_adjoint(S1, 256, B, 64, tb, false, "bc_deS");                // e_ij part (first bond)
-    part_adjoint(S2, 256, B, 128, tb, true, "bc_deS");                // e_ik part (second bond)
+    if (B > 0) {  // e_ij (first bond) and e_ik (second bond) parts: tb = [S1 | S2] · [W[64:128]ᵀ ; W[128:192]ᵀ]
+      RowGemm G;
+      G.A.seg[0] = aseg(S1, 512, Kx);
+      G.A.seg[1] = aseg(S2, 512, Kx);
+      G.A.nseg = 2;
+      G.M = (int)B; G.K = 2 * Kx; G.nchunk = 1; G.tc = 1;
+      Chunk &C = G.ch[0];
+      for (int c = 0; c < nw; ++c) {
+        C.W[c] = WTp(c) + 64; C.ldw[c] = 256; C.wk0[c] = 64 * c;
+        C.W[nw + c] = WTp(c) + 128; C.ldw[nw + c] = 256; C.wk0[nw + c] = Kx + 64 * c;
+      }
+      C.wk0[2 * nw] = 2 * Kx; C.nwb = 2 * nw;
+      C.out = tb; C.ldo = 64;
+      G.tag = "bc_deS";
+      rowgemm(ctx, G);
+    }
     rows_add(ctx, B, g->bond_edge, tb, de);                          // bond rows -> their edges
     return;
   }
@@ -613,24 +645,24 @@ void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float 
   }
   {  // S1[b] = Σ_{angles with first bond b} dZ, S2[b] = Σ_{angles with second bond b} dZ (swap
      // order), Sv[i] = Σ_{bonds b at centre i} S1[b]
-    SegSrc s;
-    s.in = dZ; s.ld = 256; s.ptr = g->angle_ptr; s.rows = A;
-    segsum(ctx, B, S1, 256, 0, 1, &s, "segsum_bc_S", Kx);
-    s.perm = g->swap;
-    segsum(ctx, B, S2, 256, 0, 1, &s, "segsum_bc_S", Kx);
+    SegSrc s[2];
+    s[0].in = dZ; s[0].ld = 256; s[0].ptr = g->angle_ptr; s[0].rows = A;
+    s[1] = s[0]; s[1].perm = g->swap;
+    const int off[2] = {0, 256};                       // S1 | S2 rows of one [B, 512] table, one launch
+    segsum(ctx, B, S1, 512, 0, 2, s, "segsum_bc_S", Kx, off);
     SegSrc u;
-    u.in = S1; u.ld = 256; u.ptr = g->bond_ptr; u.rows = B;
+    u.in = S1; u.ld = 512; u.ptr = g->bond_ptr; u.rows = B;
     segsum(ctx, N, Sv, 256, 0, 1, &u, "segsum_bc_S", Kx);
   }
   {  // dW (bond W1 and angle W): a part over angles (with the biases), v / e_ij / e_ik parts over
      // atoms and bonds
-    auto wpart = [&](const ASeg &x, int64_t rows, const float *D, int r0, int with_bias, const char *tag) {
+    auto wpart = [&](const ASeg &x, int64_t rows, const float *D, int ldd, int r0, int with_bias, const char *tag) {
       if (rows <= 0) return;
       WGrad wg;
       wg.A.seg[0] = x;
       wg.A.nseg = 1;
       wg.M = (int)rows; wg.K = 64; wg.tc = 1;
-      wg.D = D; wg.ldd = 256; wg.N = Kx; wg.bias = with_bias;
+      wg.D = D; wg.ldd = ldd; wg.N = Kx; wg.bias = with_bias;
       for (int c = 0; c < nw; ++c) {
         wg.dst[c].W = Gp(c) + (size_t)r0 * 64; wg.dst[c].ldw = 64;
         if (with_bias) wg.dst[c].b = Bw.G(c < 2 ? bp + (c ? ".gate.b1" : ".core.b1") : ap + (c == 3 ? ".gate.b" : ".core.b"));
@@ -638,10 +670,10 @@ void bc_bwd_body(Bwd &Bw, int t, bool angle_branch, const float *v, const float 
       wg.tag = tag;
       wgrad(ctx, wg);
     };
-    wpart(aseg(a, 64, 64), A, dZ, 192, 1, "bc_W1_wg");
-    wpart(aseg(v, 64, 64), N, Sv, 0, 0, "bc_W1p_wg");
-    wpart(aseg(e, 64, 64, g->bond_edge, E), B, S1, 64, 0, "bc_W1p_wg");
-    wpart(aseg(e, 64, 64, g->bond_edge, E), B, S2, 128, 0, "bc_W1p_wg");
+    wpart(aseg(a, 64, 64), A, dZ, 256, 192, 1, "bc_W1_wg");
+    wpart(aseg(v, 64, 64), N, Sv, 256, 0, 0, "bc_W1p_wg");
+    wpart(aseg(e, 64, 64, g->bond_edge, E), B, S1, 512, 64, 0, "bc_W1p_wg");
+    wpart(aseg(e, 64, 64, g->bond_edge, E), B, S2, 512, 128, 0, "bc_W1p_wg");
   }
   SegSrc s[2];
   s[0] = SegSrc(); s[0].in = q1; s[0].ptr = g->angle_ptr; s[0].rows = A;

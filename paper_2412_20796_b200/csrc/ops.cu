@@ -223,7 +223,7 @@ static int seg_split(int64_t mean, int64_t targets) {
 // ---------------------------------------------------------------------------
 // segmented sums (warp per target row, 2 columns per lane, fixed order)
 // ---------------------------------------------------------------------------
-struct SegArgs { SegSrc s[3]; int n; };
+struct SegArgs { SegSrc s[3]; int n; int sep; int outoff[3]; };   // sep: source k -> its own output (grid.z)
 
 // rows [r0, r1) of S (through S.perm) added in order into acc (lane hl = float4 column quad of a
 // 256-B row): row indices are fetched 16 at a time (coalesced) and broadcast by shuffle; U rows
@@ -272,6 +272,7 @@ __global__ void __launch_bounds__(256) k_segsum(int64_t targets, float *__restri
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       if (k >= a.n) break;
+      if (a.sep && k != (int)blockIdx.z) continue;
       const SegSrc &S = a.s[k];
       const int64_t sg = S.segmap ? (int64_t)__ldg(S.segmap + t) : t + S.ptr_off;
       if (sg < 0) continue;
@@ -296,7 +297,7 @@ __global__ void __launch_bounds__(256) k_segsum(int64_t targets, float *__restri
   } else if (t >= targets) {
     return;
   }
-  float4 *o = (float4 *)(out + t * ldo + 64 * blockIdx.y) + hl;
+  float4 *o = (float4 *)(out + t * ldo + 64 * blockIdx.y + (a.sep ? a.outoff[blockIdx.z] : 0)) + hl;
   if (accumulate) { const float4 p = *o; acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w; }
   *o = acc;
 }
@@ -658,12 +659,17 @@ void gate_bwd(chg_ctx *ctx, int64_t rows, const float *y, int ldy, GateLN ln, in
 }
 
 void segsum(chg_ctx *ctx, int64_t targets, float *out, int ldo, int accumulate, int nsrc, const SegSrc *src,
-            const char *tag, int ncols) {
+            const char *tag, int ncols, const int *outoff) {
   if (targets <= 0) return;
   if (ncols % 64 || ncols <= 0) CHG_THROW(CHG_ERR_STATE, "segsum: ncols %d not a multiple of 64", ncols);
   const int ng = ncols / 64;
   SegArgs a;
   a.n = nsrc;
+  a.sep = outoff != nullptr;
+  for (int k = 0; k < 3; ++k) a.outoff[k] = (outoff && k < nsrc) ? outoff[k] : 0;
+  if (a.sep)
+    for (int k = 0; k < nsrc; ++k)
+      if (outoff[k] & 3) CHG_THROW(CHG_ERR_STATE, "segsum: output offsets must be multiples of 4");
   double bytes = targets * 256.0 * ng * (1 + accumulate);
   for (int k = 0; k < nsrc; ++k) {
     a.s[k] = src[k];
@@ -679,7 +685,7 @@ void segsum(chg_ctx *ctx, int64_t targets, float *out, int ldo, int accumulate, 
   const int64_t mean = rows / std::max<int64_t>(targets, 1);
   const int H = seg_split(mean, targets);
   ProfScope ps(ctx, tag, 0.0, bytes);
-  const dim3 grid(ceil_div(targets * 16 * H, 256), ng);
+  const dim3 grid(ceil_div(targets * 16 * H, 256), ng, a.sep ? nsrc : 1);
   // 8 rows in flight per lane on long segments; 4 on short ones (fewer registers, more warps)
   auto go = [&](auto kern) { launch_k(ctx, kern, grid, 256, 0, ctx->stream, targets, out, ldo, accumulate, a); };
   const bool deep = mean >= 16;
@@ -697,6 +703,7 @@ void segsum_linear(chg_ctx *ctx, int64_t targets, int nsrc, const SegSrc *src, f
   if (targets <= 0) return;
   SegArgs a;
   a.n = nsrc;
+  a.sep = 0;
   double bytes = targets * (256.0 * (2 + (resid ? 1 : 0)));
   int64_t rows = 0;
   for (int k = 0; k < nsrc; ++k) {

@@ -22,9 +22,10 @@ struct SegSrc { const float *in = nullptr; const int32_t *ptr = nullptr; const i
                 int ld = 64;        // row stride of `in` (floats, multiple of 4)
                 int64_t rows = 0;   // total input rows summed (algorithmic-bytes bookkeeping only)
 };
-// ncols (multiple of 64): column groups of 64 summed by grid.y (input column 64·y of every source)
+// ncols (multiple of 64): column groups of 64 summed by grid.y (input column 64·y of every source).
+// outoff != nullptr: the sources are NOT added — source k is summed into out + outoff[k] (grid.z)
 void segsum(chg_ctx *ctx, int64_t targets, float *out, int ldo, int accumulate, int nsrc, const SegSrc *src,
-            const char *tag = "segsum", int ncols = 64);
+            const char *tag = "segsum", int ncols = 64, const int *outoff = nullptr);
 
 // segmented sum fused with the 64x64 linear that consumes it: agg = Σ rows (stored),
 // out = (agg·W + bias) + resid (bias / resid optional); W row-major [64][64]
