@@ -373,23 +373,6 @@ static void launch_wgrad_reduce(chg_ctx *ctx, const WGrad &g, const float *parti
   red_push(ctx, j);
 }
 
-bool rowgemm_gate(chg_ctx *ctx, const RowGemm &g) {
-  if (g.M <= 0) return true;
-  if (g.gate.on && g.tc && ctx->use_tc && ctx->cur_model && ctx->cur_wt) {
-    RowGemm h = g;
-    bool ok = true;
-    for (int c = 0; c < h.nchunk && ok; ++c)
-      for (int b = 0; b < h.ch[c].nwb && ok; ++b)
-        ok = kmajor_of(ctx->cur_model, ctx->cur_wt, h.ch[c].W[b], h.ch[c].ldw[b], &h.ch[c].Wk[b], &h.ch[c].ldwk[b]);
-    static const bool no_fuse = getenv("CHG_NO_GATE_FUSION") != nullptr;   // A/B knob
-    if (ok && !no_fuse && rowgemm_tc(ctx, h)) return true;
-  }
-  RowGemm h = g;
-  h.gate.on = 0;
-  rowgemm(ctx, h);
-  return false;
-}
-
 void wgrad(chg_ctx *ctx, const WGrad &g) {
   if (ctx->no_param_grads) return;
   int Kp = g.K + (g.bias ? 1 : 0);

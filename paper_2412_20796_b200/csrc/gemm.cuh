@@ -54,21 +54,7 @@ struct Chunk {
   int ldwk[8] = {};
 };
 
-// GatedMLP output stage fused into the epilogue: for the chunk pair (c = core, c + 1 =
-// gate) of 64 columns each, y = the pair's pre-LN outputs (still stored when write_y, for the
-// backward) and out = φ ⊙ w (mode 0), φ ⊙ w[i1] ⊙ w[i2] (mode 1) or resid + φ (mode 2) with
-// φ = σ(LN_g(y_g)) ⊙ SiLU(LN_c(y_c)) — the k_gate_fwd contract (ops.cuh GateMode)
-struct GateEpi {
-  int on = 0, c = 0, mode = 0, write_y = 1;
-  const float *gc = nullptr, *bc = nullptr, *gg = nullptr, *bg = nullptr;
-  const float *w = nullptr;
-  const int32_t *i1 = nullptr, *i2 = nullptr;
-  const float *resid = nullptr;
-  float *out = nullptr;                                // [M, 64]
-};
-
 struct RowGemm {
-  GateEpi gate;
   AOp A;
   int M = 0;
   int K = 0;                     // reduction length (per chunk)
@@ -102,9 +88,6 @@ void tc_repack_all(chg_ctx *ctx, chg_model *m);   // forward start (TF32 mode): 
 void tc_cache_free(chg_model *m);
 void rowgemm(chg_ctx *ctx, const RowGemm &g);      // tcgen05 when ctx->use_tc and eligible, else SIMT
 bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g);   // false if the shape does not fit the tensor-core path
-// rowgemm with a fused GatedMLP output stage (g.gate.on): true if the fused epilogue ran (tensor-core
-// path); false: the GEMM ran without it and the caller applies gate_fwd
-bool rowgemm_gate(chg_ctx *ctx, const RowGemm &g);
 void wgrad(chg_ctx *ctx, const WGrad &g);
 bool wgrad_tc(chg_ctx *ctx, const WGrad &g, float **partial, int *Kp, int *splits, bool *bias_done);
 

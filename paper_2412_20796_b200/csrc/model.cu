@@ -22,7 +22,7 @@ struct Fwd {
   chg_ctx *ctx;
   chg_model *m;
   chg_graph *g;
-  int train;                       // 0: the pre-LN activations y are not stored (no backward)
+  int train;                       // train-mode forward (activations kept for chg_backward)
   float *buf(const std::string &n, int64_t rows, int cols) {
     float *q = ctx->getf(n, (size_t)std::max<int64_t>(rows, 1) * cols);
     ctx->dbg[n] = {q, rows, cols, cols};
@@ -77,17 +77,6 @@ static void part_product(chg_ctx *ctx, const ASeg &x, int64_t rows, const float 
   rowgemm(ctx, G);
 }
 
-// the GatedMLP output stage fused into a GEMM epilogue (GateEpi, gemm.cuh): chunks (c, c + 1) =
-// (core, gate) pre-LN outputs
-static void set_gate(RowGemm &G, const Fwd &F, const std::string &pre, int mode, const float *w, const int32_t *i1,
-                     const int32_t *i2, const float *resid, float *out, int c = 0) {
-  GateEpi &E = G.gate;
-  E.on = 1; E.c = c; E.mode = mode; E.write_y = F.train;
-  E.gc = F.m->p(pre + ".ln_core.g"); E.bc = F.m->p(pre + ".ln_core.b");
-  E.gg = F.m->p(pre + ".ln_gate.g"); E.bg = F.m->p(pre + ".ln_gate.b");
-  E.w = w; E.i1 = i1; E.i2 = i2; E.resid = resid; E.out = out;
-}
-
 // --- Atom Conv (Eq. 4) ------------------------------------------------------
 void atom_conv_fwd(Fwd &F, int t, const float *v, const float *e, const float *ea, float *v_out) {
   chg_ctx *ctx = F.ctx;
@@ -130,10 +119,10 @@ void atom_conv_fwd(Fwd &F, int t, const float *v, const float *e, const float *e
     G.ch[1] = chunk1(m->p(pre + ".gate.W2"), 64, 64, m->p(pre + ".gate.b2"), y + 64, 128);
     G.ch[1].a_k0 = 64;
     G.tag = "ac_f2";
-    // m_e = eᵃ_e ⊙ σ(LN_g(y_g)) ⊙ SiLU(LN_c(y_c)): fused into the epilogue on the tensor-core path
-    set_gate(G, F, pre, GATE_MUL_W, ea, nullptr, nullptr, nullptr, msg);
-    if (!rowgemm_gate(ctx, G)) gate_fwd(ctx, E, y, 128, F.ln(pre), GATE_MUL_W, ea, nullptr, nullptr, nullptr, msg);
+    rowgemm(ctx, G);
   }
+  // m_e = eᵃ_e ⊙ σ(LN_g(y_g)) ⊙ SiLU(LN_c(y_c))
+  gate_fwd(ctx, E, y, 128, F.ln(pre), GATE_MUL_W, ea, nullptr, nullptr, nullptr, msg);
   // agg_i = Σ_{e at centre i} m_e and v' = v + agg · W_out + b_out in one pass
   SegSrc s;
   s.in = msg; s.ptr = g->row_ptr; s.rows = E;
@@ -165,7 +154,6 @@ void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float
   float *ya = angle_branch ? F.buf("bc_ya_" + ts, A, 128) : nullptr;
   float *aggb = F.buf("bc_aggb_" + ts, B, 64);
   float *q = ctx->getf("msg_angle", std::max<int64_t>(A, 1) * 64);
-  bool angle_done = false;
   if (A > 0) {
     const float *W[4], *bias[4];
     const int nw = bc_first_weights(m, t, angle_branch, W, bias);
@@ -192,9 +180,7 @@ void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float
       C.ngadd = 3;
     }
     G.tag = "bc_f1";
-    // a' = a + φ_a (angle update, Eq. 6) fused into the angle pair's epilogue on the tensor-core path
-    if (angle_branch) set_gate(G, F, ap, GATE_RESID, nullptr, nullptr, nullptr, a, a_out, 2);
-    angle_done = rowgemm_gate(ctx, G) && angle_branch;
+    rowgemm(ctx, G);
     RowGemm H;
     H.A.seg[0] = aseg(z1, 128, 128);
     H.A.nseg = 1; H.A.act = 1;
@@ -203,20 +189,17 @@ void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float
     H.ch[1] = chunk1(m->p(bp + ".gate.W2"), 64, 64, m->p(bp + ".gate.b2"), yb + 64, 128);
     H.ch[1].a_k0 = 64;
     H.tag = "bc_f2";
-    // q = eᵇ_ij ⊙ eᵇ_ik ⊙ φ_e (fused into the epilogue on the tensor-core path)
-    set_gate(H, F, bp, GATE_MUL_W1W2, eb, g->angle_b1, g->angle_b2, nullptr, q);
-    if (!rowgemm_gate(ctx, H))
-      gate_fwd(ctx, A, yb, 128, F.ln(bp), GATE_MUL_W1W2, eb, g->angle_b1, g->angle_b2, nullptr, q);
+    rowgemm(ctx, H);
+    // q = eᵇ_ij ⊙ eᵇ_ik ⊙ φ_e
+    gate_fwd(ctx, A, yb, 128, F.ln(bp), GATE_MUL_W1W2, eb, g->angle_b1, g->angle_b2, nullptr, q);
   }
-  {  // aggb = Σ over angles with first bond b (empty -> 0) fused with its product by W_out (B
-     // bond rows only); then e' = e + 𝓛_e(agg) on all E edges (Q16): bond row (or nothing) + bias
-    float *tmp = ctx->getf("bc_out_tmp", (size_t)std::max<int64_t>(B, 1) * 64);
+  {  // e' = e + 𝓛_e(agg) on all E edges (Q16): agg = Σ over the angles whose first bond is the
+     // edge's bond (empty for non-bond edges -> bias only); aggb (per bond) kept for the backward
     SegSrc s;
-    s.in = q; s.ptr = g->angle_ptr; s.rows = A;
-    segsum_linear(ctx, B, 1, &s, aggb, m->p(bp + ".out.W"), nullptr, nullptr, tmp, "segsum_bc");
-    edge_update(ctx, E, e, m->p(bp + ".out.b"), g->bond_id, tmp, e_out);
+    s.in = q; s.ptr = g->angle_ptr; s.segmap = g->bond_id; s.rows = A;
+    segsum_linear(ctx, E, 1, &s, aggb, m->p(bp + ".out.W"), m->p(bp + ".out.b"), e, e_out, "segsum_bc", 1);
   }
-  if (angle_branch && A > 0 && !angle_done)   // a' = a + φ_a
+  if (angle_branch && A > 0)   // a' = a + φ_a
     gate_fwd(ctx, A, ya, 128, F.ln(ap), GATE_RESID, nullptr, nullptr, nullptr, a, a_out);
 }
 

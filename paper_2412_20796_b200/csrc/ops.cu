@@ -308,7 +308,8 @@ __global__ void __launch_bounds__(256) k_segsum(int64_t targets, float *__restri
 template <int H, int U>
 __global__ void __launch_bounds__(256) k_segsum_linear(int64_t targets, SegArgs a, float *__restrict__ agg,
                                                        const float *__restrict__ W, const float *__restrict__ bias,
-                                                       const float *__restrict__ resid, float *__restrict__ out) {
+                                                       const float *__restrict__ resid, float *__restrict__ out,
+                                                       int agg_by_seg) {
   pdl_begin();
   __shared__ __align__(16) float sW[64][64];
   __shared__ float4 part[16][16];
@@ -349,7 +350,12 @@ __global__ void __launch_bounds__(256) k_segsum_linear(int64_t targets, SegArgs 
   } else if (t >= targets) {
     return;
   }
-  ((float4 *)(agg + t * 64))[hl] = acc;
+  if (agg_by_seg) {                                 // agg row = the segment (e.g. the bond of edge t)
+    const int32_t sg = __ldg(a.s[0].segmap + t);
+    if (sg >= 0) ((float4 *)(agg + (int64_t)sg * 64))[hl] = acc;
+  } else {
+    ((float4 *)(agg + t * 64))[hl] = acc;
+  }
   float o[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int k = 0; k < 64; ++k) {
@@ -699,7 +705,8 @@ void segsum(chg_ctx *ctx, int64_t targets, float *out, int ldo, int accumulate, 
 }
 
 void segsum_linear(chg_ctx *ctx, int64_t targets, int nsrc, const SegSrc *src, float *agg, const float *W,
-                   const float *bias, const float *resid, float *out, const char *tag) {
+                   const float *bias, const float *resid, float *out, const char *tag, int agg_by_seg) {
+  if (agg_by_seg && (nsrc != 1 || !src[0].segmap)) CHG_THROW(CHG_ERR_STATE, "segsum_linear: agg_by_seg needs one mapped source");
   if (targets <= 0) return;
   SegArgs a;
   a.n = nsrc;
@@ -716,7 +723,7 @@ void segsum_linear(chg_ctx *ctx, int64_t targets, int nsrc, const SegSrc *src, f
   const int H = seg_split(mean, targets);
   ProfScope ps(ctx, tag, 2.0 * targets * 64 * 64, bytes);
   const int grid = ceil_div(targets * 16 * H, 256);
-  auto go = [&](auto kern) { launch_k(ctx, kern, grid, 256, 0, ctx->stream, targets, a, agg, W, bias, resid, out); };
+  auto go = [&](auto kern) { launch_k(ctx, kern, grid, 256, 0, ctx->stream, targets, a, agg, W, bias, resid, out, agg_by_seg); };
   const bool deep = mean >= 16;
   switch (H) {
     case 8: deep ? go(k_segsum_linear<8, 8>) : go(k_segsum_linear<8, 4>); break;

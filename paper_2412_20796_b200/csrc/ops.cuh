@@ -29,8 +29,9 @@ void segsum(chg_ctx *ctx, int64_t targets, float *out, int ldo, int accumulate, 
 
 // segmented sum fused with the 64x64 linear that consumes it: agg = Σ rows (stored),
 // out = (agg·W + bias) + resid (bias / resid optional); W row-major [64][64]
+// agg_by_seg = 1: one source with a segmap; agg is stored at row segmap[t] (skipped when < 0)
 void segsum_linear(chg_ctx *ctx, int64_t targets, int nsrc, const SegSrc *src, float *agg, const float *W,
-                   const float *bias, const float *resid, float *out, const char *tag);
+                   const float *bias, const float *resid, float *out, const char *tag, int agg_by_seg = 0);
 
 // embedding gradient: dW[z - 1] += Σ_{i: Z_i = z} dv[i] (species 1..n_species); per-block
 // species bins reduced by the batched reduction (reduce.cu); deterministic

@@ -314,107 +314,6 @@ __device__ __noinline__ void epi_rows_any(const Chunk &C, int act, const float *
   }
 }
 
-// staging box -> one TMA store of a 32 x 32 block of chunk c (lane = row; see the tstore epilogue)
-__device__ __forceinline__ void stage_store(const TcMaps &TM, float *stg, int &sc, int lane, int sw, int c, int j0,
-                                            int row0, int M, const float *v, bool round) {
-  float *st = stg + (sc % TM.nst) * 1024;
-  if (lane == 0) {
-    if (TM.nst > 1) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-    else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-  }
-  __syncwarp();
-  float4 *srow = reinterpret_cast<float4 *>(st) + lane * 8;
-#pragma unroll
-  for (int q4 = 0; q4 < 8; ++q4)
-    srow[q4 ^ sw] = round ? make_float4(tf32_round(v[4 * q4]), tf32_round(v[4 * q4 + 1]), tf32_round(v[4 * q4 + 2]),
-                                        tf32_round(v[4 * q4 + 3]))
-                          : make_float4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  __syncwarp();
-  if (lane == 0 && row0 < M) {
-#pragma unroll
-    for (int cc = 0; cc < 4; ++cc)
-      if (cc == c) tma_store_2d(&TM.o[cc], smem_u32(st), j0, row0);
-  }
-  ++sc;
-}
-
-// Fused GatedMLP output stage (GateEpi): this warp holds columns j0..j0+31 of its 32 rows for the
-// core chunk (v, prepared) and loads the same columns of the gate chunk; the LayerNorm statistics
-// over each branch's 64 columns combine the two warps of the TMEM lane quarter (the other holds
-// the other 32 columns) through shared memory and a named barrier; two passes (mean, then the
-// centred second moment) as in k_gate_fwd.
-__device__ __noinline__ void gate_pair(const RowGemm &g, const TcPlan &P, const Chunk &C, float *v, uint32_t tacc,
-                                       int j0, int m, int lq, int half, int lane, int sw, int row0, float *stg, int &sc,
-                                       const TcMaps &TM) {
-  __shared__ float gx[4][2][32][2];
-  const GateEpi &GE = g.gate;
-  const int cg = GE.c + 1;
-  const Chunk &Cg = g.ch[cg];
-  uint32_t r[32];
-  tmem_ld32(tacc + P.coff[cg] + j0, r);
-  float *u = reinterpret_cast<float *>(r);
-  if (Cg.bias) {
-#pragma unroll
-    for (int q = 0; q < 32; ++q) u[q] += __ldg(Cg.bias + j0 + q);
-  }
-  if (m < g.M) {
-    for (int k = 0; k < Cg.ngadd; ++k) {                 // gathered row additions (factorised layer 1)
-      const int rr = Cg.gidx[k] ? __ldg(Cg.gidx[k] + m) : m;
-      const float4 *src = reinterpret_cast<const float4 *>(Cg.gadd[k] + (size_t)rr * Cg.ldga[k] + j0);
-#pragma unroll
-      for (int q4 = 0; q4 < 8; ++q4) {
-        const float4 t = __ldg(src + q4);
-        u[4 * q4] += t.x; u[4 * q4 + 1] += t.y; u[4 * q4 + 2] += t.z; u[4 * q4 + 3] += t.w;
-      }
-    }
-  }
-  if (GE.write_y) {                                      // pre-LN y of both branches (backward)
-    stage_store(TM, stg, sc, lane, sw, GE.c, j0, row0, g.M, v, C.round_out != 0);
-    stage_store(TM, stg, sc, lane, sw, cg, j0, row0, g.M, u, Cg.round_out != 0);
-  }
-  const uint32_t bar = 1 + lq, nthr = 64;
-  float sc_ = 0.f, sg_ = 0.f;
-#pragma unroll
-  for (int q = 0; q < 32; ++q) { sc_ += v[q]; sg_ += u[q]; }
-  gx[lq][half][lane][0] = sc_; gx[lq][half][lane][1] = sg_;
-  asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nthr) : "memory");
-  const float muc = (gx[lq][0][lane][0] + gx[lq][1][lane][0]) * (1.0f / 64.0f);
-  const float mug = (gx[lq][0][lane][1] + gx[lq][1][lane][1]) * (1.0f / 64.0f);
-  asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nthr) : "memory");
-  float vc = 0.f, vg = 0.f;
-#pragma unroll
-  for (int q = 0; q < 32; ++q) { vc += (v[q] - muc) * (v[q] - muc); vg += (u[q] - mug) * (u[q] - mug); }
-  gx[lq][half][lane][0] = vc; gx[lq][half][lane][1] = vg;
-  asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nthr) : "memory");
-  const float rc = rsqrtf((gx[lq][0][lane][0] + gx[lq][1][lane][0]) * (1.0f / 64.0f) + 1e-5f);
-  const float rg = rsqrtf((gx[lq][0][lane][1] + gx[lq][1][lane][1]) * (1.0f / 64.0f) + 1e-5f);
-  asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nthr) : "memory");
-  if (m >= g.M) return;
-  const float *w1 = nullptr, *w2 = nullptr;
-  if (GE.mode == 0) w1 = GE.w + (size_t)m * 64;
-  else if (GE.mode == 1) { w1 = GE.w + (size_t)__ldg(GE.i1 + m) * 64; w2 = GE.w + (size_t)__ldg(GE.i2 + m) * 64; }
-  else w1 = GE.resid + (size_t)m * 64;
-  float4 *dst = reinterpret_cast<float4 *>(GE.out + (size_t)m * 64 + j0);
-#pragma unroll
-  for (int q4 = 0; q4 < 8; ++q4) {
-    const float4 a1 = __ldg(reinterpret_cast<const float4 *>(w1 + j0) + q4);
-    const float4 a2 = GE.mode == 1 ? __ldg(reinterpret_cast<const float4 *>(w2 + j0) + q4) : make_float4(1.f, 1.f, 1.f, 1.f);
-    float o[4];
-    const float aa1[4] = {a1.x, a1.y, a1.z, a1.w}, aa2[4] = {a2.x, a2.y, a2.z, a2.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int q = 4 * q4 + e, n = j0 + q;
-      // LN affine vectors at canonical flat offsets (8-B aligned): scalar loads (L1-resident)
-      const float nc = __ldg(GE.gc + n) * (v[q] - muc) * rc + __ldg(GE.bc + n);
-      const float ng = __ldg(GE.gg + n) * (u[q] - mug) * rg + __ldg(GE.bg + n);
-      const float phi = sigmoidf_(ng) * siluf_(nc);
-      o[e] = GE.mode == 2 ? aa1[e] + phi : GE.mode == 1 ? phi * aa1[e] * aa2[e] : phi * aa1[e];
-    }
-    dst[q4] = make_float4(o[0], o[1], o[2], o[3]);
-  }
-}
-
 __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_constant__ RowGemm g, const TcPlan P,
                                                                const uint32_t *__restrict__ bimg, int ntiles,
                                                                int skip, const __grid_constant__ TcMaps TM) {
@@ -721,7 +620,6 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
         ep_mark();
         for (int i = 0; i < nmy; ++i) {
           const int c = mc[i], j0 = mj[i];
-          if (g.gate.on && c == g.gate.c + 1) continue;  // processed with its core partner below
           const Chunk &C = g.ch[c];
           uint32_t r[32];
           tmem_ld32(tmem + lane_base + a * tcols + P.coff[c] + j0, r);
@@ -731,11 +629,6 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
             for (int q = 0; q < 32; ++q) v[q] += __ldg(C.bias + j0 + q);
           }
           const int m = row0 + lane;
-          if (g.gate.on && c == g.gate.c) {
-            gate_pair(g, P, C, v, tmem + lane_base + a * tcols, j0, m, lq, half, lane, sw, row0, stg, sc, TM);
-            ep_mark();
-            continue;
-          }
           if (C.ngadd && m < g.M) {                     // gathered row additions (factorised layer 1)
 #pragma unroll 1
             for (int k = 0; k < C.ngadd; ++k) {
@@ -1282,11 +1175,6 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
           ++n;
         }
         h.nchunk = n;
-        // the fused gate stage goes with the group holding its (core, gate) pair
-        h.gate.on = g.gate.on && g.gate.c >= c0 && g.gate.c + 1 < c0 + n;
-        h.gate.c = g.gate.c - c0;
-        if (g.gate.on && !h.gate.on && g.gate.c >= c0 && g.gate.c < c0 + n)
-          CHG_THROW(CHG_ERR_STATE, "rowgemm_tc %s: gate pair split across column groups", g.tag);
         if (!rowgemm_tc(ctx, h)) CHG_THROW(CHG_ERR_STATE, "rowgemm_tc %s: 3xTF32 column group does not fit", g.tag);
         c0 += n;
       }
@@ -1317,15 +1205,6 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   for (int c = 0; c < g.nchunk; ++c)                  // gathered additions: 16-B rows, no TMA-operand chunk
     for (int k = 0; k < g.ch[c].ngadd; ++k)
       if (((uintptr_t)g.ch[c].gadd[k] & 15) || (g.ch[c].ldga[k] & 3) || g.ch[c].mul || g.ch[c].resid) return false;
-  if (g.gate.on) {                                     // fused gate stage: a (core, gate) pair of plain 64-col chunks
-    const int c = g.gate.c;
-    if (c < 0 || c + 1 >= g.nchunk || g.ch[c].ncols != 64 || g.ch[c + 1].ncols != 64) return false;
-    for (int k = c; k <= c + 1; ++k)
-      if (g.ch[k].mul || g.ch[k].resid || g.ch[k].pre || g.ch[k].sout) return false;
-    if (((uintptr_t)g.gate.out & 15) || (g.gate.mode != 2 && ((uintptr_t)g.gate.w & 15)) ||
-        (g.gate.mode == 2 && ((uintptr_t)g.gate.resid & 15)))
-      return false;
-  }
   P.lo = lo;
   P.width = hi - lo;
   P.ntot = off;
@@ -1381,7 +1260,6 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   bool has_sout = false, has_round = false;
   for (int c = 0; c < g.nchunk; ++c) { has_sout |= g.ch[c].sout != nullptr; has_round |= g.ch[c].round_out != 0; }
   if ((has_sout || has_round) && !TM.tstore) return false;          // only the TMA-store epilogue writes sout / rounded out
-  if (g.gate.on && !TM.tstore) return false;                         // the fused gate stage lives in that epilogue
   const size_t epi_b = TM.tstore ? 0 : (size_t)NEPI * 32 * 33 * 4;
   auto fixed_of = [&](int nsa) {
     return 1024 + nsa * achunk + 8 * (3 * nsa + 2 * NSB + 4) + 16 + epi_b;

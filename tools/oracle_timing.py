@@ -30,7 +30,7 @@ def step(b, p, cfg, st):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--c3-structures", type=int, default=128)
+    ap.add_argument("--c3-structures", type=int, default=64)
     a = ap.parse_args()
     cfg = ModelConfig()
     p0 = init_flat_params(param_layout(cfg), seed=0).astype(np.float32).astype(np.float64)
@@ -43,6 +43,7 @@ def main():
         p = step(b, p, cfg, st)
         dt = time.time() - t0
         out[name] = {"structures": b.n_struct, "atoms": b.n_atoms, "s_per_step": dt, "structures_per_s": b.n_struct / dt}
+        print(json.dumps({name: out[name]}), file=sys.stderr, flush=True)
     b5 = make_config_batch("C5")
     t0 = time.time()
     g5 = build_graph_batch(b5)
