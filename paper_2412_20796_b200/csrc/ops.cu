@@ -357,12 +357,16 @@ __global__ void __launch_bounds__(256) k_segsum_linear(int64_t targets, SegArgs 
     ((float4 *)(agg + t * 64))[hl] = acc;
   }
   float o[4] = {0.f, 0.f, 0.f, 0.f};
+  // a target without a segment (a non-bond edge, Q16) has agg = 0: agg·W = 0 exactly, skipped
+  const bool empty = agg_by_seg && __ldg(a.s[0].segmap + t) < 0;
+  if (!empty) {
 #pragma unroll
   for (int k = 0; k < 64; ++k) {
     const float c = (k & 3) == 0 ? acc.x : (k & 3) == 1 ? acc.y : (k & 3) == 2 ? acc.z : acc.w;
     const float ak = __shfl_sync(hmask, c, k >> 2, 16);
     const float4 w = *(const float4 *)&sW[k][4 * hl];
     o[0] = fmaf(ak, w.x, o[0]); o[1] = fmaf(ak, w.y, o[1]); o[2] = fmaf(ak, w.z, o[2]); o[3] = fmaf(ak, w.w, o[3]);
+  }
   }
   if (bias) {
 #pragma unroll

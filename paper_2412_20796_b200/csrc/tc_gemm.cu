@@ -1062,6 +1062,242 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols) : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// tcgen05 weight-gradient GEMM with MN-major operands (k_wgrad_mn):
+//   G[k, n] = Σ_m A(m, k) · D(m, n) as the UMMA D_mma[M = k][N = n] = Σ_{K = m} A_mma · B_mma
+//   where A_mma (k × m) and B_mma (n × m) are read MN-MAJOR: the smem tile of 32 rows m ×
+//   32 features holds each row's features contiguously — exactly the row-major layout of the
+//   activations — so TMA loads the rows as they are (SWIZZLE_128B boxes of RS rows × 32 fp32)
+//   and gathered rows arrive by 16-B cp.async into the same swizzled slots; no transpose.
+//   MN-major TF32 operands need the 128B_BASE32B smem layout (descriptor layout type 1; TMA
+//   CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B): 32 features per 128-B row, the 32-B chunk c of row r
+//   stored at chunk c ^ (r & 3) (a 512-B swizzle atom of 4 rows); canonical form (16-B units)
+//   ((8, n), (4, k)) : ((1, LBO), (8, SBO)) — the next 32 features at LBO = one box (RS·128 B),
+//   the next 4 rows at SBO = 512 B; an MMA K step (8 rows) advances 1 KB.
+//   Warps 0-3 load (TMA by thread 0, gathers by all 128), warps 4-11 convert in place (lane =
+//   column: SiLU for act, TF32 rounding or the 3xTF32 split hi | lo, and the column sums of D
+//   = the bias gradient, one D box per warp for the whole kernel), warp 12 issues the MMAs,
+//   warps 0-3 drain TMEM into the CTA's partial (TMA bulk stores; reduce.cu sums the partials).
+// ---------------------------------------------------------------------------
+constexpr int MN_RS = 32;                  // rows m per stage
+constexpr int MN_NLW = 4, MN_NCW = 8;      // loader / converter warps
+constexpr int MN_THREADS = (MN_NLW + MN_NCW + 1) * 32;
+constexpr int MN_NST = 3;
+
+struct WmPlan {
+  int Kpad, ktiles, nA, nD, Kp, rows_per_cta, split, nst;
+  uint32_t tmem_cols;
+  int abox_seg[8], abox_col[8];            // A box b: segment, first column within the segment
+  int tma_bytes;                           // TMA bytes per stage (direct A boxes + D boxes)
+  int any_gather;
+};
+struct WmMaps { CUtensorMap a[4]; CUtensorMap d; };
+
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__global__ void __launch_bounds__(MN_THREADS, 1) k_wgrad_mn(const __grid_constant__ WGrad g, const WmPlan P,
+                                                            float *__restrict__ partial,
+                                                            const __grid_constant__ WmMaps TM,
+                                                            const __grid_constant__ CUtensorMap pmap) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr uint32_t BOX = MN_RS * 128;                       // one box: RS rows x 32 fp32
+  const int nbox = P.nA + P.nD;
+  const uint32_t half_bytes = nbox * BOX;                     // hi part of a stage
+  const uint32_t st_bytes = half_bytes << P.split;            // [A hi | D hi] (| [A lo | D lo])
+  const int NST = P.nst;
+  uint64_t *loaded = (uint64_t *)(smem + NST * st_bytes);
+  uint64_t *full = loaded + MN_NST;
+  uint64_t *empty = full + MN_NST;
+  uint64_t *done = empty + MN_NST;
+  uint32_t *tslot = (uint32_t *)(done + 1);
+
+  const int r0 = blockIdx.x * P.rows_per_cta;
+  const int r1 = min(g.M, r0 + P.rows_per_cta);
+  const int nchunks = r1 > r0 ? (r1 - r0 + MN_RS - 1) / MN_RS : 0;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                 "r"(P.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&loaded[i], MN_NLW * 32);
+      mbar_init(&full[i], MN_NCW);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // padding feature boxes (k >= K, never loaded) are zero in every stage, hi and lo
+  for (int s = 0; s < NST; ++s)
+    for (int b = g.K / 32; b < P.nA; ++b)
+      for (int h = 0; h <= P.split; ++h)
+        for (int i = tid; i < (int)(BOX / 16); i += blockDim.x)
+          reinterpret_cast<uint4 *>(smem + s * st_bytes + h * half_bytes + b * BOX)[i] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  pdl_begin();
+  const uint32_t tmem = *tslot;
+  const int nAk = g.K / 32;                                   // loaded A boxes
+
+  if (warp < MN_NLW) {
+    // ---------------- loaders ----------------
+    const int q = tid & 7, rb = tid >> 3;                     // 16-B unit, row (rows rb, rb + 16)
+    for (int c = 0; c < nchunks; ++c) {
+      const int s = c % NST, u = c / NST;
+      if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+      const int m0 = r0 + c * MN_RS;
+      uint8_t *st = smem + s * st_bytes;
+      if (tid == 0) {
+        if (P.tma_bytes) mbar_expect_tx_only(&loaded[s], P.tma_bytes);
+        for (int b = 0; b < nAk; ++b) {
+          const int sg = P.abox_seg[b];
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (k == sg && !g.A.seg[k].idx) tma_load_2d(smem_u32(st + b * BOX), &TM.a[k], P.abox_col[b], m0, &loaded[s]);
+        }
+        for (int b = 0; b < P.nD; ++b) tma_load_2d(smem_u32(st + (P.nA + b) * BOX), &TM.d, 32 * b, m0, &loaded[s]);
+      }
+      if (P.any_gather) {
+        for (int b = 0; b < nAk; ++b) {
+          const ASeg &S = g.A.seg[P.abox_seg[b]];
+          if (!S.idx) continue;
+          const uint32_t dst0 = smem_u32(st + b * BOX);
+#pragma unroll
+          for (int i = 0; i < MN_RS / 16; ++i) {
+            const int row = rb + 16 * i, m = m0 + row;
+            const int r = (m < r1) ? __ldg(S.idx + m) : -1;
+            const uint32_t dst = dst0 + row * 128 + ((((q >> 1) ^ (row & 3)) << 1 | (q & 1)) << 4);
+            if (r >= 0) cp_async16(dst, S.base + (size_t)r * S.ld + P.abox_col[b] + 4 * q, 16);
+            else cp_async16(dst, S.base, 0);
+          }
+        }
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&loaded[s])) : "memory");
+    }
+  } else if (warp < MN_NLW + MN_NCW) {
+    // ---------------- converters: lane = column of a box, rows in order ----------------
+    const int cw = warp - MN_NLW;
+    const int sw_lane = lane >> 2, e = lane & 3;              // 16-B unit and element of column `lane`
+    const int ch = sw_lane >> 1, hu = sw_lane & 1;            // its 32-B chunk and half
+    float bsum[2] = {0.f, 0.f};                               // column sums of my D boxes (bias)
+    for (int c = 0; c < nchunks; ++c) {
+      const int s = c % NST, u = c / NST;
+      mbar_wait(&loaded[s], u & 1);
+      uint8_t *st = smem + s * st_bytes;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int b = cw + MN_NCW * t;
+        if (b >= nbox || (b < P.nA && b >= nAk)) continue;    // no box / padding features
+        const bool isA = b < P.nA;
+        const bool act = isA && g.A.act == 1;
+        uint8_t *box = st + b * BOX;
+        float acc = 0.f;
+#pragma unroll 8
+        for (int r = 0; r < MN_RS; ++r) {
+          const uint32_t off = r * 128 + (((ch ^ (r & 3)) << 1 | hu) << 4) + e * 4;
+          float x = *reinterpret_cast<const float *>(box + off);
+          if (act) x = silu_fast(x);
+          if (!isA) acc += x;
+          const uint32_t h = to_tf32(x);
+          *reinterpret_cast<uint32_t *>(box + off) = h;
+          if (P.split) *reinterpret_cast<uint32_t *>(box + half_bytes + off) = to_tf32(x - __uint_as_float(h));
+        }
+        if (!isA) bsum[t] += acc;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[s]);
+    }
+    if (g.bias) {                                            // bias row K of this CTA's partial
+      float *Pout = partial + (size_t)blockIdx.x * P.Kp * g.N + (size_t)g.K * g.N;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int b = cw + MN_NCW * t;
+        if (b >= P.nA && b < nbox) Pout[32 * (b - P.nA) + lane] = bsum[t];
+      }
+    }
+  } else if (lane == 0) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) |
+                           ((uint32_t)(g.N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    for (int c = 0; c < nchunks; ++c) {
+      const int s = c % NST, u = c / NST;
+      mbar_wait(&full[s], u & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t base = smem_u32(smem + s * st_bytes);
+      for (int tt = 0; tt < P.ktiles; ++tt) {
+#pragma unroll
+        for (int j = 0; j < MN_RS / 8; ++j) {
+          const uint32_t a0 = base + tt * 4 * BOX + j * 1024, d0 = base + P.nA * BOX + j * 1024;
+          const uint64_t ad = make_desc(a0, BOX, 512) | ((uint64_t)1 << 61);     // SWIZZLE_128B_BASE32B
+          const uint64_t bd = make_desc(d0, BOX, 512) | ((uint64_t)1 << 61);
+          const uint32_t acc = (c > 0 || j > 0) ? 1u : 0u;
+          if (P.split) {
+            const uint64_t ad_lo = make_desc(a0 + half_bytes, BOX, 512) | ((uint64_t)1 << 61);
+            const uint64_t bd_lo = make_desc(d0 + half_bytes, BOX, 512) | ((uint64_t)1 << 61);
+            mma_tf32(tmem + tt * g.N, ad_lo, bd, idesc, acc);
+            mma_tf32(tmem + tt * g.N, ad, bd_lo, idesc, 1u);
+            mma_tf32(tmem + tt * g.N, ad, bd, idesc, 1u);
+          } else {
+            mma_tf32(tmem + tt * g.N, ad, bd, idesc, acc);
+          }
+        }
+      }
+      mma_commit(&empty[s]);
+    }
+    mma_commit(done);
+  }
+
+  // ---------------- epilogue: TMEM -> partial rows (thread = gradient row k) ----------------
+  if (warp < 4) {
+    if (nchunks > 0) mbar_wait(done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    float *stg = (float *)(smem + warp * 4096);
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const int sw = lane & 7;
+    for (int tt = 0; tt < P.ktiles; ++tt) {
+      const int k0 = tt * 128 + warp * 32;
+      for (int j0 = 0; j0 < g.N; j0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + lane_base + tt * g.N + j0, r);
+        if (k0 >= g.K) continue;
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+        float4 *srow = reinterpret_cast<float4 *>(stg) + lane * 8;
+#pragma unroll
+        for (int q4 = 0; q4 < 8; ++q4)
+          srow[q4 ^ sw] = nchunks > 0 ? make_float4(__uint_as_float(r[4 * q4]), __uint_as_float(r[4 * q4 + 1]),
+                                                    __uint_as_float(r[4 * q4 + 2]), __uint_as_float(r[4 * q4 + 3]))
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                           reinterpret_cast<uint64_t>(&pmap)),
+                       "r"(j0), "r"(k0), "r"((int)blockIdx.x), "r"(smem_u32(stg))
+                       : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols) : "memory");
+}
+
 struct TcCache {
   std::map<std::string, int> index;
   std::vector<PackJob> jobs;
@@ -1381,10 +1617,96 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   return true;
 }
 
+
+// MN-major weight gradient (k_wgrad_mn): false when an operand cannot be TMA / cp.async staged
+static bool wgrad_mn(chg_ctx *ctx, const WGrad &g, float **partial_out, int *Kp_out, int *splits_out) {
+  static const bool off = getenv("CHG_WG_TRANSPOSE") != nullptr;   // A/B knob: the transposing producers
+  EncodeTiledFn fn = encode_fn();
+  if (off || !fn || g.didx || (g.ldd % 4) || ((uintptr_t)g.D & 15) || g.K > 256 || g.N > 256 || g.K % 32 || g.N % 32)
+    return false;
+  WmPlan P{};
+  P.Kpad = (g.K + 127) / 128 * 128;
+  P.ktiles = P.Kpad / 128;
+  P.nA = P.Kpad / 32;
+  P.nD = g.N / 32;
+  P.Kp = g.K + (g.bias ? 1 : 0);
+  P.split = ctx->tc_split ? 1 : 0;
+  const int cols = P.ktiles * g.N;
+  if (cols > 512) return false;
+  P.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
+  WmMaps TM;
+  memset(&TM, 0, sizeof(TM));
+  int direct_boxes = 0;
+  {
+    int sg = 0, start = 0;
+    for (int b = 0; b < g.K / 32; ++b) {
+      while (sg < g.A.nseg && 32 * b >= start + g.A.seg[sg].width) start += g.A.seg[sg++].width;
+      if (sg >= g.A.nseg) return false;
+      P.abox_seg[b] = sg;
+      P.abox_col[b] = 32 * b - start;
+      if (g.A.seg[sg].idx) P.any_gather = 1;
+      else ++direct_boxes;
+    }
+    for (int s = 0; s < g.A.nseg; ++s) {
+      const ASeg &S = g.A.seg[s];
+      if (S.width % 32 || S.ld % 4 || ((uintptr_t)S.base & 15)) return false;
+      if (S.idx) continue;
+      cuuint64_t dim[2] = {(cuuint64_t)S.width, (cuuint64_t)g.M};
+      cuuint64_t stride[1] = {(cuuint64_t)S.ld * 4};
+      cuuint32_t box[2] = {32, MN_RS}, es[2] = {1, 1};
+      if (fn(&TM.a[s], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)S.base, dim, stride, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    }
+    cuuint64_t dim[2] = {(cuuint64_t)g.N, (cuuint64_t)g.M};
+    cuuint64_t stride[1] = {(cuuint64_t)g.ldd * 4};
+    cuuint32_t box[2] = {32, MN_RS}, es[2] = {1, 1};
+    if (fn(&TM.d, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)g.D, dim, stride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  P.tma_bytes = (direct_boxes + P.nD) * MN_RS * 128;
+  const size_t st_bytes = ((size_t)(P.nA + P.nD) * MN_RS * 128) << P.split;
+  const size_t fixed = 1024 + 8 * (3 * MN_NST + 1) + 16;
+  P.nst = (int)std::min<size_t>(MN_NST, (224 * 1024 - fixed) / st_bytes);
+  if (P.nst < 2) return false;
+  const size_t smem = fixed + P.nst * st_bytes;
+  const int sms = device_sm_count();
+  const int chunks = (g.M + MN_RS - 1) / MN_RS;
+  const int grid = std::max(1, std::min(sms, chunks));
+  P.rows_per_cta = (chunks + grid - 1) / grid * MN_RS;
+  const int splits = (g.M + P.rows_per_cta - 1) / P.rows_per_cta;
+  float *partial = red_partial(ctx, (size_t)splits * P.Kp * g.N);
+  if ((uintptr_t)partial & 15) return false;
+  CUtensorMap pmap;
+  {
+    cuuint64_t dim[3] = {(cuuint64_t)g.N, (cuuint64_t)g.K, (cuuint64_t)splits};
+    cuuint64_t stride[2] = {(cuuint64_t)g.N * 4, (cuuint64_t)P.Kp * g.N * 4};
+    cuuint32_t box[3] = {32, 32, 1}, es[3] = {1, 1, 1};
+    if (fn(&pmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, partial, dim, stride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  smem_optin((const void *)k_wgrad_mn, 224 * 1024);
+  ProfScope ps(ctx, g.tag ? g.tag : "wgrad_tc", 2.0 * g.M * (double)P.Kp * g.N,
+               gemm_a_bytes(g.A, g.M, 0, g.K) + (double)g.M * 4.0 * g.N + 4.0 * P.Kp * g.N);
+  launch_k(ctx, k_wgrad_mn, splits, MN_THREADS, smem, ctx->stream, g, P, partial, TM, pmap);
+  check_launch(ctx);
+  *partial_out = partial;
+  *Kp_out = P.Kp;
+  *splits_out = splits;
+  return true;
+}
+
 // Weight gradient on tcgen05 (TF32).  Returns false when the shape does not fit
 // (caller uses the SIMT kernel).  Writes partials [splits][Kp][N] for the batched reduction (reduce.cu).
 bool wgrad_tc(chg_ctx *ctx, const WGrad &g, float **partial_out, int *Kp_out, int *splits_out, bool *bias_done) {
   if (g.M <= 0 || g.K <= 0 || g.K % 32 || g.N % 32 || g.N > 256 || g.K > 256 || (g.ldd % 4)) return false;
+  if (wgrad_mn(ctx, g, partial_out, Kp_out, splits_out)) {
+    *bias_done = true;
+    return true;
+  }
   if ((uintptr_t)g.D & 15) return false;
   for (int s = 0; s < g.A.nseg; ++s) {
     const ASeg &S = g.A.seg[s];
