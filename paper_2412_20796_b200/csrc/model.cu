@@ -770,7 +770,10 @@ static void backward_core(chg_ctx *ctx, chg_model *m, chg_graph *g, const LossSe
   ac_bwd_head(Bw, T, dv, dagg);
   join_side(ctx);                                   // de complete before the atom conv adds to it
   ac_bwd_body(Bw, T, V(T), Ef(T), ea, dagg, dv, de, dea);
-  red_flush(ctx);
+  // the split-partial reductions run per layer when the layer's gradients feed a bucketed
+  // allreduce (NEXT-3); otherwise all of them in one launch at the end of the backward
+  const bool per_layer = ctx->grad_overlap && ctx->nccl_comm && ctx->nranks > 1;
+  if (per_layer) red_flush(ctx);
   ctx->ar_buckets = 0;
   grad_bucket(ctx, m, {{"head_"}, {"atom" + std::to_string(T) + "."}});
   for (int t = T - 1; t >= 0; --t) {
@@ -800,7 +803,7 @@ static void backward_core(chg_ctx *ctx, chg_model *m, chg_graph *g, const LossSe
       ctx->forked = false;
     }
     bc_bwd_body(Bw, t, ab, V(t), Ef(t), Af(t), eb, daggb, dv, de, da, deb, 2);
-    red_flush(ctx);
+    if (per_layer) red_flush(ctx);
     const std::string ts = std::to_string(t);
     grad_bucket(ctx, m, {{"atom" + ts + "."}, {"bond" + ts + "."}, {"angle" + ts + "."}});
   }

@@ -1395,12 +1395,15 @@ static int encode_op_map(CUtensorMap *m, const float *base, int ncols, int rows,
 bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   if (g.M <= 0 || g.K % KC != 0 || g.nchunk < 1) return false;
   const int split = ctx->tc_split ? 1 : 0;
+  // small problems (at most one 128-row tile per SM: the per-atom / per-bond products) need no
+  // A pipeline: one stage, which leaves room for a 256-column [hi | lo] weight image
+  const bool one_wave = ceil_div(g.M, TCM) <= device_sm_count();
   if (split && g.nchunk > 1) {
     // 3xTF32 stages hold [hi | lo] operands: at most 128 output columns per launch, so wider
     // GEMMs (bc_f1, bc_dX, ac_dX) run as launches over groups of their output chunks
     int cols = 0;
     for (int c = 0; c < g.nchunk; ++c) cols += (g.ch[c].ncols + 31) / 32 * 32;
-    if (cols > 128) {
+    if (cols > 128 && !(one_wave && g.K <= 64)) {
       int c0 = 0;
       while (c0 < g.nchunk) {
         RowGemm h = g;
@@ -1479,7 +1482,7 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   }
   const int nkc = P.width / KC;
   const size_t bchunk = ((size_t)KC * P.bnt * 4) << split, achunk = ((size_t)KC * TCM * 4) << split;
-  const int nsa_min = split ? 2 : 4;
+  const int nsa_min = split ? (one_wave ? 1 : 2) : 4;
   // TMA-store epilogue (lane = row) when every chunk's output is a plain [M][32k] table
   static const bool no_tstore = getenv("CHG_TC_NO_TSTORE") != nullptr;   // A/B knob
   TcMaps TM;
