@@ -1079,6 +1079,10 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_wgrad_tc(const __grid_constan
 //   = the bias gradient, one D box per warp for the whole kernel), warp 12 issues the MMAs,
 //   warps 0-3 drain TMEM into the CTA's partial (TMA bulk stores; reduce.cu sums the partials).
 // ---------------------------------------------------------------------------
+#ifdef CHG_TC_DEBUG
+__device__ int g_trace_wg = 0;
+__device__ __forceinline__ int getenv_trace_wg() { return g_trace_wg; }
+#endif
 constexpr int MN_RS = 32;                  // rows m per stage
 constexpr int MN_NLW = 4, MN_NCW = 8;      // loader / converter warps
 constexpr int MN_THREADS = (MN_NLW + MN_NCW + 1) * 32;
@@ -1118,6 +1122,12 @@ __global__ void __launch_bounds__(MN_THREADS, 1) k_wgrad_mn(const __grid_constan
   const int r0 = blockIdx.x * P.rows_per_cta;
   const int r1 = min(g.M, r0 + P.rows_per_cta);
   const int nchunks = r1 > r0 ? (r1 - r0 + MN_RS - 1) / MN_RS : 0;
+#ifdef CHG_TC_DEBUG
+  // per-CTA timeline of CTA 0 (debug builds, CHG_WG_TRACE=1): load issued, converted, MMA issued
+  __shared__ uint64_t tr_t0, tr_ld[16], tr_cv[16], tr_mm[16];
+  auto now = []() { uint64_t t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; };
+  if (tid == 0) tr_t0 = now();
+#endif
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
@@ -1182,6 +1192,9 @@ __global__ void __launch_bounds__(MN_THREADS, 1) k_wgrad_mn(const __grid_constan
         }
       }
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&loaded[s])) : "memory");
+#ifdef CHG_TC_DEBUG
+      if (tid == 0 && c < 16) tr_ld[c] = now();
+#endif
     }
   } else if (warp < MN_NLW + MN_NCW) {
     // ---------------- converters: lane = column of a box, rows in order ----------------
@@ -1216,6 +1229,9 @@ __global__ void __launch_bounds__(MN_THREADS, 1) k_wgrad_mn(const __grid_constan
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[s]);
+#ifdef CHG_TC_DEBUG
+      if (cw == 0 && lane == 0 && c < 16) tr_cv[c] = now();
+#endif
     }
     if (g.bias) {                                            // bias row K of this CTA's partial
       float *Pout = partial + (size_t)blockIdx.x * P.Kp * g.N + (size_t)g.K * g.N;
@@ -1253,6 +1269,9 @@ __global__ void __launch_bounds__(MN_THREADS, 1) k_wgrad_mn(const __grid_constan
         }
       }
       mma_commit(&empty[s]);
+#ifdef CHG_TC_DEBUG
+      if (c < 16) tr_mm[c] = now();
+#endif
     }
     mma_commit(done);
   }
@@ -1260,6 +1279,17 @@ __global__ void __launch_bounds__(MN_THREADS, 1) k_wgrad_mn(const __grid_constan
   // ---------------- epilogue: TMEM -> partial rows (thread = gradient row k) ----------------
   if (warp < 4) {
     if (nchunks > 0) mbar_wait(done, 0);
+#ifdef CHG_TC_DEBUG
+    if (tid == 0 && blockIdx.x == 0 && getenv_trace_wg()) {
+      const uint64_t t = now();
+      printf("WGTRACE K %d N %d chunks %d nst %d split %d | mma_done %.2f us |", g.K, g.N, nchunks, NST, P.split,
+             (t - tr_t0) * 1e-3);
+      for (int c = 0; c < min(16, nchunks); ++c)
+        printf(" [%d ld %.2f cv %.2f mm %.2f]", c, (tr_ld[c] - tr_t0) * 1e-3, (tr_cv[c] - tr_t0) * 1e-3,
+               (tr_mm[c] - tr_t0) * 1e-3);
+      printf("\n");
+    }
+#endif
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     float *stg = (float *)(smem + warp * 4096);
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
@@ -1692,6 +1722,11 @@ static bool wgrad_mn(chg_ctx *ctx, const WGrad &g, float **partial_out, int *Kp_
       return false;
   }
   smem_optin((const void *)k_wgrad_mn, 224 * 1024);
+#ifdef CHG_TC_DEBUG
+  static const int trace = getenv("CHG_WG_TRACE") ? 1 : 0;
+  static bool set = false;
+  if (!set) { cudaMemcpyToSymbol(g_trace_wg, &trace, sizeof(int)); set = true; }
+#endif
   ProfScope ps(ctx, g.tag ? g.tag : "wgrad_tc", 2.0 * g.M * (double)P.Kp * g.N,
                gemm_a_bytes(g.A, g.M, 0, g.K) + (double)g.M * 4.0 * g.N + 4.0 * P.Kp * g.N);
   launch_k(ctx, k_wgrad_mn, splits, MN_THREADS, smem, ctx->stream, g, P, partial, TM, pmap);
