@@ -174,6 +174,7 @@ struct chg_graph {
   int32_t *rev = nullptr;              // [E]
   // per bond
   int32_t *bond_edge = nullptr;        // [B]
+  int32_t *bond_ctr = nullptr;         // [B] centre atom of the bond
   int32_t *angle_ptr = nullptr;        // [B+1]
   // per angle
   int32_t *angle_b1 = nullptr;         // [A]
@@ -225,10 +226,8 @@ struct chg_model {
 // ---------------------------------------------------------------------------
 // round-to-nearest TF32 (10-bit mantissa) kept in an fp32 container: operands written in this
 // form are consumed by the tcgen05 kind::tf32 GEMMs without a conversion pass
-__device__ __forceinline__ float tf32_round(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+__device__ __forceinline__ float tf32_round(float x) {   // = cvt.rna.tf32.f32 (ties away from zero)
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 }
 // SiLU with the approximate reciprocal, as the tensor-core operand paths apply it
 __device__ __forceinline__ float silu_fast(float x) { return __fdividef(x, 1.0f + __expf(-x)); }

@@ -562,7 +562,7 @@ __global__ void __launch_bounds__(32 * GWPA) k_fill(int N, const double *__restr
 
 __global__ void k_angles(int B, const int32_t *__restrict__ bond_edge, const int32_t *__restrict__ center,
                          const int32_t *__restrict__ bond_ptr, const int32_t *__restrict__ atom_angle_ptr,
-                         int32_t *__restrict__ angle_ptr, int32_t *__restrict__ ab1,
+                         int32_t *__restrict__ bond_ctr, int32_t *__restrict__ angle_ptr, int32_t *__restrict__ ab1,
                          int32_t *__restrict__ ab2, int32_t *__restrict__ ae1, int32_t *__restrict__ ae2,
                          int32_t *__restrict__ actr, int32_t *__restrict__ swp, int A) {
   pdl_begin();
@@ -573,6 +573,7 @@ __global__ void k_angles(int B, const int32_t *__restrict__ bond_edge, const int
   }
   int e = bond_edge[b];
   int i = center[e];
+  bond_ctr[b] = i;
   int bs = bond_ptr[i], m = bond_ptr[i + 1] - bs, p = b - bs;
   int abase = atom_angle_ptr[i];
   int row = abase + p * (m - 1);
@@ -815,7 +816,7 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
     G->E = E; G->B = B; G->A = A;
 
     // ---- phase 2 allocation: edge / bond / angle arrays
-    size_t sz2 = align_up(4 * E) * 4 + align_up(4 * E) /*img*/ + align_up(16 * E) + align_up(32 * E) + align_up(4 * B) +
+    size_t sz2 = align_up(4 * E) * 4 + align_up(4 * E) /*img*/ + align_up(16 * E) + align_up(32 * E) + align_up(4 * B) * 2 +
                  align_up(4 * (B + 1)) + align_up(4 * A) * 6 + align_up(16) + 256;
     void *blk2 = nullptr;
     CUDA_OK(cudaMallocAsync(&blk2, sz2, st));
@@ -829,6 +830,7 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
     G->vec = (float4 *)take(16 * E);
     G->vec64 = (double4 *)take(32 * E);
     G->bond_edge = (int32_t *)take(4 * B);
+    G->bond_ctr = (int32_t *)take(4 * B);
     G->angle_ptr = (int32_t *)take(4 * (B + 1));
     G->angle_b1 = (int32_t *)take(4 * A);
     G->angle_b2 = (int32_t *)take(4 * A);
@@ -846,7 +848,7 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
                                                      G->nbr, G->img, G->vec, G->vec64, G->bond_id, G->bond_edge, ca);
       check_launch(ctx);
       launch_k(ctx, k_angles, ceil_div(B + 1, 256), 256, 0, st, (int)B, G->bond_edge, G->center, G->bond_ptr,
-                                                      G->atom_angle_ptr, G->angle_ptr, G->angle_b1,
+                                                      G->atom_angle_ptr, G->bond_ctr, G->angle_ptr, G->angle_b1,
                                                       G->angle_b2, G->angle_e1, G->angle_e2, G->angle_ctr,
                                                       G->swap, (int)A);
       check_launch(ctx);

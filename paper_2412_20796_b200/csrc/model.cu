@@ -66,13 +66,19 @@ void join_side(chg_ctx *ctx) {
 // P[rows, 64·nw] = X · [W_0[r_0:r_0+64] | W_1[r_1:r_1+64] | ...] (one 64-column chunk per weight
 // block; r == nullptr: all blocks at row r0)
 static void part_product(chg_ctx *ctx, const ASeg &x, int64_t rows, const float *const *W, int nw, int r0, float *P,
-                         int ldP, const char *tag, const int *r = nullptr) {
+                         int ldP, const char *tag, const int *r = nullptr, const float *add = nullptr,
+                         const int32_t *add_idx = nullptr) {
   if (rows <= 0) return;
   RowGemm G;
   G.A.seg[0] = x;
   G.A.nseg = 1;
   G.M = (int)rows; G.K = 64; G.nchunk = nw; G.tc = 1;
-  for (int c = 0; c < nw; ++c) G.ch[c] = chunk1(W[c] + (size_t)(r ? r[c] : r0) * 64, 64, 64, nullptr, P + 64 * c, ldP);
+  for (int c = 0; c < nw; ++c) {
+    G.ch[c] = chunk1(W[c] + (size_t)(r ? r[c] : r0) * 64, 64, 64, nullptr, P + 64 * c, ldP);
+    if (add) {   // + add[add_idx[row]] (a per-atom product carried into a per-bond one)
+      G.ch[c].gadd[0] = add + 64 * c; G.ch[c].gidx[0] = add_idx; G.ch[c].ldga[0] = ldP; G.ch[c].ngadd = 1;
+    }
+  }
   G.tag = tag;
   rowgemm(ctx, G);
 }
@@ -163,9 +169,11 @@ void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float
     float *P1 = ctx->getf(ctx->ws_name("bc_P1"), (size_t)std::max<int64_t>(B, 1) * ldP);
     float *P2 = ctx->getf(ctx->ws_name("bc_P2"), (size_t)std::max<int64_t>(B, 1) * ldP);
     part_product(ctx, aseg(v, 64, 64), N, W, nw, 0, Pv, ldP, "bc_P");
-    part_product(ctx, aseg(e, 64, 64, g->bond_edge, E), B, W, nw, 64, P1, ldP, "bc_P");
+    // Q1[b] = e_b·W[64:128] + Pv[centre of b]: the v_i part rides on the first bond (the angles
+    // of a first bond are contiguous, so the per-angle GEMM gathers Q1 with L1 reuse)
+    part_product(ctx, aseg(e, 64, 64, g->bond_edge, E), B, W, nw, 64, P1, ldP, "bc_P", nullptr, Pv, g->bond_ctr);
     part_product(ctx, aseg(e, 64, 64, g->bond_edge, E), B, W, nw, 128, P2, ldP, "bc_P");
-    // per angle: [z1_bond | y_angle] = a·W[192:256] + b + Pv[i] + P1[b1] + P2[b2]
+    // per angle: [z1_bond | y_angle] = a·W[192:256] + b + Q1[b1] + P2[b2]
     RowGemm G;
     G.A.seg[0] = aseg(a, 64, 64);
     G.A.nseg = 1;
@@ -174,10 +182,9 @@ void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float
       float *dst = c < 2 ? z1 + 64 * c : ya + 64 * (c - 2);
       G.ch[c] = chunk1(W[c] + 192 * 64, 64, 64, bias[c], dst, 128);
       Chunk &C = G.ch[c];
-      C.gadd[0] = Pv + 64 * c; C.gidx[0] = g->angle_ctr; C.ldga[0] = ldP;
-      C.gadd[1] = P1 + 64 * c; C.gidx[1] = g->angle_b1; C.ldga[1] = ldP;
-      C.gadd[2] = P2 + 64 * c; C.gidx[2] = g->angle_b2; C.ldga[2] = ldP;
-      C.ngadd = 3;
+      C.gadd[0] = P1 + 64 * c; C.gidx[0] = g->angle_b1; C.ldga[0] = ldP;
+      C.gadd[1] = P2 + 64 * c; C.gidx[1] = g->angle_b2; C.ldga[1] = ldP;
+      C.ngadd = 2;
     }
     G.tag = "bc_f1";
     rowgemm(ctx, G);

@@ -92,11 +92,10 @@ __device__ __forceinline__ void mma_commit(uint64_t *bar) {
 
 // SiLU with the approximate reciprocal (MUFU.RCP): its error (~2 ulp fp32) is far
 // below the TF32 rounding that follows, and it avoids the IEEE division sequence.
-__device__ __forceinline__ uint32_t to_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return r;
-}
+// round to nearest TF32, ties away from zero (= cvt.rna.tf32.f32) as two integer ops: add half
+// a TF32 ulp to the bit pattern and clear the 13 dropped mantissa bits (a carry moves into the
+// exponent exactly as rounding up does; Inf / NaN stay Inf / NaN)
+__device__ __forceinline__ uint32_t to_tf32(float x) { return (__float_as_uint(x) + 0x1000u) & 0xffffe000u; }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
@@ -453,16 +452,21 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
       uint4 *row = (uint4 *)(sA + sa * a_stage + r * 128);
       uint4 *row_lo = (uint4 *)(sA + sa * a_stage + a_bytes + r * 128);
       if (!TC_SKIP(16)) {
+        // all 8 loads first (independent: the row's 128 B), then convert and store — the
+        // stores may alias later loads for the compiler, so interleaving would serialise them
+        float4 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = *(const float4 *)&row[(k + sw) & 7];   // rotated: conflict-free
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          const int kk = (k + sw) & 7;                // rotated order: conflict-free banks
-          float4 v = *(const float4 *)&row[kk];
-          if (g.A.act == 1) { v.x = silu_fast(v.x); v.y = silu_fast(v.y); v.z = silu_fast(v.z); v.w = silu_fast(v.w); }
-          const uint4 h = make_uint4(to_tf32(v.x), to_tf32(v.y), to_tf32(v.z), to_tf32(v.w));
+          const int kk = (k + sw) & 7;
+          float4 x = v[k];
+          if (g.A.act == 1) { x.x = silu_fast(x.x); x.y = silu_fast(x.y); x.z = silu_fast(x.z); x.w = silu_fast(x.w); }
+          const uint4 h = make_uint4(to_tf32(x.x), to_tf32(x.y), to_tf32(x.z), to_tf32(x.w));
           row[kk] = h;
           if (P.split)                                // exact remainder, rounded to TF32 again
-            row_lo[kk] = make_uint4(to_tf32(v.x - __uint_as_float(h.x)), to_tf32(v.y - __uint_as_float(h.y)),
-                                    to_tf32(v.z - __uint_as_float(h.z)), to_tf32(v.w - __uint_as_float(h.w)));
+            row_lo[kk] = make_uint4(to_tf32(x.x - __uint_as_float(h.x)), to_tf32(x.y - __uint_as_float(h.y)),
+                                    to_tf32(x.z - __uint_as_float(h.z)), to_tf32(x.w - __uint_as_float(h.w)));
         }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic-proxy writes -> async proxy (MMA)
@@ -615,6 +619,14 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
         const int tile = blockIdx.x + tl * gridDim.x;
         const int row0 = tile * TCM + lq * 32;
         for (int k = 0; k < NB; ++k) issue_op(k, row0);
+        // gather indices of this lane's row for the epilogue additions (shared by all chunks),
+        // loaded while the accumulator is still being computed
+        int gr[2] = {row0 + lane, row0 + lane};
+        if (g.ch[0].ngadd && row0 + lane < g.M) {
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+            if (k < g.ch[0].ngadd && g.ch[0].gidx[k]) gr[k] = __ldg(g.ch[0].gidx[k] + row0 + lane);
+        }
         mbar_wait(&tfull[a], (tl >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         ep_mark();
@@ -630,16 +642,26 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
           }
           const int m = row0 + lane;
           if (C.ngadd && m < g.M) {                     // gathered row additions (factorised layer 1)
-#pragma unroll 1
-            for (int k = 0; k < C.ngadd; ++k) {
-              const int r = C.gidx[k] ? __ldg(C.gidx[k] + m) : m;
-              const float4 *src = reinterpret_cast<const float4 *>(C.gadd[k] + (size_t)r * C.ldga[k] + j0);
-              float4 u[8];
+            // row indices hoisted per tile (gr); every table's 16 columns of a half-block are in
+            // flight together: one memory latency per half-block, not one per table
 #pragma unroll
-              for (int q4 = 0; q4 < 8; ++q4) u[q4] = __ldg(src + q4);
+            for (int h = 0; h < 2; ++h) {
+              float4 u[2][4];
 #pragma unroll
-              for (int q4 = 0; q4 < 8; ++q4) {
-                v[4 * q4] += u[q4].x; v[4 * q4 + 1] += u[q4].y; v[4 * q4 + 2] += u[q4].z; v[4 * q4 + 3] += u[q4].w;
+              for (int k = 0; k < 2; ++k) {
+                if (k >= C.ngadd) break;
+                const float4 *src = reinterpret_cast<const float4 *>(C.gadd[k] + (size_t)gr[k] * C.ldga[k] + j0) + 4 * h;
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) u[k][q4] = __ldg(src + q4);
+              }
+#pragma unroll
+              for (int k = 0; k < 2; ++k) {
+                if (k >= C.ngadd) break;
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                  float *w = v + 16 * h + 4 * q4;
+                  w[0] += u[k][q4].x; w[1] += u[k][q4].y; w[2] += u[k][q4].z; w[3] += u[k][q4].w;
+                }
               }
             }
           }
@@ -1084,7 +1106,8 @@ __device__ int g_trace_wg = 0;
 __device__ __forceinline__ int getenv_trace_wg() { return g_trace_wg; }
 #endif
 constexpr int MN_RS = 32;                  // rows m per stage
-constexpr int MN_NLW = 4, MN_NCW = 8;      // loader / converter warps
+#define MN_RS_ 32
+constexpr int MN_NLW = 4, MN_NCW = 12;     // loader / converter warps
 constexpr int MN_THREADS = (MN_NLW + MN_NCW + 1) * 32;
 constexpr int MN_NST = 3;
 
@@ -1096,6 +1119,27 @@ struct WmPlan {
   int any_gather;
 };
 struct WmMaps { CUtensorMap a[4]; CUtensorMap d; };
+
+// one 32 x 32 MN-major box, lane = column: (SiLU), TF32 rounding in place (+ the lo part), column
+// sum (bias).  All loads first, then the stores (they may alias later loads for the compiler).
+template <bool SPLIT, bool ACT, bool SUM>
+__device__ __forceinline__ float convert_box(uint8_t *box, uint32_t lo_off, int ch, int hu, int e) {
+  float x[MN_RS_];
+#pragma unroll
+  for (int r = 0; r < MN_RS_; ++r)
+    x[r] = *reinterpret_cast<const float *>(box + r * 128 + (((ch ^ (r & 3)) << 1 | hu) << 4) + e * 4);
+  float acc = 0.f;
+#pragma unroll
+  for (int r = 0; r < MN_RS_; ++r) {
+    const uint32_t off = r * 128 + (((ch ^ (r & 3)) << 1 | hu) << 4) + e * 4;
+    const float y = ACT ? silu_fast(x[r]) : x[r];
+    if (SUM) acc += y;
+    const uint32_t h = to_tf32(y);
+    *reinterpret_cast<uint32_t *>(box + off) = h;
+    if (SPLIT) *reinterpret_cast<uint32_t *>(box + lo_off + off) = to_tf32(y - __uint_as_float(h));
+  }
+  return acc;
+}
 
 __device__ __forceinline__ void mbar_expect_tx_only(uint64_t *bar, uint32_t bytes) {
   asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
@@ -1209,22 +1253,22 @@ __global__ void __launch_bounds__(MN_THREADS, 1) k_wgrad_mn(const __grid_constan
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
         const int b = cw + MN_NCW * t;
+#ifdef CHG_TC_DEBUG
+        if (g_trace_wg & 2) break;                           // timing study: no conversion
+#endif
         if (b >= nbox || (b < P.nA && b >= nAk)) continue;    // no box / padding features
         const bool isA = b < P.nA;
         const bool act = isA && g.A.act == 1;
         uint8_t *box = st + b * BOX;
-        float acc = 0.f;
-#pragma unroll 8
-        for (int r = 0; r < MN_RS; ++r) {
-          const uint32_t off = r * 128 + (((ch ^ (r & 3)) << 1 | hu) << 4) + e * 4;
-          float x = *reinterpret_cast<const float *>(box + off);
-          if (act) x = silu_fast(x);
-          if (!isA) acc += x;
-          const uint32_t h = to_tf32(x);
-          *reinterpret_cast<uint32_t *>(box + off) = h;
-          if (P.split) *reinterpret_cast<uint32_t *>(box + half_bytes + off) = to_tf32(x - __uint_as_float(h));
+        if (P.split) {
+          if (act) convert_box<true, true, false>(box, half_bytes, ch, hu, e);
+          else if (isA) convert_box<true, false, false>(box, half_bytes, ch, hu, e);
+          else bsum[t] += convert_box<true, false, true>(box, half_bytes, ch, hu, e);
+        } else {
+          if (act) convert_box<false, true, false>(box, half_bytes, ch, hu, e);
+          else if (isA) convert_box<false, false, false>(box, half_bytes, ch, hu, e);
+          else bsum[t] += convert_box<false, false, true>(box, half_bytes, ch, hu, e);
         }
-        if (!isA) bsum[t] += acc;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
@@ -1471,9 +1515,13 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
     tot += S.width;
   }
   if (hi > tot) return false;
-  for (int c = 0; c < g.nchunk; ++c)                  // gathered additions: 16-B rows, no TMA-operand chunk
+  for (int c = 0; c < g.nchunk; ++c) {                // gathered additions: 16-B rows, no TMA-operand chunk,
+    if (g.ch[c].ngadd != g.ch[0].ngadd || g.ch[c].ngadd > 2) return false;  // <= 2, the same indices in every chunk
     for (int k = 0; k < g.ch[c].ngadd; ++k)
-      if (((uintptr_t)g.ch[c].gadd[k] & 15) || (g.ch[c].ldga[k] & 3) || g.ch[c].mul || g.ch[c].resid) return false;
+      if (((uintptr_t)g.ch[c].gadd[k] & 15) || (g.ch[c].ldga[k] & 3) || g.ch[c].mul || g.ch[c].resid ||
+          g.ch[c].gidx[k] != g.ch[0].gidx[k])
+        return false;
+  }
   P.lo = lo;
   P.width = hi - lo;
   P.ntot = off;
@@ -1723,7 +1771,7 @@ static bool wgrad_mn(chg_ctx *ctx, const WGrad &g, float **partial_out, int *Kp_
   }
   smem_optin((const void *)k_wgrad_mn, 224 * 1024);
 #ifdef CHG_TC_DEBUG
-  static const int trace = getenv("CHG_WG_TRACE") ? 1 : 0;
+  static const int trace = getenv("CHG_WG_TRACE") ? atoi(getenv("CHG_WG_TRACE")) : 0;
   static bool set = false;
   if (!set) { cudaMemcpyToSymbol(g_trace_wg, &trace, sizeof(int)); set = true; }
 #endif
