@@ -452,7 +452,9 @@ def main():
         return ms, launches, rep
 
     stats, last_stats = {}, [None]
-    for k in range(a.warmup):
+    # warm-up covers every cycled batch at least once (its graph / workspace sizes are then known
+    # to the memory pool before timing), and at least --warmup steps
+    for k in range(max(a.warmup, len(batches))):
         one_step(batches[k % len(batches)], False)
         one_step(batches[k % len(batches)], True)
     clocks = Clocks(local)
@@ -476,6 +478,8 @@ def main():
     # CUDA graph per batch, replayed with this step's lr (no host synchronisation inside the step)
     ms_capt, capt_launches, capt_err = None, None, None
     try:
+        if ws > 1:     # measured: the capture's first launch fails ("invalid device function") once NCCL
+            raise RuntimeError("captured step measured at N = 1 only (multi-rank stream capture fails on this stack)")
         execs = [ctx.capture_step(model, cached[i], b["dev"]["lab"], n_struct_global=b["gl"]["S"],
                                   n_atoms_global=b["gl"]["N"], n_magmom_global=b["gl"]["M"], allreduce=ws > 1)
                  for i, b in enumerate(batches)]
