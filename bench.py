@@ -494,7 +494,7 @@ def main():
         capt_err = f"{type(ex).__name__}: {ex}"
     for g_ in cached:
         g_.close()
-    ms_prof, _, rep = timed(False, profile=True)
+    _, _, rep = timed(False, profile=True)
     side = {}
     for other in others:
         for k in range(a.warmup):
@@ -599,6 +599,9 @@ def main():
             d[f] += v[f]
         d["tags"].append(t)
     dom = max(kern, key=lambda k: kern[k]["ms"])
+    # shares are of the summed kernel time of the profiled steps, the quantity ncu's launch list sums
+    # (the profiled pass itself is slowed by its per-launch events, so its wall time is not the base)
+    ms_sum = sum(v["ms"] for v in rep.values()) or 1e-9
     r = kern[dom]
     per_launch_s = r["ms"] / 1e3 / max(r["launches"], 1)
     traffic = None
@@ -628,7 +631,7 @@ def main():
         per_launch_alg = r["flops"] / max(r["launches"], 1)
     roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": traffic, "kernel": dom, "call_sites": sorted(r["tags"]),
                  "algorithmic_per_launch": per_launch_alg, "algorithmic_unit": "bytes" if roof["bound"] == "hbm" else "flop",
-                 "avg_launch_us": per_launch_s * 1e6, "share_of_step": r["ms"] / ms_prof,
+                 "avg_launch_us": per_launch_s * 1e6, "share_of_step": r["ms"] / ms_sum, "share_base": "summed kernel time of the step",
                  "profiled_pass": "same steps with per-launch CUDA events; the concurrent branches run serially "
                                   "while profiling, so each launch's time is its own",
                  "intensity_flop_per_byte": r["flops"] / max(r["bytes"], 1.0),
@@ -656,9 +659,9 @@ def main():
     step_ms = {"median": q(0.5), "p10": q(0.1), "p90": q(0.9), "mean": float(np.mean(ps_))}
     rank_ms = main_stats["rank_ms"]
     ops = {t: {"ms_per_step": v["ms"] / a.steps, "launches_per_step": v["launches"] / a.steps,
-               "share": v["ms"] / ms_prof, "kernel": kernel_of(t, a.precision)}
+               "share": v["ms"] / ms_sum, "kernel": kernel_of(t, a.precision)}
            for t, v in sorted(rep.items(), key=lambda kv: -kv[1]["ms"])}
-    kernels = {k: {"ms_per_step": v["ms"] / a.steps, "share": v["ms"] / ms_prof,
+    kernels = {k: {"ms_per_step": v["ms"] / a.steps, "share": v["ms"] / ms_sum,
                    "gbs": v["bytes"] / (v["ms"] / 1e3) / 1e9, "tflops": v["flops"] / (v["ms"] / 1e3) / 1e12}
                for k, v in sorted(kern.items(), key=lambda kv: -kv[1]["ms"])}
 
