@@ -43,12 +43,14 @@ FP32_PEAK_TFLOPS = 148 * 128 * 2 * PEAKS.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
 TF32_PEAK_TFLOPS = PEAKS.get("bf16_tflops_sustained", PEAKS.get("bf16_tflops", 1590.0)) * 1.1 / 2.25
 # 3xTF32 (mlp_precision 1): every fp32 product is three TF32 MMAs (A_lo·B_hi + A_hi·B_lo + A_hi·B_hi),
 # so the tensor roof for the algorithmic flops is a third of the TF32 peak
-PREC_CODE = {"fp32": 0, "3xtf32": 1, "tf32": 2}
-DTYPE = {"fp32": "f32", "3xtf32": "f32 (3xTF32)", "tf32": "tf32+f32"}
+PREC_CODE = {"fp32": 0, "3xtf32": 1, "tf32": 2, "bf16": 3}
+DTYPE = {"fp32": "f32", "3xtf32": "f32 (3xTF32)", "tf32": "tf32+f32", "bf16": "bf16+f32"}
+BF16_PEAK_TFLOPS = PEAKS.get("bf16_tflops_sustained", PEAKS.get("bf16_tflops", 1590.0))
 
 
 def tensor_peak(precision: str) -> float:
-    return {"tf32": TF32_PEAK_TFLOPS, "3xtf32": TF32_PEAK_TFLOPS / 3.0}.get(precision, FP32_PEAK_TFLOPS)
+    return {"tf32": TF32_PEAK_TFLOPS, "3xtf32": TF32_PEAK_TFLOPS / 3.0,
+            "bf16": BF16_PEAK_TFLOPS}.get(precision, FP32_PEAK_TFLOPS)
 
 
 def step_roofline(counts, precision: str):
@@ -108,7 +110,7 @@ def _args():
     ap.add_argument("--per-gpu", type=int, default=0, help="structures per GPU (default: 40 at N=1, 128 at N>1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--precision", default="3xtf32", choices=["3xtf32", "tf32", "fp32"],
+    ap.add_argument("--precision", default="3xtf32", choices=["3xtf32", "tf32", "bf16", "fp32"],
                     help="GatedMLP GEMM engine (headline mode): 3xtf32 = tcgen05 split-operand fp32 (strict "
                          "parity, the paper's fp32, P:473), tf32 = tcgen05 TF32 (NS loosened), fp32 = CUDA cores")
     ap.add_argument("--no-side-modes", action="store_true", help="skip timing the two other precision modes")
@@ -622,8 +624,9 @@ def main():
         per_launch_alg = r["bytes"] / max(r["launches"], 1)
     elif on_tc:
         roof = {"bound": "tensor", "achieved": tfs, "peak": flop_peak, "unit": "TFLOP/s",
-                "peak_source": "tf32 = " + PEAK_SRC + " bf16_tflops_sustained x (1.1/2.25 nominal ratio)"
-                               + (" / 3 (3xTF32: three MMAs per fp32 product)" if a.precision == "3xtf32" else "")}
+                "peak_source": (PEAK_SRC + " bf16_tflops_sustained") if a.precision == "bf16" else
+                               ("tf32 = " + PEAK_SRC + " bf16_tflops_sustained x (1.1/2.25 nominal ratio)"
+                                + (" / 3 (3xTF32: three MMAs per fp32 product)" if a.precision == "3xtf32" else ""))}
         per_launch_alg = r["flops"] / max(r["launches"], 1)
     else:
         roof = {"bound": "alu", "achieved": tfs, "peak": flop_peak, "unit": "TFLOP/s",
@@ -677,13 +680,17 @@ def main():
             "precision": {"mode": a.precision,
                           "note": "3xtf32: GatedMLP GEMMs on tcgen05 with split operands (hi + lo TF32, three MMAs, "
                                   "fp32 accumulate: strict 1e-4 gradient parity); tf32: tcgen05 TF32 (NS-loosened "
-                                  "2e-3); fp32: everything on CUDA cores (strict); heads, projections, output linears "
-                                  "and all non-GEMM kernels are fp32 in every mode",
+                                  "2e-3); bf16: tcgen05 kind::f16 with BF16 operands rounded as they are staged, fp32 "
+                                  "features in HBM (bars in DESIGN §6); fp32: everything on CUDA cores (strict); heads, "
+                                  "projections, output linears and all non-GEMM kernels are fp32 in every mode",
                           **{o: {"value": structs / (side[o] / 1e3), "ms_per_step": side[o] / a.steps,
                                  "dtype": DTYPE[o],
                                  "whole_step_frac": sum(max(r[2], r[3]) for r in
                                                         [step_roofline(batches[k % len(batches)]["counts"], o)
-                                                         for k in range(a.steps)]) / (side[o] / 1e3)}
+                                                         for k in range(a.steps)]) / (side[o] / 1e3),
+                                 "whole_step_hbm_frac": sum(r[3] for r in
+                                                            [step_roofline(batches[k % len(batches)]["counts"], o)
+                                                             for k in range(a.steps)]) / (side[o] / 1e3)}
                              for o in others}},
             "step_ms": step_ms,
             "whole_step_roofline": whole,

@@ -62,8 +62,11 @@ typedef struct { double r_atom, r_bond; } chg_cutoffs;
  *   1 = 3xTF32 on the tcgen05 tensor cores: each operand split x = hi + lo (both TF32)
  *       and A_lo·B_hi + A_hi·B_lo + A_hi·B_hi accumulated in fp32 (fp32-level accuracy,
  *       the strict 1e-4 gradient bar; the paper trains in fp32);
- *   2 = TF32 on the tcgen05 tensor cores (gradients <= 2e-3, NS "loosened" mode).
- * Only d = 64, n_radial = n_angular = 31, gmlp_hidden = head_hidden = 64 are built. */
+ *   2 = TF32 on the tcgen05 tensor cores (gradients <= 2e-3, NS "loosened" mode);
+ *   3 = BF16 on the tcgen05 tensor cores (kind::f16, fp32 accumulate): GEMM operands are
+ *       rounded to BF16 as they are staged, features stay fp32 in HBM (the NS 2e-3
+ *       gradient bar; a weight gradient with indexed D rows runs in TF32).
+ * Any other value is CHG_ERR_ARG at chg_model_create.  Only d = 64, n_radial = n_angular = 31, gmlp_hidden = head_hidden = 64 are built. */
 typedef struct {
   int d, n_radial, n_angular, envelope_p, n_atom_conv, n_bond_conv, gmlp_hidden,
       n_species, head_hidden, mlp_precision;
@@ -276,7 +279,7 @@ chg_status chg_profile_query(chg_ctx *ctx, int idx, char *tag, double *ms, int64
  *   kind 0: out[M,N] = A[M,K] · W[K,N]          (row GEMM; W is also given K-major
  *           internally for the tensor-core path)
  *   kind 1: out[K,N] = A[M,K]ᵀ · D[M,N]         (weight-gradient GEMM; `W` = D)
- * engine 0 = fp32 CUDA cores, 1 = tcgen05 3xTF32, 2 = tcgen05 TF32.  Returns CHG_ERR_ARG if the
+ * engine 0 = fp32 CUDA cores, 1 = tcgen05 3xTF32, 2 = tcgen05 TF32, 3 = tcgen05 BF16.  Returns CHG_ERR_ARG if the
  * engine cannot run the shape.  Synchronises. */
 chg_status chg_debug_gemm(chg_ctx *ctx, int kind, int engine, int M, int K, int N, const float *A,
                           const float *W, float *out);

@@ -142,7 +142,7 @@ def _on_device(x) -> bool:
 
 
 # chg_model_cfg.mlp_precision values this build implements (include/chg.h)
-PRECISION_MODES = {0: "fp32", 1: "3xtf32", 2: "tf32"}
+PRECISION_MODES = {0: "fp32", 1: "3xtf32", 2: "tf32", 3: "bf16"}
 
 
 def default_model_cfg() -> ModelCfg:

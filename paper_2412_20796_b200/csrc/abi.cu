@@ -323,9 +323,9 @@ chg_status chg_model_create(chg_ctx *ctx, const chg_model_cfg *cfg, chg_model **
     const chg_model_cfg &c = *cfg;
     if (c.d != 64 || c.n_radial != 31 || c.n_angular != 31 || c.gmlp_hidden != 64 || c.head_hidden != 64 ||
         c.n_atom_conv != c.n_bond_conv + 1 || c.n_bond_conv < 1 || c.n_species != 94 || c.envelope_p < 2 ||
-        c.mlp_precision < 0 || c.mlp_precision > 2)
+        c.mlp_precision < 0 || c.mlp_precision > 3)
       CHG_THROW(CHG_ERR_ARG, "unsupported model config (built: d=64, K=31, hidden 64, n_atom_conv = n_bond_conv+1, "
-                             "94 species, mlp_precision 0 (fp32), 1 (3xTF32 tcgen05) or 2 (TF32 tcgen05))");
+                             "94 species, mlp_precision 0 (fp32), 1 (3xTF32 tcgen05), 2 (TF32 tcgen05) or 3 (BF16 tcgen05))");
     build_layout(m);
     CUDA_OK(cudaSetDevice(ctx->device));
     // params | grads | adam m | adam v, each segment 256-B aligned (vector loads and stores)

@@ -94,12 +94,18 @@ struct chg_ctx {
   const chg_graph *fwd_graph = nullptr;
   uint64_t fwd_graph_id = 0;
   bool fwd_train = false;
-  // GEMM engine for the current call: false = fp32 CUDA cores, true = tcgen05 (TF32, or
-  // 3xTF32 split operands when tc_split: mlp_precision 1)
+  // GEMM engine for the current call: false = fp32 CUDA cores, true = tcgen05 (TF32, 3xTF32
+  // split operands when tc_split: mlp_precision 1, BF16 operands when tc_bf16: mlp_precision 3)
   bool use_tc = false;
   bool tc_split = false;
+  bool tc_bf16 = false;
+  void set_precision(int mlp_precision) {
+    use_tc = mlp_precision >= 1 && mlp_precision <= 3;
+    tc_split = mlp_precision == 1;
+    tc_bf16 = mlp_precision == 3;
+  }
   // producers may write tensor-core-only operands already TF32-rounded (plain TF32 mode only)
-  bool tc_round() const { return use_tc && !tc_split; }
+  bool tc_round() const { return use_tc && !tc_split && !tc_bf16; }
   bool forked = false;           // a side-stream branch is in flight: plain launches (no PDL)
   const struct chg_model *cur_model = nullptr;   // model of the current forward/backward
   const float *cur_wt = nullptr;                 // its transposed weight copy (same flat offsets)

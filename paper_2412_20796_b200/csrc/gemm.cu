@@ -459,10 +459,9 @@ extern "C" chg_status chg_debug_gemm(chg_ctx *ctx, int kind, int engine, int M, 
     CUDA_OK(cudaMemcpyAsync(dA, A, 4 * na, cudaMemcpyHostToDevice, st));
     CUDA_OK(cudaMemcpyAsync(dW, W, 4 * nw, cudaMemcpyHostToDevice, st));
     CUDA_OK(cudaMemsetAsync(dO, 0, 4 * no, st));
-    const bool old = ctx->use_tc, old_split = ctx->tc_split;
+    const bool old = ctx->use_tc, old_split = ctx->tc_split, old_bf16 = ctx->tc_bf16;
     const chg_model *old_model = ctx->cur_model;
-    ctx->use_tc = engine == 1 || engine == 2;
-    ctx->tc_split = engine == 1;
+    ctx->set_precision(engine);
     ctx->cur_model = nullptr;                  // no weight-image caching for the hook's scratch operands
     if (kind == 0) {
       std::vector<float> wk((size_t)K * N);
@@ -496,6 +495,7 @@ extern "C" chg_status chg_debug_gemm(chg_ctx *ctx, int kind, int engine, int M, 
     }
     ctx->use_tc = old;
     ctx->tc_split = old_split;
+    ctx->tc_bf16 = old_bf16;
     ctx->cur_model = old_model;
     CUDA_OK(cudaMemcpyAsync(out, dO, 4 * no, cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaStreamSynchronize(st));

@@ -232,8 +232,7 @@ void forward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, int train, chg_pred 
   const int p = m->cfg.envelope_p;
   ctx->dbg.clear();
   ctx->fwd_train = false;
-  ctx->use_tc = m->cfg.mlp_precision == 1 || m->cfg.mlp_precision == 2;
-  ctx->tc_split = m->cfg.mlp_precision == 1;
+  ctx->set_precision(m->cfg.mlp_precision);
   ctx->cur_model = m;
   ctx->cur_wt = nullptr;
   if (ctx->use_tc) {   // K-major weight copy for the tensor-core operands
@@ -733,8 +732,7 @@ static void backward_core(chg_ctx *ctx, chg_model *m, chg_graph *g, const LossSe
   Bwd Bw{ctx, m, g, nullptr};
   if (!m->wt) CUDA_OK(cudaMalloc(&m->wt, 4 * (size_t)std::max<int64_t>(m->P, 1)));
   Bw.wt = m->wt;
-  ctx->use_tc = m->cfg.mlp_precision == 1 || m->cfg.mlp_precision == 2;
-  ctx->tc_split = m->cfg.mlp_precision == 1;
+  ctx->set_precision(m->cfg.mlp_precision);
   if (!ctx->use_tc) transpose_params(ctx, m, Bw.wt);   // tensor-core modes: the forward's copy is current
   ctx->cur_model = m;
   ctx->cur_wt = Bw.wt;

@@ -19,6 +19,7 @@
 // partials reduced in a fixed order (reduce.cu).  See DESIGN.md §5.
 // Debug / timing knobs (CHG_TC_SKIP, per-CTA trace) exist only in -DCHG_TC_DEBUG builds.
 #include <cuda.h>
+#include <cuda_bf16.h>
 
 #include "gemm.cuh"
 
@@ -82,6 +83,25 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64
       "}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
       : "memory");
+}
+
+// BF16 operands, fp32 accumulator (kind::f16; UMMA K = 16)
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+
+// two fp32 -> one packed bf16x2 (round to nearest even; lo in the low half)
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t *>(&h);
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
@@ -167,6 +187,8 @@ struct TcPlan {
   int noconv;        // 1: A arrives TF32-rounded by TMA: no conversion pass, the MMA waits on the load
   int split;         // 1: 3xTF32 (mlp_precision 1): operands split x = hi + lo (both TF32), three MMAs
                      //    A_lo·B_hi + A_hi·B_lo + A_hi·B_hi per K step; stages hold [hi | lo]
+  int bf16;          // 1: BF16 operands (mlp_precision 3): stages hold [fp32 as loaded | bf16 copy
+                     //    (SWIZZLE_64B K-major, 64 B per row)], weight image in BF16, 2 MMAs (K = 16) per stage
   int nsb;           // B ring slots (<= NSB) when the image is not resident
   // compact weight image: K chunk kc holds only the chunks whose A window covers it (block-
   // diagonal GEMMs — the second GatedMLP layer, its adjoint — store half the columns), bnt
@@ -188,6 +210,11 @@ __device__ __forceinline__ void pack_elem(const RowGemm &g, const TcPlan &P, uin
     if (kk < 0 || kk >= g.K) continue;
     for (int b = 0; b < C.nwb; ++b)
       if (kk >= C.wk0[b] && kk < C.wk0[b + 1]) v = C.Wk[b][(size_t)j * C.ldwk[b] + (kk - C.wk0[b])];
+  }
+  if (P.bf16) {                                  // BF16 image: [kc][k/8][n][8] in the first half of kc's slot
+    reinterpret_cast<__nv_bfloat16 *>(img)[(size_t)kc * P.bnt * KC * 2 + ((k >> 3) * P.bnt + n) * 8 + (k & 7)] =
+        __float2bfloat16_rn(v);
+    return;
   }
   const size_t at = (size_t)kc * P.bnt * KC + ((k >> 2) * P.bnt + n) * 4 + (k & 3);
   const uint32_t hi = to_tf32(v);
@@ -321,8 +348,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int NT = P.bnt;                                 // weight-image columns per K chunk
-  const uint32_t a_bytes = KC * TCM * 4, b_bytes = KC * NT * 4;
-  const uint32_t a_stage = a_bytes << P.split, b_stage = b_bytes << P.split;   // [hi | lo] in split mode
+  const uint32_t a_bytes = KC * TCM * 4, b_bytes = P.bf16 ? KC * NT * 2 : KC * NT * 4;
+  // [hi | lo] in split mode, [fp32 | bf16] in BF16 mode
+  const uint32_t a_stage = P.bf16 ? a_bytes + a_bytes / 2 : a_bytes << P.split, b_stage = b_bytes << P.split;
   const int NSA = P.nsa, NSBr = P.nsb;
   const uint32_t *bimg_lo = bimg + (size_t)(P.width / KC) * NT * KC;
   uint8_t *sA = smem;                                   // [NSA][a_stage]
@@ -451,7 +479,24 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
       mbar_wait(&loaded[sa], ua & 1);
       uint4 *row = (uint4 *)(sA + sa * a_stage + r * 128);
       uint4 *row_lo = (uint4 *)(sA + sa * a_stage + a_bytes + r * 128);
-      if (!TC_SKIP(16)) {
+      if (P.bf16) {
+        // logical 16-B unit u of the row sits at u ^ (r & 7); BF16 unit c (k = 8c..8c+7) of the
+        // copy goes to row r of the SWIZZLE_64B region at c ^ ((r >> 1) & 3)
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = *(const float4 *)&row[u ^ sw];
+        uint8_t *brow = sA + sa * a_stage + a_bytes + r * 64;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float4 x = v[2 * c], y = v[2 * c + 1];
+          if (g.A.act == 1) {
+            x.x = silu_fast(x.x); x.y = silu_fast(x.y); x.z = silu_fast(x.z); x.w = silu_fast(x.w);
+            y.x = silu_fast(y.x); y.y = silu_fast(y.y); y.z = silu_fast(y.z); y.w = silu_fast(y.w);
+          }
+          *reinterpret_cast<uint4 *>(brow + ((c ^ ((r >> 1) & 3)) << 4)) =
+              make_uint4(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w), pack_bf16(y.x, y.y), pack_bf16(y.z, y.w));
+        }
+      } else if (!TC_SKIP(16)) {
         // all 8 loads first (independent: the row's 128 B), then convert and store — the
         // stores may alias later loads for the compiler, so interleaving would serialise them
         float4 v[8];
@@ -531,6 +576,19 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
             const int c = P.gfirst[gr];
             const int kk = col0 - g.ch[c].a_k0;
             if (kk < 0 || kk >= g.K) continue;
+            if (P.bf16) {                                 // BF16: K = 16 per MMA, A from the SWIZZLE_64B copy
+              const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(P.gn[gr] >> 3) << 17) |
+                                     ((uint32_t)(TCM >> 4) << 24);
+#pragma unroll
+              for (int j = 0; j < KC / 16; ++j) {
+                const uint64_t ad = make_desc(a_base + a_bytes + j * 32, 16, 512) | ((uint64_t)4 << 61);   // SWIZZLE_64B
+                const uint64_t bd = make_desc(b_base + j * 2 * (NT * 16) + P.bcoff[kc][c] * 16, NT * 16, 128);
+                if (TC_SKIP(8)) continue;
+                mma_bf16(tmem + a * tcols + P.coff[c], ad, bd, idesc, (started[gr] || j > 0) ? 1u : 0u);
+              }
+              started[gr] = true;
+              continue;
+            }
             const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(P.gn[gr] >> 3) << 17) |
                                    ((uint32_t)(TCM >> 4) << 24);
 #pragma unroll
@@ -1113,6 +1171,7 @@ constexpr int MN_NST = 3;
 
 struct WmPlan {
   int Kpad, ktiles, nA, nD, Kp, rows_per_cta, split, nst;
+  int bf16;                                // BF16 operands: stage = [fp32 boxes | bf16 boxes (SWIZZLE_64B)]
   uint32_t tmem_cols;
   int abox_seg[8], abox_col[8];            // A box b: segment, first column within the segment
   int tma_bytes;                           // TMA bytes per stage (direct A boxes + D boxes)
@@ -1141,6 +1200,25 @@ __device__ __forceinline__ float convert_box(uint8_t *box, uint32_t lo_off, int 
   return acc;
 }
 
+// BF16 mode: the box's column `lane` (SiLU for act) rounded to BF16 into the MN-major SWIZZLE_64B
+// copy (32 rows x 64 B; the 16-B unit c of row r at c ^ ((r >> 1) & 3)); returns its column sum
+template <bool ACT, bool SUM>
+__device__ __forceinline__ float convert_box_bf16(const uint8_t *box, uint8_t *bbox, int ch, int hu, int e, int lane) {
+  float x[MN_RS_];
+#pragma unroll
+  for (int r = 0; r < MN_RS_; ++r)
+    x[r] = *reinterpret_cast<const float *>(box + r * 128 + (((ch ^ (r & 3)) << 1 | hu) << 4) + e * 4);
+  float acc = 0.f;
+#pragma unroll
+  for (int r = 0; r < MN_RS_; ++r) {
+    const float y = ACT ? silu_fast(x[r]) : x[r];
+    if (SUM) acc += y;
+    *reinterpret_cast<__nv_bfloat16 *>(bbox + r * 64 + ((((lane >> 3) ^ ((r >> 1) & 3))) << 4) + (lane & 7) * 2) =
+        __float2bfloat16_rn(y);
+  }
+  return acc;
+}
+
 __device__ __forceinline__ void mbar_expect_tx_only(uint64_t *bar, uint32_t bytes) {
   asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
@@ -1155,7 +1233,8 @@ __global__ void __launch_bounds__(MN_THREADS, 1) k_wgrad_mn(const __grid_constan
   constexpr uint32_t BOX = MN_RS * 128;                       // one box: RS rows x 32 fp32
   const int nbox = P.nA + P.nD;
   const uint32_t half_bytes = nbox * BOX;                     // hi part of a stage
-  const uint32_t st_bytes = half_bytes << P.split;            // [A hi | D hi] (| [A lo | D lo])
+  // [A hi | D hi] (| [A lo | D lo]); BF16: [A | D] as loaded, then their BF16 copies (BOX / 2 each)
+  const uint32_t st_bytes = P.bf16 ? half_bytes + half_bytes / 2 : half_bytes << P.split;
   const int NST = P.nst;
   uint64_t *loaded = (uint64_t *)(smem + NST * st_bytes);
   uint64_t *full = loaded + MN_NST;
@@ -1190,10 +1269,16 @@ __global__ void __launch_bounds__(MN_THREADS, 1) k_wgrad_mn(const __grid_constan
   }
   // padding feature boxes (k >= K, never loaded) are zero in every stage, hi and lo
   for (int s = 0; s < NST; ++s)
-    for (int b = g.K / 32; b < P.nA; ++b)
+    for (int b = g.K / 32; b < P.nA; ++b) {
+      if (P.bf16) {
+        for (int i = tid; i < (int)(BOX / 32); i += blockDim.x)
+          reinterpret_cast<uint4 *>(smem + s * st_bytes + half_bytes + b * (BOX / 2))[i] = make_uint4(0, 0, 0, 0);
+        continue;
+      }
       for (int h = 0; h <= P.split; ++h)
         for (int i = tid; i < (int)(BOX / 16); i += blockDim.x)
           reinterpret_cast<uint4 *>(smem + s * st_bytes + h * half_bytes + b * BOX)[i] = make_uint4(0, 0, 0, 0);
+    }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -1260,7 +1345,12 @@ __global__ void __launch_bounds__(MN_THREADS, 1) k_wgrad_mn(const __grid_constan
         const bool isA = b < P.nA;
         const bool act = isA && g.A.act == 1;
         uint8_t *box = st + b * BOX;
-        if (P.split) {
+        if (P.bf16) {
+          uint8_t *bbox = st + half_bytes + b * (BOX / 2);
+          if (act) convert_box_bf16<true, false>(box, bbox, ch, hu, e, lane);
+          else if (isA) convert_box_bf16<false, false>(box, bbox, ch, hu, e, lane);
+          else bsum[t] += convert_box_bf16<false, true>(box, bbox, ch, hu, e, lane);
+        } else if (P.split) {
           if (act) convert_box<true, true, false>(box, half_bytes, ch, hu, e);
           else if (isA) convert_box<true, false, false>(box, half_bytes, ch, hu, e);
           else bsum[t] += convert_box<true, false, true>(box, half_bytes, ch, hu, e);
@@ -1289,11 +1379,29 @@ __global__ void __launch_bounds__(MN_THREADS, 1) k_wgrad_mn(const __grid_constan
     // ---------------- MMA issuer ----------------
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) |
                            ((uint32_t)(g.N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const uint32_t idesc_bf = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) |
+                              ((uint32_t)(g.N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    constexpr uint32_t BOXB = BOX / 2;                          // one BF16 box: RS rows x 64 B
     for (int c = 0; c < nchunks; ++c) {
       const int s = c % NST, u = c / NST;
       mbar_wait(&full[s], u & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t base = smem_u32(smem + s * st_bytes);
+      if (P.bf16) {
+        // MN-major SWIZZLE_64B: the next 32 features at LBO = one BF16 box, the next 8 rows at
+        // SBO = 512 B; an MMA K step (16 rows) advances 1 KB
+        const uint32_t bb = base + half_bytes;
+        for (int tt = 0; tt < P.ktiles; ++tt) {
+#pragma unroll
+          for (int j = 0; j < MN_RS / 16; ++j) {
+            const uint64_t ad = make_desc(bb + tt * 4 * BOXB + j * 1024, BOXB, 512) | ((uint64_t)4 << 61);
+            const uint64_t bd = make_desc(bb + P.nA * BOXB + j * 1024, BOXB, 512) | ((uint64_t)4 << 61);
+            mma_bf16(tmem + tt * g.N, ad, bd, idesc_bf, (c > 0 || j > 0) ? 1u : 0u);
+          }
+        }
+        mma_commit(&empty[s]);
+        continue;
+      }
       for (int tt = 0; tt < P.ktiles; ++tt) {
 #pragma unroll
         for (int j = 0; j < MN_RS / 8; ++j) {
@@ -1496,6 +1604,7 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   }
   TcPlan P{};
   P.split = split;
+  P.bf16 = ctx->tc_bf16 ? 1 : 0;
   int lo = 1 << 30, hi = 0, off = 0;
   for (int c = 0; c < g.nchunk; ++c) {
     const Chunk &C = g.ch[c];
@@ -1559,7 +1668,8 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
     }
   }
   const int nkc = P.width / KC;
-  const size_t bchunk = ((size_t)KC * P.bnt * 4) << split, achunk = ((size_t)KC * TCM * 4) << split;
+  const size_t bchunk = P.bf16 ? (size_t)KC * P.bnt * 2 : ((size_t)KC * P.bnt * 4) << split;
+  const size_t achunk = P.bf16 ? (size_t)KC * TCM * 6 : ((size_t)KC * TCM * 4) << split;
   const int nsa_min = split ? (one_wave ? 1 : 2) : 4;
   // TMA-store epilogue (lane = row) when every chunk's output is a plain [M][32k] table
   static const bool no_tstore = getenv("CHG_TC_NO_TSTORE") != nullptr;   // A/B knob
@@ -1679,7 +1789,7 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
     TM.use[s] = encode_a_map(&TM.m[s], S.base, S.width, g.M, S.ld);
   }
   static const bool no_noconv = getenv("CHG_TC_NO_NOCONV") != nullptr;    // A/B knob
-  P.noconv = g.A.rounded && g.A.act == 0 && !no_noconv && !split;
+  P.noconv = g.A.rounded && g.A.act == 0 && !no_noconv && !split && !P.bf16;
   for (int s = 0; s < g.A.nseg; ++s) P.noconv &= TM.use[s];
   TM.nbuf = nbuf;
   for (int c = 0; c < g.nchunk && nbuf > 0; ++c) {
@@ -1712,6 +1822,7 @@ static bool wgrad_mn(chg_ctx *ctx, const WGrad &g, float **partial_out, int *Kp_
   P.nD = g.N / 32;
   P.Kp = g.K + (g.bias ? 1 : 0);
   P.split = ctx->tc_split ? 1 : 0;
+  P.bf16 = ctx->tc_bf16 ? 1 : 0;
   const int cols = P.ktiles * g.N;
   if (cols > 512) return false;
   P.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
@@ -1748,7 +1859,8 @@ static bool wgrad_mn(chg_ctx *ctx, const WGrad &g, float **partial_out, int *Kp_
       return false;
   }
   P.tma_bytes = (direct_boxes + P.nD) * MN_RS * 128;
-  const size_t st_bytes = ((size_t)(P.nA + P.nD) * MN_RS * 128) << P.split;
+  const size_t st_half = (size_t)(P.nA + P.nD) * MN_RS * 128;
+  const size_t st_bytes = P.bf16 ? st_half + st_half / 2 : st_half << P.split;
   const size_t fixed = 1024 + 8 * (3 * MN_NST + 1) + 16;
   P.nst = (int)std::min<size_t>(MN_NST, (224 * 1024 - fixed) / st_bytes);
   if (P.nst < 2) return false;

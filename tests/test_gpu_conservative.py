@@ -63,15 +63,17 @@ def test_conservative_forces_stress(ctx, params, case, prec):
     F, S = ref["forces"].detach().numpy(), ref["stress"].detach().numpy()
     E = ref["energy"].detach().numpy()
     natoms = np.diff(b.atom_ptr)
-    if prec != 2:      # fp32 strict and 3xTF32: the NS F / sigma / E bars
-                       # (TF32: F and sigma are position / strain GRADIENTS: NS-loosened 2e-3 relative)
+    if prec in (0, 1):  # fp32 strict and 3xTF32: the NS F / sigma / E bars
+                        # (TF32: F and sigma are position / strain GRADIENTS: NS-loosened 2e-3 relative;
+                        # BF16: 2e-2 relative)
         assert np.max(np.abs(out["forces"] - F)) <= 1e-4, np.max(np.abs(out["forces"] - F))
         assert np.max(np.abs(out["stress"] - S)) <= 1e-4, np.max(np.abs(out["stress"] - S))
         epa = E / natoms
         assert np.all(np.abs(out["energy_per_atom"] - epa) <= 1e-5 * np.maximum(np.abs(epa), 1.0))
     else:
-        assert _rel(out["forces"], F) <= 2e-3, _rel(out["forces"], F)
-        assert _rel(out["stress"], S) <= 2e-3, _rel(out["stress"], S)
+        bar = 2e-3 if prec == 2 else 2e-2
+        assert _rel(out["forces"], F) <= bar, _rel(out["forces"], F)
+        assert _rel(out["stress"], S) <= bar, _rel(out["stress"], S)
     # parameter gradients untouched; the activations were consumed
     assert np.all(m.grads() == 0)
     with pytest.raises(chg.ChgError) as e:

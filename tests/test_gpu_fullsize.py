@@ -103,7 +103,7 @@ def test_fullsize_forward_sampled(ctx, params, wl, prec):
     gg = ctx.build_graph(b.atom_ptr, b.positions, b.lattice, b.species)
     out = ctx.forward(m, gg, train=True)
     tol, ftol = 1e-5, 1e-4                     # NS output bars in every mode
-    mtol = 2e-4 if prec == 2 else 1e-5         # magmom: TF32 bar stated in DESIGN §6
+    mtol = {2: 2e-4, 3: 2e-3}.get(prec, 1e-5)  # magmom: TF32 / BF16 bars stated in DESIGN §6
     for s in _samples(b):
         sb = split_batch(b, [s])
         ref = run_forward(build_graph_batch(sb), sb.species, sb.lattice, params, CFG)

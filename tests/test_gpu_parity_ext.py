@@ -17,10 +17,13 @@
   fp32 CUDA cores 5e-4 [1.2e-4, C4]; 3xTF32 5e-3 [1.2e-3, C4 bond W1: the tensor core's
   accumulation is not IEEE round-to-nearest, ~10x the SIMT error, while its per-tensor error
   2.9e-5 meets the NS 1e-4]; TF32 0.15 [0.061, C4: single elements that are sums of
-  cancelling TF32 products].
+  cancelling TF32 products]; BF16 1.0 [0.59, C2] with per-tensor 1.5e-2 [7.3e-3]: BF16 does
+  NOT meet the NS 2e-3 per-tensor bar on the angle-update tensors (reported), and
+  its element-wise bar is no localisation check — the fp32 / 3xTF32 / TF32 modes carry that.
 * Output bars (NS): E/atom 1e-5 max(|eps|, 1 eV), F 1e-4 eV/A, sigma 1e-4 GPa in
   every mode; magmom 1e-5 muB (fp32 strict, 3xTF32), 2e-4 muB (TF32: m is a linear map of v^4,
-  whose TF32 feature error is ~1e-5 relative; measured 5.9e-5, profiles/r01_tf32_parity_errors.json).
+  whose TF32 feature error is ~1e-5 relative; measured 5.9e-5, profiles/r01_tf32_parity_errors.json),
+  2e-3 muB (BF16, measured 5.9e-4).
 * Labels: a NULL label array skips its task (chg_labels), all NULL is CHG_ERR_ARG.
 """
 import json
@@ -49,6 +52,11 @@ MODES = {0: dict(name="fp32", grad=1e-4, elem=5e-4, mag=1e-5),
          2: dict(name="tf32", grad=2e-3, elem=0.15, mag=2e-4)}
 if 1 in chg.PRECISION_MODES:
     MODES[1] = dict(name="3xtf32", grad=1e-4, elem=5e-3, mag=1e-5)
+if 3 in chg.PRECISION_MODES:
+    # BF16 operands (8-bit significand): the NS 2e-3 per-tensor bar fails on the angle-update
+    # GatedMLP tensors (measured worst 7.3e-3, median 1.7e-3: profiles/r02_mode_errors_bf16.json);
+    # the bars below are the measured worst x ~2, stated in DESIGN §6; loss terms 1e-3 relative
+    MODES[3] = dict(name="bf16", grad=1.5e-2, elem=1.0, mag=2e-3, loss=1e-3)
 REPORT = {}
 OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
 
@@ -137,7 +145,7 @@ def test_c3_full_backward(ctx, params, prec):
     errs = _check_outputs(out, {k: torch.as_tensor(v) for k, v in R["out"].items()}, bars)
     REPORT[f"c3_outputs_{bars['name']}"] = errs
     for k, key in enumerate(["total", "E", "F", "S", "M"]):
-        assert abs(loss[k] - R["terms"][key]) <= 1e-5 * max(abs(R["terms"][key]), 1e-6), key
+        assert abs(loss[k] - R["terms"][key]) <= bars.get("loss", 1e-5) * max(abs(R["terms"][key]), 1e-6), key
     _check_grads(m.grads(), R["gref"], bars, f"c3_grads_{bars['name']}")
     g.close(); m.close()
 
@@ -226,7 +234,7 @@ def test_edge_cases_forward_backward(ctx, params, prec, cut):
     REPORT[f"edge_{cut[0]}_outputs_{bars['name']}"] = _check_outputs(
         out, {k: torch.as_tensor(v) for k, v in ref.items()}, bars)
     for k, key in enumerate(["total", "E", "F", "S", "M"]):
-        assert abs(loss[k] - terms[key]) <= 1e-5 * max(abs(terms[key]), 1e-6), key
+        assert abs(loss[k] - terms[key]) <= bars.get("loss", 1e-5) * max(abs(terms[key]), 1e-6), key
     _check_grads(m.grads(), gref, bars, f"edge_{cut[0]}_grads_{bars['name']}")
     g.close(); m.close()
 
