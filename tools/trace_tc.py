@@ -7,7 +7,7 @@ from paper_2412_20796_b200 import chg
 os.environ.setdefault("CHG_SERIAL", "1")
 b = make_config_batch(sys.argv[1] if len(sys.argv) > 1 else "C2")
 ctx = chg.Context(0)
-cfg = chg.default_model_cfg(); cfg.mlp_precision = 2
+cfg = chg.default_model_cfg(); cfg.mlp_precision = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 m = chg.Model(ctx, cfg)
 m.set_params(init_flat_params([(n, s) for n, s, _ in m.layout()], seed=0).astype(np.float32))
 g = ctx.build_graph(b.atom_ptr, b.positions, b.lattice, b.species)
