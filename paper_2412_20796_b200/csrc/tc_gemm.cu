@@ -185,6 +185,8 @@ struct TcPlan {
   int nsa;           // A stages
   int bres;          // 1: the whole weight image is loaded once per CTA (no per-stage B traffic)
   int noconv;        // 1: A arrives TF32-rounded by TMA: no conversion pass, the MMA waits on the load
+  int lconv;         // 1: every A segment arrives by TMA and needs conversion: the weight warp issues
+                     //    the A boxes and warps 0-7 all convert (thread = row, half a row each)
   int split;         // 1: 3xTF32 (mlp_precision 1): operands split x = hi + lo (both TF32), three MMAs
                      //    A_lo·B_hi + A_hi·B_lo + A_hi·B_hi per K step; stages hold [hi | lo]
   int bf16;          // 1: BF16 operands (mlp_precision 3): stages hold [fp32 as loaded | bf16 copy
@@ -380,7 +382,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
   int nep = 0;
   if (TC_SKIP(32) && tid < 48) trace_ep[tid] = 0;
   if (tid == 0) {
-    for (int i = 0; i < NSA; ++i) { mbar_init(&fullA[i], 4); mbar_init(&emptyA[i], 1); mbar_init(&loaded[i], 128); }
+    for (int i = 0; i < NSA; ++i) {
+      mbar_init(&fullA[i], P.lconv ? 8 : 4);
+      mbar_init(&emptyA[i], 1);
+      mbar_init(&loaded[i], P.lconv ? 1 : 128);
+    }
     for (int i = 0; i < NSB; ++i) { mbar_init(&fullB[i], 1); mbar_init(&emptyB[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], NEPI); }
     for (int i = 0; i < 2 * NEPI; ++i) mbar_init(&ebar[i], 1);
@@ -401,7 +407,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
   const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   const int total = my_tiles * nkc;
 
-  if (warp < 4) {
+  if (warp < 4 && !P.lconv) {
     // ---------------- A loaders (4 warps): cp.async 16 B straight into the 128B-swizzled slots ----------------
     // A stage layout (SWIZZLE_128B, K-major): row r's 32 tf32 occupy bytes [r*128, r*128+128),
     // 16-B unit u stored at unit u ^ (r & 7).  Thread = (q: unit, rb); rows rb + 16 i.
@@ -470,16 +476,51 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
         trace_ld[gi] = t;
       }
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if (warp < 8) {
     // ---------------- A converters: thread = row; SiLU (GEMM2 input) + TF32 RN in place ----------------
-    const int r = tid - 128;
+    // warps 4-7 (the whole row), or warps 0-7 when every A box arrives by TMA (lconv: half a row
+    // each — two warps per SMSP share the latency-bound conversion)
+    const int r = tid & 127;
     const int sw = r & 7;
+    const int hb = P.lconv ? (tid >> 7) * 4 : 0;      // first logical 16-B unit of this thread's part
     for (int gi = 0; gi < (P.noconv ? 0 : total); ++gi) {
       const int sa = gi % NSA, ua = gi / NSA;
       mbar_wait(&loaded[sa], ua & 1);
       uint4 *row = (uint4 *)(sA + sa * a_stage + r * 128);
       uint4 *row_lo = (uint4 *)(sA + sa * a_stage + a_bytes + r * 128);
-      if (P.bf16) {
+      if (P.lconv) {
+        // logical units hb..hb+3 (physical u ^ sw): SiLU, then TF32 (hi | lo) in place or the BF16 copy
+        float4 v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = *(const float4 *)&row[(hb + k) ^ sw];
+        if (g.A.act == 1) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            v[k].x = silu_fast(v[k].x); v[k].y = silu_fast(v[k].y); v[k].z = silu_fast(v[k].z); v[k].w = silu_fast(v[k].w);
+          }
+        }
+        if (P.bf16) {
+          uint8_t *brow = sA + sa * a_stage + a_bytes + r * 64;
+#pragma unroll
+          for (int c2 = 0; c2 < 2; ++c2) {
+            const int c = (hb >> 1) + c2;
+            const float4 x = v[2 * c2], y = v[2 * c2 + 1];
+            *reinterpret_cast<uint4 *>(brow + ((c ^ ((r >> 1) & 3)) << 4)) =
+                make_uint4(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w), pack_bf16(y.x, y.y), pack_bf16(y.z, y.w));
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int pu = (hb + k) ^ sw;
+            const float4 x = v[k];
+            const uint4 h = make_uint4(to_tf32(x.x), to_tf32(x.y), to_tf32(x.z), to_tf32(x.w));
+            row[pu] = h;
+            if (P.split)
+              row_lo[pu] = make_uint4(to_tf32(x.x - __uint_as_float(h.x)), to_tf32(x.y - __uint_as_float(h.y)),
+                                      to_tf32(x.z - __uint_as_float(h.z)), to_tf32(x.w - __uint_as_float(h.w)));
+          }
+        }
+      } else if (P.bf16) {
         // logical 16-B unit u of the row sits at u ^ (r & 7); BF16 unit c (k = 8c..8c+7) of the
         // copy goes to row r of the SWIZZLE_64B region at c ^ ((r >> 1) & 3)
         float4 v[8];
@@ -524,8 +565,43 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
       }
     }
   } else if (warp == 8) {
-    // ---------------- B producer ----------------
-    if (lane == 0 && P.bres) {                          // whole image once: one barrier, nkc bulk copies
+    // ---------------- B producer (and, for lconv, the A TMA producer) ----------------
+    auto issue_a = [&](int gi) {                        // lconv: stage gi's A box by TMA (one thread)
+      const int tl = gi / nkc, kc = gi % nkc;
+      const int tile = blockIdx.x + tl * gridDim.x;
+      const int sa = gi % NSA, ua = gi / NSA;
+      if (ua > 0) mbar_wait(&emptyA[sa], (ua - 1) & 1);
+      const int col = P.lo + kc * KC;
+      int start = 0;
+      mbar_expect_tx(&loaded[sa], a_bytes);
+#pragma unroll
+      for (int sg = 0; sg < 4; ++sg) {
+        if (sg >= g.A.nseg) break;
+        const int w = g.A.seg[sg].width;
+        if (col >= start && col < start + w)
+          tma_load_2d(smem_u32(sA + sa * a_stage), &TM.m[sg], col - start, tile * TCM, &loaded[sa]);
+        start += w;
+      }
+    };
+    if (lane == 0 && P.lconv && P.bres) {               // resident image first, then the A stream
+      if (total > 0) {
+        mbar_expect_tx(&fullB[0], b_stage * nkc);
+        for (int kc = 0; kc < nkc; ++kc) {
+          bulk_g2s(sB + kc * b_stage, bimg + (size_t)kc * NT * KC, b_bytes, &fullB[0]);
+          if (P.split) bulk_g2s(sB + kc * b_stage + b_bytes, bimg_lo + (size_t)kc * NT * KC, b_bytes, &fullB[0]);
+        }
+      }
+      for (int gi = 0; gi < total; ++gi) issue_a(gi);
+    } else if (lane == 0 && P.lconv) {                  // A box and weight chunk of each stage in order
+      for (int gi = 0; gi < total; ++gi) {
+        issue_a(gi);
+        const int kc = gi % nkc, sb = gi % NSBr, ub = gi / NSBr;
+        if (ub > 0) mbar_wait(&emptyB[sb], (ub - 1) & 1);
+        mbar_expect_tx(&fullB[sb], b_stage);
+        bulk_g2s(sB + sb * b_stage, bimg + (size_t)kc * NT * KC, b_bytes, &fullB[sb]);
+        if (P.split) bulk_g2s(sB + sb * b_stage + b_bytes, bimg_lo + (size_t)kc * NT * KC, b_bytes, &fullB[sb]);
+      }
+    } else if (lane == 0 && P.bres) {                   // whole image once: one barrier, nkc bulk copies
       if (total > 0) {
         if TC_SKIP(4) {
           mbar_arrive(&fullB[0]);
@@ -1791,6 +1867,9 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   static const bool no_noconv = getenv("CHG_TC_NO_NOCONV") != nullptr;    // A/B knob
   P.noconv = g.A.rounded && g.A.act == 0 && !no_noconv && !split && !P.bf16;
   for (int s = 0; s < g.A.nseg; ++s) P.noconv &= TM.use[s];
+  static const bool no_lconv = getenv("CHG_TC_NO_LCONV") != nullptr;      // A/B knob
+  P.lconv = !P.noconv && !no_lconv && g.A.nseg > 0;
+  for (int s = 0; s < g.A.nseg; ++s) P.lconv &= TM.use[s];
   TM.nbuf = nbuf;
   for (int c = 0; c < g.nchunk && nbuf > 0; ++c) {
     const Chunk &C = g.ch[c];
@@ -1800,9 +1879,9 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   }
   static const bool verbose = getenv("CHG_TC_VERBOSE") != nullptr;
   if (verbose)
-    fprintf(stderr, "rowgemm_tc %s: M %d K %d nseg %d tma %d%d%d%d nsa %d bres %d tstore %d nst %d nbuf %d noconv %d smem %zu\n",
+    fprintf(stderr, "rowgemm_tc %s: M %d K %d nseg %d tma %d%d%d%d nsa %d bres %d tstore %d nst %d nbuf %d noconv %d lconv %d smem %zu\n",
             g.tag ? g.tag : "?", g.M, g.K, g.A.nseg, TM.use[0], TM.use[1], TM.use[2], TM.use[3], P.nsa, P.bres,
-            TM.tstore, TM.nst, nbuf, P.noconv, smem);
+            TM.tstore, TM.nst, nbuf, P.noconv, P.lconv, smem);
   launch_k(ctx, k_rowgemm_tc, grid, WS_THREADS, smem, ctx->stream, g, P, img, ntiles, skip, TM);
   check_launch(ctx);
   return true;

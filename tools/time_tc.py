@@ -12,7 +12,7 @@ TAGS = {"ac_f1", "ac_f2", "bc_f1", "bc_f2", "ac_dZ", "ac_dX", "bc_dZ", "bc_dX"}
 os.environ.setdefault("CHG_SERIAL", "1")
 b = make_config_batch(sys.argv[1] if len(sys.argv) > 1 else "C2")
 ctx = chg.Context(0)
-cfg = chg.default_model_cfg(); cfg.mlp_precision = 2
+cfg = chg.default_model_cfg(); cfg.mlp_precision = int(os.environ.get("CHG_PREC", "2"))
 m = chg.Model(ctx, cfg)
 m.set_params(init_flat_params([(n, s) for n, s, _ in m.layout()], seed=0).astype(np.float32))
 g = ctx.build_graph(b.atom_ptr, b.positions, b.lattice, b.species)
