@@ -371,6 +371,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
   float *stg0 = obuf0 + NEPI * TM.nbuf * 1024;          // TMA-store staging [8 warps][TM.nst][32 x 32]
   uint64_t *ebar = (uint64_t *)(stg0 + (TM.tstore ? NEPI * TM.nst * 1024 : 0));
   const uint32_t tcols = P.tmem_cols;                   // per accumulator buffer
+  __shared__ uint64_t tr_entry, tr_setup;               // debug trace: kernel entry, setup done
+  if (TC_SKIP(32) && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_entry));
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
@@ -395,6 +397,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (TC_SKIP(32) && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_setup));
   pdl_begin();                                    // the setup above overlaps the predecessor's tail
   const uint32_t tmem = *tslot;
   if (TC_SKIP(32) && tid == 0) {
@@ -926,7 +929,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
   if (TC_SKIP(32) && blockIdx.x == 0 && tid == 0) {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    printf("TRACE tiles %d nkc %d grid %d | start->chunk ends (us):", my_tiles, nkc, (int)gridDim.x);
+    printf("TRACE tiles %d nkc %d grid %d | entry->setup %.2f ->pdl %.2f | start->chunk ends (us):", my_tiles, nkc,
+           (int)gridDim.x, (tr_setup - tr_entry) * 1e-3, (trace_ts[0] - tr_setup) * 1e-3);
     for (int i = 1; i <= min(30, total); ++i) printf(" %.2f", (trace_ts[i] - trace_ts[0]) * 1e-3);
     printf(" | loader issued:");
     for (int i = 0; i < min(30, total); ++i) printf(" %.2f", (trace_ld[i] - trace_ts[0]) * 1e-3);
