@@ -95,7 +95,8 @@ void atom_conv_fwd(Fwd &F, int t, const float *v, const float *e, const float *e
   float *agg = F.buf("ac_agg_" + std::to_string(t), N, 64);
   float *msg = ctx->getf("msg_edge", std::max<int64_t>(E, 1) * 64);
   const float *W1c = m->p(pre + ".core.W1"), *W1g = m->p(pre + ".gate.W1");
-  {  // per atom: Pa = v · [W1c_i | W1g_i | W1c_j | W1g_j]  (rows 0..63: v_i part, 64..127: v_j part)
+  static const bool fact_full = getenv("CHG_FACT_FULL") != nullptr;   // A/B knob: both v parts as tables
+  if (fact_full) {  // per atom: Pa = v · [W1c_i | W1g_i | W1c_j | W1g_j]  (rows 0..63: v_i part, 64..127: v_j part)
     float *Pa = ctx->getf(ctx->ws_name("ac_P"), (size_t)std::max<int64_t>(N, 1) * 256);
     const float *Wi[4] = {W1c, W1g, W1c, W1g};
     const int ri[4] = {0, 0, 64, 64};
@@ -112,6 +113,30 @@ void atom_conv_fwd(Fwd &F, int t, const float *v, const float *e, const float *e
       C.gadd[0] = Pa + 64 * c; C.gidx[0] = g->center; C.ldga[0] = 256;
       C.gadd[1] = Pa + 128 + 64 * c; C.gidx[1] = g->nbr; C.ldga[1] = 256;
       C.ngadd = 2;
+    }
+    G.tag = "ac_f1";
+    rowgemm(ctx, G);
+  } else {  // per atom: Pa = v · [W1c_i | W1g_i] (the centre part: rows of one centre are contiguous
+            // in the CSR edge order, so the epilogue's gathered addition is an L1 broadcast)
+    float *Pa = ctx->getf(ctx->ws_name("ac_P"), (size_t)std::max<int64_t>(N, 1) * 128);
+    const float *Wi[2] = {W1c, W1g};
+    part_product(ctx, aseg(v, 64, 64), N, Wi, 2, 0, Pa, 128, "ac_P");
+    // per edge: z1 = [e | v_j] · [W1[128:192] ; W1[64:128]] + b1 + Pa[i]: the neighbour rows (random
+    // gathers) are A operand rows, loaded asynchronously by the loader warps
+    RowGemm G;
+    G.A.seg[0] = aseg(e, 64, 64);
+    G.A.seg[1] = aseg(v, 64, 64, g->nbr, N);
+    G.A.nseg = 2;
+    G.M = (int)E; G.K = 128; G.nchunk = 2; G.tc = 1;
+    const float *W1[2] = {W1c, W1g};
+    const float *b1[2] = {m->p(pre + ".core.b1"), m->p(pre + ".gate.b1")};
+    for (int c = 0; c < 2; ++c) {
+      Chunk &C = G.ch[c];
+      C = chunk1(W1[c] + 128 * 64, 64, 64, b1[c], z1 + 64 * c, 128);
+      C.W[1] = W1[c] + 64 * 64; C.ldw[1] = 64;
+      C.wk0[0] = 0; C.wk0[1] = 64; C.wk0[2] = 128; C.nwb = 2;
+      C.gadd[0] = Pa + 64 * c; C.gidx[0] = g->center; C.ldga[0] = 128;
+      C.ngadd = 1;
     }
     G.tag = "ac_f1";
     rowgemm(ctx, G);
@@ -172,19 +197,38 @@ void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float
     // Q1[b] = e_b·W[64:128] + Pv[centre of b]: the v_i part rides on the first bond (the angles
     // of a first bond are contiguous, so the per-angle GEMM gathers Q1 with L1 reuse)
     part_product(ctx, aseg(e, 64, 64, g->bond_edge, E), B, W, nw, 64, P1, ldP, "bc_P", nullptr, Pv, g->bond_ctr);
-    part_product(ctx, aseg(e, 64, 64, g->bond_edge, E), B, W, nw, 128, P2, ldP, "bc_P");
-    // per angle: [z1_bond | y_angle] = a·W[192:256] + b + Q1[b1] + P2[b2]
+    static const bool fact_full = getenv("CHG_FACT_FULL") != nullptr;   // A/B knob (atom_conv_fwd)
     RowGemm G;
-    G.A.seg[0] = aseg(a, 64, 64);
-    G.A.nseg = 1;
-    G.M = (int)A; G.K = 64; G.nchunk = nw; G.tc = 1;
-    for (int c = 0; c < nw; ++c) {
-      float *dst = c < 2 ? z1 + 64 * c : ya + 64 * (c - 2);
-      G.ch[c] = chunk1(W[c] + 192 * 64, 64, 64, bias[c], dst, 128);
-      Chunk &C = G.ch[c];
-      C.gadd[0] = P1 + 64 * c; C.gidx[0] = g->angle_b1; C.ldga[0] = ldP;
-      C.gadd[1] = P2 + 64 * c; C.gidx[1] = g->angle_b2; C.ldga[1] = ldP;
-      C.ngadd = 2;
+    if (fact_full) {
+      // per angle: [z1_bond | y_angle] = a·W[192:256] + b + Q1[b1] + P2[b2]
+      part_product(ctx, aseg(e, 64, 64, g->bond_edge, E), B, W, nw, 128, P2, ldP, "bc_P");
+      G.A.seg[0] = aseg(a, 64, 64);
+      G.A.nseg = 1;
+      G.M = (int)A; G.K = 64; G.nchunk = nw; G.tc = 1;
+      for (int c = 0; c < nw; ++c) {
+        float *dst = c < 2 ? z1 + 64 * c : ya + 64 * (c - 2);
+        G.ch[c] = chunk1(W[c] + 192 * 64, 64, 64, bias[c], dst, 128);
+        Chunk &C = G.ch[c];
+        C.gadd[0] = P1 + 64 * c; C.gidx[0] = g->angle_b1; C.ldga[0] = ldP;
+        C.gadd[1] = P2 + 64 * c; C.gidx[1] = g->angle_b2; C.ldga[1] = ldP;
+        C.ngadd = 2;
+      }
+    } else {
+      // per angle: [z1_bond | y_angle] = [a | e_ik] · [W[192:256] ; W[128:192]] + b + Q1[b1]: the
+      // second bond's edge rows (random gathers) are A operand rows, loaded by the loader warps
+      G.A.seg[0] = aseg(a, 64, 64);
+      G.A.seg[1] = aseg(e, 64, 64, g->angle_e2, E);
+      G.A.nseg = 2;
+      G.M = (int)A; G.K = 128; G.nchunk = nw; G.tc = 1;
+      for (int c = 0; c < nw; ++c) {
+        float *dst = c < 2 ? z1 + 64 * c : ya + 64 * (c - 2);
+        G.ch[c] = chunk1(W[c] + 192 * 64, 64, 64, bias[c], dst, 128);
+        Chunk &C = G.ch[c];
+        C.W[1] = W[c] + 128 * 64; C.ldw[1] = 64;
+        C.wk0[0] = 0; C.wk0[1] = 64; C.wk0[2] = 128; C.nwb = 2;
+        C.gadd[0] = P1 + 64 * c; C.gidx[0] = g->angle_b1; C.ldga[0] = ldP;
+        C.ngadd = 1;
+      }
     }
     G.tag = "bc_f1";
     rowgemm(ctx, G);

@@ -197,6 +197,11 @@ struct TcPlan {
   // columns per K chunk, chunk c at column bcoff[kc][c] (-1: not active in kc)
   int bnt;
   int16_t bcoff[16][4];
+  // column split of one-wave dense GEMMs (every chunk reads the same A window): CTA (tile =
+  // blockIdx.x, part = blockIdx.y) computes chunks [cs_c0, cs_c1) only — image columns
+  // [cs_n0, cs_n0 + cs_nt) — so small-M launches spread over more SMs with a smaller weight slice
+  int csplit;
+  int cs_c0[4], cs_c1[4], cs_n0[4], cs_nt[4];
 };
 
 // B image: img[kc][q][n][4] = tf32(W_chunk(n - bcoff[kc][c], k = lo + kc·KC - a_k0 + 4q + r))
@@ -349,12 +354,15 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
   // SWIZZLE_128B operand atoms need 1024-B aligned stage bases
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int NT = P.bnt;                                 // weight-image columns per K chunk
+  const int part = P.csplit > 1 ? (int)blockIdx.y : 0;
+  const int NTg = P.bnt;                                // weight-image columns per K chunk (global image)
+  const int NT = P.csplit > 1 ? P.cs_nt[part] : NTg;    // ... of this CTA's slice (shared memory)
+  const int cb0 = P.csplit > 1 ? P.cs_c0[part] : 0, cb1 = P.csplit > 1 ? P.cs_c1[part] : g.nchunk;
   const uint32_t a_bytes = KC * TCM * 4, b_bytes = P.bf16 ? KC * NT * 2 : KC * NT * 4;
   // [hi | lo] in split mode, [fp32 | bf16] in BF16 mode
   const uint32_t a_stage = P.bf16 ? a_bytes + a_bytes / 2 : a_bytes << P.split, b_stage = b_bytes << P.split;
   const int NSA = P.nsa, NSBr = P.nsb;
-  const uint32_t *bimg_lo = bimg + (size_t)(P.width / KC) * NT * KC;
+  const uint32_t *bimg_lo = bimg + (size_t)(P.width / KC) * NTg * KC;
   uint8_t *sA = smem;                                   // [NSA][a_stage]
   uint8_t *sB = smem + NSA * a_stage;                   // [P.bst][b_stage]
   uint64_t *fullA = (uint64_t *)(sB + P.bst * b_stage);
@@ -586,13 +594,26 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
         start += w;
       }
     };
+    // weight chunk kc -> dst (hi, then lo in split mode): one bulk copy, or under a column split
+    // the slice's columns, one copy per 16-B k group (image rows [kc][q][n] are column-contiguous)
+    auto load_b = [&](uint8_t *dst, int kc, uint64_t *bar) {
+      for (int h = 0; h <= P.split; ++h) {
+        const uint32_t *src = (h ? bimg_lo : bimg) + (size_t)kc * NTg * KC;
+        uint8_t *d = dst + h * b_bytes;
+        if (P.csplit <= 1) {
+          bulk_g2s(d, src, b_bytes, bar);
+        } else {
+          const int nq = P.bf16 ? KC / 8 : KC / 4;
+          for (int q = 0; q < nq; ++q)
+            bulk_g2s(d + q * NT * 16, reinterpret_cast<const uint8_t *>(src) + ((size_t)q * NTg + P.cs_n0[part]) * 16,
+                     NT * 16, bar);
+        }
+      }
+    };
     if (lane == 0 && P.lconv && P.bres) {               // resident image first, then the A stream
       if (total > 0) {
         mbar_expect_tx(&fullB[0], b_stage * nkc);
-        for (int kc = 0; kc < nkc; ++kc) {
-          bulk_g2s(sB + kc * b_stage, bimg + (size_t)kc * NT * KC, b_bytes, &fullB[0]);
-          if (P.split) bulk_g2s(sB + kc * b_stage + b_bytes, bimg_lo + (size_t)kc * NT * KC, b_bytes, &fullB[0]);
-        }
+        for (int kc = 0; kc < nkc; ++kc) load_b(sB + kc * b_stage, kc, &fullB[0]);
       }
       for (int gi = 0; gi < total; ++gi) issue_a(gi);
     } else if (lane == 0 && P.lconv) {                  // A box and weight chunk of each stage in order
@@ -601,8 +622,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
         const int kc = gi % nkc, sb = gi % NSBr, ub = gi / NSBr;
         if (ub > 0) mbar_wait(&emptyB[sb], (ub - 1) & 1);
         mbar_expect_tx(&fullB[sb], b_stage);
-        bulk_g2s(sB + sb * b_stage, bimg + (size_t)kc * NT * KC, b_bytes, &fullB[sb]);
-        if (P.split) bulk_g2s(sB + sb * b_stage + b_bytes, bimg_lo + (size_t)kc * NT * KC, b_bytes, &fullB[sb]);
+        load_b(sB + sb * b_stage, kc, &fullB[sb]);
       }
     } else if (lane == 0 && P.bres) {                   // whole image once: one barrier, nkc bulk copies
       if (total > 0) {
@@ -610,10 +630,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
           mbar_arrive(&fullB[0]);
         } else {
           mbar_expect_tx(&fullB[0], b_stage * nkc);
-          for (int kc = 0; kc < nkc; ++kc) {
-            bulk_g2s(sB + kc * b_stage, bimg + (size_t)kc * NT * KC, b_bytes, &fullB[0]);
-            if (P.split) bulk_g2s(sB + kc * b_stage + b_bytes, bimg_lo + (size_t)kc * NT * KC, b_bytes, &fullB[0]);
-          }
+          for (int kc = 0; kc < nkc; ++kc) load_b(sB + kc * b_stage, kc, &fullB[0]);
         }
       }
     } else if (lane == 0) {
@@ -624,8 +641,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
           mbar_arrive(&fullB[sb]);
         } else {
           mbar_expect_tx(&fullB[sb], b_stage);
-          bulk_g2s(sB + sb * b_stage, bimg + (size_t)kc * NT * KC, b_bytes, &fullB[sb]);
-          if (P.split) bulk_g2s(sB + sb * b_stage + b_bytes, bimg_lo + (size_t)kc * NT * KC, b_bytes, &fullB[sb]);
+          load_b(sB + sb * b_stage, kc, &fullB[sb]);
         }
       }
     }
@@ -651,34 +667,38 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t a_base = smem_u32(sA + sa * a_stage), b_base = smem_u32(sB + sb * b_stage);
           const int col0 = P.lo + kc * KC;
-          for (int gr = 0; gr < P.ngrp; ++gr) {
-            const int c = P.gfirst[gr];
+          // MMA groups; under a column split one group: this CTA's chunks, N = its slice width
+          const int ngr = P.csplit > 1 ? 1 : P.ngrp;
+          for (int gr = 0; gr < ngr; ++gr) {
+            const int c = P.csplit > 1 ? cb0 : P.gfirst[gr];
+            const int gnv = P.csplit > 1 ? NT : P.gn[gr];
+            const int boff = P.csplit > 1 ? 0 : P.bcoff[kc][c];
             const int kk = col0 - g.ch[c].a_k0;
             if (kk < 0 || kk >= g.K) continue;
             if (P.bf16) {                                 // BF16: K = 16 per MMA, A from the SWIZZLE_64B copy
-              const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(P.gn[gr] >> 3) << 17) |
+              const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(gnv >> 3) << 17) |
                                      ((uint32_t)(TCM >> 4) << 24);
 #pragma unroll
               for (int j = 0; j < KC / 16; ++j) {
                 const uint64_t ad = make_desc(a_base + a_bytes + j * 32, 16, 512) | ((uint64_t)4 << 61);   // SWIZZLE_64B
-                const uint64_t bd = make_desc(b_base + j * 2 * (NT * 16) + P.bcoff[kc][c] * 16, NT * 16, 128);
+                const uint64_t bd = make_desc(b_base + j * 2 * (NT * 16) + boff * 16, NT * 16, 128);
                 if (TC_SKIP(8)) continue;
                 mma_bf16(tmem + a * tcols + P.coff[c], ad, bd, idesc, (started[gr] || j > 0) ? 1u : 0u);
               }
               started[gr] = true;
               continue;
             }
-            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(P.gn[gr] >> 3) << 17) |
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(gnv >> 3) << 17) |
                                    ((uint32_t)(TCM >> 4) << 24);
 #pragma unroll
             for (int j = 0; j < KC / 8; ++j) {
               uint64_t ad = make_desc(a_base + j * 32, 16, 1024) | ((uint64_t)2 << 61);   // SWIZZLE_128B
-              uint64_t bd = make_desc(b_base + j * 2 * (NT * 16) + P.bcoff[kc][c] * 16, NT * 16, 128);
+              uint64_t bd = make_desc(b_base + j * 2 * (NT * 16) + boff * 16, NT * 16, 128);
               const uint32_t acc = (started[gr] || j > 0) ? 1u : 0u;
               if (TC_SKIP(8)) continue;                   // debug: no tensor-core work
               if (P.split) {                              // 3xTF32: small terms first, then hi·hi
                 const uint64_t ad_lo = make_desc(a_base + a_bytes + j * 32, 16, 1024) | ((uint64_t)2 << 61);
-                const uint64_t bd_lo = make_desc(b_base + b_bytes + j * 2 * (NT * 16) + P.bcoff[kc][c] * 16, NT * 16, 128);
+                const uint64_t bd_lo = make_desc(b_base + b_bytes + j * 2 * (NT * 16) + boff * 16, NT * 16, 128);
                 mma_tf32(tmem + a * tcols + P.coff[c], ad_lo, bd, idesc, acc);
                 mma_tf32(tmem + a * tcols + P.coff[c], ad, bd_lo, idesc, 1u);
                 mma_tf32(tmem + a * tcols + P.coff[c], ad, bd, idesc, 1u);
@@ -714,7 +734,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
     int nmy = 0, mc[8], mj[8];
     {
       int blk = 0;
-      for (int c = 0; c < g.nchunk; ++c)
+      for (int c = cb0; c < cb1; ++c)
         for (int j0 = 0; j0 < P.cpad[c]; j0 += 32, ++blk)
           if ((blk & 1) == half && nmy < 8) { mc[nmy] = c; mj[nmy] = j0; ++nmy; }
     }
@@ -1748,7 +1768,36 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
     }
   }
   const int nkc = P.width / KC;
-  const size_t bchunk = P.bf16 ? (size_t)KC * P.bnt * 2 : ((size_t)KC * P.bnt * 4) << split;
+  // column split (one-wave, dense: one MMA group, every chunk active in every K chunk): parts of
+  // whole chunks on blockIdx.y, as many as fit one wave (<= 4)
+  P.csplit = 1;
+  static const bool no_csplit = getenv("CHG_TC_NO_CSPLIT") != nullptr;   // A/B knob
+  {
+    const int ntl = ceil_div(g.M, TCM), sms = device_sm_count();
+    bool dense = P.ngrp == 1 && g.nchunk >= 2 && !no_csplit;
+    for (int kc = 0; kc < nkc && dense; ++kc)
+      for (int c = 0; c < g.nchunk; ++c) dense &= P.bcoff[kc][c] == P.bcoff[0][c] && P.bcoff[kc][c] >= 0;
+    int G = 1;
+    while (dense && G * 2 <= g.nchunk && g.nchunk % (G * 2) == 0 && ntl * G * 2 <= sms) G *= 2;
+    if (G > 1) {
+      P.csplit = G;
+      const int per = g.nchunk / G;
+      for (int y = 0; y < G; ++y) {
+        P.cs_c0[y] = y * per;
+        P.cs_c1[y] = (y + 1) * per;
+        P.cs_n0[y] = P.bcoff[0][y * per];
+        int w = 0;
+        for (int c = y * per; c < (y + 1) * per; ++c) w += (g.ch[c].ncols + 31) / 32 * 32;
+        P.cs_nt[y] = w;
+      }
+    }
+  }
+  int bnt_s = P.bnt;                                  // weight-image columns per CTA in shared memory
+  if (P.csplit > 1) {
+    bnt_s = 0;
+    for (int y = 0; y < P.csplit; ++y) bnt_s = std::max(bnt_s, P.cs_nt[y]);
+  }
+  const size_t bchunk = P.bf16 ? (size_t)KC * bnt_s * 2 : ((size_t)KC * bnt_s * 4) << split;
   const size_t achunk = P.bf16 ? (size_t)KC * TCM * 6 : ((size_t)KC * TCM * 4) << split;
   const int nsa_min = split ? (one_wave ? 1 : 2) : 4;
   // TMA-store epilogue (lane = row) when every chunk's output is a plain [M][32k] table
@@ -1883,10 +1932,10 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   }
   static const bool verbose = getenv("CHG_TC_VERBOSE") != nullptr;
   if (verbose)
-    fprintf(stderr, "rowgemm_tc %s: M %d K %d nseg %d tma %d%d%d%d nsa %d bres %d tstore %d nst %d nbuf %d noconv %d lconv %d smem %zu\n",
+    fprintf(stderr, "rowgemm_tc %s: M %d K %d nseg %d tma %d%d%d%d nsa %d bres %d tstore %d nst %d nbuf %d noconv %d lconv %d csplit %d smem %zu\n",
             g.tag ? g.tag : "?", g.M, g.K, g.A.nseg, TM.use[0], TM.use[1], TM.use[2], TM.use[3], P.nsa, P.bres,
-            TM.tstore, TM.nst, nbuf, P.noconv, P.lconv, smem);
-  launch_k(ctx, k_rowgemm_tc, grid, WS_THREADS, smem, ctx->stream, g, P, img, ntiles, skip, TM);
+            TM.tstore, TM.nst, nbuf, P.noconv, P.lconv, P.csplit, smem);
+  launch_k(ctx, k_rowgemm_tc, dim3(grid, P.csplit), WS_THREADS, smem, ctx->stream, g, P, img, ntiles, skip, TM);
   check_launch(ctx);
   return true;
 }
