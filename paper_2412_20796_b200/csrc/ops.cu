@@ -645,7 +645,8 @@ void gate_fwd(chg_ctx *ctx, int64_t rows, const float *y, int ldy, GateLN ln, in
               const int32_t *i1, const int32_t *i2, const float *resid, float *out) {
   if (rows <= 0) return;
   ProfScope ps(ctx, "gate_fwd", 0.0, rows * (512.0 + 256.0 + (mode == GATE_MUL_W1W2 ? 520.0 : 256.0)));
-  const int grid = (int)std::min<int64_t>(ceil_div(rows * 16, 256), 148 * 8);   // 2 rows per warp, grid-stride
+  static const int bps = getenv("CHG_GATEF_BPS") ? atoi(getenv("CHG_GATEF_BPS")) : 3;   // A/B knob: blocks per SM (80 registers: 3 resident)
+  const int grid = (int)std::min<int64_t>(ceil_div(rows * 16, 256), (int64_t)device_sm_count() * bps);   // 2 rows per warp, grid-stride
   launch_k(ctx, k_gate_fwd, grid, 256, 0, ctx->stream, rows, y, ldy, ln, mode, w, i1, i2, resid, out);
   check_launch(ctx);
 }
@@ -653,7 +654,10 @@ void gate_fwd(chg_ctx *ctx, int64_t rows, const float *y, int ldy, GateLN ln, in
 void gate_bwd(chg_ctx *ctx, int64_t rows, const float *y, int ldy, GateLN ln, int mode, const float *w,
               const int32_t *i1, const int32_t *i2, const float *dout, const int32_t *didx, float *dy, int lddy,
               float *dw_acc, float *q1, float *q2, GateLNGrad g) {
-  int64_t rpb = std::max<int64_t>(64, (rows + 591) / 592);
+  // one wave: 2 blocks per SM (128 registers -> 2 resident; A/B knob CHG_GATE_BPS)
+  static const int bps = getenv("CHG_GATE_BPS") ? atoi(getenv("CHG_GATE_BPS")) : 2;
+  const int64_t nbt = (int64_t)device_sm_count() * bps;
+  int64_t rpb = std::max<int64_t>(64, (rows + nbt - 1) / nbt);
   int nb = rows > 0 ? ceil_div(rows, rpb) : 0;
   if (nb == 0) return;
   float *part = red_partial(ctx, (size_t)nb * 256);
