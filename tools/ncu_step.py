@@ -11,7 +11,7 @@ from chg_inputs import init_flat_params, make_config_batch
 from paper_2412_20796_b200 import chg
 
 cfgname = sys.argv[1] if len(sys.argv) > 1 else "C2"
-prec = {"tf32": 2, "3xtf32": 1, "fp32": 0}[sys.argv[2] if len(sys.argv) > 2 else "tf32"]
+prec = {"tf32": 2, "3xtf32": 1, "fp32": 0, "bf16": 3}[sys.argv[2] if len(sys.argv) > 2 else "tf32"]
 b = make_config_batch(cfgname)
 ctx = chg.Context(0)
 cfg = chg.default_model_cfg(); cfg.mlp_precision = prec
