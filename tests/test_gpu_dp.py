@@ -1,7 +1,7 @@
 """Multi-GPU data parallelism through the C ABI (needs >= 2 GPUs; skipped otherwise).
 
 Runs tools/dp_check.py under torchrun: balanced shards, global loss normalisers and the
-library's NCCL allreduce reproduce the one-GPU full-batch gradient (fp32 1e-4, tf32 2e-3),
+library's NCCL allreduce reproduce the one-GPU full-batch gradient (fp32 / 3xTF32 1e-4, TF32 / BF16 2e-3),
 and every rank holds bit-identical parameters after the Adam step.
 """
 import json
@@ -24,7 +24,7 @@ def _ngpu():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("overlap", [False, True])
-@pytest.mark.parametrize("prec", [0, 1, 2])
+@pytest.mark.parametrize("prec", [0, 1, 2, 3])
 def test_dp_allreduce_matches_single_gpu(prec, overlap):
     n = _ngpu()
     if n < 2:

@@ -67,7 +67,7 @@ def main():
         mom1 = m1.get(2).astype(np.float64) / 0.1
         rel = float(np.linalg.norm(mom - mom1) / np.linalg.norm(mom1))
         lrel = float(abs(lt[0].item() - loss1[0]) / abs(loss1[0]))
-        tol = 2e-3 if prec == 2 else 1e-4
+        tol = 2e-3 if prec in (2, 3) else 1e-4   # TF32 / BF16: NS-loosened bar
         ok = identical and rel <= tol and lrel <= 1e-5
         print(json.dumps({"world_size": ws, "mlp_precision": prec, "grad_overlap": overlap, "structures": glob.n_struct,
                           "per_rank_structures": np.bincount(rank_of, minlength=ws).tolist(),
