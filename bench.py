@@ -563,18 +563,21 @@ def main():
         # forces on device, kick), device-timed, for the C5 cell and an 8-atom cell (Table II size)
         from paper_2412_20796_b200.md import NVE, maxwell_boltzmann
 
-        def md_ms(b, mass):
+        def md_ms(b, mass, per=1, **kw):
+            """median device ms per MD step; per steps per timed call (captured: one chunk of
+            replays between two moved-atom checks)"""
             md = NVE(ctx, model5, b.atom_ptr, b.positions, b.lattice, b.species, mass,
-                     maxwell_boltzmann(mass, 300.0, 0), dt_fs=0.5)
-            md.step(a.warmup)
+                     maxwell_boltzmann(mass, 300.0, 0), dt_fs=0.5, **kw)
+            md.step(max(a.warmup, per))
             evm = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
             barrier()
             for k in range(a.steps):
                 evm[k][0].record(stream)
-                md.step(1)
+                md.step(per)
                 evm[k][1].record(stream)
             barrier()
-            tm = sorted(s.elapsed_time(e) for s, e in evm)
+            tm = sorted(s.elapsed_time(e) / per for s, e in evm)
+            md.close()
             return tm[len(tm) // 2]
         b8 = make_config_batch("C1")
         c5 = {"workload": "C5: one 4,096-atom LiFePO4-like cell (graph build + forward + force/stress readout)",
@@ -584,6 +587,12 @@ def main():
                                    "(includes the host copy of the outputs)",
               "md_step_ms_median": {"C5_4096_atoms": md_ms(b5, np.full(b5.n_atoms, 30.0)),
                                     "C1_Si8": md_ms(b8, np.full(b8.n_atoms, 28.0855))},
+              "md_step_ms_median_captured": {
+                  "C5_4096_atoms": md_ms(b5, np.full(b5.n_atoms, 30.0), per=10, skin=1.0, captured=True),
+                  "C1_Si8": md_ms(b8, np.full(b8.n_atoms, 28.0855), per=10, skin=1.0, captured=True)},
+              "md_captured_note": "skin graph (lists r + 1 Å, bases zero beyond r) refreshed every step; "
+                                  "the step (kick+drift, geometry refresh, conservative forces, kick) replayed "
+                                  "as one CUDA graph, 10 replays between moved-atom checks",
               "md_note": "NEXT-2 velocity-Verlet NVE step: chg_md_verlet kick+drift, graph rebuild from device "
                          "positions, chg_forward_conservative (device outputs), kick; dt 0.5 fs"}
 

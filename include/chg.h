@@ -217,6 +217,41 @@ chg_status chg_forward_conservative(chg_ctx *ctx, chg_model *m, chg_graph *g, ch
 chg_status chg_md_verlet(chg_ctx *ctx, int64_t n_atoms, double *positions, double *velocities, const float *forces,
                          const double *inv_mass, double dt_fs, int drift);
 
+/* Fixed-topology (Verlet skin) graphs, so that an MD step has constant sizes and can be
+ * captured.  chg_build_graph_skin builds the lists of chg_build_graph with the LIST cutoffs
+ * r_atom + skin and r_bond + skin while the model keeps r_atom / r_bond: the radial bases
+ * and their envelope u(r / r_c) are exactly zero for r >= r_c (u(1) = u'(1) = u''(1) = 0,
+ * reading Q2), so the extra pairs carry zero messages (Eq. 4 / 5 are products with eᵃ, eᵇ) and
+ * the energy and conservative forces equal those of the exact lists (summation order aside)
+ * for as long as no atom has moved more than skin / 2 since the build.  Same arguments and
+ * errors as chg_build_graph plus 0 <= skin < r_atom (CHG_ERR_ARG).
+ * chg_graph_refresh recomputes every edge's geometry of such a graph from new positions
+ * (DEVICE fp64 [N*3], same atom order) by the build's canonical fp64 evaluation; the lists,
+ * bond flags and angles stay those of the build.  flag (DEVICE int32, may be NULL) is set to 1
+ * — never cleared — when an atom moved more than skin / 2 since the build: rebuild then.
+ * Enqueued on the ctx stream, no host synchronisation. */
+chg_status chg_build_graph_skin(chg_ctx *ctx, int32_t n_struct, const int64_t *atom_ptr,
+                                const double *positions, const double *lattice,
+                                const int32_t *species, chg_cutoffs cutoffs, double skin,
+                                int inputs_on_device, chg_graph **out);
+chg_status chg_graph_refresh(chg_ctx *ctx, chg_graph *g, const double *positions, int32_t *flag);
+
+/* Captured MD step: chg_md_capture records one velocity-Verlet step on a
+ * skin graph — kick + drift (chg_md_verlet drift = 1), chg_graph_refresh(positions, flag),
+ * chg_forward_conservative into out (DEVICE pointers, on_device = 1; out->forces required) and
+ * the closing kick — as one CUDA graph; it first runs chg_forward_conservative once (sizing the
+ * workspaces; out then holds the forces of the current positions, as the first kick needs).
+ * chg_md_run replays it n_steps times on the ctx stream (no host work per step).  All
+ * pointers must stay valid while the exec is used; it is bound to (ctx, model, g) and becomes
+ * invalid (CHG_ERR_STATE) when a ctx workspace was re-allocated after the capture.  The caller
+ * checks flag between runs (it only grows) and rebuilds the graph and the exec when it is set. */
+typedef struct chg_md_exec chg_md_exec;
+chg_status chg_md_capture(chg_ctx *ctx, chg_model *m, chg_graph *g, double *positions, double *velocities,
+                          const double *inv_mass, double dt_fs, const chg_pred *out, int32_t *flag,
+                          chg_md_exec **exec);
+chg_status chg_md_run(chg_ctx *ctx, chg_md_exec *x, int n_steps);
+void chg_md_exec_destroy(chg_md_exec *x);
+
 /* ---- A7-A8 loss + backward (first-order only) ---------
  * Computes the Huber loss of the last train-mode forward and ACCUMULATES
  * dL/dθ into the model's gradient vector.  loss_out (host, optional) =

@@ -65,7 +65,8 @@ SYMBOLS = ["chg_ctx_create", "chg_ctx_destroy", "chg_last_error", "chg_sync", "c
            "chg_model_num_params", "chg_model_set", "chg_model_get", "chg_model_device_ptr", "chg_forward",
            "chg_forward_conservative",
            "chg_backward", "chg_step", "chg_balance", "chg_profile", "chg_profile_query", "chg_debug_gemm", "chg_debug_get",
-           "chg_capture_step", "chg_exec_step", "chg_exec_destroy", "chg_ctx_set_grad_overlap"]
+           "chg_capture_step", "chg_exec_step", "chg_exec_destroy", "chg_ctx_set_grad_overlap",
+           "chg_build_graph_skin", "chg_graph_refresh", "chg_md_capture", "chg_md_run", "chg_md_exec_destroy"]
 
 _lib = None
 
@@ -115,6 +116,11 @@ def load(path: str = LIB_PATH):
         "chg_exec_step": (C.c_int, [vp, vp, C.POINTER(AdamCfg)]),
         "chg_exec_destroy": (None, [vp]),
         "chg_ctx_set_grad_overlap": (C.c_int, [vp, C.c_int]),
+        "chg_build_graph_skin": (C.c_int, [vp, i32, vp, vp, vp, vp, Cutoffs, C.c_double, C.c_int, C.POINTER(vp)]),
+        "chg_graph_refresh": (C.c_int, [vp, vp, vp, vp]),
+        "chg_md_capture": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_double, C.POINTER(Pred), vp, C.POINTER(vp)]),
+        "chg_md_run": (C.c_int, [vp, vp, C.c_int]),
+        "chg_md_exec_destroy": (None, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -207,7 +213,10 @@ class Context:
         self._check(self.lib.chg_md_verlet(self.h, n, _ptr(positions), _ptr(velocities), _ptr(forces), _ptr(inv_mass),
                                            float(dt_fs), int(bool(drift))))
 
-    def build_graph(self, atom_ptr, positions, lattice, species, r_atom: float = 5.0, r_bond: float = 3.0) -> "Graph":
+    def build_graph(self, atom_ptr, positions, lattice, species, r_atom: float = 5.0, r_bond: float = 3.0,
+                    skin: float = 0.0) -> "Graph":
+        """chg_build_graph; skin > 0: chg_build_graph_skin (lists with r + skin, model cutoffs r:
+        a fixed-topology graph for chg_graph_refresh / captured MD steps)."""
         ap = np.ascontiguousarray(np.asarray(atom_ptr, np.int64))
         dev = _on_device(positions)
         if not dev:
@@ -215,9 +224,30 @@ class Context:
             lattice = np.ascontiguousarray(np.asarray(lattice, np.float64))
             species = np.ascontiguousarray(np.asarray(species, np.int32))
         h = C.c_void_p()
-        self._check(self.lib.chg_build_graph(self.h, ap.shape[0] - 1, _ptr(ap), _ptr(positions), _ptr(lattice),
-                                             _ptr(species), Cutoffs(r_atom, r_bond), int(dev), C.byref(h)))
+        if skin > 0:
+            self._check(self.lib.chg_build_graph_skin(self.h, ap.shape[0] - 1, _ptr(ap), _ptr(positions),
+                                                      _ptr(lattice), _ptr(species), Cutoffs(r_atom, r_bond),
+                                                      float(skin), int(dev), C.byref(h)))
+        else:
+            self._check(self.lib.chg_build_graph(self.h, ap.shape[0] - 1, _ptr(ap), _ptr(positions), _ptr(lattice),
+                                                 _ptr(species), Cutoffs(r_atom, r_bond), int(dev), C.byref(h)))
         return Graph(self, h, ap.shape[0] - 1)
+
+    def refresh_graph(self, graph: "Graph", positions, flag=None):
+        """chg_graph_refresh: the skin graph's edge geometry from new DEVICE positions; flag (device
+        int32 tensor, optional) is set to 1 when an atom moved more than skin / 2 since the build."""
+        self._check(self.lib.chg_graph_refresh(self.h, graph.h, _ptr(positions), _ptr(flag)))
+
+    def md_capture(self, model: "Model", graph: "Graph", positions, velocities, inv_mass, dt_fs: float, out: Dict,
+                   flag=None) -> "MDExec":
+        """chg_md_capture: one velocity-Verlet step on a skin graph (kick + drift, geometry refresh,
+        conservative forces into `out` — dict of device tensors, forces required — kick) as a CUDA
+        graph; .run(n) replays it."""
+        p = Pred(*(_ptr(out.get(k)) for k in ("energy", "energy_per_atom", "forces", "stress", "magmom")), 1)
+        h = C.c_void_p()
+        self._check(self.lib.chg_md_capture(self.h, model.h, graph.h, _ptr(positions), _ptr(velocities),
+                                            _ptr(inv_mass), float(dt_fs), C.byref(p), _ptr(flag), C.byref(h)))
+        return MDExec(self, h, (positions, velocities, inv_mass, out, flag, graph, model))
 
     # ---- compute
     def forward(self, model: "Model", graph: "Graph", train: bool = True, out: Optional[Dict] = None,
@@ -371,6 +401,27 @@ class Graph:
         if getattr(self, "h", None) and getattr(self.ctx, "h", None):
             self.ctx.lib.chg_graph_destroy(self.h)
         self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class MDExec:
+    """A captured MD step (chg_md_exec); .run(n) replays it n times on the ctx stream."""
+
+    def __init__(self, ctx: "Context", h, keep):
+        self.ctx, self.h, self._keep = ctx, h, keep
+
+    def run(self, n: int = 1):
+        self.ctx._check(self.ctx.lib.chg_md_run(self.ctx.h, self.h, int(n)))
+
+    def close(self):
+        if self.h:
+            self.ctx.lib.chg_md_exec_destroy(self.h)
+            self.h = None
 
     def __del__(self):
         try:

@@ -15,6 +15,7 @@
 void destroy_graph_impl(chg_graph *G);
 void graph_fill_counts(chg_graph *G);
 void derivative_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, chg_pred *out);
+extern "C" void graph_use(chg_ctx *ctx, chg_graph *g);
 void md_verlet(chg_ctx *ctx, int64_t n, double *pos, double *vel, const float *F, const double *inv_mass, double dt,
                int drift);
 
@@ -262,6 +263,26 @@ chg_status chg_build_graph(chg_ctx *ctx, int32_t n_struct, const int64_t *atom_p
     CUDA_OK(cudaSetDevice(ctx->device));
     *out = build_graph_impl(ctx, n_struct, atom_ptr, positions, lattice, species, cutoffs.r_atom,
                             cutoffs.r_bond, inputs_on_device, 94);
+  });
+}
+
+chg_status chg_build_graph_skin(chg_ctx *ctx, int32_t n_struct, const int64_t *atom_ptr, const double *positions,
+                                const double *lattice, const int32_t *species, chg_cutoffs cutoffs, double skin,
+                                int inputs_on_device, chg_graph **out) {
+  if (!ctx || !out) return CHG_ERR_ARG;
+  ABI_GUARD(ctx, {
+    CUDA_OK(cudaSetDevice(ctx->device));
+    *out = build_graph_impl(ctx, n_struct, atom_ptr, positions, lattice, species, cutoffs.r_atom,
+                            cutoffs.r_bond, inputs_on_device, 94, skin);
+  });
+}
+
+chg_status chg_graph_refresh(chg_ctx *ctx, chg_graph *g, const double *positions, int32_t *flag) {
+  if (!ctx || !g || (g->N > 0 && !positions)) return CHG_ERR_ARG;
+  ABI_GUARD(ctx, {
+    CUDA_OK(cudaSetDevice(ctx->device));
+    graph_use(ctx, g);
+    graph_refresh(ctx, g, positions, flag);
   });
 }
 

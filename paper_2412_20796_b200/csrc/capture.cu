@@ -12,6 +12,7 @@
 #include "ops.cuh"
 
 extern "C" void graph_use(chg_ctx *ctx, chg_graph *g);   // abi.cu
+void derivative_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, chg_pred *out);   // model.cu
 
 struct chg_exec {
   chg_ctx *ctx = nullptr;
@@ -136,6 +137,88 @@ chg_status chg_exec_step(chg_ctx *ctx, chg_exec *x, const chg_adam_cfg *adam) {
     ctx->err = e.msg;
     return e.code;
   }
+}
+
+// ---------------------------------------------------------------------------
+// captured MD step (skin graph): kick + drift, geometry refresh, conservative forces, kick
+// ---------------------------------------------------------------------------
+struct chg_md_exec {
+  chg_ctx *ctx = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  uint64_t ws_gen = 0;
+  int64_t launches = 0;
+};
+
+chg_status chg_md_capture(chg_ctx *ctx, chg_model *m, chg_graph *g, double *pos, double *vel, const double *inv_mass,
+                          double dt, const chg_pred *out, int32_t *flag, chg_md_exec **xo) {
+  if (!ctx || !m || !g || !out || !xo || (g->N > 0 && (!pos || !vel || !inv_mass || !out->forces))) return CHG_ERR_ARG;
+  if (m->ctx != ctx) { ctx->err = "model bound to another ctx"; return CHG_ERR_ARG; }
+  if (!out->on_device) { ctx->err = "chg_md_capture needs device outputs (on_device = 1)"; return CHG_ERR_ARG; }
+  chg_md_exec *x = new chg_md_exec();
+  bool began = false;
+  try {
+    CUDA_OK(cudaSetDevice(ctx->device));
+    graph_use(ctx, g);
+    chg_pred o = *out;
+    // one real pass: sizes every workspace / weight image, and out->forces = F(current positions)
+    derivative_impl(ctx, m, g, &o);
+    if (ctx->use_tc) tc_repack_all(ctx, m);
+    CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    x->ctx = ctx;
+    const int64_t l0 = ctx->launches;
+    cudaGetLastError();
+    CUDA_OK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    began = true;
+    ctx->capturing = true;
+    md_verlet(ctx, g->N, pos, vel, out->forces, inv_mass, dt, 1);
+    graph_refresh(ctx, g, pos, flag);
+    derivative_impl(ctx, m, g, &o);
+    md_verlet(ctx, g->N, pos, vel, out->forces, inv_mass, dt, 0);
+    ctx->capturing = false;
+    began = false;
+    CUDA_OK(cudaStreamEndCapture(ctx->stream, &x->graph));
+    x->launches = ctx->launches - l0;
+    ctx->launches = l0;
+    CUDA_OK(cudaGraphInstantiate(&x->exec, x->graph, 0));
+    x->ws_gen = ctx->ws_gen;
+    *xo = x;
+    return CHG_OK;
+  } catch (const ChgError &e) {
+    ctx->capturing = false;
+    if (began) {
+      cudaGraph_t junk = nullptr;
+      cudaStreamEndCapture(ctx->stream, &junk);
+      if (junk) cudaGraphDestroy(junk);
+    }
+    cudaGetLastError();
+    ctx->err = e.msg;
+    chg_md_exec_destroy(x);
+    return e.code;
+  }
+}
+
+chg_status chg_md_run(chg_ctx *ctx, chg_md_exec *x, int n_steps) {
+  if (!ctx || !x || x->ctx != ctx || n_steps < 0) return CHG_ERR_ARG;
+  try {
+    CUDA_OK(cudaSetDevice(ctx->device));
+    if (x->ws_gen != ctx->ws_gen)
+      CHG_THROW(CHG_ERR_STATE, "a ctx workspace was re-allocated after this MD step was captured: capture again");
+    for (int k = 0; k < n_steps; ++k) CUDA_OK(cudaGraphLaunch(x->exec, ctx->stream));
+    ctx->launches += x->launches * n_steps;
+    return CHG_OK;
+  } catch (const ChgError &e) {
+    ctx->err = e.msg;
+    return e.code;
+  }
+}
+
+void chg_md_exec_destroy(chg_md_exec *x) {
+  if (!x) return;
+  if (x->ctx) cudaStreamSynchronize(x->ctx->stream);
+  if (x->exec) cudaGraphExecDestroy(x->exec);
+  if (x->graph) cudaGraphDestroy(x->graph);
+  delete x;
 }
 
 void chg_exec_destroy(chg_exec *x) {

@@ -157,7 +157,13 @@ struct chg_graph {
   uint64_t id = 0;
   int S = 0;
   int64_t N = 0, E = 0, B = 0, A = 0;
-  double r_atom = 5.0, r_bond = 3.0;
+  double r_atom = 5.0, r_bond = 3.0;   // model cutoffs (bases and envelopes)
+  // fixed-topology (Verlet skin) graphs for captured MD steps: lists built with r + skin,
+  // geometry refreshed from new positions by graph_refresh (pos0: positions at the build,
+  // geo_dev: the per-structure lattice / inverse table of the build)
+  double skin = 0.0;
+  double *pos0 = nullptr;
+  void *geo_dev = nullptr;
   std::vector<int64_t> atom_ptr_h;     // [S+1]
   std::vector<int64_t> counts_h;       // [S*4] N,E,B,A (filled on demand: graph_fill_counts)
   bool counts_ready = false;
@@ -333,6 +339,9 @@ void backward_impl(chg_ctx *ctx, chg_model *m, chg_graph *g, const chg_labels *l
                    double *loss_out);
 void step_impl(chg_ctx *ctx, chg_model *m, const chg_adam_cfg *cfg, int flag_slot /* -1: next free */);
 void check_pending(chg_ctx *ctx, bool block);       // deferred finite checks (CHG_ERR_NONFINITE)
+// graph.cu: recompute every edge's geometry of a skin graph from positions (device); flag
+// (device int32, may be null) <- 1 when an atom moved more than skin / 2 since the build
+void graph_refresh(chg_ctx *ctx, chg_graph *g, const double *pos, int32_t *flag);
 void push_pending(chg_ctx *ctx, int slot, const chg_model *m);
 int next_flag_slot(chg_ctx *ctx);
 
@@ -344,4 +353,4 @@ void red_flush(chg_ctx *ctx);                          // one launch for every r
 // graph.cu
 chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const double *pos,
                             const double *lat, const int32_t *species, double r_atom, double r_bond,
-                            int on_device, int n_species);
+                            int on_device, int n_species, double skin = 0.0);

@@ -18,6 +18,7 @@
 namespace {
 
 __device__ __forceinline__ void envelope_du(double xi, int p, double &u, double &du) {
+  if (xi >= 1.0) { u = 0.0; du = 0.0; return; }       // clamped beyond the cutoff (proj.cu)
   double xp1 = 1.0;                                   // xi^(p-1)
   for (int k = 0; k < p - 1; ++k) xp1 *= xi;
   const double xp = xp1 * xi;

@@ -627,12 +627,16 @@ struct GraphBlocks { void *a = nullptr, *b = nullptr; };
 static uint64_t g_graph_counter = 0;
 
 chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const double *pos,
-                            const double *lat, const int32_t *species, double r_atom, double r_bond,
-                            int on_device, int n_species) {
+                            const double *lat, const int32_t *species, double r_atom_model, double r_bond_model,
+                            int on_device, int n_species, double skin) {
   if (S < 0 || (S > 0 && (!atom_ptr || !pos || !lat || !species)))
     CHG_THROW(CHG_ERR_ARG, "null input");
-  if (!(r_bond > 0 && r_bond <= r_atom) || !std::isfinite(r_atom))
-    CHG_THROW(CHG_ERR_ARG, "need 0 < r_bond <= r_atom (got %g, %g)", r_atom, r_bond);
+  if (!(r_bond_model > 0 && r_bond_model <= r_atom_model) || !std::isfinite(r_atom_model))
+    CHG_THROW(CHG_ERR_ARG, "need 0 < r_bond <= r_atom (got %g, %g)", r_atom_model, r_bond_model);
+  if (!(skin >= 0.0 && skin < r_atom_model) || !std::isfinite(skin))
+    CHG_THROW(CHG_ERR_ARG, "need 0 <= skin < r_atom (got %g)", skin);
+  // the lists are built with the list cutoffs r + skin; the model (bases, envelopes) keeps r
+  const double r_atom = r_atom_model + skin, r_bond = r_bond_model + skin;
   if (S > 0 && atom_ptr[0] != 0) CHG_THROW(CHG_ERR_ARG, "atom_ptr[0] must be 0");
   for (int s = 0; s < S; ++s)
     if (atom_ptr[s + 1] < atom_ptr[s]) CHG_THROW(CHG_ERR_ARG, "atom_ptr not monotone at %d", s);
@@ -677,8 +681,9 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
   G->id = ++g_graph_counter;
   G->S = S;
   G->N = N;
-  G->r_atom = r_atom;
-  G->r_bond = r_bond;
+  G->r_atom = r_atom_model;
+  G->r_bond = r_bond_model;
+  G->skin = skin;
   G->atom_ptr_h.assign(atom_ptr, atom_ptr + S + 1);
   if (S == 0) G->atom_ptr_h.assign(1, 0);
   GraphBlocks *bl = new GraphBlocks();
@@ -710,6 +715,8 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
     G->inv_natoms = (float *)take(4 * (size_t)S);
     StructGeo *d_geo = (StructGeo *)take(sizeof(StructGeo) * geo.size());
     double *d_pos = (double *)take(8 * 3 * N);
+    G->pos0 = d_pos;                                  // kept with the graph (skin refresh)
+    G->geo_dev = d_geo;
     double *d_frac = (double *)take(8 * 3 * N);
     int32_t *cnt_e = (int32_t *)take(4 * N);
     int32_t *cnt_b = (int32_t *)take(4 * N);
@@ -870,6 +877,54 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
   CUDA_OK(cudaEventCreateWithFlags(&G->ready, cudaEventDisableTiming));
   CUDA_OK(cudaEventRecord(G->ready, st));
   return G;
+}
+
+// ---------------------------------------------------------------------------
+// fixed-topology refresh (skin graphs, captured MD steps): every edge's geometry from the new
+// positions by the same canonical fp64 evaluation as the build (bit-identical to a fresh
+// build's value for that pair); the lists, bond flags and angles stay those of the build
+// ---------------------------------------------------------------------------
+__global__ void k_refresh(int E, const double *__restrict__ pos, const StructGeo *__restrict__ geo,
+                          const int32_t *__restrict__ soa, const int32_t *__restrict__ center,
+                          const int32_t *__restrict__ nbr, const char4 *__restrict__ img, float4 *__restrict__ vec,
+                          double4 *__restrict__ vec64) {
+  pdl_begin();
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const int i = center[e], j = nbr[e];
+  const char4 n = img[e];
+  double dx, dy, dz, q;
+  eval_pair(pos, geo[soa[i]].L, i, j, n.x, n.y, n.z, dx, dy, dz, q);
+  const double rr = sqrt(q);
+  vec[e] = make_float4((float)dx, (float)dy, (float)dz, (float)rr);
+  vec64[e] = make_double4(dx, dy, dz, rr);
+}
+
+// flag <- 1 when some atom moved more than skin / 2 since the build (the Verlet-list bound:
+// then a pair may have crossed the model cutoff without being in the lists)
+__global__ void k_moved(int N, const double *__restrict__ pos, const double *__restrict__ pos0, double lim2,
+                        int32_t *__restrict__ flag) {
+  pdl_begin();
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= N) return;
+  const double dx = pos[3 * a] - pos0[3 * a], dy = pos[3 * a + 1] - pos0[3 * a + 1], dz = pos[3 * a + 2] - pos0[3 * a + 2];
+  if (dx * dx + dy * dy + dz * dz > lim2) *flag = 1;
+}
+
+void graph_refresh(chg_ctx *ctx, chg_graph *G, const double *pos, int32_t *flag) {
+  if (!G->geo_dev || !G->pos0) CHG_THROW(CHG_ERR_STATE, "graph has no build geometry");
+  const int64_t E = G->E, N = G->N;
+  ProfScope ps(ctx, "graph_refresh", 0.0, 64.0 * E + 48.0 * N);
+  if (E) {
+    launch_k(ctx, k_refresh, ceil_div(E, 256), 256, 0, ctx->stream, (int)E, pos, (const StructGeo *)G->geo_dev,
+             G->struct_of_atom, G->center, G->nbr, G->img, G->vec, G->vec64);
+    check_launch(ctx);
+  }
+  if (flag && N) {
+    const double h = 0.5 * G->skin;
+    launch_k(ctx, k_moved, ceil_div(N, 256), 256, 0, ctx->stream, (int)N, pos, G->pos0, h * h, flag);
+    check_launch(ctx);
+  }
 }
 
 // Per-structure counts (chg_graph_counts) read on demand: the build itself synchronises

@@ -21,7 +21,10 @@ namespace {
 constexpr int PT = 64;            // rows per tile
 constexpr int PBP = 33;           // smem pitch of basis tiles [64][33]
 
+// u(ξ) for ξ < 1 and 0 beyond (u(1) = u'(1) = u''(1) = 0, so the clamp is smooth): pairs of a
+// skin graph beyond the model cutoff then carry exactly zero bases
 __device__ __forceinline__ double envelope_p(double xi, int p) {
+  if (xi >= 1.0) return 0.0;
   double xp = 1.0;
   for (int k = 0; k < p; ++k) xp *= xi;
   double a = 0.5 * (p + 1) * (p + 2), b = (double)p * (p + 2), c = 0.5 * p * (p + 1);

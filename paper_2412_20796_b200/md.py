@@ -5,6 +5,16 @@ every step runs in libchg: chg_md_verlet (kick + drift) -> chg_build_graph from 
 positions (cell lists for large cells) -> chg_forward_conservative (F = -dE/dr, on-device
 outputs) -> chg_md_verlet (kick).  Units: eV, Å, amu, fs.  Positions are not wrapped into the
 cell (the builder accepts any Cartesian positions).
+
+skin > 0: a fixed-topology Verlet list (chg_build_graph_skin: lists with r + skin, bases zero
+beyond r) whose geometry is refreshed every step (chg_graph_refresh), so the step has constant
+sizes; captured = True records it as one CUDA graph (chg_md_capture) and replays it
+(chg_md_run) in chunks of `check_every` steps.  After each chunk the moved-atom flag is read
+(set once an atom moved more than skin / 2 since the build) and the lists are rebuilt and the
+step re-captured.  The energies and forces equal those of rebuilt-every-step lists while every
+atom stays within skin / 2 of its build position; the flag is read every `check_every` steps,
+so an atom would have to move faster than (skin / 2) / (check_every · dt) — 0.05 Å/fs (5 km/s)
+at the defaults skin = 1 Å, 10 steps, 1 fs — to cross it between two checks.
 """
 from __future__ import annotations
 
@@ -18,11 +28,17 @@ KB_EV = 8.617333262e-5               # Boltzmann constant, eV/K
 
 class NVE:
     def __init__(self, ctx: chg.Context, model: chg.Model, atom_ptr, positions, lattice, species, masses,
-                 velocities=None, dt_fs: float = 1.0, r_atom: float = 5.0, r_bond: float = 3.0):
+                 velocities=None, dt_fs: float = 1.0, r_atom: float = 5.0, r_bond: float = 3.0,
+                 skin: float = 0.0, captured: bool = False, check_every: int = 10):
         import torch
         dev = torch.device("cuda", ctx.device)
         self.ctx, self.model, self.dt = ctx, model, float(dt_fs)
         self.r_atom, self.r_bond = r_atom, r_bond
+        if captured and skin <= 0:
+            raise ValueError("a captured MD step needs a skin graph (skin > 0)")
+        self.skin, self.captured, self.check_every = float(skin), bool(captured), max(1, int(check_every))
+        self.graph, self.exec, self.rebuilds = None, None, 0
+        self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
         self.ap = np.ascontiguousarray(np.asarray(atom_ptr, np.int64))
         n, S = int(self.ap[-1]), self.ap.shape[0] - 1
         f64 = dict(dtype=torch.float64, device=dev)
@@ -39,23 +55,68 @@ class NVE:
                     "magmom": torch.zeros(n, **f32)}
         self.steps = 0
         torch.cuda.current_stream(dev).synchronize()   # state tensors written on torch's stream
-        self._forces()
+        if self.skin > 0:
+            self._rebuild()
+        else:
+            self._forces()
         self.ctx.sync()
 
     def _forces(self):
+        if self.skin > 0:                              # fixed topology: refresh the geometry only
+            self.ctx.refresh_graph(self.graph, self.pos, self.flag)
+            self.ctx.forward_conservative(self.model, self.graph, out=self.out)
+            return
         g = self.ctx.build_graph(self.ap, self.pos, self.lat, self.spec, self.r_atom, self.r_bond)
         self.ctx.forward_conservative(self.model, g, out=self.out)
         g.close()
 
+    def _rebuild(self):
+        """New skin lists at the current positions (+ forces there, + a new capture)."""
+        if self.exec is not None:
+            self.exec.close()
+            self.exec = None
+        if self.graph is not None:
+            self.graph.close()
+        self.graph = self.ctx.build_graph(self.ap, self.pos, self.lat, self.spec, self.r_atom, self.r_bond,
+                                          skin=self.skin)
+        self.flag.zero_()
+        import torch
+        torch.cuda.current_stream(self.flag.device).synchronize()   # zeroed before the ctx stream reads it
+        if self.captured:                              # the capture's warm-up pass computes the forces
+            self.exec = self.ctx.md_capture(self.model, self.graph, self.pos, self.vel, self.inv_m, self.dt,
+                                            self.out, self.flag)
+        else:
+            self.ctx.forward_conservative(self.model, self.graph, out=self.out)
+        self.rebuilds += 1
+
     def step(self, n: int = 1):
-        """n velocity-Verlet steps (graph rebuilt every step).  Returns after the work on the
-        ctx stream has finished, so pos / vel / out may be read or edited on any stream."""
-        for _ in range(n):
-            self.ctx.md_verlet(self.pos, self.vel, self.out["forces"], self.inv_m, self.dt, drift=True)
-            self._forces()
-            self.ctx.md_verlet(self.pos, self.vel, self.out["forces"], self.inv_m, self.dt, drift=False)
-            self.steps += 1
+        """n velocity-Verlet steps.  Returns after the work on the ctx stream has finished, so
+        pos / vel / out may be read or edited on any stream."""
+        done = 0
+        while done < n:
+            k = min(self.check_every, n - done) if self.skin > 0 else n - done
+            if self.captured:
+                self.exec.run(k)
+            else:
+                for _ in range(k):
+                    self.ctx.md_verlet(self.pos, self.vel, self.out["forces"], self.inv_m, self.dt, drift=True)
+                    self._forces()
+                    self.ctx.md_verlet(self.pos, self.vel, self.out["forces"], self.inv_m, self.dt, drift=False)
+            done += k
+            self.steps += k
+            if self.skin > 0:
+                self.ctx.sync()
+                if int(self.flag.item()):              # an atom left its skin / 2 sphere: new lists
+                    self._rebuild()
         self.ctx.sync()
+
+    def close(self):
+        if self.exec is not None:
+            self.exec.close()
+            self.exec = None
+        if self.graph is not None:
+            self.graph.close()
+            self.graph = None
 
     # ---- observation (host copies; wait for the ctx stream first) -------------------
     def potential_energy(self) -> np.ndarray:

@@ -83,3 +83,89 @@ def test_nve_time_reversible(ctx):
     md.step(20)
     assert np.abs(md.pos.cpu().numpy() - x0).max() < 1e-5
     m.close()
+
+
+# ---- NEXT-2: fixed-topology (skin) graphs and the captured MD step --------------------------
+
+def _cons(ctx, m, g):
+    out = ctx.forward_conservative(m, g)
+    return out["energy"].astype(np.float64), out["forces"].astype(np.float64)
+
+
+def test_skin_graph_equals_exact_lists(ctx):
+    """Pairs of a skin graph beyond the model cutoffs carry zero bases (clamped envelope, reading
+    Q2): energy and conservative forces equal the exact lists' (summation order aside), at the
+    build positions and after chg_graph_refresh at displaced ones; the moved flag follows skin/2."""
+    import torch
+    b = si_diamond()
+    m = _model(ctx)
+    pos = torch.as_tensor(b.positions, device="cuda").contiguous()
+    lat = torch.as_tensor(b.lattice, device="cuda").contiguous()
+    sp = torch.as_tensor(b.species, device="cuda").contiguous()
+    gs = ctx.build_graph(b.atom_ptr, pos, lat, sp, 5.0, 3.0, skin=1.0)
+    ge = ctx.build_graph(b.atom_ptr, pos, lat, sp, 5.0, 3.0)
+    ns, ne = gs.counts(), ge.counts()
+    assert all(x >= y for x, y in zip(ns, ne)) and ns[1] > ne[1] and ns[2] > ne[2]   # strictly more pairs / bonds
+    es, fs = _cons(ctx, m, gs)
+    ee, fe = _cons(ctx, m, ge)
+    assert np.abs(es - ee).max() <= 1e-5 * max(1.0, np.abs(ee).max())
+    assert np.abs(fs - fe).max() <= 1e-5
+    ge.close()
+    # displaced positions: refresh the skin graph, compare with exact lists built there
+    rng = np.random.default_rng(3)
+    x1 = b.positions + rng.uniform(-0.2, 0.2, b.positions.shape)       # |dx| < skin / 2
+    pos.copy_(torch.as_tensor(x1, device="cuda"))
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    ctx.refresh_graph(gs, pos, flag)
+    es, fs = _cons(ctx, m, gs)
+    ge = ctx.build_graph(b.atom_ptr, pos, lat, sp, 5.0, 3.0)
+    ee, fe = _cons(ctx, m, ge)
+    assert np.abs(es - ee).max() <= 1e-5 * max(1.0, np.abs(ee).max())
+    assert np.abs(fs - fe).max() <= 1e-5
+    ctx.sync()
+    assert int(flag.item()) == 0
+    pos[0, 0] += 1.0                                                   # one atom beyond skin / 2 (|x1 - x0| <= 0.2)
+    torch.cuda.synchronize()
+    ctx.refresh_graph(gs, pos, flag)
+    ctx.sync()
+    assert int(flag.item()) == 1
+    gs.close(); ge.close(); m.close()
+
+
+def test_captured_md_step_matches_uncaptured(ctx):
+    """chg_md_capture / chg_md_run replay exactly the skin-graph step enqueued call by call, and
+    the skin MD trajectory follows the rebuilt-every-step one."""
+    b = si_diamond()
+    mass = np.full(b.positions.shape[0], 28.0855)
+    v0 = maxwell_boltzmann(mass, 300.0, seed=4)
+    m = _model(ctx)
+    runs = {}
+    for name, kw in (("rebuild", {}), ("skin", dict(skin=1.0)), ("captured", dict(skin=1.0, captured=True))):
+        md = NVE(ctx, m, b.atom_ptr, b.positions, b.lattice, b.species, mass, v0, dt_fs=0.5, **kw)
+        md.step(30)
+        runs[name] = (md.pos.cpu().numpy().copy(), md.vel.cpu().numpy().copy(), md.total_energy())
+        md.close()
+    assert np.array_equal(runs["skin"][0], runs["captured"][0])
+    assert np.array_equal(runs["skin"][1], runs["captured"][1])
+    assert np.abs(runs["skin"][0] - runs["rebuild"][0]).max() < 1e-6
+    assert np.abs(runs["skin"][2] - runs["rebuild"][2]).max() < 1e-5
+    m.close()
+
+
+def test_captured_md_rebuilds_when_atoms_move(ctx):
+    """A fast atom trips the skin / 2 flag: the lists are rebuilt and the step re-captured, and
+    the trajectory still follows the rebuilt-every-step one."""
+    b = si_diamond()
+    mass = np.full(b.positions.shape[0], 28.0855)
+    v0 = np.zeros_like(b.positions)
+    v0[0] = (0.02, 0.0, 0.0)                                           # 0.02 Å/fs: 0.3 Å per 30 steps
+    m = _model(ctx)
+    ref = NVE(ctx, m, b.atom_ptr, b.positions, b.lattice, b.species, mass, v0, dt_fs=0.5)
+    ref.step(60)
+    md = NVE(ctx, m, b.atom_ptr, b.positions, b.lattice, b.species, mass, v0, dt_fs=0.5, skin=0.4, captured=True,
+             check_every=5)
+    md.step(60)
+    assert md.rebuilds >= 2
+    assert np.abs(md.pos.cpu().numpy() - ref.pos.cpu().numpy()).max() < 1e-6
+    md.close(); ref.close(); m.close()
