@@ -202,6 +202,10 @@ struct TcPlan {
   // [cs_n0, cs_n0 + cs_nt) — so small-M launches spread over more SMs with a smaller weight slice
   int csplit;
   int cs_c0[4], cs_c1[4], cs_n0[4], cs_nt[4];
+  // split-K of one-wave single-chunk GEMMs with a plain epilogue: CTA (tile, y = blockIdx.y) sums
+  // K chunks [y·kper, (y+1)·kper) and stores its raw partial tile at rows y·kmpad + m of the
+  // partial buffer; k_splitk_sum adds the partials in order (+ bias + resid) — deterministic
+  int ksplit, kper, kmpad;
 };
 
 // B image: img[kc][q][n][4] = tf32(W_chunk(n - bcoff[kc][c], k = lo + kc·KC - a_k0 + 4q + r))
@@ -414,7 +418,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
     trace_ts[0] = t;
   }
 
-  const int nkc = P.width / KC;
+  // K chunks of this CTA: all, or [kcb, kcb + nkc) under a split-K; kc below is local, kcb + kc global
+  const int kcb = P.ksplit > 1 ? (int)blockIdx.y * P.kper : 0;
+  const int nkc = P.ksplit > 1 ? min(P.kper, P.width / KC - kcb) : P.width / KC;
   const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   const int total = my_tiles * nkc;
 
@@ -441,7 +447,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
         }
       }
       if (ua > 0) mbar_wait(&emptyA[sa], (ua - 1) & 1);
-      const int col = P.lo + kc * KC;
+      const int col = P.lo + (kcb + kc) * KC;
       int seg = 0, start = 0;
       bool found = false;
 #pragma unroll
@@ -582,7 +588,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
       const int tile = blockIdx.x + tl * gridDim.x;
       const int sa = gi % NSA, ua = gi / NSA;
       if (ua > 0) mbar_wait(&emptyA[sa], (ua - 1) & 1);
-      const int col = P.lo + kc * KC;
+      const int col = P.lo + (kcb + kc) * KC;
       int start = 0;
       mbar_expect_tx(&loaded[sa], a_bytes);
 #pragma unroll
@@ -613,7 +619,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
     if (lane == 0 && P.lconv && P.bres) {               // resident image first, then the A stream
       if (total > 0) {
         mbar_expect_tx(&fullB[0], b_stage * nkc);
-        for (int kc = 0; kc < nkc; ++kc) load_b(sB + kc * b_stage, kc, &fullB[0]);
+        for (int kc = 0; kc < nkc; ++kc) load_b(sB + kc * b_stage, kcb + kc, &fullB[0]);
       }
       for (int gi = 0; gi < total; ++gi) issue_a(gi);
     } else if (lane == 0 && P.lconv) {                  // A box and weight chunk of each stage in order
@@ -622,7 +628,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
         const int kc = gi % nkc, sb = gi % NSBr, ub = gi / NSBr;
         if (ub > 0) mbar_wait(&emptyB[sb], (ub - 1) & 1);
         mbar_expect_tx(&fullB[sb], b_stage);
-        load_b(sB + sb * b_stage, kc, &fullB[sb]);
+        load_b(sB + sb * b_stage, kcb + kc, &fullB[sb]);
       }
     } else if (lane == 0 && P.bres) {                   // whole image once: one barrier, nkc bulk copies
       if (total > 0) {
@@ -630,7 +636,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
           mbar_arrive(&fullB[0]);
         } else {
           mbar_expect_tx(&fullB[0], b_stage * nkc);
-          for (int kc = 0; kc < nkc; ++kc) load_b(sB + kc * b_stage, kc, &fullB[0]);
+          for (int kc = 0; kc < nkc; ++kc) load_b(sB + kc * b_stage, kcb + kc, &fullB[0]);
         }
       }
     } else if (lane == 0) {
@@ -641,7 +647,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
           mbar_arrive(&fullB[sb]);
         } else {
           mbar_expect_tx(&fullB[sb], b_stage);
-          load_b(sB + sb * b_stage, kc, &fullB[sb]);
+          load_b(sB + sb * b_stage, kcb + kc, &fullB[sb]);
         }
       }
     }
@@ -666,13 +672,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
           }
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t a_base = smem_u32(sA + sa * a_stage), b_base = smem_u32(sB + sb * b_stage);
-          const int col0 = P.lo + kc * KC;
+          const int col0 = P.lo + (kcb + kc) * KC;
           // MMA groups; under a column split one group: this CTA's chunks, N = its slice width
           const int ngr = P.csplit > 1 ? 1 : P.ngrp;
           for (int gr = 0; gr < ngr; ++gr) {
             const int c = P.csplit > 1 ? cb0 : P.gfirst[gr];
             const int gnv = P.csplit > 1 ? NT : P.gn[gr];
-            const int boff = P.csplit > 1 ? 0 : P.bcoff[kc][c];
+            const int boff = P.csplit > 1 ? 0 : P.bcoff[kcb + kc][c];
             const int kk = col0 - g.ch[c].a_k0;
             if (kk < 0 || kk >= g.K) continue;
             if (P.bf16) {                                 // BF16: K = 16 per MMA, A from the SWIZZLE_64B copy
@@ -875,7 +881,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
               for (int cc = 0; cc < 4; ++cc)
                 if (cc == c) {
                   if (TM.radd[cc]) tma_store_add_2d(&TM.o[cc], smem_u32(st), j0, row0);
-                  else tma_store_2d(pass ? &TM.o2[cc] : &TM.o[cc], smem_u32(st), j0, row0);
+                  else tma_store_2d(pass ? &TM.o2[cc] : &TM.o[cc], smem_u32(st), j0,
+                                    row0 + (P.ksplit > 1 ? (int)blockIdx.y * P.kmpad : 0));
                 }
             }
             ++sc;
@@ -1674,7 +1681,9 @@ static int encode_op_map(CUtensorMap *m, const float *base, int ncols, int rows,
 }
 
 // Returns false if the GEMM does not fit this path (caller uses the SIMT kernel).
-bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
+// ksplit > 1: g is the partial-output GEMM of a split-K (raw accumulators stored at rows
+// y·kmpad + m of g.ch[0].out, k_splitk_sum finishes it; see rowgemm_tc below)
+static bool rowgemm_tc_impl(chg_ctx *ctx, const RowGemm &g, int ksplit, int kper, int kmpad) {
   if (g.M <= 0 || g.K % KC != 0 || g.nchunk < 1) return false;
   const int split = ctx->tc_split ? 1 : 0;
   // small problems (at most one 128-row tile per SM: the per-atom / per-bond products) need no
@@ -1696,7 +1705,8 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
           ++n;
         }
         h.nchunk = n;
-        if (!rowgemm_tc(ctx, h)) CHG_THROW(CHG_ERR_STATE, "rowgemm_tc %s: 3xTF32 column group does not fit", g.tag);
+        if (!rowgemm_tc_impl(ctx, h, 1, 0, 0))
+          CHG_THROW(CHG_ERR_STATE, "rowgemm_tc %s: 3xTF32 column group does not fit", g.tag);
         c0 += n;
       }
       return true;
@@ -1705,6 +1715,9 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   TcPlan P{};
   P.split = split;
   P.bf16 = ctx->tc_bf16 ? 1 : 0;
+  P.ksplit = ksplit > 1 ? ksplit : 1;
+  P.kper = kper;
+  P.kmpad = kmpad;
   int lo = 1 << 30, hi = 0, off = 0;
   for (int c = 0; c < g.nchunk; ++c) {
     const Chunk &C = g.ch[c];
@@ -1808,7 +1821,7 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
   for (int c = 0; c < g.nchunk && TM.tstore; ++c) {
     const Chunk &C = g.ch[c];
     if (C.pre || C.ncols % 32 || !C.out) TM.tstore = 0;
-    else if (!encode_op_map(&TM.o[c], C.out, C.ncols, g.M, C.ldo, true)) TM.tstore = 0;
+    else if (!encode_op_map(&TM.o[c], C.out, C.ncols, P.ksplit > 1 ? P.ksplit * P.kmpad : g.M, C.ldo, true)) TM.tstore = 0;
     else if (C.sout && !encode_op_map(&TM.o2[c], C.sout, C.ncols, g.M, C.ldso, true)) TM.tstore = 0;
   }
   for (int c = 0; c < g.nchunk && TM.tstore; ++c)
@@ -1935,11 +1948,71 @@ bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
     fprintf(stderr, "rowgemm_tc %s: M %d K %d nseg %d tma %d%d%d%d nsa %d bres %d tstore %d nst %d nbuf %d noconv %d lconv %d csplit %d smem %zu\n",
             g.tag ? g.tag : "?", g.M, g.K, g.A.nseg, TM.use[0], TM.use[1], TM.use[2], TM.use[3], P.nsa, P.bres,
             TM.tstore, TM.nst, nbuf, P.noconv, P.lconv, P.csplit, smem);
-  launch_k(ctx, k_rowgemm_tc, dim3(grid, P.csplit), WS_THREADS, smem, ctx->stream, g, P, img, ntiles, skip, TM);
+  if (P.ksplit > 1 && (!TM.tstore || P.csplit > 1)) CHG_THROW(CHG_ERR_STATE, "rowgemm_tc %s: split-K plan", g.tag);
+  launch_k(ctx, k_rowgemm_tc, dim3(grid, P.ksplit > 1 ? P.ksplit : P.csplit), WS_THREADS, smem, ctx->stream, g, P, img,
+           ntiles, skip, TM);
   check_launch(ctx);
   return true;
 }
 
+
+namespace {
+// out[m][n] = resid[m][n] + bias[n] + Σ_y part[y·mpad + m][n]  (fixed order: deterministic)
+__global__ void k_splitk_sum(int M, int ncols, int G, const float *__restrict__ part, int mpad, int ldp,
+                             const float *__restrict__ bias, const float *__restrict__ resid, int ldr,
+                             float *__restrict__ out, int ldo) {
+  pdl_begin();
+  const int nq = ncols >> 2;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)M * nq; i += (int64_t)gridDim.x * blockDim.x) {
+    const int m = (int)(i / nq), q = (int)(i % nq);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int y = 0; y < G; ++y) {
+      const float4 v = *reinterpret_cast<const float4 *>(part + ((size_t)y * mpad + m) * ldp + 4 * q);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    if (bias) {
+      const float4 b = *reinterpret_cast<const float4 *>(bias + 4 * q);
+      acc.x += b.x; acc.y += b.y; acc.z += b.z; acc.w += b.w;
+    }
+    if (resid) {
+      const float4 r = *reinterpret_cast<const float4 *>(resid + (size_t)m * ldr + 4 * q);
+      acc.x += r.x; acc.y += r.y; acc.z += r.z; acc.w += r.w;
+    }
+    *reinterpret_cast<float4 *>(out + (size_t)m * ldo + 4 * q) = acc;
+  }
+}
+}  // namespace
+
+// Split-K for one-wave single-chunk GEMMs with a long K and a plain epilogue (bias / residual
+// only: the per-atom / per-bond adjoint GEMMs, K = 256-512 on a few tiles): G CTAs per tile
+// each sum K / G, raw partial tiles are stored by TMA and added in a fixed order by
+// k_splitk_sum — more SMs busy, each with a fraction of the MMA / load / conversion chain.
+bool rowgemm_tc(chg_ctx *ctx, const RowGemm &g) {
+  static const bool no_ksplit = getenv("CHG_TC_NO_KSPLIT") != nullptr;   // A/B knob
+  const Chunk &C = g.ch[0];
+  const int ntiles = g.M > 0 ? ceil_div(g.M, TCM) : 0, sms = device_sm_count();
+  const int nkc = g.K / KC;
+  const bool plain = g.nchunk == 1 && g.act == 0 && !C.mul && !C.pre && !C.sout && !C.round_out && C.ngadd == 0 &&
+                     C.out && C.ncols % 32 == 0 && C.ldo % 4 == 0 && (!C.resid || C.ldr % 4 == 0) &&
+                     C.a_k0 == 0 && g.K % KC == 0;
+  int G = 1;
+  while (plain && !no_ksplit && ntiles > 0 && nkc / (G * 2) >= 2 && ntiles * G * 2 <= sms) G *= 2;
+  if (G == 1) return rowgemm_tc_impl(ctx, g, 1, 0, 0);
+  const int kper = (nkc + G - 1) / G;
+  G = (nkc + kper - 1) / kper;
+  const int mpad = ntiles * TCM, ldp = C.ncols;
+  float *part = ctx->getf(ctx->ws_name("tc_ksplit"), (size_t)G * mpad * ldp);   // stream-private (forked branches)
+  RowGemm h = g;
+  Chunk &H = h.ch[0];
+  H.out = part; H.ldo = ldp; H.bias = nullptr; H.resid = nullptr; H.ldr = 0;
+  if (!rowgemm_tc_impl(ctx, h, G, kper, mpad)) return false;
+  const int64_t n4 = (int64_t)g.M * (C.ncols / 4);
+  ProfScope ps(ctx, g.tag ? g.tag : "rowgemm_tc", 0.0, 4.0 * g.M * C.ncols * (G + 1 + (C.resid ? 1 : 0)));
+  launch_k(ctx, k_splitk_sum, (unsigned)std::min<int64_t>(ceil_div(n4, 256), 4 * sms), 256, 0, ctx->stream, g.M,
+           C.ncols, G, (const float *)part, mpad, ldp, C.bias, C.resid, C.ldr, C.out, C.ldo);
+  check_launch(ctx);
+  return true;
+}
 
 // MN-major weight gradient (k_wgrad_mn): false when an operand cannot be TMA / cp.async staged
 static bool wgrad_mn(chg_ctx *ctx, const WGrad &g, float **partial_out, int *Kp_out, int *splits_out) {

@@ -27,7 +27,8 @@ def ctx():
 
 
 @pytest.mark.parametrize("engine", [0, 1, 2, 3])
-@pytest.mark.parametrize("M,K,N", [(1000, 64, 128), (130, 192, 128), (4097, 256, 256), (1, 64, 64), (777, 128, 192)])
+@pytest.mark.parametrize("M,K,N", [(1000, 64, 128), (130, 192, 128), (4097, 256, 256), (1, 64, 64), (777, 128, 192),
+                                   (777, 256, 64), (1000, 512, 64), (9000, 256, 64)])
 def test_row_gemm(ctx, engine, M, K, N):
     rng = np.random.default_rng(M + K + N)
     A = rng.normal(size=(M, K)).astype(np.float32)
