@@ -101,10 +101,12 @@ def _args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batches", type=int, default=4, help="distinct pre-generated batches cycled through")
-    ap.add_argument("--prefetch", default="off", choices=["e2e", "all", "off"],
-                    help="graph prefetch on a builder context (SURVEY NEXT-3) in the e2e pass, in every pass, "
-                         "or never (default: measured at C2, the builder's small kernels share SMs with the "
-                         "persistent GEMMs and the overlap gains nothing; DESIGN.md §12)")
+    ap.add_argument("--prefetch", default="auto", choices=["auto", "e2e", "all", "off"],
+                    help="graph prefetch on a builder context (SURVEY NEXT-3): all = the next step's graph is "
+                         "built on a high-priority stream during this step in every pass (measured +1.7 %% at C2, "
+                         "+1.2 %% at C3 on one GPU, +1.2 %% at N = 2, but a 20 %% outlier at N = 4 next to NCCL); "
+                         "e2e = in the e2e pass only; off = every build inline; auto (default) = all at N = 1, off "
+                         "at N > 1 (DESIGN.md §12)")
     ap.add_argument("--workload", default="auto", choices=["auto", "C2", "C3", "C4"],
                     help="auto: C2 at N=1, C3 at N>1; C4: skewed 4-400-atom oxides (BASELINE configs[3])")
     ap.add_argument("--per-gpu", type=int, default=0, help="structures per GPU (default: 40 at N=1, 128 at N>1)")
@@ -369,6 +371,8 @@ def main():
     # stream while this step's forward / backward run; the step's end waits for that build, so
     # every build stays inside a timed step window (the first step builds its own inline)
     # (high-priority stream: its short kernels are scheduled first whenever SMs free up)
+    if a.prefetch == "auto":
+        a.prefetch = "all" if ws == 1 else "off"
     bstream = None if a.prefetch == "off" else torch.cuda.Stream(device=local, priority=-5)
     builder = None if a.prefetch == "off" else chg.Context(local, stream=bstream.cuda_stream)
 
@@ -408,7 +412,7 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    def timed(on_host: bool, profile: bool = False, model=None, bl=None, cached=None, execs=None):
+    def timed(on_host: bool, profile: bool = False, model=None, bl=None, cached=None, execs=None, inline=False):
         """K steps; cached = prebuilt graphs per batch (SURVEY §8(d) item 3: graph build outside);
         execs = captured steps per batch (chg_capture_step: one CUDA graph replay per step)."""
         bl = bl or batches
@@ -421,7 +425,7 @@ def main():
         gnext = None
         for k in range(a.steps):
             b = bl[k % len(bl)]
-            use = builder is not None and not profile and (on_host or a.prefetch == "all")
+            use = builder is not None and not profile and not inline and (on_host or a.prefetch == "all")
             nxt = bl[(k + 1) % len(bl)] if (use and k + 1 < a.steps) else None
             ev[k][0].record(stream)
             if execs is not None:
@@ -511,10 +515,11 @@ def main():
         c3 = make_batches("C3", 128, 2)
         for k in range(a.warmup):
             one_step(c3[k % len(c3)], False)
-        ms_c3, _, _ = timed(False, bl=c3)
+        ms_c3, _, _ = timed(False, bl=c3, inline=True)    # graph builds inline, as in the N > 1 runs
         s_c3 = sum(c3[k % len(c3)]["gl"]["S"] for k in range(a.steps))
         roof_c3 = [step_roofline(c3[k % len(c3)]["counts"], a.precision) for k in range(a.steps)]
-        weak_base = {"workload": "C3: 128 MPtrj-shaped structures on 1 GPU (the per-GPU work of the N > 1 runs)",
+        weak_base = {"workload": "C3: 128 MPtrj-shaped structures on 1 GPU (the per-GPU work of the N > 1 runs; "
+                                 "graph builds inline as at N > 1)",
                      "value": s_c3 / (ms_c3 / 1e3), "unit": "structures/s", "ms_per_step": ms_c3 / a.steps,
                      "whole_step_frac": sum(max(r[2], r[3]) for r in roof_c3) / (ms_c3 / 1e3)}
         _, _, rep_c3 = timed(False, profile=True, bl=c3)         # gather-scatter GB/s at C3 (§8(d) item 7)
