@@ -460,9 +460,14 @@ def main():
     stats, last_stats = {}, [None]
     # warm-up covers every cycled batch at least once (its graph / workspace sizes are then known
     # to the memory pool before timing), and at least --warmup steps
-    for k in range(max(a.warmup, len(batches))):
-        one_step(batches[k % len(batches)], False)
-        one_step(batches[k % len(batches)], True)
+    # (with graph prefetch the warm-up runs the prefetching loop too: the builder context's own
+    # workspaces and pinned buffers are sized before timing — else the first timed step pays them)
+    nwu = max(a.warmup, len(batches))
+    for on_host in (False, True):
+        gnext = None
+        for k in range(nwu):
+            nxt = batches[(k + 1) % len(batches)] if (builder is not None and k + 1 < nwu) else None
+            _, gnext = one_step(batches[k % len(batches)], on_host, g=gnext, nxt=nxt)
     clocks = Clocks(local)
     clocks.start()
     time.sleep(0.3)                                   # nvidia-smi's first sample lands before the timing
@@ -708,6 +713,7 @@ def main():
                                                              for k in range(a.steps)]) / (side[o] / 1e3)}
                              for o in others}},
             "step_ms": step_ms,
+            "per_step_ms": [round(x, 4) for x in main_stats["per_step"]],
             "whole_step_roofline": whole,
             "cached_graph": {"value": structs / (ms_cached / 1e3), "unit": "structures/s",
                              "ms_per_step": ms_cached / a.steps,
