@@ -53,6 +53,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       : "memory");
 }
 
+// tensor-map descriptors are fetched into the TMA unit's cache before the PDL wait, so their
+// first use (the first A box, the first store) does not pay the fetch
+__device__ __forceinline__ void prefetch_tmap(const void *map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
@@ -410,6 +416,14 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_rowgemm_tc(const __grid_const
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (TC_SKIP(32) && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_setup));
+  if (tid == 0) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < g.A.nseg && TM.use[k]) prefetch_tmap(&TM.m[k]);
+      if (k < g.nchunk && TM.tstore) prefetch_tmap(&TM.o[k]);
+      if (k < g.nchunk && TM.use_e[k]) prefetch_tmap(&TM.e[k]);
+    }
+  }
   pdl_begin();                                    // the setup above overlaps the predecessor's tail
   const uint32_t tmem = *tslot;
   if (TC_SKIP(32) && tid == 0) {
@@ -1390,6 +1404,13 @@ __global__ void __launch_bounds__(MN_THREADS, 1) k_wgrad_mn(const __grid_constan
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (tid == 0) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (k < g.A.nseg && !g.A.seg[k].idx) prefetch_tmap(&TM.a[k]);
+    prefetch_tmap(&TM.d);
+    prefetch_tmap(&pmap);
+  }
   pdl_begin();
   const uint32_t tmem = *tslot;
   const int nAk = g.K / 32;                                   // loaded A boxes
