@@ -1,3 +1,4 @@
+#include <chrono>
 // graph.cu — A1: periodic atom graph, bond graph and angle list on the GPU.
 //
 // Paper: P:95 (§II-B(1) graph extraction), Alg. 1 lines P:253-256 (r_j += I@L,
@@ -701,7 +702,12 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
     for (int ss = 0; ss < S; ++ss) any_cells = any_cells || atom_ptr[ss + 1] - atom_ptr[ss] >= CELL_MIN;
     if (any_cells) sz_atom += align_up(4 * N) * 4 + align_up(4 * (N + 1));
     void *blk1 = nullptr;
+    const auto tm0 = std::chrono::steady_clock::now();
     CUDA_OK(cudaMallocAsync(&blk1, sz_atom, st));
+    if (getenv("CHG_GRAPH_TIMING")) {
+      const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tm0).count();
+      if (ms > 2.0) fprintf(stderr, "graph build: cudaMallocAsync(blk1 %zu B) %.1f ms\n", sz_atom, ms);
+    }
     bl->a = blk1;
     char *c = (char *)blk1;
     auto take = [&](size_t bytes) { void *p = c; c += align_up(bytes); return p; };
@@ -809,7 +815,13 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
     long long *h_tot = (long long *)ctx->pinned_get(64);
     CUDA_OK(cudaMemcpyAsync(h_tot, d_tot, 32, cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaMemcpyAsync(((char *)h_tot) + 32, flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    static const bool gtime = getenv("CHG_GRAPH_TIMING") != nullptr;   // debug: slow size readbacks
+    const auto tq0 = std::chrono::steady_clock::now();
     CUDA_OK(cudaStreamSynchronize(st));
+    if (gtime) {
+      const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tq0).count();
+      if (ms > 5.0) fprintf(stderr, "graph build: size readback waited %.1f ms (N %lld)\n", ms, (long long)N);
+    }
     int hflag = *(int *)(((char *)h_tot) + 32), hbad = *(int *)(((char *)h_tot) + 36);
     if (hflag & 16) CHG_THROW(CHG_ERR_GEOMETRY, "structure %d: non-finite lattice", hbad);
     if (hflag & 32) CHG_THROW(CHG_ERR_GEOMETRY, "structure %d: |det L| <= 1e-6", hbad);
@@ -826,7 +838,12 @@ chg_graph *build_graph_impl(chg_ctx *ctx, int S, const int64_t *atom_ptr, const 
     size_t sz2 = align_up(4 * E) * 4 + align_up(4 * E) /*img*/ + align_up(16 * E) + align_up(32 * E) + align_up(4 * B) * 2 +
                  align_up(4 * (B + 1)) + align_up(4 * A) * 6 + align_up(16) + 256;
     void *blk2 = nullptr;
+    const auto tm1 = std::chrono::steady_clock::now();
     CUDA_OK(cudaMallocAsync(&blk2, sz2, st));
+    if (getenv("CHG_GRAPH_TIMING")) {
+      const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tm1).count();
+      if (ms > 2.0) fprintf(stderr, "graph build: cudaMallocAsync(blk2 %zu B) %.1f ms\n", sz2, ms);
+    }
     bl->b = blk2;
     c = (char *)blk2;
     G->center = (int32_t *)take(4 * E);
