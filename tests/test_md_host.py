@@ -28,3 +28,16 @@ def test_maxwell_boltzmann_temperature_and_momentum():
     ke = 0.5 * (m[:, None] * v * v).sum() * EV_PER_AMU_A2_FS2
     t = 2.0 * ke / (3.0 * len(m) * KB_EV)
     assert abs(t - 300.0) < 6.0
+
+
+def test_captured_md_needs_a_skin_graph():
+    """NVE(captured=True) replays a fixed-topology step: without a skin (lists rebuilt every step)
+    there is nothing to capture — refused before any device work."""
+    import pytest
+    from paper_2412_20796_b200.md import NVE
+
+    class _Ctx:
+        device = 0
+
+    with pytest.raises(ValueError):
+        NVE(_Ctx(), None, [0, 1], np.zeros((1, 3)), np.eye(3)[None], [14], [28.0], captured=True, skin=0.0)
