@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(256) k_reduce_all(const __grid_constant__ RedB
     if (J.stride % 4 == 0) {                // 16-B rows: one float4 per partial row
       const float4 *p = (const float4 *)J.part + q;
       const int64_t st4 = J.stride / 4;
-#pragma unroll 4
+#pragma unroll 8
       for (int sp = grp; sp < J.splits; sp += G) {
         const float4 u = __ldcg(p + (size_t)sp * st4);
         s.x += u.x; s.y += u.y; s.z += u.z; s.w += u.w;
@@ -130,9 +130,11 @@ void red_flush(chg_ctx *ctx) {
     for (int k = 0; k < B.n; ++k) {
       B.j[k] = ctx->red_jobs[j0 + k];
       B.j[k].block0 = blocks;
-      // ~4-8 partial rows per thread: G = 256 / qpb split groups (8..64, a power of two)
+      // ~8-16 partial rows per thread: G = 256 / qpb split groups (8..32, a power of two; measured)
+      static const int gmax = getenv("CHG_RED_GMAX") ? atoi(getenv("CHG_RED_GMAX")) : 32;   // A/B knob
+      static const int rpt = getenv("CHG_RED_RPT") ? atoi(getenv("CHG_RED_RPT")) : 16;      // A/B knob
       int G = 8;
-      while (G < 64 && G * 8 < B.j[k].splits) G *= 2;
+      while (G < gmax && G * rpt < B.j[k].splits) G *= 2;
       B.j[k].qpb = 256 / G;
       blocks += ceil_div(ceil_div(B.j[k].n, 4), B.j[k].qpb);
       bytes += 4.0 * B.j[k].n * (B.j[k].splits + 2.0);
