@@ -192,7 +192,6 @@ void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float
     // per atom (v_i part) and per bond (e_ij, e_ik parts) products of the packed first layers
     float *Pv = ctx->getf(ctx->ws_name("bc_Pv"), (size_t)std::max<int64_t>(N, 1) * ldP);
     float *P1 = ctx->getf(ctx->ws_name("bc_P1"), (size_t)std::max<int64_t>(B, 1) * ldP);
-    float *P2 = ctx->getf(ctx->ws_name("bc_P2"), (size_t)std::max<int64_t>(B, 1) * ldP);
     part_product(ctx, aseg(v, 64, 64), N, W, nw, 0, Pv, ldP, "bc_P");
     // Q1[b] = e_b·W[64:128] + Pv[centre of b]: the v_i part rides on the first bond (the angles
     // of a first bond are contiguous, so the per-angle GEMM gathers Q1 with L1 reuse)
@@ -201,6 +200,7 @@ void bond_conv_fwd(Fwd &F, int t, bool angle_branch, const float *v, const float
     RowGemm G;
     if (fact_full) {
       // per angle: [z1_bond | y_angle] = a·W[192:256] + b + Q1[b1] + P2[b2]
+      float *P2 = ctx->getf(ctx->ws_name("bc_P2"), (size_t)std::max<int64_t>(B, 1) * ldP);
       part_product(ctx, aseg(e, 64, 64, g->bond_edge, E), B, W, nw, 128, P2, ldP, "bc_P");
       G.A.seg[0] = aseg(a, 64, 64);
       G.A.nseg = 1;
