@@ -26,8 +26,8 @@ def ctx():
     c.close()
 
 
-def _model(ctx):
-    cfg = chg.default_model_cfg(); cfg.mlp_precision = 0
+def _model(ctx, prec=0):
+    cfg = chg.default_model_cfg(); cfg.mlp_precision = prec
     m = chg.Model(ctx, cfg)
     m.set_params(init_flat_params([(n, s) for n, s, _ in m.layout()], seed=0).astype(np.float32))
     return m
@@ -133,13 +133,15 @@ def test_skin_graph_equals_exact_lists(ctx):
     gs.close(); ge.close(); m.close()
 
 
-def test_captured_md_step_matches_uncaptured(ctx):
+@pytest.mark.parametrize("prec", [0, 1])
+def test_captured_md_step_matches_uncaptured(ctx, prec):
     """chg_md_capture / chg_md_run replay exactly the skin-graph step enqueued call by call, and
-    the skin MD trajectory follows the rebuilt-every-step one."""
+    the skin MD trajectory follows the rebuilt-every-step one (fp32 CUDA cores and 3xTF32
+    tensor cores inside the captured graph)."""
     b = si_diamond()
     mass = np.full(b.positions.shape[0], 28.0855)
     v0 = maxwell_boltzmann(mass, 300.0, seed=4)
-    m = _model(ctx)
+    m = _model(ctx, prec)
     runs = {}
     for name, kw in (("rebuild", {}), ("skin", dict(skin=1.0)), ("captured", dict(skin=1.0, captured=True))):
         md = NVE(ctx, m, b.atom_ptr, b.positions, b.lattice, b.species, mass, v0, dt_fs=0.5, **kw)
