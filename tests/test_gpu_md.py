@@ -171,3 +171,36 @@ def test_captured_md_rebuilds_when_atoms_move(ctx):
     assert md.rebuilds >= 2
     assert np.abs(md.pos.cpu().numpy() - ref.pos.cpu().numpy()).max() < 1e-6
     md.close(); ref.close(); m.close()
+
+
+def test_refresh_geometry_is_bit_identical_to_a_fresh_build(ctx):
+    """chg_graph_refresh evaluates each listed pair by the build's canonical fp64 expression: the
+    refreshed vectors equal, bit for bit, those of a graph built afresh at the new positions
+    (pairs present in both lists; the pair sets may differ at the list cutoff)."""
+    import torch
+    b = si_diamond()
+    pos = torch.as_tensor(b.positions, device="cuda").contiguous()
+    lat = torch.as_tensor(b.lattice, device="cuda").contiguous()
+    sp = torch.as_tensor(b.species, device="cuda").contiguous()
+    gs = ctx.build_graph(b.atom_ptr, pos, lat, sp, 5.0, 3.0, skin=0.6)
+    x1 = b.positions + np.random.default_rng(5).uniform(-0.25, 0.25, b.positions.shape)
+    pos.copy_(torch.as_tensor(x1, device="cuda"))
+    torch.cuda.synchronize()
+    ctx.refresh_graph(gs, pos)
+    gf = ctx.build_graph(b.atom_ptr, pos, lat, sp, 5.0, 3.0, skin=0.6)
+    ctx.sync()
+
+    def pairs(g):
+        x = g.export()
+        rp, out = x["row_ptr"], {}
+        for i in range(len(rp) - 1):
+            for e in range(rp[i], rp[i + 1]):
+                out[(i, int(x["nbr"][e]), tuple(int(t) for t in x["img"][e]))] = x["vec"][e]
+        return out
+
+    ps, pf = pairs(gs), pairs(gf)
+    common = set(ps) & set(pf)
+    assert len(common) > 0.95 * max(len(ps), len(pf))
+    for k in common:
+        assert np.array_equal(ps[k], pf[k]), k
+    gs.close(); gf.close()
