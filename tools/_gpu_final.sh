@@ -4,10 +4,4 @@ timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/f_tests.log 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/f_smoke.log 2>&1
 timeout 900 python bench.py > gpurun_out/f_bench.log 2>&1
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/f_ref.log 2>&1
-timeout 600 python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/n_plain_bench.log 2>&1 && \
-timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/n_ncu_bench.log 2>&1
-for W in C2 C3; do
-timeout 300 python tools/ncu_step.py $W 3xtf32 > gpurun_out/n_plain_step.log 2>&1 && \
-timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/step_3xtf32_${W}.csv python tools/ncu_step.py $W 3xtf32 > /dev/null 2>&1
-done
-tail -3 gpurun_out/f_tests.log; tail -1 gpurun_out/f_smoke.log; grep -o '"value": [0-9.]*' gpurun_out/f_bench.log | head -1
+tail -2 gpurun_out/f_tests.log; tail -1 gpurun_out/f_smoke.log; grep -o '"value": [0-9.]*' gpurun_out/f_bench.log | head -1
